@@ -1,0 +1,728 @@
+// libcf device compiler: lowers a cf::Graph to the table the persistent driver kernel
+// interprets (program.h).
+//
+// Every node becomes a device node. Control-flow primitives, integer/bool scalar ops,
+// TensorArray and Stack ops are evaluated by the driver itself (device-resident control,
+// north star subsystem (1)); float-tensor ops become "heavy" instances executed by the
+// worker CTAs. Each heavy output gets a static placement:
+//   * TA    -- written straight into the TensorArray slot its TAWrite targets (zero-copy
+//              TensorArray write);
+//   * ARENA -- one slot per iteration, for values that reach a StackPush: the stack then
+//              holds pointers to immutable slots (the contiguous-array lowering of stacks
+//              when "the loop variables have a static shape and the iteration count has a
+//              static upper bound");
+//   * RING  -- K+1 slots for everything else in a loop: the parallel_iterations window
+//               guarantees a slot is dead before it is reused;
+//   * ROOT  -- one buffer for values outside loops.
+#include "compiler.h"
+
+#include <algorithm>
+#include <cstring>
+#include <functional>
+#include <set>
+#include <sstream>
+
+namespace cf {
+
+using namespace cfdev;
+
+namespace {
+
+int32_t dev_dt(int32_t d, int32_t precision) {
+  (void)precision;
+  switch (d) {
+    case BOOL: return D_BOOL;
+    case I32: return D_I32;
+    case I64: return D_I64;
+    case F32:
+    case F64:
+    case BF16: return D_F32;
+    default: return D_NONE;
+  }
+}
+int dev_size(int32_t d) {
+  switch (d) {
+    case D_BOOL: return 1;
+    case D_I32: return 4;
+    case D_I64: return 8;
+    case D_F32: return 4;
+    case D_BF16: return 2;
+    default: return 0;
+  }
+}
+
+struct Compiler {
+  const Graph& g;
+  CompileOpts o;
+  HostProgram P;
+  std::vector<int> vbase, ctrl_vid, frame_of;   // per node
+  std::vector<std::vector<std::pair<int, int>>> cons;   // per value: (consumer node, input idx)
+  std::map<std::string, int> frame_id;
+  std::vector<int> frame_ctx;
+  std::map<int, int> ta_id;           // TACreate node -> ta id
+  std::map<int, int> stack_id;        // StackCreate node -> stack id
+  std::vector<std::vector<std::pair<int, int>>> extra_edges;   // per frame: (before, after)
+
+  Compiler(const Graph& gg, const CompileOpts& oo) : g(gg), o(oo) {}
+
+  int vid(TRef t) const { return vbase[t.node] + t.port; }
+  bool is_heavy(const Node& n) const {
+    if (n.op == "Placeholder" || n.op == "Const" || n.op == "Identity" || n.op == "StopGradient" ||
+        n.op == "Reshape" || n.op == "Switch" || n.op == "Merge" || n.op == "Enter" ||
+        n.op == "Exit" || n.op == "NextIteration" || n.op.rfind("TA", 0) == 0 ||
+        n.op.rfind("Stack", 0) == 0)
+      return false;
+    for (auto d : n.odt)
+      if (is_float(d)) return true;
+    return false;
+  }
+
+  [[noreturn]] void unsupported(const Node& n, const std::string& why) {
+    throw CfError(CF_E_UNSUPPORTED, "device compiler: node " + std::to_string(n.id) + " (" +
+                                        n.op + "): " + why);
+  }
+
+  int add_buf(size_t bytes, bool zero, const std::string& what, const void* init = nullptr) {
+    BufPlan b;
+    b.bytes = std::max<size_t>(bytes, 16);
+    b.zero = zero;
+    b.what = what;
+    if (init) {
+      b.init.resize(bytes);
+      std::memcpy(b.init.data(), init, bytes);
+    }
+    P.bufs.push_back(std::move(b));
+    return (int)P.bufs.size() - 1;
+  }
+
+  // trace a TensorArray handle back to its static TA id
+  int trace_ta(TRef h, int depth = 0) {
+    if (depth > 64) throw CfError(CF_E_UNSUPPORTED, "TensorArray handle routing too deep");
+    const Node& n = g.nodes[h.node];
+    if (n.op == "TACreate") return ta_id.at(n.id);
+    if (n.op == "TAGrad") {
+      int f = trace_ta(n.in[0], depth + 1);
+      return P.tas[f].grad_id;
+    }
+    if (n.op == "Enter" || n.op == "Identity" || n.op == "Switch" || n.op == "Exit" ||
+        n.op == "NextIteration")
+      return trace_ta(n.in[0], depth + 1);
+    if (n.op == "Merge") return trace_ta(n.in[0], depth + 1);
+    throw CfError(CF_E_UNSUPPORTED, "TensorArray handle from op " + n.op);
+  }
+
+  void run(const std::vector<TRef>& fetches) {
+    const int N = (int)g.nodes.size();
+    vbase.resize(N);
+    ctrl_vid.resize(N);
+    int nv = 0;
+    for (int i = 0; i < N; ++i) {
+      vbase[i] = nv;
+      nv += (int)g.nodes[i].odt.size();
+    }
+    for (int i = 0; i < N; ++i) ctrl_vid[i] = nv++;
+    P.n_vids = nv;
+    cons.assign(nv, {});
+    for (auto& n : g.nodes)
+      for (size_t j = 0; j < n.in.size(); ++j) cons[vid(n.in[j])].push_back({n.id, (int)j});
+
+    // ---- frames
+    frame_of.assign(N, -1);
+    for (auto& name : g.frame_order) {
+      int c = g.whiles.at(name);
+      if (g.enclosing_while(g.ctxs[c].parent) >= 0)
+        throw CfError(CF_E_UNSUPPORTED, "nested while_loop (frame " + name + ") not lowered yet");
+      frame_id[name] = (int)frame_ctx.size();
+      frame_ctx.push_back(c);
+      P.frame_names.push_back(name);
+    }
+    for (auto& n : g.nodes) {
+      int w = g.enclosing_while(n.ctx);
+      if (w >= 0) frame_of[n.id] = frame_id.at(g.ctxs[w].name);
+    }
+    extra_edges.assign(frame_ctx.size() + 1, {});
+
+    // ---- TensorArrays and stacks
+    for (auto& n : g.nodes) {
+      if (n.op == "TACreate") {
+        DTA t{};
+        t.size = (int32_t)n.attrs.i("size");
+        int32_t d = dev_dt((int32_t)n.attrs.i("dtype"), o.precision);
+        t.dt = d;
+        t.elem_bytes = numel(n.attrs.v("elem_shape")) * dev_size(d);
+        t.grad_id = -1;
+        ta_id[n.id] = (int)P.tas.size();
+        P.tas.push_back(t);
+      }
+    }
+    for (auto& n : g.nodes) {
+      if (n.op == "TAGrad") {
+        int f = trace_ta(n.in[0]);
+        if (P.tas[f].grad_id < 0) {
+          DTA t = P.tas[f];
+          t.is_grad = 1;
+          t.grad_id = -1;
+          P.tas[f].grad_id = (int)P.tas.size();
+          P.tas.push_back(t);
+        }
+      }
+    }
+    for (size_t k = 0; k < P.tas.size(); ++k) {
+      DTA& t = P.tas[k];
+      t.base = add_buf((size_t)t.size * t.elem_bytes, t.is_grad != 0,
+                       std::string(t.is_grad ? "grad " : "") + "TensorArray " + std::to_string(k));
+    }
+    int slot_total = 0;
+    for (auto& t : P.tas) slot_total += t.size;
+    P.ta_slots = slot_total;
+
+    // ---- frame bounds (iteration upper bound from TensorArray sizes, or opts)
+    std::vector<int64_t> bound(frame_ctx.size(), 0);
+    for (auto& n : g.nodes) {
+      int f = frame_of[n.id];
+      if (f < 0) continue;
+      if (n.op == "TARead" || n.op == "TAWrite")
+        bound[f] = std::max<int64_t>(bound[f], P.tas[trace_ta(n.in[0])].size);
+    }
+    for (size_t f = 0; f < frame_ctx.size(); ++f) {
+      if (o.max_iterations > 0) bound[f] = o.max_iterations;
+      if (bound[f] <= 0)
+        throw CfError(CF_E_UNSUPPORTED, "cannot bound iterations of frame " + P.frame_names[f] +
+                                            " (no TensorArray; set max_iterations)");
+    }
+    for (auto& n : g.nodes) {
+      if (n.op == "StackCreate") {
+        DStack s{};
+        auto it = frame_id.find(n.attrs.s("frame"));
+        if (it == frame_id.end()) unsupported(n, "stack of unknown frame");
+        s.capacity = (int32_t)bound[it->second];
+        s.entry_off = P.stack_pool;
+        P.stack_pool += s.capacity;
+        stack_id[n.id] = (int)P.stacks.size();
+        P.stacks.push_back(s);
+      }
+    }
+
+    // ---- device nodes
+    P.nodes.resize(N);
+    int max_cond = -1;
+    std::vector<int> heavy_nodes;
+    for (auto& n : g.nodes) {
+      DNode d{};
+      d.n_in = (int)n.in.size();
+      d.in_off = (int)P.in_vids.size();
+      for (auto& t : n.in) P.in_vids.push_back(vid(t));
+      d.n_ctrl = (int)n.ctrl.size();
+      d.ctrl_off = (int)P.in_vids.size();
+      for (int c : n.ctrl) P.in_vids.push_back(ctrl_vid[c]);
+      d.n_out = (int)n.odt.size();
+      d.out_vid = vbase[n.id];
+      d.ctrl_vid = ctrl_vid[n.id];
+      d.place_off = -1;
+      for (auto& a : d.aux) a = 0;
+      const std::string& op = n.op;
+      int32_t odt = n.odt.empty() ? -1 : n.odt[0];
+      if (op == "Placeholder") {
+        d.op = OP_PLACEHOLDER;
+        FeedInfo fi;
+        fi.vid = vbase[n.id];
+        fi.graph_dt = odt;
+        fi.dev_dt = dev_dt(odt, o.precision);
+        fi.bytes = numel(n.osh[0]) * dev_size(fi.dev_dt);
+        fi.scalar_ctrl = !is_float(odt) && n.osh[0].empty();
+        P.feeds[n.attrs.s("name")] = fi;
+      } else if (op == "Const") {
+        d.op = OP_CONST;
+        if (odt == FLOW || odt == RES) {
+          d.op = OP_FLOW;
+        } else if (!is_float(odt) && n.osh[0].empty()) {
+          d.aux[0] = 1;
+          int64_t v = 0;
+          if (odt == I64) std::memcpy(&v, n.data.data(), 8);
+          else if (odt == I32) { int32_t x; std::memcpy(&x, n.data.data(), 4); v = x; }
+          else if (odt == BOOL) v = n.data[0] != 0;
+          d.imm[0] = v;
+          d.aux[1] = dev_dt(odt, o.precision);
+        } else {
+          int32_t dd = dev_dt(odt, o.precision);
+          std::vector<uint8_t> bytes((size_t)numel(n.osh[0]) * dev_size(dd));
+          if (odt == F64) {
+            for (int64_t k = 0; k < numel(n.osh[0]); ++k) {
+              double x;
+              std::memcpy(&x, n.data.data() + 8 * k, 8);
+              float f = (float)x;
+              std::memcpy(bytes.data() + 4 * k, &f, 4);
+            }
+          } else {
+            std::memcpy(bytes.data(), n.data.data(), std::min(bytes.size(), n.data.size()));
+          }
+          d.aux[0] = 0;
+          d.aux[1] = dd;
+          d.imm[0] = add_buf(bytes.size(), false, "const " + std::to_string(n.id), bytes.data());
+        }
+      } else if (op == "Identity" || op == "StopGradient" || op == "Reshape" ||
+                 (op == "Cast" && is_float(odt) && is_float(g.dtype(n.in[0])))) {
+        d.op = OP_PASS;
+      } else if (op == "Switch") {
+        d.op = OP_SWITCH;
+        d.aux[0] = n.attrs.has("cond_id") ? (int)n.attrs.i("cond_id") : -1;
+        d.aux[1] = n.attrs.b("loop");
+        if (d.aux[0] > max_cond) max_cond = d.aux[0];
+      } else if (op == "Merge") {
+        if (n.attrs.b("loop")) {
+          d.op = OP_MERGE_LOOP;
+          d.aux[0] = frame_id.at(n.attrs.s("frame"));
+        } else {
+          d.op = OP_MERGE;
+        }
+      } else if (op == "Enter") {
+        d.op = OP_ENTER;
+        d.aux[0] = frame_id.at(n.attrs.s("frame"));
+      } else if (op == "Exit") {
+        d.op = OP_EXIT;
+        d.aux[0] = frame_id.at(n.attrs.s("frame"));
+      } else if (op == "NextIteration") {
+        d.op = OP_NEXTITER;
+        d.aux[0] = frame_id.at(n.attrs.s("frame"));
+      } else if (op == "TACreate") {
+        d.op = OP_TA_CREATE;
+        d.aux[0] = ta_id.at(n.id);
+      } else if (op == "TARead") {
+        d.op = OP_TA_READ;
+      } else if (op == "TAWrite") {
+        d.op = OP_TA_WRITE;
+      } else if (op == "TAStack") {
+        d.op = OP_TA_STACK;
+      } else if (op == "TAUnstack") {
+        d.op = OP_TA_UNSTACK;
+      } else if (op == "TAGrad") {
+        d.op = OP_TA_GRAD;
+        d.aux[0] = trace_ta(TRef{n.id, 0});
+      } else if (op == "StackCreate") {
+        d.op = OP_STACK_CREATE;
+        d.aux[0] = stack_id.at(n.id);
+      } else if (op == "StackPush") {
+        d.op = OP_STACK_PUSH;
+      } else if (op == "StackPop") {
+        d.op = OP_STACK_POP;
+      } else if (odt == FLOW) {
+        d.op = OP_FLOW;
+      } else if (!is_heavy(n)) {
+        // integer / bool control arithmetic on the device driver
+        bool all_scalar = true;
+        for (auto& t : n.in) all_scalar &= g.shape(t).empty();
+        if (op == "ReduceMax" || op == "ReduceMin") {
+          if (g.shape(n.in[0]).size() != 1) unsupported(n, "integer reduction of rank != 1");
+          d.op = OP_REDUCE_I;
+          d.aux[0] = op == "ReduceMin";
+          d.aux[1] = (int)g.shape(n.in[0])[0];
+          d.aux[2] = dev_dt(g.dtype(n.in[0]), o.precision);
+        } else if (op == "Slice" && g.shape(n.in[0]).size() == 1) {
+          d.op = OP_SLICE_I;
+          int32_t dd = dev_dt(g.dtype(n.in[0]), o.precision);
+          d.imm[0] = n.attrs.v("begin").at(0) * dev_size(dd);
+          d.aux[1] = dd;
+        } else if (all_scalar) {
+          d.op = OP_SCALAR;
+          static const std::map<std::string, int> sc = {
+              {"Add", SC_ADD}, {"Sub", SC_SUB}, {"Mul", SC_MUL}, {"Less", SC_LESS},
+              {"LessEqual", SC_LEQ}, {"Greater", SC_GREATER}, {"Equal", SC_EQ},
+              {"LogicalAnd", SC_AND}, {"LogicalNot", SC_NOT}, {"Cast", SC_CAST}};
+          auto it = sc.find(op);
+          if (it == sc.end()) unsupported(n, "integer op not lowered");
+          d.aux[0] = it->second;
+          d.aux[1] = dev_dt(odt, o.precision);
+        } else {
+          unsupported(n, "non-scalar integer/bool tensor op");
+        }
+      } else {
+        d.op = OP_HEAVY;
+        heavy_nodes.push_back(n.id);
+        lower_heavy(n, d);
+      }
+      P.nodes[n.id] = d;
+    }
+    P.n_conds = max_cond + 1;
+
+    // ---- placements of heavy outputs
+    for (int nid : heavy_nodes) place_outputs(g.nodes[nid]);
+
+    // ---- evaluation orders
+    build_orders(bound);
+
+    // ---- fetches
+    for (auto& t : fetches) {
+      FetchInfo fi;
+      fi.vid = vid(t);
+      int32_t d = g.dtype(t);
+      fi.dev_dt = dev_dt(d, o.precision);
+      fi.bytes = numel(g.shape(t)) * dev_size(fi.dev_dt);
+      P.fetches.push_back(fi);
+      P.fetch_vids.push_back(fi.vid);
+    }
+
+    // ---- bounds for runtime pools
+    int64_t per_iter_heavy = 0, root_heavy = 0, max_tiles = 1;
+    std::vector<int64_t> frame_heavy(frame_ctx.size(), 0);
+    for (int nid : heavy_nodes) {
+      int f = frame_of[nid];
+      int k = g.nodes[nid].op == "LSTMCellGrad" ? 2 : 1;
+      if (f >= 0) frame_heavy[f] += k + 4;
+      else root_heavy += k + 1;
+    }
+    for (auto& n : g.nodes)
+      if (n.op == "TAWrite" || n.op == "TAStack" || n.op == "TAUnstack") {
+        int f = frame_of[n.id];
+        if (f >= 0) frame_heavy[f] += 2;
+        else root_heavy += 2;
+      }
+    int64_t total = root_heavy + 64 + (int64_t)fetches.size();
+    for (size_t f = 0; f < frame_ctx.size(); ++f) total += frame_heavy[f] * (bound[f] + 1);
+    (void)per_iter_heavy;
+    (void)max_tiles;
+    P.inst_bound = total + 1024;
+    P.branch_bound = 1;
+    for (auto b : bound) P.branch_bound = (int)std::max<int64_t>(P.branch_bound, b + 1);
+
+    // ---- describe
+    std::ostringstream ds;
+    ds << "nodes=" << N << " values=" << P.n_vids << " frames=" << frame_ctx.size()
+       << " tas=" << P.tas.size() << " stacks=" << P.stacks.size()
+       << " heavy_nodes=" << heavy_nodes.size() << " inst_bound=" << P.inst_bound << "\n";
+    size_t tot = 0;
+    for (auto& b : P.bufs) tot += b.bytes;
+    ds << "device bytes=" << tot << " buffers=" << P.bufs.size() << "\n";
+    for (size_t f = 0; f < frame_ctx.size(); ++f)
+      ds << "frame " << P.frame_names[f] << " K=" << P.frames[f].K << " bound=" << bound[f]
+         << " body=" << P.frames[f].n_body << "\n";
+    int counts[4] = {0, 0, 0, 0};
+    for (auto& pl : P.places) counts[pl.kind]++;
+    ds << "placements root=" << counts[0] << " ring=" << counts[1] << " arena=" << counts[2]
+       << " ta=" << counts[3] << "\n";
+    P.describe = ds.str();
+  }
+
+  void lower_heavy(const Node& n, DNode& d) {
+    const std::string& op = n.op;
+    auto ew = [&](int sub) {
+      d.aux[0] = HK_EW;
+      d.aux[1] = sub;
+      d.imm[0] = numel(n.osh[0]);
+      int flags = 0;
+      for (size_t j = 0; j < n.in.size() && j < 8; ++j)
+        if (g.shape(n.in[j]).empty() && !n.osh[0].empty()) flags |= 1 << j;
+      d.aux[2] = flags;
+    };
+    if (op == "Add") return ew(EW_ADD);
+    if (op == "Sub") return ew(EW_SUB);
+    if (op == "Mul") return ew(EW_MUL);
+    if (op == "Neg") return ew(EW_NEG);
+    if (op == "Sigmoid") return ew(EW_SIGMOID);
+    if (op == "Tanh") return ew(EW_TANH);
+    if (op == "Relu") return ew(EW_RELU);
+    if (op == "ReluGrad") return ew(EW_RELUGRAD);
+    if (op == "ZerosLike") return ew(EW_ZEROS);
+    if (op == "AddN") {
+      if (n.in.size() > 8) unsupported(n, "AddN of more than 8");
+      return ew(EW_ADDN);
+    }
+    if (op == "BiasAdd") {
+      ew(EW_BIASADD);
+      d.imm[1] = n.osh[0].at(1);
+      return;
+    }
+    if (op == "Select") {
+      ew(EW_SELECT);
+      d.imm[1] = g.shape(n.in[0]).empty() ? 0 : (n.osh[0].size() == 2 && g.shape(n.in[0]).size() == 1
+                                                     ? n.osh[0][1] : 1);
+      d.aux[3] = g.shape(n.in[0]).empty() ? 1 : 0;
+      return;
+    }
+    if (op == "Fill") {
+      d.aux[0] = HK_FILL;
+      d.imm[0] = numel(n.osh[0]);
+      return;
+    }
+    if (op == "ReduceSum") {
+      if (n.attrs.i("axis", -1) == 0) {
+        auto s = g.shape(n.in[0]);
+        if (s.size() != 2) unsupported(n, "ReduceSum(axis=0) needs rank 2");
+        d.aux[0] = HK_REDUCE_SUM0;
+        d.imm[0] = s[0];
+        d.imm[1] = s[1];
+      } else {
+        d.aux[0] = HK_REDUCE_SUM;
+        d.imm[0] = numel(g.shape(n.in[0]));
+      }
+      return;
+    }
+    if (op == "MatMul") {
+      d.aux[0] = HK_MATMUL;
+      d.aux[1] = (n.attrs.b("ta") ? 1 : 0) | (n.attrs.b("tb") ? 2 : 0);
+      auto sa = g.shape(n.in[0]), sb = g.shape(n.in[1]);
+      d.imm[0] = n.osh[0][0];
+      d.imm[1] = n.osh[0][1];
+      d.imm[2] = n.attrs.b("ta") ? sa[0] : sa[1];
+      d.imm[3] = sa[1] | (sb[1] << 32);   // leading dims of A and B
+      return;
+    }
+    if (op == "LSTMCell" || op == "LSTMCellGrad") {
+      d.aux[0] = op == "LSTMCell" ? HK_LSTM_FWD : HK_LSTM_BWD_EW;
+      d.aux[1] = n.attrs.b("masked");
+      d.imm[0] = g.shape(n.in[0])[0];
+      d.imm[1] = g.shape(n.in[0])[1];
+      d.imm[2] = g.shape(n.in[1])[1];
+      double fb = n.attrs.f("forget_bias", 0.0);
+      float ff = (float)fb;
+      int32_t fbits;
+      std::memcpy(&fbits, &ff, 4);
+      d.aux[2] = fbits;
+      return;
+    }
+    unsupported(n, "float op not lowered");
+  }
+
+  // routing closure of a value through control-flow primitives and views
+  void closure(int v0, bool* pinned, int* ta_write, int frame) {
+    std::set<int> seen{v0};
+    std::vector<std::pair<int, bool>> st{{v0, true}};   // (vid, same iteration)
+    *pinned = false;
+    *ta_write = -1;
+    while (!st.empty()) {
+      auto [v, same] = st.back();
+      st.pop_back();
+      for (auto [c, idx] : cons[v]) {
+        const Node& cn = g.nodes[c];
+        const std::string& op = cn.op;
+        if (op == "StackPush" && idx == 1) *pinned = true;
+        if (op == "TAWrite" && idx == 2 && same && frame_of[c] == frame && *ta_write < 0)
+          *ta_write = c;
+        bool route = op == "Identity" || op == "StopGradient" || op == "Reshape" ||
+                     op == "Switch" || op == "Merge" || op == "NextIteration" || op == "Exit";
+        if (!route || (op == "Switch" && idx != 0)) continue;
+        bool nsame = same && op != "NextIteration" && op != "Exit";
+        for (int p = 0; p < (int)cn.odt.size(); ++p) {
+          int w = vbase[c] + p;
+          if (seen.insert(w).second) st.push_back({w, nsame});
+        }
+      }
+    }
+  }
+
+  std::vector<int64_t> frame_bound_cache;
+
+  void place_outputs(const Node& n) {
+    DNode& d = P.nodes[n.id];
+    d.place_off = (int)P.places.size();
+    int f = frame_of[n.id];
+    int nout = (int)n.odt.size();
+    int extra = (n.op == "LSTMCellGrad") ? 1 : 0;   // dz scratch
+    for (int p = 0; p < nout + extra; ++p) {
+      PlaceDesc pl{};
+      Shape shp;
+      int32_t dd;
+      if (p < nout) {
+        shp = n.osh[p];
+        dd = dev_dt(n.odt[p], o.precision);
+      } else {
+        shp = {g.shape(n.in[0])[0], 4 * g.shape(n.in[1])[1]};
+        dd = D_F32;
+      }
+      pl.dt = dd;
+      pl.elem_bytes = numel(shp) * dev_size(dd);
+      int64_t alloc_elem = pl.elem_bytes;
+      if (n.op == "ReduceSum" && n.attrs.i("axis", -1) != 0) alloc_elem = 8192;  // scalar + partials at +4 KiB
+      pl.elem_bytes = alloc_elem;
+      bool pinned = false;
+      int taw = -1;
+      if (p < nout) closure(vbase[n.id] + p, &pinned, &taw, f);
+      if (f < 0) {
+        pl.kind = PL_ROOT;
+        pl.slots = 1;
+        pl.base = add_buf(alloc_elem, false, "root " + n.op + std::to_string(n.id));
+      } else if (taw >= 0 && P.tas[trace_ta(g.nodes[taw].in[0])].elem_bytes ==
+                                 numel(shp) * dev_size(dd) &&
+                 P.tas[trace_ta(g.nodes[taw].in[0])].dt == dd) {
+        const Node& w = g.nodes[taw];
+        pl.kind = PL_TA;
+        pl.ta = trace_ta(w.in[0]);
+        pl.index_vid = vid(w.in[1]);
+        pl.elem_bytes = numel(shp) * dev_size(dd);
+        // the write index and the handle must be evaluated before this heavy node
+        extra_edges[f].push_back({w.in[1].node, n.id});
+        extra_edges[f].push_back({w.in[0].node, n.id});
+      } else if (pinned) {
+        pl.kind = PL_ARENA;
+        pl.slots = -1;   // patched with the frame bound
+        pl.base = -1;
+      } else {
+        int K = o.parallel_iterations > 0 ? o.parallel_iterations : g.ctxs[frame_ctx[f]].K;
+        pl.kind = PL_RING;
+        pl.slots = K + 1;
+        pl.base = add_buf((size_t)alloc_elem * (K + 1), false, "ring " + n.op + std::to_string(n.id));
+      }
+      P.places.push_back(pl);
+    }
+  }
+
+  void build_orders(const std::vector<int64_t>& bound) {
+    const int N = (int)g.nodes.size();
+    // arena allocation needs the bound
+    for (int i = 0; i < N; ++i) {
+      const DNode& d = P.nodes[i];
+      if (d.op != OP_HEAVY) continue;
+      int f = frame_of[i];
+      int nout = d.n_out + (g.nodes[i].op == "LSTMCellGrad" ? 1 : 0);
+      for (int p = 0; p < nout; ++p) {
+        PlaceDesc& pl = P.places[d.place_off + p];
+        if (pl.kind == PL_ARENA) {
+          pl.slots = (int32_t)bound[f];
+          pl.base = add_buf((size_t)pl.elem_bytes * bound[f], false,
+                            "arena " + g.nodes[i].op + std::to_string(i));
+        }
+      }
+    }
+    // ---- frames
+    P.frames.resize(frame_ctx.size());
+    int iter_base = 0;
+    for (size_t f = 0; f < frame_ctx.size(); ++f) {
+      int c = frame_ctx[f];
+      const Ctx& ctx = g.ctxs[c];
+      std::vector<int> body, enters, exits;
+      for (int i = 0; i < N; ++i) {
+        if (frame_of[i] != (int)f) continue;
+        if (g.nodes[i].op == "Enter" && g.nodes[i].attrs.s("frame") == ctx.name) enters.push_back(i);
+        else body.push_back(i);
+      }
+      for (int i = 0; i < N; ++i)
+        if (g.nodes[i].op == "Exit" && g.nodes[i].attrs.s("frame") == ctx.name) exits.push_back(i);
+      std::set<int> bset(body.begin(), body.end());
+      std::map<int, std::vector<int>> succ;
+      std::map<int, int> indeg;
+      for (int i : body) indeg[i] = 0;
+      auto edge = [&](int a, int b) {
+        if (!bset.count(a) || !bset.count(b) || a == b) return;
+        succ[a].push_back(b);
+        indeg[b]++;
+      };
+      for (int i : body) {
+        const Node& n = g.nodes[i];
+        if (P.nodes[i].op == OP_MERGE_LOOP) continue;   // sources within an iteration
+        for (auto& t : n.in) edge(t.node, i);
+        for (int c : n.ctrl) edge(c, i);
+      }
+      for (auto& [a, b] : extra_edges[f]) edge(a, b);
+      std::vector<int> ord;
+      std::vector<int> ready;
+      for (int i : body)
+        if (indeg[i] == 0) ready.push_back(i);
+      std::sort(ready.rbegin(), ready.rend());
+      while (!ready.empty()) {
+        int v = ready.back();
+        ready.pop_back();
+        ord.push_back(v);
+        for (int w : succ[v])
+          if (--indeg[w] == 0) {
+            ready.push_back(w);
+            std::sort(ready.rbegin(), ready.rend());
+          }
+      }
+      if (ord.size() != body.size())
+        throw CfError(CF_E_INVALID_GRAPH, "frame " + ctx.name + " body has a cycle without NextIteration");
+      DFrame& F = P.frames[f];
+      F.K = o.parallel_iterations > 0 ? o.parallel_iterations : ctx.K;
+      F.bound = (int32_t)bound[f];
+      F.body_off = (int)P.order.size();
+      F.n_body = (int)ord.size();
+      P.order.insert(P.order.end(), ord.begin(), ord.end());
+      F.enter_off = (int)P.order.size();
+      F.n_enter = (int)enters.size();
+      P.order.insert(P.order.end(), enters.begin(), enters.end());
+      F.exit_off = (int)P.order.size();
+      F.n_exit = (int)exits.size();
+      P.order.insert(P.order.end(), exits.begin(), exits.end());
+      F.counter_switch = ctx.loop_vars.at(0).sw;
+      F.counter_enter = ctx.loop_vars.at(0).enter;
+      F.iter_base = iter_base;
+      iter_base += (int)bound[f] + 2;
+    }
+    P.iter_counters = iter_base;
+    // ---- root steps: root nodes + frames as super nodes
+    // item id: node i -> i ; frame f -> N + f
+    std::vector<int> items;
+    for (int i = 0; i < N; ++i)
+      if (frame_of[i] < 0 && g.nodes[i].op != "Exit") items.push_back(i);
+    for (size_t f = 0; f < frame_ctx.size(); ++f) items.push_back(N + (int)f);
+    auto item_of = [&](int node) -> int {
+      if (frame_of[node] >= 0) return N + frame_of[node];
+      if (g.nodes[node].op == "Exit") return N + frame_id.at(g.nodes[node].attrs.s("frame"));
+      return node;
+    };
+    std::map<int, std::set<int>> succ;
+    std::map<int, int> indeg;
+    for (int it : items) indeg[it] = 0;
+    auto edge = [&](int a, int b) {
+      if (a == b) return;
+      if (succ[a].insert(b).second) indeg[b]++;
+    };
+    for (int i = 0; i < N; ++i) {
+      int dst = item_of(i);
+      for (auto& t : g.nodes[i].in) edge(item_of(t.node), dst);
+      for (int c : g.nodes[i].ctrl) edge(item_of(c), dst);
+    }
+    // pops after pushes: frame that pushes precedes the frame that pops
+    for (auto& n : g.nodes) {
+      if (n.op != "StackPop") continue;
+      int sid = -1;
+      TRef h = n.in[0];
+      for (int k = 0; k < 64 && sid < 0; ++k) {
+        const Node& hn = g.nodes[h.node];
+        if (hn.op == "StackCreate") sid = hn.id;
+        else if (!hn.in.empty()) h = hn.in[0];
+        else break;
+      }
+      if (sid < 0) continue;
+      for (auto& m : g.nodes)
+        if (m.op == "StackPush") {
+          TRef hh = m.in[0];
+          for (int k = 0; k < 64; ++k) {
+            const Node& hn = g.nodes[hh.node];
+            if (hn.op == "StackCreate") {
+              if (hn.id == sid) edge(item_of(m.id), item_of(n.id));
+              break;
+            }
+            if (hn.in.empty()) break;
+            hh = hn.in[0];
+          }
+        }
+    }
+    std::vector<int> ready, ord;
+    for (int it : items)
+      if (indeg[it] == 0) ready.push_back(it);
+    std::sort(ready.rbegin(), ready.rend());
+    while (!ready.empty()) {
+      int v = ready.back();
+      ready.pop_back();
+      ord.push_back(v);
+      for (int w : succ[v])
+        if (--indeg[w] == 0) {
+          ready.push_back(w);
+          std::sort(ready.rbegin(), ready.rend());
+        }
+    }
+    if (ord.size() != items.size()) throw CfError(CF_E_INVALID_GRAPH, "root graph has a cycle");
+    for (int it : ord) P.root_steps.push_back(it >= N ? -(it - N + 1) : it);
+  }
+};
+
+}  // namespace
+
+HostProgram compile(const Graph& g, const CompileOpts& o, const std::vector<TRef>& fetches) {
+  auto errs = g.validate();
+  if (!errs.empty()) throw CfError(CF_E_INVALID_GRAPH, errs[0]);
+  Compiler c(g, o);
+  c.run(fetches);
+  return std::move(c.P);
+}
+
+}  // namespace cf

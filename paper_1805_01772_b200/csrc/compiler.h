@@ -1,0 +1,66 @@
+// Host compiler: cf::Graph -> device program (program.h) + buffer plan.
+#pragma once
+#include <map>
+#include <string>
+#include <vector>
+
+#include "ir.h"
+#include "program.h"
+
+namespace cf {
+
+struct BufPlan {
+  size_t bytes = 0;
+  bool zero = false;                 // zero-filled at every run start
+  std::vector<uint8_t> init;         // uploaded once (constants)
+  std::string what;
+};
+
+struct FeedInfo {
+  int vid = -1;
+  int32_t graph_dt = 0;
+  int32_t dev_dt = 0;
+  int64_t bytes = 0;
+  bool scalar_ctrl = false;
+};
+
+struct FetchInfo {
+  int vid = -1;
+  int32_t dev_dt = 0;
+  int64_t bytes = 0;
+};
+
+struct HostProgram {
+  std::vector<cfdev::DNode> nodes;
+  std::vector<int32_t> in_vids;
+  std::vector<cfdev::PlaceDesc> places;
+  std::vector<cfdev::DFrame> frames;
+  std::vector<int32_t> order;
+  std::vector<int32_t> root_steps;
+  std::vector<cfdev::DTA> tas;
+  std::vector<cfdev::DStack> stacks;
+  std::vector<int32_t> fetch_vids;
+  std::vector<std::string> frame_names;
+  int n_vids = 0;
+  int n_conds = 0;
+  int branch_bound = 1;
+  int iter_counters = 0;
+  int stack_pool = 0;
+  int ta_slots = 0;
+  int64_t inst_bound = 0;            // upper bound of heavy instances per run
+  int64_t tile_bound = 0;            // max tiles of one instance
+  std::vector<BufPlan> bufs;
+  std::map<std::string, FeedInfo> feeds;
+  std::vector<FetchInfo> fetches;
+  std::string describe;
+};
+
+struct CompileOpts {
+  int32_t precision = CF_F32;
+  int32_t parallel_iterations = 0;
+  int64_t max_iterations = 0;
+};
+
+HostProgram compile(const Graph& g, const CompileOpts& o, const std::vector<TRef>& fetches);
+
+}  // namespace cf

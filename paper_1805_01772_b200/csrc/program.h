@@ -1,0 +1,216 @@
+// Device program: what the host compiler (compiler.cpp) hands to the persistent driver
+// kernel (runtime.cu). Plain structs, identical layout on host and device.
+#pragma once
+#include <cstdint>
+
+namespace cfdev {
+
+// ---- token: the device form of the paper's (value, is_dead, tag) tuple.
+// The tag is implicit: the driver evaluates one iteration of a frame at a time, so every
+// token in the table belongs to the current (frame, iteration); tensors flowing across
+// iterations carry their storage address, which encodes the producing iteration.
+enum TokKind : uint8_t { TK_UNSET = 0, TK_IMM = 1, TK_PTR = 2, TK_HANDLE = 3, TK_FLOW = 4 };
+enum DevDT : uint8_t { D_BOOL = 0, D_I32 = 1, D_I64 = 2, D_F32 = 3, D_BF16 = 5, D_NONE = 7 };
+
+struct Tok {
+  int64_t v;       // immediate scalar, device address, or handle id
+  int32_t writer;  // heavy instance producing the bytes at v (-1: ready)
+  uint8_t dead;
+  uint8_t kind;
+  uint8_t dt;
+  uint8_t pad;
+};
+static_assert(sizeof(Tok) == 16, "Tok layout");
+
+// ---- interpreter opcodes
+enum Op : int32_t {
+  OP_NOP = 0,
+  OP_PLACEHOLDER,   // token preset at run start
+  OP_CONST,         // aux0: 1 = immediate scalar (imm0), 0 = pointer (imm0 = device address)
+  OP_PASS,          // Identity / StopGradient / Reshape (views)
+  OP_SWITCH,        // aux0: cond_id (-1 loop), aux1: is loop switch
+  OP_MERGE,         // cond merge
+  OP_MERGE_LOOP,    // aux0: frame; in0 = Enter, in1 = NextIteration
+  OP_ENTER,         // aux0: frame
+  OP_EXIT,          // aux0: frame
+  OP_NEXTITER,      // aux0: frame
+  OP_SCALAR,        // aux0: scalar sub-op (SC_*)
+  OP_REDUCE_I,      // aux0: 0 max, 1 min; aux1: element count
+  OP_SLICE_I,       // 1-D int/bool slice view: imm0 = byte offset
+  OP_FLOW,          // flow-valued arithmetic (Add/AddN/Const/ZerosLike of flows)
+  OP_TA_CREATE,     // aux0: ta id
+  OP_TA_READ,       // aux0: ta id (static, for checks)
+  OP_TA_WRITE,
+  OP_TA_STACK,
+  OP_TA_UNSTACK,
+  OP_TA_GRAD,       // aux0: grad ta id
+  OP_STACK_CREATE,  // aux0: stack id
+  OP_STACK_PUSH,
+  OP_STACK_POP,
+  OP_HEAVY,         // aux0: heavy kind (HK_*), aux1: sub-op / flags
+  OP__COUNT
+};
+
+enum ScalarOp : int32_t {
+  SC_ADD = 0, SC_SUB, SC_MUL, SC_LESS, SC_LEQ, SC_GREATER, SC_EQ, SC_AND, SC_NOT, SC_CAST
+};
+
+// ---- heavy work kinds (executed by worker CTAs, tiled)
+enum HeavyKind : int32_t {
+  HK_NOP = 0,       // join: completes when its dependencies complete (0 tiles)
+  HK_EW,            // elementwise; sub = EW_*
+  HK_FILL,          // out[i] = scalar at p1 (or imm)
+  HK_COPY,          // bytes
+  HK_REDUCE_SUM,    // all elements -> scalar (deterministic two-level)
+  HK_REDUCE_SUM0,   // [M,N] -> [N]
+  HK_MATMUL,        // sub bit0 ta, bit1 tb
+  HK_LSTM_FWD,      // fused LSTM cell (sub bit0: masked)
+  HK_LSTM_BWD_EW,   // dz, dc_prev
+  HK_LSTM_BWD_MM,   // dxh = dz W, dW = dz^T [x,h], db = colsum dz
+  HK_ACC,           // dst += src (grad TensorArray double write)
+  HK__COUNT
+};
+
+enum EwOp : int32_t {
+  EW_ADD = 0, EW_SUB, EW_MUL, EW_NEG, EW_SIGMOID, EW_TANH, EW_RELU, EW_RELUGRAD,
+  EW_BIASADD, EW_SELECT, EW_ADDN, EW_ZEROS
+};
+
+// ---- placement of a heavy output (SURVEY.md §7.2 "static buffer pointer per (edge, slot)")
+enum Place : int32_t { PL_ROOT = 0, PL_RING = 1, PL_ARENA = 2, PL_TA = 3 };
+
+struct PlaceDesc {
+  int32_t kind;
+  int32_t slots;       // RING: R = K + 1; ARENA: frame iteration bound
+  int32_t ta;          // PL_TA: static TensorArray id
+  int32_t index_vid;   // PL_TA: value id of the write index
+  int64_t base;        // device address (ROOT / RING / ARENA)
+  int64_t elem_bytes;
+  int32_t dt;          // DevDT of the stored elements
+  int32_t pad;
+};
+
+struct DNode {
+  int32_t op;
+  int32_t n_in;
+  int32_t in_off;      // into prog.in_vids
+  int32_t n_ctrl;
+  int32_t ctrl_off;    // into prog.in_vids (value ids of producers' ctrl tokens)
+  int32_t n_out;
+  int32_t out_vid;     // first output value id
+  int32_t ctrl_vid;    // this node's own ctrl token
+  int32_t place_off;   // into prog.places (n_out entries) for heavy nodes; -1 otherwise
+  int32_t aux[7];
+  int64_t imm[4];      // op-specific sizes / constants
+};
+static_assert(sizeof(DNode) % 8 == 0, "DNode layout");
+
+struct DFrame {
+  int32_t K;            // parallel_iterations
+  int32_t bound;        // iteration bound (arena slots / stack capacity)
+  int32_t body_off, n_body;     // node ids in evaluation order, into prog.order
+  int32_t enter_off, n_enter;   // Enter node ids
+  int32_t exit_off, n_exit;     // Exit node ids
+  int32_t counter_switch;       // node id of the hidden counter's Switch
+  int32_t counter_enter;        // node id of the hidden counter's Enter
+  int32_t iter_base;            // offset into per-iteration counters (size bound + 1)
+  int32_t pad;
+};
+
+struct DTA {
+  int64_t base;         // static buffer (device)
+  int64_t elem_bytes;
+  int32_t size;
+  int32_t is_grad;
+  int32_t grad_id;      // id of its gradient TA (-1 none)
+  int32_t dt;
+};
+
+struct DStack {
+  int32_t capacity;
+  int32_t entry_off;    // into the stack entry pool (Tok)
+};
+
+// Root program step: a node id (>= 0) or a frame (-(frame + 1)).
+struct Prog {
+  int32_t n_nodes, n_vids, n_frames, n_tas, n_stacks;
+  int32_t n_root_steps;
+  int32_t n_fetch;
+  int32_t n_conds;
+  int32_t branch_bound;         // iterations recorded per cond in the branch-bit array
+  int32_t pad;
+  const DNode* nodes;
+  const int32_t* in_vids;
+  const PlaceDesc* places;
+  const DFrame* frames;
+  const int32_t* order;         // frame bodies / enters / exits
+  const int32_t* root_steps;
+  const DTA* tas;
+  const DStack* stacks;
+  const int32_t* fetch_vids;
+};
+
+// ---- heavy instance record (written by the driver, read by workers)
+struct Inst {
+  int32_t kind, sub;
+  int32_t ntiles, frame;
+  int32_t iter, pad;
+  int64_t n, m, k;      // sizes
+  int64_t p[14];        // pointers
+  int64_t s[4];         // scalars
+};
+
+// ---- run-time state shared by the driver CTA and the worker CTAs
+struct RunState {
+  // job queue: entries = (inst << 20 | tile) encoded as uint64; tail published by driver
+  unsigned long long q_head;     // claimed by workers (atomicAdd)
+  unsigned long long q_tail;     // published by driver (release)
+  unsigned long long q_done;     // tiles finished (for ring capacity)
+  int32_t quit;                  // 1 = workers exit
+  int32_t error;                 // cf_status from the device
+  unsigned long long cq_tail;    // completion queue reserve (workers)
+  unsigned long long cq_head;    // consumed by driver
+  int64_t error_info;
+  // trace
+  int32_t trip[16];
+  int32_t max_inflight[16];
+  long long pushes, pops;
+  int32_t max_depth, exit_fires;
+  long long instances, tiles, dead_skipped;
+  unsigned long long t_start, t_end;
+};
+
+struct RunArgs {
+  Prog prog;
+  RunState* st;
+  Tok* toks;                 // [n_vids]
+  Tok* stack_pool;           // stack entries
+  int32_t* stack_depth;      // [n_stacks]
+  int64_t* ta_base;          // [n_tas] runtime base (may alias on unstack)
+  int32_t* ta_writer;        // [sum sizes] per-slot writer instance
+  uint8_t* ta_written;       // [sum sizes]
+  int32_t* ta_slot_off;      // [n_tas] offset into ta_writer / ta_written
+  Inst* insts;               // [inst_cap]
+  int32_t inst_cap;
+  int32_t* inst_pending;     // deps outstanding
+  uint8_t* inst_done;
+  int32_t* inst_tiles_done;  // atomic per instance
+  int32_t* succ_head;        // per instance edge list head (-1)
+  int32_t* edge_next;        // [edge_cap]
+  int32_t* edge_to;
+  int32_t edge_cap;
+  unsigned long long* queue; // [q_cap]
+  unsigned long long q_cap;
+  int32_t* cq;               // [cq_cap] completion queue (inst + 1; 0 = empty)
+  unsigned long long cq_cap;
+  int32_t* iter_outstanding; // per frame iteration
+  uint8_t* branch_bits;      // [n_conds * branch_bound]
+  void** fetch_out;          // caller buffers
+  uint8_t* fetch_dead;
+  int64_t* fetch_bytes;
+  int64_t watchdog_ns;
+  int32_t sched_seed;
+  int32_t num_workers;
+};
+
+}  // namespace cfdev

@@ -1,0 +1,1667 @@
+// libcf device runtime: ONE persistent kernel per cf_run.
+//
+//   block 0, thread 0  -- the device-resident loop driver: the paper's local executor
+//                          moved onto the GPU. It evaluates every control
+//                         node (Switch/Merge/Enter/Exit/NextIteration, the loop predicate,
+//                         TensorArray and Stack bookkeeping) with the evaluation rules of
+//                         PAPER.md:712-735, skips dead work, admits
+//                         iteration i only when i - oldest_incomplete < K
+//                         and turns every live float op into a tiled "heavy instance" whose
+//                         dependencies it tracks. No host round trip per iteration.
+//   blocks 1..G-1      -- workers: claim tiles from the job queue in publication order,
+//                         execute them, report instance completion.
+//
+// The driver publishes an instance only when all its producers completed, so workers never
+// wait on data; ordering is release (worker) -> acquire (driver) -> release (driver) ->
+// acquire (worker), with __threadfence() (which also invalidates L1) on both sides.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "compiler.h"
+#include "ir.h"
+#include "program.h"
+
+using namespace cfdev;
+
+namespace cf {
+void set_error(const std::string& m);
+}
+const cf::Graph& cf_graph_ir(const cf_graph* g);
+
+#define CUDA_OK(x)                                                                       \
+  do {                                                                                   \
+    cudaError_t e_ = (x);                                                                \
+    if (e_ != cudaSuccess)                                                               \
+      throw cf::CfError(CF_E_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_));     \
+  } while (0)
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kEwTile = 4096;
+
+// ----------------------------------------------------------------------------- helpers
+__device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long* p) {
+  return *(volatile const unsigned long long*)p;
+}
+__device__ __forceinline__ int ld_volatile_i32(const int* p) { return *(volatile const int*)p; }
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void backoff(int& n) {
+  if (n < 8) {
+    ++n;
+    return;
+  }
+  __nanosleep(n < 64 ? 32 : 256);
+  if (n < 64) ++n;
+}
+
+__device__ __forceinline__ float sigm(float x) { return 1.0f / (1.0f + __expf(-x)); }
+__device__ __forceinline__ float tanh_f(float x) { return tanhf(x); }
+
+// ----------------------------------------------------------------------------- worker tiles
+template <class LA, class LB, class EP>
+__device__ void gemm_tile64(float* sm, int m0, int n0, int M, int N, int K, LA la, LB lb, EP ep) {
+  float* As = sm;            // [16][64]
+  float* Bs = sm + 16 * 64;  // [16][64]
+  const int tid = threadIdx.x;
+  const int ty = tid / 16, tx = tid % 16;
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < K; k0 += 16) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      int idx = tid + i * 256;
+      int kk = idx / 64, mm = idx % 64;
+      int m = m0 + mm, k = k0 + kk;
+      As[kk * 64 + mm] = (m < M && k < K) ? la(m, k) : 0.0f;
+      int n = n0 + mm;
+      Bs[kk * 64 + mm] = (n < N && k < K) ? lb(k, n) : 0.0f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      float a[4], b[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        a[j] = As[kk * 64 + ty * 4 + j];
+        b[j] = Bs[kk * 64 + tx * 4 + j];
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int m = m0 + ty * 4 + i, n = n0 + tx * 4 + j;
+      if (m < M && n < N) ep(m, n, acc[i][j]);
+    }
+}
+
+__device__ void tile_ew(const Inst& I, int tile) {
+  const int64_t n = I.n;
+  const int64_t b0 = (int64_t)tile * kEwTile;
+  const int64_t e1 = min(n, b0 + kEwTile);
+  const int op = I.sub;
+  const int flags = (int)I.s[1];
+  float* out = (float*)I.p[13];
+  auto in = [&](int j, int64_t e) -> float {
+    const float* p = (const float*)I.p[j];
+    return (flags >> j & 1) ? p[0] : p[e];
+  };
+  for (int64_t e = b0 + threadIdx.x; e < e1; e += kThreads) {
+    float r = 0.0f;
+    switch (op) {
+      case EW_ADD: r = in(0, e) + in(1, e); break;
+      case EW_SUB: r = in(0, e) - in(1, e); break;
+      case EW_MUL: r = in(0, e) * in(1, e); break;
+      case EW_NEG: r = -in(0, e); break;
+      case EW_SIGMOID: r = 1.0f / (1.0f + expf(-in(0, e))); break;
+      case EW_TANH: r = tanhf(in(0, e)); break;
+      case EW_RELU: r = fmaxf(in(0, e), 0.0f); break;
+      case EW_RELUGRAD: r = in(1, e) > 0.0f ? in(0, e) : 0.0f; break;
+      case EW_BIASADD: r = in(0, e) + ((const float*)I.p[1])[e % I.m]; break;
+      case EW_SELECT: {
+        const uint8_t* c = (const uint8_t*)I.p[0];
+        bool cv = I.s[2] ? c[0] != 0 : (I.m > 0 ? c[e / I.m] != 0 : c[e] != 0);
+        r = cv ? in(1, e) : in(2, e);
+        break;
+      }
+      case EW_ADDN: {
+        for (int j = 0; j < (int)I.s[0]; ++j) r += in(j, e);
+        break;
+      }
+      case EW_ZEROS: r = 0.0f; break;
+    }
+    out[e] = r;
+  }
+}
+
+__device__ void tile_fill(const Inst& I, int tile) {
+  float v = I.p[0] ? *(const float*)I.p[0] : __int_as_float((int)I.s[0]);
+  float* out = (float*)I.p[13];
+  int64_t b0 = (int64_t)tile * kEwTile, e1 = min(I.n, b0 + kEwTile);
+  for (int64_t e = b0 + threadIdx.x; e < e1; e += kThreads) out[e] = v;
+}
+
+__device__ void tile_copy(const Inst& I, int tile) {
+  // I.n bytes; 64 KiB per tile
+  const int64_t chunk = 65536;
+  int64_t b0 = (int64_t)tile * chunk, e1 = min(I.n, b0 + chunk);
+  const uint8_t* src = (const uint8_t*)I.p[0];
+  uint8_t* dst = (uint8_t*)I.p[13];
+  bool aligned = ((I.p[0] | I.p[13]) & 15) == 0;
+  if (aligned) {
+    int64_t v0 = b0 / 16, v1 = e1 / 16;
+    for (int64_t e = v0 + threadIdx.x; e < v1; e += kThreads)
+      ((int4*)dst)[e] = ((const int4*)src)[e];
+    for (int64_t e = v1 * 16 + threadIdx.x; e < e1; e += kThreads) dst[e] = src[e];
+  } else {
+    for (int64_t e = b0 + threadIdx.x; e < e1; e += kThreads) dst[e] = src[e];
+  }
+}
+
+__device__ void tile_acc(const Inst& I, int tile) {
+  const float* src = (const float*)I.p[0];
+  float* dst = (float*)I.p[13];
+  int64_t b0 = (int64_t)tile * kEwTile, e1 = min(I.n, b0 + kEwTile);
+  for (int64_t e = b0 + threadIdx.x; e < e1; e += kThreads) dst[e] += src[e];
+}
+
+__device__ float block_sum(float v, float* red) {
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  float s = 0.0f;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < kThreads / 32; ++w) s += red[w];
+  __syncthreads();
+  return s;
+}
+
+// deterministic: tile t sums a fixed contiguous chunk; the last tile sums partials in order
+__device__ void tile_reduce_sum(const Inst& I, int tile, float* sm) {
+  const float* x = (const float*)I.p[0];
+  float* out = (float*)I.p[13];
+  float* partial = out + 1024;   // placement reserves 1024 partial floats at +4 KiB
+  int64_t chunk = (I.n + I.ntiles - 1) / I.ntiles;
+  int64_t b0 = (int64_t)tile * chunk, e1 = min(I.n, b0 + chunk);
+  float s = 0.0f;
+  for (int64_t e = b0 + threadIdx.x; e < e1; e += kThreads) s += x[e];
+  s = block_sum(s, sm);
+  if (threadIdx.x == 0) partial[tile] = s;
+}
+__device__ void finalize_reduce_sum(const Inst& I, float* sm) {
+  float* out = (float*)I.p[13];
+  const volatile float* partial = out + 1024;
+  if (threadIdx.x == 0) {
+    float s = 0.0f;
+    for (int t = 0; t < I.ntiles; ++t) s += partial[t];
+    out[0] = s;
+  }
+  (void)sm;
+}
+
+__device__ void tile_reduce_sum0(const Inst& I, int tile) {
+  const float* x = (const float*)I.p[0];
+  float* out = (float*)I.p[13];
+  int64_t M = I.m, N = I.n;
+  int64_t c = (int64_t)tile * kThreads + threadIdx.x;
+  if (c >= N) return;
+  float s = 0.0f;
+  for (int64_t r = 0; r < M; ++r) s += x[r * N + c];
+  out[c] = s;
+}
+
+__device__ void tile_matmul(const Inst& I, int tile, float* sm) {
+  int M = (int)I.m, N = (int)I.n, K = (int)I.k;
+  bool ta = I.sub & 1, tb = I.sub & 2;
+  int64_t lda = I.s[0], ldb = I.s[1];
+  const float* A = (const float*)I.p[0];
+  const float* B = (const float*)I.p[1];
+  float* C = (float*)I.p[13];
+  int tn = (N + 63) / 64;
+  int m0 = (tile / tn) * 64, n0 = (tile % tn) * 64;
+  gemm_tile64(
+      sm, m0, n0, M, N, K,
+      [&](int m, int k) { return ta ? A[(int64_t)k * lda + m] : A[(int64_t)m * lda + k]; },
+      [&](int k, int n) { return tb ? B[(int64_t)n * ldb + k] : B[(int64_t)k * ldb + n]; },
+      [&](int m, int n, float v) { C[(int64_t)m * N + n] = v; });
+}
+
+// Fused LSTM cell forward (reading R9): tile = 32 batch rows x 32 hidden units; each thread
+// owns 4 rows x 1 unit x all 4 gates, so the sigma/tanh/state epilogue is thread-local.
+__device__ void tile_lstm_fwd(const Inst& I, int tile, float* sm) {
+  const int B = (int)I.m, In = (int)I.k, H = (int)I.n;
+  const int KT = In + H;
+  const float* x = (const float*)I.p[0];
+  const float* h = (const float*)I.p[1];
+  const float* c = (const float*)I.p[2];
+  const float* W = (const float*)I.p[3];
+  const float* bias = (const float*)I.p[4];
+  const int64_t* lens = (const int64_t*)I.p[5];
+  float* h_next = (float*)I.p[8];
+  float* c_next = (float*)I.p[9];
+  float* out = (float*)I.p[10];
+  float* gates = (float*)I.p[11];
+  const bool masked = I.sub & 1;
+  const int64_t t = I.s[0];
+  const float fbias = __int_as_float((int)I.s[1]);
+  const int n_ut = (H + 31) / 32;
+  const int r0 = (tile / n_ut) * 32, u0 = (tile % n_ut) * 32;
+  float* Xs = sm;               // [32 k][33]
+  float* Ws = sm + 32 * 33;     // [32 k][129]
+  const int tid = threadIdx.x, ty = tid / 32, tx = tid % 32;
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < KT; k0 += 32) {
+    for (int idx = tid; idx < 32 * 32; idx += kThreads) {
+      int rr = idx / 32, kk = idx % 32;
+      int r = r0 + rr, k = k0 + kk;
+      float v = 0.0f;
+      if (r < B && k < KT) v = k < In ? x[(int64_t)r * In + k] : h[(int64_t)r * H + (k - In)];
+      Xs[kk * 33 + rr] = v;
+    }
+    for (int idx = tid; idx < 128 * 32; idx += kThreads) {
+      int col = idx / 32, kk = idx % 32;
+      int g = col / 32, u = u0 + col % 32, k = k0 + kk;
+      Ws[kk * 129 + col] = (u < H && k < KT) ? W[(int64_t)(g * H + u) * KT + k] : 0.0f;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int kk = 0; kk < 32; ++kk) {
+      float a[4], w[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) a[j] = Xs[kk * 33 + ty * 4 + j];
+#pragma unroll
+      for (int g = 0; g < 4; ++g) w[g] = Ws[kk * 129 + g * 32 + tx];
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int g = 0; g < 4; ++g) acc[j][g] = fmaf(a[j], w[g], acc[j][g]);
+    }
+    __syncthreads();
+  }
+  const int u = u0 + tx;
+  if (u >= H) return;
+  const float bi = bias[u], bf = bias[H + u], bg = bias[2 * H + u], bo = bias[3 * H + u];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int r = r0 + ty * 4 + j;
+    if (r >= B) continue;
+    const int64_t o = (int64_t)r * H + u;
+    float ig = 1.0f / (1.0f + expf(-(acc[j][0] + bi)));
+    float fg = 1.0f / (1.0f + expf(-(acc[j][1] + bf + fbias)));
+    float gg = tanhf(acc[j][2] + bg);
+    float og = 1.0f / (1.0f + expf(-(acc[j][3] + bo)));
+    float cp = c[o];
+    float cn = fg * cp + ig * gg;
+    float hn = og * tanhf(cn);
+    bool live = !masked || t < lens[r];
+    h_next[o] = live ? hn : h[o];
+    c_next[o] = live ? cn : cp;
+    out[o] = live ? hn : 0.0f;
+    float* gr = gates + (int64_t)r * 4 * H;
+    gr[u] = ig;
+    gr[H + u] = fg;
+    gr[2 * H + u] = gg;
+    gr[3 * H + u] = og;
+  }
+}
+
+// LSTM cell backward, elementwise part: dz (pre-activation grads) and dc_prev.
+__device__ void tile_lstm_bwd_ew(const Inst& I, int tile) {
+  const int B = (int)I.m, H = (int)I.n;
+  const float* c = (const float*)I.p[2];
+  const float* gates = (const float*)I.p[4];
+  const int64_t* lens = (const int64_t*)I.p[5];
+  const float* dhn = (const float*)I.p[6];
+  const float* dcn = (const float*)I.p[7];
+  const float* dout = (const float*)I.p[8];
+  float* dc = (float*)I.p[9];
+  float* dz = (float*)I.p[10];
+  const bool masked = I.sub & 1;
+  const int64_t t = I.s[0];
+  int64_t b0 = (int64_t)tile * kEwTile, e1 = min((int64_t)B * H, b0 + kEwTile);
+  for (int64_t e = b0 + threadIdx.x; e < e1; e += kThreads) {
+    int64_t r = e / H, u = e % H;
+    const float* gr = gates + r * 4 * H;
+    float ig = gr[u], fg = gr[H + u], gg = gr[2 * H + u], og = gr[3 * H + u];
+    float cp = c[e];
+    float cn = fg * cp + ig * gg;
+    float tc = tanhf(cn);
+    float dh = dhn[e] + dout[e];
+    float dcs = dh * og * (1.0f - tc * tc) + dcn[e];
+    float dzi = dcs * gg * ig * (1.0f - ig);
+    float dzf = dcs * cp * fg * (1.0f - fg);
+    float dzg = dcs * ig * (1.0f - gg * gg);
+    float dzo = dh * tc * og * (1.0f - og);
+    float dcp = dcs * fg;
+    if (masked && !(t < lens[r])) {
+      dzi = dzf = dzg = dzo = 0.0f;
+      dcp = dcn[e];
+    }
+    float* zr = dz + r * 4 * H;
+    zr[u] = dzi;
+    zr[H + u] = dzf;
+    zr[2 * H + u] = dzg;
+    zr[3 * H + u] = dzo;
+    dc[e] = dcp;
+  }
+}
+
+// LSTM cell backward, contractions: d[x,h] = dz W ; dW = dz^T [x,h] ; db = colsum(dz).
+__device__ void tile_lstm_bwd_mm(const Inst& I, int tile, float* sm) {
+  const int B = (int)I.m, In = (int)I.k, H = (int)I.n, KT = In + H, G = 4 * H;
+  const float* x = (const float*)I.p[0];
+  const float* h = (const float*)I.p[1];
+  const float* W = (const float*)I.p[3];
+  const int64_t* lens = (const int64_t*)I.p[5];
+  const float* dhn = (const float*)I.p[6];
+  const float* dz = (const float*)I.p[10];
+  float* dx = (float*)I.p[11];
+  float* dh = (float*)I.p[12];
+  float* dW = (float*)I.p[13];
+  float* db = (float*)I.s[3];
+  const bool masked = I.sub & 1;
+  const int64_t t = I.s[0];
+  const int tA = ((B + 63) / 64) * ((KT + 63) / 64);
+  const int tB = ((G + 63) / 64) * ((KT + 63) / 64);
+  if (tile < tA) {
+    int tn = (KT + 63) / 64;
+    int m0 = (tile / tn) * 64, n0 = (tile % tn) * 64;
+    gemm_tile64(
+        sm, m0, n0, B, KT, G, [&](int m, int k) { return dz[(int64_t)m * G + k]; },
+        [&](int k, int n) { return W[(int64_t)k * KT + n]; },
+        [&](int m, int n, float v) {
+          if (n < In) {
+            dx[(int64_t)m * In + n] = v;
+          } else {
+            int64_t o = (int64_t)m * H + (n - In);
+            dh[o] = (masked && !(t < lens[m])) ? dhn[o] : v;
+          }
+        });
+  } else if (tile < tA + tB) {
+    int tt = tile - tA;
+    int tn = (KT + 63) / 64;
+    int m0 = (tt / tn) * 64, n0 = (tt % tn) * 64;
+    gemm_tile64(
+        sm, m0, n0, G, KT, B, [&](int m, int k) { return dz[(int64_t)k * G + m]; },
+        [&](int k, int n) { return n < In ? x[(int64_t)k * In + n] : h[(int64_t)k * H + (n - In)]; },
+        [&](int m, int n, float v) { dW[(int64_t)m * KT + n] = v; });
+  } else {
+    int tt = tile - tA - tB;
+    int col = tt * kThreads + threadIdx.x;
+    if (col < G) {
+      float s = 0.0f;
+      for (int r = 0; r < B; ++r) s += dz[(int64_t)r * G + col];
+      db[col] = s;
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------- driver
+enum EvalResult { EV_OK = 0, EV_BLOCKED = 1, EV_ERROR = 2 };
+
+struct Driver {
+  const RunArgs& A;
+  const Prog& P;
+  RunState* st;
+  int32_t ninst = 0, nedge = 0;
+  unsigned long long q_tail = 0, cq_head = 0;
+  int64_t outstanding = 0;     // created - completed
+  int32_t root_pc = 0, cur_frame = -1, iter = 0, body_pc = 0;
+  bool iter_started = false, fetched = false;
+  int32_t oldest = 0;
+  unsigned long long last_progress = 0;
+
+  __device__ Driver(const RunArgs& a) : A(a), P(a.prog), st(a.st) {}
+
+  __device__ void fail(int code, int64_t info) {
+    if (st->error == 0) {
+      st->error = code;
+      st->error_info = info;
+    }
+  }
+
+  __device__ Tok& tok(int vid) { return A.toks[vid]; }
+  __device__ const DNode& node(int id) { return P.nodes[id]; }
+  __device__ int in_vid(const DNode& d, int j) { return P.in_vids[d.in_off + j]; }
+  __device__ Tok& in_tok(const DNode& d, int j) { return A.toks[in_vid(d, j)]; }
+
+  __device__ bool writer_done(int32_t w) { return w < 0 || *(volatile uint8_t*)&A.inst_done[w]; }
+
+  // scalar value of a token; false if its bytes are not produced yet
+  __device__ bool scalar(const Tok& t, int64_t* out) {
+    if (t.kind == TK_IMM) {
+      *out = t.v;
+      return true;
+    }
+    if (t.kind != TK_PTR) {
+      *out = 0;
+      return true;
+    }
+    if (!writer_done(t.writer)) return false;
+    __threadfence();
+    switch (t.dt) {
+      case D_BOOL: *out = *(const volatile uint8_t*)t.v; break;
+      case D_I32: *out = *(const volatile int32_t*)t.v; break;
+      case D_I64: *out = *(const volatile int64_t*)t.v; break;
+      case D_F32: {
+        float f = *(const volatile float*)t.v;
+        *out = (int64_t)f;
+        break;
+      }
+      default: *out = 0;
+    }
+    return true;
+  }
+
+  __device__ void set_out(const DNode& d, int port, const Tok& t) { A.toks[d.out_vid + port] = t; }
+  __device__ void set_dead_all(const DNode& d) {
+    for (int p = 0; p < d.n_out; ++p) {
+      Tok t{};
+      t.dead = 1;
+      t.writer = -1;
+      A.toks[d.out_vid + p] = t;
+    }
+  }
+
+  // ---------------------------------------------------------------- instances
+  __device__ int32_t new_inst(int kind, int sub, int ntiles) {
+    if (ninst >= A.inst_cap) {
+      fail(CF_E_STACK_BUDGET, -1);
+      return -1;
+    }
+    int32_t id = ninst++;
+    Inst& I = A.insts[id];
+    I.kind = kind;
+    I.sub = sub;
+    I.ntiles = max(ntiles, 1);
+    I.frame = cur_frame;
+    I.iter = cur_frame >= 0 ? iter : 0;
+    for (int j = 0; j < 14; ++j) I.p[j] = 0;
+    for (int j = 0; j < 4; ++j) I.s[j] = 0;
+    I.n = I.m = I.k = 0;
+    A.inst_pending[id] = 0;
+    A.succ_head[id] = -1;
+    A.inst_done[id] = 0;
+    return id;
+  }
+  __device__ void add_dep(int32_t id, int32_t w) {
+    if (w < 0 || A.inst_done[w]) return;
+    // dedupe against the most recent edge of w
+    int32_t h = A.succ_head[w];
+    if (h >= 0 && A.edge_to[h] == id) return;
+    if (nedge >= A.edge_cap) {
+      fail(CF_E_STACK_BUDGET, -2);
+      return;
+    }
+    int32_t e = nedge++;
+    A.edge_to[e] = id;
+    A.edge_next[e] = h;
+    A.succ_head[w] = e;
+    A.inst_pending[id]++;
+  }
+  __device__ void publish(int32_t id) {
+    const Inst& I = A.insts[id];
+    unsigned long long n = (unsigned long long)I.ntiles;
+    int spins = 0;
+    while (q_tail + n - ld_volatile_u64(&st->q_done) > A.q_cap / 2) {
+      backoff(spins);
+      if (st->error) return;
+    }
+    for (unsigned long long t = 0; t < n; ++t)
+      A.queue[(q_tail + t) % A.q_cap] = ((unsigned long long)id << 32) | t;
+    q_tail += n;
+    __threadfence();
+    *(volatile unsigned long long*)&st->q_tail = q_tail;
+  }
+  __device__ void submit(int32_t id) {
+    if (id < 0) return;
+    outstanding++;
+    st->instances++;
+    st->tiles += A.insts[id].ntiles;
+    if (cur_frame >= 0) A.iter_outstanding[P.frames[cur_frame].iter_base + iter]++;
+    if (A.inst_pending[id] == 0) publish(id);
+  }
+  __device__ void complete(int32_t id) {
+    A.inst_done[id] = 1;
+    outstanding--;
+    const Inst& I = A.insts[id];
+    if (I.frame >= 0) A.iter_outstanding[P.frames[I.frame].iter_base + I.iter]--;
+    for (int32_t e = A.succ_head[id]; e >= 0; e = A.edge_next[e]) {
+      int32_t s = A.edge_to[e];
+      if (--A.inst_pending[s] == 0) publish(s);
+    }
+  }
+  __device__ bool drain() {
+    bool any = false;
+    for (int k = 0; k < 256; ++k) {
+      int* p = &A.cq[cq_head % A.cq_cap];
+      int v = ld_volatile_i32(p);
+      if (v == 0) break;
+      *(volatile int*)p = 0;
+      cq_head++;
+      __threadfence();
+      complete(v - 1);
+      any = true;
+    }
+    return any;
+  }
+
+  // ---------------------------------------------------------------- placement
+  __device__ bool place(const DNode& d, int port, int64_t* ptr) {
+    const PlaceDesc& pl = P.places[d.place_off + port];
+    int it = cur_frame >= 0 ? iter : 0;
+    switch (pl.kind) {
+      case PL_ROOT: *ptr = pl.base; return true;
+      case PL_RING: *ptr = pl.base + (int64_t)(it % pl.slots) * pl.elem_bytes; return true;
+      case PL_ARENA:
+        if (it >= pl.slots) {
+          fail(CF_E_STACK_BUDGET, it);
+          return false;
+        }
+        *ptr = pl.base + (int64_t)it * pl.elem_bytes;
+        return true;
+      case PL_TA: {
+        int64_t ix;
+        if (!scalar(A.toks[pl.index_vid], &ix)) return false;
+        const DTA& ta = P.tas[pl.ta];
+        if (ix < 0 || ix >= ta.size) {
+          fail(CF_E_SHAPE, ix);
+          return false;
+        }
+        *ptr = A.ta_base[pl.ta] + ix * pl.elem_bytes;
+        return true;
+      }
+    }
+    return false;
+  }
+  __device__ Tok ptr_tok(int64_t p, int32_t writer, int dt) {
+    Tok t{};
+    t.v = p;
+    t.writer = writer;
+    t.kind = TK_PTR;
+    t.dt = (uint8_t)dt;
+    return t;
+  }
+
+  // ---------------------------------------------------------------- heavy ops
+  __device__ int eval_heavy(const DNode& d) {
+    const int kind = d.aux[0];
+    int64_t outp[6] = {0, 0, 0, 0, 0, 0};
+    int nplace = d.n_out + (kind == HK_LSTM_BWD_EW ? 1 : 0);
+    for (int p = 0; p < nplace; ++p)
+      if (!place(d, p, &outp[p])) return st->error ? EV_ERROR : EV_BLOCKED;
+    auto ip = [&](int j) { return in_tok(d, j).v; };
+    auto dep_all = [&](int32_t id) {
+      for (int j = 0; j < d.n_in; ++j) add_dep(id, in_tok(d, j).writer);
+    };
+    if (kind == HK_LSTM_FWD || kind == HK_LSTM_BWD_EW) {
+      const bool masked = d.aux[1] & 1;
+      int64_t t = 0;
+      if (masked && !scalar(in_tok(d, 5), &t)) return EV_BLOCKED;
+      const int64_t B = d.imm[0], In = d.imm[1], H = d.imm[2];
+      if (kind == HK_LSTM_FWD) {
+        int ntiles = (int)(((B + 31) / 32) * ((H + 31) / 32));
+        int32_t id = new_inst(HK_LSTM_FWD, masked, ntiles);
+        if (id < 0) return EV_ERROR;
+        Inst& I = A.insts[id];
+        I.m = B; I.k = In; I.n = H;
+        for (int j = 0; j < 5; ++j) I.p[j] = ip(j);
+        I.p[5] = masked ? ip(6) : 0;
+        for (int p = 0; p < 4; ++p) I.p[8 + p] = outp[p];
+        I.s[0] = t;
+        I.s[1] = d.aux[2];
+        dep_all(id);
+        for (int p = 0; p < 4; ++p) set_out(d, p, ptr_tok(outp[p], id, D_F32));
+        submit(id);
+      } else {
+        // inputs: x h c W gates [t len] dh_next dc_next dout
+        int o = masked ? 7 : 5;
+        int ntiles_ew = (int)((B * H + kEwTile - 1) / kEwTile);
+        int32_t e = new_inst(HK_LSTM_BWD_EW, masked, ntiles_ew);
+        if (e < 0) return EV_ERROR;
+        {
+          Inst& I = A.insts[e];
+          I.m = B; I.k = In; I.n = H;
+          I.p[2] = ip(2);
+          I.p[4] = ip(4);
+          I.p[5] = masked ? ip(6) : 0;
+          I.p[6] = ip(o);
+          I.p[7] = ip(o + 1);
+          I.p[8] = ip(o + 2);
+          I.p[9] = outp[2];
+          I.p[10] = outp[5];
+          I.s[0] = t;
+          dep_all(e);
+        }
+        const int64_t KT = In + H, G = 4 * H;
+        int tA = (int)(((B + 63) / 64) * ((KT + 63) / 64));
+        int tB = (int)(((G + 63) / 64) * ((KT + 63) / 64));
+        int tC = (int)((G + kThreads - 1) / kThreads);
+        int32_t m = new_inst(HK_LSTM_BWD_MM, masked, tA + tB + tC);
+        if (m < 0) return EV_ERROR;
+        {
+          Inst& I = A.insts[m];
+          I.m = B; I.k = In; I.n = H;
+          I.p[0] = ip(0);
+          I.p[1] = ip(1);
+          I.p[3] = ip(3);
+          I.p[5] = masked ? ip(6) : 0;
+          I.p[6] = ip(o);
+          I.p[10] = outp[5];
+          I.p[11] = outp[0];
+          I.p[12] = outp[1];
+          I.p[13] = outp[3];
+          I.s[3] = outp[4];
+          I.s[0] = t;
+          dep_all(m);
+          add_dep(m, e);
+        }
+        set_out(d, 0, ptr_tok(outp[0], m, D_F32));
+        set_out(d, 1, ptr_tok(outp[1], m, D_F32));
+        set_out(d, 2, ptr_tok(outp[2], e, D_F32));
+        set_out(d, 3, ptr_tok(outp[3], m, D_F32));
+        set_out(d, 4, ptr_tok(outp[4], m, D_F32));
+        submit(e);
+        submit(m);
+      }
+      return EV_OK;
+    }
+    int32_t id = -1;
+    switch (kind) {
+      case HK_EW: {
+        int64_t n = d.imm[0];
+        id = new_inst(HK_EW, d.aux[1], (int)((n + kEwTile - 1) / kEwTile));
+        if (id < 0) return EV_ERROR;
+        Inst& I = A.insts[id];
+        I.n = n;
+        I.m = d.imm[1];
+        for (int j = 0; j < d.n_in && j < 8; ++j) I.p[j] = ip(j);
+        I.p[13] = outp[0];
+        I.s[0] = d.n_in;
+        I.s[1] = d.aux[2];
+        I.s[2] = d.aux[3];
+        break;
+      }
+      case HK_FILL: {
+        int64_t n = d.imm[0];
+        id = new_inst(HK_FILL, 0, (int)((n + kEwTile - 1) / kEwTile));
+        if (id < 0) return EV_ERROR;
+        Inst& I = A.insts[id];
+        I.n = n;
+        I.p[0] = ip(0);
+        I.p[13] = outp[0];
+        break;
+      }
+      case HK_REDUCE_SUM: {
+        int64_t n = d.imm[0];
+        int64_t nt0 = (n + kEwTile - 1) / kEwTile;
+        int nt = (int)(nt0 < 1024 ? nt0 : 1024);
+        id = new_inst(HK_REDUCE_SUM, 0, max(nt, 1));
+        if (id < 0) return EV_ERROR;
+        Inst& I = A.insts[id];
+        I.n = n;
+        I.p[0] = ip(0);
+        I.p[13] = outp[0];
+        break;
+      }
+      case HK_REDUCE_SUM0: {
+        id = new_inst(HK_REDUCE_SUM0, 0, (int)((d.imm[1] + kThreads - 1) / kThreads));
+        if (id < 0) return EV_ERROR;
+        Inst& I = A.insts[id];
+        I.m = d.imm[0];
+        I.n = d.imm[1];
+        I.p[0] = ip(0);
+        I.p[13] = outp[0];
+        break;
+      }
+      case HK_MATMUL: {
+        int64_t M = d.imm[0], N = d.imm[1], K = d.imm[2];
+        id = new_inst(HK_MATMUL, d.aux[1], (int)(((M + 63) / 64) * ((N + 63) / 64)));
+        if (id < 0) return EV_ERROR;
+        Inst& I = A.insts[id];
+        I.m = M; I.n = N; I.k = K;
+        I.p[0] = ip(0);
+        I.p[1] = ip(1);
+        I.p[13] = outp[0];
+        I.s[0] = d.imm[3] & 0xffffffffLL;
+        I.s[1] = d.imm[3] >> 32;
+        break;
+      }
+      default:
+        fail(CF_E_UNSUPPORTED, kind);
+        return EV_ERROR;
+    }
+    dep_all(id);
+    set_out(d, 0, ptr_tok(outp[0], id, D_F32));
+    submit(id);
+    return EV_OK;
+  }
+
+  __device__ int32_t copy_inst(int64_t dst, int64_t src, int64_t bytes, int32_t dep) {
+    int32_t id = new_inst(HK_COPY, 0, (int)((bytes + 65535) / 65536));
+    if (id < 0) return -1;
+    Inst& I = A.insts[id];
+    I.n = bytes;
+    I.p[0] = src;
+    I.p[13] = dst;
+    add_dep(id, dep);
+    submit(id);
+    return id;
+  }
+
+  // ---------------------------------------------------------------- node evaluation
+  __device__ int eval(int nid) {
+    const DNode& d = node(nid);
+    const int op = d.op;
+    bool dead = false;
+    if (op != OP_MERGE && op != OP_MERGE_LOOP) {
+      for (int j = 0; j < d.n_in; ++j) dead |= in_tok(d, j).dead != 0;
+      for (int j = 0; j < d.n_ctrl; ++j) dead |= A.toks[P.in_vids[d.ctrl_off + j]].dead != 0;
+    }
+    int res = EV_OK;
+    bool ctrl_dead = dead;
+    switch (op) {
+      case OP_NOP:
+      case OP_PLACEHOLDER:
+        break;
+      case OP_CONST: {
+        Tok t{};
+        t.writer = -1;
+        t.dead = dead;
+        if (d.aux[0] == 1) {
+          t.kind = TK_IMM;
+          t.v = d.imm[0];
+        } else {
+          t.kind = TK_PTR;
+          t.v = d.imm[0];
+        }
+        t.dt = (uint8_t)d.aux[1];
+        set_out(d, 0, t);
+        break;
+      }
+      case OP_PASS:
+      case OP_FLOW: {
+        Tok t = d.n_in ? in_tok(d, 0) : Tok{};
+        if (op == OP_FLOW) {
+          t = Tok{};
+          t.kind = TK_FLOW;
+          t.writer = -1;
+        }
+        t.dead = dead;
+        for (int p = 0; p < d.n_out; ++p) set_out(d, p, t);
+        break;
+      }
+      case OP_SWITCH: {
+        Tok dv = in_tok(d, 0);
+        const Tok& pt = in_tok(d, 1);
+        Tok o0 = dv, o1 = dv;
+        if (dv.dead || pt.dead || dead) {
+          o0.dead = o1.dead = 1;
+          ctrl_dead = true;
+        } else {
+          int64_t pv;
+          if (!scalar(pt, &pv)) return EV_BLOCKED;
+          o0.dead = pv != 0;   // false port: dead iff p
+          o1.dead = pv == 0;   // true port: dead iff !p
+          if (d.aux[0] >= 0 && d.aux[0] < P.n_conds) {
+            int it = cur_frame >= 0 ? iter : 0;
+            if (it < P.branch_bound) A.branch_bits[d.aux[0] * P.branch_bound + it] = pv ? 2 : 1;
+          }
+        }
+        set_out(d, 0, o0);
+        set_out(d, 1, o1);
+        break;
+      }
+      case OP_MERGE: {
+        const Tok& a = in_tok(d, 0);
+        const Tok& b = in_tok(d, 1);
+        Tok o = !a.dead ? a : b;   // "if is_dead(d1) then d2 else d1"
+        set_out(d, 0, o);
+        ctrl_dead = o.dead;
+        break;
+      }
+      case OP_MERGE_LOOP: {
+        Tok o = iter == 0 ? in_tok(d, 0) : in_tok(d, 1);
+        set_out(d, 0, o);
+        ctrl_dead = o.dead;
+        break;
+      }
+      case OP_NEXTITER:
+        set_out(d, 0, in_tok(d, 0));
+        break;
+      case OP_ENTER:
+      case OP_EXIT:
+        set_out(d, 0, in_tok(d, 0));
+        break;
+      case OP_SCALAR: {
+        if (dead) {
+          set_dead_all(d);
+          break;
+        }
+        int64_t a = 0, b = 0;
+        if (!scalar(in_tok(d, 0), &a)) return EV_BLOCKED;
+        if (d.n_in > 1 && !scalar(in_tok(d, 1), &b)) return EV_BLOCKED;
+        int64_t r = 0;
+        switch (d.aux[0]) {
+          case SC_ADD: r = a + b; break;
+          case SC_SUB: r = a - b; break;
+          case SC_MUL: r = a * b; break;
+          case SC_LESS: r = a < b; break;
+          case SC_LEQ: r = a <= b; break;
+          case SC_GREATER: r = a > b; break;
+          case SC_EQ: r = a == b; break;
+          case SC_AND: r = (a != 0) && (b != 0); break;
+          case SC_NOT: r = a == 0; break;
+          case SC_CAST: r = d.aux[1] == D_BOOL ? (a != 0) : a; break;
+        }
+        Tok t{};
+        t.kind = TK_IMM;
+        t.v = r;
+        t.writer = -1;
+        t.dt = (uint8_t)d.aux[1];
+        set_out(d, 0, t);
+        break;
+      }
+      case OP_REDUCE_I: {
+        if (dead) {
+          set_dead_all(d);
+          break;
+        }
+        const Tok& v = in_tok(d, 0);
+        if (!writer_done(v.writer)) return EV_BLOCKED;
+        __threadfence();
+        int n = d.aux[1];
+        int64_t r = 0;
+        if (d.aux[2] == D_I64) {
+          const int64_t* p = (const int64_t*)v.v;
+          r = p[0];
+          for (int k = 1; k < n; ++k) r = d.aux[0] ? min(r, p[k]) : max(r, p[k]);
+        } else {
+          const int32_t* p = (const int32_t*)v.v;
+          r = p[0];
+          for (int k = 1; k < n; ++k) {
+            int64_t q = p[k];
+            r = d.aux[0] ? (q < r ? q : r) : (q > r ? q : r);
+          }
+        }
+        Tok t{};
+        t.kind = TK_IMM;
+        t.v = r;
+        t.writer = -1;
+        t.dt = (uint8_t)d.aux[2];
+        set_out(d, 0, t);
+        break;
+      }
+      case OP_SLICE_I: {
+        Tok t = in_tok(d, 0);
+        t.v += d.imm[0];
+        t.dead = dead;
+        set_out(d, 0, t);
+        break;
+      }
+      case OP_TA_CREATE: {
+        Tok h{};
+        h.kind = TK_HANDLE;
+        h.v = d.aux[0];
+        h.writer = -1;
+        h.dead = dead;
+        Tok f{};
+        f.kind = TK_FLOW;
+        f.writer = -1;
+        f.dead = dead;
+        set_out(d, 0, h);
+        set_out(d, 1, f);
+        break;
+      }
+      case OP_TA_GRAD: {
+        Tok h{};
+        h.kind = TK_HANDLE;
+        h.v = d.aux[0];
+        h.writer = -1;
+        h.dead = dead;
+        Tok f{};
+        f.kind = TK_FLOW;
+        f.writer = -1;
+        f.dead = dead;
+        set_out(d, 0, h);
+        set_out(d, 1, f);
+        break;
+      }
+      case OP_TA_READ: {
+        if (dead) {
+          set_dead_all(d);
+          break;
+        }
+        int ta = (int)in_tok(d, 0).v;
+        int64_t ix;
+        if (!scalar(in_tok(d, 1), &ix)) return EV_BLOCKED;
+        const DTA& T = P.tas[ta];
+        if (ix < 0 || ix >= T.size) {
+          fail(CF_E_SHAPE, ix);
+          return EV_ERROR;
+        }
+        int so = A.ta_slot_off[ta] + (int)ix;
+        if (!T.is_grad && !A.ta_written[so]) {
+          fail(CF_E_INVALID_GRAPH, ix);
+          return EV_ERROR;
+        }
+        set_out(d, 0, ptr_tok(A.ta_base[ta] + ix * T.elem_bytes, A.ta_writer[so], T.dt));
+        break;
+      }
+      case OP_TA_WRITE: {
+        Tok f{};
+        f.kind = TK_FLOW;
+        f.writer = -1;
+        f.dead = dead;
+        if (!dead) {
+          int ta = (int)in_tok(d, 0).v;
+          int64_t ix;
+          if (!scalar(in_tok(d, 1), &ix)) return EV_BLOCKED;
+          const DTA& T = P.tas[ta];
+          if (ix < 0 || ix >= T.size) {
+            fail(CF_E_SHAPE, ix);
+            return EV_ERROR;
+          }
+          int so = A.ta_slot_off[ta] + (int)ix;
+          const Tok& v = in_tok(d, 2);
+          int64_t dst = A.ta_base[ta] + ix * T.elem_bytes;
+          if (A.ta_written[so]) {
+            if (!T.is_grad) {
+              fail(CF_E_DOUBLE_WRITE, ix);
+              return EV_ERROR;
+            }
+            // grad TensorArray: "holds the sum of the partial gradients"
+            int32_t id = new_inst(HK_ACC, 0, (int)((T.elem_bytes / 4 + kEwTile - 1) / kEwTile));
+            if (id < 0) return EV_ERROR;
+            A.insts[id].n = T.elem_bytes / 4;
+            A.insts[id].p[0] = v.v;
+            A.insts[id].p[13] = dst;
+            add_dep(id, v.writer);
+            add_dep(id, A.ta_writer[so]);
+            submit(id);
+            A.ta_writer[so] = id;
+          } else if (v.v == dst) {
+            A.ta_writer[so] = v.writer;    // producer was placed in the slot: zero-copy
+          } else {
+            A.ta_writer[so] = copy_inst(dst, v.v, T.elem_bytes, v.writer);
+          }
+          A.ta_written[so] = 1;
+        }
+        set_out(d, 0, f);
+        break;
+      }
+      case OP_TA_STACK: {
+        if (dead) {
+          set_dead_all(d);
+          break;
+        }
+        int ta = (int)in_tok(d, 0).v;
+        const DTA& T = P.tas[ta];
+        int32_t join = new_inst(HK_NOP, 0, 1);
+        if (join < 0) return EV_ERROR;
+        for (int i = 0; i < T.size; ++i) {
+          int so = A.ta_slot_off[ta] + i;
+          if (!T.is_grad && !A.ta_written[so]) {
+            fail(CF_E_INVALID_GRAPH, i);
+            return EV_ERROR;
+          }
+          add_dep(join, A.ta_writer[so]);
+        }
+        submit(join);
+        set_out(d, 0, ptr_tok(A.ta_base[ta], join, T.dt));
+        break;
+      }
+      case OP_TA_UNSTACK: {
+        Tok f{};
+        f.kind = TK_FLOW;
+        f.writer = -1;
+        f.dead = dead;
+        if (!dead) {
+          int ta = (int)in_tok(d, 0).v;
+          const DTA& T = P.tas[ta];
+          const Tok& v = in_tok(d, 1);
+          bool any = false;
+          for (int i = 0; i < T.size; ++i) any |= A.ta_written[A.ta_slot_off[ta] + i] != 0;
+          if (!any) {
+            A.ta_base[ta] = v.v;   // alias the unstacked tensor (no copy)
+            for (int i = 0; i < T.size; ++i) {
+              A.ta_writer[A.ta_slot_off[ta] + i] = v.writer;
+              A.ta_written[A.ta_slot_off[ta] + i] = 1;
+            }
+          } else {
+            fail(CF_E_DOUBLE_WRITE, 0);
+            return EV_ERROR;
+          }
+        }
+        set_out(d, 0, f);
+        break;
+      }
+      case OP_STACK_CREATE: {
+        Tok h{};
+        h.kind = TK_HANDLE;
+        h.v = d.aux[0];
+        h.writer = -1;
+        h.dead = dead;
+        set_out(d, 0, h);
+        break;
+      }
+      case OP_STACK_PUSH: {
+        if (!dead) {
+          int s = (int)in_tok(d, 0).v;
+          const DStack& S = P.stacks[s];
+          int dp = A.stack_depth[s];
+          if (dp >= S.capacity) {
+            fail(CF_E_STACK_BUDGET, dp);
+            return EV_ERROR;
+          }
+          A.stack_pool[S.entry_off + dp] = in_tok(d, 1);
+          A.stack_depth[s] = dp + 1;
+          st->pushes++;
+          if (dp + 1 > st->max_depth) st->max_depth = dp + 1;
+        }
+        break;
+      }
+      case OP_STACK_POP: {
+        if (dead) {
+          set_dead_all(d);
+          break;
+        }
+        int s = (int)in_tok(d, 0).v;
+        const DStack& S = P.stacks[s];
+        int dp = A.stack_depth[s];
+        if (dp <= 0) {
+          fail(CF_E_POP_EMPTY, s);
+          return EV_ERROR;
+        }
+        Tok t = A.stack_pool[S.entry_off + dp - 1];
+        A.stack_depth[s] = dp - 1;
+        t.dead = 0;
+        set_out(d, 0, t);
+        st->pops++;
+        break;
+      }
+      case OP_HEAVY: {
+        if (dead) {
+          set_dead_all(d);
+          st->dead_skipped++;
+          break;
+        }
+        res = eval_heavy(d);
+        break;
+      }
+      default:
+        fail(CF_E_UNSUPPORTED, op);
+        return EV_ERROR;
+    }
+    if (res != EV_OK) return res;
+    Tok c{};
+    c.dead = ctrl_dead;
+    c.writer = -1;
+    c.kind = TK_FLOW;
+    A.toks[d.ctrl_vid] = c;
+    return EV_OK;
+  }
+
+  // ---------------------------------------------------------------- frames
+  __device__ void start_frame(int f) {
+    const DFrame& F = P.frames[f];
+    for (int k = 0; k < F.n_enter; ++k) {
+      const DNode& e = node(P.order[F.enter_off + k]);
+      set_out(e, 0, in_tok(e, 0));
+      Tok c{};
+      c.dead = in_tok(e, 0).dead;
+      c.writer = -1;
+      A.toks[e.ctrl_vid] = c;
+    }
+    cur_frame = f;
+    iter = 0;
+    oldest = 0;
+    body_pc = 0;
+    iter_started = false;
+  }
+
+  // one step of control evaluation; returns true on progress
+  __device__ bool step() {
+    if (cur_frame < 0) {
+      if (root_pc >= P.n_root_steps) {
+        if (!fetched) {
+          issue_fetches();
+          fetched = true;
+          return true;
+        }
+        return false;
+      }
+      int s = P.root_steps[root_pc];
+      if (s >= 0) {
+        int r = eval(s);
+        if (r != EV_OK) return false;
+        root_pc++;
+        return true;
+      }
+      start_frame(-s - 1);
+      return true;
+    }
+    const DFrame& F = P.frames[cur_frame];
+    if (!iter_started) {
+      while (oldest < iter && A.iter_outstanding[F.iter_base + oldest] == 0) oldest++;
+      if (iter - oldest >= F.K) return false;   // parallel_iterations window
+      if (iter > F.bound) {
+        fail(CF_E_STACK_BUDGET, iter);
+        return false;
+      }
+      int infl = iter - oldest + 1;
+      if (cur_frame < 16 && infl > st->max_inflight[cur_frame]) st->max_inflight[cur_frame] = infl;
+      iter_started = true;
+      body_pc = 0;
+    }
+    bool progress = false;
+    while (body_pc < F.n_body) {
+      int r = eval(P.order[F.body_off + body_pc]);
+      if (r != EV_OK) return progress;
+      body_pc++;
+      progress = true;
+    }
+    // the counter's Switch decides: true port dead => the predicate was false (or the frame
+    // is dead) => Exit fires once with this iteration's values (reading R2)
+    const DNode& cs = node(F.counter_switch);
+    if (A.toks[cs.out_vid + 1].dead) {
+      for (int k = 0; k < F.n_exit; ++k) {
+        const DNode& x = node(P.order[F.exit_off + k]);
+        set_out(x, 0, in_tok(x, 0));
+        Tok c{};
+        c.dead = in_tok(x, 0).dead;
+        c.writer = -1;
+        A.toks[x.ctrl_vid] = c;
+      }
+      st->exit_fires += F.n_exit;
+      if (cur_frame < 16) st->trip[cur_frame] = iter;
+      cur_frame = -1;
+      root_pc++;
+      return true;
+    }
+    iter++;
+    iter_started = false;
+    return true;
+  }
+
+  __device__ void issue_fetches() {
+    for (int i = 0; i < P.n_fetch; ++i) {
+      const Tok& t = A.toks[P.fetch_vids[i]];
+      if (t.dead) {
+        A.fetch_dead[i] = 1;
+        continue;
+      }
+      A.fetch_dead[i] = 0;
+      int64_t bytes = A.fetch_bytes[i];
+      if (t.kind == TK_IMM) {
+        uint8_t* o = (uint8_t*)A.fetch_out[i];
+        int64_t v = t.v;
+        for (int b = 0; b < bytes && b < 8; ++b) o[b] = (uint8_t)(v >> (8 * b));
+      } else if (t.kind == TK_PTR && bytes > 0) {
+        copy_inst((int64_t)A.fetch_out[i], t.v, bytes, t.writer);
+      }
+    }
+  }
+
+  __device__ void run() {
+    st->t_start = globaltimer();
+    last_progress = st->t_start;
+    while (true) {
+      bool p = drain();
+      if (st->error) break;
+      p |= step();
+      if (st->error) break;
+      if (fetched && cur_frame < 0 && root_pc >= P.n_root_steps && outstanding == 0) break;
+      unsigned long long now = globaltimer();
+      if (p) {
+        last_progress = now;
+      } else if ((long long)(now - last_progress) > A.watchdog_ns) {
+        fail(CF_E_DEADLOCK, outstanding);
+        break;
+      }
+    }
+    st->t_end = globaltimer();
+    __threadfence();
+    *(volatile int*)&st->quit = 1;
+  }
+};
+
+__device__ void worker_loop(const RunArgs& A) {
+  __shared__ __align__(16) float sm[32 * 33 + 32 * 129 + 64];
+  __shared__ unsigned long long s_entry;
+  __shared__ int s_last;
+  RunState* st = A.st;
+  while (true) {
+    if (threadIdx.x == 0) {
+      unsigned long long idx = atomicAdd(&st->q_head, 1ULL);
+      int spins = 0;
+      unsigned long long e = ~0ULL;
+      while (true) {
+        if (idx < ld_volatile_u64(&st->q_tail)) {
+          __threadfence();
+          e = ((volatile unsigned long long*)A.queue)[idx % A.q_cap];
+          break;
+        }
+        if (ld_volatile_i32(&st->quit)) break;
+        backoff(spins);
+      }
+      __threadfence();
+      s_entry = e;
+    }
+    __syncthreads();
+    unsigned long long e = s_entry;
+    if (e == ~0ULL) return;
+    const int32_t id = (int32_t)(e >> 32);
+    const int tile = (int)(e & 0xffffffffULL);
+    __shared__ Inst s_inst;
+    if (threadIdx.x < (int)(sizeof(Inst) / 8))
+      ((int64_t*)&s_inst)[threadIdx.x] = ((volatile const int64_t*)(A.insts + id))[threadIdx.x];
+    __syncthreads();
+    const Inst I = s_inst;
+    switch (I.kind) {
+      case HK_NOP: break;
+      case HK_EW: tile_ew(I, tile); break;
+      case HK_FILL: tile_fill(I, tile); break;
+      case HK_COPY: tile_copy(I, tile); break;
+      case HK_ACC: tile_acc(I, tile); break;
+      case HK_REDUCE_SUM: tile_reduce_sum(I, tile, sm); break;
+      case HK_REDUCE_SUM0: tile_reduce_sum0(I, tile); break;
+      case HK_MATMUL: tile_matmul(I, tile, sm); break;
+      case HK_LSTM_FWD: tile_lstm_fwd(I, tile, sm); break;
+      case HK_LSTM_BWD_EW: tile_lstm_bwd_ew(I, tile); break;
+      case HK_LSTM_BWD_MM: tile_lstm_bwd_mm(I, tile, sm); break;
+      default: break;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      int old = atomicAdd(&A.inst_tiles_done[id], 1);
+      s_last = (old == I.ntiles - 1);
+      atomicAdd(&st->q_done, 1ULL);
+    }
+    __syncthreads();
+    if (s_last) {
+      if (I.kind == HK_REDUCE_SUM) {
+        __threadfence();
+        finalize_reduce_sum(I, sm);
+        __syncthreads();
+      }
+      if (threadIdx.x == 0) {
+        __threadfence();
+        unsigned long long slot = atomicAdd(&st->cq_tail, 1ULL);
+        int* p = &A.cq[slot % A.cq_cap];
+        int spins = 0;
+        while (ld_volatile_i32(p) != 0) {
+          if (ld_volatile_i32(&st->quit)) break;
+          backoff(spins);
+        }
+        __threadfence();
+        *(volatile int*)p = id + 1;
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 1) cf_driver_kernel(RunArgs A) {
+  if (blockIdx.x == 0) {
+    if (threadIdx.x == 0) {
+      Driver d(A);
+      d.run();
+    }
+    return;
+  }
+  worker_loop(A);
+}
+
+}  // namespace
+
+// ============================================================================= host side
+struct cf_session {
+  cf::HostProgram P;
+  int device = 0;
+  int precision = CF_F32;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int grid = 0;
+  std::vector<void*> allocs;
+  std::vector<void*> buf_ptr;
+  RunArgs args{};
+  // device copies of tables
+  void* d_tables = nullptr;
+  RunState* d_state = nullptr;
+  void** d_fetch_out = nullptr;
+  uint8_t* d_fetch_dead = nullptr;
+  int64_t* d_fetch_bytes = nullptr;
+  int64_t* d_ta_base_init = nullptr;
+  std::vector<int64_t> ta_base_host;
+  size_t state_bytes = 0;
+  void* d_state_block = nullptr;   // zeroed at every run
+  std::vector<std::pair<void*, size_t>> zero_each_run;
+  std::vector<std::pair<void*, int>> fill_ff_each_run;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  int64_t watchdog_ns = 60LL * 1000 * 1000 * 1000;
+  int sched_seed = 0;
+};
+
+namespace {
+
+template <class T>
+T* upload(cf_session* s, const std::vector<T>& v) {
+  size_t bytes = std::max<size_t>(v.size() * sizeof(T), 16);
+  void* p = nullptr;
+  CUDA_OK(cudaMalloc(&p, bytes));
+  s->allocs.push_back(p);
+  if (!v.empty()) CUDA_OK(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return (T*)p;
+}
+
+void* dalloc(cf_session* s, size_t bytes) {
+  void* p = nullptr;
+  CUDA_OK(cudaMalloc(&p, std::max<size_t>(bytes, 16)));
+  s->allocs.push_back(p);
+  return p;
+}
+
+void build_session(cf_session* s, const cf::Graph& g, const cf_run_opts* o,
+                   const std::vector<cf::TRef>& fetches) {
+  cf::CompileOpts co;
+  if (o) {
+    co.precision = o->precision ? o->precision : CF_F32;
+    co.parallel_iterations = o->parallel_iterations;
+    co.max_iterations = o->max_iterations;
+    s->device = o->device;
+    if (o->watchdog_ms > 0) s->watchdog_ns = o->watchdog_ms * 1000000LL;
+    s->sched_seed = o->sched_seed;
+  }
+  if (co.precision != CF_F32 && co.precision != CF_BF16)
+    throw cf::CfError(CF_E_DTYPE, "precision must be CF_F32 or CF_BF16");
+  if (co.precision == CF_BF16)
+    throw cf::CfError(CF_E_UNSUPPORTED, "CF_BF16 path not built in this library version");
+  s->precision = co.precision;
+  s->P = cf::compile(g, co, fetches);
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    throw cf::CfError(CF_E_CUDA, "no CUDA device (libcf has no CPU fallback)");
+  CUDA_OK(cudaSetDevice(s->device));
+  if (o && o->stream) {
+    s->stream = (cudaStream_t)o->stream;
+  } else {
+    CUDA_OK(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+    s->own_stream = true;
+  }
+  CUDA_OK(cudaEventCreate(&s->ev0));
+  CUDA_OK(cudaEventCreate(&s->ev1));
+  cf::HostProgram& P = s->P;
+  // ---- buffers
+  s->buf_ptr.resize(P.bufs.size());
+  for (size_t b = 0; b < P.bufs.size(); ++b) {
+    void* p = dalloc(s, P.bufs[b].bytes);
+    s->buf_ptr[b] = p;
+    if (!P.bufs[b].init.empty())
+      CUDA_OK(cudaMemcpy(p, P.bufs[b].init.data(), P.bufs[b].init.size(), cudaMemcpyHostToDevice));
+    if (P.bufs[b].zero) s->zero_each_run.push_back({p, P.bufs[b].bytes});
+  }
+  auto addr = [&](int64_t id) { return (int64_t)(uintptr_t)s->buf_ptr.at(id); };
+  for (auto& pl : P.places)
+    if (pl.kind != PL_TA) pl.base = addr(pl.base);
+  for (auto& n : P.nodes)
+    if (n.op == OP_CONST && n.aux[0] == 0) n.imm[0] = addr(n.imm[0]);
+  for (auto& t : P.tas) t.base = addr(t.base);
+  s->ta_base_host.clear();
+  for (auto& t : P.tas) s->ta_base_host.push_back(t.base);
+  // ---- tables
+  RunArgs& A = s->args;
+  Prog& pg = A.prog;
+  pg.n_nodes = (int)P.nodes.size();
+  pg.n_vids = P.n_vids;
+  pg.n_frames = (int)P.frames.size();
+  pg.n_tas = (int)P.tas.size();
+  pg.n_stacks = (int)P.stacks.size();
+  pg.n_root_steps = (int)P.root_steps.size();
+  pg.n_fetch = (int)P.fetches.size();
+  pg.n_conds = P.n_conds;
+  pg.branch_bound = P.branch_bound;
+  pg.nodes = upload(s, P.nodes);
+  pg.in_vids = upload(s, P.in_vids);
+  pg.places = upload(s, P.places);
+  pg.frames = upload(s, P.frames);
+  pg.order = upload(s, P.order);
+  pg.root_steps = upload(s, P.root_steps);
+  pg.tas = upload(s, P.tas);
+  pg.stacks = upload(s, P.stacks);
+  pg.fetch_vids = upload(s, P.fetch_vids);
+  // ---- runtime state
+  A.st = (RunState*)dalloc(s, sizeof(RunState));
+  s->zero_each_run.push_back({A.st, sizeof(RunState)});
+  A.toks = (Tok*)dalloc(s, sizeof(Tok) * P.n_vids);
+  s->zero_each_run.push_back({A.toks, sizeof(Tok) * P.n_vids});
+  A.stack_pool = (Tok*)dalloc(s, sizeof(Tok) * std::max(P.stack_pool, 1));
+  A.stack_depth = (int32_t*)dalloc(s, 4 * std::max<size_t>(P.stacks.size(), 1));
+  s->zero_each_run.push_back({A.stack_depth, 4 * std::max<size_t>(P.stacks.size(), 1)});
+  A.ta_base = (int64_t*)dalloc(s, 8 * std::max<size_t>(P.tas.size(), 1));
+  std::vector<int32_t> slot_off;
+  int so = 0;
+  for (auto& t : P.tas) {
+    slot_off.push_back(so);
+    so += t.size;
+  }
+  A.ta_slot_off = upload(s, slot_off);
+  A.ta_writer = (int32_t*)dalloc(s, 4 * std::max(so, 1));
+  s->fill_ff_each_run.push_back({A.ta_writer, 4 * std::max(so, 1)});
+  A.ta_written = (uint8_t*)dalloc(s, std::max(so, 1));
+  s->zero_each_run.push_back({A.ta_written, (size_t)std::max(so, 1)});
+  int64_t cap = P.inst_bound;
+  A.inst_cap = (int32_t)cap;
+  A.insts = (Inst*)dalloc(s, sizeof(Inst) * cap);
+  A.inst_pending = (int32_t*)dalloc(s, 4 * cap);
+  A.inst_done = (uint8_t*)dalloc(s, cap);
+  A.inst_tiles_done = (int32_t*)dalloc(s, 4 * cap);
+  s->zero_each_run.push_back({A.inst_tiles_done, (size_t)(4 * cap)});
+  A.succ_head = (int32_t*)dalloc(s, 4 * cap);
+  A.edge_cap = (int32_t)std::min<int64_t>(cap * 24, 1LL << 30);
+  A.edge_next = (int32_t*)dalloc(s, 4 * (size_t)A.edge_cap);
+  A.edge_to = (int32_t*)dalloc(s, 4 * (size_t)A.edge_cap);
+  A.q_cap = 1ULL << 22;
+  A.queue = (unsigned long long*)dalloc(s, 8 * A.q_cap);
+  A.cq_cap = 1ULL << 16;
+  A.cq = (int32_t*)dalloc(s, 4 * A.cq_cap);
+  s->zero_each_run.push_back({A.cq, 4 * A.cq_cap});
+  A.iter_outstanding = (int32_t*)dalloc(s, 4 * std::max(P.iter_counters, 1));
+  s->zero_each_run.push_back({A.iter_outstanding, 4 * (size_t)std::max(P.iter_counters, 1)});
+  size_t bb = (size_t)std::max(P.n_conds, 1) * P.branch_bound;
+  A.branch_bits = (uint8_t*)dalloc(s, bb);
+  s->zero_each_run.push_back({A.branch_bits, bb});
+  std::vector<int64_t> fb;
+  for (auto& f : P.fetches) fb.push_back(f.bytes);
+  A.fetch_bytes = upload(s, fb);
+  A.fetch_out = (void**)dalloc(s, 8 * std::max<size_t>(P.fetches.size(), 1));
+  A.fetch_dead = (uint8_t*)dalloc(s, std::max<size_t>(P.fetches.size(), 1));
+  A.watchdog_ns = s->watchdog_ns;
+  A.sched_seed = s->sched_seed;
+  // ---- grid: one CTA per SM, all co-resident (cooperative launch)
+  int sms = 0, per_sm = 0;
+  CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->device));
+  CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cf_driver_kernel, kThreads, 0));
+  if (per_sm < 1) throw cf::CfError(CF_E_CUDA, "driver kernel cannot be resident");
+  int workers = o && o->num_workers > 0 ? o->num_workers : sms - 1;
+  s->grid = std::min(workers + 1, sms * per_sm);
+  A.num_workers = s->grid - 1;
+}
+
+}  // namespace
+
+extern "C" {
+
+cf_status cf_session_create(const cf_graph* g, const cf_run_opts* opts, int32_t n_fetch,
+                            const cf_tensor* fetches, cf_session** out) {
+  cf_session* s = nullptr;
+  try {
+    if (!g || !out) throw cf::CfError(CF_E_INVALID_GRAPH, "null argument");
+    const cf::Graph& ir = cf_graph_ir(g);
+    std::vector<cf::TRef> fv;
+    for (int i = 0; i < n_fetch; ++i) {
+      if (fetches[i].node < 0 || fetches[i].node >= (int)ir.nodes.size())
+        throw cf::CfError(CF_E_INVALID_GRAPH, "bad fetch tensor");
+      fv.push_back(cf::TRef{fetches[i].node, fetches[i].port});
+    }
+    s = new cf_session();
+    build_session(s, ir, opts, fv);
+    *out = s;
+    return CF_OK;
+  } catch (const cf::CfError& e) {
+    cf::set_error(e.what());
+    if (s) cf_session_destroy(s);
+    return e.code;
+  } catch (const std::exception& e) {
+    cf::set_error(std::string("internal: ") + e.what());
+    if (s) cf_session_destroy(s);
+    return CF_E_INVALID_GRAPH;
+  }
+}
+
+cf_status cf_run(cf_session* s, int32_t n_feed, const char* const* feed_names,
+                 const cf_buffer* feeds, cf_buffer* outs, uint8_t* out_dead, cf_trace* trace) {
+  try {
+    if (!s) throw cf::CfError(CF_E_INVALID_GRAPH, "null session");
+    cf::HostProgram& P = s->P;
+    RunArgs& A = s->args;
+    CUDA_OK(cudaSetDevice(s->device));
+    for (auto& [p, b] : s->zero_each_run) CUDA_OK(cudaMemsetAsync(p, 0, b, s->stream));
+    for (auto& [p, b] : s->fill_ff_each_run) CUDA_OK(cudaMemsetAsync(p, 0xff, b, s->stream));
+    // token presets: placeholders
+    std::vector<Tok> preset;
+    std::vector<int> preset_vid;
+    std::map<std::string, int> seen;
+    for (int i = 0; i < n_feed; ++i) seen[feed_names[i]] = i;
+    for (auto& [name, fi] : P.feeds) {
+      auto it = seen.find(name);
+      if (it == seen.end()) throw cf::CfError(CF_E_MISSING_FEED, "no feed for placeholder " + name);
+      const cf_buffer& b = feeds[it->second];
+      if (!b.data && fi.bytes > 0) throw cf::CfError(CF_E_MISSING_FEED, "null feed " + name);
+      if (b.dtype != fi.dev_dt)
+        throw cf::CfError(CF_E_DTYPE, "feed " + name + " has dtype " + std::to_string(b.dtype) +
+                                          ", session expects " + std::to_string(fi.dev_dt));
+      Tok t{};
+      t.kind = TK_PTR;
+      t.v = (int64_t)(uintptr_t)b.data;
+      t.writer = -1;
+      t.dt = (uint8_t)fi.dev_dt;
+      preset.push_back(t);
+      preset_vid.push_back(fi.vid);
+    }
+    // ta bases reset (unstack may alias)
+    CUDA_OK(cudaMemcpyAsync(A.ta_base, s->ta_base_host.data(), 8 * s->ta_base_host.size(),
+                            cudaMemcpyHostToDevice, s->stream));
+    for (size_t k = 0; k < preset.size(); ++k)
+      CUDA_OK(cudaMemcpyAsync(A.toks + preset_vid[k], &preset[k], sizeof(Tok),
+                              cudaMemcpyHostToDevice, s->stream));
+    std::vector<void*> fo(P.fetches.size());
+    for (size_t i = 0; i < P.fetches.size(); ++i) {
+      fo[i] = outs ? outs[i].data : nullptr;
+      if (outs && outs[i].dtype != P.fetches[i].dev_dt && P.fetches[i].bytes > 0)
+        throw cf::CfError(CF_E_DTYPE, "fetch buffer " + std::to_string(i) + " dtype mismatch");
+    }
+    if (!fo.empty())
+      CUDA_OK(cudaMemcpyAsync(A.fetch_out, fo.data(), 8 * fo.size(), cudaMemcpyHostToDevice, s->stream));
+    // the copies above read pageable host memory; make them complete before it goes away
+    CUDA_OK(cudaStreamSynchronize(s->stream));
+    void* kargs[] = {(void*)&A};
+    CUDA_OK(cudaEventRecord(s->ev0, s->stream));
+    CUDA_OK(cudaLaunchCooperativeKernel((void*)cf_driver_kernel, dim3(s->grid), dim3(kThreads), kargs,
+                                        0, s->stream));
+    CUDA_OK(cudaEventRecord(s->ev1, s->stream));
+    CUDA_OK(cudaStreamSynchronize(s->stream));
+    RunState st;
+    CUDA_OK(cudaMemcpy(&st, A.st, sizeof(RunState), cudaMemcpyDeviceToHost));
+    if (st.error) {
+      throw cf::CfError(st.error, "device driver error " + std::to_string(st.error) + " (info " +
+                                      std::to_string(st.error_info) + ")");
+    }
+    std::vector<uint8_t> dead(std::max<size_t>(P.fetches.size(), 1));
+    CUDA_OK(cudaMemcpy(dead.data(), A.fetch_dead, dead.size(), cudaMemcpyDeviceToHost));
+    if (out_dead)
+      for (size_t i = 0; i < P.fetches.size(); ++i) out_dead[i] = dead[i];
+    if (trace) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, s->ev0, s->ev1);
+      trace->wall_ms = ms;
+      trace->n_frames = (int32_t)P.frames.size();
+      for (int f = 0; f < 16; ++f) {
+        trace->trip_count[f] = st.trip[f];
+        trace->max_inflight[f] = st.max_inflight[f];
+      }
+      trace->pushes = st.pushes;
+      trace->pops = st.pops;
+      trace->max_depth = st.max_depth;
+      trace->exit_fires = st.exit_fires;
+      trace->instances = st.instances;
+      trace->tiles = st.tiles;
+      trace->dead_skipped = st.dead_skipped;
+      int nb = P.n_conds * P.branch_bound;
+      trace->n_branch_bits = nb;
+      if (trace->branch_bits && trace->branch_bits_cap > 0)
+        CUDA_OK(cudaMemcpy(trace->branch_bits, A.branch_bits,
+                           std::min(nb, trace->branch_bits_cap), cudaMemcpyDeviceToHost));
+    }
+    return CF_OK;
+  } catch (const cf::CfError& e) {
+    cf::set_error(e.what());
+    return e.code;
+  } catch (const std::exception& e) {
+    cf::set_error(std::string("internal: ") + e.what());
+    return CF_E_CUDA;
+  }
+}
+
+cf_status cf_session_feed_dtype(const cf_session* s, const char* name, int32_t* dtype) {
+  if (!s || !name || !dtype) return CF_E_INVALID_GRAPH;
+  auto it = s->P.feeds.find(name);
+  if (it == s->P.feeds.end()) {
+    cf::set_error(std::string("no placeholder ") + name);
+    return CF_E_MISSING_FEED;
+  }
+  *dtype = it->second.dev_dt;
+  return CF_OK;
+}
+
+cf_status cf_session_fetch_dtype(const cf_session* s, int32_t i, int32_t* dtype) {
+  if (!s || !dtype || i < 0 || i >= (int)s->P.fetches.size()) return CF_E_INVALID_GRAPH;
+  *dtype = s->P.fetches[i].dev_dt;
+  return CF_OK;
+}
+
+cf_status cf_session_describe(const cf_session* s, char* buf, size_t cap) {
+  if (!s || !buf || !cap) return CF_E_INVALID_GRAPH;
+  std::string d = s->P.describe + "grid=" + std::to_string(s->grid) + "\n";
+  std::strncpy(buf, d.c_str(), cap - 1);
+  buf[cap - 1] = 0;
+  return CF_OK;
+}
+
+void cf_session_destroy(cf_session* s) {
+  if (!s) return;
+  for (void* p : s->allocs) cudaFree(p);
+  if (s->ev0) cudaEventDestroy(s->ev0);
+  if (s->ev1) cudaEventDestroy(s->ev1);
+  if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
+  delete s;
+}
+
+}  // extern "C"

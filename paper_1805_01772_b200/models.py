@@ -1,0 +1,151 @@
+"""dynamic_rnn LSTM built on the C-ABI ("We implemented the dynamic_rnn
+operator in TensorFlow using while-loops and TensorArray objects").
+
+Variable-length semantics (reading R10, TF dynamic_rnn): the loop runs t < T;
+the body is ``cond(t < max_len, cell_branch, empty_update)`` and inside the cell branch
+``cond(t < min_len, cells, masked_cells)``; a finished row keeps its state and emits zeros.
+The loss is the random projection of reading R11. The optional MoE-style gated branch
+(BASELINE.json configs[4]) adds ``y_l = out_l + cond(route[t, l], relu(out_l WA_l),
+relu(out_l WB_l))`` after every layer.
+
+Graph structure is the same as the oracle's builder produces for the same program
+(tests/test_structure.py compares op counts), so the device's control trace can be compared
+with the oracle's bit for bit.
+"""
+from __future__ import annotations
+
+import dataclasses
+from typing import Dict, List
+
+from . import cf
+from .cf import BOOL, F32, I64, Graph, Tensor
+
+
+@dataclasses.dataclass
+class RNNProgram:
+    g: Graph
+    fetch: Dict[str, Tensor]
+    grads: Dict[str, Tensor]
+    T: int
+    B: int
+    I: int
+    H: int
+    L: int
+
+    def fetch_names(self) -> List[str]:
+        return list(self.fetch) + list(self.grads)
+
+    def fetch_tensors(self) -> List[Tensor]:
+        return [self.fetch[n] for n in self.fetch] + [self.grads[n] for n in self.grads]
+
+
+def dynamic_rnn_lstm(T: int, B: int, I: int, H: int, L: int = 1, parallel_iterations: int = 32,
+                     length_conds: bool = True, moe: bool = False, forget_bias: float = 0.0,
+                     with_grads: bool = True) -> RNNProgram:
+    g = Graph()
+    x = g.placeholder("x", F32, (T, B, I))
+    lens = g.placeholder("len", I64, (B,))
+    Ws, bs, h0, c0, WA, WB = [], [], [], [], [], []
+    for l in range(L):
+        il = I if l == 0 else H
+        Ws.append(g.placeholder(f"W{l}", F32, (4 * H, il + H)))
+        bs.append(g.placeholder(f"b{l}", F32, (4 * H,)))
+        h0.append(g.placeholder(f"h0_{l}", F32, (B, H)))
+        c0.append(g.placeholder(f"c0_{l}", F32, (B, H)))
+        if moe:
+            WA.append(g.placeholder(f"WA{l}", F32, (H, H)))
+            WB.append(g.placeholder(f"WB{l}", F32, (H, H)))
+    route_ta = None
+    if moe:
+        route = g.placeholder("route", BOOL, (T, L))
+        route_ta = g.tensor_array(T, BOOL, (L,)).unstack(route)
+    x_ta = g.tensor_array(T, F32, (B, I)).unstack(x)
+    out_tas = [g.tensor_array(T, F32, (B, H)) for _ in range(L)]
+    max_len = g.op1("ReduceMax", [lens])
+    min_len = g.op1("ReduceMin", [lens])
+    t_bound = g.const(T, I64)
+
+    def pred(t, *rest):
+        return g.op1("Less", [t, t_bound])
+
+    def body(t, *vs):
+        hs, cs, flows = vs[:L], vs[L:2 * L], vs[2 * L:3 * L]
+        x_t = x_ta.read(t)
+        r_t = route_ta.read(t) if moe else None
+
+        def cells(masked):
+            inp, outs, nh, nc = x_t, [], [], []
+            for l in range(L):
+                ins = [inp, hs[l], cs[l], Ws[l], bs[l]] + ([t, lens] if masked else [])
+                hn, cn, o, _g = g.op("LSTMCell", ins, {"masked": masked, "forget_bias": forget_bias})
+                if moe:
+                    r = g.op1("Reshape", [g.op1("Slice", [r_t], {"begin": (l,), "size": (1,)})],
+                              {"shape": ()})
+                    oo, wa, wb = o, WA[l], WB[l]
+                    e = g.cond(r, lambda: [g.op1("Relu", [g.op1("MatMul", [oo, wa])])],
+                               lambda: [g.op1("Relu", [g.op1("MatMul", [oo, wb])])], 1)[0]
+                    o = g.op1("Add", [o, e])
+                outs.append(o)
+                nh.append(hn)
+                nc.append(cn)
+                inp = o
+            return outs + nh + nc
+
+        if length_conds:
+            def cell_branch():
+                return g.cond(g.op1("Less", [t, min_len]), lambda: cells(False),
+                              lambda: cells(True), 3 * L)
+
+            def empty_update():
+                return [g.const([[0.0] * H] * B, F32) for _ in range(L)] + list(hs) + list(cs)
+            res = g.cond(g.op1("Less", [t, max_len]), cell_branch, empty_update, 3 * L)
+        else:
+            res = cells(True)
+        outs, nh, nc = res[:L], res[L:2 * L], res[2 * L:]
+        nf = [out_tas[l].with_flow(flows[l]).write(t, outs[l]).flow for l in range(L)]
+        return [g.op1("Add", [t, g.const(1, I64)])] + nh + nc + nf
+
+    res = g.while_loop(pred, body, [g.const(0, I64)] + h0 + c0 + [ta.flow for ta in out_tas],
+                       parallel_iterations, name="rnn")
+    hT, cT, fT = res[1:1 + L], res[1 + L:1 + 2 * L], res[1 + 2 * L:]
+    out_top = out_tas[L - 1].with_flow(fT[L - 1]).stack()
+    R_out = g.placeholder("R_out", F32, (T, B, H))
+    y = g.op1("ReduceSum", [g.op1("Mul", [R_out, out_top])])
+    for l in range(L):
+        Rh = g.placeholder(f"R_h{l}", F32, (B, H))
+        Rc = g.placeholder(f"R_c{l}", F32, (B, H))
+        y = g.op1("Add", [y, g.op1("Add", [g.op1("ReduceSum", [g.op1("Mul", [Rh, hT[l]])]),
+                                           g.op1("ReduceSum", [g.op1("Mul", [Rc, cT[l]])])])])
+    fetch = {"y": y, "out": out_top}
+    for l in range(L):
+        fetch[f"hT{l}"] = hT[l]
+        fetch[f"cT{l}"] = cT[l]
+    grads = {}
+    if with_grads:
+        names, xs = ["x"], [x]
+        for l in range(L):
+            names += [f"W{l}", f"b{l}", f"h0_{l}", f"c0_{l}"]
+            xs += [Ws[l], bs[l], h0[l], c0[l]]
+            if moe:
+                names += [f"WA{l}", f"WB{l}"]
+                xs += [WA[l], WB[l]]
+        for nm, gt in zip(names, g.gradients(y, xs)):
+            grads["d" + nm] = gt
+    return RNNProgram(g, fetch, grads, T, B, I, H, L)
+
+
+def feeds_to_device(feeds, device="cuda", float_dtype=None):
+    """numpy feeds (synth.rnn_inputs) -> contiguous CUDA tensors in the session dtypes."""
+    import numpy as np
+    import torch
+    fd = float_dtype or torch.float32
+    out = {}
+    for k, v in feeds.items():
+        v = np.asarray(v)
+        if v.dtype == np.float64:
+            out[k] = torch.from_numpy(v).to(device=device, dtype=fd).contiguous()
+        elif v.dtype == np.bool_:
+            out[k] = torch.from_numpy(v).to(device=device).contiguous()
+        else:
+            out[k] = torch.from_numpy(v.astype(np.int64)).to(device=device).contiguous()
+    return out

@@ -1,0 +1,116 @@
+"""GPU parity: the CUDA path (through the C-ABI) vs the fp64 oracle on the same seeded inputs.
+
+Bar (BASELINE.json north_star): control decisions bit-exact (trip counts, branches taken,
+stack push/pop counts, Exit firings); forward outputs and gradients within max relative
+error 1e-5 on the fp32 path, measured normwise per tensor (reading R15:
+max|g - o| / max|o|).
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import __graft_entry__  # noqa: E402
+
+__graft_entry__.build()
+
+from paper_1805_01772_b200 import cf  # noqa: E402
+from paper_1805_01772_b200.models import dynamic_rnn_lstm, feeds_to_device  # noqa: E402
+
+from oracle.models import dynamic_rnn_lstm as oracle_rnn  # noqa: E402
+from oracle.models import run_program  # noqa: E402
+from synth import rnn_inputs  # noqa: E402
+
+
+def normwise(v, r):
+    r = np.asarray(r, dtype=np.float64)
+    return float(np.abs(np.asarray(v, dtype=np.float64) - r).max() / max(np.abs(r).max(), 1e-30))
+
+
+def run_device(T, B, I, H, L, f, K=0, **kw):
+    p = dynamic_rnn_lstm(T, B, I, H, L, **kw)
+    s = cf.Session(p.g, p.fetch_tensors(), precision=cf.F32, parallel_iterations=K)
+    n_conds = 64
+    outs, dead, tr = s.run(feeds_to_device(f), trace=True, branch_cap=n_conds * (T + 1))
+    torch.cuda.synchronize()
+    vals = {n: o.double().cpu().numpy() for n, o in zip(p.fetch_names(), outs)}
+    return vals, dead, tr
+
+
+def check_parity(T, B, I, H, L, mode, seed, K=None, tol=1e-5, **kw):
+    f = rnn_inputs(T, B, I, H, L, seed=seed, len_mode=mode, moe=kw.get("moe", False))
+    dev, dead, tr = run_device(T, B, I, H, L, f, K=K or 0, **kw)
+    q = oracle_rnn(T, B, I, H, L, **kw)
+    ref, otr = run_program(q, f, K=K, return_trace=True)
+    assert not any(dead)
+    errs = {k: normwise(dev[k], ref[k]) for k in ref}
+    worst = max(errs.values())
+    assert worst <= tol, sorted(errs.items(), key=lambda kv: -kv[1])[:4]
+    # ---- control trace, bit-exact
+    assert tr["trip_count"] == [otr.trip_counts[((), "rnn")], otr.trip_counts[((), "rnn_grad")]]
+    assert tr["pushes"] == sum(otr.pushes.values())
+    assert tr["pops"] == sum(otr.pops.values()) == tr["pushes"]
+    assert tr["exit_fires"] == sum(otr.exit_fires.values())
+    bb = T + 1
+    bits = tr["branch_bits"]
+    for (cid, tag), v in otr.branch.items():
+        it = tag[-1][1] if tag else 0
+        assert bits[cid * bb + it] == (2 if v else 1), (cid, tag, v)
+    n_dev = sum(1 for b in bits if b)
+    assert n_dev == len({(c, (t[-1][1] if t else 0)) for (c, t) in otr.branch})
+    return worst, tr
+
+
+@pytest.mark.parametrize("mode", ["full", "uniform", "with_zero"])
+def test_cfg1_tiny(mode):
+    """BASELINE.json configs[0]: 1 layer, hidden 8, batch 2, seq_len 5 (I = 4)."""
+    check_parity(5, 2, 4, 8, 1, mode, seed=0)
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_multilayer_ragged(seed):
+    """3 layers, odd sizes (ragged tiles everywhere), t >= max_len takes empty_update."""
+    check_parity(7, 37, 13, 45, 3, "capped", seed=seed)
+
+
+def test_multi_tile_lengths():
+    """Several GEMM tiles in every dimension, variable lengths, 2 layers."""
+    check_parity(9, 70, 40, 72, 2, "uniform", seed=4)
+
+
+@pytest.mark.parametrize("K", [1, 2, 8, 32])
+def test_parallel_iterations_bit_identical(K):
+    T, B, I, H, L = 8, 33, 20, 40, 2
+    f = rnn_inputs(T, B, I, H, L, seed=7, len_mode="uniform")
+    base, _, _ = run_device(T, B, I, H, L, f, K=1)
+    dev, _, tr = run_device(T, B, I, H, L, f, K=K)
+    for k in base:
+        assert np.array_equal(base[k], dev[k]), k
+    assert max(tr["max_inflight"]) <= K
+
+
+def test_moe_gated_branch():
+    """cond nested in the loop body with exact route bits (BASELINE.json configs[4] shape)."""
+    check_parity(6, 16, 24, 32, 2, "uniform", seed=3, moe=True)
+
+
+def test_cfg2_dynamic_rnn():
+    """BASELINE.json configs[1]: 1 layer, hidden 512, batch 64, seq_len 100, variable
+    lengths via cond/dead tokens; the capped variant runs the dead empty_update branch."""
+    worst, tr = check_parity(100, 64, 512, 512, 1, "uniform", seed=0)
+    assert tr["trip_count"] == [100, 100]
+
+
+def test_cfg2_capped_lengths():
+    check_parity(100, 64, 512, 512, 1, "capped", seed=1)
+
+
+def test_missing_feed_is_an_error():
+    p = dynamic_rnn_lstm(3, 2, 2, 4, 1)
+    s = cf.Session(p.g, p.fetch_tensors())
+    f = feeds_to_device(rnn_inputs(3, 2, 2, 4, 1, seed=0))
+    del f["x"]
+    with pytest.raises(cf.CfError) as e:
+        s.run(f)
+    assert e.value.code == "CF_E_MISSING_FEED"
