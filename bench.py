@@ -1,0 +1,312 @@
+#!/usr/bin/env python
+"""Benchmark: LSTM fwd+bwd sequence-steps/s through the dynamic-control-flow engine.
+
+One "step" = one cf_run: the whole hot path (while_loop forward with StackPush, gradient
+loop with StackPop, TensorArray reads/writes, length conds) over one batch of synthetic
+input, ONE launch of the persistent driver kernel. Workload (--config, default cfg3):
+
+  cfg3  8-layer LSTM, hidden 1024, batch 512, seq_len 200, full lengths (BASELINE.json
+        configs[2]; the metric's 1/2/4/8-B200 configuration)
+  cfg2  1 layer, hidden 512, batch 64, seq_len 100, variable lengths (configs[1])
+  cfg4  1 layer, hidden 2048, batch 256, seq_len 4000 (configs[3])
+
+sequence-steps/s = sum_b len_b (live sample-timesteps) / step time.
+--impl reference times the fp64 CPU oracle (the only reference that exists: the paper ships
+no code) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "cfg3": dict(T=200, B=512, I=1024, H=1024, L=8, len_mode="full"),
+    "cfg2": dict(T=100, B=64, I=512, H=512, L=1, len_mode="uniform"),
+    "cfg4": dict(T=4000, B=256, I=2048, H=2048, L=1, len_mode="full"),
+    "tiny": dict(T=5, B=2, I=4, H=8, L=1, len_mode="full"),
+}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+                "sm_max_mhz": 1965.0, "_fallback": True}
+
+
+class Clocks:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev=0):
+        self.dev, self.rows, self.proc = dev, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm = [float(r[1]) for r in self.rows if len(r) > 8 and r[1].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            for k, nm in enumerate(names):
+                if len(r) > 5 + k and r[5 + k].lower() == "active":
+                    reasons.add(nm)
+        mx = float(self.rows[0][2]) if self.rows and self.rows[0][2].replace(".", "").isdigit() else None
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def flops_per_step(c, lens_sum):
+    """Algorithmic FLOPs: 24*H*(I_l+H) per live sample-step per layer (fwd 8, bwd 16)."""
+    H, I, L = c["H"], c["I"], c["L"]
+    per = 0
+    for l in range(L):
+        il = I if l == 0 else H
+        per += 24 * H * (il + H)
+    return per * lens_sum
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def run_reference(args, c, cfg_name):
+    """The fp64 oracle on the host cores, each step a bounded sample (truncated T)."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    import numpy as np
+    from oracle.models import dynamic_rnn_lstm, run_program
+    from synth import rnn_inputs
+    T_s = max(2, min(c["T"], args.ref_T))
+    p = dynamic_rnn_lstm(T_s, c["B"], c["I"], c["H"], c["L"])
+    f = rnn_inputs(T_s, c["B"], c["I"], c["H"], c["L"], seed=0, len_mode=c["len_mode"])
+    lens_sum = int(np.minimum(f["len"], T_s).sum())
+    for _ in range(args.warmup_ref):
+        run_program(p, f)
+    ts = []
+    for _ in range(args.steps_ref):
+        t0 = time.perf_counter()
+        run_program(p, f)
+        ts.append(time.perf_counter() - t0)
+    t = statistics.median(ts)
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    v = lens_sum / t
+    line = {"impl": "reference", "metric": "LSTM fwd+bwd sequence-steps/sec", "value": v,
+            "unit": "sequence-steps/s", "n_gpus": world, "steps": args.steps_ref,
+            "warmup": args.warmup_ref, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg_name, **{k: c[k] for k in ("T", "B", "I", "H", "L")},
+                       "sample_T": T_s},
+            "cpu_baseline": {"value": v, "unit": "sequence-steps/s", "cores": cores, "kind": "oracle",
+                             "sample": f"{cfg_name} truncated to T={T_s} (full B/H/L), median of "
+                                       f"{args.steps_ref}"},
+            "e2e": {"value": v, "unit": "sequence-steps/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(c, cfg_name, T_s):
+    import numpy as np
+    from oracle.models import dynamic_rnn_lstm, run_program
+    from synth import rnn_inputs
+    p = dynamic_rnn_lstm(T_s, c["B"], c["I"], c["H"], c["L"])
+    f = rnn_inputs(T_s, c["B"], c["I"], c["H"], c["L"], seed=0, len_mode=c["len_mode"])
+    lens_sum = int(np.minimum(f["len"], T_s).sum())
+    t0 = time.perf_counter()
+    run_program(p, f)
+    t = time.perf_counter() - t0
+    return {"value": lens_sum / t, "unit": "sequence-steps/s", "cores": os.cpu_count(),
+            "kind": "oracle", "sample": f"{cfg_name} truncated to T={T_s} (full B/H/L), one run, "
+                                        f"{t:.1f} s"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg3", choices=list(CONFIGS))
+    ap.add_argument("--precision", default="f32", choices=["f32", "bf16"])
+    ap.add_argument("--K", type=int, default=0, help="parallel_iterations override (0 = 32)")
+    ap.add_argument("--ref-T", type=int, default=8)
+    ap.add_argument("--steps-ref", type=int, default=3)
+    ap.add_argument("--warmup-ref", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-T", type=int, default=4)
+    args = ap.parse_args()
+    c = CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, c, args.config)
+
+    import numpy as np
+    import torch
+    import __graft_entry__
+    __graft_entry__.build()
+    from paper_1805_01772_b200 import cf
+    from paper_1805_01772_b200.models import dynamic_rnn_lstm, feeds_to_device
+    from synth import rnn_inputs
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        pg = dist
+    W = max(args.warmup, 3)
+    prec = cf.F32 if args.precision == "f32" else cf.BF16
+    p = dynamic_rnn_lstm(c["T"], c["B"], c["I"], c["H"], c["L"])
+    stream = torch.cuda.current_stream()
+    sess = cf.Session(p.g, p.fetch_tensors(), precision=prec, parallel_iterations=args.K,
+                      device=local, stream=stream.cuda_stream)
+    f = rnn_inputs(c["T"], c["B"], c["I"], c["H"], c["L"], seed=rank, len_mode=c["len_mode"])
+    lens_sum = int(f["len"].sum())
+    dev = feeds_to_device(f, device=f"cuda:{local}")
+    outs = sess.alloc_outputs(device=f"cuda:{local}")
+    for _ in range(W):
+        sess.run(dev, outs)
+    torch.cuda.synchronize()
+    if pg:
+        pg.barrier()
+    kernel_ms = []
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            _, _, tr = sess.run(dev, outs, trace=True)
+            kernel_ms.append(tr["wall_ms"])
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    if pg:
+        pg.barrier()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    if pg:
+        t = torch.tensor([ms], device=f"cuda:{local}")
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        ms = float(t.item())
+    # ---- end to end through the public API with HOST buffers (pinned), per step:
+    #      H2D of the step's data (x, lengths, loss projections) + D2H of the loss
+    data_names = ["x", "len", "R_out"] + [f"R_h{l}" for l in range(c["L"])] + \
+        [f"R_c{l}" for l in range(c["L"])]
+    host = {k: v.cpu().pin_memory() for k, v in dev.items() if k in data_names}
+    h2d = sum(v.numel() * v.element_size() for v in host.values())
+    y_host = torch.empty(outs[0].shape, dtype=outs[0].dtype).pin_memory()
+    d2h = y_host.numel() * y_host.element_size()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2e_steps = max(2, min(args.steps, 5))
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        for k, v in host.items():
+            dev[k].copy_(v, non_blocking=True)
+        sess.run(dev, outs)
+        y_host.copy_(outs[0], non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / e2e_steps
+    if pg:
+        t = torch.tensor([e2e_ms], device=f"cuda:{local}")
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    if rank != 0:
+        if pg:
+            pg.destroy_process_group()
+        return
+    pk = peaks()
+    fl = flops_per_step(c, lens_sum)
+    kms = statistics.mean(kernel_ms)
+    if prec == cf.F32:
+        mhz = pk.get("sm_max_mhz", 1965.0)
+        peak = 148 * 128 * 2 * mhz * 1e6 / 1e12       # fp32 FFMA lanes x 2 flop x clock
+        roof = {"bound": "alu", "achieved": fl / (kms * 1e-3) / 1e12, "peak": peak,
+                "unit": "TFLOP/s", "frac": None, "traffic": None,
+                "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 x sm_max_mhz (DESIGN.md)",
+                "kernel": "cf_driver_kernel (persistent; all heavy work)"}
+    else:
+        peak = pk.get("bf16_tflops_sustained", 1360.6)
+        roof = {"bound": "tensor", "achieved": fl / (kms * 1e-3) / 1e12, "peak": peak,
+                "unit": "TFLOP/s", "frac": None, "traffic": None,
+                "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained",
+                "kernel": "cf_driver_kernel (persistent; all heavy work)"}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    traffic_file = os.path.join(ROOT, "profiles", f"traffic_{args.config}_{args.precision}.json")
+    if os.path.exists(traffic_file):
+        try:
+            roof["traffic"] = json.load(open(traffic_file)).get("bytes_per_launch")
+        except Exception:
+            pass
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        cpu = cpu_baseline(c, args.config, min(args.cpu_T, c["T"]))
+    line = {
+        "metric": "LSTM fwd+bwd sequence-steps/sec",
+        "value": lens_sum * world / (ms * 1e-3),
+        "unit": "sequence-steps/s",
+        "n_gpus": world, "steps": args.steps, "warmup": W, "ms_per_step": ms,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": args.precision,
+        "data": "synthetic (seeded; synth.rnn_inputs)",
+        "config": {"workload": args.config, **{k: c[k] for k in ("T", "B", "I", "H", "L")},
+                   "lengths": c["len_mode"], "parallel_iterations": args.K or 32,
+                   "parallelism": "replicas" if world > 1 else "single",
+                   "l2": "inputs/activations > L2 (no flush needed)"},
+        "loop_iterations_per_s": c["T"] / (ms * 1e-3),
+        "kernel_ms": kms,
+        "tflops": fl / (ms * 1e-3) / 1e12,
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "clocks": clk.summary(),
+        "e2e": {"value": lens_sum * world / (e2e_ms * 1e-3), "unit": "sequence-steps/s",
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": args.steps,
+    }
+    print(json.dumps(line), flush=True)
+    if pg:
+        pg.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,21 @@
+/*
+ * cf_debug.h -- test hooks of libcf. NOT part of the product API: used by tests/ to check the
+ * sm_100a tcgen05 tile engine in isolation against a plain matmul.
+ */
+#ifndef CF_DEBUG_H_
+#define CF_DEBUG_H_
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+/* C[M][N] (fp32, row-major, device) = sum_k A(m,k) * B(n,k) with bf16 device inputs:
+ *   A: a_mn = 0 -> stored [M][K] (K-major); a_mn = 1 -> stored [K][M] (MN-major)
+ *   B: b_mn = 0 -> stored [N][K] (K-major); b_mn = 1 -> stored [K][N] (MN-major)
+ * bn = 128 or 256 (tile N). M, N, K multiples of 64 (M, N: any; K: multiple of 64).
+ * Synchronous on `stream`. Returns 0 or CF_E_CUDA (15; message in cf_last_error()). */
+int32_t cf_debug_tc_gemm(int32_t M, int32_t N, int32_t K, int32_t bn, int32_t a_mn, int32_t b_mn,
+                         const void* A, const void* B, float* C, void* stream);
+#ifdef __cplusplus
+}
+#endif
+#endif

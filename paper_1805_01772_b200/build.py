@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libcf.so")
-SOURCES = ["ir.cpp", "autodiff.cpp", "capi.cpp", "compiler.cpp", "runtime.cu"]
+SOURCES = ["ir.cpp", "autodiff.cpp", "capi.cpp", "compiler.cpp", "runtime.cu", "debug.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-std=c++17", "-O3", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall", "-diag-suppress", "177,550"]
@@ -19,7 +19,7 @@ def _stale() -> bool:
         return True
     t = os.path.getmtime(LIB)
     deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + \
-        [os.path.join(HERE, "..", "include", "cf.h"), __file__]
+        [os.path.join(HERE, "..", "include", f) for f in ("cf.h", "cf_debug.h")] + [__file__]
     return any(os.path.getmtime(p) > t for p in deps if os.path.exists(p))
 
 

@@ -107,6 +107,9 @@ _sig = {
     "cf_session_fetch_dtype": (C.c_int32, [_P, C.c_int32, C.POINTER(C.c_int32)]),
     "cf_session_describe": (C.c_int32, [_P, C.c_char_p, C.c_size_t]),
     "cf_session_destroy": (None, [_P]),
+    # include/cf_debug.h (test hooks)
+    "cf_debug_tc_gemm": (C.c_int32, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                     C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
 }
 for _name, (_res, _args) in _sig.items():
     _f = getattr(_lib, _name)
@@ -477,6 +480,12 @@ class Session:
                 "branch_bits": bytes(bits)[:min(branch_cap, tr.n_branch_bits)] if bits else b"",
             }
         return outs, [bool(dead[i]) for i in range(len(outs))], tdict
+
+
+def debug_tc_gemm(M, N, K, bn, a_mn, b_mn, A, B, Cout, stream=None):
+    """Test hook (include/cf_debug.h): C = A(m,k) . B(n,k) on the tcgen05 tile engine."""
+    _check(_lib.cf_debug_tc_gemm(M, N, K, bn, a_mn, b_mn, A.data_ptr(), B.data_ptr(),
+                                 Cout.data_ptr(), stream))
 
 
 def version() -> str:

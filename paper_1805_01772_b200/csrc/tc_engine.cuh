@@ -1,0 +1,143 @@
+// tcgen05 GEMM tile engine: one 128 x BN output tile per call, warp-specialized inside a
+// 256-thread CTA (warp 0 lane 0 = TMA producer, warp 1 lane 0 = MMA issuer, all 8 warps =
+// epilogue readers of TMEM). A 4-stage smem ring (full/empty mbarriers) pipelines TMA and MMA
+// across the K loop; running k-block counters keep barrier phases consistent across tiles.
+#pragma once
+#include <cuda.h>
+
+#include "tc.cuh"
+
+namespace tc {
+
+constexpr int BM = 128;
+constexpr int BK = 64;
+constexpr int kStages = 4;
+constexpr int kStageA = BM * BK * 2;      // 16 KiB
+constexpr int kStageBmax = 256 * BK * 2;  // 32 KiB
+constexpr int kSmemTC = kStages * (kStageA + kStageBmax) + 1024 /*align*/ + 256 /*barriers*/;
+
+struct TcShared {
+  uint8_t* a[kStages];
+  uint8_t* b[kStages];
+  uint64_t* full;    // [kStages]
+  uint64_t* empty;   // [kStages]
+  uint64_t* done;    // [1]
+  uint32_t* tmem_slot;
+};
+
+// carve the dynamic smem buffer (1024-aligned for SWIZZLE_128B)
+__device__ inline TcShared tc_carve(uint8_t* dyn) {
+  TcShared s;
+  uintptr_t base = ((uintptr_t)dyn + 1023) & ~(uintptr_t)1023;
+  uint8_t* p = (uint8_t*)base;
+  for (int i = 0; i < kStages; ++i) {
+    s.a[i] = p;
+    p += kStageA;
+  }
+  for (int i = 0; i < kStages; ++i) {
+    s.b[i] = p;
+    p += kStageBmax;
+  }
+  s.full = (uint64_t*)p;
+  s.empty = s.full + kStages;
+  s.done = s.empty + kStages;
+  s.tmem_slot = (uint32_t*)(s.done + 1);
+  return s;
+}
+
+// one-time per CTA: barrier init (thread 0) + TMEM allocation (warp 2); all threads sync
+__device__ inline void tc_setup(TcShared& s) {
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kStages; ++i) {
+      mbar_init(&s.full[i], 1);
+      mbar_init(&s.empty[i], 1);
+    }
+    mbar_init(s.done, 1);
+    fence_barrier_init();
+  }
+  if (threadIdx.x / 32 == 2) tmem_alloc<256>(s.tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+}
+__device__ inline void tc_teardown(TcShared& s) {
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (threadIdx.x / 32 == 2) tmem_dealloc<256>(*s.tmem_slot);
+}
+
+// box load request: which map, coordinates, smem byte offset within the stage buffer
+struct Box {
+  const CUtensorMap* map;
+  int c0, c1, c2;
+  int off;
+};
+
+// Operand plan callbacks: fill up to 4 boxes for operand A / B of k-block kb; return count.
+// Run the K loop of one tile. `cnt` is the CTA-wide running k-block counter (same value in
+// the producer and MMA threads), `tiles` the running tile counter (epilogue done-barrier
+// phase). After return, all threads may read the accumulator with tmem_ld16.
+template <class PlanA, class PlanB>
+__device__ inline void tc_tile(TcShared& s, int nk, int bn, int a_mn, int b_mn, uint32_t& cnt,
+                               uint32_t& tiles, PlanA plan_a, PlanB plan_b) {
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t stage_b = (uint32_t)bn * BK * 2;
+  if (warp == 0 && lane == 0) {
+    uint32_t c = cnt;
+    for (int kb = 0; kb < nk; ++kb, ++c) {
+      const int st = c % kStages;
+      const uint32_t round = c / kStages;
+      mbar_wait(&s.empty[st], (round & 1) ^ 1);
+      mbar_arrive_expect_tx(&s.full[st], kStageA + stage_b);
+      Box bx[4];
+      int na = plan_a(kb, bx);
+      for (int i = 0; i < na; ++i)
+        tma_load_3d(s.a[st] + bx[i].off, bx[i].map, &s.full[st], bx[i].c0, bx[i].c1, bx[i].c2);
+      int nb = plan_b(kb, bx);
+      for (int i = 0; i < nb; ++i)
+        tma_load_3d(s.b[st] + bx[i].off, bx[i].map, &s.full[st], bx[i].c0, bx[i].c1, bx[i].c2);
+    }
+  } else if (warp == 1 && lane == 0) {
+    const uint32_t idesc = idesc_bf16(BM, bn, a_mn, b_mn);
+    const uint32_t tmem = *s.tmem_slot;
+    uint32_t c = cnt;
+    for (int kb = 0; kb < nk; ++kb, ++c) {
+      const int st = c % kStages;
+      const uint32_t round = c / kStages;
+      mbar_wait(&s.full[st], round & 1);
+      tc_fence_after();
+      const uint32_t sa = smem_u32(s.a[st]), sb = smem_u32(s.b[st]);
+#pragma unroll
+      for (int k = 0; k < BK / 16; ++k) {
+        uint64_t da = a_mn ? sdesc_sw128(sa + k * 2048, 8192, 1024) : sdesc_sw128(sa + k * 32, 16, 1024);
+        uint64_t db = b_mn ? sdesc_sw128(sb + k * 2048, 8192, 1024) : sdesc_sw128(sb + k * 32, 16, 1024);
+        mma_bf16(tmem, da, db, idesc, (kb | k) != 0);
+      }
+      mma_commit(&s.empty[st]);   // frees the stage when these MMAs have read it
+    }
+    mma_commit(s.done);           // accumulator complete
+  }
+  cnt += nk;
+  // everyone waits for the accumulator
+  mbar_wait(s.done, tiles & 1);
+  tiles++;
+  tc_fence_after();
+}
+
+// accumulator element access for the epilogue: warp w reads TMEM lanes 32*(w%4)..+31 (tile
+// rows), columns [col0, col0+16)
+__device__ inline void tc_acc16(TcShared& s, int col0, float* v) {
+  const int warp = threadIdx.x / 32;
+  const uint32_t taddr = *s.tmem_slot + ((uint32_t)(32 * (warp % 4)) << 16) + (uint32_t)col0;
+  tmem_ld16(taddr, v);
+}
+
+// end of tile: all TMEM reads done before the next tile's MMAs overwrite the accumulator
+__device__ inline void tc_tile_end() {
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+}
+
+}  // namespace tc

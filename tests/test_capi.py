@@ -18,11 +18,11 @@ from oracle.graph import Builder  # noqa: E402
 from oracle.autodiff import gradients as oracle_gradients  # noqa: E402
 from oracle.models import dynamic_rnn_lstm as oracle_rnn  # noqa: E402
 
-HDR = os.path.join(os.path.dirname(__file__), "..", "include", "cf.h")
+HDRS = [os.path.join(os.path.dirname(__file__), "..", "include", h) for h in ("cf.h", "cf_debug.h")]
 
 
 def declared_functions():
-    src = open(HDR).read()
+    src = "".join(open(h).read() for h in HDRS)
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
     return sorted(set(re.findall(r"\b(cf_[a-z_0-9]+)\s*\(", src)) -
                   {"cf_pred_fn", "cf_body_fn", "cf_branch_fn", "cf_status"})
