@@ -199,9 +199,10 @@ def main():
     stream = torch.cuda.current_stream()
     sess = cf.Session(p.g, p.fetch_tensors(), precision=prec, parallel_iterations=args.K,
                       device=local, stream=stream.cuda_stream)
-    f = rnn_inputs(c["T"], c["B"], c["I"], c["H"], c["L"], seed=rank, len_mode=c["len_mode"])
+    f = rnn_inputs(c["T"], c["B"], c["I"], c["H"], c["L"], seed=rank, len_mode=c["len_mode"],
+                   bf16=prec == cf.BF16)
     lens_sum = int(f["len"].sum())
-    dev = feeds_to_device(f, device=f"cuda:{local}")
+    dev = feeds_to_device(f, device=f"cuda:{local}", session=sess)
     outs = sess.alloc_outputs(device=f"cuda:{local}")
     for _ in range(W):
         sess.run(dev, outs)

@@ -62,10 +62,99 @@ struct Compiler {
   std::map<int, int> ta_id;           // TACreate node -> ta id
   std::map<int, int> stack_id;        // StackCreate node -> stack id
   std::vector<std::vector<std::pair<int, int>>> extra_edges;   // per frame: (before, after)
+  std::vector<uint8_t> vdt;           // device dtype per value id
+  std::vector<int> ta_dt;             // device dtype per TensorArray
+  std::map<int, int> acc_of_loopvar;  // loop Merge node -> acc id
+  std::map<int, int> acc_of_add;      // fused Add node -> acc id
+  std::map<std::pair<int, int>, int> acc_of_src;   // (LSTMCellGrad node, port) -> acc id
+  std::vector<std::pair<int, int>> reg_bufs;       // (buffer id, registry index)
+  bool bf16() const { return o.precision == CF_BF16; }
 
   Compiler(const Graph& gg, const CompileOpts& oo) : g(gg), o(oo) {}
 
   int vid(TRef t) const { return vbase[t.node] + t.port; }
+  int32_t vdt_of(TRef t) const { return vdt[vid(t)]; }
+
+  // handle -> creator node (TACreate / TAGrad / StackCreate) through routing
+  int trace_creator(TRef h) const {
+    for (int k = 0; k < 256; ++k) {
+      const Node& n = g.nodes[h.node];
+      if (n.op == "TACreate" || n.op == "StackCreate") return n.id;
+      if (n.op == "TAGrad" && h.port == 0) return n.id;
+      if (n.in.empty()) break;
+      h = n.in[0];
+    }
+    return -1;
+  }
+
+  // Device dtypes (reading R16 / DESIGN.md "bf16 policy"): values connected through routing
+  // (Switch/Merge/Enter/Exit/NextIteration/Identity), TensorArray slots and stacks share one
+  // storage dtype; in bf16 mode the LSTM GEMM operands (x, h, gates, out) are bf16, every
+  // other float (cell state c, gradients, accumulators, loss) stays fp32.
+  void assign_dtypes() {
+    const int N = (int)g.nodes.size();
+    int nv = P.n_vids;
+    int extra = (int)P.tas.size() + (int)P.stacks.size();
+    std::vector<int> uf(nv + extra);
+    for (size_t i = 0; i < uf.size(); ++i) uf[i] = (int)i;
+    std::function<int(int)> find = [&](int x) { return uf[x] == x ? x : uf[x] = find(uf[x]); };
+    auto unite = [&](int a, int b) { uf[find(a)] = find(b); };
+    auto ta_cls = [&](int ta) { return nv + ta; };
+    auto st_cls = [&](int sid) { return nv + (int)P.tas.size() + sid; };
+    for (int i = 0; i < N; ++i) {
+      const Node& n = g.nodes[i];
+      const std::string& op = n.op;
+      int o0 = vbase[i];
+      if (op == "Identity" || op == "StopGradient" || op == "Reshape" || op == "Enter" ||
+          op == "Exit" || op == "NextIteration" ||
+          (op == "Cast" && is_float(n.odt[0]) && is_float(g.dtype(n.in[0]))))
+        unite(vid(n.in[0]), o0);
+      else if (op == "Switch") {
+        unite(vid(n.in[0]), o0);
+        unite(vid(n.in[0]), o0 + 1);
+      } else if (op == "Merge") {
+        unite(vid(n.in[0]), o0);
+        unite(vid(n.in[1]), o0);
+      } else if (op == "TAWrite" || op == "TARead" || op == "TAUnstack" || op == "TAStack") {
+        int ta = trace_ta(n.in[0]);
+        if (op == "TAWrite") unite(vid(n.in[2]), ta_cls(ta));
+        if (op == "TARead" || op == "TAStack") unite(o0, ta_cls(ta));
+        if (op == "TAUnstack") unite(vid(n.in[1]), ta_cls(ta));
+      } else if (op == "StackPush" || op == "StackPop") {
+        int c = trace_creator(n.in[0]);
+        if (c >= 0 && stack_id.count(c)) {
+          int sid = stack_id.at(c);
+          unite(op == "StackPush" ? vid(n.in[1]) : o0, st_cls(sid));
+        }
+      }
+    }
+    std::vector<uint8_t> want(uf.size(), 0);
+    if (bf16()) {
+      for (int i = 0; i < N; ++i) {
+        const Node& n = g.nodes[i];
+        if (n.op == "LSTMCell") {
+          for (int j : {0, 1}) want[find(vid(n.in[j]))] = 1;
+          for (int p : {0, 2, 3}) want[find(vbase[i] + p)] = 1;
+        } else if (n.op == "LSTMCellGrad") {
+          for (int j : {0, 1, 4}) want[find(vid(n.in[j]))] = 1;
+        }
+      }
+    }
+    vdt.assign(nv, D_NONE);
+    for (int i = 0; i < N; ++i) {
+      const Node& n = g.nodes[i];
+      for (size_t p = 0; p < n.odt.size(); ++p) {
+        int v = vbase[i] + (int)p;
+        int32_t d = n.odt[p];
+        vdt[v] = is_float(d) ? (want[find(v)] ? D_BF16 : D_F32) : (uint8_t)dev_dt(d, o.precision);
+      }
+    }
+    ta_dt.assign(P.tas.size(), D_F32);
+    for (size_t t = 0; t < P.tas.size(); ++t) {
+      int32_t gd = P.tas[t].dt;   // graph dtype stored temporarily
+      ta_dt[t] = is_float(gd) ? (want[find(ta_cls((int)t))] ? D_BF16 : D_F32) : dev_dt(gd, o.precision);
+    }
+  }
   bool is_heavy(const Node& n) const {
     if (n.op == "Placeholder" || n.op == "Const" || n.op == "Identity" || n.op == "StopGradient" ||
         n.op == "Reshape" || n.op == "Switch" || n.op == "Merge" || n.op == "Enter" ||
@@ -147,12 +236,12 @@ struct Compiler {
       if (n.op == "TACreate") {
         DTA t{};
         t.size = (int32_t)n.attrs.i("size");
-        int32_t d = dev_dt((int32_t)n.attrs.i("dtype"), o.precision);
-        t.dt = d;
-        t.elem_bytes = numel(n.attrs.v("elem_shape")) * dev_size(d);
+        t.dt = (int32_t)n.attrs.i("dtype");   // graph dtype until assign_dtypes()
+        t.elem_bytes = numel(n.attrs.v("elem_shape"));   // elements until assign_dtypes()
         t.grad_id = -1;
         ta_id[n.id] = (int)P.tas.size();
         P.tas.push_back(t);
+        ta_shape.push_back(n.attrs.v("elem_shape"));
       }
     }
     for (auto& n : g.nodes) {
@@ -164,13 +253,24 @@ struct Compiler {
           t.grad_id = -1;
           P.tas[f].grad_id = (int)P.tas.size();
           P.tas.push_back(t);
+          ta_shape.push_back(ta_shape[f]);
         }
       }
     }
+    // stack ids (capacity set after bounds)
+    for (auto& n : g.nodes)
+      if (n.op == "StackCreate") {
+        stack_id[n.id] = (int)P.stacks.size();
+        P.stacks.push_back(DStack{});
+      }
+    assign_dtypes();
     for (size_t k = 0; k < P.tas.size(); ++k) {
       DTA& t = P.tas[k];
+      t.dt = ta_dt[k];
+      t.elem_bytes *= dev_size(t.dt);
       t.base = add_buf((size_t)t.size * t.elem_bytes, t.is_grad != 0,
                        std::string(t.is_grad ? "grad " : "") + "TensorArray " + std::to_string(k));
+      if (t.dt == D_BF16) register_buf((int)t.base, t.size, ta_rows_cols(k));
     }
     int slot_total = 0;
     for (auto& t : P.tas) slot_total += t.size;
@@ -192,16 +292,15 @@ struct Compiler {
     }
     for (auto& n : g.nodes) {
       if (n.op == "StackCreate") {
-        DStack s{};
+        DStack& s = P.stacks[stack_id.at(n.id)];
         auto it = frame_id.find(n.attrs.s("frame"));
         if (it == frame_id.end()) unsupported(n, "stack of unknown frame");
         s.capacity = (int32_t)bound[it->second];
         s.entry_off = P.stack_pool;
         P.stack_pool += s.capacity;
-        stack_id[n.id] = (int)P.stacks.size();
-        P.stacks.push_back(s);
       }
     }
+    detect_accumulators();
 
     // ---- device nodes
     P.nodes.resize(N);
@@ -227,7 +326,7 @@ struct Compiler {
         FeedInfo fi;
         fi.vid = vbase[n.id];
         fi.graph_dt = odt;
-        fi.dev_dt = dev_dt(odt, o.precision);
+        fi.dev_dt = vdt[vbase[n.id]];
         fi.bytes = numel(n.osh[0]) * dev_size(fi.dev_dt);
         fi.scalar_ctrl = !is_float(odt) && n.osh[0].empty();
         P.feeds[n.attrs.s("name")] = fi;
@@ -244,21 +343,33 @@ struct Compiler {
           d.imm[0] = v;
           d.aux[1] = dev_dt(odt, o.precision);
         } else {
-          int32_t dd = dev_dt(odt, o.precision);
-          std::vector<uint8_t> bytes((size_t)numel(n.osh[0]) * dev_size(dd));
-          if (odt == F64) {
-            for (int64_t k = 0; k < numel(n.osh[0]); ++k) {
+          int32_t dd = vdt[vbase[n.id]];
+          int64_t ne = numel(n.osh[0]);
+          std::vector<uint8_t> bytes((size_t)ne * dev_size(dd));
+          for (int64_t k = 0; k < ne && is_float(odt); ++k) {
+            float f;
+            if (odt == F64) {
               double x;
               std::memcpy(&x, n.data.data() + 8 * k, 8);
-              float f = (float)x;
+              f = (float)x;
+            } else {
+              std::memcpy(&f, n.data.data() + 4 * k, 4);
+            }
+            if (dd == D_BF16) {
+              uint32_t u;
+              std::memcpy(&u, &f, 4);
+              u = (u + 0x7FFF + ((u >> 16) & 1)) >> 16;
+              uint16_t h = (uint16_t)u;
+              std::memcpy(bytes.data() + 2 * k, &h, 2);
+            } else {
               std::memcpy(bytes.data() + 4 * k, &f, 4);
             }
-          } else {
-            std::memcpy(bytes.data(), n.data.data(), std::min(bytes.size(), n.data.size()));
           }
+          if (!is_float(odt)) std::memcpy(bytes.data(), n.data.data(), std::min(bytes.size(), n.data.size()));
           d.aux[0] = 0;
           d.aux[1] = dd;
           d.imm[0] = add_buf(bytes.size(), false, "const " + std::to_string(n.id), bytes.data());
+          if (dd == D_BF16 && n.osh[0].size() >= 2) register_shape((int)d.imm[0], n.osh[0], 1);
         }
       } else if (op == "Identity" || op == "StopGradient" || op == "Reshape" ||
                  (op == "Cast" && is_float(odt) && is_float(g.dtype(n.in[0])))) {
@@ -307,6 +418,9 @@ struct Compiler {
         d.op = OP_STACK_POP;
       } else if (odt == FLOW) {
         d.op = OP_FLOW;
+      } else if (acc_of_add.count(n.id)) {
+        d.op = OP_ACC;
+        d.aux[0] = acc_of_add.at(n.id);
       } else if (!is_heavy(n)) {
         // integer / bool control arithmetic on the device driver
         bool all_scalar = true;
@@ -354,8 +468,7 @@ struct Compiler {
     for (auto& t : fetches) {
       FetchInfo fi;
       fi.vid = vid(t);
-      int32_t d = g.dtype(t);
-      fi.dev_dt = dev_dt(d, o.precision);
+      fi.dev_dt = vdt[fi.vid];
       fi.bytes = numel(g.shape(t)) * dev_size(fi.dev_dt);
       P.fetches.push_back(fi);
       P.fetch_vids.push_back(fi.vid);
@@ -366,7 +479,7 @@ struct Compiler {
     std::vector<int64_t> frame_heavy(frame_ctx.size(), 0);
     for (int nid : heavy_nodes) {
       int f = frame_of[nid];
-      int k = g.nodes[nid].op == "LSTMCellGrad" ? 2 : 1;
+      int k = g.nodes[nid].op == "LSTMCellGrad" ? 3 : 1;
       if (f >= 0) frame_heavy[f] += k + 4;
       else root_heavy += k + 1;
     }
@@ -376,7 +489,8 @@ struct Compiler {
         if (f >= 0) frame_heavy[f] += 2;
         else root_heavy += 2;
       }
-    int64_t total = root_heavy + 64 + (int64_t)fetches.size();
+    int64_t total = root_heavy + 64 + (int64_t)fetches.size() + 2 * (int64_t)heavy_nodes.size() +
+                    2 * (int64_t)P.accs.size();
     for (size_t f = 0; f < frame_ctx.size(); ++f) total += frame_heavy[f] * (bound[f] + 1);
     (void)per_iter_heavy;
     (void)max_tiles;
@@ -395,10 +509,11 @@ struct Compiler {
     for (size_t f = 0; f < frame_ctx.size(); ++f)
       ds << "frame " << P.frame_names[f] << " K=" << P.frames[f].K << " bound=" << bound[f]
          << " body=" << P.frames[f].n_body << "\n";
-    int counts[4] = {0, 0, 0, 0};
+    int counts[5] = {0, 0, 0, 0, 0};
     for (auto& pl : P.places) counts[pl.kind]++;
+    ds << "accumulators=" << P.accs.size() << " tma_operands=" << P.reg.size() << "\n";
     ds << "placements root=" << counts[0] << " ring=" << counts[1] << " arena=" << counts[2]
-       << " ta=" << counts[3] << "\n";
+       << " ta=" << counts[3] << " acc=" << counts[4] << "\n";
     P.describe = ds.str();
   }
 
@@ -467,6 +582,12 @@ struct Compiler {
       return;
     }
     if (op == "LSTMCell" || op == "LSTMCellGrad") {
+      if (bf16()) {
+        int64_t I = g.shape(n.in[0])[1], H = g.shape(n.in[1])[1];
+        if (I % 256 != 0 || H % 256 != 0)
+          unsupported(n, "bf16 tcgen05 LSTM path needs input and hidden sizes that are multiples "
+                         "of 256 (use CF_F32 for other shapes)");
+      }
       d.aux[0] = op == "LSTMCell" ? HK_LSTM_FWD : HK_LSTM_BWD_EW;
       d.aux[1] = n.attrs.b("masked");
       d.imm[0] = g.shape(n.in[0])[0];
@@ -477,6 +598,8 @@ struct Compiler {
       int32_t fbits;
       std::memcpy(&fbits, &ff, 4);
       d.aux[2] = fbits;
+      d.aux[3] = acc_of_src.count({n.id, 3}) ? acc_of_src.at({n.id, 3}) : -1;
+      d.aux[4] = acc_of_src.count({n.id, 4}) ? acc_of_src.at({n.id, 4}) : -1;
       return;
     }
     unsupported(n, "float op not lowered");
@@ -510,59 +633,184 @@ struct Compiler {
   }
 
   std::vector<int64_t> frame_bound_cache;
+  std::vector<Shape> ta_shape;
+
+  // ---- TMA operand registry (bf16 buffers viewed as [slots][rows][cols])
+  void register_buf(int buf, int slots, std::pair<int, int> rc) {
+    if (rc.first <= 0 || rc.second <= 0 || rc.second % 64 != 0) return;
+    DReg r{};
+    r.base = buf;
+    r.slots = slots;
+    r.rows = rc.first;
+    r.cols = rc.second;
+    r.slot_bytes = (int64_t)rc.first * rc.second * 2;
+    P.reg.push_back(r);
+  }
+  void register_shape(int buf, const Shape& shp, int slots) {
+    if (shp.size() == 2) register_buf(buf, slots, {(int)shp[0], (int)shp[1]});
+    else if (shp.size() == 3) register_buf(buf, slots * (int)shp[0], {(int)shp[1], (int)shp[2]});
+  }
+  std::pair<int, int> ta_rows_cols(size_t k) {
+    const Shape& s = ta_shape.at(k);
+    if (s.size() != 2) return {0, 0};
+    return {(int)s[0], (int)s[1]};
+  }
+
+  // ---- in-place accumulator fusion: loop variable v with
+  //   Switch_v:1 -> Add(., X) -> NextIteration_v   and X routed (within the iteration) from
+  //   LSTMCellGrad dW/db outputs or zero constants  ==>  one fp32 buffer updated in place.
+  void detect_accumulators() {
+    for (size_t f = 0; f < frame_ctx.size(); ++f) {
+      const Ctx& ctx = g.ctxs[frame_ctx[f]];
+      for (size_t j = 1; j < ctx.loop_vars.size(); ++j) {
+        const LoopVar& lv = ctx.loop_vars[j];
+        if (!is_float(g.nodes[lv.merge].odt[0])) continue;
+        const auto& sc = cons[vbase[lv.sw] + 1];
+        if (sc.size() != 1) continue;
+        const Node& add = g.nodes[sc[0].first];
+        if (add.op != "Add" || add.in.size() != 2) continue;
+        const auto& ac = cons[vbase[add.id]];
+        if (ac.size() != 1 || ac[0].first != lv.next) continue;
+        TRef other = add.in[sc[0].second == 0 ? 1 : 0];
+        if (g.shape(other) != g.nodes[lv.merge].osh[0]) continue;
+        // backward routing closure of `other`
+        std::vector<TRef> st{other};
+        std::set<int> seen;
+        std::vector<std::pair<int, int>> srcs;
+        bool ok = true;
+        int port_kind = -1;
+        while (!st.empty() && ok) {
+          TRef t = st.back();
+          st.pop_back();
+          if (!seen.insert(vid(t)).second) continue;
+          const Node& p = g.nodes[t.node];
+          if (p.op == "Merge" && !p.attrs.b("loop")) {
+            st.push_back(p.in[0]);
+            st.push_back(p.in[1]);
+          } else if (p.op == "Identity" || (p.op == "Switch" && !p.attrs.b("loop"))) {
+            st.push_back(p.in[0]);
+          } else if (p.op == "LSTMCellGrad" && (t.port == 3 || t.port == 4)) {
+            if (port_kind >= 0 && port_kind != t.port) ok = false;
+            port_kind = t.port;
+            // the port must only feed this routing chain
+            for (auto [c, idx] : cons[vid(t)]) {
+              const std::string& cop = g.nodes[c].op;
+              if (!(cop == "Merge" || cop == "Identity" || cop == "Switch" || c == add.id)) ok = false;
+            }
+            srcs.push_back({p.id, t.port});
+          } else if (p.op == "Const") {
+            for (auto b : p.data) ok &= (b == 0);
+          } else {
+            ok = false;
+          }
+        }
+        if (!ok || srcs.empty()) continue;
+        DAcc a{};
+        a.frame = (int)f;
+        a.bytes = numel(g.nodes[lv.merge].osh[0]) * 4;
+        a.base = add_buf(a.bytes, false, "accumulator " + std::to_string(lv.merge));
+        TRef init = g.nodes[lv.enter].in[0];
+        a.init_vid = vid(init);
+        const Node& in = g.nodes[init.node];
+        a.init_zero = in.op == "Const" && std::all_of(in.data.begin(), in.data.end(), [](uint8_t b) { return b == 0; });
+        int id = (int)P.accs.size();
+        P.accs.push_back(a);
+        acc_of_loopvar[lv.merge] = id;
+        acc_of_add[add.id] = id;
+        for (auto& sp : srcs) acc_of_src[sp] = id;
+      }
+    }
+  }
+
+  // number of placement slots of a heavy node: outputs + internal scratch / prep buffers
+  int n_places(const Node& n) const {
+    int np = (int)n.odt.size();
+    if (n.op == "LSTMCellGrad") np += bf16() ? 2 : 1;   // dz scratch (+ W^T prep)
+    if (n.op == "LSTMCell" && bf16()) np += 1;           // gate-interleaved W prep
+    return np;
+  }
 
   void place_outputs(const Node& n) {
     DNode& d = P.nodes[n.id];
     d.place_off = (int)P.places.size();
     int f = frame_of[n.id];
     int nout = (int)n.odt.size();
-    int extra = (n.op == "LSTMCellGrad") ? 1 : 0;   // dz scratch
-    for (int p = 0; p < nout + extra; ++p) {
+    const int np = n_places(n);
+    for (int p = 0; p < np; ++p) {
       PlaceDesc pl{};
       Shape shp;
       int32_t dd;
-      if (p < nout) {
+      bool internal = p >= nout;
+      enum { NONE, DZ, WPREP, WTPREP } kind = NONE;
+      int64_t extra_bytes = 0;
+      if (!internal) {
         shp = n.osh[p];
-        dd = dev_dt(n.odt[p], o.precision);
+        dd = vdt[vbase[n.id] + p];
+      } else if (n.op == "LSTMCellGrad" && p == nout) {
+        kind = DZ;
+        int64_t B = g.shape(n.in[0])[0], H = g.shape(n.in[1])[1];
+        shp = {B, 4 * H};
+        dd = bf16() ? D_BF16 : D_F32;
+        if (bf16()) extra_bytes = ((B + 127) / 128) * 4 * H * 4;   // db partials
       } else {
-        shp = {g.shape(n.in[0])[0], 4 * g.shape(n.in[1])[1]};
-        dd = D_F32;
+        kind = n.op == "LSTMCell" ? WPREP : WTPREP;
+        Shape w = g.shape(n.in[3]);
+        shp = kind == WPREP ? w : Shape{w[1], w[0]};
+        dd = D_BF16;
       }
       pl.dt = dd;
-      pl.elem_bytes = numel(shp) * dev_size(dd);
-      int64_t alloc_elem = pl.elem_bytes;
-      if (n.op == "ReduceSum" && n.attrs.i("axis", -1) != 0) alloc_elem = 8192;  // scalar + partials at +4 KiB
-      pl.elem_bytes = alloc_elem;
+      int64_t body = numel(shp) * dev_size(dd);
+      pl.elem_bytes = ((body + 1023) / 1024) * 1024 + extra_bytes;
+      if (!internal) pl.elem_bytes = body;
+      if (n.op == "ReduceSum" && n.attrs.i("axis", -1) != 0) pl.elem_bytes = 8192;  // + partials
       bool pinned = false;
       int taw = -1;
-      if (p < nout) closure(vbase[n.id] + p, &pinned, &taw, f);
-      if (f < 0) {
+      if (!internal) closure(vbase[n.id] + p, &pinned, &taw, f);
+      auto acc_it = acc_of_src.find({n.id, p});
+      if (acc_it != acc_of_src.end()) {
+        pl.kind = PL_ACC;
+        pl.slots = acc_it->second;   // acc id
+        pl.base = -1;
+        pl.dt = D_F32;
+      } else if (kind == WPREP || kind == WTPREP || f < 0) {
         pl.kind = PL_ROOT;
         pl.slots = 1;
-        pl.base = add_buf(alloc_elem, false, "root " + n.op + std::to_string(n.id));
-      } else if (taw >= 0 && P.tas[trace_ta(g.nodes[taw].in[0])].elem_bytes ==
-                                 numel(shp) * dev_size(dd) &&
+        pl.base = add_buf(pl.elem_bytes, false, "root " + n.op + std::to_string(n.id));
+        if (dd == D_BF16) register_shape((int)pl.base, shp, 1);
+      } else if (taw >= 0 && P.tas[trace_ta(g.nodes[taw].in[0])].elem_bytes == body &&
                  P.tas[trace_ta(g.nodes[taw].in[0])].dt == dd) {
         const Node& w = g.nodes[taw];
         pl.kind = PL_TA;
         pl.ta = trace_ta(w.in[0]);
         pl.index_vid = vid(w.in[1]);
-        pl.elem_bytes = numel(shp) * dev_size(dd);
         // the write index and the handle must be evaluated before this heavy node
         extra_edges[f].push_back({w.in[1].node, n.id});
         extra_edges[f].push_back({w.in[0].node, n.id});
       } else if (pinned) {
         pl.kind = PL_ARENA;
-        pl.slots = -1;   // patched with the frame bound
+        pl.slots = -1;   // allocated with the frame bound
         pl.base = -1;
       } else {
         int K = o.parallel_iterations > 0 ? o.parallel_iterations : g.ctxs[frame_ctx[f]].K;
         pl.kind = PL_RING;
         pl.slots = K + 1;
-        pl.base = add_buf((size_t)alloc_elem * (K + 1), false, "ring " + n.op + std::to_string(n.id));
+        pl.base = add_buf((size_t)pl.elem_bytes * (K + 1), false, "ring " + n.op + std::to_string(n.id));
+        if (dd == D_BF16 && shp.size() == 2)
+          register_buf_stride((int)pl.base, K + 1, (int)shp[0], (int)shp[1], pl.elem_bytes);
       }
       P.places.push_back(pl);
     }
+  }
+
+  void register_buf_stride(int buf, int slots, int rows, int cols, int64_t slot_bytes) {
+    if (cols % 64 != 0) return;
+    DReg r{};
+    r.base = buf;
+    r.slots = slots;
+    r.rows = rows;
+    r.cols = cols;
+    r.slot_bytes = slot_bytes;
+    P.reg.push_back(r);
   }
 
   void build_orders(const std::vector<int64_t>& bound) {
@@ -572,13 +820,16 @@ struct Compiler {
       const DNode& d = P.nodes[i];
       if (d.op != OP_HEAVY) continue;
       int f = frame_of[i];
-      int nout = d.n_out + (g.nodes[i].op == "LSTMCellGrad" ? 1 : 0);
-      for (int p = 0; p < nout; ++p) {
+      int np = n_places(g.nodes[i]);
+      for (int p = 0; p < np; ++p) {
         PlaceDesc& pl = P.places[d.place_off + p];
         if (pl.kind == PL_ARENA) {
           pl.slots = (int32_t)bound[f];
           pl.base = add_buf((size_t)pl.elem_bytes * bound[f], false,
                             "arena " + g.nodes[i].op + std::to_string(i));
+          if (pl.dt == D_BF16 && p < (int)g.nodes[i].osh.size() && g.nodes[i].osh[p].size() == 2)
+            register_buf_stride((int)pl.base, (int)bound[f], (int)g.nodes[i].osh[p][0],
+                                (int)g.nodes[i].osh[p][1], pl.elem_bytes);
         }
       }
     }
@@ -645,6 +896,13 @@ struct Compiler {
       F.counter_enter = ctx.loop_vars.at(0).enter;
       F.iter_base = iter_base;
       iter_base += (int)bound[f] + 2;
+      F.acc_off = (int)P.order.size();
+      F.n_acc = 0;
+      for (size_t a = 0; a < P.accs.size(); ++a)
+        if (P.accs[a].frame == (int)f) {
+          P.order.push_back((int)a);
+          F.n_acc++;
+        }
     }
     P.iter_counters = iter_base;
     // ---- root steps: root nodes + frames as super nodes
@@ -722,6 +980,8 @@ HostProgram compile(const Graph& g, const CompileOpts& o, const std::vector<TRef
   if (!errs.empty()) throw CfError(CF_E_INVALID_GRAPH, errs[0]);
   Compiler c(g, o);
   c.run(fetches);
+  c.P.vdt = c.vdt;
+  c.P.precision = o.precision;
   return std::move(c.P);
 }
 

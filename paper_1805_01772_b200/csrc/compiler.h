@@ -40,6 +40,10 @@ struct HostProgram {
   std::vector<cfdev::DTA> tas;
   std::vector<cfdev::DStack> stacks;
   std::vector<int32_t> fetch_vids;
+  std::vector<cfdev::DAcc> accs;
+  std::vector<cfdev::DReg> reg;       // base = buffer id until the runtime patches it
+  std::vector<uint8_t> vdt;
+  int32_t precision = CF_F32;
   std::vector<std::string> frame_names;
   int n_vids = 0;
   int n_conds = 0;

@@ -48,6 +48,7 @@ enum Op : int32_t {
   OP_STACK_PUSH,
   OP_STACK_POP,
   OP_HEAVY,         // aux0: heavy kind (HK_*), aux1: sub-op / flags
+  OP_ACC,           // fused accumulator Add (aux0: acc id): output = the accumulator buffer
   OP__COUNT
 };
 
@@ -68,6 +69,12 @@ enum HeavyKind : int32_t {
   HK_LSTM_BWD_EW,   // dz, dc_prev
   HK_LSTM_BWD_MM,   // dxh = dz W, dW = dz^T [x,h], db = colsum dz
   HK_ACC,           // dst += src (grad TensorArray double write)
+  HK_PREP_WP,       // bf16 gate-interleaved W rows for the forward GEMM (B operand)
+  HK_PREP_WT,       // bf16 W^T for the d[x,h] GEMM (B operand)
+  HK_LSTM_FWD_TC,   // tcgen05 gate GEMM + fused LSTM epilogue
+  HK_LSTM_BWD_EW_BF,// dz (bf16) + dc + db partials
+  HK_LSTM_DXH_TC,   // tcgen05 d[x,h] = dz W
+  HK_LSTM_DW_TC,    // tcgen05 dW (+)= dz^T [x,h] (MN-major operands) + db
   HK__COUNT
 };
 
@@ -77,7 +84,7 @@ enum EwOp : int32_t {
 };
 
 // ---- placement of a heavy output (SURVEY.md §7.2 "static buffer pointer per (edge, slot)")
-enum Place : int32_t { PL_ROOT = 0, PL_RING = 1, PL_ARENA = 2, PL_TA = 3 };
+enum Place : int32_t { PL_ROOT = 0, PL_RING = 1, PL_ARENA = 2, PL_TA = 3, PL_ACC = 4 };
 
 struct PlaceDesc {
   int32_t kind;
@@ -105,6 +112,24 @@ struct DNode {
 };
 static_assert(sizeof(DNode) % 8 == 0, "DNode layout");
 
+// Fused loop accumulator ("sum gradients eagerly into new loop
+// variables"): one buffer updated in place by its producers, initialised at frame start.
+struct DAcc {
+  int64_t base;         // device buffer (fp32)
+  int64_t bytes;
+  int32_t frame;
+  int32_t init_vid;     // value id of the loop variable's init (Enter input)
+  int32_t init_zero;    // 1: init is a zeros constant (fill), else copy from init_vid
+  int32_t pad;
+};
+
+// TMA operand registry entry: a bf16 buffer viewed as [slots][rows][cols]
+struct DReg {
+  int64_t base;
+  int64_t slot_bytes;
+  int32_t slots, rows, cols, map0;   // map0: index of its 3 tensor maps (KA, KB, MN)
+};
+
 struct DFrame {
   int32_t K;            // parallel_iterations
   int32_t bound;        // iteration bound (arena slots / stack capacity)
@@ -114,6 +139,7 @@ struct DFrame {
   int32_t counter_switch;       // node id of the hidden counter's Switch
   int32_t counter_enter;        // node id of the hidden counter's Enter
   int32_t iter_base;            // offset into per-iteration counters (size bound + 1)
+  int32_t acc_off, n_acc;       // accumulators initialised at frame start (into prog.order)
   int32_t pad;
 };
 
@@ -148,6 +174,13 @@ struct Prog {
   const DTA* tas;
   const DStack* stacks;
   const int32_t* fetch_vids;
+  const DAcc* accs;
+  int32_t n_accs;
+  int32_t n_reg;                // registry entries (static part; feeds appended per run)
+  const DReg* reg;
+  const void* maps;             // CUtensorMap[3 * n_reg], 64-byte aligned
+  int32_t precision;            // 3 = f32 SIMT, 5 = bf16 tcgen05
+  int32_t pad2;
 };
 
 // ---- heavy instance record (written by the driver, read by workers)
@@ -156,8 +189,9 @@ struct Inst {
   int32_t ntiles, frame;
   int32_t iter, pad;
   int64_t n, m, k;      // sizes
-  int64_t p[14];        // pointers
-  int64_t s[4];         // scalars
+  int64_t p[20];        // pointers (p[13] = primary output for generic kinds)
+  int64_t s[8];         // scalars
+  int64_t dts;          // device dtypes: input j at bits [4j, 4j+4), output at [32, 36)
 };
 
 // ---- run-time state shared by the driver CTA and the worker CTAs
@@ -211,6 +245,9 @@ struct RunArgs {
   int64_t watchdog_ns;
   int32_t sched_seed;
   int32_t num_workers;
+  int32_t* prep_inst;        // [n_nodes] per-run weight-prep instance of LSTM nodes (-1)
+  int32_t* acc_writer;       // [n_accs] latest instance writing each accumulator
+  const uint8_t* vdt;        // [n_vids] device dtype of every value
 };
 
 }  // namespace cfdev

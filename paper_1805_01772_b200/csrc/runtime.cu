@@ -27,6 +27,8 @@
 #include "compiler.h"
 #include "ir.h"
 #include "program.h"
+#include "tiles_tc.cuh"
+#include "tmap.h"
 
 using namespace cfdev;
 
@@ -118,10 +120,10 @@ __device__ void tile_ew(const Inst& I, int tile) {
   const int64_t e1 = min(n, b0 + kEwTile);
   const int op = I.sub;
   const int flags = (int)I.s[1];
-  float* out = (float*)I.p[13];
+  void* out = (void*)I.p[13];
+  const int odt = (int)((I.dts >> 32) & 15);
   auto in = [&](int j, int64_t e) -> float {
-    const float* p = (const float*)I.p[j];
-    return (flags >> j & 1) ? p[0] : p[e];
+    return ldf((const void*)I.p[j], (int)((I.dts >> (4 * j)) & 15), (flags >> j & 1) ? 0 : e);
   };
   for (int64_t e = b0 + threadIdx.x; e < e1; e += kThreads) {
     float r = 0.0f;
@@ -134,7 +136,7 @@ __device__ void tile_ew(const Inst& I, int tile) {
       case EW_TANH: r = tanhf(in(0, e)); break;
       case EW_RELU: r = fmaxf(in(0, e), 0.0f); break;
       case EW_RELUGRAD: r = in(1, e) > 0.0f ? in(0, e) : 0.0f; break;
-      case EW_BIASADD: r = in(0, e) + ((const float*)I.p[1])[e % I.m]; break;
+      case EW_BIASADD: r = in(0, e) + ldf((const void*)I.p[1], (int)((I.dts >> 4) & 15), e % I.m); break;
       case EW_SELECT: {
         const uint8_t* c = (const uint8_t*)I.p[0];
         bool cv = I.s[2] ? c[0] != 0 : (I.m > 0 ? c[e / I.m] != 0 : c[e] != 0);
@@ -147,15 +149,15 @@ __device__ void tile_ew(const Inst& I, int tile) {
       }
       case EW_ZEROS: r = 0.0f; break;
     }
-    out[e] = r;
+    stf(out, odt, e, r);
   }
 }
 
 __device__ void tile_fill(const Inst& I, int tile) {
-  float v = I.p[0] ? *(const float*)I.p[0] : __int_as_float((int)I.s[0]);
-  float* out = (float*)I.p[13];
+  float v = I.p[0] ? ldf((const void*)I.p[0], (int)(I.dts & 15), 0) : __int_as_float((int)I.s[0]);
+  const int odt = (int)((I.dts >> 32) & 15);
   int64_t b0 = (int64_t)tile * kEwTile, e1 = min(I.n, b0 + kEwTile);
-  for (int64_t e = b0 + threadIdx.x; e < e1; e += kThreads) out[e] = v;
+  for (int64_t e = b0 + threadIdx.x; e < e1; e += kThreads) stf((void*)I.p[13], odt, e, v);
 }
 
 __device__ void tile_copy(const Inst& I, int tile) {
@@ -176,10 +178,10 @@ __device__ void tile_copy(const Inst& I, int tile) {
 }
 
 __device__ void tile_acc(const Inst& I, int tile) {
-  const float* src = (const float*)I.p[0];
-  float* dst = (float*)I.p[13];
+  const int sdt = (int)(I.dts & 15), odt = (int)((I.dts >> 32) & 15);
   int64_t b0 = (int64_t)tile * kEwTile, e1 = min(I.n, b0 + kEwTile);
-  for (int64_t e = b0 + threadIdx.x; e < e1; e += kThreads) dst[e] += src[e];
+  for (int64_t e = b0 + threadIdx.x; e < e1; e += kThreads)
+    stf((void*)I.p[13], odt, e, ldf((void*)I.p[13], odt, e) + ldf((const void*)I.p[0], sdt, e));
 }
 
 __device__ float block_sum(float v, float* red) {
@@ -195,13 +197,14 @@ __device__ float block_sum(float v, float* red) {
 
 // deterministic: tile t sums a fixed contiguous chunk; the last tile sums partials in order
 __device__ void tile_reduce_sum(const Inst& I, int tile, float* sm) {
-  const float* x = (const float*)I.p[0];
+  const void* x = (const void*)I.p[0];
+  const int xdt = (int)(I.dts & 15);
   float* out = (float*)I.p[13];
   float* partial = out + 1024;   // placement reserves 1024 partial floats at +4 KiB
   int64_t chunk = (I.n + I.ntiles - 1) / I.ntiles;
   int64_t b0 = (int64_t)tile * chunk, e1 = min(I.n, b0 + chunk);
   float s = 0.0f;
-  for (int64_t e = b0 + threadIdx.x; e < e1; e += kThreads) s += x[e];
+  for (int64_t e = b0 + threadIdx.x; e < e1; e += kThreads) s += ldf(x, xdt, e);
   s = block_sum(s, sm);
   if (threadIdx.x == 0) partial[tile] = s;
 }
@@ -217,30 +220,30 @@ __device__ void finalize_reduce_sum(const Inst& I, float* sm) {
 }
 
 __device__ void tile_reduce_sum0(const Inst& I, int tile) {
-  const float* x = (const float*)I.p[0];
-  float* out = (float*)I.p[13];
+  const void* x = (const void*)I.p[0];
+  const int xdt = (int)(I.dts & 15), odt = (int)((I.dts >> 32) & 15);
   int64_t M = I.m, N = I.n;
   int64_t c = (int64_t)tile * kThreads + threadIdx.x;
   if (c >= N) return;
   float s = 0.0f;
-  for (int64_t r = 0; r < M; ++r) s += x[r * N + c];
-  out[c] = s;
+  for (int64_t r = 0; r < M; ++r) s += ldf(x, xdt, r * N + c);
+  stf((void*)I.p[13], odt, c, s);
 }
 
 __device__ void tile_matmul(const Inst& I, int tile, float* sm) {
   int M = (int)I.m, N = (int)I.n, K = (int)I.k;
   bool ta = I.sub & 1, tb = I.sub & 2;
   int64_t lda = I.s[0], ldb = I.s[1];
-  const float* A = (const float*)I.p[0];
-  const float* B = (const float*)I.p[1];
-  float* C = (float*)I.p[13];
+  const void* A = (const void*)I.p[0];
+  const void* B = (const void*)I.p[1];
+  const int adt = (int)(I.dts & 15), bdt = (int)((I.dts >> 4) & 15), odt = (int)((I.dts >> 32) & 15);
   int tn = (N + 63) / 64;
   int m0 = (tile / tn) * 64, n0 = (tile % tn) * 64;
   gemm_tile64(
       sm, m0, n0, M, N, K,
-      [&](int m, int k) { return ta ? A[(int64_t)k * lda + m] : A[(int64_t)m * lda + k]; },
-      [&](int k, int n) { return tb ? B[(int64_t)n * ldb + k] : B[(int64_t)k * ldb + n]; },
-      [&](int m, int n, float v) { C[(int64_t)m * N + n] = v; });
+      [&](int m, int k) { return ldf(A, adt, ta ? (int64_t)k * lda + m : (int64_t)m * lda + k); },
+      [&](int k, int n) { return ldf(B, bdt, tb ? (int64_t)n * ldb + k : (int64_t)k * ldb + n); },
+      [&](int m, int n, float v) { stf((void*)I.p[13], odt, (int64_t)m * N + n, v); });
 }
 
 // Fused LSTM cell forward (reading R9): tile = 32 batch rows x 32 hidden units; each thread
@@ -401,14 +404,17 @@ __device__ void tile_lstm_bwd_mm(const Inst& I, int tile, float* sm) {
     gemm_tile64(
         sm, m0, n0, G, KT, B, [&](int m, int k) { return dz[(int64_t)k * G + m]; },
         [&](int k, int n) { return n < In ? x[(int64_t)k * In + n] : h[(int64_t)k * H + (n - In)]; },
-        [&](int m, int n, float v) { dW[(int64_t)m * KT + n] = v; });
+        [&](int m, int n, float v) {
+          float* d = dW + (int64_t)m * KT + n;
+          *d = (I.s[6] & 1) ? *d + v : v;
+        });
   } else {
     int tt = tile - tA - tB;
     int col = tt * kThreads + threadIdx.x;
     if (col < G) {
       float s = 0.0f;
       for (int r = 0; r < B; ++r) s += dz[(int64_t)r * G + col];
-      db[col] = s;
+      db[col] = (I.s[6] & 2) ? db[col] + s : s;
     }
   }
 }
@@ -577,6 +583,7 @@ struct Driver {
         }
         *ptr = pl.base + (int64_t)it * pl.elem_bytes;
         return true;
+      case PL_ACC: *ptr = P.accs[pl.slots].base; return true;
       case PL_TA: {
         int64_t ix;
         if (!scalar(A.toks[pl.index_vid], &ix)) return false;
@@ -601,16 +608,161 @@ struct Driver {
   }
 
   // ---------------------------------------------------------------- heavy ops
-  __device__ int eval_heavy(const DNode& d) {
+  // ---------------------------------------------------------------- operand registry
+  // pointer -> (tensor map, slot) for a bf16 [rows][cols] GEMM operand; kind 0 = K-major A
+  // (box 64x128), 1 = K-major B (box 64x256), 2 = MN-major (box 64x64)
+  __device__ bool resolve(int64_t p, int rows, int cols, int kind, int64_t* map, int64_t* slot) {
+    for (int i = 0; i < P.n_reg; ++i) {
+      const DReg& r = P.reg[i];
+      if (r.rows != rows || r.cols != cols) continue;
+      if (p < r.base || p >= r.base + (int64_t)r.slots * r.slot_bytes) continue;
+      int64_t off = p - r.base;
+      if (off % r.slot_bytes) continue;
+      *slot = off / r.slot_bytes;
+      *map = (int64_t)((const uint8_t*)P.maps + (int64_t)(r.map0 + kind) * 128);
+      return true;
+    }
+    fail(CF_E_UNSUPPORTED, -100 - rows);
+    return false;
+  }
+
+  __device__ int64_t pack_dts(const DNode& d, int out_dt) {
+    int64_t w = 0;
+    for (int j = 0; j < d.n_in && j < 8; ++j) w |= (int64_t)(in_tok(d, j).dt & 15) << (4 * j);
+    w |= (int64_t)(out_dt & 15) << 32;
+    return w;
+  }
+
+  // per-run weight preparation (bf16 permuted W / W^T), created on first use of the node
+  __device__ int32_t prep(const DNode& d, int nid, int kind, int64_t dst) {
+    if (A.prep_inst[nid] >= 0) return A.prep_inst[nid];
+    const int64_t In = d.imm[1], H = d.imm[2], KT = In + H;
+    int ntiles = kind == HK_PREP_WP ? (int)((4 * H + 15) / 16) : (int)((KT / 64) * (4 * H / 128));
+    int32_t id = new_inst(kind, 0, ntiles);
+    if (id < 0) return -1;
+    Inst& I = A.insts[id];
+    I.n = H;
+    I.k = KT;
+    I.p[0] = in_tok(d, 3).v;
+    I.p[13] = dst;
+    add_dep(id, in_tok(d, 3).writer);
+    submit(id);
+    A.prep_inst[nid] = id;
+    return id;
+  }
+
+  __device__ int eval_lstm_tc(const DNode& d, int nid, const int64_t* outp) {
     const int kind = d.aux[0];
-    int64_t outp[6] = {0, 0, 0, 0, 0, 0};
-    int nplace = d.n_out + (kind == HK_LSTM_BWD_EW ? 1 : 0);
+    const bool masked = d.aux[1] & 1;
+    int64_t t = 0;
+    if (masked && !scalar(in_tok(d, 5), &t)) return EV_BLOCKED;
+    const int64_t B = d.imm[0], In = d.imm[1], H = d.imm[2], KT = In + H;
+    auto ip = [&](int j) { return in_tok(d, j).v; };
+    if (kind == HK_LSTM_FWD) {
+      int32_t pw = prep(d, nid, HK_PREP_WP, outp[4]);
+      int64_t mx, sx, mh, sh, mw, sw;
+      if (!resolve(ip(0), (int)B, (int)In, 0, &mx, &sx) || !resolve(ip(1), (int)B, (int)H, 0, &mh, &sh) ||
+          !resolve(outp[4], (int)(4 * H), (int)KT, 1, &mw, &sw))
+        return EV_ERROR;
+      int32_t id = new_inst(HK_LSTM_FWD_TC, masked, (int)(((B + 127) / 128) * (H / 64)));
+      if (id < 0) return EV_ERROR;
+      Inst& I = A.insts[id];
+      I.m = B; I.k = In; I.n = H;
+      I.p[0] = mx; I.p[1] = mh; I.p[2] = ip(2); I.p[3] = mw; I.p[4] = ip(4);
+      I.p[5] = masked ? ip(6) : 0;
+      I.p[6] = ip(1);
+      for (int p = 0; p < 4; ++p) I.p[8 + p] = outp[p];
+      I.s[0] = t; I.s[1] = d.aux[2]; I.s[2] = sx; I.s[3] = sh;
+      for (int j = 0; j < d.n_in; ++j) add_dep(id, in_tok(d, j).writer);
+      add_dep(id, pw);
+      set_out(d, 0, ptr_tok(outp[0], id, D_BF16));
+      set_out(d, 1, ptr_tok(outp[1], id, D_F32));
+      set_out(d, 2, ptr_tok(outp[2], id, D_BF16));
+      set_out(d, 3, ptr_tok(outp[3], id, D_BF16));
+      submit(id);
+      return EV_OK;
+    }
+    // ---- backward: EW (dz, dc, db partials) -> DXH (dx, dh) and DW (dW, db)
+    const int o = masked ? 7 : 5;
+    const int64_t dz_ptr = outp[5];
+    const int64_t dz_bytes = ((B * 4 * H * 2 + 1023) / 1024) * 1024;
+    int32_t pw = prep(d, nid, HK_PREP_WT, outp[6]);
+    int32_t e = new_inst(HK_LSTM_BWD_EW_BF, masked, (int)(((B + 127) / 128) * (H / 64)));
+    if (e < 0) return EV_ERROR;
+    {
+      Inst& I = A.insts[e];
+      I.m = B; I.k = In; I.n = H;
+      I.p[2] = ip(2); I.p[4] = ip(4); I.p[5] = masked ? ip(6) : 0;
+      I.p[6] = ip(o); I.p[7] = ip(o + 1); I.p[8] = ip(o + 2);
+      I.p[9] = outp[2]; I.p[10] = dz_ptr;
+      I.s[0] = t; I.s[4] = in_tok(d, o + 2).dt; I.s[5] = dz_bytes;
+      for (int j = 0; j < d.n_in; ++j) add_dep(e, in_tok(d, j).writer);
+    }
+    int64_t mz, sz, mwt, swt, mzn, szn, mxn, sxn, mhn, shn;
+    if (!resolve(dz_ptr, (int)B, (int)(4 * H), 0, &mz, &sz) ||
+        !resolve(outp[6], (int)KT, (int)(4 * H), 1, &mwt, &swt) ||
+        !resolve(dz_ptr, (int)B, (int)(4 * H), 2, &mzn, &szn) ||
+        !resolve(ip(0), (int)B, (int)In, 2, &mxn, &sxn) ||
+        !resolve(ip(1), (int)B, (int)H, 2, &mhn, &shn))
+      return EV_ERROR;
+    int32_t x = new_inst(HK_LSTM_DXH_TC, masked, (int)(((B + 127) / 128) * (KT / 256)));
+    if (x < 0) return EV_ERROR;
+    {
+      Inst& I = A.insts[x];
+      I.m = B; I.k = In; I.n = H;
+      I.p[0] = mz; I.p[1] = mwt; I.p[5] = masked ? ip(6) : 0; I.p[6] = ip(o);
+      I.p[11] = outp[0]; I.p[12] = outp[1];
+      I.s[0] = t; I.s[2] = sz;
+      add_dep(x, e);
+      add_dep(x, pw);
+      add_dep(x, in_tok(d, o).writer);
+    }
+    const int acc_w = d.aux[3], acc_b = d.aux[4];
+    int32_t w = new_inst(HK_LSTM_DW_TC, masked,
+                         (int)((4 * H / 128) * (KT / 256) + (4 * H + 255) / 256));
+    if (w < 0) return EV_ERROR;
+    {
+      Inst& I = A.insts[w];
+      I.m = B; I.k = In; I.n = H;
+      I.p[0] = mzn; I.p[1] = mxn; I.p[2] = mhn;
+      I.p[3] = outp[3]; I.p[4] = outp[4]; I.p[5] = dz_ptr + dz_bytes;
+      I.s[2] = szn; I.s[3] = sxn; I.s[4] = shn;
+      I.s[6] = (acc_w >= 0 ? 1 : 0) | (acc_b >= 0 ? 2 : 0);
+      add_dep(w, e);
+      add_dep(w, in_tok(d, 0).writer);
+      add_dep(w, in_tok(d, 1).writer);
+      if (acc_w >= 0) add_dep(w, A.acc_writer[acc_w]);
+      if (acc_b >= 0) add_dep(w, A.acc_writer[acc_b]);
+    }
+    set_out(d, 0, ptr_tok(outp[0], x, D_F32));
+    set_out(d, 1, ptr_tok(outp[1], x, D_F32));
+    set_out(d, 2, ptr_tok(outp[2], e, D_F32));
+    set_out(d, 3, ptr_tok(outp[3], w, D_F32));
+    set_out(d, 4, ptr_tok(outp[4], w, D_F32));
+    submit(e);
+    submit(x);
+    submit(w);
+    if (acc_w >= 0) A.acc_writer[acc_w] = w;
+    if (acc_b >= 0) A.acc_writer[acc_b] = w;
+    return EV_OK;
+  }
+
+  // ---------------------------------------------------------------- heavy ops
+  __device__ int eval_heavy(const DNode& d, int nid) {
+    const int kind = d.aux[0];
+    int64_t outp[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const bool tcm = P.precision == D_BF16;
+    int nplace = d.n_out;
+    if (kind == HK_LSTM_BWD_EW) nplace += tcm ? 2 : 1;
+    if (kind == HK_LSTM_FWD && tcm) nplace += 1;
     for (int p = 0; p < nplace; ++p)
       if (!place(d, p, &outp[p])) return st->error ? EV_ERROR : EV_BLOCKED;
+    if (tcm && (kind == HK_LSTM_FWD || kind == HK_LSTM_BWD_EW)) return eval_lstm_tc(d, nid, outp);
     auto ip = [&](int j) { return in_tok(d, j).v; };
     auto dep_all = [&](int32_t id) {
       for (int j = 0; j < d.n_in; ++j) add_dep(id, in_tok(d, j).writer);
     };
+    const int odt = P.places[d.place_off].dt;
     if (kind == HK_LSTM_FWD || kind == HK_LSTM_BWD_EW) {
       const bool masked = d.aux[1] & 1;
       int64_t t = 0;
@@ -656,6 +808,7 @@ struct Driver {
         int tC = (int)((G + kThreads - 1) / kThreads);
         int32_t m = new_inst(HK_LSTM_BWD_MM, masked, tA + tB + tC);
         if (m < 0) return EV_ERROR;
+        const int acc_w = d.aux[3], acc_b = d.aux[4];
         {
           Inst& I = A.insts[m];
           I.m = B; I.k = In; I.n = H;
@@ -670,8 +823,11 @@ struct Driver {
           I.p[13] = outp[3];
           I.s[3] = outp[4];
           I.s[0] = t;
+          I.s[6] = (acc_w >= 0 ? 1 : 0) | (acc_b >= 0 ? 2 : 0);
           dep_all(m);
           add_dep(m, e);
+          if (acc_w >= 0) add_dep(m, A.acc_writer[acc_w]);
+          if (acc_b >= 0) add_dep(m, A.acc_writer[acc_b]);
         }
         set_out(d, 0, ptr_tok(outp[0], m, D_F32));
         set_out(d, 1, ptr_tok(outp[1], m, D_F32));
@@ -680,6 +836,8 @@ struct Driver {
         set_out(d, 4, ptr_tok(outp[4], m, D_F32));
         submit(e);
         submit(m);
+        if (acc_w >= 0) A.acc_writer[acc_w] = m;
+        if (acc_b >= 0) A.acc_writer[acc_b] = m;
       }
       return EV_OK;
     }
@@ -697,6 +855,7 @@ struct Driver {
         I.s[0] = d.n_in;
         I.s[1] = d.aux[2];
         I.s[2] = d.aux[3];
+        I.dts = pack_dts(d, odt);
         break;
       }
       case HK_FILL: {
@@ -707,6 +866,7 @@ struct Driver {
         I.n = n;
         I.p[0] = ip(0);
         I.p[13] = outp[0];
+        I.dts = pack_dts(d, odt);
         break;
       }
       case HK_REDUCE_SUM: {
@@ -719,6 +879,7 @@ struct Driver {
         I.n = n;
         I.p[0] = ip(0);
         I.p[13] = outp[0];
+        I.dts = pack_dts(d, odt);
         break;
       }
       case HK_REDUCE_SUM0: {
@@ -729,6 +890,7 @@ struct Driver {
         I.n = d.imm[1];
         I.p[0] = ip(0);
         I.p[13] = outp[0];
+        I.dts = pack_dts(d, odt);
         break;
       }
       case HK_MATMUL: {
@@ -742,6 +904,7 @@ struct Driver {
         I.p[13] = outp[0];
         I.s[0] = d.imm[3] & 0xffffffffLL;
         I.s[1] = d.imm[3] >> 32;
+        I.dts = pack_dts(d, odt);
         break;
       }
       default:
@@ -749,7 +912,7 @@ struct Driver {
         return EV_ERROR;
     }
     dep_all(id);
-    set_out(d, 0, ptr_tok(outp[0], id, D_F32));
+    set_out(d, 0, ptr_tok(outp[0], id, odt));
     submit(id);
     return EV_OK;
   }
@@ -1097,13 +1260,21 @@ struct Driver {
         st->pops++;
         break;
       }
+      case OP_ACC: {
+        // fused accumulator: the producers already added in place
+        const DAcc& a = P.accs[d.aux[0]];
+        Tok t = ptr_tok(a.base, A.acc_writer[d.aux[0]], D_F32);
+        t.dead = dead;
+        set_out(d, 0, t);
+        break;
+      }
       case OP_HEAVY: {
         if (dead) {
           set_dead_all(d);
           st->dead_skipped++;
           break;
         }
-        res = eval_heavy(d);
+        res = eval_heavy(d, nid);
         break;
       }
       default:
@@ -1135,6 +1306,26 @@ struct Driver {
     oldest = 0;
     body_pc = 0;
     iter_started = false;
+    // fused accumulators start from the loop variable's initial value
+    for (int k = 0; k < F.n_acc; ++k) {
+      int a = P.order[F.acc_off + k];
+      const DAcc& ac = P.accs[a];
+      int32_t id;
+      if (ac.init_zero) {
+        id = new_inst(HK_FILL, 0, (int)((ac.bytes / 4 + kEwTile - 1) / kEwTile));
+        if (id < 0) return;
+        A.insts[id].n = ac.bytes / 4;
+        A.insts[id].p[0] = 0;
+        A.insts[id].s[0] = 0;
+        A.insts[id].p[13] = ac.base;
+        A.insts[id].dts = (int64_t)D_F32 << 32;
+        submit(id);
+      } else {
+        const Tok& it0 = A.toks[ac.init_vid];
+        id = copy_inst(ac.base, it0.v, ac.bytes, it0.writer);
+      }
+      A.acc_writer[a] = id;
+    }
   }
 
   // one step of control evaluation; returns true on progress
@@ -1247,7 +1438,15 @@ __device__ void worker_loop(const RunArgs& A) {
   __shared__ __align__(16) float sm[32 * 33 + 32 * 129 + 64];
   __shared__ unsigned long long s_entry;
   __shared__ int s_last;
+  extern __shared__ __align__(1024) uint8_t dyn_smem[];
   RunState* st = A.st;
+  const bool tcmode = A.prog.precision == D_BF16;
+  tc::TcShared ts{};
+  uint32_t tc_cnt = 0, tc_tiles = 0;
+  if (tcmode) {
+    ts = tc::tc_carve(dyn_smem);
+    tc::tc_setup(ts);
+  }
   while (true) {
     if (threadIdx.x == 0) {
       unsigned long long idx = atomicAdd(&st->q_head, 1ULL);
@@ -1263,11 +1462,12 @@ __device__ void worker_loop(const RunArgs& A) {
         backoff(spins);
       }
       __threadfence();
+      if (A.prog.precision == D_BF16) tc::fence_proxy_async_global();
       s_entry = e;
     }
     __syncthreads();
     unsigned long long e = s_entry;
-    if (e == ~0ULL) return;
+    if (e == ~0ULL) break;
     const int32_t id = (int32_t)(e >> 32);
     const int tile = (int)(e & 0xffffffffULL);
     __shared__ Inst s_inst;
@@ -1287,8 +1487,16 @@ __device__ void worker_loop(const RunArgs& A) {
       case HK_LSTM_FWD: tile_lstm_fwd(I, tile, sm); break;
       case HK_LSTM_BWD_EW: tile_lstm_bwd_ew(I, tile); break;
       case HK_LSTM_BWD_MM: tile_lstm_bwd_mm(I, tile, sm); break;
+      case HK_PREP_WP: tile_prep_wp(I, tile); break;
+      case HK_PREP_WT: tile_prep_wt(I, tile, (float*)dyn_smem); break;
+      case HK_LSTM_FWD_TC: tile_lstm_fwd_tc(I, tile, ts, tc_cnt, tc_tiles); break;
+      case HK_LSTM_BWD_EW_BF: tile_lstm_bwd_ew_bf(I, tile, sm); break;
+      case HK_LSTM_DXH_TC: tile_lstm_dxh_tc(I, tile, ts, tc_cnt, tc_tiles); break;
+      case HK_LSTM_DW_TC: tile_lstm_dw_tc(I, tile, ts, tc_cnt, tc_tiles); break;
       default: break;
     }
+    // epilogue stores (generic proxy) must be visible to later TMA (async proxy) reads
+    if (tcmode) tc::fence_proxy_async_global();
     __syncthreads();
     if (threadIdx.x == 0) {
       __threadfence();
@@ -1317,6 +1525,7 @@ __device__ void worker_loop(const RunArgs& A) {
       }
     }
   }
+  if (tcmode) tc::tc_teardown(ts);
 }
 
 __global__ void __launch_bounds__(kThreads, 1) cf_driver_kernel(RunArgs A) {
@@ -1358,6 +1567,10 @@ struct cf_session {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   int64_t watchdog_ns = 60LL * 1000 * 1000 * 1000;
   int sched_seed = 0;
+  int dyn_smem = 0;
+  std::vector<DReg> reg_host;
+  std::vector<CUtensorMap> maps_host;
+  int n_reg_static = 0;
 };
 
 namespace {
@@ -1392,8 +1605,6 @@ void build_session(cf_session* s, const cf::Graph& g, const cf_run_opts* o,
   }
   if (co.precision != CF_F32 && co.precision != CF_BF16)
     throw cf::CfError(CF_E_DTYPE, "precision must be CF_F32 or CF_BF16");
-  if (co.precision == CF_BF16)
-    throw cf::CfError(CF_E_UNSUPPORTED, "CF_BF16 path not built in this library version");
   s->precision = co.precision;
   s->P = cf::compile(g, co, fetches);
   int ndev = 0;
@@ -1420,10 +1631,12 @@ void build_session(cf_session* s, const cf::Graph& g, const cf_run_opts* o,
   }
   auto addr = [&](int64_t id) { return (int64_t)(uintptr_t)s->buf_ptr.at(id); };
   for (auto& pl : P.places)
-    if (pl.kind != PL_TA) pl.base = addr(pl.base);
+    if (pl.kind != PL_TA && pl.kind != PL_ACC) pl.base = addr(pl.base);
   for (auto& n : P.nodes)
     if (n.op == OP_CONST && n.aux[0] == 0) n.imm[0] = addr(n.imm[0]);
   for (auto& t : P.tas) t.base = addr(t.base);
+  for (auto& a : P.accs) a.base = addr(a.base);
+  for (auto& r : P.reg) r.base = addr(r.base);
   s->ta_base_host.clear();
   for (auto& t : P.tas) s->ta_base_host.push_back(t.base);
   // ---- tables
@@ -1447,6 +1660,37 @@ void build_session(cf_session* s, const cf::Graph& g, const cf_run_opts* o,
   pg.tas = upload(s, P.tas);
   pg.stacks = upload(s, P.stacks);
   pg.fetch_vids = upload(s, P.fetch_vids);
+  pg.accs = upload(s, P.accs);
+  pg.n_accs = (int)P.accs.size();
+  pg.precision = s->precision == CF_BF16 ? D_BF16 : D_F32;
+  // ---- TMA operand registry: 3 tensor maps per bf16 buffer (K-major A / B boxes, MN box);
+  //      feeds are appended at every cf_run
+  {
+    int n_static = (int)P.reg.size();
+    int cap = n_static + (int)P.feeds.size() + 1;
+    std::vector<CUtensorMap> maps((size_t)3 * cap);
+    for (int i = 0; i < n_static; ++i) {
+      DReg& r = P.reg[i];
+      r.map0 = 3 * i;
+      maps[3 * i + 0] = cf::make_map_bf16_strided((void*)r.base, r.cols, r.rows, r.slots, r.slot_bytes, 64, 128);
+      maps[3 * i + 1] = cf::make_map_bf16_strided((void*)r.base, r.cols, r.rows, r.slots, r.slot_bytes, 64, 256);
+      maps[3 * i + 2] = cf::make_map_bf16_strided((void*)r.base, r.cols, r.rows, r.slots, r.slot_bytes, 64, 64);
+    }
+    s->reg_host = P.reg;
+    s->reg_host.resize(cap);
+    s->maps_host = maps;
+    s->n_reg_static = n_static;
+    pg.reg = (const DReg*)dalloc(s, sizeof(DReg) * cap);
+    pg.maps = dalloc(s, sizeof(CUtensorMap) * 3 * cap);
+    CUDA_OK(cudaMemcpy((void*)pg.reg, s->reg_host.data(), sizeof(DReg) * cap, cudaMemcpyHostToDevice));
+    CUDA_OK(cudaMemcpy((void*)pg.maps, maps.data(), sizeof(CUtensorMap) * 3 * cap, cudaMemcpyHostToDevice));
+    pg.n_reg = n_static;
+  }
+  A.vdt = upload(s, P.vdt);
+  A.prep_inst = (int32_t*)dalloc(s, 4 * P.nodes.size());
+  s->fill_ff_each_run.push_back({A.prep_inst, (int)(4 * P.nodes.size())});
+  A.acc_writer = (int32_t*)dalloc(s, 4 * std::max<size_t>(P.accs.size(), 1));
+  s->fill_ff_each_run.push_back({A.acc_writer, (int)(4 * std::max<size_t>(P.accs.size(), 1))});
   // ---- runtime state
   A.st = (RunState*)dalloc(s, sizeof(RunState));
   s->zero_each_run.push_back({A.st, sizeof(RunState)});
@@ -1497,8 +1741,10 @@ void build_session(cf_session* s, const cf::Graph& g, const cf_run_opts* o,
   A.sched_seed = s->sched_seed;
   // ---- grid: one CTA per SM, all co-resident (cooperative launch)
   int sms = 0, per_sm = 0;
+  s->dyn_smem = s->precision == CF_BF16 ? tc::kSmemTC : 0;
+  CUDA_OK(cudaFuncSetAttribute(cf_driver_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, s->dyn_smem));
   CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->device));
-  CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cf_driver_kernel, kThreads, 0));
+  CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cf_driver_kernel, kThreads, s->dyn_smem));
   if (per_sm < 1) throw cf::CfError(CF_E_CUDA, "driver kernel cannot be resident");
   int workers = o && o->num_workers > 0 ? o->num_workers : sms - 1;
   s->grid = std::min(workers + 1, sms * per_sm);
@@ -1566,6 +1812,39 @@ cf_status cf_run(cf_session* s, int32_t n_feed, const char* const* feed_names,
       preset.push_back(t);
       preset_vid.push_back(fi.vid);
     }
+    // bf16 feeds become TMA operands: registry entries + tensor maps for this run
+    if (s->precision == CF_BF16) {
+      int n = s->n_reg_static;
+      for (int i = 0; i < n_feed; ++i) {
+        auto it = P.feeds.find(feed_names[i]);
+        if (it == P.feeds.end() || it->second.dev_dt != D_BF16) continue;
+        const cf_buffer& b = feeds[i];
+        int64_t rows, cols, slots;
+        if (b.rank == 2) { slots = 1; rows = b.shape[0]; cols = b.shape[1]; }
+        else if (b.rank == 3) { slots = b.shape[0]; rows = b.shape[1]; cols = b.shape[2]; }
+        else continue;
+        if (cols % 64 || n >= (int)s->reg_host.size()) continue;
+        DReg r{};
+        r.base = (int64_t)(uintptr_t)b.data;
+        r.slots = (int32_t)slots; r.rows = (int32_t)rows; r.cols = (int32_t)cols;
+        r.slot_bytes = rows * cols * 2;
+        r.map0 = 3 * n;
+        s->reg_host[n] = r;
+        s->maps_host[3 * n + 0] = cf::make_map_bf16_strided(b.data, cols, rows, slots, r.slot_bytes, 64, 128);
+        s->maps_host[3 * n + 1] = cf::make_map_bf16_strided(b.data, cols, rows, slots, r.slot_bytes, 64, 256);
+        s->maps_host[3 * n + 2] = cf::make_map_bf16_strided(b.data, cols, rows, slots, r.slot_bytes, 64, 64);
+        ++n;
+      }
+      int nf = n - s->n_reg_static;
+      if (nf > 0) {
+        CUDA_OK(cudaMemcpyAsync((void*)(A.prog.reg + s->n_reg_static), s->reg_host.data() + s->n_reg_static,
+                                sizeof(DReg) * nf, cudaMemcpyHostToDevice, s->stream));
+        CUDA_OK(cudaMemcpyAsync((uint8_t*)A.prog.maps + sizeof(CUtensorMap) * 3 * s->n_reg_static,
+                                s->maps_host.data() + 3 * s->n_reg_static, sizeof(CUtensorMap) * 3 * nf,
+                                cudaMemcpyHostToDevice, s->stream));
+      }
+      A.prog.n_reg = n;
+    }
     // ta bases reset (unstack may alias)
     CUDA_OK(cudaMemcpyAsync(A.ta_base, s->ta_base_host.data(), 8 * s->ta_base_host.size(),
                             cudaMemcpyHostToDevice, s->stream));
@@ -1585,7 +1864,7 @@ cf_status cf_run(cf_session* s, int32_t n_feed, const char* const* feed_names,
     void* kargs[] = {(void*)&A};
     CUDA_OK(cudaEventRecord(s->ev0, s->stream));
     CUDA_OK(cudaLaunchCooperativeKernel((void*)cf_driver_kernel, dim3(s->grid), dim3(kThreads), kargs,
-                                        0, s->stream));
+                                        s->dyn_smem, s->stream));
     CUDA_OK(cudaEventRecord(s->ev1, s->stream));
     CUDA_OK(cudaStreamSynchronize(s->stream));
     RunState st;

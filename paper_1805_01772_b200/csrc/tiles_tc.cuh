@@ -1,0 +1,369 @@
+// bf16 tensor-core tiles of the LSTM cell (forward and backward) for the persistent worker.
+//
+// Forward (reading R9): Z = [x_t, h_{t-1}] W^T + b as ONE tcgen05 GEMM per 128-row x 256-col
+// tile, where the 256 columns are the four gates (i, f, g, o) of 64 hidden units (W rows
+// permuted once per run by HK_PREP_WP). Every TMEM lane (= batch row) therefore holds all four
+// gates of its units and the sigma / tanh / cell-update / length-mask epilogue is
+// thread-local; it writes h (bf16), c (fp32), out (bf16) and the saved gates (bf16, the
+// StackPush of PAPER.md:1046-1066 landing directly in its arena slot).
+//
+// Backward: an elementwise tile computes dz (pre-activation gate grads, bf16) and dc; then
+//   d[x,h] = dz W     : tcgen05, A = dz (K-major), B = W^T (K-major, HK_PREP_WT)
+//   dW (+)= dz^T [x,h]: tcgen05 with MN-major A (dz) and B (x, h) straight from the saved
+//                        activations -- no transposed copies; fp32 read-modify-write into the
+//                        fused accumulator ("sum of the gradients ... at
+//                        each iteration"); db from per-row-tile partials in a fixed order.
+#pragma once
+#include <cuda_bf16.h>
+
+#include "program.h"
+#include "tc_engine.cuh"
+
+namespace cfdev {
+
+__device__ __forceinline__ float bf2f(__nv_bfloat16 v) { return __bfloat162float(v); }
+__device__ __forceinline__ float ldf(const void* p, int dt, int64_t i) {
+  return dt == D_BF16 ? __bfloat162float(((const __nv_bfloat16*)p)[i]) : ((const float*)p)[i];
+}
+__device__ __forceinline__ void stf(void* p, int dt, int64_t i, float v) {
+  if (dt == D_BF16) ((__nv_bfloat16*)p)[i] = __float2bfloat16(v);
+  else ((float*)p)[i] = v;
+}
+__device__ __forceinline__ float sigmoidf_(float x) { return 1.0f / (1.0f + __expf(-x)); }
+__device__ __forceinline__ float tanhf_(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+struct bf16x8 {
+  __nv_bfloat162 v[4];
+};
+__device__ __forceinline__ void store_bf16x16(__nv_bfloat16* dst, const float* v) {
+  bf16x8 a, b;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    a.v[i] = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+    b.v[i] = __floats2bfloat162_rn(v[8 + 2 * i], v[8 + 2 * i + 1]);
+  }
+  ((uint4*)dst)[0] = *(uint4*)&a;
+  ((uint4*)dst)[1] = *(uint4*)&b;
+}
+__device__ __forceinline__ void load_bf16x16(const __nv_bfloat16* src, float* v) {
+  uint4 ra = ((const uint4*)src)[0], rb = ((const uint4*)src)[1];
+  const __nv_bfloat162* a = (const __nv_bfloat162*)&ra;
+  const __nv_bfloat162* b = (const __nv_bfloat162*)&rb;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float2 x = __bfloat1622float2(a[i]), y = __bfloat1622float2(b[i]);
+    v[2 * i] = x.x;
+    v[2 * i + 1] = x.y;
+    v[8 + 2 * i] = y.x;
+    v[8 + 2 * i + 1] = y.y;
+  }
+}
+
+// ---------------------------------------------------------------- weight preparation
+// Wp[n][k] = bf16(W[src(n)][k]); n = j*256 + g*64 + u' -> src = g*H + j*64 + u'
+__device__ void tile_prep_wp(const Inst& I, int tile) {
+  const int64_t H = I.n, KT = I.k;
+  const float* W = (const float*)I.p[0];
+  __nv_bfloat16* Wp = (__nv_bfloat16*)I.p[13];
+  const int rows_per_tile = 16;
+  for (int rr = 0; rr < rows_per_tile; ++rr) {
+    int64_t n = (int64_t)tile * rows_per_tile + rr;
+    if (n >= 4 * H) break;
+    int64_t j = n / 256, r = n % 256, g = r / 64, u = j * 64 + r % 64;
+    const float* src = W + (g * H + u) * KT;
+    __nv_bfloat16* dst = Wp + n * KT;
+    for (int64_t k = threadIdx.x * 2; k < KT; k += 512)
+      *(__nv_bfloat162*)(dst + k) = __floats2bfloat162_rn(src[k], src[k + 1]);
+  }
+}
+// WT[n][g] = bf16(W[g][n]); W: [G = 4H][KT]; tile = 64 (n) x 128 (g)
+__device__ void tile_prep_wt(const Inst& I, int tile, float* sm) {
+  const int64_t G = 4 * I.n, KT = I.k;
+  const float* W = (const float*)I.p[0];
+  __nv_bfloat16* WT = (__nv_bfloat16*)I.p[13];
+  const int64_t tg = G / 128;
+  const int64_t n0 = (tile / tg) * 64, g0 = (tile % tg) * 128;
+  float* t = sm;   // [128][65]
+  for (int idx = threadIdx.x; idx < 128 * 64; idx += 256) {
+    int gg = idx / 64, nn = idx % 64;
+    t[gg * 65 + nn] = W[(g0 + gg) * KT + n0 + nn];
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < 64 * 128; idx += 256) {
+    int nn = idx / 128, gg = idx % 128;
+    WT[(n0 + nn) * G + g0 + gg] = __float2bfloat16(t[gg * 65 + nn]);
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------- forward
+// p: 0 x-map, 1 h-map, 2 c_prev(f32), 3 Wp-map, 4 bias(f32), 5 lens(i64), 6 h_prev(bf16),
+//    8 h_next(bf16), 9 c_next(f32), 10 out(bf16), 11 gates(bf16, tile-interleaved)
+// s: 0 t, 1 forget bias bits, 2 x slot, 3 h slot
+__device__ void tile_lstm_fwd_tc(const Inst& I, int tile, tc::TcShared& ts, uint32_t& cnt,
+                                 uint32_t& ntile) {
+  const int B = (int)I.m, In = (int)I.k, H = (int)I.n;
+  const int nkx = In / 64, nk = (In + H) / 64;
+  const int tn = H / 64;
+  const int mt = tile / tn, nt = tile % tn;
+  const int m0 = mt * tc::BM;
+  const CUtensorMap* mx = (const CUtensorMap*)I.p[0];
+  const CUtensorMap* mh = (const CUtensorMap*)I.p[1];
+  const CUtensorMap* mw = (const CUtensorMap*)I.p[3];
+  const int sx = (int)I.s[2], sh = (int)I.s[3];
+  auto plan_a = [&](int kb, tc::Box* b) {
+    if (kb < nkx) b[0] = {mx, kb * 64, m0, sx, 0};
+    else b[0] = {mh, (kb - nkx) * 64, m0, sh, 0};
+    return 1;
+  };
+  auto plan_b = [&](int kb, tc::Box* b) {
+    b[0] = {mw, kb * 64, nt * 256, 0, 0};
+    return 1;
+  };
+  tc::tc_tile(ts, nk, 256, 0, 0, cnt, ntile, plan_a, plan_b);
+  // ---- fused epilogue
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int r = m0 + 32 * (warp % 4) + lane;
+  const bool masked = I.sub & 1;
+  const int64_t t = I.s[0];
+  const float fb = __int_as_float((int)I.s[1]);
+  const float* bias = (const float*)I.p[4];
+  const float* c_prev = (const float*)I.p[2];
+  const __nv_bfloat16* h_prev = (const __nv_bfloat16*)I.p[6];
+  const int64_t* lens = (const int64_t*)I.p[5];
+  __nv_bfloat16* h_next = (__nv_bfloat16*)I.p[8];
+  float* c_next = (float*)I.p[9];
+  __nv_bfloat16* out = (__nv_bfloat16*)I.p[10];
+  __nv_bfloat16* gates = (__nv_bfloat16*)I.p[11];
+  const bool live = r < B && (!masked || t < lens[r]);
+  for (int cu = (warp / 4) * 32; cu < (warp / 4) * 32 + 32; cu += 16) {
+    float zi[16], zf[16], zg[16], zo[16];
+    tc::tc_acc16(ts, 0 * 64 + cu, zi);
+    tc::tc_acc16(ts, 1 * 64 + cu, zf);
+    tc::tc_acc16(ts, 2 * 64 + cu, zg);
+    tc::tc_acc16(ts, 3 * 64 + cu, zo);
+    if (r >= B) continue;
+    const int u0 = nt * 64 + cu;
+    const int64_t o = (int64_t)r * H + u0;
+    float cp[16], hn[16], cn[16], hp[16];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) *(float4*)&cp[4 * q] = ((const float4*)(c_prev + o))[q];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      zi[i] = sigmoidf_(zi[i] + bias[u0 + i]);
+      zf[i] = sigmoidf_(zf[i] + bias[H + u0 + i] + fb);
+      zg[i] = tanhf_(zg[i] + bias[2 * H + u0 + i]);
+      zo[i] = sigmoidf_(zo[i] + bias[3 * H + u0 + i]);
+      cn[i] = zf[i] * cp[i] + zi[i] * zg[i];
+      hn[i] = zo[i] * tanhf_(cn[i]);
+    }
+    __nv_bfloat16* gr = gates + (int64_t)r * 4 * H + nt * 256 + cu;
+    store_bf16x16(gr + 0, zi);
+    store_bf16x16(gr + 64, zf);
+    store_bf16x16(gr + 128, zg);
+    store_bf16x16(gr + 192, zo);
+    if (live) {
+      store_bf16x16(h_next + o, hn);
+      store_bf16x16(out + o, hn);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) ((float4*)(c_next + o))[q] = *(float4*)&cn[4 * q];
+    } else {
+      // finished row (reading R10): state copied through, output zero
+      load_bf16x16(h_prev + o, hp);
+      store_bf16x16(h_next + o, hp);
+      float z[16] = {};
+      store_bf16x16(out + o, z);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) ((float4*)(c_next + o))[q] = *(float4*)&cp[4 * q];
+    }
+  }
+  tc::tc_tile_end();
+}
+
+// ---------------------------------------------------------------- backward elementwise
+// p: 2 c_prev(f32), 4 gates(bf16 interleaved), 5 lens, 6 dh_next(f32), 7 dc_next(f32),
+//    8 dout(dt s[4]), 9 dc(f32 out), 10 dz(bf16 out, [B][4H] natural) + partials
+// tile = 128 rows x 64 units; thread: unit t%64, rows t/64 + 4i
+__device__ void tile_lstm_bwd_ew_bf(const Inst& I, int tile, float* sm) {
+  const int B = (int)I.m, H = (int)I.n;
+  const int tu = H / 64;
+  const int rt = tile / tu, ut = tile % tu;
+  const int u = ut * 64 + threadIdx.x % 64, rg = threadIdx.x / 64;
+  const float* c_prev = (const float*)I.p[2];
+  const __nv_bfloat16* gates = (const __nv_bfloat16*)I.p[4];
+  const int64_t* lens = (const int64_t*)I.p[5];
+  const float* dhn = (const float*)I.p[6];
+  const float* dcn = (const float*)I.p[7];
+  const void* dout = (const void*)I.p[8];
+  const int dout_dt = (int)I.s[4];
+  float* dc = (float*)I.p[9];
+  __nv_bfloat16* dz = (__nv_bfloat16*)I.p[10];
+  float* partial = (float*)(I.p[10] + I.s[5]);
+  const bool masked = I.sub & 1;
+  const int64_t t = I.s[0];
+  float sdb[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int i = 0; i < 32; ++i) {
+    const int r = rt * 128 + rg + 4 * i;
+    if (r >= B) break;
+    const int64_t e = (int64_t)r * H + u;
+    const __nv_bfloat16* gr = gates + (int64_t)r * 4 * H + ut * 256 + threadIdx.x % 64;
+    float ig = bf2f(gr[0]), fg = bf2f(gr[64]), gg = bf2f(gr[128]), og = bf2f(gr[192]);
+    float cp = c_prev[e];
+    float cn = fg * cp + ig * gg;
+    float tc_ = tanhf(cn);
+    float dh = dhn[e] + ldf(dout, dout_dt, e);
+    float dcs = dh * og * (1.0f - tc_ * tc_) + dcn[e];
+    float z0 = dcs * gg * ig * (1.0f - ig);
+    float z1 = dcs * cp * fg * (1.0f - fg);
+    float z2 = dcs * ig * (1.0f - gg * gg);
+    float z3 = dh * tc_ * og * (1.0f - og);
+    float dcp = dcs * fg;
+    if (masked && !(t < lens[r])) {
+      z0 = z1 = z2 = z3 = 0.0f;
+      dcp = dcn[e];
+    }
+    __nv_bfloat16* zr = dz + (int64_t)r * 4 * H;
+    __nv_bfloat16 b0 = __float2bfloat16(z0), b1 = __float2bfloat16(z1), b2 = __float2bfloat16(z2),
+                  b3 = __float2bfloat16(z3);
+    zr[u] = b0;
+    zr[H + u] = b1;
+    zr[2 * H + u] = b2;
+    zr[3 * H + u] = b3;
+    // db sums the bf16-rounded dz, exactly what the dW GEMM consumes
+    sdb[0] += bf2f(b0);
+    sdb[1] += bf2f(b1);
+    sdb[2] += bf2f(b2);
+    sdb[3] += bf2f(b3);
+    dc[e] = dcp;
+  }
+  // reduce the 4 row groups: sm[rg][g][64]
+  for (int g = 0; g < 4; ++g) sm[(rg * 4 + g) * 64 + threadIdx.x % 64] = sdb[g];
+  __syncthreads();
+  if (rg == 0) {
+    for (int g = 0; g < 4; ++g) {
+      float s = 0.f;
+      for (int q = 0; q < 4; ++q) s += sm[(q * 4 + g) * 64 + threadIdx.x % 64];
+      partial[(int64_t)rt * 4 * H + g * H + u] = s;
+    }
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------- backward d[x,h]
+// p: 0 dz-map (KA), 1 WT-map (KB), 5 lens, 6 dh_next(f32), 11 dx(f32), 12 dh(f32); s: 0 t, 2 dz slot
+__device__ void tile_lstm_dxh_tc(const Inst& I, int tile, tc::TcShared& ts, uint32_t& cnt,
+                                 uint32_t& ntile) {
+  const int B = (int)I.m, In = (int)I.k, H = (int)I.n, KT = In + H;
+  const int tn = KT / 256;
+  const int mt = tile / tn, nt = tile % tn;
+  const int m0 = mt * tc::BM;
+  const CUtensorMap* mz = (const CUtensorMap*)I.p[0];
+  const CUtensorMap* mwt = (const CUtensorMap*)I.p[1];
+  const int sz = (int)I.s[2];
+  auto plan_a = [&](int kb, tc::Box* b) {
+    b[0] = {mz, kb * 64, m0, sz, 0};
+    return 1;
+  };
+  auto plan_b = [&](int kb, tc::Box* b) {
+    b[0] = {mwt, kb * 64, nt * 256, 0, 0};
+    return 1;
+  };
+  tc::tc_tile(ts, (4 * H) / 64, 256, 0, 0, cnt, ntile, plan_a, plan_b);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int r = m0 + 32 * (warp % 4) + lane;
+  const bool masked = I.sub & 1;
+  const int64_t t = I.s[0];
+  const int64_t* lens = (const int64_t*)I.p[5];
+  const float* dhn = (const float*)I.p[6];
+  float* dx = (float*)I.p[11];
+  float* dh = (float*)I.p[12];
+  const bool dead_row = r < B && masked && !(t < lens[r]);
+  for (int c = (warp / 4) * 128; c < (warp / 4) * 128 + 128; c += 16) {
+    float v[16];
+    tc::tc_acc16(ts, c, v);
+    if (r >= B) continue;
+    const int n = nt * 256 + c;
+    if (n < In) {
+      float* d = dx + (int64_t)r * In + n;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) ((float4*)d)[q] = *(float4*)&v[4 * q];
+    } else {
+      const int64_t o = (int64_t)r * H + (n - In);
+      if (dead_row) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) *(float4*)&v[4 * q] = ((const float4*)(dhn + o))[q];
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) ((float4*)(dh + o))[q] = *(float4*)&v[4 * q];
+    }
+  }
+  tc::tc_tile_end();
+}
+
+// ---------------------------------------------------------------- backward dW / db
+// p: 0 dz-map (MN), 1 x-map (MN), 2 h-map (MN), 3 dW(f32), 4 db(f32), 5 partials(f32)
+// s: 2 dz slot, 3 x slot, 4 h slot, 6 flags (bit0: accumulate dW, bit1: accumulate db)
+__device__ void tile_lstm_dw_tc(const Inst& I, int tile, tc::TcShared& ts, uint32_t& cnt,
+                                uint32_t& ntile) {
+  const int B = (int)I.m, In = (int)I.k, H = (int)I.n, KT = In + H, G = 4 * H;
+  const int tn = KT / 256;
+  const int n_dw = (G / tc::BM) * tn;
+  const int flags = (int)I.s[6];
+  if (tile >= n_dw) {
+    // db tile: 256 gate columns; fixed-order sum over the row-tile partials
+    const int c = (tile - n_dw) * 256 + threadIdx.x;
+    const float* partial = (const float*)I.p[5];
+    float* db = (float*)I.p[4];
+    if (c < G) {
+      float s = 0.f;
+      for (int rt = 0; rt < (B + 127) / 128; ++rt) s += partial[(int64_t)rt * G + c];
+      db[c] = (flags & 2) ? db[c] + s : s;
+    }
+    return;
+  }
+  const int mt = tile / tn, nt = tile % tn;
+  const int m0 = mt * tc::BM;
+  const CUtensorMap* mz = (const CUtensorMap*)I.p[0];
+  const bool xpart = nt * 256 < In;
+  const CUtensorMap* mb = (const CUtensorMap*)(xpart ? I.p[1] : I.p[2]);
+  const int col0 = xpart ? nt * 256 : nt * 256 - In;
+  const int sz = (int)I.s[2], sb = (int)(xpart ? I.s[3] : I.s[4]);
+  auto plan_a = [&](int kb, tc::Box* b) {
+    b[0] = {mz, m0, kb * 64, sz, 0};
+    b[1] = {mz, m0 + 64, kb * 64, sz, 8192};
+    return 2;
+  };
+  auto plan_b = [&](int kb, tc::Box* b) {
+    for (int j = 0; j < 4; ++j) b[j] = {mb, col0 + 64 * j, kb * 64, sb, j * 8192};
+    return 4;
+  };
+  tc::tc_tile(ts, (B + 63) / 64, 256, 1, 1, cnt, ntile, plan_a, plan_b);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int m = m0 + 32 * (warp % 4) + lane;
+  float* dW = (float*)I.p[3] + (int64_t)m * KT + nt * 256;
+  const bool acc = flags & 1;
+  for (int c = (warp / 4) * 128; c < (warp / 4) * 128 + 128; c += 16) {
+    float v[16];
+    tc::tc_acc16(ts, c, v);
+    float4* d = (float4*)(dW + c);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      float4 x = *(float4*)&v[4 * q];
+      if (acc) {
+        float4 y = d[q];
+        x.x += y.x;
+        x.y += y.y;
+        x.z += y.z;
+        x.w += y.w;
+      }
+      d[q] = x;
+    }
+  }
+  tc::tc_tile_end();
+}
+
+}  // namespace cfdev

@@ -45,4 +45,22 @@ inline CUtensorMap make_map_bf16(const void* base, uint64_t cols, uint64_t rows,
   return m;
 }
 
+// same, with an explicit slot stride (slots may carry trailing scratch bytes)
+inline CUtensorMap make_map_bf16_strided(const void* base, uint64_t cols, uint64_t rows,
+                                         uint64_t slots, uint64_t slot_bytes, uint32_t box_c,
+                                         uint32_t box_r) {
+  CUtensorMap m;
+  cuuint64_t dims[3] = {cols, rows, slots};
+  cuuint64_t strides[2] = {cols * 2, slot_bytes};
+  cuuint32_t box[3] = {box_c, box_r, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = get_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims,
+                            strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    throw std::runtime_error("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return m;
+}
+
 }  // namespace cf

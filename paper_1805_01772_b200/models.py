@@ -134,16 +134,20 @@ def dynamic_rnn_lstm(T: int, B: int, I: int, H: int, L: int = 1, parallel_iterat
     return RNNProgram(g, fetch, grads, T, B, I, H, L)
 
 
-def feeds_to_device(feeds, device="cuda", float_dtype=None):
-    """numpy feeds (synth.rnn_inputs) -> contiguous CUDA tensors in the session dtypes."""
+def feeds_to_device(feeds, device="cuda", session=None):
+    """numpy feeds (synth.rnn_inputs) -> contiguous CUDA tensors in the session's feed dtypes
+    (bf16 for the LSTM GEMM operands on the CF_BF16 path, fp32 / int64 / bool otherwise)."""
     import numpy as np
     import torch
-    fd = float_dtype or torch.float32
+    tdt = {cf.F32: torch.float32, cf.BF16: torch.bfloat16}
     out = {}
     for k, v in feeds.items():
         v = np.asarray(v)
         if v.dtype == np.float64:
-            out[k] = torch.from_numpy(v).to(device=device, dtype=fd).contiguous()
+            dt = torch.float32
+            if session is not None:
+                dt = tdt.get(session.feed_dtype(k), torch.float32)
+            out[k] = torch.from_numpy(v).to(device=device, dtype=torch.float32).to(dt).contiguous()
         elif v.dtype == np.bool_:
             out[k] = torch.from_numpy(v).to(device=device).contiguous()
         else:

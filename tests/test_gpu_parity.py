@@ -28,19 +28,20 @@ def normwise(v, r):
     return float(np.abs(np.asarray(v, dtype=np.float64) - r).max() / max(np.abs(r).max(), 1e-30))
 
 
-def run_device(T, B, I, H, L, f, K=0, **kw):
+def run_device(T, B, I, H, L, f, K=0, precision=None, **kw):
     p = dynamic_rnn_lstm(T, B, I, H, L, **kw)
-    s = cf.Session(p.g, p.fetch_tensors(), precision=cf.F32, parallel_iterations=K)
+    s = cf.Session(p.g, p.fetch_tensors(), precision=precision or cf.F32, parallel_iterations=K)
     n_conds = 64
-    outs, dead, tr = s.run(feeds_to_device(f), trace=True, branch_cap=n_conds * (T + 1))
+    outs, dead, tr = s.run(feeds_to_device(f, session=s), trace=True, branch_cap=n_conds * (T + 1))
     torch.cuda.synchronize()
     vals = {n: o.double().cpu().numpy() for n, o in zip(p.fetch_names(), outs)}
     return vals, dead, tr
 
 
-def check_parity(T, B, I, H, L, mode, seed, K=None, tol=1e-5, **kw):
-    f = rnn_inputs(T, B, I, H, L, seed=seed, len_mode=mode, moe=kw.get("moe", False))
-    dev, dead, tr = run_device(T, B, I, H, L, f, K=K or 0, **kw)
+def check_parity(T, B, I, H, L, mode, seed, K=None, tol=1e-5, precision=None, **kw):
+    bf = precision == cf.BF16
+    f = rnn_inputs(T, B, I, H, L, seed=seed, len_mode=mode, moe=kw.get("moe", False), bf16=bf)
+    dev, dead, tr = run_device(T, B, I, H, L, f, K=K or 0, precision=precision, **kw)
     q = oracle_rnn(T, B, I, H, L, **kw)
     ref, otr = run_program(q, f, K=K, return_trace=True)
     assert not any(dead)
@@ -114,3 +115,33 @@ def test_missing_feed_is_an_error():
     with pytest.raises(cf.CfError) as e:
         s.run(f)
     assert e.value.code == "CF_E_MISSING_FEED"
+
+
+# ---------------------------------------------------------------- bf16 tcgen05 path
+BF16_TOL = 2e-2   # north star: max relative error 2e-2 on the bf16 tensor-core path
+
+
+def test_bf16_small_ragged_batch():
+    """2 layers, batch 40 (one partial 128-row tile), variable lengths."""
+    check_parity(5, 40, 256, 256, 2, "uniform", seed=0, tol=BF16_TOL, precision=cf.BF16)
+
+
+def test_bf16_multilayer_capped():
+    """3 layers, batch 130 (two row tiles, ragged), H != I, empty_update branch taken."""
+    check_parity(8, 130, 256, 512, 3, "capped", seed=1, tol=BF16_TOL, precision=cf.BF16)
+
+
+def test_bf16_cfg2_shape():
+    """BASELINE.json configs[1] shape on the tcgen05 path."""
+    check_parity(100, 64, 512, 512, 1, "uniform", seed=2, tol=BF16_TOL, precision=cf.BF16)
+
+
+@pytest.mark.parametrize("K", [1, 32])
+def test_bf16_parallel_iterations_bit_identical(K):
+    T, B, I, H, L = 6, 96, 256, 256, 2
+    f = rnn_inputs(T, B, I, H, L, seed=5, len_mode="uniform", bf16=True)
+    base, _, _ = run_device(T, B, I, H, L, f, K=8, precision=cf.BF16)
+    dev, _, tr = run_device(T, B, I, H, L, f, K=K, precision=cf.BF16)
+    for k in base:
+        assert np.array_equal(base[k], dev[k]), k
+    assert max(tr["max_inflight"]) <= K
