@@ -108,6 +108,8 @@ _sig = {
     "cf_session_describe": (C.c_int32, [_P, C.c_char_p, C.c_size_t]),
     "cf_session_destroy": (None, [_P]),
     # include/cf_debug.h (test hooks)
+    "cf_debug_session_profile": (C.c_int32, [_P, C.c_void_p, C.c_int64, C.POINTER(C.c_int64),
+                                             C.c_void_p]),
     "cf_debug_tc_gemm": (C.c_int32, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                      C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
 }
@@ -385,7 +387,7 @@ class Session:
     def __init__(self, g: Graph, fetches: Sequence[Tensor], precision: int = F32,
                  parallel_iterations: int = 0, device: int = 0, stream=None,
                  max_iterations: int = 0, watchdog_ms: int = 0, num_workers: int = 0,
-                 sched_seed: int = 0):
+                 sched_seed: int = 0, profile: bool = False):
         self.g = g
         self.fetches = list(fetches)
         o = cf_run_opts()
@@ -397,6 +399,7 @@ class Session:
         o.max_iterations = max_iterations
         o.watchdog_ms = watchdog_ms
         o.sched_seed = sched_seed
+        o.reserved[0] = 1 if profile else 0
         arr = (cf_tensor * max(len(fetches), 1))(*[t.c for t in fetches])
         h = _P()
         _check(_lib.cf_session_create(g.h, C.byref(o), len(fetches), arr, C.byref(h)))
@@ -414,6 +417,23 @@ class Session:
                 _lib.cf_session_destroy(self.h)
         except Exception:
             pass
+
+    def profile(self):
+        """Per-instance device timing of the last run (needs profile=True): numpy array of
+        [create, publish, first_start, last_end, busy_ns, kind, ntiles] rows and (t0, t1)."""
+        import numpy as np
+        n = C.c_int64()
+        t = (C.c_uint64 * 66)()
+        _check(_lib.cf_debug_session_profile(self.h, None, 0, C.byref(n), t))
+        buf = np.zeros(6 * n.value, dtype=np.uint64)
+        _check(_lib.cf_debug_session_profile(self.h, buf.ctypes.data, buf.size, C.byref(n), t))
+        r = buf.reshape(-1, 6)
+        out = np.zeros((r.shape[0], 7), dtype=np.float64)
+        out[:, :5] = r[:, :5].astype(np.float64)
+        out[:, 5] = (r[:, 5] >> np.uint64(32)).astype(np.float64)
+        out[:, 6] = (r[:, 5] & np.uint64(0xffffffff)).astype(np.float64)
+        self.driver_ops = [(int(t[2 + k]), int(t[34 + k])) for k in range(32)]
+        return out, (float(t[0]), float(t[1]))
 
     def feed_dtype(self, name: str) -> int:
         d = C.c_int32()

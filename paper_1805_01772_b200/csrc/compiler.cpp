@@ -28,6 +28,8 @@ using namespace cfdev;
 
 namespace {
 
+constexpr int kDwChunk = 8;   // gradient-loop steps accumulated per dW tile (K = 8 * batch)
+
 int32_t dev_dt(int32_t d, int32_t precision) {
   (void)precision;
   switch (d) {
@@ -794,9 +796,11 @@ struct Compiler {
         int K = o.parallel_iterations > 0 ? o.parallel_iterations : g.ctxs[frame_ctx[f]].K;
         pl.kind = PL_RING;
         pl.slots = K + 1;
-        pl.base = add_buf((size_t)pl.elem_bytes * (K + 1), false, "ring " + n.op + std::to_string(n.id));
+        // chunked dW reads the dz of the last kDwChunk steps: keep them alive past the window
+        if (kind == DZ && bf16()) pl.slots = K + kDwChunk + 1;
+        pl.base = add_buf((size_t)pl.elem_bytes * pl.slots, false, "ring " + n.op + std::to_string(n.id));
         if (dd == D_BF16 && shp.size() == 2)
-          register_buf_stride((int)pl.base, K + 1, (int)shp[0], (int)shp[1], pl.elem_bytes);
+          register_buf_stride((int)pl.base, pl.slots, (int)shp[0], (int)shp[1], pl.elem_bytes);
       }
       P.places.push_back(pl);
     }
@@ -896,6 +900,23 @@ struct Compiler {
       F.counter_enter = ctx.loop_vars.at(0).enter;
       F.iter_base = iter_base;
       iter_base += (int)bound[f] + 2;
+      // body program: node records in evaluation order with rebased input ids, so the
+      // driver can stage one frame's control program in shared memory
+      F.bn_off = (int)P.body_nodes.size();
+      F.bi_off = (int)P.body_ivids.size();
+      for (int v : ord) {
+        DNode bn = P.nodes[v];
+        int base = (int)P.body_ivids.size() - F.bi_off;
+        for (int j = 0; j < bn.n_in; ++j) P.body_ivids.push_back(P.in_vids[bn.in_off + j]);
+        for (int j = 0; j < bn.n_ctrl; ++j) P.body_ivids.push_back(P.in_vids[bn.ctrl_off + j]);
+        bn.in_off = base;
+        bn.ctrl_off = base + bn.n_in;
+        P.body_nodes.push_back(bn);
+      }
+      F.bi_count = (int)P.body_ivids.size() - F.bi_off;
+      while (P.body_ivids.size() % 4) P.body_ivids.push_back(0);   // 16 B aligned segments
+      P.max_body = std::max(P.max_body, (int)ord.size());
+      P.max_bi = std::max(P.max_bi, F.bi_count);
       F.acc_off = (int)P.order.size();
       F.n_acc = 0;
       for (size_t a = 0; a < P.accs.size(); ++a)

@@ -43,6 +43,9 @@ struct HostProgram {
   std::vector<cfdev::DAcc> accs;
   std::vector<cfdev::DReg> reg;       // base = buffer id until the runtime patches it
   std::vector<uint8_t> vdt;
+  std::vector<cfdev::DNode> body_nodes;
+  std::vector<int32_t> body_ivids;
+  int max_body = 0, max_bi = 0;
   int32_t precision = CF_F32;
   std::vector<std::string> frame_names;
   int n_vids = 0;

@@ -140,6 +140,8 @@ struct DFrame {
   int32_t counter_enter;        // node id of the hidden counter's Enter
   int32_t iter_base;            // offset into per-iteration counters (size bound + 1)
   int32_t acc_off, n_acc;       // accumulators initialised at frame start (into prog.order)
+  int32_t bn_off;               // body program: DNodes in evaluation order (prog.body_nodes)
+  int32_t bi_off, bi_count;     // their input ids (prog.body_ivids), offsets rebased
   int32_t pad;
 };
 
@@ -179,6 +181,10 @@ struct Prog {
   int32_t n_reg;                // registry entries (static part; feeds appended per run)
   const DReg* reg;
   const void* maps;             // CUtensorMap[3 * n_reg], 64-byte aligned
+  const DNode* body_nodes;      // per-frame body programs (staged into driver smem)
+  const int32_t* body_ivids;
+  int32_t max_body, max_bi;     // largest body (nodes, input ids)
+  int32_t n_places, iter_counters;
   int32_t precision;            // 3 = f32 SIMT, 5 = bf16 tcgen05
   int32_t pad2;
 };
@@ -197,8 +203,10 @@ struct Inst {
 // ---- run-time state shared by the driver CTA and the worker CTAs
 struct RunState {
   // job queue: entries = (inst << 20 | tile) encoded as uint64; tail published by driver
-  unsigned long long q_head;     // claimed by workers (atomicAdd)
+  unsigned long long q_head;     // high-priority ring: claimed by workers (CAS)
   unsigned long long q_tail;     // published by driver (release)
+  unsigned long long lq_head;    // low-priority ring (filler work: dW chunks, preps)
+  unsigned long long lq_tail;
   unsigned long long q_done;     // tiles finished (for ring capacity)
   int32_t quit;                  // 1 = workers exit
   int32_t error;                 // cf_status from the device
@@ -212,6 +220,7 @@ struct RunState {
   int32_t max_depth, exit_fires;
   long long instances, tiles, dead_skipped;
   unsigned long long t_start, t_end;
+  long long op_count[32], op_cycles[32];   // driver self-profile per opcode (+ drain at 31)
 };
 
 struct RunArgs {
@@ -245,6 +254,13 @@ struct RunArgs {
   int64_t watchdog_ns;
   int32_t sched_seed;
   int32_t num_workers;
+  int64_t dyn_smem;          // dynamic shared memory per CTA (driver: token table if it fits)
+  int64_t* inst_aux;         // [inst_cap][48] per-instance side data (chunked dW steps)
+  int32_t* dw_count;         // [n_nodes] pending dW steps per LSTMCellGrad node (chunking)
+  int64_t* dw_pend;          // [n_nodes][8][8] pending step records
+  unsigned long long* lq;    // low-priority job ring (same capacity as queue)
+  unsigned long long* prof;  // optional: per instance {create, publish, first start, last end,
+                             //  busy ns, kind|ntiles} (profiling hook, cf_debug.h)
   int32_t* prep_inst;        // [n_nodes] per-run weight-prep instance of LSTM nodes (-1)
   int32_t* acc_writer;       // [n_accs] latest instance writing each accumulator
   const uint8_t* vdt;        // [n_vids] device dtype of every value

@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <new>
 #include <chrono>
 #include <cstdio>
 #include <cstring>
@@ -54,6 +55,14 @@ __device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned lon
   return *(volatile const unsigned long long*)p;
 }
 __device__ __forceinline__ int ld_volatile_i32(const int* p) { return *(volatile const int*)p; }
+__device__ __forceinline__ int ld_acquire_i32(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -120,6 +129,30 @@ __device__ void tile_ew(const Inst& I, int tile) {
   const int64_t e1 = min(n, b0 + kEwTile);
   const int op = I.sub;
   const int flags = (int)I.s[1];
+  // fast path: fp32 binary add/sub/mul/addn2 without broadcast, 16 B vectors, 4 in flight
+  const bool vec = flags == 0 && (I.dts & 0xF000000FFLL) == ((int64_t)D_F32 << 32 | D_F32 << 4 | D_F32) &&
+                   (op == EW_ADD || op == EW_SUB || op == EW_MUL || (op == EW_ADDN && I.s[0] == 2)) &&
+                   ((I.p[0] | I.p[1] | I.p[13]) & 15) == 0 && (e1 - b0) == kEwTile;
+  if (vec) {
+    const float4* a = (const float4*)I.p[0] + b0 / 4;
+    const float4* b = (const float4*)I.p[1] + b0 / 4;
+    float4* o = (float4*)I.p[13] + b0 / 4;
+    float4 x[4], y[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      x[j] = a[threadIdx.x + j * kThreads];
+      y[j] = b[threadIdx.x + j * kThreads];
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float4 r;
+      if (op == EW_MUL) r = make_float4(x[j].x * y[j].x, x[j].y * y[j].y, x[j].z * y[j].z, x[j].w * y[j].w);
+      else if (op == EW_SUB) r = make_float4(x[j].x - y[j].x, x[j].y - y[j].y, x[j].z - y[j].z, x[j].w - y[j].w);
+      else r = make_float4(x[j].x + y[j].x, x[j].y + y[j].y, x[j].z + y[j].z, x[j].w + y[j].w);
+      o[threadIdx.x + j * kThreads] = r;
+    }
+    return;
+  }
   void* out = (void*)I.p[13];
   const int odt = (int)((I.dts >> 32) & 15);
   auto in = [&](int j, int64_t e) -> float {
@@ -169,8 +202,15 @@ __device__ void tile_copy(const Inst& I, int tile) {
   bool aligned = ((I.p[0] | I.p[13]) & 15) == 0;
   if (aligned) {
     int64_t v0 = b0 / 16, v1 = e1 / 16;
-    for (int64_t e = v0 + threadIdx.x; e < v1; e += kThreads)
-      ((int4*)dst)[e] = ((const int4*)src)[e];
+    int64_t e = v0 + threadIdx.x;
+    for (; e + 3 * kThreads < v1; e += 4 * kThreads) {
+      int4 r[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) r[j] = ((const int4*)src)[e + j * kThreads];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) ((int4*)dst)[e + j * kThreads] = r[j];
+    }
+    for (; e < v1; e += kThreads) ((int4*)dst)[e] = ((const int4*)src)[e];
     for (int64_t e = v1 * 16 + threadIdx.x; e < e1; e += kThreads) dst[e] = src[e];
   } else {
     for (int64_t e = b0 + threadIdx.x; e < e1; e += kThreads) dst[e] = src[e];
@@ -433,8 +473,51 @@ struct Driver {
   bool iter_started = false, fetched = false;
   int32_t oldest = 0;
   unsigned long long last_progress = 0;
+  int64_t pend_mz = 0;
+  int32_t last_dw = -1;
+  unsigned long long lq_tail = 0;
+  unsigned long long q_done_seen = 0;
 
-  __device__ Driver(const RunArgs& a) : A(a), P(a.prog), st(a.st) {}
+  // driver-private state; shared memory when it fits (see cf_driver_kernel), else global
+  const PlaceDesc* places_;
+  const DReg* reg_;
+  int32_t* stack_depth_;
+  int32_t* prep_inst_;
+  int32_t* dw_count_;
+  int32_t* acc_writer_;
+  int32_t* iter_out_;
+  uint8_t* inst_done_;
+  long long n_push = 0, n_pop = 0, n_dead = 0, n_inst = 0, n_tiles = 0;
+  long long op_cnt[32] = {}, op_cyc[32] = {};
+  int32_t max_depth = 0, n_exitf = 0;
+  Tok* toks_;            // token table: driver-CTA shared memory when it fits, else global
+  const int32_t* iv_;    // input-id table of the nodes being evaluated
+  const DNode* bn_;      // current frame's body program (smem copy or global)
+  DNode* sm_nodes_;      // smem staging area (nullptr: no room)
+  int32_t* sm_iv_;
+  volatile int* req_;    // helper-warp copy protocol (block 0 warps 1..7)
+
+  __device__ Driver(const RunArgs& a, Tok* t, DNode* smn, int32_t* smi, volatile int* req)
+      : A(a), P(a.prog), st(a.st), places_(a.prog.places), reg_(a.prog.reg),
+        stack_depth_(a.stack_depth), prep_inst_(a.prep_inst), dw_count_(a.dw_count),
+        acc_writer_(a.acc_writer), iter_out_(a.iter_outstanding), inst_done_(a.inst_done),
+        toks_(t), iv_(a.prog.in_vids), bn_(nullptr), sm_nodes_(smn), sm_iv_(smi), req_(req) {}
+
+  // ask the helper warps to copy [src, src+bytes) -> dst (16 B aligned), wait for them
+  __device__ void helper_copy(void* dst0, const void* src0, int64_t b0, void* dst1, const void* src1,
+                              int64_t b1) {
+    int64_t* q = (int64_t*)(req_ + 4);
+    q[0] = (int64_t)dst0; q[1] = (int64_t)src0; q[2] = b0;
+    q[3] = (int64_t)dst1; q[4] = (int64_t)src1; q[5] = b1;
+    __threadfence_block();
+    int seq = req_[0] + 1;
+    req_[1] = 0;
+    __threadfence_block();
+    req_[0] = seq;
+    while (req_[1] < 7) {
+    }
+    __threadfence_block();
+  }
 
   __device__ void fail(int code, int64_t info) {
     if (st->error == 0) {
@@ -443,12 +526,14 @@ struct Driver {
     }
   }
 
-  __device__ Tok& tok(int vid) { return A.toks[vid]; }
+  __device__ Tok& tok(int vid) { return toks_[vid]; }
   __device__ const DNode& node(int id) { return P.nodes[id]; }
-  __device__ int in_vid(const DNode& d, int j) { return P.in_vids[d.in_off + j]; }
-  __device__ Tok& in_tok(const DNode& d, int j) { return A.toks[in_vid(d, j)]; }
+  __device__ int in_vid(const DNode& d, int j) { return iv_[d.in_off + j]; }
+  __device__ Tok& in_tok(const DNode& d, int j) { return toks_[in_vid(d, j)]; }
+  // frame-level nodes (Enter / Exit) always index the global input-id table
+  __device__ Tok& in_tok_g(const DNode& d, int j) { return toks_[P.in_vids[d.in_off + j]]; }
 
-  __device__ bool writer_done(int32_t w) { return w < 0 || *(volatile uint8_t*)&A.inst_done[w]; }
+  __device__ bool writer_done(int32_t w) { return w < 0 || inst_done_[w]; }
 
   // scalar value of a token; false if its bytes are not produced yet
   __device__ bool scalar(const Tok& t, int64_t* out) {
@@ -476,18 +561,18 @@ struct Driver {
     return true;
   }
 
-  __device__ void set_out(const DNode& d, int port, const Tok& t) { A.toks[d.out_vid + port] = t; }
+  __device__ void set_out(const DNode& d, int port, const Tok& t) { toks_[d.out_vid + port] = t; }
   __device__ void set_dead_all(const DNode& d) {
     for (int p = 0; p < d.n_out; ++p) {
       Tok t{};
       t.dead = 1;
       t.writer = -1;
-      A.toks[d.out_vid + p] = t;
+      toks_[d.out_vid + p] = t;
     }
   }
 
   // ---------------------------------------------------------------- instances
-  __device__ int32_t new_inst(int kind, int sub, int ntiles) {
+  __noinline__ __device__ int32_t new_inst(int kind, int sub, int ntiles) {
     if (ninst >= A.inst_cap) {
       fail(CF_E_STACK_BUDGET, -1);
       return -1;
@@ -504,11 +589,20 @@ struct Driver {
     I.n = I.m = I.k = 0;
     A.inst_pending[id] = 0;
     A.succ_head[id] = -1;
-    A.inst_done[id] = 0;
+    inst_done_[id] = 0;
+    if (A.prof) {
+      unsigned long long* pr = A.prof + 6 * (int64_t)id;
+      pr[0] = globaltimer();
+      pr[1] = 0;
+      pr[2] = ~0ULL;
+      pr[3] = 0;
+      pr[4] = 0;
+      pr[5] = ((unsigned long long)kind << 32) | (unsigned)max(ntiles, 1);
+    }
     return id;
   }
-  __device__ void add_dep(int32_t id, int32_t w) {
-    if (w < 0 || A.inst_done[w]) return;
+  __noinline__ __device__ void add_dep(int32_t id, int32_t w) {
+    if (w < 0 || inst_done_[w]) return;
     // dedupe against the most recent edge of w
     int32_t h = A.succ_head[w];
     if (h >= 0 && A.edge_to[h] == id) return;
@@ -522,47 +616,56 @@ struct Driver {
     A.succ_head[w] = e;
     A.inst_pending[id]++;
   }
-  __device__ void publish(int32_t id) {
+  // two rings: critical-path work (high) and filler work (low: dW chunks) so that the
+  // recurrence never queues behind throughput work
+  __noinline__ __device__ void publish(int32_t id) {
     const Inst& I = A.insts[id];
     unsigned long long n = (unsigned long long)I.ntiles;
+    const bool low = I.kind == HK_LSTM_DW_TC;
     int spins = 0;
-    while (q_tail + n - ld_volatile_u64(&st->q_done) > A.q_cap / 2) {
-      backoff(spins);
-      if (st->error) return;
+    if (q_tail + lq_tail + n - q_done_seen > A.q_cap / 4) {
+      q_done_seen = ld_volatile_u64(&st->q_done);
+      while (q_tail + lq_tail + n - q_done_seen > A.q_cap / 2) {
+        backoff(spins);
+        if (st->error) return;
+        q_done_seen = ld_volatile_u64(&st->q_done);
+      }
     }
+    if (A.prof) A.prof[6 * (int64_t)id + 1] = globaltimer();
+    unsigned long long* ring = low ? A.lq : A.queue;
+    unsigned long long& tail = low ? lq_tail : q_tail;
     for (unsigned long long t = 0; t < n; ++t)
-      A.queue[(q_tail + t) % A.q_cap] = ((unsigned long long)id << 32) | t;
-    q_tail += n;
-    __threadfence();
-    *(volatile unsigned long long*)&st->q_tail = q_tail;
+      ring[(tail + t) % A.q_cap] = ((unsigned long long)id << 32) | t;
+    tail += n;
+    // release: instance record + queue entries visible before the new tail
+    st_release_u64(low ? &st->lq_tail : &st->q_tail, tail);
   }
-  __device__ void submit(int32_t id) {
+  __device__ void submit(int32_t id, bool = false) {
     if (id < 0) return;
     outstanding++;
-    st->instances++;
-    st->tiles += A.insts[id].ntiles;
-    if (cur_frame >= 0) A.iter_outstanding[P.frames[cur_frame].iter_base + iter]++;
+    n_inst++;
+    n_tiles += A.insts[id].ntiles;
+    if (cur_frame >= 0) iter_out_[P.frames[cur_frame].iter_base + iter]++;
     if (A.inst_pending[id] == 0) publish(id);
   }
-  __device__ void complete(int32_t id) {
-    A.inst_done[id] = 1;
+  __noinline__ __device__ void complete(int32_t id) {
+    inst_done_[id] = 1;
     outstanding--;
     const Inst& I = A.insts[id];
-    if (I.frame >= 0) A.iter_outstanding[P.frames[I.frame].iter_base + I.iter]--;
+    if (I.frame >= 0) iter_out_[P.frames[I.frame].iter_base + I.iter]--;
     for (int32_t e = A.succ_head[id]; e >= 0; e = A.edge_next[e]) {
       int32_t s = A.edge_to[e];
       if (--A.inst_pending[s] == 0) publish(s);
     }
   }
-  __device__ bool drain() {
+  __noinline__ __device__ bool drain() {
     bool any = false;
     for (int k = 0; k < 256; ++k) {
       int* p = &A.cq[cq_head % A.cq_cap];
-      int v = ld_volatile_i32(p);
+      int v = ld_acquire_i32(p);   // pairs with the worker's release of its completion
       if (v == 0) break;
       *(volatile int*)p = 0;
       cq_head++;
-      __threadfence();
       complete(v - 1);
       any = true;
     }
@@ -570,8 +673,8 @@ struct Driver {
   }
 
   // ---------------------------------------------------------------- placement
-  __device__ bool place(const DNode& d, int port, int64_t* ptr) {
-    const PlaceDesc& pl = P.places[d.place_off + port];
+  __noinline__ __device__ bool place(const DNode& d, int port, int64_t* ptr) {
+    const PlaceDesc& pl = places_[d.place_off + port];
     int it = cur_frame >= 0 ? iter : 0;
     switch (pl.kind) {
       case PL_ROOT: *ptr = pl.base; return true;
@@ -586,7 +689,7 @@ struct Driver {
       case PL_ACC: *ptr = P.accs[pl.slots].base; return true;
       case PL_TA: {
         int64_t ix;
-        if (!scalar(A.toks[pl.index_vid], &ix)) return false;
+        if (!scalar(toks_[pl.index_vid], &ix)) return false;
         const DTA& ta = P.tas[pl.ta];
         if (ix < 0 || ix >= ta.size) {
           fail(CF_E_SHAPE, ix);
@@ -611,9 +714,9 @@ struct Driver {
   // ---------------------------------------------------------------- operand registry
   // pointer -> (tensor map, slot) for a bf16 [rows][cols] GEMM operand; kind 0 = K-major A
   // (box 64x128), 1 = K-major B (box 64x256), 2 = MN-major (box 64x64)
-  __device__ bool resolve(int64_t p, int rows, int cols, int kind, int64_t* map, int64_t* slot) {
+  __noinline__ __device__ bool resolve(int64_t p, int rows, int cols, int kind, int64_t* map, int64_t* slot) {
     for (int i = 0; i < P.n_reg; ++i) {
-      const DReg& r = P.reg[i];
+      const DReg& r = reg_[i];
       if (r.rows != rows || r.cols != cols) continue;
       if (p < r.base || p >= r.base + (int64_t)r.slots * r.slot_bytes) continue;
       int64_t off = p - r.base;
@@ -634,8 +737,8 @@ struct Driver {
   }
 
   // per-run weight preparation (bf16 permuted W / W^T), created on first use of the node
-  __device__ int32_t prep(const DNode& d, int nid, int kind, int64_t dst) {
-    if (A.prep_inst[nid] >= 0) return A.prep_inst[nid];
+  __noinline__ __device__ int32_t prep(const DNode& d, int nid, int kind, int64_t dst) {
+    if (prep_inst_[nid] >= 0) return prep_inst_[nid];
     const int64_t In = d.imm[1], H = d.imm[2], KT = In + H;
     int ntiles = kind == HK_PREP_WP ? (int)((4 * H + 15) / 16) : (int)((KT / 64) * (4 * H / 128));
     int32_t id = new_inst(kind, 0, ntiles);
@@ -647,11 +750,11 @@ struct Driver {
     I.p[13] = dst;
     add_dep(id, in_tok(d, 3).writer);
     submit(id);
-    A.prep_inst[nid] = id;
+    prep_inst_[nid] = id;
     return id;
   }
 
-  __device__ int eval_lstm_tc(const DNode& d, int nid, const int64_t* outp) {
+  __noinline__ __device__ int eval_lstm_tc(const DNode& d, int nid, const int64_t* outp) {
     const int kind = d.aux[0];
     const bool masked = d.aux[1] & 1;
     int64_t t = 0;
@@ -718,37 +821,68 @@ struct Driver {
       add_dep(x, in_tok(d, o).writer);
     }
     const int acc_w = d.aux[3], acc_b = d.aux[4];
-    int32_t w = new_inst(HK_LSTM_DW_TC, masked,
-                         (int)((4 * H / 128) * (KT / 256) + (4 * H + 255) / 256));
-    if (w < 0) return EV_ERROR;
+    // dW / db: steps are queued and multiplied in chunks of up to 8 (K = 8 B) when both
+    // gradients accumulate in place; otherwise one step per instance
     {
-      Inst& I = A.insts[w];
-      I.m = B; I.k = In; I.n = H;
-      I.p[0] = mzn; I.p[1] = mxn; I.p[2] = mhn;
-      I.p[3] = outp[3]; I.p[4] = outp[4]; I.p[5] = dz_ptr + dz_bytes;
-      I.s[2] = szn; I.s[3] = sxn; I.s[4] = shn;
-      I.s[6] = (acc_w >= 0 ? 1 : 0) | (acc_b >= 0 ? 2 : 0);
-      add_dep(w, e);
-      add_dep(w, in_tok(d, 0).writer);
-      add_dep(w, in_tok(d, 1).writer);
-      if (acc_w >= 0) add_dep(w, A.acc_writer[acc_w]);
-      if (acc_b >= 0) add_dep(w, A.acc_writer[acc_b]);
+      int cnt = dw_count_[nid];
+      int64_t* rec = A.dw_pend + ((int64_t)nid * 8 + cnt) * 10;
+      rec[0] = szn; rec[1] = mxn; rec[2] = sxn; rec[3] = mhn; rec[4] = shn;
+      rec[5] = dz_ptr + dz_bytes;
+      rec[6] = e; rec[7] = in_tok(d, 0).writer; rec[8] = in_tok(d, 1).writer;
+      A.dw_pend[(int64_t)nid * 80 + 9] = mzn;   // dz map (same for all steps of the node)
+      dw_count_[nid] = cnt + 1;
+      pend_mz = mzn;
+      if (!(acc_w >= 0 && acc_b >= 0) || cnt + 1 == 8) {
+        if (flush_dw(d, nid, mzn, outp[3], outp[4]) < 0) return EV_ERROR;
+      }
     }
     set_out(d, 0, ptr_tok(outp[0], x, D_F32));
     set_out(d, 1, ptr_tok(outp[1], x, D_F32));
     set_out(d, 2, ptr_tok(outp[2], e, D_F32));
-    set_out(d, 3, ptr_tok(outp[3], w, D_F32));
-    set_out(d, 4, ptr_tok(outp[4], w, D_F32));
+    set_out(d, 3, ptr_tok(outp[3], acc_w >= 0 ? acc_writer_[acc_w] : last_dw, D_F32));
+    set_out(d, 4, ptr_tok(outp[4], acc_b >= 0 ? acc_writer_[acc_b] : last_dw, D_F32));
     submit(e);
     submit(x);
-    submit(w);
-    if (acc_w >= 0) A.acc_writer[acc_w] = w;
-    if (acc_b >= 0) A.acc_writer[acc_b] = w;
     return EV_OK;
   }
 
+  // create the dW/db instance for the queued steps of LSTMCellGrad node nid
+  __noinline__ __device__ int32_t flush_dw(const DNode& d, int nid, int64_t mzn, int64_t dw_ptr, int64_t db_ptr) {
+    const int cnt = dw_count_[nid];
+    if (cnt == 0) return 0;
+    const int64_t B = d.imm[0], In = d.imm[1], H = d.imm[2], KT = In + H;
+    const int acc_w = d.aux[3], acc_b = d.aux[4];
+    int32_t w = new_inst(HK_LSTM_DW_TC, d.aux[1] & 1,
+                         (int)((4 * H / 128) * (KT / 256) + (4 * H + 255) / 256));
+    if (w < 0) return -1;
+    Inst& I = A.insts[w];
+    I.m = B; I.k = In; I.n = H;
+    I.p[0] = mzn;
+    I.p[3] = acc_w >= 0 ? P.accs[acc_w].base : dw_ptr;
+    I.p[4] = acc_b >= 0 ? P.accs[acc_b].base : db_ptr;
+    int64_t* ax = A.inst_aux + (int64_t)w * 48;
+    I.p[6] = (int64_t)ax;
+    I.s[6] = (acc_w >= 0 ? 1 : 0) | (acc_b >= 0 ? 2 : 0);
+    I.s[7] = cnt;
+    for (int q = 0; q < cnt; ++q) {
+      const int64_t* rec = A.dw_pend + ((int64_t)nid * 8 + q) * 10;
+      for (int k = 0; k < 6; ++k) ax[q * 6 + k] = rec[k];
+      add_dep(w, (int32_t)rec[6]);
+      add_dep(w, (int32_t)rec[7]);
+      add_dep(w, (int32_t)rec[8]);
+    }
+    if (acc_w >= 0) add_dep(w, acc_writer_[acc_w]);
+    if (acc_b >= 0) add_dep(w, acc_writer_[acc_b]);
+    submit(w, true);
+    if (acc_w >= 0) acc_writer_[acc_w] = w;
+    if (acc_b >= 0) acc_writer_[acc_b] = w;
+    dw_count_[nid] = 0;
+    last_dw = w;
+    return w;
+  }
+
   // ---------------------------------------------------------------- heavy ops
-  __device__ int eval_heavy(const DNode& d, int nid) {
+  __noinline__ __device__ int eval_heavy(const DNode& d, int nid) {
     const int kind = d.aux[0];
     int64_t outp[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     const bool tcm = P.precision == D_BF16;
@@ -762,7 +896,7 @@ struct Driver {
     auto dep_all = [&](int32_t id) {
       for (int j = 0; j < d.n_in; ++j) add_dep(id, in_tok(d, j).writer);
     };
-    const int odt = P.places[d.place_off].dt;
+    const int odt = places_[d.place_off].dt;
     if (kind == HK_LSTM_FWD || kind == HK_LSTM_BWD_EW) {
       const bool masked = d.aux[1] & 1;
       int64_t t = 0;
@@ -826,8 +960,8 @@ struct Driver {
           I.s[6] = (acc_w >= 0 ? 1 : 0) | (acc_b >= 0 ? 2 : 0);
           dep_all(m);
           add_dep(m, e);
-          if (acc_w >= 0) add_dep(m, A.acc_writer[acc_w]);
-          if (acc_b >= 0) add_dep(m, A.acc_writer[acc_b]);
+          if (acc_w >= 0) add_dep(m, acc_writer_[acc_w]);
+          if (acc_b >= 0) add_dep(m, acc_writer_[acc_b]);
         }
         set_out(d, 0, ptr_tok(outp[0], m, D_F32));
         set_out(d, 1, ptr_tok(outp[1], m, D_F32));
@@ -836,8 +970,8 @@ struct Driver {
         set_out(d, 4, ptr_tok(outp[4], m, D_F32));
         submit(e);
         submit(m);
-        if (acc_w >= 0) A.acc_writer[acc_w] = m;
-        if (acc_b >= 0) A.acc_writer[acc_b] = m;
+        if (acc_w >= 0) acc_writer_[acc_w] = m;
+        if (acc_b >= 0) acc_writer_[acc_b] = m;
       }
       return EV_OK;
     }
@@ -917,7 +1051,7 @@ struct Driver {
     return EV_OK;
   }
 
-  __device__ int32_t copy_inst(int64_t dst, int64_t src, int64_t bytes, int32_t dep) {
+  __noinline__ __device__ int32_t copy_inst(int64_t dst, int64_t src, int64_t bytes, int32_t dep) {
     int32_t id = new_inst(HK_COPY, 0, (int)((bytes + 65535) / 65536));
     if (id < 0) return -1;
     Inst& I = A.insts[id];
@@ -930,13 +1064,78 @@ struct Driver {
   }
 
   // ---------------------------------------------------------------- node evaluation
-  __device__ int eval(int nid) {
-    const DNode& d = node(nid);
+  // Hot path: the routing primitives evaluated hundreds of times per iteration stay in a
+  // small function (I-cache); everything else goes through eval_cold.
+  __noinline__ __device__ int eval(const DNode& d, int nid) {
+    const int op = d.op;
+    if (op == OP_SWITCH || op == OP_MERGE || op == OP_MERGE_LOOP || op == OP_NEXTITER ||
+        op == OP_PASS || (op == OP_CONST && d.aux[0] == 1)) {
+      bool dead = false;
+      if (op != OP_MERGE && op != OP_MERGE_LOOP) {
+        for (int j = 0; j < d.n_in; ++j) dead |= toks_[iv_[d.in_off + j]].dead != 0;
+        for (int j = 0; j < d.n_ctrl; ++j) dead |= toks_[iv_[d.ctrl_off + j]].dead != 0;
+      }
+      bool ctrl_dead = dead;
+      if (op == OP_SWITCH) {
+        Tok dv = toks_[iv_[d.in_off]];
+        const Tok& pt = toks_[iv_[d.in_off + 1]];
+        Tok o0 = dv, o1 = dv;
+        if (dead) {
+          o0.dead = o1.dead = 1;
+        } else {
+          int64_t pv;
+          if (pt.kind == TK_IMM) pv = pt.v;
+          else if (!scalar(pt, &pv)) return EV_BLOCKED;
+          o0.dead = pv != 0;   // false port: dead iff p
+          o1.dead = pv == 0;   // true port: dead iff !p
+          if (d.aux[0] >= 0) {
+            int it = cur_frame >= 0 ? iter : 0;
+            if (it < P.branch_bound) A.branch_bits[d.aux[0] * P.branch_bound + it] = pv ? 2 : 1;
+          }
+        }
+        toks_[d.out_vid] = o0;
+        toks_[d.out_vid + 1] = o1;
+      } else if (op == OP_MERGE) {
+        const Tok& a = toks_[iv_[d.in_off]];
+        const Tok& b = toks_[iv_[d.in_off + 1]];
+        Tok o = !a.dead ? a : b;   // "if is_dead(d1) then d2 else d1"
+        toks_[d.out_vid] = o;
+        ctrl_dead = o.dead;
+      } else if (op == OP_MERGE_LOOP) {
+        Tok o = toks_[iv_[d.in_off + (iter == 0 ? 0 : 1)]];
+        toks_[d.out_vid] = o;
+        ctrl_dead = o.dead;
+      } else if (op == OP_NEXTITER) {
+        toks_[d.out_vid] = toks_[iv_[d.in_off]];
+      } else if (op == OP_PASS) {
+        Tok t = toks_[iv_[d.in_off]];
+        t.dead = dead;
+        for (int p = 0; p < d.n_out; ++p) toks_[d.out_vid + p] = t;
+      } else {
+        Tok t{};
+        t.writer = -1;
+        t.dead = dead;
+        t.kind = TK_IMM;
+        t.v = d.imm[0];
+        t.dt = (uint8_t)d.aux[1];
+        toks_[d.out_vid] = t;
+      }
+      Tok c{};
+      c.dead = ctrl_dead;
+      c.writer = -1;
+      c.kind = TK_FLOW;
+      toks_[d.ctrl_vid] = c;
+      return EV_OK;
+    }
+    return eval_cold(d, nid);
+  }
+
+  __noinline__ __device__ int eval_cold(const DNode& d, int nid) {
     const int op = d.op;
     bool dead = false;
     if (op != OP_MERGE && op != OP_MERGE_LOOP) {
       for (int j = 0; j < d.n_in; ++j) dead |= in_tok(d, j).dead != 0;
-      for (int j = 0; j < d.n_ctrl; ++j) dead |= A.toks[P.in_vids[d.ctrl_off + j]].dead != 0;
+      for (int j = 0; j < d.n_ctrl; ++j) dead |= toks_[iv_[d.ctrl_off + j]].dead != 0;
     }
     int res = EV_OK;
     bool ctrl_dead = dead;
@@ -1229,15 +1428,15 @@ struct Driver {
         if (!dead) {
           int s = (int)in_tok(d, 0).v;
           const DStack& S = P.stacks[s];
-          int dp = A.stack_depth[s];
+          int dp = stack_depth_[s];
           if (dp >= S.capacity) {
             fail(CF_E_STACK_BUDGET, dp);
             return EV_ERROR;
           }
           A.stack_pool[S.entry_off + dp] = in_tok(d, 1);
-          A.stack_depth[s] = dp + 1;
-          st->pushes++;
-          if (dp + 1 > st->max_depth) st->max_depth = dp + 1;
+          stack_depth_[s] = dp + 1;
+          n_push++;
+          if (dp + 1 > max_depth) max_depth = dp + 1;
         }
         break;
       }
@@ -1248,22 +1447,22 @@ struct Driver {
         }
         int s = (int)in_tok(d, 0).v;
         const DStack& S = P.stacks[s];
-        int dp = A.stack_depth[s];
+        int dp = stack_depth_[s];
         if (dp <= 0) {
           fail(CF_E_POP_EMPTY, s);
           return EV_ERROR;
         }
         Tok t = A.stack_pool[S.entry_off + dp - 1];
-        A.stack_depth[s] = dp - 1;
+        stack_depth_[s] = dp - 1;
         t.dead = 0;
         set_out(d, 0, t);
-        st->pops++;
+        n_pop++;
         break;
       }
       case OP_ACC: {
         // fused accumulator: the producers already added in place
         const DAcc& a = P.accs[d.aux[0]];
-        Tok t = ptr_tok(a.base, A.acc_writer[d.aux[0]], D_F32);
+        Tok t = ptr_tok(a.base, acc_writer_[d.aux[0]], D_F32);
         t.dead = dead;
         set_out(d, 0, t);
         break;
@@ -1271,7 +1470,7 @@ struct Driver {
       case OP_HEAVY: {
         if (dead) {
           set_dead_all(d);
-          st->dead_skipped++;
+          n_dead++;
           break;
         }
         res = eval_heavy(d, nid);
@@ -1286,20 +1485,30 @@ struct Driver {
     c.dead = ctrl_dead;
     c.writer = -1;
     c.kind = TK_FLOW;
-    A.toks[d.ctrl_vid] = c;
+    toks_[d.ctrl_vid] = c;
     return EV_OK;
   }
 
   // ---------------------------------------------------------------- frames
-  __device__ void start_frame(int f) {
+  __noinline__ __device__ void start_frame(int f) {
     const DFrame& F = P.frames[f];
     for (int k = 0; k < F.n_enter; ++k) {
       const DNode& e = node(P.order[F.enter_off + k]);
-      set_out(e, 0, in_tok(e, 0));
+      set_out(e, 0, in_tok_g(e, 0));
       Tok c{};
-      c.dead = in_tok(e, 0).dead;
+      c.dead = in_tok_g(e, 0).dead;
       c.writer = -1;
-      A.toks[e.ctrl_vid] = c;
+      toks_[e.ctrl_vid] = c;
+    }
+    // the frame's control program: staged in shared memory when there is room
+    if (sm_nodes_) {
+      helper_copy(sm_nodes_, P.body_nodes + F.bn_off, (int64_t)F.n_body * sizeof(DNode), sm_iv_,
+                  P.body_ivids + F.bi_off, (int64_t)F.bi_count * 4);
+      bn_ = sm_nodes_;
+      iv_ = sm_iv_;
+    } else {
+      bn_ = P.body_nodes + F.bn_off;
+      iv_ = P.body_ivids + F.bi_off;
     }
     cur_frame = f;
     iter = 0;
@@ -1321,11 +1530,92 @@ struct Driver {
         A.insts[id].dts = (int64_t)D_F32 << 32;
         submit(id);
       } else {
-        const Tok& it0 = A.toks[ac.init_vid];
+        const Tok& it0 = toks_[ac.init_vid];
         id = copy_inst(ac.base, it0.v, ac.bytes, it0.writer);
       }
-      A.acc_writer[a] = id;
+      acc_writer_[a] = id;
     }
+  }
+
+  // The per-iteration control loop: kept small and out of line so that its instructions stay
+  // resident in the SM's instruction cache (the routing primitives dominate the node count).
+  // The per-iteration control loop. Routing primitives are ~90% of the evaluations, so they
+  // get a tiny straight-line path (16-byte token moves, no calls) at the head of the loop;
+  // everything else goes through the out-of-line eval().
+  __noinline__ __device__ bool run_body(const DFrame& F) {
+    bool progress = false;
+    const bool prof = A.prof != nullptr;
+    int4* tk = (int4*)toks_;
+    const int32_t* iv = iv_;
+    const int n_body = F.n_body;
+    const int it = iter;
+    const int bb = P.branch_bound;
+    uint8_t* bbits = A.branch_bits;
+    int pc = body_pc;
+    while (pc < n_body) {
+      if ((pc & 15) == 0) drain();
+      const DNode* d = bn_ + pc;
+      const int op = d->op;
+      // token word w: dead (bits 0-7) | kind (8-15) | dt (16-23)
+      if (op == OP_SWITCH && d->n_ctrl == 0) {
+        const int4 dv = tk[iv[d->in_off]];
+        const int4 pt = tk[iv[d->in_off + 1]];
+        if (((pt.w >> 8) & 0xff) == TK_IMM || ((dv.w | pt.w) & 0xff)) {
+          int4 o0 = dv, o1 = dv;
+          const int dead = (dv.w | pt.w) & 0xff;
+          if (dead) {
+            o0.w |= 1;
+            o1.w |= 1;
+          } else {
+            const bool p = (pt.x | pt.y) != 0;
+            o0.w = (o0.w & ~0xff) | (p ? 1 : 0);   // false port dead iff p
+            o1.w = (o1.w & ~0xff) | (p ? 0 : 1);
+            if (d->aux[0] >= 0 && it < bb) bbits[d->aux[0] * bb + it] = p ? 2 : 1;
+          }
+          tk[d->out_vid] = o0;
+          tk[d->out_vid + 1] = o1;
+          tk[d->ctrl_vid] = make_int4(0, 0, -1, (TK_FLOW << 8) | dead);
+          ++pc;
+          progress = true;
+          continue;
+        }
+      } else if (op == OP_MERGE) {
+        const int4 a = tk[iv[d->in_off]];
+        const int4 b = tk[iv[d->in_off + 1]];
+        const int4 o = (a.w & 0xff) ? b : a;   // "if is_dead(d1) then d2 else d1"
+        tk[d->out_vid] = o;
+        tk[d->ctrl_vid] = make_int4(0, 0, -1, (TK_FLOW << 8) | (o.w & 0xff));
+        ++pc;
+        progress = true;
+        continue;
+      } else if (op == OP_MERGE_LOOP) {
+        const int4 o = tk[iv[d->in_off + (it == 0 ? 0 : 1)]];
+        tk[d->out_vid] = o;
+        tk[d->ctrl_vid] = make_int4(0, 0, -1, (TK_FLOW << 8) | (o.w & 0xff));
+        ++pc;
+        progress = true;
+        continue;
+      } else if (op == OP_NEXTITER && d->n_ctrl == 0) {
+        const int4 o = tk[iv[d->in_off]];
+        tk[d->out_vid] = o;
+        tk[d->ctrl_vid] = make_int4(0, 0, -1, (TK_FLOW << 8) | (o.w & 0xff));
+        ++pc;
+        progress = true;
+        continue;
+      }
+      body_pc = pc;
+      long long c0 = prof ? clock64() : 0;
+      int r = eval(*d, P.order[F.body_off + pc]);
+      if (prof) {
+        op_cyc[op & 31] += clock64() - c0;
+        op_cnt[op & 31]++;
+      }
+      if (r != EV_OK) return progress;
+      ++pc;
+      progress = true;
+    }
+    body_pc = pc;
+    return progress;
   }
 
   // one step of control evaluation; returns true on progress
@@ -1341,7 +1631,7 @@ struct Driver {
       }
       int s = P.root_steps[root_pc];
       if (s >= 0) {
-        int r = eval(s);
+        int r = eval(node(s), s);
         if (r != EV_OK) return false;
         root_pc++;
         return true;
@@ -1351,7 +1641,7 @@ struct Driver {
     }
     const DFrame& F = P.frames[cur_frame];
     if (!iter_started) {
-      while (oldest < iter && A.iter_outstanding[F.iter_base + oldest] == 0) oldest++;
+      while (oldest < iter && iter_out_[F.iter_base + oldest] == 0) oldest++;
       if (iter - oldest >= F.K) return false;   // parallel_iterations window
       if (iter > F.bound) {
         fail(CF_E_STACK_BUDGET, iter);
@@ -1362,26 +1652,34 @@ struct Driver {
       iter_started = true;
       body_pc = 0;
     }
-    bool progress = false;
-    while (body_pc < F.n_body) {
-      int r = eval(P.order[F.body_off + body_pc]);
-      if (r != EV_OK) return progress;
-      body_pc++;
-      progress = true;
-    }
+    bool progress = run_body(F);
+    if (body_pc < F.n_body) return progress;
     // the counter's Switch decides: true port dead => the predicate was false (or the frame
     // is dead) => Exit fires once with this iteration's values (reading R2)
     const DNode& cs = node(F.counter_switch);
-    if (A.toks[cs.out_vid + 1].dead) {
+    if (toks_[cs.out_vid + 1].dead) {
+      // flush partially filled dW chunks before the accumulators leave the frame
+      for (int k = 0; k < F.n_body; ++k) {
+        const int nid = P.order[F.body_off + k];
+        const DNode& dn = node(nid);
+        if (dn.op == OP_HEAVY && dn.aux[0] == HK_LSTM_BWD_EW && dw_count_[nid] > 0) {
+          if (flush_dw(dn, nid, A.dw_pend[(int64_t)nid * 80 + 9], 0, 0) < 0) return false;
+        }
+      }
+      iv_ = P.in_vids;
+      bn_ = nullptr;
       for (int k = 0; k < F.n_exit; ++k) {
         const DNode& x = node(P.order[F.exit_off + k]);
-        set_out(x, 0, in_tok(x, 0));
+        Tok xt = in_tok_g(x, 0);
+        for (int a = 0; a < P.n_accs; ++a)
+          if (xt.kind == TK_PTR && xt.v == P.accs[a].base) xt.writer = acc_writer_[a];
+        set_out(x, 0, xt);
         Tok c{};
-        c.dead = in_tok(x, 0).dead;
+        c.dead = xt.dead;
         c.writer = -1;
-        A.toks[x.ctrl_vid] = c;
+        toks_[x.ctrl_vid] = c;
       }
-      st->exit_fires += F.n_exit;
+      n_exitf += F.n_exit;
       if (cur_frame < 16) st->trip[cur_frame] = iter;
       cur_frame = -1;
       root_pc++;
@@ -1392,9 +1690,9 @@ struct Driver {
     return true;
   }
 
-  __device__ void issue_fetches() {
+  __noinline__ __device__ void issue_fetches() {
     for (int i = 0; i < P.n_fetch; ++i) {
-      const Tok& t = A.toks[P.fetch_vids[i]];
+      const Tok& t = toks_[P.fetch_vids[i]];
       if (t.dead) {
         A.fetch_dead[i] = 1;
         continue;
@@ -1411,7 +1709,25 @@ struct Driver {
     }
   }
 
+  __device__ void calibrate() {
+    // driver self-calibration (profiling): cycles per primitive, into op_cyc[24..27]
+    long long c0 = clock64();
+    for (int i = 0; i < 1000; ++i) asm volatile("");
+    long long c1 = clock64();
+    volatile Tok* tv = toks_;
+    for (int i = 0; i < 1000; ++i) { Tok t = ((Tok*)tv)[i % 64]; ((Tok*)tv)[64 + (i % 64)] = t; }
+    long long c2 = clock64();
+    for (int i = 0; i < 1000; ++i) A.branch_bits[i % 64] = 0;
+    long long c3 = clock64();
+    int acc = 0;
+    for (int i = 0; i < 1000; ++i) acc += ((volatile int*)iv_)[i % 64];
+    long long c4 = clock64();
+    op_cyc[26] = c1 - c0; op_cyc[27] = c2 - c1; op_cyc[28] = c3 - c2; op_cyc[29] = c4 - c3 + (acc == 12345);
+    op_cnt[26] = op_cnt[27] = op_cnt[28] = op_cnt[29] = 1000;
+  }
+
   __device__ void run() {
+    if (A.prof) calibrate();
     st->t_start = globaltimer();
     last_progress = st->t_start;
     while (true) {
@@ -1428,6 +1744,17 @@ struct Driver {
         break;
       }
     }
+    for (int k = 0; k < 32; ++k) {
+      st->op_count[k] = op_cnt[k];
+      st->op_cycles[k] = op_cyc[k];
+    }
+    st->pushes = n_push;
+    st->pops = n_pop;
+    st->dead_skipped = n_dead;
+    st->instances = n_inst;
+    st->tiles = n_tiles;
+    st->max_depth = max_depth;
+    st->exit_fires = n_exitf;
     st->t_end = globaltimer();
     __threadfence();
     *(volatile int*)&st->quit = 1;
@@ -1449,14 +1776,27 @@ __device__ void worker_loop(const RunArgs& A) {
   }
   while (true) {
     if (threadIdx.x == 0) {
-      unsigned long long idx = atomicAdd(&st->q_head, 1ULL);
+      // claim from the high-priority ring first, then the low one (CAS on the heads)
       int spins = 0;
       unsigned long long e = ~0ULL;
       while (true) {
-        if (idx < ld_volatile_u64(&st->q_tail)) {
-          __threadfence();
-          e = ((volatile unsigned long long*)A.queue)[idx % A.q_cap];
-          break;
+        unsigned long long h = ld_volatile_u64(&st->q_head);
+        if (h < ld_volatile_u64(&st->q_tail)) {
+          if (atomicCAS(&st->q_head, h, h + 1) == h) {
+            __threadfence();
+            e = ((volatile unsigned long long*)A.queue)[h % A.q_cap];
+            break;
+          }
+          continue;
+        }
+        unsigned long long l = ld_volatile_u64(&st->lq_head);
+        if (l < ld_volatile_u64(&st->lq_tail)) {
+          if (atomicCAS(&st->lq_head, l, l + 1) == l) {
+            __threadfence();
+            e = ((volatile unsigned long long*)A.lq)[l % A.q_cap];
+            break;
+          }
+          continue;
         }
         if (ld_volatile_i32(&st->quit)) break;
         backoff(spins);
@@ -1470,6 +1810,7 @@ __device__ void worker_loop(const RunArgs& A) {
     if (e == ~0ULL) break;
     const int32_t id = (int32_t)(e >> 32);
     const int tile = (int)(e & 0xffffffffULL);
+    unsigned long long t_tile0 = A.prof ? globaltimer() : 0;
     __shared__ Inst s_inst;
     if (threadIdx.x < (int)(sizeof(Inst) / 8))
       ((int64_t*)&s_inst)[threadIdx.x] = ((volatile const int64_t*)(A.insts + id))[threadIdx.x];
@@ -1499,6 +1840,13 @@ __device__ void worker_loop(const RunArgs& A) {
     if (tcmode) tc::fence_proxy_async_global();
     __syncthreads();
     if (threadIdx.x == 0) {
+      if (A.prof) {
+        unsigned long long t1 = globaltimer();
+        unsigned long long* pr = A.prof + 6 * (int64_t)id;
+        atomicMin(&pr[2], t_tile0);
+        atomicMax(&pr[3], t1);
+        atomicAdd(&pr[4], t1 - t_tile0);
+      }
       __threadfence();
       int old = atomicAdd(&A.inst_tiles_done[id], 1);
       s_last = (old == I.ntiles - 1);
@@ -1528,11 +1876,101 @@ __device__ void worker_loop(const RunArgs& A) {
   if (tcmode) tc::tc_teardown(ts);
 }
 
-__global__ void __launch_bounds__(kThreads, 1) cf_driver_kernel(RunArgs A) {
+__global__ void __launch_bounds__(kThreads, 1) cf_driver_kernel(RunArgs A_param) {
+  // kernel parameters are addressed through references below; keep them in shared memory
+  // (a reference to the parameter block would force a local-memory copy)
+  __shared__ __align__(16) RunArgs A;
+  if (threadIdx.x == 0) A = A_param;
+  __syncthreads();
   if (blockIdx.x == 0) {
+    extern __shared__ __align__(1024) uint8_t drv_smem[];
+    __shared__ int req[16];   // [0] seq (-1: quit), [1] helpers done, [4..15] copy args
+    Tok* toks = A.toks;
+    DNode* smn = nullptr;
+    int32_t* smi = nullptr;
+    const int64_t tok_b = (int64_t)A.prog.n_vids * (int64_t)sizeof(Tok);
+    const int64_t node_b = (int64_t)A.prog.max_body * (int64_t)sizeof(DNode);
+    const int64_t iv_b = ((int64_t)A.prog.max_bi * 4 + 15) / 16 * 16;
+    if (tok_b <= A.dyn_smem) {
+      // stage the token table (placeholders preset by the host) in shared memory
+      Tok* sm = (Tok*)drv_smem;
+      for (int i = threadIdx.x; i < A.prog.n_vids; i += blockDim.x) sm[i] = A.toks[i];
+      toks = sm;
+      const int64_t tok_pad = (tok_b + 15) / 16 * 16;
+      if (tok_pad + node_b + iv_b <= A.dyn_smem) {
+        smn = (DNode*)(drv_smem + tok_pad);
+        smi = (int32_t*)(drv_smem + tok_pad + node_b);
+      }
+    }
+    // further driver-private arrays into the remaining shared memory
+    int64_t used = 0;
+    if (toks != A.toks) used = (tok_b + 15) / 16 * 16 + (smn ? node_b + iv_b : 0);
+    auto carve = [&](int64_t bytes) -> uint8_t* {
+      bytes = (bytes + 15) / 16 * 16;
+      if (toks == A.toks || used + bytes > A.dyn_smem) return nullptr;
+      uint8_t* p = drv_smem + used;
+      used += bytes;
+      return p;
+    };
+    const Prog& P = A.prog;
+    PlaceDesc* s_pl = (PlaceDesc*)carve((int64_t)P.n_places * sizeof(PlaceDesc));
+    DReg* s_reg = (DReg*)carve((int64_t)P.n_reg * sizeof(DReg));
+    int32_t* s_sd = (int32_t*)carve(4 * (int64_t)P.n_stacks);
+    int32_t* s_prep = (int32_t*)carve(4 * (int64_t)P.n_nodes);
+    int32_t* s_dwc = (int32_t*)carve(4 * (int64_t)P.n_nodes);
+    int32_t* s_accw = (int32_t*)carve(4 * (int64_t)P.n_accs);
+    int32_t* s_iter = (int32_t*)carve(4 * (int64_t)P.iter_counters);
+    uint8_t* s_done = (uint8_t*)carve(A.inst_cap);
+    for (int i = threadIdx.x; s_pl && i < P.n_places; i += blockDim.x) s_pl[i] = P.places[i];
+    for (int i = threadIdx.x; s_reg && i < P.n_reg; i += blockDim.x) s_reg[i] = P.reg[i];
+    for (int i = threadIdx.x; s_sd && i < P.n_stacks; i += blockDim.x) s_sd[i] = 0;
+    for (int i = threadIdx.x; s_prep && i < P.n_nodes; i += blockDim.x) s_prep[i] = -1;
+    for (int i = threadIdx.x; s_dwc && i < P.n_nodes; i += blockDim.x) s_dwc[i] = 0;
+    for (int i = threadIdx.x; s_accw && i < P.n_accs; i += blockDim.x) s_accw[i] = -1;
+    for (int i = threadIdx.x; s_iter && i < P.iter_counters; i += blockDim.x) s_iter[i] = 0;
     if (threadIdx.x == 0) {
-      Driver d(A);
+      req[0] = 0;
+      req[1] = 0;
+    }
+    __syncthreads();
+    // the driver object itself lives in shared memory: its members are touched on every node
+    // evaluation, and local memory would go to L2 (this SM has almost no L1 left)
+    __shared__ __align__(16) unsigned char drv_obj[sizeof(Driver)];
+    if (threadIdx.x == 0) {
+      Driver& d = *new (drv_obj) Driver(A, toks, smn, smi, req);
+      if (s_pl) d.places_ = s_pl;
+      if (s_reg) d.reg_ = s_reg;
+      if (s_sd) d.stack_depth_ = s_sd;
+      if (s_prep) d.prep_inst_ = s_prep;
+      if (s_dwc) d.dw_count_ = s_dwc;
+      if (s_accw) d.acc_writer_ = s_accw;
+      if (s_iter) d.iter_out_ = s_iter;
+      if (s_done) d.inst_done_ = s_done;
       d.run();
+      *(volatile int*)&req[0] = -1;
+    } else if (threadIdx.x >= 32) {
+      // helper warps: cooperative smem staging on request from the driver thread
+      int seen = 0;
+      const int h = threadIdx.x - 32, nh = blockDim.x - 32;
+      while (true) {
+        int q = *(volatile int*)&req[0];
+        if (q < 0) break;
+        if (q == seen) {
+          __nanosleep(500);
+          continue;
+        }
+        seen = q;
+        const int64_t* a = (const int64_t*)(req + 4);
+        for (int part = 0; part < 2; ++part) {
+          int4* dst = (int4*)a[3 * part];
+          const int4* src = (const int4*)a[3 * part + 1];
+          int64_t n = (a[3 * part + 2] + 15) / 16;
+          for (int64_t i = h; i < n; i += nh) dst[i] = src[i];
+        }
+        __threadfence_block();
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0) atomicAdd(&req[1], 1);
+      }
     }
     return;
   }
@@ -1634,6 +2072,8 @@ void build_session(cf_session* s, const cf::Graph& g, const cf_run_opts* o,
     if (pl.kind != PL_TA && pl.kind != PL_ACC) pl.base = addr(pl.base);
   for (auto& n : P.nodes)
     if (n.op == OP_CONST && n.aux[0] == 0) n.imm[0] = addr(n.imm[0]);
+  for (auto& n : P.body_nodes)
+    if (n.op == OP_CONST && n.aux[0] == 0) n.imm[0] = addr(n.imm[0]);
   for (auto& t : P.tas) t.base = addr(t.base);
   for (auto& a : P.accs) a.base = addr(a.base);
   for (auto& r : P.reg) r.base = addr(r.base);
@@ -1660,6 +2100,12 @@ void build_session(cf_session* s, const cf::Graph& g, const cf_run_opts* o,
   pg.tas = upload(s, P.tas);
   pg.stacks = upload(s, P.stacks);
   pg.fetch_vids = upload(s, P.fetch_vids);
+  pg.body_nodes = upload(s, P.body_nodes);
+  pg.body_ivids = upload(s, P.body_ivids);
+  pg.max_body = P.max_body;
+  pg.max_bi = P.max_bi;
+  pg.n_places = (int)P.places.size();
+  pg.iter_counters = P.iter_counters;
   pg.accs = upload(s, P.accs);
   pg.n_accs = (int)P.accs.size();
   pg.precision = s->precision == CF_BF16 ? D_BF16 : D_F32;
@@ -1687,6 +2133,10 @@ void build_session(cf_session* s, const cf::Graph& g, const cf_run_opts* o,
     pg.n_reg = n_static;
   }
   A.vdt = upload(s, P.vdt);
+  A.inst_aux = (int64_t*)dalloc(s, 8 * 48 * (size_t)P.inst_bound);
+  A.dw_count = (int32_t*)dalloc(s, 4 * P.nodes.size());
+  s->zero_each_run.push_back({A.dw_count, 4 * P.nodes.size()});
+  A.dw_pend = (int64_t*)dalloc(s, 8 * 80 * P.nodes.size());
   A.prep_inst = (int32_t*)dalloc(s, 4 * P.nodes.size());
   s->fill_ff_each_run.push_back({A.prep_inst, (int)(4 * P.nodes.size())});
   A.acc_writer = (int32_t*)dalloc(s, 4 * std::max<size_t>(P.accs.size(), 1));
@@ -1724,6 +2174,7 @@ void build_session(cf_session* s, const cf::Graph& g, const cf_run_opts* o,
   A.edge_to = (int32_t*)dalloc(s, 4 * (size_t)A.edge_cap);
   A.q_cap = 1ULL << 22;
   A.queue = (unsigned long long*)dalloc(s, 8 * A.q_cap);
+  A.lq = (unsigned long long*)dalloc(s, 8 * A.q_cap);
   A.cq_cap = 1ULL << 16;
   A.cq = (int32_t*)dalloc(s, 4 * A.cq_cap);
   s->zero_each_run.push_back({A.cq, 4 * A.cq_cap});
@@ -1738,10 +2189,20 @@ void build_session(cf_session* s, const cf::Graph& g, const cf_run_opts* o,
   A.fetch_out = (void**)dalloc(s, 8 * std::max<size_t>(P.fetches.size(), 1));
   A.fetch_dead = (uint8_t*)dalloc(s, std::max<size_t>(P.fetches.size(), 1));
   A.watchdog_ns = s->watchdog_ns;
+  A.prof = nullptr;
+  if (o && o->reserved[0]) A.prof = (unsigned long long*)dalloc(s, 6 * 8 * (size_t)cap);
   A.sched_seed = s->sched_seed;
   // ---- grid: one CTA per SM, all co-resident (cooperative launch)
   int sms = 0, per_sm = 0;
   s->dyn_smem = s->precision == CF_BF16 ? tc::kSmemTC : 0;
+  size_t tok_bytes = (sizeof(Tok) * (size_t)P.n_vids + 15) / 16 * 16;
+  size_t body_bytes = sizeof(DNode) * (size_t)P.max_body + ((size_t)P.max_bi * 4 + 15) / 16 * 16;
+  const size_t smem_cap = 196 * 1024;
+  if (tok_bytes + body_bytes <= smem_cap && (int)(tok_bytes + body_bytes) > s->dyn_smem)
+    s->dyn_smem = (int)(tok_bytes + body_bytes);
+  else if (tok_bytes <= smem_cap && (int)tok_bytes > s->dyn_smem)
+    s->dyn_smem = (int)tok_bytes;
+  A.dyn_smem = s->dyn_smem;
   CUDA_OK(cudaFuncSetAttribute(cf_driver_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, s->dyn_smem));
   CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->device));
   CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cf_driver_kernel, kThreads, s->dyn_smem));
@@ -1931,6 +2392,29 @@ cf_status cf_session_describe(const cf_session* s, char* buf, size_t cap) {
   std::string d = s->P.describe + "grid=" + std::to_string(s->grid) + "\n";
   std::strncpy(buf, d.c_str(), cap - 1);
   buf[cap - 1] = 0;
+  return CF_OK;
+}
+
+// profiling hook (include/cf_debug.h): per-instance timing of the last cf_run
+int32_t cf_debug_session_profile(const cf_session* s, unsigned long long* out, int64_t cap,
+                                 int64_t* n_inst, unsigned long long* t0) {
+  if (!s || !s->args.prof) return CF_E_INVALID_GRAPH;
+  RunState st;
+  if (cudaMemcpy(&st, s->args.st, sizeof(RunState), cudaMemcpyDeviceToHost) != cudaSuccess) return CF_E_CUDA;
+  int64_t n = std::min<int64_t>(st.instances + 64, s->args.inst_cap);
+  if (n_inst) *n_inst = n;
+  if (t0) {
+    t0[0] = st.t_start;
+    t0[1] = st.t_end;
+    for (int k = 0; k < 32; ++k) {
+      t0[2 + k] = (unsigned long long)st.op_count[k];
+      t0[34 + k] = (unsigned long long)st.op_cycles[k];
+    }
+  }
+  if (out && cap > 0) {
+    int64_t k = std::min(cap, 6 * n);
+    if (cudaMemcpy(out, s->args.prof, 8 * k, cudaMemcpyDeviceToHost) != cudaSuccess) return CF_E_CUDA;
+  }
   return CF_OK;
 }
 

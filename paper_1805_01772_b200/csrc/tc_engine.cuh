@@ -83,7 +83,10 @@ __device__ inline void tc_tile(TcShared& s, int nk, int bn, int a_mn, int b_mn, 
                                uint32_t& tiles, PlanA plan_a, PlanB plan_b) {
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t stage_b = (uint32_t)bn * BK * 2;
-  if (warp == 0 && lane == 0) {
+  // Role warps: lane 0 works, lanes 1-31 park at __syncwarp (NOT in a suspending
+  // mbarrier.try_wait, which would stall the working lane of the same warp).
+  if (warp == 0) {
+    if (lane == 0) {
     uint32_t c = cnt;
     for (int kb = 0; kb < nk; ++kb, ++c) {
       const int st = c % kStages;
@@ -98,7 +101,10 @@ __device__ inline void tc_tile(TcShared& s, int nk, int bn, int a_mn, int b_mn, 
       for (int i = 0; i < nb; ++i)
         tma_load_3d(s.b[st] + bx[i].off, bx[i].map, &s.full[st], bx[i].c0, bx[i].c1, bx[i].c2);
     }
-  } else if (warp == 1 && lane == 0) {
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {
     const uint32_t idesc = idesc_bf16(BM, bn, a_mn, b_mn);
     const uint32_t tmem = *s.tmem_slot;
     uint32_t c = cnt;
@@ -117,6 +123,8 @@ __device__ inline void tc_tile(TcShared& s, int nk, int bn, int a_mn, int b_mn, 
       mma_commit(&s.empty[st]);   // frees the stage when these MMAs have read it
     }
     mma_commit(s.done);           // accumulator complete
+    }
+    __syncwarp();
   }
   cnt += nk;
   // everyone waits for the accumulator

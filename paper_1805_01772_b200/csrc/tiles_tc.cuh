@@ -206,39 +206,59 @@ __device__ void tile_lstm_bwd_ew_bf(const Inst& I, int tile, float* sm) {
   const bool masked = I.sub & 1;
   const int64_t t = I.s[0];
   float sdb[4] = {0.f, 0.f, 0.f, 0.f};
-  for (int i = 0; i < 32; ++i) {
-    const int r = rt * 128 + rg + 4 * i;
-    if (r >= B) break;
-    const int64_t e = (int64_t)r * H + u;
-    const __nv_bfloat16* gr = gates + (int64_t)r * 4 * H + ut * 256 + threadIdx.x % 64;
-    float ig = bf2f(gr[0]), fg = bf2f(gr[64]), gg = bf2f(gr[128]), og = bf2f(gr[192]);
-    float cp = c_prev[e];
-    float cn = fg * cp + ig * gg;
-    float tc_ = tanhf(cn);
-    float dh = dhn[e] + ldf(dout, dout_dt, e);
-    float dcs = dh * og * (1.0f - tc_ * tc_) + dcn[e];
-    float z0 = dcs * gg * ig * (1.0f - ig);
-    float z1 = dcs * cp * fg * (1.0f - fg);
-    float z2 = dcs * ig * (1.0f - gg * gg);
-    float z3 = dh * tc_ * og * (1.0f - og);
-    float dcp = dcs * fg;
-    if (masked && !(t < lens[r])) {
-      z0 = z1 = z2 = z3 = 0.0f;
-      dcp = dcn[e];
+  const int nrow = min(128, B - rt * 128);
+  for (int i0 = 0; i0 < 32; i0 += 4) {
+    float ig[4], fg[4], gg[4], og[4], cp[4], dhv[4], dcn_[4];
+    int64_t len4[4];
+    bool ok[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int rr = rg + 4 * (i0 + j);
+      ok[j] = rr < nrow;
+      const int r = rt * 128 + (ok[j] ? rr : 0);
+      const int64_t e = (int64_t)r * H + u;
+      const __nv_bfloat16* gr = gates + (int64_t)r * 4 * H + ut * 256 + threadIdx.x % 64;
+      ig[j] = bf2f(gr[0]);
+      fg[j] = bf2f(gr[64]);
+      gg[j] = bf2f(gr[128]);
+      og[j] = bf2f(gr[192]);
+      cp[j] = c_prev[e];
+      dhv[j] = dhn[e] + ldf(dout, dout_dt, e);
+      dcn_[j] = dcn[e];
+      len4[j] = masked ? lens[r] : 0;
     }
-    __nv_bfloat16* zr = dz + (int64_t)r * 4 * H;
-    __nv_bfloat16 b0 = __float2bfloat16(z0), b1 = __float2bfloat16(z1), b2 = __float2bfloat16(z2),
-                  b3 = __float2bfloat16(z3);
-    zr[u] = b0;
-    zr[H + u] = b1;
-    zr[2 * H + u] = b2;
-    zr[3 * H + u] = b3;
-    // db sums the bf16-rounded dz, exactly what the dW GEMM consumes
-    sdb[0] += bf2f(b0);
-    sdb[1] += bf2f(b1);
-    sdb[2] += bf2f(b2);
-    sdb[3] += bf2f(b3);
-    dc[e] = dcp;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (!ok[j]) continue;
+      const int r = rt * 128 + rg + 4 * (i0 + j);
+      const int64_t e = (int64_t)r * H + u;
+      float cn = fg[j] * cp[j] + ig[j] * gg[j];
+      float tc_ = tanhf(cn);
+      float dh = dhv[j];
+      float dcs = dh * og[j] * (1.0f - tc_ * tc_) + dcn_[j];
+      float z0 = dcs * gg[j] * ig[j] * (1.0f - ig[j]);
+      float z1 = dcs * cp[j] * fg[j] * (1.0f - fg[j]);
+      float z2 = dcs * ig[j] * (1.0f - gg[j] * gg[j]);
+      float z3 = dh * tc_ * og[j] * (1.0f - og[j]);
+      float dcp = dcs * fg[j];
+      if (masked && !(t < len4[j])) {
+        z0 = z1 = z2 = z3 = 0.0f;
+        dcp = dcn_[j];
+      }
+      __nv_bfloat16* zr = dz + (int64_t)r * 4 * H;
+      __nv_bfloat16 b0 = __float2bfloat16(z0), b1 = __float2bfloat16(z1),
+                    b2 = __float2bfloat16(z2), b3 = __float2bfloat16(z3);
+      zr[u] = b0;
+      zr[H + u] = b1;
+      zr[2 * H + u] = b2;
+      zr[3 * H + u] = b3;
+      // db sums the bf16-rounded dz, exactly what the dW GEMM consumes
+      sdb[0] += bf2f(b0);
+      sdb[1] += bf2f(b1);
+      sdb[2] += bf2f(b2);
+      sdb[3] += bf2f(b3);
+      dc[e] = dcp;
+    }
   }
   // reduce the 4 row groups: sm[rg][g][64]
   for (int g = 0; g < 4; ++g) sm[(rg * 4 + g) * 64 + threadIdx.x % 64] = sdb[g];
@@ -305,22 +325,28 @@ __device__ void tile_lstm_dxh_tc(const Inst& I, int tile, tc::TcShared& ts, uint
 }
 
 // ---------------------------------------------------------------- backward dW / db
-// p: 0 dz-map (MN), 1 x-map (MN), 2 h-map (MN), 3 dW(f32), 4 db(f32), 5 partials(f32)
-// s: 2 dz slot, 3 x slot, 4 h slot, 6 flags (bit0: accumulate dW, bit1: accumulate db)
+// Chunked over up to 8 gradient-loop steps (K = steps x B): the fp32 read-modify-write of the
+// accumulator is paid once per chunk. p: 0 dz-map (MN), 3 dW(f32), 4 db(f32), 6 step records
+// (6 x i64 per step: dz slot, x-map, x slot, h-map, h slot, db-partials ptr);
+// s: 6 flags (bit0 accumulate dW, bit1 accumulate db), 7 number of steps
 __device__ void tile_lstm_dw_tc(const Inst& I, int tile, tc::TcShared& ts, uint32_t& cnt,
                                 uint32_t& ntile) {
   const int B = (int)I.m, In = (int)I.k, H = (int)I.n, KT = In + H, G = 4 * H;
   const int tn = KT / 256;
   const int n_dw = (G / tc::BM) * tn;
   const int flags = (int)I.s[6];
+  const int ns = (int)I.s[7];
+  const int64_t* ax = (const int64_t*)I.p[6];
   if (tile >= n_dw) {
-    // db tile: 256 gate columns; fixed-order sum over the row-tile partials
+    // db tile: 256 gate columns; fixed-order sum over steps and row-tile partials
     const int c = (tile - n_dw) * 256 + threadIdx.x;
-    const float* partial = (const float*)I.p[5];
     float* db = (float*)I.p[4];
     if (c < G) {
       float s = 0.f;
-      for (int rt = 0; rt < (B + 127) / 128; ++rt) s += partial[(int64_t)rt * G + c];
+      for (int q = 0; q < ns; ++q) {
+        const float* partial = (const float*)ax[q * 6 + 5];
+        for (int rt = 0; rt < (B + 127) / 128; ++rt) s += partial[(int64_t)rt * G + c];
+      }
       db[c] = (flags & 2) ? db[c] + s : s;
     }
     return;
@@ -329,39 +355,46 @@ __device__ void tile_lstm_dw_tc(const Inst& I, int tile, tc::TcShared& ts, uint3
   const int m0 = mt * tc::BM;
   const CUtensorMap* mz = (const CUtensorMap*)I.p[0];
   const bool xpart = nt * 256 < In;
-  const CUtensorMap* mb = (const CUtensorMap*)(xpart ? I.p[1] : I.p[2]);
   const int col0 = xpart ? nt * 256 : nt * 256 - In;
-  const int sz = (int)I.s[2], sb = (int)(xpart ? I.s[3] : I.s[4]);
+  const int nkb = (B + 63) / 64;
   auto plan_a = [&](int kb, tc::Box* b) {
-    b[0] = {mz, m0, kb * 64, sz, 0};
-    b[1] = {mz, m0 + 64, kb * 64, sz, 8192};
+    const int q = kb / nkb, r = kb % nkb;
+    const int sz = (int)ax[q * 6 + 0];
+    b[0] = {mz, m0, r * 64, sz, 0};
+    b[1] = {mz, m0 + 64, r * 64, sz, 8192};
     return 2;
   };
   auto plan_b = [&](int kb, tc::Box* b) {
-    for (int j = 0; j < 4; ++j) b[j] = {mb, col0 + 64 * j, kb * 64, sb, j * 8192};
+    const int q = kb / nkb, r = kb % nkb;
+    const CUtensorMap* mb = (const CUtensorMap*)ax[q * 6 + (xpart ? 1 : 3)];
+    const int sb = (int)ax[q * 6 + (xpart ? 2 : 4)];
+    for (int j = 0; j < 4; ++j) b[j] = {mb, col0 + 64 * j, r * 64, sb, j * 8192};
     return 4;
   };
-  tc::tc_tile(ts, (B + 63) / 64, 256, 1, 1, cnt, ntile, plan_a, plan_b);
+  tc::tc_tile(ts, ns * nkb, 256, 1, 1, cnt, ntile, plan_a, plan_b);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int m = m0 + 32 * (warp % 4) + lane;
   float* dW = (float*)I.p[3] + (int64_t)m * KT + nt * 256;
   const bool acc = flags & 1;
-  for (int c = (warp / 4) * 128; c < (warp / 4) * 128 + 128; c += 16) {
-    float v[16];
+  for (int c = (warp / 4) * 128; c < (warp / 4) * 128 + 128; c += 32) {
+    float v[32];
     tc::tc_acc16(ts, c, v);
+    tc::tc_acc16(ts, c + 16, v + 16);
     float4* d = (float4*)(dW + c);
+    if (acc) {
+      float4 old[8];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      float4 x = *(float4*)&v[4 * q];
-      if (acc) {
-        float4 y = d[q];
-        x.x += y.x;
-        x.y += y.y;
-        x.z += y.z;
-        x.w += y.w;
+      for (int q = 0; q < 8; ++q) old[q] = d[q];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        v[4 * q] += old[q].x;
+        v[4 * q + 1] += old[q].y;
+        v[4 * q + 2] += old[q].z;
+        v[4 * q + 3] += old[q].w;
       }
-      d[q] = x;
     }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) d[q] = *(float4*)&v[4 * q];
   }
   tc::tc_tile_end();
 }
