@@ -166,13 +166,13 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg3", choices=list(CONFIGS))
-    ap.add_argument("--precision", default="f32", choices=["f32", "bf16"])
+    ap.add_argument("--precision", default="bf16", choices=["f32", "bf16"])
     ap.add_argument("--K", type=int, default=0, help="parallel_iterations override (0 = 32)")
     ap.add_argument("--ref-T", type=int, default=8)
     ap.add_argument("--steps-ref", type=int, default=3)
     ap.add_argument("--warmup-ref", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-T", type=int, default=4)
+    ap.add_argument("--cpu-T", type=int, default=12)
     args = ap.parse_args()
     c = CONFIGS[args.config]
     if args.impl == "reference":
