@@ -486,7 +486,7 @@ struct Driver {
   int32_t* dw_count_;
   int32_t* acc_writer_;
   int32_t* iter_out_;
-  uint8_t* inst_done_;
+  const DStack* stacks_;
   long long n_push = 0, n_pop = 0, n_dead = 0, n_inst = 0, n_tiles = 0;
   long long op_cnt[32] = {}, op_cyc[32] = {};
   int32_t max_depth = 0, n_exitf = 0;
@@ -500,7 +500,7 @@ struct Driver {
   __device__ Driver(const RunArgs& a, Tok* t, DNode* smn, int32_t* smi, volatile int* req)
       : A(a), P(a.prog), st(a.st), places_(a.prog.places), reg_(a.prog.reg),
         stack_depth_(a.stack_depth), prep_inst_(a.prep_inst), dw_count_(a.dw_count),
-        acc_writer_(a.acc_writer), iter_out_(a.iter_outstanding), inst_done_(a.inst_done),
+        acc_writer_(a.acc_writer), iter_out_(a.iter_outstanding), stacks_(a.prog.stacks),
         toks_(t), iv_(a.prog.in_vids), bn_(nullptr), sm_nodes_(smn), sm_iv_(smi), req_(req) {}
 
   // ask the helper warps to copy [src, src+bytes) -> dst (16 B aligned), wait for them
@@ -533,7 +533,7 @@ struct Driver {
   // frame-level nodes (Enter / Exit) always index the global input-id table
   __device__ Tok& in_tok_g(const DNode& d, int j) { return toks_[P.in_vids[d.in_off + j]]; }
 
-  __device__ bool writer_done(int32_t w) { return w < 0 || inst_done_[w]; }
+  __device__ bool writer_done(int32_t w) { return done(w); }
 
   // scalar value of a token; false if its bytes are not produced yet
   __device__ bool scalar(const Tok& t, int64_t* out) {
@@ -572,24 +572,47 @@ struct Driver {
   }
 
   // ---------------------------------------------------------------- instances
+  // ---- in-flight instance bookkeeping: a shared-memory ring indexed by id & kRingMask.
+  // A slot is reused only after its previous occupant completed, so `done(w)` is simply
+  // "the slot no longer holds w". Successor edges stay in global memory (written here, read
+  // once at completion).
+  static constexpr int kRing = 1024, kRingMask = kRing - 1;
+  int32_t* r_id;     // occupant id (-1 free)
+  int32_t* r_pend;   // producers outstanding
+  int32_t* r_succ;   // successor edge list head
+  int32_t* r_last;   // last successor added (dedupe)
+  int32_t* r_nt;     // tiles
+  int32_t* r_kfi;    // kind (8) | frame + 1 (8) | iter (16)
+
+  __device__ bool done(int32_t w) const { return w < 0 || r_id[w & kRingMask] != w; }
+
   __noinline__ __device__ int32_t new_inst(int kind, int sub, int ntiles) {
     if (ninst >= A.inst_cap) {
       fail(CF_E_STACK_BUDGET, -1);
       return -1;
     }
     int32_t id = ninst++;
+    const int sl = id & kRingMask;
+    while (r_id[sl] != -1) {   // ring full: wait for the oldest in-flight instance
+      drain();
+      if (st->error) return -1;
+    }
+    ntiles = max(ntiles, 1);
+    r_id[sl] = id;
+    r_pend[sl] = 0;
+    r_succ[sl] = -1;
+    r_last[sl] = -1;
+    r_nt[sl] = ntiles;
+    r_kfi[sl] = (kind & 255) | (((cur_frame + 1) & 255) << 8) | ((cur_frame >= 0 ? iter : 0) << 16);
     Inst& I = A.insts[id];
     I.kind = kind;
     I.sub = sub;
-    I.ntiles = max(ntiles, 1);
+    I.ntiles = ntiles;
     I.frame = cur_frame;
     I.iter = cur_frame >= 0 ? iter : 0;
     for (int j = 0; j < 14; ++j) I.p[j] = 0;
     for (int j = 0; j < 4; ++j) I.s[j] = 0;
     I.n = I.m = I.k = 0;
-    A.inst_pending[id] = 0;
-    A.succ_head[id] = -1;
-    inst_done_[id] = 0;
     if (A.prof) {
       unsigned long long* pr = A.prof + 6 * (int64_t)id;
       pr[0] = globaltimer();
@@ -597,31 +620,31 @@ struct Driver {
       pr[2] = ~0ULL;
       pr[3] = 0;
       pr[4] = 0;
-      pr[5] = ((unsigned long long)kind << 32) | (unsigned)max(ntiles, 1);
+      pr[5] = ((unsigned long long)kind << 32) | (unsigned)ntiles;
     }
     return id;
   }
   __noinline__ __device__ void add_dep(int32_t id, int32_t w) {
-    if (w < 0 || inst_done_[w]) return;
-    // dedupe against the most recent edge of w
-    int32_t h = A.succ_head[w];
-    if (h >= 0 && A.edge_to[h] == id) return;
+    if (done(w)) return;
+    const int ws = w & kRingMask;
+    if (r_last[ws] == id) return;   // dedupe repeated inputs from the same producer
     if (nedge >= A.edge_cap) {
       fail(CF_E_STACK_BUDGET, -2);
       return;
     }
     int32_t e = nedge++;
     A.edge_to[e] = id;
-    A.edge_next[e] = h;
-    A.succ_head[w] = e;
-    A.inst_pending[id]++;
+    A.edge_next[e] = r_succ[ws];
+    r_succ[ws] = e;
+    r_last[ws] = id;
+    r_pend[id & kRingMask]++;
   }
   // two rings: critical-path work (high) and filler work (low: dW chunks) so that the
   // recurrence never queues behind throughput work
   __noinline__ __device__ void publish(int32_t id) {
-    const Inst& I = A.insts[id];
-    unsigned long long n = (unsigned long long)I.ntiles;
-    const bool low = I.kind == HK_LSTM_DW_TC;
+    const int sl = id & kRingMask;
+    unsigned long long n = (unsigned long long)r_nt[sl];
+    const bool low = (r_kfi[sl] & 255) == HK_LSTM_DW_TC;
     int spins = 0;
     if (q_tail + lq_tail + n - q_done_seen > A.q_cap / 4) {
       q_done_seen = ld_volatile_u64(&st->q_done);
@@ -642,20 +665,26 @@ struct Driver {
   }
   __device__ void submit(int32_t id, bool = false) {
     if (id < 0) return;
+    const int sl = id & kRingMask;
     outstanding++;
     n_inst++;
-    n_tiles += A.insts[id].ntiles;
+    n_tiles += r_nt[sl];
     if (cur_frame >= 0) iter_out_[P.frames[cur_frame].iter_base + iter]++;
-    if (A.inst_pending[id] == 0) publish(id);
+    if (r_pend[sl] == 0) publish(id);
   }
   __noinline__ __device__ void complete(int32_t id) {
-    inst_done_[id] = 1;
+    const int sl = id & kRingMask;
     outstanding--;
-    const Inst& I = A.insts[id];
-    if (I.frame >= 0) iter_out_[P.frames[I.frame].iter_base + I.iter]--;
-    for (int32_t e = A.succ_head[id]; e >= 0; e = A.edge_next[e]) {
-      int32_t s = A.edge_to[e];
-      if (--A.inst_pending[s] == 0) publish(s);
+    const int kfi = r_kfi[sl];
+    const int fr = ((kfi >> 8) & 255) - 1;
+    if (fr >= 0) iter_out_[P.frames[fr].iter_base + (kfi >> 16)]--;
+    int32_t e = r_succ[sl];
+    r_id[sl] = -1;   // done
+    while (e >= 0) {
+      const int32_t s2 = A.edge_to[e];
+      const int32_t nx = A.edge_next[e];
+      if (--r_pend[s2 & kRingMask] == 0) publish(s2);
+      e = nx;
     }
   }
   __noinline__ __device__ bool drain() {
@@ -1427,7 +1456,7 @@ struct Driver {
       case OP_STACK_PUSH: {
         if (!dead) {
           int s = (int)in_tok(d, 0).v;
-          const DStack& S = P.stacks[s];
+          const DStack& S = stacks_[s];
           int dp = stack_depth_[s];
           if (dp >= S.capacity) {
             fail(CF_E_STACK_BUDGET, dp);
@@ -1446,7 +1475,7 @@ struct Driver {
           break;
         }
         int s = (int)in_tok(d, 0).v;
-        const DStack& S = P.stacks[s];
+        const DStack& S = stacks_[s];
         int dp = stack_depth_[s];
         if (dp <= 0) {
           fail(CF_E_POP_EMPTY, s);
@@ -1888,23 +1917,26 @@ __global__ void __launch_bounds__(kThreads, 1) cf_driver_kernel(RunArgs A_param)
     Tok* toks = A.toks;
     DNode* smn = nullptr;
     int32_t* smi = nullptr;
+    const int64_t ring_b = 6 * 4 * 1024;   // in-flight instance ring (always in smem)
+    uint8_t* base = drv_smem + ring_b;
+    const int64_t avail = A.dyn_smem - ring_b;
     const int64_t tok_b = (int64_t)A.prog.n_vids * (int64_t)sizeof(Tok);
     const int64_t node_b = (int64_t)A.prog.max_body * (int64_t)sizeof(DNode);
     const int64_t iv_b = ((int64_t)A.prog.max_bi * 4 + 15) / 16 * 16;
-    if (tok_b <= A.dyn_smem) {
+    if (tok_b <= avail) {
       // stage the token table (placeholders preset by the host) in shared memory
-      Tok* sm = (Tok*)drv_smem;
+      Tok* sm = (Tok*)base;
       for (int i = threadIdx.x; i < A.prog.n_vids; i += blockDim.x) sm[i] = A.toks[i];
       toks = sm;
       const int64_t tok_pad = (tok_b + 15) / 16 * 16;
-      if (tok_pad + node_b + iv_b <= A.dyn_smem) {
-        smn = (DNode*)(drv_smem + tok_pad);
-        smi = (int32_t*)(drv_smem + tok_pad + node_b);
+      if (tok_pad + node_b + iv_b <= avail) {
+        smn = (DNode*)(base + tok_pad);
+        smi = (int32_t*)(base + tok_pad + node_b);
       }
     }
     // further driver-private arrays into the remaining shared memory
-    int64_t used = 0;
-    if (toks != A.toks) used = (tok_b + 15) / 16 * 16 + (smn ? node_b + iv_b : 0);
+    int64_t used = ring_b;
+    if (toks != A.toks) used += (tok_b + 15) / 16 * 16 + (smn ? node_b + iv_b : 0);
     auto carve = [&](int64_t bytes) -> uint8_t* {
       bytes = (bytes + 15) / 16 * 16;
       if (toks == A.toks || used + bytes > A.dyn_smem) return nullptr;
@@ -1920,7 +1952,8 @@ __global__ void __launch_bounds__(kThreads, 1) cf_driver_kernel(RunArgs A_param)
     int32_t* s_dwc = (int32_t*)carve(4 * (int64_t)P.n_nodes);
     int32_t* s_accw = (int32_t*)carve(4 * (int64_t)P.n_accs);
     int32_t* s_iter = (int32_t*)carve(4 * (int64_t)P.iter_counters);
-    uint8_t* s_done = (uint8_t*)carve(A.inst_cap);
+    int32_t* s_ring = (int32_t*)drv_smem;
+    DStack* s_stk = (DStack*)carve((int64_t)P.n_stacks * sizeof(DStack));
     for (int i = threadIdx.x; s_pl && i < P.n_places; i += blockDim.x) s_pl[i] = P.places[i];
     for (int i = threadIdx.x; s_reg && i < P.n_reg; i += blockDim.x) s_reg[i] = P.reg[i];
     for (int i = threadIdx.x; s_sd && i < P.n_stacks; i += blockDim.x) s_sd[i] = 0;
@@ -1928,6 +1961,8 @@ __global__ void __launch_bounds__(kThreads, 1) cf_driver_kernel(RunArgs A_param)
     for (int i = threadIdx.x; s_dwc && i < P.n_nodes; i += blockDim.x) s_dwc[i] = 0;
     for (int i = threadIdx.x; s_accw && i < P.n_accs; i += blockDim.x) s_accw[i] = -1;
     for (int i = threadIdx.x; s_iter && i < P.iter_counters; i += blockDim.x) s_iter[i] = 0;
+    for (int i = threadIdx.x; s_ring && i < 1024; i += blockDim.x) s_ring[i] = -1;
+    for (int i = threadIdx.x; s_stk && i < P.n_stacks; i += blockDim.x) s_stk[i] = P.stacks[i];
     if (threadIdx.x == 0) {
       req[0] = 0;
       req[1] = 0;
@@ -1945,7 +1980,17 @@ __global__ void __launch_bounds__(kThreads, 1) cf_driver_kernel(RunArgs A_param)
       if (s_dwc) d.dw_count_ = s_dwc;
       if (s_accw) d.acc_writer_ = s_accw;
       if (s_iter) d.iter_out_ = s_iter;
-      if (s_done) d.inst_done_ = s_done;
+      if (!s_ring) {
+        d.fail(CF_E_UNSUPPORTED, -7);   // no room for the in-flight ring
+      } else {
+        d.r_id = s_ring;
+        d.r_pend = s_ring + 1024;
+        d.r_succ = s_ring + 2048;
+        d.r_last = s_ring + 3072;
+        d.r_nt = s_ring + 4096;
+        d.r_kfi = s_ring + 5120;
+      }
+      if (s_stk) d.stacks_ = s_stk;
       d.run();
       *(volatile int*)&req[0] = -1;
     } else if (threadIdx.x >= 32) {
@@ -2195,13 +2240,15 @@ void build_session(cf_session* s, const cf::Graph& g, const cf_run_opts* o,
   // ---- grid: one CTA per SM, all co-resident (cooperative launch)
   int sms = 0, per_sm = 0;
   s->dyn_smem = s->precision == CF_BF16 ? tc::kSmemTC : 0;
-  size_t tok_bytes = (sizeof(Tok) * (size_t)P.n_vids + 15) / 16 * 16;
-  size_t body_bytes = sizeof(DNode) * (size_t)P.max_body + ((size_t)P.max_bi * 4 + 15) / 16 * 16;
-  const size_t smem_cap = 196 * 1024;
-  if (tok_bytes + body_bytes <= smem_cap && (int)(tok_bytes + body_bytes) > s->dyn_smem)
-    s->dyn_smem = (int)(tok_bytes + body_bytes);
-  else if (tok_bytes <= smem_cap && (int)tok_bytes > s->dyn_smem)
-    s->dyn_smem = (int)tok_bytes;
+  // driver CTA: ring + tokens + body program + private arrays; capped below the opt-in limit
+  size_t need = 6 * 4 * 1024;
+  need += (sizeof(Tok) * (size_t)P.n_vids + 15) / 16 * 16;
+  need += sizeof(DNode) * (size_t)P.max_body + ((size_t)P.max_bi * 4 + 15) / 16 * 16;
+  need += sizeof(PlaceDesc) * P.places.size() + sizeof(DReg) * (P.reg.size() + P.feeds.size() + 1);
+  need += sizeof(DStack) * P.stacks.size() + 8 * P.nodes.size() + 4 * (P.accs.size() + P.iter_counters);
+  need += 16 * 12;
+  const size_t smem_cap = 200 * 1024;
+  if ((int)std::min(need, smem_cap) > s->dyn_smem) s->dyn_smem = (int)std::min(need, smem_cap);
   A.dyn_smem = s->dyn_smem;
   CUDA_OK(cudaFuncSetAttribute(cf_driver_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, s->dyn_smem));
   CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->device));
