@@ -128,6 +128,7 @@ struct DReg {
   int64_t base;
   int64_t slot_bytes;
   int32_t slots, rows, cols, map0;   // map0: index of its 3 tensor maps (KA, KB, MN)
+  double inv_slot;                    // 1 / slot_bytes (division-free slot index on device)
 };
 
 struct DFrame {
@@ -235,14 +236,12 @@ struct RunArgs {
   int32_t* ta_slot_off;      // [n_tas] offset into ta_writer / ta_written
   Inst* insts;               // [inst_cap]
   int32_t inst_cap;
-  int32_t* inst_pending;     // deps outstanding
-  uint8_t* inst_done;
+  int32_t* tile_next;        // per instance: next tile to claim (atomic, workers)
   int32_t* inst_tiles_done;  // atomic per instance
-  int32_t* succ_head;        // per instance edge list head (-1)
   int32_t* edge_next;        // [edge_cap]
   int32_t* edge_to;
   int32_t edge_cap;
-  unsigned long long* queue; // [q_cap]
+  unsigned long long* queue; // [q_cap] ready instance ids (tiles claimed via tile_next)
   unsigned long long q_cap;
   int32_t* cq;               // [cq_cap] completion queue (inst + 1; 0 = empty)
   unsigned long long cq_cap;

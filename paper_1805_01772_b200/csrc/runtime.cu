@@ -585,8 +585,21 @@ struct Driver {
   int32_t* r_kfi;    // kind (8) | frame + 1 (8) | iter (16)
 
   __device__ bool done(int32_t w) const { return w < 0 || r_id[w & kRingMask] != w; }
+  // region profiler (profiling runs only): cycles + count into op_cyc/op_cnt[slot]
+  struct Region {
+    Driver* d; int slot; long long c0;
+#ifdef __CUDA_ARCH__
+    __device__ Region(Driver* dd, int s) : d(dd), slot(s), c0(dd->A.prof ? clock64() : 0) {}
+    __device__ ~Region() {
+      if (d->A.prof) { d->op_cyc[slot] += clock64() - c0; d->op_cnt[slot]++; }
+    }
+#else
+    __device__ Region(Driver* dd, int s) : d(dd), slot(s), c0(0) {}
+#endif
+  };
 
   __noinline__ __device__ int32_t new_inst(int kind, int sub, int ntiles) {
+    Region rg(this, 26);
     if (ninst >= A.inst_cap) {
       fail(CF_E_STACK_BUDGET, -1);
       return -1;
@@ -642,24 +655,16 @@ struct Driver {
   // two rings: critical-path work (high) and filler work (low: dW chunks) so that the
   // recurrence never queues behind throughput work
   __noinline__ __device__ void publish(int32_t id) {
+    Region rg(this, 27);
     const int sl = id & kRingMask;
-    unsigned long long n = (unsigned long long)r_nt[sl];
     const bool low = (r_kfi[sl] & 255) == HK_LSTM_DW_TC;
-    int spins = 0;
-    if (q_tail + lq_tail + n - q_done_seen > A.q_cap / 4) {
-      q_done_seen = ld_volatile_u64(&st->q_done);
-      while (q_tail + lq_tail + n - q_done_seen > A.q_cap / 2) {
-        backoff(spins);
-        if (st->error) return;
-        q_done_seen = ld_volatile_u64(&st->q_done);
-      }
-    }
+    // one entry per instance; workers claim its tiles through tile_next[id]. At most kRing
+    // instances are in flight, so the 2^22-entry rings never wrap onto live entries.
     if (A.prof) A.prof[6 * (int64_t)id + 1] = globaltimer();
     unsigned long long* ring = low ? A.lq : A.queue;
     unsigned long long& tail = low ? lq_tail : q_tail;
-    for (unsigned long long t = 0; t < n; ++t)
-      ring[(tail + t) % A.q_cap] = ((unsigned long long)id << 32) | t;
-    tail += n;
+    ring[tail & (A.q_cap - 1)] = (unsigned long long)id;
+    tail += 1;
     // release: instance record + queue entries visible before the new tail
     st_release_u64(low ? &st->lq_tail : &st->q_tail, tail);
   }
@@ -688,9 +693,10 @@ struct Driver {
     }
   }
   __noinline__ __device__ bool drain() {
+    Region rg(this, 29);
     bool any = false;
     for (int k = 0; k < 256; ++k) {
-      int* p = &A.cq[cq_head % A.cq_cap];
+      int* p = &A.cq[cq_head & (A.cq_cap - 1)];
       int v = ld_acquire_i32(p);   // pairs with the worker's release of its completion
       if (v == 0) break;
       *(volatile int*)p = 0;
@@ -703,6 +709,7 @@ struct Driver {
 
   // ---------------------------------------------------------------- placement
   __noinline__ __device__ bool place(const DNode& d, int port, int64_t* ptr) {
+    Region rg(this, 31);
     const PlaceDesc& pl = places_[d.place_off + port];
     int it = cur_frame >= 0 ? iter : 0;
     switch (pl.kind) {
@@ -744,13 +751,25 @@ struct Driver {
   // pointer -> (tensor map, slot) for a bf16 [rows][cols] GEMM operand; kind 0 = K-major A
   // (box 64x128), 1 = K-major B (box 64x256), 2 = MN-major (box 64x64)
   __noinline__ __device__ bool resolve(int64_t p, int rows, int cols, int kind, int64_t* map, int64_t* slot) {
-    for (int i = 0; i < P.n_reg; ++i) {
+    Region rg(this, 28);
+    // entries are sorted by base (host): binary search for the last base <= p, then the
+    // entries sharing that base (one buffer registered under several shapes)
+    int lo = 0, hi = P.n_reg - 1, at = -1;
+    while (lo <= hi) {
+      const int mid = (lo + hi) >> 1;
+      if (reg_[mid].base <= p) { at = mid; lo = mid + 1; } else hi = mid - 1;
+    }
+    for (int i = at; i >= 0 && reg_[i].base == reg_[at].base; --i) {
       const DReg& r = reg_[i];
       if (r.rows != rows || r.cols != cols) continue;
-      if (p < r.base || p >= r.base + (int64_t)r.slots * r.slot_bytes) continue;
-      int64_t off = p - r.base;
-      if (off % r.slot_bytes) continue;
-      *slot = off / r.slot_bytes;
+      if (p >= r.base + (int64_t)r.slots * r.slot_bytes) continue;
+      const int64_t off = p - r.base;
+      int64_t q = (int64_t)((double)off * r.inv_slot);
+      int64_t rem = off - q * r.slot_bytes;
+      if (rem < 0) { --q; rem += r.slot_bytes; }
+      else if (rem >= r.slot_bytes) { ++q; rem -= r.slot_bytes; }
+      if (rem) continue;
+      *slot = q;
       *map = (int64_t)((const uint8_t*)P.maps + (int64_t)(r.map0 + kind) * 128);
       return true;
     }
@@ -1572,6 +1591,7 @@ struct Driver {
   // get a tiny straight-line path (16-byte token moves, no calls) at the head of the loop;
   // everything else goes through the out-of-line eval().
   __noinline__ __device__ bool run_body(const DFrame& F) {
+    Region rg(this, 25);
     bool progress = false;
     const bool prof = A.prof != nullptr;
     int4* tk = (int4*)toks_;
@@ -1756,13 +1776,14 @@ struct Driver {
   }
 
   __device__ void run() {
-    if (A.prof) calibrate();
     st->t_start = globaltimer();
     last_progress = st->t_start;
     while (true) {
+      long long ci = A.prof ? clock64() : 0;
       bool p = drain();
       if (st->error) break;
       p |= step();
+      if (A.prof && !p) { op_cyc[30] += clock64() - ci; op_cnt[30]++; }
       if (st->error) break;
       if (fetched && cur_frame < 0 && root_pc >= P.n_root_steps && outstanding == 0) break;
       unsigned long long now = globaltimer();
@@ -1808,25 +1829,29 @@ __device__ void worker_loop(const RunArgs& A) {
       // claim from the high-priority ring first, then the low one (CAS on the heads)
       int spins = 0;
       unsigned long long e = ~0ULL;
+      // queue entries are instance ids; a tile is claimed with one atomicAdd on the
+      // instance's tile counter, and whoever takes (or overshoots) the last tile advances
+      // the head past the instance
+      auto claim = [&](unsigned long long* headp, unsigned long long* tailp,
+                       const unsigned long long* ring) -> int {
+        unsigned long long h = ld_volatile_u64(headp);
+        if (h >= ld_volatile_u64(tailp)) return 0;
+        __threadfence();
+        const int32_t id = (int32_t)((volatile const unsigned long long*)ring)[h & (A.q_cap - 1)];
+        const int nt = ((volatile const Inst*)(A.insts + id))->ntiles;
+        const int t = atomicAdd(&A.tile_next[id], 1);
+        if (t >= nt - 1) atomicCAS(headp, h, h + 1);
+        if (t >= nt) return 2;
+        e = ((unsigned long long)id << 32) | (unsigned)t;
+        return 1;
+      };
       while (true) {
-        unsigned long long h = ld_volatile_u64(&st->q_head);
-        if (h < ld_volatile_u64(&st->q_tail)) {
-          if (atomicCAS(&st->q_head, h, h + 1) == h) {
-            __threadfence();
-            e = ((volatile unsigned long long*)A.queue)[h % A.q_cap];
-            break;
-          }
-          continue;
-        }
-        unsigned long long l = ld_volatile_u64(&st->lq_head);
-        if (l < ld_volatile_u64(&st->lq_tail)) {
-          if (atomicCAS(&st->lq_head, l, l + 1) == l) {
-            __threadfence();
-            e = ((volatile unsigned long long*)A.lq)[l % A.q_cap];
-            break;
-          }
-          continue;
-        }
+        int r = claim(&st->q_head, &st->q_tail, A.queue);
+        if (r == 1) break;
+        if (r == 2) continue;
+        r = claim(&st->lq_head, &st->lq_tail, A.lq);
+        if (r == 1) break;
+        if (r == 2) continue;
         if (ld_volatile_i32(&st->quit)) break;
         backoff(spins);
       }
@@ -1891,7 +1916,7 @@ __device__ void worker_loop(const RunArgs& A) {
       if (threadIdx.x == 0) {
         __threadfence();
         unsigned long long slot = atomicAdd(&st->cq_tail, 1ULL);
-        int* p = &A.cq[slot % A.cq_cap];
+        int* p = &A.cq[slot & (A.cq_cap - 1)];
         int spins = 0;
         while (ld_volatile_i32(p) != 0) {
           if (ld_volatile_i32(&st->quit)) break;
@@ -2054,6 +2079,7 @@ struct cf_session {
   std::vector<DReg> reg_host;
   std::vector<CUtensorMap> maps_host;
   int n_reg_static = 0;
+  std::vector<DReg> reg_sorted;   // per-run upload, sorted by base
 };
 
 namespace {
@@ -2209,11 +2235,10 @@ void build_session(cf_session* s, const cf::Graph& g, const cf_run_opts* o,
   int64_t cap = P.inst_bound;
   A.inst_cap = (int32_t)cap;
   A.insts = (Inst*)dalloc(s, sizeof(Inst) * cap);
-  A.inst_pending = (int32_t*)dalloc(s, 4 * cap);
-  A.inst_done = (uint8_t*)dalloc(s, cap);
+  A.tile_next = (int32_t*)dalloc(s, 4 * cap);
+  s->zero_each_run.push_back({A.tile_next, (size_t)(4 * cap)});
   A.inst_tiles_done = (int32_t*)dalloc(s, 4 * cap);
   s->zero_each_run.push_back({A.inst_tiles_done, (size_t)(4 * cap)});
-  A.succ_head = (int32_t*)dalloc(s, 4 * cap);
   A.edge_cap = (int32_t)std::min<int64_t>(cap * 24, 1LL << 30);
   A.edge_next = (int32_t*)dalloc(s, 4 * (size_t)A.edge_cap);
   A.edge_to = (int32_t*)dalloc(s, 4 * (size_t)A.edge_cap);
@@ -2345,12 +2370,17 @@ cf_status cf_run(cf_session* s, int32_t n_feed, const char* const* feed_names,
       }
       int nf = n - s->n_reg_static;
       if (nf > 0) {
-        CUDA_OK(cudaMemcpyAsync((void*)(A.prog.reg + s->n_reg_static), s->reg_host.data() + s->n_reg_static,
-                                sizeof(DReg) * nf, cudaMemcpyHostToDevice, s->stream));
         CUDA_OK(cudaMemcpyAsync((uint8_t*)A.prog.maps + sizeof(CUtensorMap) * 3 * s->n_reg_static,
                                 s->maps_host.data() + 3 * s->n_reg_static, sizeof(CUtensorMap) * 3 * nf,
                                 cudaMemcpyHostToDevice, s->stream));
       }
+      // the device looks entries up by binary search over base
+      s->reg_sorted.assign(s->reg_host.begin(), s->reg_host.begin() + n);
+      for (auto& r : s->reg_sorted) r.inv_slot = 1.0 / (double)r.slot_bytes;
+      std::sort(s->reg_sorted.begin(), s->reg_sorted.end(),
+                [](const DReg& a, const DReg& b) { return a.base < b.base; });
+      CUDA_OK(cudaMemcpyAsync((void*)A.prog.reg, s->reg_sorted.data(), sizeof(DReg) * n,
+                              cudaMemcpyHostToDevice, s->stream));
       A.prog.n_reg = n;
     }
     // ta bases reset (unstack may alias)

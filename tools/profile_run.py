@@ -62,8 +62,8 @@ os.makedirs(os.path.dirname(a.out), exist_ok=True)
 OPS = ["NOP", "PLACEHOLDER", "CONST", "PASS", "SWITCH", "MERGE", "MERGE_LOOP", "ENTER", "EXIT",
        "NEXTITER", "SCALAR", "REDUCE_I", "SLICE_I", "FLOW", "TA_CREATE", "TA_READ", "TA_WRITE",
        "TA_STACK", "TA_UNSTACK", "TA_GRAD", "STACK_CREATE", "STACK_PUSH", "STACK_POP", "HEAVY", "ACC"]
-OPS = OPS + ["?25", "CAL_LOOP", "CAL_SMEM_TOK", "CAL_GST", "CAL_IV"]
-res["driver"] = {(OPS[k] if k < len(OPS) else ("DRAIN" if k == 31 else str(k))): {"n": n, "us": cyc / 1965.0}
+OPS = OPS + ["R_RUN_BODY", "R_NEW_INST", "R_PUBLISH", "R_RESOLVE", "R_DRAIN", "R_IDLE", "R_PLACE"]
+res["driver"] = {OPS[k]: {"n": n, "us": cyc / 1965.0}
                  for k, (n, cyc) in enumerate(s.driver_ops) if n}
 json.dump(res, open(a.out, "w"), indent=1)
 rel = rows.copy()
