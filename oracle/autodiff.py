@@ -30,8 +30,8 @@ from __future__ import annotations
 import collections
 from typing import Dict, List, Optional
 
-from .graph import (BOOL, DIFFERENTIABLE, FLOAT, FLOW, INT, RES, Builder, Ctx, GraphError,
-                    Node, T)
+from .graph import (BOOL, DIFFERENTIABLE, FLOAT, FLOW, GRAD_CHANNEL, INT, RES, Builder, Ctx,
+                    GraphError, Node, T)
 
 
 class _AD:
@@ -177,9 +177,14 @@ class _AD:
     def backprop(self, ctx: Ctx, ups: Dict[T, List[T]], wrt: List[T]) -> Dict[T, T]:
         items, topo = self._items(ctx)
         from_wrt = set(wrt)
+        # Send/Recv pairs carry the dependence across partitions: a Recv's
+        # value depends on the peer's parameters, and every Send/Recv gets its mirrored
+        # gradient message, so items holding one are never pruned (else a peer would wait).
+        comm = {k: any(n.op in ("Send", "Recv") for n in items[k]["nodes"]) for k in topo}
+        recv = {k: any(n.op == "Recv" for n in items[k]["nodes"]) for k in topo}
         for k in topo:
             it = items[k]
-            if any(t in from_wrt for t in it["inputs"]):
+            if any(t in from_wrt for t in it["inputs"]) or recv[k]:
                 from_wrt.update(it["outputs"])
         grads: Dict[T, List[T]] = collections.defaultdict(list)
         for t, gl in ups.items():
@@ -190,9 +195,9 @@ class _AD:
             for o, go in zip(it["outputs"], g_outs):
                 if go is not None:
                     grads[o] = [go]
-            if all(go is None for go in g_outs):
+            if all(go is None for go in g_outs) and not comm[k]:
                 continue
-            if not any(t in from_wrt for t in it["inputs"]):
+            if not any(t in from_wrt for t in it["inputs"]) and not comm[k]:
                 continue
             if k[0] == "node":
                 pairs = zip(it["inputs"], self.op_grad(it["nodes"][0], g_outs))
@@ -225,7 +230,7 @@ class _AD:
             for e, _ in captures[br]:
                 if e not in externals and self.dtype(e) in DIFFERENTIABLE:
                     externals.append(e)
-        if not externals:
+        if not externals and not any(n.op in ("Send", "Recv") for n in it["nodes"]):
             return []
         pred_g = self.fwd(pred)
 
@@ -313,6 +318,15 @@ class _AD:
         F = self.fwd
         if op in ("Identity", "Cast"):
             return [g]
+        if op == "Send":
+            # the gradient of a sent value comes back from the receiver on the mirrored edge
+            v = ins[0]
+            return [b.recv(F(ins[1]), n.attrs["channel"] ^ GRAD_CHANNEL, n.attrs["peer"],
+                           self.dtype(v), self.shape(v)), None]
+        if op == "Recv":
+            gv = g if g is not None else self.zeros_like_static(out)
+            b.send(gv, F(ins[0]), n.attrs["channel"] ^ GRAD_CHANNEL, n.attrs["peer"])
+            return [None]
         if op in ("StopGradient", "Placeholder", "Const", "ZerosLike", "Less", "LessEqual",
                   "Greater", "Equal", "LogicalAnd", "LogicalNot", "ReduceMax", "ReduceMin",
                   "TACreate", "StackCreate", "StackPush", "StackPop", "TAGrad"):

@@ -30,6 +30,7 @@ import numpy as np
 
 FLOAT = "f64"
 INT = "i64"
+GRAD_CHANNEL = 1 << 20     # channel id of the gradient edge mirroring a Send/Recv edge
 BOOL = "bool"
 FLOW = "flow"   # TensorArray flow scalar (ordering token); differentiable (TF convention)
 RES = "res"     # resource handle (TensorArray, Stack)
@@ -292,6 +293,13 @@ def infer(g: Graph, op: str, inputs: Sequence[T], attrs: Dict[str, Any]):
     if op == "StackPop":
         need(1)
         return [attrs["dtype"]], [tuple(attrs["elem_shape"]) if attrs.get("elem_shape") is not None else None]
+    # ---- cross-device Send / Recv (§4.4): rendezvous on (channel, tag)
+    if op == "Send":
+        need(2)     # value, ix (a scalar of the sending context; places the op in it)
+        return [], []
+    if op == "Recv":
+        need(1)     # ix (a scalar of the receiving context)
+        return [attrs["dtype"]], [tuple(attrs["shape"])]
     raise GraphError("CF_E_UNSUPPORTED", f"unknown op {op}")
 
 
@@ -438,6 +446,15 @@ class Builder:
     def mul(self, a, b): return self.op1("Mul", [a, b])
     def matmul(self, a, b, ta=False, tb=False): return self.op1("MatMul", [a, b], {"ta": ta, "tb": tb})
     def less(self, a, b): return self.op1("Less", [a, b])
+
+    # Send / Recv between partitions. `channel` names the edge; the message
+    # key is (channel, iteration tag), so a Send and its Recv must sit in mirrored contexts.
+    def send(self, v: T, ix: T, channel: int, peer: int) -> None:
+        self.op("Send", [v, ix], {"channel": channel, "peer": peer})
+
+    def recv(self, ix: T, channel: int, peer: int, dtype: str, shape) -> T:
+        return self.op1("Recv", [ix], {"channel": channel, "peer": peer, "dtype": dtype,
+                                       "shape": tuple(shape)})
     def reduce_sum(self, a): return self.op1("ReduceSum", [a])
 
     # ---- cond -------------------------------------------------------

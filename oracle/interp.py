@@ -135,13 +135,17 @@ class Trace:
         self.fires = 0
         self.dead_fires = 0
         self.live_merge_dead_inputs = 0   # a loop Merge that received a dead token
+        self.sends = 0
+        self.recvs = 0
         self.push_log: List[Tuple[int, Tuple]] = []
         self.pop_log: List[Tuple[int, Tuple]] = []
 
 
 class Interpreter:
-    def __init__(self, g: Graph, K_override: Optional[int] = None, sched_seed: Optional[int] = None):
+    def __init__(self, g: Graph, K_override: Optional[int] = None, sched_seed: Optional[int] = None,
+                 transport=None):
         self.g = g
+        self.transport = transport   # oracle.transport.*: Send/Recv between partitions
         self.K_override = K_override
         self.rng = random.Random(sched_seed) if sched_seed is not None else None
         self.cons = g.consumers()
@@ -434,6 +438,27 @@ class Interpreter:
                 # "first NextIteration starts N+1" transition is not lost
                 fr.parked[it].extend(targets)
             return
+        # ---------------- Send / Recv: the is_dead signal crosses devices;
+        # a Recv "is always ready" and takes whatever its Send delivered for this tag
+        if op in ("Send", "Recv"):
+            if self.transport is None:
+                raise InterpError("CF_E_UNSUPPORTED", f"{op} without a transport")
+            key = tuple(it for _, it in tag)
+            peer, ch = n.attrs["peer"], n.attrs["channel"]
+            if op == "Send":
+                v, ix = ins
+                dead = ctrl_dead or v.dead or ix.dead
+                self.transport.send(peer, ch, key, None if dead else np.array(v.value, copy=True), dead,
+                                    tuple(self.g.shape(n.inputs[0])))
+                tr.sends += 1
+                self._emit_ctrl(n.id, dead, tag)
+                return
+            val, mdead = self.transport.recv(peer, ch, key, tuple(n.attrs["shape"]))
+            dead = ctrl_dead or ins[0].dead or mdead
+            tr.recvs += 1
+            self._emit(n.id, 0, Token(None if dead else val, dead, tag))
+            self._emit_ctrl(n.id, dead, tag)
+            return
         # ---------------- non-control ops: dead propagation
         dead = ctrl_dead or any(t.dead for t in ins)
         nout = len(n.out_dtypes)
@@ -500,7 +525,8 @@ class Interpreter:
         return kernels.eval_op(op, vals, a)
 
 
-def run(g: Graph, feeds, fetches, K_override=None, sched_seed=None, return_trace=False):
-    it = Interpreter(g, K_override, sched_seed)
+def run(g: Graph, feeds, fetches, K_override=None, sched_seed=None, return_trace=False,
+        transport=None):
+    it = Interpreter(g, K_override, sched_seed, transport)
     vals = it.run(feeds, fetches)
     return (vals, it.trace) if return_trace else vals

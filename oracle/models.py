@@ -35,28 +35,49 @@ class RNNProgram:
     L: int
 
 
+def layer_partition(L: int, world: int, rank: int):
+    """Layers of pipeline stage `rank` (contiguous, balanced; reading R18 of DESIGN.md)."""
+    if not 1 <= world <= L:
+        raise ValueError(f"cannot split {L} layers over {world} stages")
+    base, extra = divmod(L, world)
+    l0 = rank * base + min(rank, extra)
+    return l0, l0 + base + (1 if rank < extra else 0)
+
+
 def dynamic_rnn_lstm(T_: int, B: int, I: int, H: int, L: int = 1, parallel_iterations: int = 32,
                      length_conds: bool = True, moe: bool = False, forget_bias: float = 0.0,
-                     with_grads: bool = True) -> RNNProgram:
+                     with_grads: bool = True, stage=None) -> RNNProgram:
+    """The full model, or with ``stage=(rank, world)`` the partition of pipeline stage `rank`
+    (layers ``layer_partition(L, world, rank)``): the layer input of a later stage is a Recv of
+    the previous stage's top output and a non-final stage Sends its top output on, inside the
+    loop at every iteration (§4.4). Each stage keeps its
+    own copy of the loop control: the loop and cond predicates depend only on the counter and
+    the fed lengths, so every partition computes them itself (reading R18). The stage loss is
+    the part of y owned by the stage; the stage losses sum to the full model's y."""
+    rank, world = stage if stage is not None else (0, 1)
+    l0, l1 = layer_partition(L, world, rank)
+    first, last = rank == 0, rank == world - 1
+    Ls = list(range(l0, l1))
+    n = len(Ls)
     b = Builder()
-    x = b.placeholder("x", FLOAT, (T_, B, I))
+    x = b.placeholder("x", FLOAT, (T_, B, I)) if first else None
     lens = b.placeholder("len", INT, (B,))
-    Ws, bs, h0, c0, WA, WB = [], [], [], [], [], []
-    for l in range(L):
+    Ws, bs, h0, c0, WA, WB = {}, {}, {}, {}, {}, {}
+    for l in Ls:
         il = I if l == 0 else H
-        Ws.append(b.placeholder(f"W{l}", FLOAT, (4 * H, il + H)))
-        bs.append(b.placeholder(f"b{l}", FLOAT, (4 * H,)))
-        h0.append(b.placeholder(f"h0_{l}", FLOAT, (B, H)))
-        c0.append(b.placeholder(f"c0_{l}", FLOAT, (B, H)))
+        Ws[l] = b.placeholder(f"W{l}", FLOAT, (4 * H, il + H))
+        bs[l] = b.placeholder(f"b{l}", FLOAT, (4 * H,))
+        h0[l] = b.placeholder(f"h0_{l}", FLOAT, (B, H))
+        c0[l] = b.placeholder(f"c0_{l}", FLOAT, (B, H))
         if moe:
-            WA.append(b.placeholder(f"WA{l}", FLOAT, (H, H)))
-            WB.append(b.placeholder(f"WB{l}", FLOAT, (H, H)))
+            WA[l] = b.placeholder(f"WA{l}", FLOAT, (H, H))
+            WB[l] = b.placeholder(f"WB{l}", FLOAT, (H, H))
     route_ta = None
     if moe:
         route = b.placeholder("route", BOOL, (T_, L))
         route_ta = b.tensor_array(T_, BOOL, (L,)).unstack(route)
-    x_ta = b.tensor_array(T_, FLOAT, (B, I)).unstack(x)
-    out_tas = [b.tensor_array(T_, FLOAT, (B, H)) for _ in range(L)]
+    x_ta = b.tensor_array(T_, FLOAT, (B, I)).unstack(x) if first else None
+    out_tas = [b.tensor_array(T_, FLOAT, (B, H)) for _ in Ls]
     max_len = b.op1("ReduceMax", [lens])
     min_len = b.op1("ReduceMin", [lens])
     t_bound = b.const(T_, INT)
@@ -65,14 +86,14 @@ def dynamic_rnn_lstm(T_: int, B: int, I: int, H: int, L: int = 1, parallel_itera
         return b.less(t, t_bound)
 
     def body(t, *vs):
-        hs, cs, flows = vs[:L], vs[L:2 * L], vs[2 * L:3 * L]
-        x_t = x_ta.read(t)
+        hs, cs, flows = vs[:n], vs[n:2 * n], vs[2 * n:3 * n]
+        x_t = x_ta.read(t) if first else b.recv(t, rank - 1, rank - 1, FLOAT, (B, H))
         r_t = route_ta.read(t) if moe else None
 
         def cells(masked):
             inp, outs, nh, nc = x_t, [], [], []
-            for l in range(L):
-                ins = [inp, hs[l], cs[l], Ws[l], bs[l]] + ([t, lens] if masked else [])
+            for k, l in enumerate(Ls):
+                ins = [inp, hs[k], cs[k], Ws[l], bs[l]] + ([t, lens] if masked else [])
                 hn, cn, o, _g = b.op("LSTMCell", ins, {"masked": masked, "forget_bias": forget_bias})
                 if moe:
                     r = b.op1("Reshape", [b.op1("Slice", [r_t], {"begin": (l,), "size": (1,)})],
@@ -92,32 +113,39 @@ def dynamic_rnn_lstm(T_: int, B: int, I: int, H: int, L: int = 1, parallel_itera
                 return b.cond(b.less(t, min_len), lambda: cells(False), lambda: cells(True))
 
             def empty_update():
-                return [b.zeros((B, H)) for _ in range(L)] + list(hs) + list(cs)
+                return [b.zeros((B, H)) for _ in Ls] + list(hs) + list(cs)
             res = b.cond(b.less(t, max_len), cell_branch, empty_update)
         else:
             res = cells(True)
-        outs, nh, nc = res[:L], res[L:2 * L], res[2 * L:]
-        nf = [out_tas[l].with_flow(flows[l]).write(t, outs[l]).flow for l in range(L)]
+        outs, nh, nc = res[:n], res[n:2 * n], res[2 * n:]
+        if not last:
+            b.send(outs[-1], t, rank, rank + 1)
+        nf = [out_tas[k].with_flow(flows[k]).write(t, outs[k]).flow for k in range(n)]
         return [b.add(t, b.const(1, INT))] + nh + nc + nf
 
-    res = b.while_loop(pred, body, [b.const(0, INT)] + h0 + c0 + [ta.flow for ta in out_tas],
-                       parallel_iterations, name="rnn")
-    hT, cT, fT = res[1:1 + L], res[1 + L:1 + 2 * L], res[1 + 2 * L:]
-    out_top = out_tas[L - 1].with_flow(fT[L - 1]).stack()
-    R_out = b.placeholder("R_out", FLOAT, (T_, B, H))
-    y = b.reduce_sum(b.mul(R_out, out_top))
-    for l in range(L):
+    res = b.while_loop(pred, body, [b.const(0, INT)] + [h0[l] for l in Ls] + [c0[l] for l in Ls]
+                       + [ta.flow for ta in out_tas], parallel_iterations, name="rnn")
+    hT, cT, fT = res[1:1 + n], res[1 + n:1 + 2 * n], res[1 + 2 * n:]
+    y = None
+    fetch = {}
+    if last:
+        out_top = out_tas[n - 1].with_flow(fT[n - 1]).stack()
+        R_out = b.placeholder("R_out", FLOAT, (T_, B, H))
+        y = b.reduce_sum(b.mul(R_out, out_top))
+        fetch["out"] = out_top
+    for k, l in enumerate(Ls):
         Rh = b.placeholder(f"R_h{l}", FLOAT, (B, H))
         Rc = b.placeholder(f"R_c{l}", FLOAT, (B, H))
-        y = b.add(y, b.add(b.reduce_sum(b.mul(Rh, hT[l])), b.reduce_sum(b.mul(Rc, cT[l]))))
-    fetch = {"y": y, "out": out_top}
-    for l in range(L):
-        fetch[f"hT{l}"] = hT[l]
-        fetch[f"cT{l}"] = cT[l]
+        yl = b.add(b.reduce_sum(b.mul(Rh, hT[k])), b.reduce_sum(b.mul(Rc, cT[k])))
+        y = yl if y is None else b.add(y, yl)
+    fetch = {"y": y, **fetch}
+    for k, l in enumerate(Ls):
+        fetch[f"hT{l}"] = hT[k]
+        fetch[f"cT{l}"] = cT[k]
     grads = {}
     if with_grads:
-        names, xs = ["x"], [x]
-        for l in range(L):
+        names, xs = (["x"], [x]) if first else ([], [])
+        for l in Ls:
             names += [f"W{l}", f"b{l}", f"h0_{l}", f"c0_{l}"]
             xs += [Ws[l], bs[l], h0[l], c0[l]]
             if moe:
@@ -129,12 +157,40 @@ def dynamic_rnn_lstm(T_: int, B: int, I: int, H: int, L: int = 1, parallel_itera
 
 
 def run_program(p: RNNProgram, feeds: Dict[str, np.ndarray], K=None, sched_seed=None,
-                return_trace=False):
+                return_trace=False, transport=None):
     from . import interp
     names = list(p.fetch) + list(p.grads)
     tensors = [p.fetch[n] for n in p.fetch] + [p.grads[n] for n in p.grads]
+    feeds = {k: v for k, v in feeds.items() if k in p.b.g.placeholders}
     r = interp.run(p.b.g, feeds, tensors, K_override=K, sched_seed=sched_seed,
-                   return_trace=return_trace)
+                   return_trace=return_trace, transport=transport)
     vals, tr = (r if return_trace else (r, None))
     out = dict(zip(names, vals))
     return (out, tr) if return_trace else out
+
+
+def run_pipeline_threads(T_, B, I, H, L, world, feeds, K=None, sched_seed=None, **kw):
+    """All stages of the layer pipeline in one process, one thread per stage, Send/Recv through
+    an in-process mailbox (test helper). Returns per-stage (results, trace)."""
+    import threading
+
+    from .transport import Mailbox
+    mb = Mailbox()
+    res = [None] * world
+    errs = []
+
+    def work(r):
+        try:
+            p = dynamic_rnn_lstm(T_, B, I, H, L, stage=(r, world), **kw)
+            res[r] = run_program(p, feeds, K=K, sched_seed=sched_seed, return_trace=True,
+                                 transport=mb.port(r))
+        except Exception as e:  # noqa: BLE001 -- surfaced to the caller below
+            errs.append(e)
+    th = [threading.Thread(target=work, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    if errs:
+        raise errs[0]
+    return res
