@@ -86,7 +86,11 @@ cf_status cf_const(cf_graph* g, int32_t dtype, int32_t rank, const int64_t* shap
 /* Generic op. op names: Identity Add Sub Mul Neg AddN MatMul Transpose ReduceSum ReduceMax
  * ReduceMin BiasAdd Fill ZerosLike Less LessEqual Greater Equal LogicalAnd LogicalNot Select
  * Sigmoid Tanh Relu ReluGrad Concat Slice Reshape Cast LSTMCell LSTMCellGrad StackCreate
- * StackPush StackPop. attrs: "key=value;key=v1,v2" (ints, floats, bools as 0/1).
+ * StackPush StackPop Send Recv. attrs: "key=value;key=v1,v2" (ints, floats, bools as 0/1).
+ * Send(value, ix; channel, peer) / Recv(ix; channel, peer, dtype, shape): one edge of a program
+ * partitioned across GPUs (§4.4). The message key is (channel, iteration of
+ * the enclosing loop); a dead Send delivers the is_dead signal. Gradients:
+ * grad(Send) = Recv and grad(Recv) = Send on channel ^ (1 << 20) (the mirrored edge).
  * External inputs are captured automatically: Enter into loop bodies, Switch into cond
  * branches, "one Switch for each external tensor".
  * *n_out receives the number of outputs written to out (capacity 8). */
@@ -179,6 +183,7 @@ typedef struct {
   uint8_t* branch_bits;         /* caller buffer or NULL: per (cond, iteration) taken bit */
   int32_t branch_bits_cap;
   double wall_ms;               /* device time of the run (CUDA events)                 */
+  int64_t sends, recvs;         /* cross-GPU messages sent / received, live or dead (a14)  */
 } cf_trace;
 
 /* Compile the graph for the device (placement of every value, lowering to the device
@@ -198,6 +203,30 @@ cf_status cf_session_fetch_dtype(const cf_session* s, int32_t i, int32_t* dtype)
 /* Human-readable summary of the compiled program (node kinds, placements, bytes). */
 cf_status cf_session_describe(const cf_session* s, char* buf, size_t cap);
 void cf_session_destroy(cf_session* s);
+
+/* ---- multi-GPU layer pipeline ---------------------
+ * A graph holding Send/Recv nodes is one partition of a program split across GPUs, one
+ * process per GPU. Every Send/Recv is one half of a channel; the session keeps its halves in
+ * one device allocation: the receiving half holds `slots` payload slots + 64-bit flags written
+ * by the sender over NVLink, the sending half holds 64-bit acks + a "run done" word written
+ * by the receiver. slots = parallel_iterations + 1 of the enclosing loop.
+ *
+ * cf_session_channels: this session's halves, 7 int64 per row: channel, role (0 = receives,
+ *   1 = sends), peer rank, slots, payload bytes, device dtype, byte offset in the allocation.
+ *   *n = number of rows (rows beyond cap are not written; table may be NULL).
+ * cf_session_ipc_handle: the allocation's cudaIpcMemHandle_t (CF_IPC_HANDLE_BYTES bytes,
+ *   zeros if the session has no channel).
+ * cf_session_connect: import a peer's handle + table (exchanged by the caller, e.g. with
+ *   torch.distributed.all_gather_object) before the first cf_run. CF_E_UNSUPPORTED when the
+ *   peer lacks the mirrored half or the halves disagree (slots, payload bytes, dtype);
+ *   CF_E_CUDA when the handle cannot be opened (peers must be separate processes).
+ * cf_run on a session with an unconnected channel fails with CF_E_UNSUPPORTED. All partitions
+ * must call cf_run the same number of times (run epochs tag the messages). */
+#define CF_IPC_HANDLE_BYTES 64
+cf_status cf_session_channels(const cf_session* s, int32_t cap, int64_t* table, int32_t* n);
+cf_status cf_session_ipc_handle(const cf_session* s, void* handle);
+cf_status cf_session_connect(cf_session* s, int32_t peer, const void* handle, int32_t n,
+                             const int64_t* table);
 
 #ifdef __cplusplus
 }

@@ -56,7 +56,7 @@ class cf_trace(C.Structure):
                 ("max_depth", C.c_int32), ("exit_fires", C.c_int32), ("instances", C.c_int64),
                 ("tiles", C.c_int64), ("dead_skipped", C.c_int64), ("n_branch_bits", C.c_int32),
                 ("branch_bits", C.POINTER(C.c_uint8)), ("branch_bits_cap", C.c_int32),
-                ("wall_ms", C.c_double)]
+                ("wall_ms", C.c_double), ("sends", C.c_int64), ("recvs", C.c_int64)]
 
 
 PRED_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_int32, C.POINTER(cf_tensor),
@@ -66,6 +66,8 @@ BODY_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_int32, C.POINTER(cf_tensor),
 BRANCH_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_int32, C.POINTER(cf_tensor), C.c_void_p)
 
 _P = C.c_void_p
+IPC_HANDLE_BYTES = 64
+GRAD_CHANNEL = 1 << 20
 _sig = {
     "cf_last_error": (C.c_char_p, []),
     "cf_version": (C.c_char_p, []),
@@ -107,6 +109,9 @@ _sig = {
     "cf_session_fetch_dtype": (C.c_int32, [_P, C.c_int32, C.POINTER(C.c_int32)]),
     "cf_session_describe": (C.c_int32, [_P, C.c_char_p, C.c_size_t]),
     "cf_session_destroy": (None, [_P]),
+    "cf_session_channels": (C.c_int32, [_P, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int32)]),
+    "cf_session_ipc_handle": (C.c_int32, [_P, C.c_void_p]),
+    "cf_session_connect": (C.c_int32, [_P, C.c_int32, C.c_void_p, C.c_int32, C.POINTER(C.c_int64)]),
     # include/cf_debug.h (test hooks)
     "cf_debug_session_profile": (C.c_int32, [_P, C.c_void_p, C.c_int64, C.POINTER(C.c_int64),
                                              C.c_void_p]),
@@ -335,6 +340,15 @@ class Graph:
         _check(st)
         return [self._t(outs[i]) for i in range(n_out)]
 
+    # cross-GPU edges of a partitioned program; channel ^ GRAD_CHANNEL is
+    # the mirrored gradient edge
+    def send(self, v: Tensor, ix: Tensor, channel: int, peer: int) -> None:
+        self.op("Send", [v, ix], {"channel": channel, "peer": peer})
+
+    def recv(self, ix: Tensor, channel: int, peer: int, dtype: int, shape: Sequence[int]) -> Tensor:
+        return self.op1("Recv", [ix], {"channel": channel, "peer": peer, "dtype": dtype,
+                                       "shape": list(shape)})
+
     def tensor_array(self, size: int, dtype: int, elem_shape: Sequence[int]) -> TensorArray:
         sh = (C.c_int64 * max(len(elem_shape), 1))(*elem_shape)
         h, f = cf_tensor(), cf_tensor()
@@ -435,6 +449,42 @@ class Session:
         self.driver_ops = [(int(t[2 + k]), int(t[34 + k])) for k in range(32)]
         return out, (float(t[0]), float(t[1]))
 
+    # ---- multi-GPU pipeline (include/cf.h "multi-GPU layer pipeline")
+    def channels(self):
+        """This session's channel halves: list of (channel, role, peer, slots, bytes, dtype,
+        offset); role 0 = receives, 1 = sends."""
+        n = C.c_int32()
+        _check(_lib.cf_session_channels(self.h, 0, None, C.byref(n)))
+        tab = (C.c_int64 * max(7 * n.value, 1))()
+        _check(_lib.cf_session_channels(self.h, n.value, tab, C.byref(n)))
+        return [tuple(tab[7 * i + k] for k in range(7)) for i in range(n.value)]
+
+    def ipc_handle(self) -> bytes:
+        buf = C.create_string_buffer(IPC_HANDLE_BYTES)
+        _check(_lib.cf_session_ipc_handle(self.h, buf))
+        return buf.raw
+
+    def connect(self, peer: int, handle: bytes, table) -> None:
+        flat = [int(v) for row in table for v in row]
+        tab = (C.c_int64 * max(len(flat), 1))(*flat)
+        _check(_lib.cf_session_connect(self.h, peer, C.c_char_p(handle), len(table), tab))
+
+    def connect_pipeline(self, group=None) -> None:
+        """Exchange channel memory with every other rank through torch.distributed (any
+        backend) and connect the peers this partition talks to."""
+        import torch.distributed as dist
+        mine = (dist.get_rank(group), self.ipc_handle(), self.channels())
+        allv = [None] * dist.get_world_size(group)
+        dist.all_gather_object(allv, mine, group=group)
+        peers = {c[2] for c in mine[2]}
+        for rank, handle, table in allv:
+            if rank in peers:
+                self.connect(rank, handle, table)
+
+    def has_feed(self, name: str) -> bool:
+        d = C.c_int32()
+        return _lib.cf_session_feed_dtype(self.h, name.encode(), C.byref(d)) == 0
+
     def feed_dtype(self, name: str) -> int:
         d = C.c_int32()
         _check(_lib.cf_session_feed_dtype(self.h, name.encode(), C.byref(d)))
@@ -496,6 +546,7 @@ class Session:
                 "pushes": tr.pushes, "pops": tr.pops, "max_depth": tr.max_depth,
                 "exit_fires": tr.exit_fires, "instances": tr.instances, "tiles": tr.tiles,
                 "dead_skipped": tr.dead_skipped, "wall_ms": tr.wall_ms,
+                "sends": tr.sends, "recvs": tr.recvs,
                 "n_branch_bits": tr.n_branch_bits,
                 "branch_bits": bytes(bits)[:min(branch_cap, tr.n_branch_bits)] if bits else b"",
             }

@@ -183,8 +183,18 @@ class AD {
     std::vector<int> topo;
     items(ctx, &its, &topo);
     std::set<TRef> from_wrt(wrt.begin(), wrt.end());
+    // Send/Recv pairs carry the dependence across partitions: a Recv's value depends on the
+    // peer's parameters, and every Send/Recv gets its mirrored gradient message, so items
+    // holding one are never pruned (the peer would wait forever otherwise).
+    std::vector<char> comm(its.size(), 0), recv(its.size(), 0);
+    for (size_t k = 0; k < its.size(); ++k)
+      for (int id : its[k].nodes) {
+        const std::string& o = g_.nodes[id].op;
+        if (o == "Send" || o == "Recv") comm[k] = 1;
+        if (o == "Recv") recv[k] = 1;
+      }
     for (int k : topo) {
-      bool hit = false;
+      bool hit = recv[k] != 0;
       for (auto& t : its[k].inputs) hit |= from_wrt.count(t) > 0;
       if (hit) from_wrt.insert(its[k].outputs.begin(), its[k].outputs.end());
     }
@@ -204,8 +214,8 @@ class AD {
           g_outs.push_back(TRef{});
         }
       }
-      if (!any) continue;
-      bool reach = false;
+      if (!any && !comm[*r]) continue;
+      bool reach = comm[*r] != 0;
       for (auto& t : it.inputs) reach |= from_wrt.count(t) > 0;
       if (!reach) continue;
       std::vector<std::pair<TRef, TRef>> pairs;
@@ -251,7 +261,9 @@ class AD {
         if (differentiable(g_.dtype(e)) &&
             std::find(externals.begin(), externals.end(), e) == externals.end())
           externals.push_back(e);
-    if (externals.empty()) return {};
+    bool has_comm = false;
+    for (int id : it.nodes) has_comm |= g_.nodes[id].op == "Send" || g_.nodes[id].op == "Recv";
+    if (externals.empty() && !has_comm) return {};
     TRef pred_g = fwd(pred);
     std::vector<const Node*> merges;
     for (auto& o : it.outputs) merges.push_back(&g_.nodes[o.node]);
@@ -363,6 +375,23 @@ class AD {
       return g_.constant(F32, {}, &v);
     };
     if (op == "Identity" || op == "Cast") return {g};
+    if (op == "Send") {
+      // the gradient of a sent value comes back from the receiver on the mirrored edge
+      Attrs a;
+      a.set("channel", n.attrs.i("channel") ^ kGradChannel);
+      a.set("peer", n.attrs.i("peer"));
+      a.set("dtype", g_.dtype(in[0]));
+      a.setv("shape", g_.shape(in[0]));
+      return {g_.op1("Recv", {fwd(in[1])}, a), TRef{}};
+    }
+    if (op == "Recv") {
+      TRef gv = g.valid() ? g : zeros_like(out);
+      Attrs a;
+      a.set("channel", n.attrs.i("channel") ^ kGradChannel);
+      a.set("peer", n.attrs.i("peer"));
+      g_.op("Send", {gv, fwd(in[0])}, a);
+      return none;
+    }
     static const std::set<std::string> nograd = {
         "StopGradient", "Placeholder", "Const", "ZerosLike", "Less", "LessEqual", "Greater",
         "Equal", "LogicalAnd", "LogicalNot", "ReduceMax", "ReduceMin", "TACreate",

@@ -418,6 +418,10 @@ struct Compiler {
         d.op = OP_STACK_PUSH;
       } else if (op == "StackPop") {
         d.op = OP_STACK_POP;
+      } else if (op == "Send" || op == "Recv") {
+        d.op = op == "Send" ? OP_SEND : OP_RECV;
+        d.aux[0] = add_chan(n);
+        if (op == "Recv") heavy_nodes.push_back(n.id);   // output placed like a heavy output
       } else if (odt == FLOW) {
         d.op = OP_FLOW;
       } else if (acc_of_add.count(n.id)) {
@@ -486,7 +490,7 @@ struct Compiler {
       else root_heavy += k + 1;
     }
     for (auto& n : g.nodes)
-      if (n.op == "TAWrite" || n.op == "TAStack" || n.op == "TAUnstack") {
+      if (n.op == "TAWrite" || n.op == "TAStack" || n.op == "TAUnstack" || n.op == "Send") {
         int f = frame_of[n.id];
         if (f >= 0) frame_heavy[f] += 2;
         else root_heavy += 2;
@@ -517,6 +521,34 @@ struct Compiler {
     ds << "placements root=" << counts[0] << " ring=" << counts[1] << " arena=" << counts[2]
        << " ta=" << counts[3] << " acc=" << counts[4] << "\n";
     P.describe = ds.str();
+  }
+
+  // one half of a Send/Recv channel. Both partitions derive slots and payload bytes the same
+  // way (K + 1 slots of the enclosing loop, payload = value shape x device dtype); the runtime
+  // checks that the halves agree when the peers connect.
+  int add_chan(const Node& n) {
+    const bool send = n.op == "Send";
+    ChanPlan c;
+    c.channel = (int32_t)n.attrs.i("channel");
+    c.role = send ? 1 : 0;
+    c.peer = (int32_t)n.attrs.i("peer");
+    c.frame = frame_of[n.id];
+    for (auto& o : P.chans)
+      if (o.channel == c.channel && o.role == c.role)
+        unsupported(n, "channel " + std::to_string(c.channel) + " used twice in one partition");
+    int K = 0;
+    if (c.frame >= 0) K = o.parallel_iterations > 0 ? o.parallel_iterations : g.ctxs[frame_ctx[c.frame]].K;
+    c.slots = K + 1;
+    int v = send ? vid(n.in[0]) : vbase[n.id];
+    c.dt = vdt[v];
+    const Shape& sh = send ? g.shape(n.in[0]) : n.osh[0];
+    c.elem_bytes = numel(sh) * dev_size(c.dt);
+    const int64_t flags = ((int64_t)c.slots * 8 + 255) / 256 * 256;
+    c.bytes = send ? flags + 256 : flags + (int64_t)c.slots * ((c.elem_bytes + 255) / 256 * 256);
+    c.offset = P.chan_bytes;
+    P.chan_bytes += c.bytes;
+    P.chans.push_back(c);
+    return (int)P.chans.size() - 1;
   }
 
   void lower_heavy(const Node& n, DNode& d) {
@@ -822,7 +854,7 @@ struct Compiler {
     // arena allocation needs the bound
     for (int i = 0; i < N; ++i) {
       const DNode& d = P.nodes[i];
-      if (d.op != OP_HEAVY) continue;
+      if (d.op != OP_HEAVY && d.op != OP_RECV) continue;
       int f = frame_of[i];
       int np = n_places(g.nodes[i]);
       for (int p = 0; p < np; ++p) {

@@ -30,6 +30,13 @@ struct FetchInfo {
   int64_t bytes = 0;
 };
 
+// one half of a cross-GPU channel (program.h DChan); offset into the session's channel memory
+struct ChanPlan {
+  int32_t channel = 0, role = 0, peer = 0, slots = 1, dt = 0, frame = -1;
+  int64_t elem_bytes = 0;
+  int64_t offset = 0, bytes = 0;
+};
+
 struct HostProgram {
   std::vector<cfdev::DNode> nodes;
   std::vector<int32_t> in_vids;
@@ -57,6 +64,8 @@ struct HostProgram {
   int64_t inst_bound = 0;            // upper bound of heavy instances per run
   int64_t tile_bound = 0;            // max tiles of one instance
   std::vector<BufPlan> bufs;
+  std::vector<ChanPlan> chans;
+  int64_t chan_bytes = 0;
   std::map<std::string, FeedInfo> feeds;
   std::vector<FetchInfo> fetches;
   std::string describe;

@@ -232,6 +232,21 @@ void infer(const Graph& g, const std::string& op, const std::vector<TRef>& in, c
   if (op == "StackCreate") return out1(RES, {});
   if (op == "StackPush") { need(2); odt->clear(); osh->clear(); return; }
   if (op == "StackPop") { need(1); return out1((int32_t)a.i("dtype"), a.v("elem_shape")); }
+  // cross-partition edges: message key = (channel, iteration tag)
+  if (op == "Send") {
+    need(2);
+    if (dt[1] != I64 || !sh[1].empty()) throw CfError(CF_E_DTYPE, "Send index must be an int64 scalar");
+    if (!a.has("channel") || !a.has("peer")) throw CfError(CF_E_ARITY, "Send needs channel and peer");
+    odt->clear();
+    osh->clear();
+    return;
+  }
+  if (op == "Recv") {
+    need(1);
+    if (dt[0] != I64 || !sh[0].empty()) throw CfError(CF_E_DTYPE, "Recv index must be an int64 scalar");
+    if (!a.has("channel") || !a.has("peer")) throw CfError(CF_E_ARITY, "Recv needs channel and peer");
+    return out1((int32_t)a.i("dtype"), a.v("shape"));
+  }
   throw CfError(CF_E_UNSUPPORTED, "unknown op " + op);
 }
 

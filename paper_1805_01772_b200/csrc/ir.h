@@ -58,6 +58,9 @@ struct Attrs {
 
 enum CtxKind { ROOT = 0, WHILE = 1, COND = 2 };
 
+// channel id of the gradient edge mirroring a Send/Recv edge
+constexpr int64_t kGradChannel = 1 << 20;
+
 struct LoopVar { int enter = -1, merge = -1, sw = -1, next = -1, exit = -1; };
 
 struct Ctx {

@@ -49,6 +49,8 @@ enum Op : int32_t {
   OP_STACK_POP,
   OP_HEAVY,         // aux0: heavy kind (HK_*), aux1: sub-op / flags
   OP_ACC,           // fused accumulator Add (aux0: acc id): output = the accumulator buffer
+  OP_SEND,          // cross-GPU Send (aux0: channel index)
+  OP_RECV,          // cross-GPU Recv (aux0: channel index); output placed like a heavy output
   OP__COUNT
 };
 
@@ -161,6 +163,23 @@ struct DStack {
 };
 
 // Root program step: a node id (>= 0) or a frame (-(frame + 1)).
+// ---- cross-GPU channel (one Send/Recv edge). Each session holds one
+// half of the channel in its IPC-exported channel memory:
+//   receiving half: flags[slots] (u64) + data[slots][elem_bytes]   (written by the sender)
+//   sending half:   acks[slots]  (u64) + done (u64)                  (written by the receiver)
+// flag = epoch << 32 | (2 * (iter + 1) + dead); ack = epoch << 32 | (iter + 1); done = epoch of
+// the receiver's last finished run. Message slot = iter % slots.
+struct DChan {
+  int32_t channel, role;     // role 0: this session receives, 1: sends
+  int32_t peer, slots;
+  int64_t elem_bytes;
+  int32_t dt, frame;
+  unsigned long long* flags;        // receiving half (local)  | sending half: peer's flags
+  uint8_t* data;                    // receiving half (local)  | sending half: peer's data
+  unsigned long long* acks;         // sending half (local)    | receiving half: peer's acks
+  unsigned long long* done;         // sending half (local)    | receiving half: peer's done
+};
+
 struct Prog {
   int32_t n_nodes, n_vids, n_frames, n_tas, n_stacks;
   int32_t n_root_steps;
@@ -187,7 +206,8 @@ struct Prog {
   int32_t max_body, max_bi;     // largest body (nodes, input ids)
   int32_t n_places, iter_counters;
   int32_t precision;            // 3 = f32 SIMT, 5 = bf16 tcgen05
-  int32_t pad2;
+  int32_t n_chans;
+  const DChan* chans;
 };
 
 // ---- heavy instance record (written by the driver, read by workers)
@@ -199,6 +219,8 @@ struct Inst {
   int64_t p[20];        // pointers (p[13] = primary output for generic kinds)
   int64_t s[8];         // scalars
   int64_t dts;          // device dtypes: input j at bits [4j, 4j+4), output at [32, 36)
+  unsigned long long* signal;        // optional: written (release, system scope) with
+  unsigned long long signal_value;   // signal_value when the last tile completes
 };
 
 // ---- run-time state shared by the driver CTA and the worker CTAs
@@ -218,6 +240,7 @@ struct RunState {
   int32_t trip[16];
   int32_t max_inflight[16];
   long long pushes, pops;
+  long long sends, recvs;
   int32_t max_depth, exit_fires;
   long long instances, tiles, dead_skipped;
   unsigned long long t_start, t_end;
@@ -263,6 +286,7 @@ struct RunArgs {
   int32_t* prep_inst;        // [n_nodes] per-run weight-prep instance of LSTM nodes (-1)
   int32_t* acc_writer;       // [n_accs] latest instance writing each accumulator
   const uint8_t* vdt;        // [n_vids] device dtype of every value
+  unsigned long long epoch;  // run counter (channel message tags)
 };
 
 }  // namespace cfdev

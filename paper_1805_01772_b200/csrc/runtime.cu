@@ -60,6 +60,15 @@ __device__ __forceinline__ int ld_acquire_i32(const int* p) {
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+// system scope: channel words written by / read from the peer GPU over NVLink
+__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 __device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
   asm volatile("st.release.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
@@ -200,7 +209,13 @@ __device__ void tile_copy(const Inst& I, int tile) {
   const uint8_t* src = (const uint8_t*)I.p[0];
   uint8_t* dst = (uint8_t*)I.p[13];
   bool aligned = ((I.p[0] | I.p[13]) & 15) == 0;
-  if (aligned) {
+  if (aligned && I.sub == 1) {
+    // channel slot written by the peer GPU: bypass L1 (a stale line of an earlier message
+    // in the same slot could otherwise be returned)
+    int64_t v0 = b0 / 16, v1 = e1 / 16;
+    for (int64_t e = v0 + threadIdx.x; e < v1; e += kThreads) ((int4*)dst)[e] = __ldcv((const int4*)src + e);
+    for (int64_t e = v1 * 16 + threadIdx.x; e < e1; e += kThreads) dst[e] = src[e];
+  } else if (aligned) {
     int64_t v0 = b0 / 16, v1 = e1 / 16;
     int64_t e = v0 + threadIdx.x;
     for (; e + 3 * kThreads < v1; e += 4 * kThreads) {
@@ -487,7 +502,7 @@ struct Driver {
   int32_t* acc_writer_;
   int32_t* iter_out_;
   const DStack* stacks_;
-  long long n_push = 0, n_pop = 0, n_dead = 0, n_inst = 0, n_tiles = 0;
+  long long n_push = 0, n_pop = 0, n_dead = 0, n_inst = 0, n_tiles = 0, n_sent = 0, n_recv = 0;
   long long op_cnt[32] = {}, op_cyc[32] = {};
   int32_t max_depth = 0, n_exitf = 0;
   Tok* toks_;            // token table: driver-CTA shared memory when it fits, else global
@@ -626,6 +641,7 @@ struct Driver {
     for (int j = 0; j < 14; ++j) I.p[j] = 0;
     for (int j = 0; j < 4; ++j) I.s[j] = 0;
     I.n = I.m = I.k = 0;
+    I.signal = nullptr;
     if (A.prof) {
       unsigned long long* pr = A.prof + 6 * (int64_t)id;
       pr[0] = globaltimer();
@@ -1099,16 +1115,71 @@ struct Driver {
     return EV_OK;
   }
 
-  __noinline__ __device__ int32_t copy_inst(int64_t dst, int64_t src, int64_t bytes, int32_t dep) {
-    int32_t id = new_inst(HK_COPY, 0, (int)((bytes + 65535) / 65536));
+  __noinline__ __device__ int32_t copy_inst(int64_t dst, int64_t src, int64_t bytes, int32_t dep,
+                                            unsigned long long* signal = nullptr,
+                                            unsigned long long signal_value = 0, int sub = 0) {
+    int32_t id = new_inst(HK_COPY, sub, (int)((bytes + 65535) / 65536));
     if (id < 0) return -1;
     Inst& I = A.insts[id];
     I.n = bytes;
     I.p[0] = src;
     I.p[13] = dst;
+    I.signal = signal;
+    I.signal_value = signal_value;
     add_dep(id, dep);
     submit(id);
     return id;
+  }
+
+  // ---------------------------------------------------------------- channels (a14)
+  // Send / Recv of iteration `it` over channel slot it % slots: the
+  // payload moves GPU -> GPU by a copy instance whose workers store straight into the peer's
+  // slot over NVLink; the last tile publishes the flag (release, system scope). The dead
+  // signal is a flag with the low bit set and no payload.
+  __noinline__ __device__ int eval_send(const DNode& d, bool dead) {
+    const DChan& C = P.chans[d.aux[0]];
+    const int it = cur_frame >= 0 ? iter : 0;
+    const int slot = it % C.slots;
+    const unsigned long long ep = A.epoch << 32;
+    if (it >= C.slots) {   // slot still holds message it - slots until the receiver acks it
+      const unsigned long long need = ep | (unsigned long long)(it - C.slots + 1);
+      if (ld_acquire_sys_u64(&C.acks[slot]) < need) return EV_BLOCKED;
+    }
+    const int64_t stride = (C.elem_bytes + 255) / 256 * 256;
+    n_sent++;
+    if (dead) {
+      st_release_sys_u64(&C.flags[slot], ep | (2ULL * (it + 1) + 1));
+      return EV_OK;
+    }
+    const Tok& v = in_tok(d, 0);
+    if (copy_inst((int64_t)(C.data + slot * stride), v.v, C.elem_bytes, v.writer, &C.flags[slot],
+                  ep | (2ULL * (it + 1))) < 0)
+      return EV_ERROR;
+    return EV_OK;
+  }
+  __noinline__ __device__ int eval_recv(const DNode& d, bool dead, bool* out_dead) {
+    const DChan& C = P.chans[d.aux[0]];
+    const int it = cur_frame >= 0 ? iter : 0;
+    const int slot = it % C.slots;
+    const unsigned long long ep = A.epoch << 32;
+    const unsigned long long live = ep | (2ULL * (it + 1));
+    const unsigned long long f = ld_acquire_sys_u64(&C.flags[slot]);
+    if (f != live && f != (live | 1)) return EV_BLOCKED;
+    n_recv++;
+    if (dead || f != live) {   // consume the message, propagate dead
+      st_release_sys_u64(&C.acks[slot], ep | (unsigned long long)(it + 1));
+      set_dead_all(d);
+      *out_dead = true;
+      return EV_OK;
+    }
+    int64_t out;
+    if (!place(d, 0, &out)) return st->error ? EV_ERROR : EV_BLOCKED;
+    const int64_t stride = (C.elem_bytes + 255) / 256 * 256;
+    int32_t id = copy_inst(out, (int64_t)(C.data + slot * stride), C.elem_bytes, -1, &C.acks[slot],
+                           ep | (unsigned long long)(it + 1), 1);
+    if (id < 0) return EV_ERROR;
+    set_out(d, 0, ptr_tok(out, id, C.dt));
+    return EV_OK;
   }
 
   // ---------------------------------------------------------------- node evaluation
@@ -1524,6 +1595,15 @@ struct Driver {
         res = eval_heavy(d, nid);
         break;
       }
+      case OP_SEND:
+        res = eval_send(d, dead);
+        break;
+      case OP_RECV: {
+        bool md = false;
+        res = eval_recv(d, dead, &md);
+        ctrl_dead |= md;
+        break;
+      }
       default:
         fail(CF_E_UNSUPPORTED, op);
         return EV_ERROR;
@@ -1607,6 +1687,7 @@ struct Driver {
       const int op = d->op;
       // token word w: dead (bits 0-7) | kind (8-15) | dt (16-23)
       if (op == OP_SWITCH && d->n_ctrl == 0) {
+        long long cs0 = prof ? clock64() : 0;
         const int4 dv = tk[iv[d->in_off]];
         const int4 pt = tk[iv[d->in_off + 1]];
         if (((pt.w >> 8) & 0xff) == TK_IMM || ((dv.w | pt.w) & 0xff)) {
@@ -1626,6 +1707,7 @@ struct Driver {
           tk[d->ctrl_vid] = make_int4(0, 0, -1, (TK_FLOW << 8) | dead);
           ++pc;
           progress = true;
+          if (prof) { op_cyc[30] += clock64() - cs0; op_cnt[30]++; }
           continue;
         }
       } else if (op == OP_MERGE) {
@@ -1778,12 +1860,27 @@ struct Driver {
   __device__ void run() {
     st->t_start = globaltimer();
     last_progress = st->t_start;
-    while (true) {
+    // a sending half may reuse its peer's slots only after the receiver finished the
+    // previous run (its `done` word carries that run's epoch)
+    for (int c = 0; c < P.n_chans; ++c) {
+      const DChan& C = P.chans[c];
+      if (C.role != 1) continue;
+      int spins = 0;
+      while (ld_acquire_sys_u64(C.done) + 1 < A.epoch) {
+        backoff(spins);
+        if ((long long)(globaltimer() - last_progress) > A.watchdog_ns) {
+          fail(CF_E_DEADLOCK, -1000 - c);
+          break;
+        }
+      }
+    }
+    last_progress = globaltimer();
+    while (!st->error) {
       long long ci = A.prof ? clock64() : 0;
       bool p = drain();
       if (st->error) break;
       p |= step();
-      if (A.prof && !p) { op_cyc[30] += clock64() - ci; op_cnt[30]++; }
+      (void)ci;
       if (st->error) break;
       if (fetched && cur_frame < 0 && root_pc >= P.n_root_steps && outstanding == 0) break;
       unsigned long long now = globaltimer();
@@ -1794,12 +1891,18 @@ struct Driver {
         break;
       }
     }
+    // receiving halves: every message of this run has been copied out of its slot
+    if (!st->error)
+      for (int c = 0; c < P.n_chans; ++c)
+        if (P.chans[c].role == 0) st_release_sys_u64(P.chans[c].done, A.epoch);
     for (int k = 0; k < 32; ++k) {
       st->op_count[k] = op_cnt[k];
       st->op_cycles[k] = op_cyc[k];
     }
     st->pushes = n_push;
     st->pops = n_pop;
+    st->sends = n_sent;
+    st->recvs = n_recv;
     st->dead_skipped = n_dead;
     st->instances = n_inst;
     st->tiles = n_tiles;
@@ -1901,6 +2004,7 @@ __device__ void worker_loop(const RunArgs& A) {
         atomicMax(&pr[3], t1);
         atomicAdd(&pr[4], t1 - t_tile0);
       }
+      if (I.signal) __threadfence_system();   // peer-visible stores before the count
       __threadfence();
       int old = atomicAdd(&A.inst_tiles_done[id], 1);
       s_last = (old == I.ntiles - 1);
@@ -1908,6 +2012,10 @@ __device__ void worker_loop(const RunArgs& A) {
     }
     __syncthreads();
     if (s_last) {
+      if (I.signal && threadIdx.x == 0) {
+        __threadfence_system();
+        st_release_sys_u64(I.signal, I.signal_value);
+      }
       if (I.kind == HK_REDUCE_SUM) {
         __threadfence();
         finalize_reduce_sum(I, sm);
@@ -2080,6 +2188,13 @@ struct cf_session {
   std::vector<CUtensorMap> maps_host;
   int n_reg_static = 0;
   std::vector<DReg> reg_sorted;   // per-run upload, sorted by base
+  // cross-GPU channels (a14): this session's halves live in one IPC-exported allocation
+  void* chan_mem = nullptr;
+  std::vector<DChan> chans;        // device view (remote pointers filled by cf_session_connect)
+  DChan* d_chans = nullptr;
+  bool chans_dirty = true;
+  std::map<int, void*> peer_mem;   // imported peer channel memory, by peer rank
+  unsigned long long epoch = 0;
 };
 
 namespace {
@@ -2204,6 +2319,34 @@ void build_session(cf_session* s, const cf::Graph& g, const cf_run_opts* o,
     pg.n_reg = n_static;
   }
   A.vdt = upload(s, P.vdt);
+  // ---- channel halves (a14): zeroed once; epochs keep runs apart
+  if (!P.chans.empty()) {
+    CUDA_OK(cudaMalloc(&s->chan_mem, (size_t)P.chan_bytes));
+    CUDA_OK(cudaMemset(s->chan_mem, 0, (size_t)P.chan_bytes));
+    for (auto& c : P.chans) {
+      DChan d{};
+      d.channel = c.channel;
+      d.role = c.role;
+      d.peer = c.peer;
+      d.slots = c.slots;
+      d.elem_bytes = c.elem_bytes;
+      d.dt = c.dt;
+      d.frame = c.frame;
+      uint8_t* base = (uint8_t*)s->chan_mem + c.offset;
+      const int64_t fb = ((int64_t)c.slots * 8 + 255) / 256 * 256;
+      if (c.role == 0) {
+        d.flags = (unsigned long long*)base;
+        d.data = base + fb;
+      } else {
+        d.acks = (unsigned long long*)base;
+        d.done = (unsigned long long*)(base + fb);
+      }
+      s->chans.push_back(d);
+    }
+    s->d_chans = (DChan*)dalloc(s, sizeof(DChan) * s->chans.size());
+  }
+  A.prog.n_chans = (int32_t)s->chans.size();
+  A.prog.chans = s->d_chans;
   A.inst_aux = (int64_t*)dalloc(s, 8 * 48 * (size_t)P.inst_bound);
   A.dw_count = (int32_t*)dalloc(s, 4 * P.nodes.size());
   s->zero_each_run.push_back({A.dw_count, 4 * P.nodes.size()});
@@ -2397,6 +2540,19 @@ cf_status cf_run(cf_session* s, int32_t n_feed, const char* const* feed_names,
     }
     if (!fo.empty())
       CUDA_OK(cudaMemcpyAsync(A.fetch_out, fo.data(), 8 * fo.size(), cudaMemcpyHostToDevice, s->stream));
+    if (!s->chans.empty()) {
+      for (auto& c : s->chans)
+        if (!(c.flags && c.data && c.acks && c.done))
+          throw cf::CfError(CF_E_UNSUPPORTED, "channel " + std::to_string(c.channel) + " to rank " +
+                                                  std::to_string(c.peer) +
+                                                  " not connected (cf_session_connect)");
+      if (s->chans_dirty) {
+        CUDA_OK(cudaMemcpyAsync(s->d_chans, s->chans.data(), sizeof(DChan) * s->chans.size(),
+                                cudaMemcpyHostToDevice, s->stream));
+        s->chans_dirty = false;
+      }
+    }
+    A.epoch = ++s->epoch;
     // the copies above read pageable host memory; make them complete before it goes away
     CUDA_OK(cudaStreamSynchronize(s->stream));
     void* kargs[] = {(void*)&A};
@@ -2431,6 +2587,8 @@ cf_status cf_run(cf_session* s, int32_t n_feed, const char* const* feed_names,
       trace->instances = st.instances;
       trace->tiles = st.tiles;
       trace->dead_skipped = st.dead_skipped;
+      trace->sends = st.sends;
+      trace->recvs = st.recvs;
       int nb = P.n_conds * P.branch_bound;
       trace->n_branch_bits = nb;
       if (trace->branch_bits && trace->branch_bits_cap > 0)
@@ -2472,6 +2630,88 @@ cf_status cf_session_describe(const cf_session* s, char* buf, size_t cap) {
   return CF_OK;
 }
 
+// ---- cross-GPU channels (include/cf.h)
+cf_status cf_session_channels(const cf_session* s, int32_t cap, int64_t* table, int32_t* n) {
+  if (!s || !n) return CF_E_INVALID_GRAPH;
+  const auto& cs = s->P.chans;
+  *n = (int32_t)cs.size();
+  for (int i = 0; i < (int)cs.size() && i < cap && table; ++i) {
+    int64_t* r = table + 7 * i;
+    r[0] = cs[i].channel;
+    r[1] = cs[i].role;
+    r[2] = cs[i].peer;
+    r[3] = cs[i].slots;
+    r[4] = cs[i].elem_bytes;
+    r[5] = cs[i].dt;
+    r[6] = cs[i].offset;
+  }
+  return CF_OK;
+}
+
+cf_status cf_session_ipc_handle(const cf_session* s, void* handle) {
+  if (!s || !handle) return CF_E_INVALID_GRAPH;
+  std::memset(handle, 0, CF_IPC_HANDLE_BYTES);
+  if (!s->chan_mem) return CF_OK;
+  cudaIpcMemHandle_t h;
+  if (cudaSetDevice(s->device) != cudaSuccess || cudaIpcGetMemHandle(&h, s->chan_mem) != cudaSuccess) {
+    cf::set_error("cudaIpcGetMemHandle failed");
+    return CF_E_CUDA;
+  }
+  static_assert(sizeof(h) <= CF_IPC_HANDLE_BYTES, "ipc handle size");
+  std::memcpy(handle, &h, sizeof(h));
+  return CF_OK;
+}
+
+cf_status cf_session_connect(cf_session* s, int32_t peer, const void* handle, int32_t n,
+                             const int64_t* table) {
+  try {
+    if (!s || !handle || (n > 0 && !table)) throw cf::CfError(CF_E_INVALID_GRAPH, "null argument");
+    bool used = false;
+    for (auto& c : s->chans) used |= c.peer == peer;
+    if (!used) return CF_OK;
+    CUDA_OK(cudaSetDevice(s->device));
+    void* base = nullptr;
+    auto it = s->peer_mem.find(peer);
+    if (it != s->peer_mem.end()) {
+      base = it->second;
+    } else {
+      cudaIpcMemHandle_t h;
+      std::memcpy(&h, handle, sizeof(h));
+      CUDA_OK(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+      s->peer_mem[peer] = base;
+    }
+    for (auto& c : s->chans) {
+      if (c.peer != peer) continue;
+      const int64_t* row = nullptr;
+      for (int i = 0; i < n; ++i)
+        if (table[7 * i] == c.channel && table[7 * i + 1] == 1 - c.role) row = table + 7 * i;
+      if (!row)
+        throw cf::CfError(CF_E_UNSUPPORTED, "rank " + std::to_string(peer) + " has no " +
+                                                (c.role ? "Recv" : "Send") + " for channel " +
+                                                std::to_string(c.channel));
+      if (row[3] != c.slots || row[4] != c.elem_bytes || row[5] != c.dt)
+        throw cf::CfError(CF_E_UNSUPPORTED, "channel " + std::to_string(c.channel) +
+                                                ": the two halves disagree on slots / payload bytes / "
+                                                "dtype (same parallel_iterations and precision on "
+                                                "both ranks?)");
+      uint8_t* pb = (uint8_t*)base + row[6];
+      const int64_t fb = ((int64_t)c.slots * 8 + 255) / 256 * 256;
+      if (c.role == 1) {
+        c.flags = (unsigned long long*)pb;
+        c.data = pb + fb;
+      } else {
+        c.acks = (unsigned long long*)pb;
+        c.done = (unsigned long long*)(pb + fb);
+      }
+    }
+    s->chans_dirty = true;
+    return CF_OK;
+  } catch (const cf::CfError& e) {
+    cf::set_error(e.what());
+    return e.code;
+  }
+}
+
 // profiling hook (include/cf_debug.h): per-instance timing of the last cf_run
 int32_t cf_debug_session_profile(const cf_session* s, unsigned long long* out, int64_t cap,
                                  int64_t* n_inst, unsigned long long* t0) {
@@ -2498,6 +2738,8 @@ int32_t cf_debug_session_profile(const cf_session* s, unsigned long long* out, i
 void cf_session_destroy(cf_session* s) {
   if (!s) return;
   for (void* p : s->allocs) cudaFree(p);
+  for (auto& [r, p] : s->peer_mem) cudaIpcCloseMemHandle(p);
+  if (s->chan_mem) cudaFree(s->chan_mem);
   if (s->ev0) cudaEventDestroy(s->ev0);
   if (s->ev1) cudaEventDestroy(s->ev1);
   if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);

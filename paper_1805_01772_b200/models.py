@@ -39,28 +39,47 @@ class RNNProgram:
         return [self.fetch[n] for n in self.fetch] + [self.grads[n] for n in self.grads]
 
 
+def layer_partition(L: int, world: int, rank: int):
+    """Layers [l0, l1) of pipeline stage `rank`: contiguous, balanced (reading R18)."""
+    if not 1 <= world <= L:
+        raise ValueError(f"cannot split {L} layers over {world} stages")
+    base, extra = divmod(L, world)
+    l0 = rank * base + min(rank, extra)
+    return l0, l0 + base + (1 if rank < extra else 0)
+
+
 def dynamic_rnn_lstm(T: int, B: int, I: int, H: int, L: int = 1, parallel_iterations: int = 32,
                      length_conds: bool = True, moe: bool = False, forget_bias: float = 0.0,
-                     with_grads: bool = True) -> RNNProgram:
+                     with_grads: bool = True, stage=None) -> RNNProgram:
+    """The full model, or with ``stage=(rank, world)`` the partition of layer-pipeline stage
+    `rank`: a later stage Recvs its layer input from
+    the previous stage and a non-final stage Sends its top output on, inside the loop, every
+    iteration; each stage runs its own copy of the loop control (reading R18). The stage loss
+    is the part of y owned by the stage (the stage losses sum to y)."""
+    rank, world = stage if stage is not None else (0, 1)
+    l0, l1 = layer_partition(L, world, rank)
+    first, last = rank == 0, rank == world - 1
+    Ls = list(range(l0, l1))
+    n = len(Ls)
     g = Graph()
-    x = g.placeholder("x", F32, (T, B, I))
+    x = g.placeholder("x", F32, (T, B, I)) if first else None
     lens = g.placeholder("len", I64, (B,))
-    Ws, bs, h0, c0, WA, WB = [], [], [], [], [], []
-    for l in range(L):
+    Ws, bs, h0, c0, WA, WB = {}, {}, {}, {}, {}, {}
+    for l in Ls:
         il = I if l == 0 else H
-        Ws.append(g.placeholder(f"W{l}", F32, (4 * H, il + H)))
-        bs.append(g.placeholder(f"b{l}", F32, (4 * H,)))
-        h0.append(g.placeholder(f"h0_{l}", F32, (B, H)))
-        c0.append(g.placeholder(f"c0_{l}", F32, (B, H)))
+        Ws[l] = g.placeholder(f"W{l}", F32, (4 * H, il + H))
+        bs[l] = g.placeholder(f"b{l}", F32, (4 * H,))
+        h0[l] = g.placeholder(f"h0_{l}", F32, (B, H))
+        c0[l] = g.placeholder(f"c0_{l}", F32, (B, H))
         if moe:
-            WA.append(g.placeholder(f"WA{l}", F32, (H, H)))
-            WB.append(g.placeholder(f"WB{l}", F32, (H, H)))
+            WA[l] = g.placeholder(f"WA{l}", F32, (H, H))
+            WB[l] = g.placeholder(f"WB{l}", F32, (H, H))
     route_ta = None
     if moe:
         route = g.placeholder("route", BOOL, (T, L))
         route_ta = g.tensor_array(T, BOOL, (L,)).unstack(route)
-    x_ta = g.tensor_array(T, F32, (B, I)).unstack(x)
-    out_tas = [g.tensor_array(T, F32, (B, H)) for _ in range(L)]
+    x_ta = g.tensor_array(T, F32, (B, I)).unstack(x) if first else None
+    out_tas = [g.tensor_array(T, F32, (B, H)) for _ in Ls]
     max_len = g.op1("ReduceMax", [lens])
     min_len = g.op1("ReduceMin", [lens])
     t_bound = g.const(T, I64)
@@ -69,14 +88,14 @@ def dynamic_rnn_lstm(T: int, B: int, I: int, H: int, L: int = 1, parallel_iterat
         return g.op1("Less", [t, t_bound])
 
     def body(t, *vs):
-        hs, cs, flows = vs[:L], vs[L:2 * L], vs[2 * L:3 * L]
-        x_t = x_ta.read(t)
+        hs, cs, flows = vs[:n], vs[n:2 * n], vs[2 * n:3 * n]
+        x_t = x_ta.read(t) if first else g.recv(t, rank - 1, rank - 1, F32, (B, H))
         r_t = route_ta.read(t) if moe else None
 
         def cells(masked):
             inp, outs, nh, nc = x_t, [], [], []
-            for l in range(L):
-                ins = [inp, hs[l], cs[l], Ws[l], bs[l]] + ([t, lens] if masked else [])
+            for k, l in enumerate(Ls):
+                ins = [inp, hs[k], cs[k], Ws[l], bs[l]] + ([t, lens] if masked else [])
                 hn, cn, o, _g = g.op("LSTMCell", ins, {"masked": masked, "forget_bias": forget_bias})
                 if moe:
                     r = g.op1("Reshape", [g.op1("Slice", [r_t], {"begin": (l,), "size": (1,)})],
@@ -94,36 +113,43 @@ def dynamic_rnn_lstm(T: int, B: int, I: int, H: int, L: int = 1, parallel_iterat
         if length_conds:
             def cell_branch():
                 return g.cond(g.op1("Less", [t, min_len]), lambda: cells(False),
-                              lambda: cells(True), 3 * L)
+                              lambda: cells(True), 3 * n)
 
             def empty_update():
-                return [g.const([[0.0] * H] * B, F32) for _ in range(L)] + list(hs) + list(cs)
-            res = g.cond(g.op1("Less", [t, max_len]), cell_branch, empty_update, 3 * L)
+                return [g.const([[0.0] * H] * B, F32) for _ in Ls] + list(hs) + list(cs)
+            res = g.cond(g.op1("Less", [t, max_len]), cell_branch, empty_update, 3 * n)
         else:
             res = cells(True)
-        outs, nh, nc = res[:L], res[L:2 * L], res[2 * L:]
-        nf = [out_tas[l].with_flow(flows[l]).write(t, outs[l]).flow for l in range(L)]
+        outs, nh, nc = res[:n], res[n:2 * n], res[2 * n:]
+        if not last:
+            g.send(outs[-1], t, rank, rank + 1)
+        nf = [out_tas[k].with_flow(flows[k]).write(t, outs[k]).flow for k in range(n)]
         return [g.op1("Add", [t, g.const(1, I64)])] + nh + nc + nf
 
-    res = g.while_loop(pred, body, [g.const(0, I64)] + h0 + c0 + [ta.flow for ta in out_tas],
-                       parallel_iterations, name="rnn")
-    hT, cT, fT = res[1:1 + L], res[1 + L:1 + 2 * L], res[1 + 2 * L:]
-    out_top = out_tas[L - 1].with_flow(fT[L - 1]).stack()
-    R_out = g.placeholder("R_out", F32, (T, B, H))
-    y = g.op1("ReduceSum", [g.op1("Mul", [R_out, out_top])])
-    for l in range(L):
+    res = g.while_loop(pred, body, [g.const(0, I64)] + [h0[l] for l in Ls] + [c0[l] for l in Ls]
+                       + [ta.flow for ta in out_tas], parallel_iterations, name="rnn")
+    hT, cT, fT = res[1:1 + n], res[1 + n:1 + 2 * n], res[1 + 2 * n:]
+    y = None
+    fetch = {}
+    if last:
+        out_top = out_tas[n - 1].with_flow(fT[n - 1]).stack()
+        R_out = g.placeholder("R_out", F32, (T, B, H))
+        y = g.op1("ReduceSum", [g.op1("Mul", [R_out, out_top])])
+        fetch["out"] = out_top
+    for k, l in enumerate(Ls):
         Rh = g.placeholder(f"R_h{l}", F32, (B, H))
         Rc = g.placeholder(f"R_c{l}", F32, (B, H))
-        y = g.op1("Add", [y, g.op1("Add", [g.op1("ReduceSum", [g.op1("Mul", [Rh, hT[l]])]),
-                                           g.op1("ReduceSum", [g.op1("Mul", [Rc, cT[l]])])])])
-    fetch = {"y": y, "out": out_top}
-    for l in range(L):
-        fetch[f"hT{l}"] = hT[l]
-        fetch[f"cT{l}"] = cT[l]
+        yl = g.op1("Add", [g.op1("ReduceSum", [g.op1("Mul", [Rh, hT[k]])]),
+                           g.op1("ReduceSum", [g.op1("Mul", [Rc, cT[k]])])])
+        y = yl if y is None else g.op1("Add", [y, yl])
+    fetch = {"y": y, **fetch}
+    for k, l in enumerate(Ls):
+        fetch[f"hT{l}"] = hT[k]
+        fetch[f"cT{l}"] = cT[k]
     grads = {}
     if with_grads:
-        names, xs = ["x"], [x]
-        for l in range(L):
+        names, xs = (["x"], [x]) if first else ([], [])
+        for l in Ls:
             names += [f"W{l}", f"b{l}", f"h0_{l}", f"c0_{l}"]
             xs += [Ws[l], bs[l], h0[l], c0[l]]
             if moe:
@@ -142,6 +168,8 @@ def feeds_to_device(feeds, device="cuda", session=None):
     tdt = {cf.F32: torch.float32, cf.BF16: torch.bfloat16}
     out = {}
     for k, v in feeds.items():
+        if session is not None and not session.has_feed(k):
+            continue   # e.g. a pipeline stage without this placeholder
         v = np.asarray(v)
         if v.dtype == np.float64:
             dt = torch.float32

@@ -39,7 +39,11 @@ def test_exports_every_declared_symbol():
 
 @pytest.mark.parametrize("args,kw", [((5, 2, 4, 8, 1), {}), ((5, 3, 4, 8, 2), {}),
                                      ((4, 2, 3, 4, 1), {"moe": True}),
-                                     ((6, 4, 4, 4, 3), {"length_conds": False})])
+                                     ((6, 4, 4, 4, 3), {"length_conds": False}),
+                                     ((5, 2, 4, 8, 4), {"stage": (0, 2)}),
+                                     ((5, 2, 4, 8, 4), {"stage": (1, 2)}),
+                                     ((5, 2, 4, 8, 3), {"stage": (1, 3)}),
+                                     ((4, 2, 3, 4, 2), {"moe": True, "stage": (1, 2)})])
 def test_structure_matches_oracle(args, kw):
     p = dev_rnn(*args, **kw)
     q = oracle_rnn(*args, **kw)
@@ -115,3 +119,19 @@ def test_unsupported_is_loud():
     with pytest.raises(cf.CfError) as e:
         cf.Session(g, [y])
     assert e.value.code in ("CF_E_UNSUPPORTED", "CF_E_CUDA")
+
+
+def test_send_recv_graph_errors_and_channels_api():
+    g = cf.Graph()
+    x = g.placeholder("x", cf.F32, (2, 2))
+    f = g.placeholder("f", cf.F32, ())
+    with pytest.raises(cf.CfError) as e:
+        g.send(x, f, 0, 1)          # index must be an int64 scalar
+    assert e.value.code == "CF_E_DTYPE"
+    i = g.const(0, cf.I64)
+    with pytest.raises(cf.CfError) as e:
+        g.op("Recv", [i], {"dtype": cf.F32, "shape": [2, 2]})   # no channel / peer
+    assert e.value.code == "CF_E_ARITY"
+    r = g.recv(i, 3, 1, cf.F32, (2, 2))
+    assert r.shape == (2, 2)
+    assert g.count_ops()["Recv"] == 1
