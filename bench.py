@@ -173,6 +173,9 @@ def main():
     ap.add_argument("--warmup-ref", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-T", type=int, default=12)
+    ap.add_argument("--parallel", default="pipeline", choices=["pipeline", "replicas"],
+                    help="N>1: layer-partitioned pipeline (strong scaling, SURVEY.md a14) or "
+                         "independent replicas (weak scaling)")
     args = ap.parse_args()
     c = CONFIGS[args.config]
     if args.impl == "reference":
@@ -195,12 +198,20 @@ def main():
         pg = dist
     W = max(args.warmup, 3)
     prec = cf.F32 if args.precision == "f32" else cf.BF16
-    p = dynamic_rnn_lstm(c["T"], c["B"], c["I"], c["H"], c["L"])
+    pipe = world > 1 and args.parallel == "pipeline"
+    if pipe and world > c["L"]:
+        raise SystemExit(f"pipeline over {world} GPUs needs >= {world} layers")
+    stage = (rank, world) if pipe else None
+    p = dynamic_rnn_lstm(c["T"], c["B"], c["I"], c["H"], c["L"], stage=stage)
     stream = torch.cuda.current_stream()
     sess = cf.Session(p.g, p.fetch_tensors(), precision=prec, parallel_iterations=args.K,
-                      device=local, stream=stream.cuda_stream)
-    f = rnn_inputs(c["T"], c["B"], c["I"], c["H"], c["L"], seed=rank, len_mode=c["len_mode"],
-                   bf16=prec == cf.BF16)
+                      device=local, stream=stream.cuda_stream,
+                      watchdog_ms=300000 if pipe else 0)
+    if pipe:
+        sess.connect_pipeline()
+    # pipeline: one model split over the ranks (same inputs everywhere); replicas: own inputs
+    f = rnn_inputs(c["T"], c["B"], c["I"], c["H"], c["L"], seed=0 if pipe else rank,
+                   len_mode=c["len_mode"], bf16=prec == cf.BF16)
     lens_sum = int(f["len"].sum())
     dev = feeds_to_device(f, device=f"cuda:{local}", session=sess)
     outs = sess.alloc_outputs(device=f"cuda:{local}")
@@ -250,12 +261,19 @@ def main():
         t = torch.tensor([e2e_ms], device=f"cuda:{local}")
         pg.all_reduce(t, op=pg.ReduceOp.MAX)
         e2e_ms = float(t.item())
+        b = torch.tensor([h2d, d2h], device=f"cuda:{local}", dtype=torch.float64)
+        pg.all_reduce(b, op=pg.ReduceOp.SUM)   # whole job: every rank's copies
+        h2d, d2h = int(b[0].item()), int(b[1].item())
     if rank != 0:
         if pg:
             pg.destroy_process_group()
         return
     pk = peaks()
     fl = flops_per_step(c, lens_sum)
+    if pipe:   # rank 0's stage: its share of the layers
+        from paper_1805_01772_b200.models import layer_partition
+        l0, l1 = layer_partition(c["L"], world, 0)
+        fl = fl * (l1 - l0) / c["L"]
     kms = statistics.mean(kernel_ms)
     if prec == cf.F32:
         mhz = pk.get("sm_max_mhz", 1965.0)
@@ -282,17 +300,18 @@ def main():
         cpu = cpu_baseline(c, args.config, min(args.cpu_T, c["T"]))
     line = {
         "metric": "LSTM fwd+bwd sequence-steps/sec",
-        "value": lens_sum * world / (ms * 1e-3),
+        "value": lens_sum * (1 if pipe else world) / (ms * 1e-3),
         "unit": "sequence-steps/s",
         "n_gpus": world, "steps": args.steps, "warmup": W, "ms_per_step": ms,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if pipe else "weak",
         "vs_baseline": None,
         "dtype": args.precision,
         "data": "synthetic (seeded; synth.rnn_inputs)",
         "config": {"workload": args.config, **{k: c[k] for k in ("T", "B", "I", "H", "L")},
                    "lengths": c["len_mode"], "parallel_iterations": args.K or 32,
-                   "parallelism": "replicas" if world > 1 else "single",
+                   "parallelism": (f"layer-pipeline{world}" if pipe else f"replicas{world}")
+                   if world > 1 else "single",
                    "l2": "inputs/activations > L2 (no flush needed)"},
         "loop_iterations_per_s": c["T"] / (ms * 1e-3),
         "kernel_ms": kms,
@@ -300,7 +319,8 @@ def main():
         "roofline": roof,
         "cpu_baseline": cpu,
         "clocks": clk.summary(),
-        "e2e": {"value": lens_sum * world / (e2e_ms * 1e-3), "unit": "sequence-steps/s",
+        "e2e": {"value": lens_sum * (1 if pipe else world) / (e2e_ms * 1e-3),
+                "unit": "sequence-steps/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": args.steps,
     }
