@@ -173,6 +173,9 @@ def main():
     ap.add_argument("--warmup-ref", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-T", type=int, default=12)
+    ap.add_argument("--stack-budget", type=int, default=0,
+                    help="device bytes for stacked activations; beyond it stacks swap to pinned "
+                         "host memory (0 = no swapping, 1 = swap every eligible value)")
     ap.add_argument("--parallel", default="pipeline", choices=["pipeline", "replicas"],
                     help="N>1: layer-partitioned pipeline (strong scaling, SURVEY.md a14) or "
                          "independent replicas (weak scaling)")
@@ -206,7 +209,7 @@ def main():
     stream = torch.cuda.current_stream()
     sess = cf.Session(p.g, p.fetch_tensors(), precision=prec, parallel_iterations=args.K,
                       device=local, stream=stream.cuda_stream,
-                      watchdog_ms=300000 if pipe else 0)
+                      watchdog_ms=300000 if pipe else 0, stack_budget_bytes=args.stack_budget)
     if pipe:
         sess.connect_pipeline()
     # pipeline: one model split over the ranks (same inputs everywhere); replicas: own inputs
@@ -230,6 +233,8 @@ def main():
             kernel_ms.append(tr["wall_ms"])
         ev1.record(stream)
         torch.cuda.synchronize()
+    swap = {"stack_budget_bytes": args.stack_budget, "swap_out": tr["swap_out"],
+            "swap_in": tr["swap_in"], "bytes_d2h": tr["bytes_d2h"], "bytes_h2d": tr["bytes_h2d"]}
     if pg:
         pg.barrier()
     ms = ev0.elapsed_time(ev1) / args.steps
@@ -247,16 +252,22 @@ def main():
     d2h = y_host.numel() * y_host.element_size()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e2e_steps = max(2, min(args.steps, 5))
+    c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    copy_ms = 0.0
     torch.cuda.synchronize()
     e0.record(stream)
     for _ in range(e2e_steps):
+        c0.record(stream)
         for k, v in host.items():
             dev[k].copy_(v, non_blocking=True)
+        c1.record(stream)
         sess.run(dev, outs)
+        copy_ms += c0.elapsed_time(c1)
         y_host.copy_(outs[0], non_blocking=True)
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1) / e2e_steps
+    copy_ms /= e2e_steps
     if pg:
         t = torch.tensor([e2e_ms], device=f"cuda:{local}")
         pg.all_reduce(t, op=pg.ReduceOp.MAX)
@@ -321,8 +332,10 @@ def main():
         "clocks": clk.summary(),
         "e2e": {"value": lens_sum * (1 if pipe else world) / (e2e_ms * 1e-3),
                 "unit": "sequence-steps/s",
-                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "h2d_ms_per_step": copy_ms},
         "gpu_launches": args.steps,
+        "stack_swap": swap,
     }
     print(json.dumps(line), flush=True)
     if pg:

@@ -166,6 +166,14 @@ typedef struct {
   int64_t watchdog_ms;          /* device watchdog; 0 = 60000                             */
   int32_t sched_seed;           /* 0 = FIFO; else shuffled worker claim order (race check) */
   int32_t reserved[7];
+  /* Stack swapping: stacked activations stay in
+   * device memory up to stack_budget_bytes; beyond it the largest stacked values (each at
+   * least swap_min_bytes) keep only a (parallel_iterations + 1)-slot device ring and move to
+   * pinned host memory after the push (device -> host on a copy stream), coming back ahead
+   * of the pop (host -> device). <= 0 = never swap (a zero-initialised struct swaps
+   * nothing); 1 = swap every eligible value. */
+  int64_t stack_budget_bytes;
+  int64_t swap_min_bytes;       /* 0 = 4096 ("do not swap small tensors") */
 } cf_run_opts;
 
 /* Control trace -- compared bit-exact with the oracle's. */
@@ -184,6 +192,8 @@ typedef struct {
   int32_t branch_bits_cap;
   double wall_ms;               /* device time of the run (CUDA events)                 */
   int64_t sends, recvs;         /* cross-GPU messages sent / received, live or dead (a14)  */
+  int64_t swap_out, swap_in;    /* stack entries moved device -> host / host -> device (a8) */
+  int64_t bytes_d2h, bytes_h2d; /* their bytes                                            */
 } cf_trace;
 
 /* Compile the graph for the device (placement of every value, lowering to the device

@@ -47,7 +47,8 @@ class cf_run_opts(C.Structure):
     _fields_ = [("precision", C.c_int32), ("parallel_iterations", C.c_int32),
                 ("device", C.c_int32), ("num_workers", C.c_int32), ("stream", C.c_void_p),
                 ("max_iterations", C.c_int64), ("watchdog_ms", C.c_int64),
-                ("sched_seed", C.c_int32), ("reserved", C.c_int32 * 7)]
+                ("sched_seed", C.c_int32), ("reserved", C.c_int32 * 7),
+                ("stack_budget_bytes", C.c_int64), ("swap_min_bytes", C.c_int64)]
 
 
 class cf_trace(C.Structure):
@@ -56,7 +57,9 @@ class cf_trace(C.Structure):
                 ("max_depth", C.c_int32), ("exit_fires", C.c_int32), ("instances", C.c_int64),
                 ("tiles", C.c_int64), ("dead_skipped", C.c_int64), ("n_branch_bits", C.c_int32),
                 ("branch_bits", C.POINTER(C.c_uint8)), ("branch_bits_cap", C.c_int32),
-                ("wall_ms", C.c_double), ("sends", C.c_int64), ("recvs", C.c_int64)]
+                ("wall_ms", C.c_double), ("sends", C.c_int64), ("recvs", C.c_int64),
+                ("swap_out", C.c_int64), ("swap_in", C.c_int64), ("bytes_d2h", C.c_int64),
+                ("bytes_h2d", C.c_int64)]
 
 
 PRED_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_int32, C.POINTER(cf_tensor),
@@ -401,7 +404,8 @@ class Session:
     def __init__(self, g: Graph, fetches: Sequence[Tensor], precision: int = F32,
                  parallel_iterations: int = 0, device: int = 0, stream=None,
                  max_iterations: int = 0, watchdog_ms: int = 0, num_workers: int = 0,
-                 sched_seed: int = 0, profile: bool = False):
+                 sched_seed: int = 0, profile: bool = False, stack_budget_bytes: int = 0,
+                 swap_min_bytes: int = 0):
         self.g = g
         self.fetches = list(fetches)
         o = cf_run_opts()
@@ -414,6 +418,8 @@ class Session:
         o.watchdog_ms = watchdog_ms
         o.sched_seed = sched_seed
         o.reserved[0] = 1 if profile else 0
+        o.stack_budget_bytes = stack_budget_bytes
+        o.swap_min_bytes = swap_min_bytes
         arr = (cf_tensor * max(len(fetches), 1))(*[t.c for t in fetches])
         h = _P()
         _check(_lib.cf_session_create(g.h, C.byref(o), len(fetches), arr, C.byref(h)))
@@ -546,7 +552,8 @@ class Session:
                 "pushes": tr.pushes, "pops": tr.pops, "max_depth": tr.max_depth,
                 "exit_fires": tr.exit_fires, "instances": tr.instances, "tiles": tr.tiles,
                 "dead_skipped": tr.dead_skipped, "wall_ms": tr.wall_ms,
-                "sends": tr.sends, "recvs": tr.recvs,
+                "sends": tr.sends, "recvs": tr.recvs, "swap_out": tr.swap_out,
+                "swap_in": tr.swap_in, "bytes_d2h": tr.bytes_d2h, "bytes_h2d": tr.bytes_h2d,
                 "n_branch_bits": tr.n_branch_bits,
                 "branch_bits": bytes(bits)[:min(branch_cap, tr.n_branch_bits)] if bits else b"",
             }

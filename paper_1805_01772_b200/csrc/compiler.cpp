@@ -515,9 +515,11 @@ struct Compiler {
     for (size_t f = 0; f < frame_ctx.size(); ++f)
       ds << "frame " << P.frame_names[f] << " K=" << P.frames[f].K << " bound=" << bound[f]
          << " body=" << P.frames[f].n_body << "\n";
-    int counts[5] = {0, 0, 0, 0, 0};
+    int counts[6] = {0, 0, 0, 0, 0, 0};
     for (auto& pl : P.places) counts[pl.kind]++;
     ds << "accumulators=" << P.accs.size() << " tma_operands=" << P.reg.size() << "\n";
+    ds << "stacks: resident bytes=" << P.stack_resident_bytes << " swapped arenas=" << P.swaps.size()
+       << " swapped bytes=" << P.stack_swapped_bytes << "\n";
     ds << "placements root=" << counts[0] << " ring=" << counts[1] << " arena=" << counts[2]
        << " ta=" << counts[3] << " acc=" << counts[4] << "\n";
     P.describe = ds.str();
@@ -851,23 +853,64 @@ struct Compiler {
 
   void build_orders(const std::vector<int64_t>& bound) {
     const int N = (int)g.nodes.size();
-    // arena allocation needs the bound
+    // arena allocation needs the bound. Stack swapping: when all arenas
+    // exceed the stack budget, the largest ones (each >= swap_min_bytes) become swapped
+    // arenas: a (K + 1)-slot device ring + host backing (reading R19).
+    struct Ar { int node, port, frame; int64_t bytes; };
+    std::vector<Ar> ars;
     for (int i = 0; i < N; ++i) {
       const DNode& d = P.nodes[i];
       if (d.op != OP_HEAVY && d.op != OP_RECV) continue;
-      int f = frame_of[i];
       int np = n_places(g.nodes[i]);
-      for (int p = 0; p < np; ++p) {
-        PlaceDesc& pl = P.places[d.place_off + p];
-        if (pl.kind == PL_ARENA) {
-          pl.slots = (int32_t)bound[f];
-          pl.base = add_buf((size_t)pl.elem_bytes * bound[f], false,
-                            "arena " + g.nodes[i].op + std::to_string(i));
-          if (pl.dt == D_BF16 && p < (int)g.nodes[i].osh.size() && g.nodes[i].osh[p].size() == 2)
-            register_buf_stride((int)pl.base, (int)bound[f], (int)g.nodes[i].osh[p][0],
-                                (int)g.nodes[i].osh[p][1], pl.elem_bytes);
-        }
+      for (int p = 0; p < np; ++p)
+        if (P.places[d.place_off + p].kind == PL_ARENA)
+          ars.push_back({i, p, frame_of[i], P.places[d.place_off + p].elem_bytes * bound[frame_of[i]]});
+    }
+    std::set<std::pair<int, int>> swap_set;
+    if (o.stack_budget_bytes >= 0) {
+      int64_t total = 0;
+      for (auto& a : ars) total += a.bytes;
+      std::vector<Ar> cand;
+      for (auto& a : ars)
+        if (P.places[P.nodes[a.node].place_off + a.port].elem_bytes >= o.swap_min_bytes) cand.push_back(a);
+      std::stable_sort(cand.begin(), cand.end(), [](const Ar& x, const Ar& y) { return x.bytes > y.bytes; });
+      for (auto& a : cand) {
+        if (total <= o.stack_budget_bytes) break;
+        swap_set.insert({a.node, a.port});
+        total -= a.bytes;
       }
+    }
+    for (auto& a : ars) {
+      const int i = a.node, p = a.port, f = a.frame;
+      PlaceDesc& pl = P.places[P.nodes[i].place_off + p];
+      int slots = (int)bound[f];
+      if (swap_set.count({i, p})) {
+        const int K = o.parallel_iterations > 0 ? o.parallel_iterations : g.ctxs[frame_ctx[f]].K;
+        slots = std::min<int>(K + 1, (int)bound[f]);
+        pl.kind = PL_SWAP;
+        pl.ta = (int32_t)P.swaps.size();   // swap id
+        SwapPlan sp;
+        sp.place = P.nodes[i].place_off + p;
+        sp.elem_bytes = pl.elem_bytes;
+        sp.ring = slots;
+        sp.capacity = (int32_t)bound[f];
+        // swap-ins land in a ring of their own, indexed by the gradient loop's iteration: the
+        // forward ring may still hold values that left the loop through an Exit
+        sp.in_buf = add_buf((size_t)pl.elem_bytes * slots, false, "swap-in ring " + std::to_string(i));
+        if (pl.dt == D_BF16 && p < (int)g.nodes[i].osh.size() && g.nodes[i].osh[p].size() == 2)
+          register_buf_stride(sp.in_buf, slots, (int)g.nodes[i].osh[p][0], (int)g.nodes[i].osh[p][1],
+                              pl.elem_bytes);
+        P.swaps.push_back(sp);
+        P.stack_swapped_bytes += a.bytes;
+      } else {
+        P.stack_resident_bytes += a.bytes;
+      }
+      pl.slots = slots;
+      pl.base = add_buf((size_t)pl.elem_bytes * slots, false,
+                        (pl.kind == PL_SWAP ? "swap ring " : "arena ") + g.nodes[i].op + std::to_string(i));
+      if (pl.dt == D_BF16 && p < (int)g.nodes[i].osh.size() && g.nodes[i].osh[p].size() == 2)
+        register_buf_stride((int)pl.base, slots, (int)g.nodes[i].osh[p][0], (int)g.nodes[i].osh[p][1],
+                            pl.elem_bytes);
     }
     // ---- frames
     P.frames.resize(frame_ctx.size());

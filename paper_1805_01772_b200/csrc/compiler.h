@@ -37,6 +37,14 @@ struct ChanPlan {
   int64_t offset = 0, bytes = 0;
 };
 
+// swapped stack arena (program.h DSwap); dev_base = buffer id until the runtime patches it
+struct SwapPlan {
+  int place = -1;          // index into places
+  int in_buf = -1;         // buffer id of the swap-in ring (pops of the gradient loop)
+  int64_t elem_bytes = 0;
+  int32_t ring = 0, capacity = 0;
+};
+
 struct HostProgram {
   std::vector<cfdev::DNode> nodes;
   std::vector<int32_t> in_vids;
@@ -65,6 +73,8 @@ struct HostProgram {
   int64_t tile_bound = 0;            // max tiles of one instance
   std::vector<BufPlan> bufs;
   std::vector<ChanPlan> chans;
+  std::vector<SwapPlan> swaps;
+  int64_t stack_resident_bytes = 0, stack_swapped_bytes = 0;
   int64_t chan_bytes = 0;
   std::map<std::string, FeedInfo> feeds;
   std::vector<FetchInfo> fetches;
@@ -75,6 +85,8 @@ struct CompileOpts {
   int32_t precision = CF_F32;
   int32_t parallel_iterations = 0;
   int64_t max_iterations = 0;
+  int64_t stack_budget_bytes = -1;   // -1: never swap
+  int64_t swap_min_bytes = 4096;
 };
 
 HostProgram compile(const Graph& g, const CompileOpts& o, const std::vector<TRef>& fetches);

@@ -77,6 +77,7 @@ enum HeavyKind : int32_t {
   HK_LSTM_BWD_EW_BF,// dz (bf16) + dc + db partials
   HK_LSTM_DXH_TC,   // tcgen05 d[x,h] = dz W
   HK_LSTM_DW_TC,    // tcgen05 dW (+)= dz^T [x,h] (MN-major operands) + db
+  HK_SWAP,          // stack swap copy on the host I/O thread's copy stream (sub 0: D2H, 1: H2D)
   HK__COUNT
 };
 
@@ -86,7 +87,8 @@ enum EwOp : int32_t {
 };
 
 // ---- placement of a heavy output (SURVEY.md §7.2 "static buffer pointer per (edge, slot)")
-enum Place : int32_t { PL_ROOT = 0, PL_RING = 1, PL_ARENA = 2, PL_TA = 3, PL_ACC = 4 };
+enum Place : int32_t { PL_ROOT = 0, PL_RING = 1, PL_ARENA = 2, PL_TA = 3, PL_ACC = 4,
+                       PL_SWAP = 5 /* stacked value with host backing: device ring of K + 1 */ };
 
 struct PlaceDesc {
   int32_t kind;
@@ -163,6 +165,18 @@ struct DStack {
 };
 
 // Root program step: a node id (>= 0) or a frame (-(frame + 1)).
+// ---- swapped stack arena: the value's device storage
+// is a ring of `ring` slots (slot = iteration % ring); each push also copies the entry to host
+// slot = push index; a pop whose ring slot no longer holds the entry brings it back first.
+struct DSwap {
+  int64_t dev_base;       // device ring
+  int64_t elem_bytes;
+  int64_t host_base;      // pinned host backing, [capacity][elem_bytes]
+  int64_t in_base;        // swap-in ring [ring][elem_bytes], slot = gradient-loop iteration % ring
+  int32_t ring, owner_off;   // owner_off: into RunArgs.swap_owner ([ring] stack entry ids)
+  int32_t capacity, pad;
+};
+
 // ---- cross-GPU channel (one Send/Recv edge). Each session holds one
 // half of the channel in its IPC-exported channel memory:
 //   receiving half: flags[slots] (u64) + data[slots][elem_bytes]   (written by the sender)
@@ -208,6 +222,8 @@ struct Prog {
   int32_t precision;            // 3 = f32 SIMT, 5 = bf16 tcgen05
   int32_t n_chans;
   const DChan* chans;
+  int32_t n_swaps, pad3;
+  const DSwap* swaps;
 };
 
 // ---- heavy instance record (written by the driver, read by workers)
@@ -241,6 +257,7 @@ struct RunState {
   int32_t max_inflight[16];
   long long pushes, pops;
   long long sends, recvs;
+  long long swap_out, swap_in, bytes_d2h, bytes_h2d;
   int32_t max_depth, exit_fires;
   long long instances, tiles, dead_skipped;
   unsigned long long t_start, t_end;
@@ -287,6 +304,14 @@ struct RunArgs {
   int32_t* acc_writer;       // [n_accs] latest instance writing each accumulator
   const uint8_t* vdt;        // [n_vids] device dtype of every value
   unsigned long long epoch;  // run counter (channel message tags)
+  // swap I/O (a8): requests go to the host I/O thread through a mapped ring; the thread's
+  // copy streams write completions (instance id + 1) into io_cq in stream order
+  int32_t* swap_owner;       // [sum of rings] stack entry id held by each device ring slot
+  unsigned long long* io_req;        // mapped host ring [io_cap][4]: src, dst, bytes, id|dir<<32
+  unsigned long long* io_req_tail;   // mapped host word: requests published
+  int32_t* io_cq;            // device ring [io_cap]
+  int32_t io_cap;
+  int32_t pad4;
 };
 
 }  // namespace cfdev

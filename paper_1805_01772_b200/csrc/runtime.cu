@@ -17,6 +17,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <thread>
 #include <new>
 #include <chrono>
 #include <cstdio>
@@ -491,6 +493,10 @@ struct Driver {
   int64_t pend_mz = 0;
   int32_t last_dw = -1;
   unsigned long long lq_tail = 0;
+  // swap I/O (a8)
+  unsigned long long io_tail = 0, io_head = 0;
+  int io_out = 0;   // swap requests not yet completed
+  long long n_swap_out = 0, n_swap_in = 0, b_d2h = 0, b_h2d = 0;
   unsigned long long q_done_seen = 0;
 
   // driver-private state; shared memory when it fits (see cf_driver_kernel), else global
@@ -673,6 +679,18 @@ struct Driver {
   __noinline__ __device__ void publish(int32_t id) {
     Region rg(this, 27);
     const int sl = id & kRingMask;
+    if ((r_kfi[sl] & 255) == HK_SWAP) {   // to the host I/O thread's copy streams
+      const Inst& I = A.insts[id];
+      unsigned long long* e = A.io_req + 4 * (io_tail & (unsigned long long)(A.io_cap - 1));
+      e[0] = (unsigned long long)I.p[0];
+      e[1] = (unsigned long long)I.p[13];
+      e[2] = (unsigned long long)I.n;
+      e[3] = (unsigned long long)(unsigned)id | ((unsigned long long)I.sub << 32);
+      io_tail++;
+      io_out++;
+      st_release_sys_u64(A.io_req_tail, io_tail);
+      return;
+    }
     const bool low = (r_kfi[sl] & 255) == HK_LSTM_DW_TC;
     // one entry per instance; workers claim its tiles through tile_next[id]. At most kRing
     // instances are in flight, so the 2^22-entry rings never wrap onto live entries.
@@ -708,9 +726,32 @@ struct Driver {
       e = nx;
     }
   }
+  // completions of swap copies: written by the copy streams into io_cq (id + 1), possibly out
+  // of order between the D2H and H2D streams; consumed slots are marked -1
+  __noinline__ __device__ bool drain_io() {
+    bool any = false;
+    const unsigned long long m = (unsigned long long)(A.io_cap - 1);
+    for (unsigned long long j = io_head; j < io_tail; ++j) {
+      volatile int* p = (volatile int*)&A.io_cq[j & m];
+      const int v = *p;
+      if (v > 0) {
+        __threadfence();
+        *p = -1;
+        io_out--;
+        complete(v - 1);
+        any = true;
+      }
+    }
+    while (io_head < io_tail && ((volatile int*)A.io_cq)[io_head & m] == -1) {
+      ((volatile int*)A.io_cq)[io_head & m] = 0;
+      io_head++;
+    }
+    return any;
+  }
   __noinline__ __device__ bool drain() {
     Region rg(this, 29);
     bool any = false;
+    if (io_out > 0) any = drain_io();
     for (int k = 0; k < 256; ++k) {
       int* p = &A.cq[cq_head & (A.cq_cap - 1)];
       int v = ld_acquire_i32(p);   // pairs with the worker's release of its completion
@@ -739,6 +780,13 @@ struct Driver {
         *ptr = pl.base + (int64_t)it * pl.elem_bytes;
         return true;
       case PL_ACC: *ptr = P.accs[pl.slots].base; return true;
+      case PL_SWAP: {
+        // the slot now holds a new value: no stack entry is resident in it until pushed
+        const int r = it % pl.slots;
+        A.swap_owner[P.swaps[pl.ta].owner_off + r] = -2;
+        *ptr = pl.base + (int64_t)r * pl.elem_bytes;
+        return true;
+      }
       case PL_TA: {
         int64_t ix;
         if (!scalar(toks_[pl.index_vid], &ix)) return false;
@@ -1136,6 +1184,65 @@ struct Driver {
   // payload moves GPU -> GPU by a copy instance whose workers store straight into the peer's
   // slot over NVLink; the last tile publishes the flag (release, system scope). The dead
   // signal is a flag with the low bit set and no payload.
+  // ---------------------------------------------------------------- stack swapping (a8)
+  // "move tensors from GPU to CPU memory when they are pushed onto stacks,
+  // and bring them back gradually before they are needed in backpropagation". A swapped value
+  // lives in a (K + 1)-slot device ring; the parallel-iterations window guarantees that the
+  // iteration which last used a ring slot has completed (including its copies) before the
+  // slot is written again, in the forward and in the gradient loop (reading R19).
+  __device__ int find_swap(int64_t p, int64_t* slot) const {
+    for (int k = 0; k < P.n_swaps; ++k) {
+      const DSwap& w = P.swaps[k];
+      if (p >= w.dev_base && p < w.dev_base + (int64_t)w.ring * w.elem_bytes) {
+        *slot = (p - w.dev_base) / w.elem_bytes;
+        return k;
+      }
+    }
+    return -1;
+  }
+  __noinline__ __device__ int swap_copy(int dir, int64_t dst, int64_t src, int64_t bytes, int32_t dep) {
+    int32_t id = new_inst(HK_SWAP, dir, 1);
+    if (id < 0) return -1;
+    Inst& I = A.insts[id];
+    I.n = bytes;
+    I.p[0] = src;
+    I.p[13] = dst;
+    add_dep(id, dep);
+    submit(id);
+    return id;
+  }
+  __noinline__ __device__ int swap_out(const Tok& v, int32_t entry, int dp) {
+    int64_t r;
+    const int k = find_swap(v.v, &r);
+    if (k < 0) return 0;
+    const DSwap& w = P.swaps[k];
+    if (dp >= w.capacity) {
+      fail(CF_E_STACK_BUDGET, dp);
+      return -1;
+    }
+    A.swap_owner[w.owner_off + r] = entry;
+    if (swap_copy(0, w.host_base + (int64_t)dp * w.elem_bytes, v.v, w.elem_bytes, v.writer) < 0) return -1;
+    n_swap_out++;
+    b_d2h += w.elem_bytes;
+    return 1;
+  }
+  __noinline__ __device__ int swap_in(Tok* t, int32_t entry, int dp) {
+    int64_t r;
+    const int k = find_swap(t->v, &r);
+    if (k < 0) return 0;
+    const DSwap& w = P.swaps[k];
+    if (A.swap_owner[w.owner_off + r] == entry) return 0;   // still resident in its ring slot
+    const int it = cur_frame >= 0 ? iter : 0;
+    const int64_t dst = w.in_base + (int64_t)(it % w.ring) * w.elem_bytes;
+    int32_t id = swap_copy(1, dst, w.host_base + (int64_t)dp * w.elem_bytes, w.elem_bytes, -1);
+    if (id < 0) return -1;
+    t->v = dst;
+    t->writer = id;
+    n_swap_in++;
+    b_h2d += w.elem_bytes;
+    return 1;
+  }
+
   __noinline__ __device__ int eval_send(const DNode& d, bool dead) {
     const DChan& C = P.chans[d.aux[0]];
     const int it = cur_frame >= 0 ? iter : 0;
@@ -1552,9 +1659,11 @@ struct Driver {
             fail(CF_E_STACK_BUDGET, dp);
             return EV_ERROR;
           }
-          A.stack_pool[S.entry_off + dp] = in_tok(d, 1);
+          const Tok& pv = in_tok(d, 1);
+          A.stack_pool[S.entry_off + dp] = pv;
           stack_depth_[s] = dp + 1;
           n_push++;
+          if (P.n_swaps && pv.kind == TK_PTR && swap_out(pv, S.entry_off + dp, dp) < 0) return EV_ERROR;
           if (dp + 1 > max_depth) max_depth = dp + 1;
         }
         break;
@@ -1574,6 +1683,7 @@ struct Driver {
         Tok t = A.stack_pool[S.entry_off + dp - 1];
         stack_depth_[s] = dp - 1;
         t.dead = 0;
+        if (P.n_swaps && t.kind == TK_PTR && swap_in(&t, S.entry_off + dp - 1, dp - 1) < 0) return EV_ERROR;
         set_out(d, 0, t);
         n_pop++;
         break;
@@ -1903,6 +2013,10 @@ struct Driver {
     st->pops = n_pop;
     st->sends = n_sent;
     st->recvs = n_recv;
+    st->swap_out = n_swap_out;
+    st->swap_in = n_swap_in;
+    st->bytes_d2h = b_d2h;
+    st->bytes_h2d = b_h2d;
     st->dead_skipped = n_dead;
     st->instances = n_inst;
     st->tiles = n_tiles;
@@ -2195,6 +2309,12 @@ struct cf_session {
   bool chans_dirty = true;
   std::map<int, void*> peer_mem;   // imported peer channel memory, by peer rank
   unsigned long long epoch = 0;
+  // stack swapping (a8): pinned host backing + the host I/O thread's request ring / streams
+  std::vector<void*> host_allocs;
+  unsigned long long* io_req_host = nullptr;    // mapped [io_cap][4]
+  unsigned long long* io_tail_host = nullptr;   // mapped, written by the driver
+  int32_t* io_ids_host = nullptr;               // pinned completion words (id + 1)
+  cudaStream_t io_d2h = nullptr, io_h2d = nullptr;
 };
 
 namespace {
@@ -2216,6 +2336,38 @@ void* dalloc(cf_session* s, size_t bytes) {
   return p;
 }
 
+// Host I/O executor (one thread per run of a session with swapped stacks): takes the driver's
+// swap requests from the mapped ring in order and issues them on the D2H / H2D copy streams,
+// each followed by a 4-byte completion write into io_cq (stream-ordered after the data).
+void io_executor(cf_session* s, std::atomic<bool>* stop, std::atomic<int>* err) {
+  cudaSetDevice(s->device);
+  const unsigned long long m = (unsigned long long)(s->args.io_cap - 1);
+  unsigned long long head = 0;
+  int idle = 0;
+  while (true) {
+    const unsigned long long tail = *(volatile unsigned long long*)s->io_tail_host;
+    if (head < tail) {
+      std::atomic_thread_fence(std::memory_order_acquire);
+      volatile unsigned long long* e = s->io_req_host + 4 * (head & m);
+      const unsigned long long src = e[0], dst = e[1], bytes = e[2], w = e[3];
+      const int id = (int)(w & 0xffffffffULL), dir = (int)(w >> 32);
+      cudaStream_t st = dir == 0 ? s->io_d2h : s->io_h2d;
+      s->io_ids_host[head & m] = id + 1;
+      cudaError_t r = cudaMemcpyAsync((void*)dst, (const void*)src, bytes,
+                                      dir == 0 ? cudaMemcpyDeviceToHost : cudaMemcpyHostToDevice, st);
+      if (r == cudaSuccess)
+        r = cudaMemcpyAsync(s->args.io_cq + (head & m), s->io_ids_host + (head & m), 4,
+                            cudaMemcpyHostToDevice, st);
+      if (r != cudaSuccess) err->store(1);
+      head++;
+      idle = 0;
+      continue;
+    }
+    if (stop->load()) break;
+    if (++idle > 64) std::this_thread::yield();
+  }
+}
+
 void build_session(cf_session* s, const cf::Graph& g, const cf_run_opts* o,
                    const std::vector<cf::TRef>& fetches) {
   cf::CompileOpts co;
@@ -2223,6 +2375,8 @@ void build_session(cf_session* s, const cf::Graph& g, const cf_run_opts* o,
     co.precision = o->precision ? o->precision : CF_F32;
     co.parallel_iterations = o->parallel_iterations;
     co.max_iterations = o->max_iterations;
+    co.stack_budget_bytes = o->stack_budget_bytes > 0 ? o->stack_budget_bytes : -1;
+    co.swap_min_bytes = o->swap_min_bytes > 0 ? o->swap_min_bytes : 4096;
     s->device = o->device;
     if (o->watchdog_ms > 0) s->watchdog_ns = o->watchdog_ms * 1000000LL;
     s->sched_seed = o->sched_seed;
@@ -2347,6 +2501,43 @@ void build_session(cf_session* s, const cf::Graph& g, const cf_run_opts* o,
   }
   A.prog.n_chans = (int32_t)s->chans.size();
   A.prog.chans = s->d_chans;
+  // ---- swapped stack arenas (a8)
+  A.io_cap = 4096;
+  if (!P.swaps.empty()) {
+    std::vector<DSwap> sw;
+    int owner_total = 0;
+    for (auto& sp : P.swaps) {
+      DSwap d{};
+      d.dev_base = P.places[sp.place].base;
+      d.in_base = (int64_t)(uintptr_t)s->buf_ptr.at(sp.in_buf);
+      d.elem_bytes = sp.elem_bytes;
+      d.ring = sp.ring;
+      d.capacity = sp.capacity;
+      d.owner_off = owner_total;
+      owner_total += sp.ring;
+      void* h = nullptr;
+      CUDA_OK(cudaHostAlloc(&h, (size_t)sp.capacity * sp.elem_bytes, cudaHostAllocPortable));
+      s->host_allocs.push_back(h);
+      d.host_base = (int64_t)(uintptr_t)h;
+      sw.push_back(d);
+    }
+    A.prog.swaps = upload(s, sw);
+    A.prog.n_swaps = (int32_t)sw.size();
+    A.swap_owner = (int32_t*)dalloc(s, 4 * (size_t)owner_total);
+    s->fill_ff_each_run.push_back({A.swap_owner, 4 * owner_total});
+    CUDA_OK(cudaHostAlloc((void**)&s->io_req_host, 32 * (size_t)A.io_cap, cudaHostAllocMapped));
+    CUDA_OK(cudaHostAlloc((void**)&s->io_tail_host, 64, cudaHostAllocMapped));
+    CUDA_OK(cudaHostAlloc((void**)&s->io_ids_host, 4 * (size_t)A.io_cap, cudaHostAllocDefault));
+    s->host_allocs.push_back(s->io_req_host);
+    s->host_allocs.push_back(s->io_tail_host);
+    s->host_allocs.push_back(s->io_ids_host);
+    CUDA_OK(cudaHostGetDevicePointer((void**)&A.io_req, s->io_req_host, 0));
+    CUDA_OK(cudaHostGetDevicePointer((void**)&A.io_req_tail, s->io_tail_host, 0));
+    A.io_cq = (int32_t*)dalloc(s, 4 * (size_t)A.io_cap);
+    s->zero_each_run.push_back({A.io_cq, 4 * (size_t)A.io_cap});
+    CUDA_OK(cudaStreamCreateWithFlags(&s->io_d2h, cudaStreamNonBlocking));
+    CUDA_OK(cudaStreamCreateWithFlags(&s->io_h2d, cudaStreamNonBlocking));
+  }
   A.inst_aux = (int64_t*)dalloc(s, 8 * 48 * (size_t)P.inst_bound);
   A.dw_count = (int32_t*)dalloc(s, 4 * P.nodes.size());
   s->zero_each_run.push_back({A.dw_count, 4 * P.nodes.size()});
@@ -2556,11 +2747,28 @@ cf_status cf_run(cf_session* s, int32_t n_feed, const char* const* feed_names,
     // the copies above read pageable host memory; make them complete before it goes away
     CUDA_OK(cudaStreamSynchronize(s->stream));
     void* kargs[] = {(void*)&A};
+    // host I/O executor for swapped stacks (separate streams for
+    // GPU-to-CPU and CPU-to-GPU transfers next to the compute stream)
+    std::atomic<bool> io_stop{false};
+    std::atomic<int> io_err{0};
+    std::thread io;
+    if (A.prog.n_swaps) {
+      *(volatile unsigned long long*)s->io_tail_host = 0;
+      io = std::thread([s, &io_stop, &io_err]() { io_executor(s, &io_stop, &io_err); });
+    }
     CUDA_OK(cudaEventRecord(s->ev0, s->stream));
-    CUDA_OK(cudaLaunchCooperativeKernel((void*)cf_driver_kernel, dim3(s->grid), dim3(kThreads), kargs,
-                                        s->dyn_smem, s->stream));
-    CUDA_OK(cudaEventRecord(s->ev1, s->stream));
-    CUDA_OK(cudaStreamSynchronize(s->stream));
+    cudaError_t lerr = cudaLaunchCooperativeKernel((void*)cf_driver_kernel, dim3(s->grid), dim3(kThreads),
+                                                   kargs, s->dyn_smem, s->stream);
+    if (lerr == cudaSuccess) lerr = cudaEventRecord(s->ev1, s->stream);
+    if (lerr == cudaSuccess) lerr = cudaStreamSynchronize(s->stream);
+    if (io.joinable()) {
+      io_stop = true;
+      io.join();
+      cudaStreamSynchronize(s->io_d2h);
+      cudaStreamSynchronize(s->io_h2d);
+    }
+    CUDA_OK(lerr);
+    if (io_err.load()) throw cf::CfError(CF_E_CUDA, "swap I/O copy failed");
     RunState st;
     CUDA_OK(cudaMemcpy(&st, A.st, sizeof(RunState), cudaMemcpyDeviceToHost));
     if (st.error) {
@@ -2589,6 +2797,10 @@ cf_status cf_run(cf_session* s, int32_t n_feed, const char* const* feed_names,
       trace->dead_skipped = st.dead_skipped;
       trace->sends = st.sends;
       trace->recvs = st.recvs;
+      trace->swap_out = st.swap_out;
+      trace->swap_in = st.swap_in;
+      trace->bytes_d2h = st.bytes_d2h;
+      trace->bytes_h2d = st.bytes_h2d;
       int nb = P.n_conds * P.branch_bound;
       trace->n_branch_bits = nb;
       if (trace->branch_bits && trace->branch_bits_cap > 0)
@@ -2739,6 +2951,9 @@ void cf_session_destroy(cf_session* s) {
   if (!s) return;
   for (void* p : s->allocs) cudaFree(p);
   for (auto& [r, p] : s->peer_mem) cudaIpcCloseMemHandle(p);
+  for (void* h : s->host_allocs) cudaFreeHost(h);
+  if (s->io_d2h) cudaStreamDestroy(s->io_d2h);
+  if (s->io_h2d) cudaStreamDestroy(s->io_h2d);
   if (s->chan_mem) cudaFree(s->chan_mem);
   if (s->ev0) cudaEventDestroy(s->ev0);
   if (s->ev1) cudaEventDestroy(s->ev1);
