@@ -518,6 +518,8 @@ struct Compiler {
     int counts[6] = {0, 0, 0, 0, 0, 0};
     for (auto& pl : P.places) counts[pl.kind]++;
     ds << "accumulators=" << P.accs.size() << " tma_operands=" << P.reg.size() << "\n";
+    ds << "structured frames=" << P.structured_frames << " cond contexts="
+       << (P.ctxs.empty() ? 0 : P.ctxs.size() - 1) << "\n";
     ds << "stacks: resident bytes=" << P.stack_resident_bytes << " swapped arenas=" << P.swaps.size()
        << " swapped bytes=" << P.stack_swapped_bytes << "\n";
     ds << "placements root=" << counts[0] << " ring=" << counts[1] << " arena=" << counts[2]
@@ -851,6 +853,67 @@ struct Compiler {
     P.reg.push_back(r);
   }
 
+  // ---- structured conds (reading R20). A frame body qualifies when every cond context in it
+  // is a builder cond (Switch/Merge only through cf_cond) holding no Send/Recv, and no control
+  // edge leaves a cond Switch. Fills alias (Switch output vid -> its data input vid) and the
+  // device context of every node of `ord`.
+  std::map<int, int> gctx_to_dctx;
+  int dctx_of(int c) {
+    if (g.ctxs[c].kind != COND) return 0;
+    auto it = gctx_to_dctx.find(c);
+    if (it != gctx_to_dctx.end()) return it->second;
+    if (P.ctxs.empty()) P.ctxs.push_back(DCtx{0, -1, 0, -1});
+    DCtx d{};
+    d.parent = dctx_of(g.ctxs[c].parent);
+    d.pred_vid = vid(g.ctxs[c].pred);
+    d.branch = g.ctxs[c].branch;
+    d.cond_id = g.ctxs[c].cond_id;
+    P.ctxs.push_back(d);
+    return gctx_to_dctx[c] = (int)P.ctxs.size() - 1;
+  }
+  bool structure_conds(const std::vector<int>& ord, std::map<int, int>* alias, std::vector<int>* nctx) {
+    std::set<int> sw;
+    for (int v : ord) {
+      const Node& n = g.nodes[v];
+      const bool in_cond = g.ctxs[n.ctx].kind == COND;
+      if (in_cond && (n.op == "Send" || n.op == "Recv")) return false;
+      if (in_cond && n.op == "Switch") {
+        if (n.attrs.b("loop")) return false;
+        sw.insert(v);
+      }
+    }
+    if (sw.empty()) return false;
+    for (int v : ord)
+      for (int c : g.nodes[v].ctrl)
+        if (sw.count(c)) return false;
+    // cond Merges must have both inputs produced inside their two branches
+    for (int v : ord)
+      if (g.nodes[v].op == "Merge" && !g.nodes[v].attrs.b("loop"))
+        if (merge_branch_ctx_g(v, 0) < 0 || merge_branch_ctx_g(v, 1) < 0) return false;
+    for (int v : sw) {
+      const Node& n = g.nodes[v];
+      (*alias)[vbase[v]] = vid(n.in[0]);
+      (*alias)[vbase[v] + 1] = vid(n.in[0]);
+    }
+    nctx->clear();
+    for (int v : ord) nctx->push_back(dctx_of(g.nodes[v].ctx));
+    if (P.ctxs.size() > 64) throw CfError(CF_E_UNSUPPORTED, "more than 63 cond contexts in one program");
+    // predicates may themselves be captures
+    for (auto& d : P.ctxs)
+      for (auto it = alias->find(d.pred_vid); it != alias->end(); it = alias->find(d.pred_vid))
+        d.pred_vid = it->second;
+    return true;
+  }
+  // graph cond context of Merge node m's input j (the branch child of m's context), or -1
+  int merge_branch_ctx_g(int m, int j) {
+    const Node& mn = g.nodes[m];
+    int c = g.nodes[mn.in[j].node].ctx;
+    while (c >= 0 && g.ctxs[c].parent != mn.ctx) c = g.ctxs[c].parent;
+    if (c < 0 || g.ctxs[c].kind != COND || g.ctxs[c].branch != j) return -1;
+    return c;
+  }
+  int merge_branch_ctx(int m, int j) { return dctx_of(merge_branch_ctx_g(m, j)); }
+
   void build_orders(const std::vector<int64_t>& bound) {
     const int N = (int)g.nodes.size();
     // arena allocation needs the bound. Stack swapping: when all arenas
@@ -959,6 +1022,35 @@ struct Compiler {
       }
       if (ord.size() != body.size())
         throw CfError(CF_E_INVALID_GRAPH, "frame " + ctx.name + " body has a cycle without NextIteration");
+      // ---- structured conds (reading R20): compile capture Switches away
+      std::map<int, int> alias;
+      std::vector<int> node_ctx;
+      if (structure_conds(ord, &alias, &node_ctx)) {
+        std::vector<int> kept, kctx;
+        for (size_t k = 0; k < ord.size(); ++k)
+          if (!(g.nodes[ord[k]].op == "Switch" && g.ctxs[g.nodes[ord[k]].ctx].kind == COND)) {
+            kept.push_back(ord[k]);
+            kctx.push_back(node_ctx[k]);
+          }
+        ord = kept;
+        node_ctx = kctx;
+        P.structured_frames++;
+      } else {
+        alias.clear();
+        node_ctx.assign(ord.size(), 0);
+      }
+      auto res = [&](int v) {
+        for (auto it = alias.find(v); it != alias.end(); it = alias.find(v)) v = it->second;
+        return v;
+      };
+      for (int v : ord) {
+        DNode& dn = P.nodes[v];
+        if (dn.place_off >= 0)
+          for (int p2 = 0; p2 < n_places(g.nodes[v]); ++p2) {
+            PlaceDesc& pl = P.places[dn.place_off + p2];
+            if (pl.kind == PL_TA) pl.index_vid = res(pl.index_vid);
+          }
+      }
       DFrame& F = P.frames[f];
       F.K = o.parallel_iterations > 0 ? o.parallel_iterations : ctx.K;
       F.bound = (int32_t)bound[f];
@@ -979,10 +1071,20 @@ struct Compiler {
       // driver can stage one frame's control program in shared memory
       F.bn_off = (int)P.body_nodes.size();
       F.bi_off = (int)P.body_ivids.size();
-      for (int v : ord) {
+      for (size_t k = 0; k < ord.size(); ++k) {
+        const int v = ord[k];
         DNode bn = P.nodes[v];
+        bn.ctx = node_ctx[k];
+        if (bn.ctx || alias.size()) P.nodes[v].ctx = bn.ctx;
+        if (bn.op == OP_MERGE && !alias.empty()) {
+          // structured cond Merge: inputs [false branch, true branch] (ir.cpp Graph::cond)
+          bn.aux[5] = merge_branch_ctx(v, 0);
+          bn.aux[6] = merge_branch_ctx(v, 1);
+          P.nodes[v].aux[5] = bn.aux[5];
+          P.nodes[v].aux[6] = bn.aux[6];
+        }
         int base = (int)P.body_ivids.size() - F.bi_off;
-        for (int j = 0; j < bn.n_in; ++j) P.body_ivids.push_back(P.in_vids[bn.in_off + j]);
+        for (int j = 0; j < bn.n_in; ++j) P.body_ivids.push_back(res(P.in_vids[bn.in_off + j]));
         for (int j = 0; j < bn.n_ctrl; ++j) P.body_ivids.push_back(P.in_vids[bn.ctrl_off + j]);
         bn.in_off = base;
         bn.ctrl_off = base + bn.n_in;

@@ -74,6 +74,8 @@ struct HostProgram {
   std::vector<BufPlan> bufs;
   std::vector<ChanPlan> chans;
   std::vector<SwapPlan> swaps;
+  std::vector<cfdev::DCtx> ctxs;     // [0] = loop level (unused entry)
+  int structured_frames = 0;
   int64_t stack_resident_bytes = 0, stack_swapped_bytes = 0;
   int64_t chan_bytes = 0;
   std::map<std::string, FeedInfo> feeds;

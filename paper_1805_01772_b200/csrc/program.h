@@ -113,8 +113,21 @@ struct DNode {
   int32_t place_off;   // into prog.places (n_out entries) for heavy nodes; -1 otherwise
   int32_t aux[7];
   int64_t imm[4];      // op-specific sizes / constants
+  int32_t ctx;         // structured cond context (prog.ctxs index; 0 = loop level)
+  int32_t pad[3];      // 16-byte records (the driver stages body programs with int4 copies)
 };
-static_assert(sizeof(DNode) % 8 == 0, "DNode layout");
+
+// Structured cond context of a frame body (reading R20): a branch of a cond is live iff its
+// parent is live and the predicate (a driver scalar) selects it; nodes of a dead branch are not
+// evaluated at all, capture Switches are compiled away, and the cond's Merges pick the live
+// branch's input.
+struct DCtx {
+  int32_t parent;      // 0 = loop level
+  int32_t pred_vid;    // value id of the cond predicate (in the parent context)
+  int32_t branch;      // 1 = true branch (Switch port 1)
+  int32_t cond_id;     // for the branch-bit trace
+};
+static_assert(sizeof(DNode) % 16 == 0, "DNode layout");
 
 // Fused loop accumulator ("sum gradients eagerly into new loop
 // variables"): one buffer updated in place by its producers, initialised at frame start.
@@ -222,8 +235,9 @@ struct Prog {
   int32_t precision;            // 3 = f32 SIMT, 5 = bf16 tcgen05
   int32_t n_chans;
   const DChan* chans;
-  int32_t n_swaps, pad3;
+  int32_t n_swaps, n_ctxs;
   const DSwap* swaps;
+  const DCtx* ctxs;
 };
 
 // ---- heavy instance record (written by the driver, read by workers)

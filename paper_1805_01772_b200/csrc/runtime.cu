@@ -511,6 +511,13 @@ struct Driver {
   long long n_push = 0, n_pop = 0, n_dead = 0, n_inst = 0, n_tiles = 0, n_sent = 0, n_recv = 0;
   long long op_cnt[32] = {}, op_cyc[32] = {};
   int32_t max_depth = 0, n_exitf = 0;
+  // structured cond contexts (reading R20): liveness per context, valid for generation lgen_
+  // (one generation per started iteration)
+  static constexpr int kMaxCtx = 64;
+  uint32_t lgen_ = 1;
+  uint32_t lstamp_[kMaxCtx];
+  int8_t lval_[kMaxCtx];
+  DCtx ctxs_[kMaxCtx];
   Tok* toks_;            // token table: driver-CTA shared memory when it fits, else global
   const int32_t* iv_;    // input-id table of the nodes being evaluated
   const DNode* bn_;      // current frame's body program (smem copy or global)
@@ -1775,6 +1782,42 @@ struct Driver {
     }
   }
 
+  // liveness of structured cond context c in the current iteration: 1 live, 0 dead, -1 the
+  // predicate is not available yet. Records the cond's branch bit like a live Switch would.
+  __noinline__ __device__ int ctx_live(int c) {
+    int chain[8];
+    int n = 0;
+    for (int x = c; x && lstamp_[x] != lgen_; x = ctxs_[x].parent) {
+      if (n == 8) {
+        fail(CF_E_UNSUPPORTED, -300);
+        return -1;
+      }
+      chain[n++] = x;
+    }
+    for (int k = n - 1; k >= 0; --k) {
+      const int x = chain[k];
+      const DCtx& cx = ctxs_[x];
+      int live = cx.parent ? lval_[cx.parent] : 1;
+      if (live) {
+        const Tok& pt = toks_[cx.pred_vid];
+        if (pt.dead) {
+          live = 0;
+        } else {
+          int64_t pv;
+          if (pt.kind == TK_IMM) pv = pt.v;
+          else if (!scalar(pt, &pv)) return -1;
+          live = (pv != 0) == (cx.branch == 1);
+          const int it = cur_frame >= 0 ? iter : 0;
+          if (cx.cond_id >= 0 && cx.cond_id < P.n_conds && it < P.branch_bound)
+            A.branch_bits[cx.cond_id * P.branch_bound + it] = pv ? 2 : 1;
+        }
+      }
+      lval_[x] = (int8_t)live;
+      lstamp_[x] = lgen_;
+    }
+    return lval_[c];
+  }
+
   // The per-iteration control loop: kept small and out of line so that its instructions stay
   // resident in the SM's instruction cache (the routing primitives dominate the node count).
   // The per-iteration control loop. Routing primitives are ~90% of the evaluations, so they
@@ -1795,6 +1838,16 @@ struct Driver {
       if ((pc & 15) == 0) drain();
       const DNode* d = bn_ + pc;
       const int op = d->op;
+      if (d->ctx) {   // node of a structured cond branch: skip it when the branch is dead
+        const int l = lval_[d->ctx] >= 0 && lstamp_[d->ctx] == lgen_ ? lval_[d->ctx] : ctx_live(d->ctx);
+        if (l < 0) break;
+        if (!l) {
+          if (op == OP_HEAVY) n_dead++;
+          ++pc;
+          progress = true;
+          continue;
+        }
+      }
       // token word w: dead (bits 0-7) | kind (8-15) | dt (16-23)
       if (op == OP_SWITCH && d->n_ctrl == 0) {
         long long cs0 = prof ? clock64() : 0;
@@ -1823,7 +1876,14 @@ struct Driver {
       } else if (op == OP_MERGE) {
         const int4 a = tk[iv[d->in_off]];
         const int4 b = tk[iv[d->in_off + 1]];
-        const int4 o = (a.w & 0xff) ? b : a;   // "if is_dead(d1) then d2 else d1"
+        int4 o = (a.w & 0xff) ? b : a;   // "if is_dead(d1) then d2 else d1"
+        if (d->aux[5]) {   // structured: the live branch's input (the other one was not evaluated)
+          const int l1 = ctx_live(d->aux[6]);
+          const int l0 = l1 > 0 ? 0 : ctx_live(d->aux[5]);
+          if (l1 < 0 || l0 < 0) break;
+          o = l1 ? b : a;
+          if (!l1 && !l0) o.w |= 1;
+        }
         tk[d->out_vid] = o;
         tk[d->ctrl_vid] = make_int4(0, 0, -1, (TK_FLOW << 8) | (o.w & 0xff));
         ++pc;
@@ -1891,6 +1951,7 @@ struct Driver {
       int infl = iter - oldest + 1;
       if (cur_frame < 16 && infl > st->max_inflight[cur_frame]) st->max_inflight[cur_frame] = infl;
       iter_started = true;
+      lgen_++;
       body_pc = 0;
     }
     bool progress = run_body(F);
@@ -2238,6 +2299,11 @@ __global__ void __launch_bounds__(kThreads, 1) cf_driver_kernel(RunArgs A_param)
         d.r_kfi = s_ring + 5120;
       }
       if (s_stk) d.stacks_ = s_stk;
+      for (int c = 0; c < P.n_ctxs && c < Driver::kMaxCtx; ++c) {
+        d.ctxs_[c] = P.ctxs[c];
+        d.lstamp_[c] = 0;
+        d.lval_[c] = 0;
+      }
       d.run();
       *(volatile int*)&req[0] = -1;
     } else if (threadIdx.x >= 32) {
@@ -2501,6 +2567,8 @@ void build_session(cf_session* s, const cf::Graph& g, const cf_run_opts* o,
   }
   A.prog.n_chans = (int32_t)s->chans.size();
   A.prog.chans = s->d_chans;
+  A.prog.n_ctxs = (int32_t)P.ctxs.size();
+  A.prog.ctxs = upload(s, P.ctxs);
   // ---- swapped stack arenas (a8)
   A.io_cap = 4096;
   if (!P.swaps.empty()) {
