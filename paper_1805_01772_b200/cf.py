@@ -443,7 +443,7 @@ class Session:
         [create, publish, first_start, last_end, busy_ns, kind, ntiles] rows and (t0, t1)."""
         import numpy as np
         n = C.c_int64()
-        t = (C.c_uint64 * 66)()
+        t = (C.c_uint64 * 130)()
         _check(_lib.cf_debug_session_profile(self.h, None, 0, C.byref(n), t))
         buf = np.zeros(6 * n.value, dtype=np.uint64)
         _check(_lib.cf_debug_session_profile(self.h, buf.ctypes.data, buf.size, C.byref(n), t))
@@ -452,7 +452,7 @@ class Session:
         out[:, :5] = r[:, :5].astype(np.float64)
         out[:, 5] = (r[:, 5] >> np.uint64(32)).astype(np.float64)
         out[:, 6] = (r[:, 5] & np.uint64(0xffffffff)).astype(np.float64)
-        self.driver_ops = [(int(t[2 + k]), int(t[34 + k])) for k in range(32)]
+        self.driver_ops = [(int(t[2 + k]), int(t[66 + k])) for k in range(64)]
         return out, (float(t[0]), float(t[1]))
 
     # ---- multi-GPU pipeline (include/cf.h "multi-GPU layer pipeline")

@@ -17,6 +17,7 @@
 #include "compiler.h"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <set>
@@ -519,7 +520,7 @@ struct Compiler {
     for (auto& pl : P.places) counts[pl.kind]++;
     ds << "accumulators=" << P.accs.size() << " tma_operands=" << P.reg.size() << "\n";
     ds << "structured frames=" << P.structured_frames << " cond contexts="
-       << (P.ctxs.empty() ? 0 : P.ctxs.size() - 1) << "\n";
+       << (P.ctxs.empty() ? 0 : P.ctxs.size() - 1) << " waves=" << P.n_waves << "\n";
     ds << "stacks: resident bytes=" << P.stack_resident_bytes << " swapped arenas=" << P.swaps.size()
        << " swapped bytes=" << P.stack_swapped_bytes << "\n";
     ds << "placements root=" << counts[0] << " ring=" << counts[1] << " arena=" << counts[2]
@@ -914,6 +915,108 @@ struct Compiler {
   }
   int merge_branch_ctx(int m, int j) { return dctx_of(merge_branch_ctx_g(m, j)); }
 
+  bool waveable(int v) const {
+    const DNode& d = P.nodes[v];
+    if (d.n_ctrl != 0) return false;
+    switch (d.op) {
+      case OP_MERGE: case OP_MERGE_LOOP: case OP_NEXTITER: case OP_SWITCH: return true;
+      case OP_STACK_PUSH: case OP_STACK_POP: return P.swaps.empty();
+      default: return false;
+    }
+  }
+  void form_waves(int f, std::vector<int>* ord, std::vector<int>* nctx, const std::map<int, int>& alias,
+                  std::vector<int>* wave_len) {
+    const int n = (int)ord->size();
+    wave_len->assign(n, 0);
+    if (std::getenv("CF_NO_LEVEL_ORDER")) return;   // debugging switch
+    std::map<int, int> pos;
+    for (int k = 0; k < n; ++k) pos[(*ord)[k]] = k;
+    std::vector<int> prod_of_vid(P.n_vids, -1);
+    for (int k = 0; k < n; ++k) {
+      const Node& nd = g.nodes[(*ord)[k]];
+      for (size_t p2 = 0; p2 < nd.odt.size(); ++p2) prod_of_vid[vbase[nd.id] + p2] = nd.id;
+    }
+    auto res = [&](int v) {
+      for (auto it = alias.find(v); it != alias.end(); it = alias.find(v)) v = it->second;
+      return v;
+    };
+    std::vector<int> level(n, 0);
+    std::vector<std::vector<int>> preds(n);
+    for (int k = 0; k < n; ++k) {
+      const int v = (*ord)[k];
+      if (P.nodes[v].op == OP_MERGE_LOOP) continue;   // sources within an iteration
+      const Node& nd = g.nodes[v];
+      for (auto& t : nd.in) {
+        int pv = prod_of_vid[res(vid(t))];
+        if (pv >= 0 && pos.count(pv)) preds[k].push_back(pos[pv]);
+      }
+      for (int c : nd.ctrl)
+        if (pos.count(c)) preds[k].push_back(pos[c]);
+    }
+    // extra edges may name a compiled-away cond Switch: use its data input's producer
+    auto node_res = [&](int a) {
+      for (int k2 = 0; k2 < 64 && !pos.count(a); ++k2) {
+        const Node& an = g.nodes[a];
+        if (an.op != "Switch" || an.in.empty()) break;
+        a = an.in[0].node;
+      }
+      return a;
+    };
+    for (auto& [a0, b] : extra_edges[f]) {
+      const int a = node_res(a0);
+      if (pos.count(a) && pos.count(b)) preds[pos[b]].push_back(pos[a]);
+    }
+    // a node of a structured cond branch reads its context's liveness, i.e. the predicates of
+    // the context chain: it must come after their producers (the compiled-away Switches
+    // carried that dependence)
+    for (int k = 0; k < n; ++k)
+      for (int c = (*nctx)[k]; c > 0; c = P.ctxs[c].parent) {
+        const int pv = prod_of_vid[P.ctxs[c].pred_vid];
+        if (pv >= 0 && pos.count(pv)) preds[k].push_back(pos[pv]);
+      }
+    for (int k = 0; k < n; ++k) {
+      const DNode& dn = P.nodes[(*ord)[k]];
+      if (dn.op == OP_MERGE && dn.aux[5] == 0 && g.nodes[(*ord)[k]].attrs.has("cond_id")) {
+        // structured Merge (aux set later): after its cond's predicate
+        for (int j = 0; j < 2; ++j) {
+          int bc = merge_branch_ctx_g((*ord)[k], j);
+          if (bc >= 0) {
+            const int pv = prod_of_vid[res(vid(g.ctxs[bc].pred))];
+            if (pv >= 0 && pos.count(pv)) preds[k].push_back(pos[pv]);
+          }
+        }
+      }
+    }
+    // a loop Merge reads the previous iteration's NextIteration token: the NextIteration of
+    // this iteration must come later (the Kahn order guarantees it; levels must too)
+    for (int k = 0; k < n; ++k)
+      if (P.nodes[(*ord)[k]].op == OP_NEXTITER)
+        for (auto [c, idx] : cons[vbase[(*ord)[k]]])
+          if (pos.count(c) && pos[c] < k) preds[k].push_back(pos[c]);
+    for (int k = 0; k < n; ++k)   // ord is topological: predecessors come first
+      for (int q : preds[k]) level[k] = std::max(level[k], level[q] + 1);
+    std::vector<int> idx(n);
+    for (int k = 0; k < n; ++k) idx[k] = k;
+    std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) {
+      if (level[a] != level[b]) return level[a] < level[b];
+      return waveable((*ord)[a]) > waveable((*ord)[b]);
+    });
+    std::vector<int> o2, c2;
+    for (int k : idx) {
+      o2.push_back((*ord)[k]);
+      c2.push_back((*nctx)[k]);
+    }
+    wave_len->assign(n, 0);
+    for (int k = 0; k < n && !std::getenv("CF_NO_WAVES");) {
+      int e = k;
+      while (e < n && waveable(o2[e]) && level[idx[e]] == level[idx[k]] && e - k < 256) ++e;
+      if (e - k >= 4) (*wave_len)[k] = e - k;
+      k = std::max(e, k + 1);
+    }
+    *ord = o2;
+    *nctx = c2;
+  }
+
   void build_orders(const std::vector<int64_t>& bound) {
     const int N = (int)g.nodes.size();
     // arena allocation needs the bound. Stack swapping: when all arenas
@@ -1051,12 +1154,19 @@ struct Compiler {
             if (pl.kind == PL_TA) pl.index_vid = res(pl.index_vid);
           }
       }
+      // ---- waves: order the body by dependency level and group each level's routing / stack
+      //      nodes (independent by construction) behind an OP_WAVE marker
+      std::vector<int> wave_len;   // per ord position: > 0 = a wave of that many starts here
+      form_waves(f, &ord, &node_ctx, alias, &wave_len);
       DFrame& F = P.frames[f];
       F.K = o.parallel_iterations > 0 ? o.parallel_iterations : ctx.K;
       F.bound = (int32_t)bound[f];
       F.body_off = (int)P.order.size();
-      F.n_body = (int)ord.size();
-      P.order.insert(P.order.end(), ord.begin(), ord.end());
+      for (size_t k = 0; k < ord.size(); ++k) {
+        if (wave_len[k] > 0) P.order.push_back(ord[k]);   // the marker's slot (never evaluated)
+        P.order.push_back(ord[k]);
+      }
+      F.n_body = (int)P.order.size() - F.body_off;
       F.enter_off = (int)P.order.size();
       F.n_enter = (int)enters.size();
       P.order.insert(P.order.end(), enters.begin(), enters.end());
@@ -1073,6 +1183,26 @@ struct Compiler {
       F.bi_off = (int)P.body_ivids.size();
       for (size_t k = 0; k < ord.size(); ++k) {
         const int v = ord[k];
+        if (wave_len[k] > 0) {
+          DNode wm{};
+          wm.op = OP_WAVE;
+          wm.aux[0] = wave_len[k];
+          unsigned long long mask = 0;   // contexts the wave's nodes read
+          for (int q = 0; q < wave_len[k]; ++q) {
+            const int u = ord[k + q];
+            if (node_ctx[k + q] > 0) mask |= 1ULL << node_ctx[k + q];
+            if (P.nodes[u].op == OP_MERGE && g.nodes[u].attrs.has("cond_id") && !alias.empty()) {
+              int c0 = merge_branch_ctx(u, 0), c1 = merge_branch_ctx(u, 1);
+              if (c0 > 0) mask |= 1ULL << c0;
+              if (c1 > 0) mask |= 1ULL << c1;
+            }
+          }
+          wm.imm[0] = (int64_t)mask;
+          wm.place_off = -1;
+          wm.in_off = wm.ctrl_off = (int)P.body_ivids.size() - F.bi_off;
+          P.body_nodes.push_back(wm);
+          P.n_waves++;
+        }
         DNode bn = P.nodes[v];
         bn.ctx = node_ctx[k];
         if (bn.ctx || alias.size()) P.nodes[v].ctx = bn.ctx;
@@ -1092,7 +1222,7 @@ struct Compiler {
       }
       F.bi_count = (int)P.body_ivids.size() - F.bi_off;
       while (P.body_ivids.size() % 4) P.body_ivids.push_back(0);   // 16 B aligned segments
-      P.max_body = std::max(P.max_body, (int)ord.size());
+      P.max_body = std::max(P.max_body, F.n_body);
       P.max_bi = std::max(P.max_bi, F.bi_count);
       F.acc_off = (int)P.order.size();
       F.n_acc = 0;

@@ -51,6 +51,8 @@ enum Op : int32_t {
   OP_ACC,           // fused accumulator Add (aux0: acc id): output = the accumulator buffer
   OP_SEND,          // cross-GPU Send (aux0: channel index)
   OP_RECV,          // cross-GPU Recv (aux0: channel index); output placed like a heavy output
+  OP_WAVE,          // body-program marker: the next aux0 nodes are independent routing / stack
+                    // nodes, evaluated in parallel by the driver CTA's helper warps
   OP__COUNT
 };
 
@@ -275,7 +277,7 @@ struct RunState {
   int32_t max_depth, exit_fires;
   long long instances, tiles, dead_skipped;
   unsigned long long t_start, t_end;
-  long long op_count[32], op_cycles[32];   // driver self-profile per opcode (+ drain at 31)
+  long long op_count[64], op_cycles[64];   // driver self-profile: opcodes [0,32), regions [32,64)
 };
 
 struct RunArgs {

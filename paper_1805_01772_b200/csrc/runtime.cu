@@ -479,6 +479,146 @@ __device__ void tile_lstm_bwd_mm(const Inst& I, int tile, float* sm) {
 // ----------------------------------------------------------------------------- driver
 enum EvalResult { EV_OK = 0, EV_BLOCKED = 1, EV_ERROR = 2 };
 
+// ---- routing / stack nodes without the general evaluator (PAPER.md:712-735 rules on 16-byte
+// tokens; token word w = dead (bits 0-7) | kind (8-15) | dt (16-23)). Shared by the driver
+// thread and the helper warps that evaluate a wave of independent nodes in parallel.
+struct FastEnv {
+  int4* tk;
+  const int32_t* iv;
+  int it, bb;
+  uint8_t* bbits;
+  const int8_t* lval;        // liveness of structured cond contexts (this iteration)
+  const DStack* stacks;
+  int32_t* depth;
+  int4* pool;
+};
+struct FastCount {
+  int push, pop, maxd, err, err_info;
+};
+// 1 = evaluated, 0 = needs the general evaluator (nothing written), -1 = error (in c.err)
+__device__ __forceinline__ int fast_node(const DNode* d, const FastEnv& e, FastCount& c) {
+  const int op = d->op;
+  int4* tk = e.tk;
+  const int32_t* iv = e.iv;
+  if (op == OP_SWITCH) {
+    if (d->n_ctrl) return 0;
+    const int4 dv = tk[iv[d->in_off]];
+    const int4 pt = tk[iv[d->in_off + 1]];
+    const int dead = (dv.w | pt.w) & 0xff;
+    if (((pt.w >> 8) & 0xff) != TK_IMM && !dead) return 0;
+    int4 o0 = dv, o1 = dv;
+    if (dead) {
+      o0.w |= 1;
+      o1.w |= 1;
+    } else {
+      const bool p = (pt.x | pt.y) != 0;
+      o0.w = (o0.w & ~0xff) | (p ? 1 : 0);   // false port dead iff p
+      o1.w = (o1.w & ~0xff) | (p ? 0 : 1);
+      if (d->aux[0] >= 0 && e.it < e.bb) e.bbits[d->aux[0] * e.bb + e.it] = p ? 2 : 1;
+    }
+    tk[d->out_vid] = o0;
+    tk[d->out_vid + 1] = o1;
+    tk[d->ctrl_vid] = make_int4(0, 0, -1, (TK_FLOW << 8) | dead);
+    return 1;
+  }
+  if (op == OP_MERGE) {
+    const int4 a = tk[iv[d->in_off]];
+    const int4 b = tk[iv[d->in_off + 1]];
+    int4 o = (a.w & 0xff) ? b : a;   // "if is_dead(d1) then d2 else d1"
+    if (d->aux[5]) {   // structured: the live branch's input (the other one was not evaluated)
+      const int l1 = e.lval[d->aux[6]], l0 = e.lval[d->aux[5]];
+      o = l1 ? b : a;
+      if (!l1 && !l0) o.w |= 1;
+    }
+    tk[d->out_vid] = o;
+    tk[d->ctrl_vid] = make_int4(0, 0, -1, (TK_FLOW << 8) | (o.w & 0xff));
+    return 1;
+  }
+  if (op == OP_MERGE_LOOP || (op == OP_NEXTITER && !d->n_ctrl)) {
+    const int4 o = tk[iv[d->in_off + (op == OP_MERGE_LOOP && e.it != 0 ? 1 : 0)]];
+    tk[d->out_vid] = o;
+    tk[d->ctrl_vid] = make_int4(0, 0, -1, (TK_FLOW << 8) | (o.w & 0xff));
+    return 1;
+  }
+  if ((op == OP_STACK_PUSH || op == OP_STACK_POP) && !d->n_ctrl) {
+    const int4 h = tk[iv[d->in_off]];
+    const int4 v = op == OP_STACK_PUSH ? tk[iv[d->in_off + 1]] : h;
+    const int dead = (h.w | v.w) & 0xff;
+    if (dead) {   // dead push: nothing stored; dead pop: dead output
+      if (op == OP_STACK_POP) {
+        int4 t = make_int4(0, 0, -1, 1);
+        tk[d->out_vid] = t;
+      }
+      tk[d->ctrl_vid] = make_int4(0, 0, -1, (TK_FLOW << 8) | 1);
+      return 1;
+    }
+    const int sid = h.x;   // TK_HANDLE: v = stack id
+    const DStack& S = e.stacks[sid];
+    const int dp = e.depth[sid];
+    int4* pool = e.pool + S.entry_off;
+    if (op == OP_STACK_PUSH) {
+      if (dp >= S.capacity) {
+        c.err = CF_E_STACK_BUDGET;
+        c.err_info = dp;
+        return -1;
+      }
+      pool[dp] = v;
+      e.depth[sid] = dp + 1;
+      c.push++;
+      c.maxd = max(c.maxd, dp + 1);
+    } else {
+      if (dp <= 0) {
+        c.err = CF_E_POP_EMPTY;
+        c.err_info = sid;
+        return -1;
+      }
+      int4 t = pool[dp - 1];
+      t.w &= ~0xff;
+      e.depth[sid] = dp - 1;
+      tk[d->out_vid] = t;
+      c.pop++;
+    }
+    tk[d->ctrl_vid] = make_int4(0, 0, -1, TK_FLOW << 8);
+    return 1;
+  }
+  return 0;
+}
+
+// helper warps serving waves: warps 1-3 and 5-7 (warp 4 shares the driver warp's scheduler)
+constexpr int kWaveWarps = 6;
+__device__ __forceinline__ int wave_lane(int tid) {
+  const int w = tid >> 5;
+  return w < 4 ? tid - 32 : tid - 64;   // 0..191 for warps 1-3, 5-7
+}
+
+// a wave request from the driver thread to the helper warps (shared memory)
+struct Wave {
+  int seq, done;          // request number / helper warps finished
+  int start, n;           // body program range
+  int nslow;
+  FastCount cnt;
+  const DNode* bn;
+  FastEnv env;
+  int slow[256];          // wave positions left for the general evaluator
+};
+
+__device__ void wave_work(Wave& w, int h, int nh) {
+  FastCount c{0, 0, 0, 0, 0};
+  for (int j = h; j < w.n; j += nh) {
+    const DNode* d = w.bn + w.start + j;
+    if (d->ctx && !w.env.lval[d->ctx]) continue;   // node of a dead cond branch
+    const int r = fast_node(d, w.env, c);
+    if (r == 0) w.slow[atomicAdd(&w.nslow, 1)] = j;
+    if (r < 0) {
+      w.cnt.err = c.err;
+      w.cnt.err_info = c.err_info;
+    }
+  }
+  if (c.push) atomicAdd(&w.cnt.push, c.push);
+  if (c.pop) atomicAdd(&w.cnt.pop, c.pop);
+  if (c.maxd) atomicMax(&w.cnt.maxd, c.maxd);
+}
+
 struct Driver {
   const RunArgs& A;
   const Prog& P;
@@ -509,7 +649,7 @@ struct Driver {
   int32_t* iter_out_;
   const DStack* stacks_;
   long long n_push = 0, n_pop = 0, n_dead = 0, n_inst = 0, n_tiles = 0, n_sent = 0, n_recv = 0;
-  long long op_cnt[32] = {}, op_cyc[32] = {};
+  long long op_cnt[64] = {}, op_cyc[64] = {};   // [0, 32) opcodes, [32, 64) regions
   int32_t max_depth = 0, n_exitf = 0;
   // structured cond contexts (reading R20): liveness per context, valid for generation lgen_
   // (one generation per started iteration)
@@ -530,6 +670,69 @@ struct Driver {
         stack_depth_(a.stack_depth), prep_inst_(a.prep_inst), dw_count_(a.dw_count),
         acc_writer_(a.acc_writer), iter_out_(a.iter_outstanding), stacks_(a.prog.stacks),
         toks_(t), iv_(a.prog.in_vids), bn_(nullptr), sm_nodes_(smn), sm_iv_(smi), req_(req) {}
+  Wave* wave_ = nullptr;
+
+  __device__ FastEnv fast_env() {
+    FastEnv e;
+    e.tk = (int4*)toks_;
+    e.iv = iv_;
+    e.it = cur_frame >= 0 ? iter : 0;
+    e.bb = P.branch_bound;
+    e.bbits = A.branch_bits;
+    e.lval = lval_;
+    e.stacks = stacks_;
+    e.depth = stack_depth_;
+    e.pool = (int4*)A.stack_pool;
+    return e;
+  }
+
+  // OP_WAVE at body position pc: liveness of the contexts its nodes need, then the helper
+  // warps evaluate the n nodes in parallel; leftovers go through the general evaluator.
+  // Returns the number of body positions consumed (n + 1), or 1 to run the nodes serially.
+  __noinline__ __device__ int run_wave(const DFrame& F, int pc, int n) {
+    Region rg(this, 32 + 13);
+    // contexts whose liveness the wave's nodes read (bit mask from the compiler, marker imm0)
+    for (unsigned long long m = (unsigned long long)bn_[pc].imm[0]; m; m &= m - 1)
+      if (ctx_live(__ffsll((long long)m) - 1) < 0) return 1;
+    Wave& w = *wave_;
+    w.start = pc + 1;
+    w.n = n;
+    w.nslow = 0;
+    w.cnt = FastCount{0, 0, 0, 0, 0};
+    w.bn = bn_;
+    w.env = fast_env();
+    w.done = 0;
+    __threadfence_block();
+    *(volatile int*)&w.seq = w.seq + 1;
+    while (*(volatile int*)&w.done < kWaveWarps) {
+    }
+    __threadfence_block();
+    n_push += w.cnt.push;
+    n_pop += w.cnt.pop;
+    if (w.cnt.maxd > max_depth) max_depth = w.cnt.maxd;
+    if (w.cnt.err) {
+      fail(w.cnt.err, w.cnt.err_info);
+      return n + 1;
+    }
+    // leftovers (e.g. a Switch whose predicate is a device value): in wave order
+    for (int a = 0; a < w.nslow; ++a)
+      for (int b = a + 1; b < w.nslow; ++b)
+        if (w.slow[b] < w.slow[a]) {
+          int t = w.slow[a];
+          w.slow[a] = w.slow[b];
+          w.slow[b] = t;
+        }
+    for (int a = 0; a < w.nslow; ++a) {
+      const int q = pc + 1 + w.slow[a];
+      while (true) {
+        const int r = eval(bn_[q], P.order[F.body_off + q]);
+        if (r == EV_OK) break;
+        if (r == EV_ERROR || st->error) return n + 1;
+        drain();   // the predicate's producer has to finish first
+      }
+    }
+    return n + 1;
+  }
 
   // ask the helper warps to copy [src, src+bytes) -> dst (16 B aligned), wait for them
   __device__ void helper_copy(void* dst0, const void* src0, int64_t b0, void* dst1, const void* src1,
@@ -627,7 +830,7 @@ struct Driver {
   };
 
   __noinline__ __device__ int32_t new_inst(int kind, int sub, int ntiles) {
-    Region rg(this, 26);
+    Region rg(this, 32 + 1);
     if (ninst >= A.inst_cap) {
       fail(CF_E_STACK_BUDGET, -1);
       return -1;
@@ -667,6 +870,7 @@ struct Driver {
     return id;
   }
   __noinline__ __device__ void add_dep(int32_t id, int32_t w) {
+    Region rg(this, 32 + 5);
     if (done(w)) return;
     const int ws = w & kRingMask;
     if (r_last[ws] == id) return;   // dedupe repeated inputs from the same producer
@@ -684,7 +888,7 @@ struct Driver {
   // two rings: critical-path work (high) and filler work (low: dW chunks) so that the
   // recurrence never queues behind throughput work
   __noinline__ __device__ void publish(int32_t id) {
-    Region rg(this, 27);
+    Region rg(this, 32 + 2);
     const int sl = id & kRingMask;
     if ((r_kfi[sl] & 255) == HK_SWAP) {   // to the host I/O thread's copy streams
       const Inst& I = A.insts[id];
@@ -719,6 +923,7 @@ struct Driver {
     if (r_pend[sl] == 0) publish(id);
   }
   __noinline__ __device__ void complete(int32_t id) {
+    Region rg(this, 32 + 12);
     const int sl = id & kRingMask;
     outstanding--;
     const int kfi = r_kfi[sl];
@@ -736,6 +941,7 @@ struct Driver {
   // completions of swap copies: written by the copy streams into io_cq (id + 1), possibly out
   // of order between the D2H and H2D streams; consumed slots are marked -1
   __noinline__ __device__ bool drain_io() {
+    Region rg(this, 32 + 11);
     bool any = false;
     const unsigned long long m = (unsigned long long)(A.io_cap - 1);
     for (unsigned long long j = io_head; j < io_tail; ++j) {
@@ -756,12 +962,14 @@ struct Driver {
     return any;
   }
   __noinline__ __device__ bool drain() {
-    Region rg(this, 29);
+    Region rg(this, 32 + 4);
     bool any = false;
     if (io_out > 0) any = drain_io();
     for (int k = 0; k < 256; ++k) {
       int* p = &A.cq[cq_head & (A.cq_cap - 1)];
-      int v = ld_acquire_i32(p);   // pairs with the worker's release of its completion
+      // relaxed poll (an acquire load would invalidate L1 at every poll); the release store
+      // that publishes successors orders this observation before them (fence.acq_rel)
+      int v = ld_volatile_i32(p);
       if (v == 0) break;
       *(volatile int*)p = 0;
       cq_head++;
@@ -773,7 +981,7 @@ struct Driver {
 
   // ---------------------------------------------------------------- placement
   __noinline__ __device__ bool place(const DNode& d, int port, int64_t* ptr) {
-    Region rg(this, 31);
+    Region rg(this, 32 + 6);
     const PlaceDesc& pl = places_[d.place_off + port];
     int it = cur_frame >= 0 ? iter : 0;
     switch (pl.kind) {
@@ -822,7 +1030,7 @@ struct Driver {
   // pointer -> (tensor map, slot) for a bf16 [rows][cols] GEMM operand; kind 0 = K-major A
   // (box 64x128), 1 = K-major B (box 64x256), 2 = MN-major (box 64x64)
   __noinline__ __device__ bool resolve(int64_t p, int rows, int cols, int kind, int64_t* map, int64_t* slot) {
-    Region rg(this, 28);
+    Region rg(this, 32 + 3);
     // entries are sorted by base (host): binary search for the last base <= p, then the
     // entries sharing that base (one buffer registered under several shapes)
     int lo = 0, hi = P.n_reg - 1, at = -1;
@@ -857,6 +1065,7 @@ struct Driver {
 
   // per-run weight preparation (bf16 permuted W / W^T), created on first use of the node
   __noinline__ __device__ int32_t prep(const DNode& d, int nid, int kind, int64_t dst) {
+    Region rg(this, 32 + 7);
     if (prep_inst_[nid] >= 0) return prep_inst_[nid];
     const int64_t In = d.imm[1], H = d.imm[2], KT = In + H;
     int ntiles = kind == HK_PREP_WP ? (int)((4 * H + 15) / 16) : (int)((KT / 64) * (4 * H / 128));
@@ -874,6 +1083,7 @@ struct Driver {
   }
 
   __noinline__ __device__ int eval_lstm_tc(const DNode& d, int nid, const int64_t* outp) {
+    Region rg(this, 32 + 9);
     const int kind = d.aux[0];
     const bool masked = d.aux[1] & 1;
     int64_t t = 0;
@@ -967,6 +1177,7 @@ struct Driver {
 
   // create the dW/db instance for the queued steps of LSTMCellGrad node nid
   __noinline__ __device__ int32_t flush_dw(const DNode& d, int nid, int64_t mzn, int64_t dw_ptr, int64_t db_ptr) {
+    Region rg(this, 32 + 8);
     const int cnt = dw_count_[nid];
     if (cnt == 0) return 0;
     const int64_t B = d.imm[0], In = d.imm[1], H = d.imm[2], KT = In + H;
@@ -1002,6 +1213,7 @@ struct Driver {
 
   // ---------------------------------------------------------------- heavy ops
   __noinline__ __device__ int eval_heavy(const DNode& d, int nid) {
+    Region rg(this, 32 + 10);
     const int kind = d.aux[0];
     int64_t outp[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     const bool tcm = P.precision == D_BF16;
@@ -1824,16 +2036,13 @@ struct Driver {
   // get a tiny straight-line path (16-byte token moves, no calls) at the head of the loop;
   // everything else goes through the out-of-line eval().
   __noinline__ __device__ bool run_body(const DFrame& F) {
-    Region rg(this, 25);
+    Region rg(this, 32 + 0);
     bool progress = false;
     const bool prof = A.prof != nullptr;
-    int4* tk = (int4*)toks_;
-    const int32_t* iv = iv_;
     const int n_body = F.n_body;
-    const int it = iter;
-    const int bb = P.branch_bound;
-    uint8_t* bbits = A.branch_bits;
     int pc = body_pc;
+    const FastEnv env = fast_env();
+    FastCount fc{0, 0, 0, 0, 0};
     while (pc < n_body) {
       if ((pc & 15) == 0) drain();
       const DNode* d = bn_ + pc;
@@ -1848,61 +2057,26 @@ struct Driver {
           continue;
         }
       }
-      // token word w: dead (bits 0-7) | kind (8-15) | dt (16-23)
-      if (op == OP_SWITCH && d->n_ctrl == 0) {
+      if (op == OP_WAVE) {
+        pc += run_wave(F, pc, d->aux[0]);
+        progress = true;
+        if (st->error) break;
+        continue;
+      }
+      if (op == OP_MERGE && d->aux[5] && (ctx_live(d->aux[6]) < 0 || ctx_live(d->aux[5]) < 0)) break;
+      if (op <= OP_NEXTITER || op == OP_STACK_PUSH || op == OP_STACK_POP) {
         long long cs0 = prof ? clock64() : 0;
-        const int4 dv = tk[iv[d->in_off]];
-        const int4 pt = tk[iv[d->in_off + 1]];
-        if (((pt.w >> 8) & 0xff) == TK_IMM || ((dv.w | pt.w) & 0xff)) {
-          int4 o0 = dv, o1 = dv;
-          const int dead = (dv.w | pt.w) & 0xff;
-          if (dead) {
-            o0.w |= 1;
-            o1.w |= 1;
-          } else {
-            const bool p = (pt.x | pt.y) != 0;
-            o0.w = (o0.w & ~0xff) | (p ? 1 : 0);   // false port dead iff p
-            o1.w = (o1.w & ~0xff) | (p ? 0 : 1);
-            if (d->aux[0] >= 0 && it < bb) bbits[d->aux[0] * bb + it] = p ? 2 : 1;
-          }
-          tk[d->out_vid] = o0;
-          tk[d->out_vid + 1] = o1;
-          tk[d->ctrl_vid] = make_int4(0, 0, -1, (TK_FLOW << 8) | dead);
+        const int r = P.n_swaps && (op == OP_STACK_PUSH || op == OP_STACK_POP) ? 0 : fast_node(d, env, fc);
+        if (r < 0) {
+          fail(fc.err, fc.err_info);
+          break;
+        }
+        if (r > 0) {
           ++pc;
           progress = true;
-          if (prof) { op_cyc[30] += clock64() - cs0; op_cnt[30]++; }
+          if (prof) { op_cyc[62] += clock64() - cs0; op_cnt[62]++; }
           continue;
         }
-      } else if (op == OP_MERGE) {
-        const int4 a = tk[iv[d->in_off]];
-        const int4 b = tk[iv[d->in_off + 1]];
-        int4 o = (a.w & 0xff) ? b : a;   // "if is_dead(d1) then d2 else d1"
-        if (d->aux[5]) {   // structured: the live branch's input (the other one was not evaluated)
-          const int l1 = ctx_live(d->aux[6]);
-          const int l0 = l1 > 0 ? 0 : ctx_live(d->aux[5]);
-          if (l1 < 0 || l0 < 0) break;
-          o = l1 ? b : a;
-          if (!l1 && !l0) o.w |= 1;
-        }
-        tk[d->out_vid] = o;
-        tk[d->ctrl_vid] = make_int4(0, 0, -1, (TK_FLOW << 8) | (o.w & 0xff));
-        ++pc;
-        progress = true;
-        continue;
-      } else if (op == OP_MERGE_LOOP) {
-        const int4 o = tk[iv[d->in_off + (it == 0 ? 0 : 1)]];
-        tk[d->out_vid] = o;
-        tk[d->ctrl_vid] = make_int4(0, 0, -1, (TK_FLOW << 8) | (o.w & 0xff));
-        ++pc;
-        progress = true;
-        continue;
-      } else if (op == OP_NEXTITER && d->n_ctrl == 0) {
-        const int4 o = tk[iv[d->in_off]];
-        tk[d->out_vid] = o;
-        tk[d->ctrl_vid] = make_int4(0, 0, -1, (TK_FLOW << 8) | (o.w & 0xff));
-        ++pc;
-        progress = true;
-        continue;
       }
       body_pc = pc;
       long long c0 = prof ? clock64() : 0;
@@ -1916,6 +2090,9 @@ struct Driver {
       progress = true;
     }
     body_pc = pc;
+    n_push += fc.push;
+    n_pop += fc.pop;
+    if (fc.maxd > max_depth) max_depth = fc.maxd;
     return progress;
   }
 
@@ -2011,23 +2188,6 @@ struct Driver {
     }
   }
 
-  __device__ void calibrate() {
-    // driver self-calibration (profiling): cycles per primitive, into op_cyc[24..27]
-    long long c0 = clock64();
-    for (int i = 0; i < 1000; ++i) asm volatile("");
-    long long c1 = clock64();
-    volatile Tok* tv = toks_;
-    for (int i = 0; i < 1000; ++i) { Tok t = ((Tok*)tv)[i % 64]; ((Tok*)tv)[64 + (i % 64)] = t; }
-    long long c2 = clock64();
-    for (int i = 0; i < 1000; ++i) A.branch_bits[i % 64] = 0;
-    long long c3 = clock64();
-    int acc = 0;
-    for (int i = 0; i < 1000; ++i) acc += ((volatile int*)iv_)[i % 64];
-    long long c4 = clock64();
-    op_cyc[26] = c1 - c0; op_cyc[27] = c2 - c1; op_cyc[28] = c3 - c2; op_cyc[29] = c4 - c3 + (acc == 12345);
-    op_cnt[26] = op_cnt[27] = op_cnt[28] = op_cnt[29] = 1000;
-  }
-
   __device__ void run() {
     st->t_start = globaltimer();
     last_progress = st->t_start;
@@ -2066,7 +2226,7 @@ struct Driver {
     if (!st->error)
       for (int c = 0; c < P.n_chans; ++c)
         if (P.chans[c].role == 0) st_release_sys_u64(P.chans[c].done, A.epoch);
-    for (int k = 0; k < 32; ++k) {
+    for (int k = 0; k < 64; ++k) {
       st->op_count[k] = op_cnt[k];
       st->op_cycles[k] = op_cyc[k];
     }
@@ -2222,6 +2382,7 @@ __global__ void __launch_bounds__(kThreads, 1) cf_driver_kernel(RunArgs A_param)
   if (blockIdx.x == 0) {
     extern __shared__ __align__(1024) uint8_t drv_smem[];
     __shared__ int req[16];   // [0] seq (-1: quit), [1] helpers done, [4..15] copy args
+    __shared__ Wave wave;     // routing waves evaluated by the helper warps
     Tok* toks = A.toks;
     DNode* smn = nullptr;
     int32_t* smi = nullptr;
@@ -2274,6 +2435,8 @@ __global__ void __launch_bounds__(kThreads, 1) cf_driver_kernel(RunArgs A_param)
     if (threadIdx.x == 0) {
       req[0] = 0;
       req[1] = 0;
+      wave.seq = 0;
+      wave.done = 0;
     }
     __syncthreads();
     // the driver object itself lives in shared memory: its members are touched on every node
@@ -2281,6 +2444,7 @@ __global__ void __launch_bounds__(kThreads, 1) cf_driver_kernel(RunArgs A_param)
     __shared__ __align__(16) unsigned char drv_obj[sizeof(Driver)];
     if (threadIdx.x == 0) {
       Driver& d = *new (drv_obj) Driver(A, toks, smn, smi, req);
+      d.wave_ = &wave;
       if (s_pl) d.places_ = s_pl;
       if (s_reg) d.reg_ = s_reg;
       if (s_sd) d.stack_depth_ = s_sd;
@@ -2308,13 +2472,23 @@ __global__ void __launch_bounds__(kThreads, 1) cf_driver_kernel(RunArgs A_param)
       *(volatile int*)&req[0] = -1;
     } else if (threadIdx.x >= 32) {
       // helper warps: cooperative smem staging on request from the driver thread
-      int seen = 0;
+      int seen = 0, wseen = 0;
       const int h = threadIdx.x - 32, nh = blockDim.x - 32;
       while (true) {
         int q = *(volatile int*)&req[0];
         if (q < 0) break;
+        const int ws = (threadIdx.x >> 5) == 4 ? wseen : *(volatile int*)&wave.seq;
+        if (ws != wseen) {
+          wseen = ws;
+          __threadfence_block();
+          wave_work(wave, wave_lane(threadIdx.x), 32 * kWaveWarps);
+          __threadfence_block();
+          __syncwarp();
+          if ((threadIdx.x & 31) == 0) atomicAdd(&wave.done, 1);
+          continue;
+        }
         if (q == seen) {
-          __nanosleep(500);
+          __nanosleep((threadIdx.x >> 5) == 4 ? 500 : 20);
           continue;
         }
         seen = q;
@@ -3003,9 +3177,9 @@ int32_t cf_debug_session_profile(const cf_session* s, unsigned long long* out, i
   if (t0) {
     t0[0] = st.t_start;
     t0[1] = st.t_end;
-    for (int k = 0; k < 32; ++k) {
+    for (int k = 0; k < 64; ++k) {
       t0[2 + k] = (unsigned long long)st.op_count[k];
-      t0[34 + k] = (unsigned long long)st.op_cycles[k];
+      t0[66 + k] = (unsigned long long)st.op_cycles[k];
     }
   }
   if (out && cap > 0) {

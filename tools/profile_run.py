@@ -61,10 +61,16 @@ for k in np.unique(rows[:, 5]).astype(int):
 os.makedirs(os.path.dirname(a.out), exist_ok=True)
 OPS = ["NOP", "PLACEHOLDER", "CONST", "PASS", "SWITCH", "MERGE", "MERGE_LOOP", "ENTER", "EXIT",
        "NEXTITER", "SCALAR", "REDUCE_I", "SLICE_I", "FLOW", "TA_CREATE", "TA_READ", "TA_WRITE",
-       "TA_STACK", "TA_UNSTACK", "TA_GRAD", "STACK_CREATE", "STACK_PUSH", "STACK_POP", "HEAVY", "ACC"]
-OPS = OPS + ["R_RUN_BODY", "R_NEW_INST", "R_PUBLISH", "R_RESOLVE", "R_DRAIN", "R_IDLE", "R_PLACE"]
+       "TA_STACK", "TA_UNSTACK", "TA_GRAD", "STACK_CREATE", "STACK_PUSH", "STACK_POP", "HEAVY", "ACC",
+       "SEND", "RECV"]
+OPS = OPS + ["?%d" % k for k in range(len(OPS), 32)]
+OPS += ["R_RUN_BODY", "R_NEW_INST", "R_PUBLISH", "R_RESOLVE", "R_DRAIN", "R_ADD_DEP", "R_PLACE",
+        "R_PREP", "R_FLUSH_DW", "R_EVAL_LSTM_TC", "R_EVAL_HEAVY", "R_DRAIN_IO", "R_COMPLETE",
+        "R_WAVE"]
+OPS = OPS + ["?%d" % k for k in range(len(OPS), 62)] + ["R_SWITCH_FAST", "?63"]
 res["driver"] = {OPS[k]: {"n": n, "us": cyc / 1965.0}
                  for k, (n, cyc) in enumerate(s.driver_ops) if n}
+res["describe"] = s.describe()
 json.dump(res, open(a.out, "w"), indent=1)
 rel = rows.copy()
 rel[:, :4] = np.where(rel[:, :4] > 1.8e19, np.nan, rel[:, :4] - t0)
