@@ -830,7 +830,6 @@ struct Driver {
   };
 
   __noinline__ __device__ int32_t new_inst(int kind, int sub, int ntiles) {
-    Region rg(this, 32 + 1);
     if (ninst >= A.inst_cap) {
       fail(CF_E_STACK_BUDGET, -1);
       return -1;
@@ -870,7 +869,6 @@ struct Driver {
     return id;
   }
   __noinline__ __device__ void add_dep(int32_t id, int32_t w) {
-    Region rg(this, 32 + 5);
     if (done(w)) return;
     const int ws = w & kRingMask;
     if (r_last[ws] == id) return;   // dedupe repeated inputs from the same producer
@@ -888,7 +886,6 @@ struct Driver {
   // two rings: critical-path work (high) and filler work (low: dW chunks) so that the
   // recurrence never queues behind throughput work
   __noinline__ __device__ void publish(int32_t id) {
-    Region rg(this, 32 + 2);
     const int sl = id & kRingMask;
     if ((r_kfi[sl] & 255) == HK_SWAP) {   // to the host I/O thread's copy streams
       const Inst& I = A.insts[id];
@@ -923,7 +920,6 @@ struct Driver {
     if (r_pend[sl] == 0) publish(id);
   }
   __noinline__ __device__ void complete(int32_t id) {
-    Region rg(this, 32 + 12);
     const int sl = id & kRingMask;
     outstanding--;
     const int kfi = r_kfi[sl];
@@ -981,7 +977,6 @@ struct Driver {
 
   // ---------------------------------------------------------------- placement
   __noinline__ __device__ bool place(const DNode& d, int port, int64_t* ptr) {
-    Region rg(this, 32 + 6);
     const PlaceDesc& pl = places_[d.place_off + port];
     int it = cur_frame >= 0 ? iter : 0;
     switch (pl.kind) {
@@ -1030,7 +1025,6 @@ struct Driver {
   // pointer -> (tensor map, slot) for a bf16 [rows][cols] GEMM operand; kind 0 = K-major A
   // (box 64x128), 1 = K-major B (box 64x256), 2 = MN-major (box 64x64)
   __noinline__ __device__ bool resolve(int64_t p, int rows, int cols, int kind, int64_t* map, int64_t* slot) {
-    Region rg(this, 32 + 3);
     // entries are sorted by base (host): binary search for the last base <= p, then the
     // entries sharing that base (one buffer registered under several shapes)
     int lo = 0, hi = P.n_reg - 1, at = -1;
@@ -1065,7 +1059,6 @@ struct Driver {
 
   // per-run weight preparation (bf16 permuted W / W^T), created on first use of the node
   __noinline__ __device__ int32_t prep(const DNode& d, int nid, int kind, int64_t dst) {
-    Region rg(this, 32 + 7);
     if (prep_inst_[nid] >= 0) return prep_inst_[nid];
     const int64_t In = d.imm[1], H = d.imm[2], KT = In + H;
     int ntiles = kind == HK_PREP_WP ? (int)((4 * H + 15) / 16) : (int)((KT / 64) * (4 * H / 128));
