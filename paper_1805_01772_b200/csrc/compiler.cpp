@@ -304,6 +304,7 @@ struct Compiler {
       }
     }
     detect_accumulators();
+    fuse_dout_sums();
 
     // ---- device nodes
     P.nodes.resize(N);
@@ -313,7 +314,19 @@ struct Compiler {
       DNode d{};
       d.n_in = (int)n.in.size();
       d.in_off = (int)P.in_vids.size();
-      for (auto& t : n.in) P.in_vids.push_back(vid(t));
+      auto fz = fused_dout.find(n.id);
+      if (fz == fused_dout.end()) {
+        for (auto& t : n.in) P.in_vids.push_back(vid(t));
+      } else {
+        // LSTMCellGrad with its dout AddN folded in: dout = AddN input 0, the other AddN
+        // inputs appended after the regular inputs (aux5 = how many)
+        const Node& an = g.nodes[fz->second];
+        const int o = n.attrs.b("masked") ? 7 : 5;
+        for (size_t j = 0; j < n.in.size(); ++j)
+          P.in_vids.push_back(vid((int)j == o + 2 ? an.in[0] : n.in[j]));
+        for (size_t j = 1; j < an.in.size(); ++j) P.in_vids.push_back(vid(an.in[j]));
+        d.n_in = (int)(n.in.size() + an.in.size() - 1);
+      }
       d.n_ctrl = (int)n.ctrl.size();
       d.ctrl_off = (int)P.in_vids.size();
       for (int c : n.ctrl) P.in_vids.push_back(ctrl_vid[c]);
@@ -425,6 +438,8 @@ struct Compiler {
         if (op == "Recv") heavy_nodes.push_back(n.id);   // output placed like a heavy output
       } else if (odt == FLOW) {
         d.op = OP_FLOW;
+      } else if (fused_addn.count(n.id)) {
+        d.op = OP_NOP;   // folded into its LSTMCellGrad consumer (not in any body program)
       } else if (acc_of_add.count(n.id)) {
         d.op = OP_ACC;
         d.aux[0] = acc_of_add.at(n.id);
@@ -460,6 +475,7 @@ struct Compiler {
         d.op = OP_HEAVY;
         heavy_nodes.push_back(n.id);
         lower_heavy(n, d);
+        if (fused_dout.count(n.id)) d.aux[5] = (int)g.nodes[fused_dout.at(n.id)].in.size() - 1;
       }
       P.nodes[n.id] = d;
     }
@@ -915,6 +931,32 @@ struct Compiler {
   }
   int merge_branch_ctx(int m, int j) { return dctx_of(merge_branch_ctx_g(m, j)); }
 
+  // ---- AddN -> LSTMCellGrad dout fusion: the gradient of a layer output is the sum of the
+  // next layer's d[x] and the output TensorArray's gradient; the cell-gradient tile adds the
+  // (up to 3) terms itself, so the sum is never materialised (one instance and one
+  // [B, H] write + read less per layer and step).
+  std::map<int, int> fused_dout;   // LSTMCellGrad node -> folded AddN node
+  std::set<int> fused_addn;
+  void fuse_dout_sums() {
+    for (const Node& n : g.nodes) {
+      if (n.op != "LSTMCellGrad") continue;
+      const int o = n.attrs.b("masked") ? 7 : 5;
+      const TRef din = n.in[o + 2];
+      const Node& a = g.nodes[din.node];
+      if (a.op != "AddN" || a.in.size() < 2 || a.in.size() > 3) continue;
+      if (cons[vid(din)].size() != 1 || a.ctx != n.ctx || frame_of[a.id] != frame_of[n.id]) continue;
+      if (acc_of_add.count(a.id) || vdt[vid(din)] != D_F32) continue;
+      bool ok = true;
+      for (auto& t : a.in) ok &= vdt[vid(t)] == D_F32 && g.shape(t) == g.shape(din);
+      if (!ok) continue;
+      fused_dout[n.id] = a.id;
+      fused_addn.insert(a.id);
+      const int f = frame_of[n.id];
+      if (f >= 0)
+        for (auto& t : a.in) extra_edges[f].push_back({t.node, n.id});
+    }
+  }
+
   bool waveable(int v) const {
     const DNode& d = P.nodes[v];
     if (d.n_ctrl != 0) return false;
@@ -1086,7 +1128,7 @@ struct Compiler {
       const Ctx& ctx = g.ctxs[c];
       std::vector<int> body, enters, exits;
       for (int i = 0; i < N; ++i) {
-        if (frame_of[i] != (int)f) continue;
+        if (frame_of[i] != (int)f || fused_addn.count(i)) continue;
         if (g.nodes[i].op == "Enter" && g.nodes[i].attrs.s("frame") == ctx.name) enters.push_back(i);
         else body.push_back(i);
       }

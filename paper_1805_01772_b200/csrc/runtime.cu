@@ -51,6 +51,7 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kEwTile = 4096;
+constexpr int kEwBig = 16384;   // elementwise (HK_EW) tile
 
 // ----------------------------------------------------------------------------- helpers
 __device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long* p) {
@@ -134,73 +135,149 @@ __device__ void gemm_tile64(float* sm, int m0, int n0, int M, int N, int K, LA l
     }
 }
 
+// elementwise tile: kEwBig elements; 8 loads per input in flight per thread (memory-latency
+// bound otherwise), dtype / broadcast decisions are warp-uniform
 __device__ void tile_ew(const Inst& I, int tile) {
   const int64_t n = I.n;
-  const int64_t b0 = (int64_t)tile * kEwTile;
-  const int64_t e1 = min(n, b0 + kEwTile);
+  const int64_t b0 = (int64_t)tile * kEwBig;
+  const int64_t e1 = min(n, b0 + kEwBig);
   const int op = I.sub;
   const int flags = (int)I.s[1];
   // fast path: fp32 binary add/sub/mul/addn2 without broadcast, 16 B vectors, 4 in flight
   const bool vec = flags == 0 && (I.dts & 0xF000000FFLL) == ((int64_t)D_F32 << 32 | D_F32 << 4 | D_F32) &&
                    (op == EW_ADD || op == EW_SUB || op == EW_MUL || (op == EW_ADDN && I.s[0] == 2)) &&
-                   ((I.p[0] | I.p[1] | I.p[13]) & 15) == 0 && (e1 - b0) == kEwTile;
+                   ((I.p[0] | I.p[1] | I.p[13]) & 15) == 0 && ((e1 - b0) & 4095) == 0;
   if (vec) {
-    const float4* a = (const float4*)I.p[0] + b0 / 4;
-    const float4* b = (const float4*)I.p[1] + b0 / 4;
-    float4* o = (float4*)I.p[13] + b0 / 4;
-    float4 x[4], y[4];
+    for (int64_t c0 = b0; c0 < e1; c0 += 4096) {
+      const float4* a = (const float4*)I.p[0] + c0 / 4;
+      const float4* b = (const float4*)I.p[1] + c0 / 4;
+      float4* o = (float4*)I.p[13] + c0 / 4;
+      float4 x[4], y[4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      x[j] = a[threadIdx.x + j * kThreads];
-      y[j] = b[threadIdx.x + j * kThreads];
-    }
+      for (int j = 0; j < 4; ++j) {
+        x[j] = a[threadIdx.x + j * kThreads];
+        y[j] = b[threadIdx.x + j * kThreads];
+      }
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      float4 r;
-      if (op == EW_MUL) r = make_float4(x[j].x * y[j].x, x[j].y * y[j].y, x[j].z * y[j].z, x[j].w * y[j].w);
-      else if (op == EW_SUB) r = make_float4(x[j].x - y[j].x, x[j].y - y[j].y, x[j].z - y[j].z, x[j].w - y[j].w);
-      else r = make_float4(x[j].x + y[j].x, x[j].y + y[j].y, x[j].z + y[j].z, x[j].w + y[j].w);
-      o[threadIdx.x + j * kThreads] = r;
+      for (int j = 0; j < 4; ++j) {
+        float4 r;
+        if (op == EW_MUL) r = make_float4(x[j].x * y[j].x, x[j].y * y[j].y, x[j].z * y[j].z, x[j].w * y[j].w);
+        else if (op == EW_SUB) r = make_float4(x[j].x - y[j].x, x[j].y - y[j].y, x[j].z - y[j].z, x[j].w - y[j].w);
+        else r = make_float4(x[j].x + y[j].x, x[j].y + y[j].y, x[j].z + y[j].z, x[j].w + y[j].w);
+        o[threadIdx.x + j * kThreads] = r;
+      }
     }
     return;
   }
   void* out = (void*)I.p[13];
   const int odt = (int)((I.dts >> 32) & 15);
+  // 4-wide path for mixed fp32 / bf16 operands and broadcast scalars (16 / 8-byte accesses)
+  const int dt0 = (int)(I.dts & 15), dt1 = (int)((I.dts >> 4) & 15);
+  const bool ok_dt = (dt0 == D_F32 || dt0 == D_BF16) && (dt1 == D_F32 || dt1 == D_BF16) &&
+                     (odt == D_F32 || odt == D_BF16);
+  if (ok_dt && (op == EW_ADD || op == EW_SUB || op == EW_MUL || (op == EW_ADDN && I.s[0] == 2)) &&
+      ((I.p[0] | I.p[1] | I.p[13]) & 7) == 0 && (b0 & 3) == 0) {
+    const int64_t e4 = b0 + ((e1 - b0) & ~(int64_t)3);
+    const bool bc0 = flags & 1, bc1 = flags & 2;
+    const float s0 = bc0 ? ldf((const void*)I.p[0], dt0, 0) : 0.f, s1 = bc1 ? ldf((const void*)I.p[1], dt1, 0) : 0.f;
+    auto ld4 = [&](int j, int dt, bool bc, float sv, int64_t e) -> float4 {
+      if (bc) return make_float4(sv, sv, sv, sv);
+      if (dt == D_F32) return *(const float4*)((const float*)I.p[j] + e);
+      const uint2 u = *(const uint2*)((const __nv_bfloat16*)I.p[j] + e);
+      const float2 a = __bfloat1622float2(*(const __nv_bfloat162*)&u.x);
+      const float2 b = __bfloat1622float2(*(const __nv_bfloat162*)&u.y);
+      return make_float4(a.x, a.y, b.x, b.y);
+    };
+    constexpr int V = 4;
+    for (int64_t base = b0 + 4 * threadIdx.x; base < e4; base += (int64_t)4 * V * kThreads) {
+      float4 x[V], y[V];
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+        int64_t e = base + (int64_t)4 * k * kThreads;
+        if (e > e4 - 4) e = e4 - 4;
+        x[k] = ld4(0, dt0, bc0, s0, e);
+        y[k] = ld4(1, dt1, bc1, s1, e);
+      }
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+        const int64_t e = base + (int64_t)4 * k * kThreads;
+        if (e >= e4) break;
+        float4 r;
+        if (op == EW_MUL) r = make_float4(x[k].x * y[k].x, x[k].y * y[k].y, x[k].z * y[k].z, x[k].w * y[k].w);
+        else if (op == EW_SUB) r = make_float4(x[k].x - y[k].x, x[k].y - y[k].y, x[k].z - y[k].z, x[k].w - y[k].w);
+        else r = make_float4(x[k].x + y[k].x, x[k].y + y[k].y, x[k].z + y[k].z, x[k].w + y[k].w);
+        if (odt == D_F32) {
+          *(float4*)((float*)out + e) = r;
+        } else {
+          __nv_bfloat162 lo = __floats2bfloat162_rn(r.x, r.y), hi = __floats2bfloat162_rn(r.z, r.w);
+          uint2 u;
+          u.x = *(unsigned*)&lo;
+          u.y = *(unsigned*)&hi;
+          *(uint2*)((__nv_bfloat16*)out + e) = u;
+        }
+      }
+    }
+    for (int64_t e = e4 + threadIdx.x; e < e1; e += kThreads) {   // ragged tail
+      const float a = bc0 ? s0 : ldf((const void*)I.p[0], dt0, e), b = bc1 ? s1 : ldf((const void*)I.p[1], dt1, e);
+      stf(out, odt, e, op == EW_MUL ? a * b : op == EW_SUB ? a - b : a + b);
+    }
+    return;
+  }
   auto in = [&](int j, int64_t e) -> float {
     return ldf((const void*)I.p[j], (int)((I.dts >> (4 * j)) & 15), (flags >> j & 1) ? 0 : e);
   };
-  for (int64_t e = b0 + threadIdx.x; e < e1; e += kThreads) {
-    float r = 0.0f;
-    switch (op) {
-      case EW_ADD: r = in(0, e) + in(1, e); break;
-      case EW_SUB: r = in(0, e) - in(1, e); break;
-      case EW_MUL: r = in(0, e) * in(1, e); break;
-      case EW_NEG: r = -in(0, e); break;
-      case EW_SIGMOID: r = 1.0f / (1.0f + expf(-in(0, e))); break;
-      case EW_TANH: r = tanhf(in(0, e)); break;
-      case EW_RELU: r = fmaxf(in(0, e), 0.0f); break;
-      case EW_RELUGRAD: r = in(1, e) > 0.0f ? in(0, e) : 0.0f; break;
-      case EW_BIASADD: r = in(0, e) + ldf((const void*)I.p[1], (int)((I.dts >> 4) & 15), e % I.m); break;
-      case EW_SELECT: {
-        const uint8_t* c = (const uint8_t*)I.p[0];
-        bool cv = I.s[2] ? c[0] != 0 : (I.m > 0 ? c[e / I.m] != 0 : c[e] != 0);
-        r = cv ? in(1, e) : in(2, e);
-        break;
-      }
-      case EW_ADDN: {
-        for (int j = 0; j < (int)I.s[0]; ++j) r += in(j, e);
-        break;
-      }
-      case EW_ZEROS: r = 0.0f; break;
+  const int nin = op == EW_ADDN ? (int)I.s[0] : (op == EW_SELECT ? 3 : (op == EW_NEG || op == EW_SIGMOID ||
+                  op == EW_TANH || op == EW_RELU || op == EW_ZEROS) ? 1 : 2);
+  constexpr int U = 8;
+  for (int64_t base = b0 + threadIdx.x; base < e1; base += (int64_t)U * kThreads) {
+    float v0[U], v1[U], v2[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int64_t e = min(base + (int64_t)k * kThreads, e1 - 1);
+      v0[k] = op == EW_ZEROS || op == EW_SELECT || op == EW_ADDN ? 0.0f : in(0, e);
+      v1[k] = nin > 1 && op != EW_BIASADD && op != EW_SELECT && op != EW_ADDN ? in(1, e) : 0.0f;
+      v2[k] = 0.0f;
+      if (op == EW_ADDN)
+        for (int j = 0; j < nin; ++j) v2[k] += in(j, e);
     }
-    stf(out, odt, e, r);
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int64_t e = base + (int64_t)k * kThreads;
+      if (e >= e1) break;
+      float r = 0.0f;
+      switch (op) {
+        case EW_ADD: r = v0[k] + v1[k]; break;
+        case EW_SUB: r = v0[k] - v1[k]; break;
+        case EW_MUL: r = v0[k] * v1[k]; break;
+        case EW_NEG: r = -v0[k]; break;
+        case EW_SIGMOID: r = 1.0f / (1.0f + expf(-v0[k])); break;
+        case EW_TANH: r = tanhf(v0[k]); break;
+        case EW_RELU: r = fmaxf(v0[k], 0.0f); break;
+        case EW_RELUGRAD: r = v1[k] > 0.0f ? v0[k] : 0.0f; break;
+        case EW_BIASADD: r = v0[k] + ldf((const void*)I.p[1], (int)((I.dts >> 4) & 15), e % I.m); break;
+        case EW_SELECT: {
+          const uint8_t* c = (const uint8_t*)I.p[0];
+          bool cv = I.s[2] ? c[0] != 0 : (I.m > 0 ? c[e / I.m] != 0 : c[e] != 0);
+          r = cv ? in(1, e) : in(2, e);
+          break;
+        }
+        case EW_ADDN: r = v2[k]; break;
+        case EW_ZEROS: r = 0.0f; break;
+      }
+      stf(out, odt, e, r);
+    }
   }
 }
 
 __device__ void tile_fill(const Inst& I, int tile) {
   float v = I.p[0] ? ldf((const void*)I.p[0], (int)(I.dts & 15), 0) : __int_as_float((int)I.s[0]);
   const int odt = (int)((I.dts >> 32) & 15);
-  int64_t b0 = (int64_t)tile * kEwTile, e1 = min(I.n, b0 + kEwTile);
+  int64_t b0 = (int64_t)tile * kEwBig, e1 = min(I.n, b0 + kEwBig);
+  if (odt == D_F32 && (I.p[13] & 15) == 0 && ((e1 - b0) & 3) == 0) {
+    float4* o = (float4*)((float*)I.p[13] + b0);
+    for (int64_t e = threadIdx.x; e < (e1 - b0) / 4; e += kThreads) o[e] = make_float4(v, v, v, v);
+    return;
+  }
   for (int64_t e = b0 + threadIdx.x; e < e1; e += kThreads) stf((void*)I.p[13], odt, e, v);
 }
 
@@ -404,6 +481,8 @@ __device__ void tile_lstm_bwd_ew(const Inst& I, int tile) {
     float cn = fg * cp + ig * gg;
     float tc = tanhf(cn);
     float dh = dhn[e] + dout[e];
+    if (I.p[14]) dh += ((const float*)I.p[14])[e];   // folded AddN terms (compiler fuse_dout_sums)
+    if (I.p[15]) dh += ((const float*)I.p[15])[e];
     float dcs = dh * og * (1.0f - tc * tc) + dcn[e];
     float dzi = dcs * gg * ig * (1.0f - ig);
     float dzf = dcs * cp * fg * (1.0f - fg);
@@ -1119,6 +1198,11 @@ struct Driver {
       I.m = B; I.k = In; I.n = H;
       I.p[2] = ip(2); I.p[4] = ip(4); I.p[5] = masked ? ip(6) : 0;
       I.p[6] = ip(o); I.p[7] = ip(o + 1); I.p[8] = ip(o + 2);
+      {   // folded AddN terms of dout (appended inputs)
+        const int nx = d.aux[5], base = d.n_in - nx;
+        I.p[14] = nx > 0 ? ip(base) : 0;
+        I.p[15] = nx > 1 ? ip(base + 1) : 0;
+      }
       I.p[9] = outp[2]; I.p[10] = dz_ptr;
       I.s[0] = t; I.s[4] = in_tok(d, o + 2).dt; I.s[5] = dz_bytes;
       for (int j = 0; j < d.n_in; ++j) add_dep(e, in_tok(d, j).writer);
@@ -1255,6 +1339,11 @@ struct Driver {
           I.p[6] = ip(o);
           I.p[7] = ip(o + 1);
           I.p[8] = ip(o + 2);
+          {
+            const int nx = d.aux[5], base = d.n_in - nx;
+            I.p[14] = nx > 0 ? ip(base) : 0;
+            I.p[15] = nx > 1 ? ip(base + 1) : 0;
+          }
           I.p[9] = outp[2];
           I.p[10] = outp[5];
           I.s[0] = t;
@@ -1303,7 +1392,7 @@ struct Driver {
     switch (kind) {
       case HK_EW: {
         int64_t n = d.imm[0];
-        id = new_inst(HK_EW, d.aux[1], (int)((n + kEwTile - 1) / kEwTile));
+        id = new_inst(HK_EW, d.aux[1], (int)((n + kEwBig - 1) / kEwBig));
         if (id < 0) return EV_ERROR;
         Inst& I = A.insts[id];
         I.n = n;
@@ -1318,7 +1407,7 @@ struct Driver {
       }
       case HK_FILL: {
         int64_t n = d.imm[0];
-        id = new_inst(HK_FILL, 0, (int)((n + kEwTile - 1) / kEwTile));
+        id = new_inst(HK_FILL, 0, (int)((n + kEwBig - 1) / kEwBig));
         if (id < 0) return EV_ERROR;
         Inst& I = A.insts[id];
         I.n = n;
@@ -1971,7 +2060,7 @@ struct Driver {
       const DAcc& ac = P.accs[a];
       int32_t id;
       if (ac.init_zero) {
-        id = new_inst(HK_FILL, 0, (int)((ac.bytes / 4 + kEwTile - 1) / kEwTile));
+        id = new_inst(HK_FILL, 0, (int)((ac.bytes / 4 + kEwBig - 1) / kEwBig));
         if (id < 0) return;
         A.insts[id].n = ac.bytes / 4;
         A.insts[id].p[0] = 0;

@@ -224,6 +224,8 @@ __device__ void tile_lstm_bwd_ew_bf(const Inst& I, int tile, float* sm) {
       og[j] = bf2f(gr[192]);
       cp[j] = c_prev[e];
       dhv[j] = dhn[e] + ldf(dout, dout_dt, e);
+      if (I.p[14]) dhv[j] += ((const float*)I.p[14])[e];   // folded AddN terms
+      if (I.p[15]) dhv[j] += ((const float*)I.p[15])[e];
       dcn_[j] = dcn[e];
       len4[j] = masked ? lens[r] : 0;
     }
