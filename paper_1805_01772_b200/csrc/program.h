@@ -274,6 +274,7 @@ struct RunState {
   long long pushes, pops;
   long long sends, recvs;
   long long swap_out, swap_in, bytes_d2h, bytes_h2d;
+  int32_t smem_mask, smem_used;   // driver arrays staged in shared memory (bit per array)
   int32_t max_depth, exit_fires;
   long long instances, tiles, dead_skipped;
   unsigned long long t_start, t_end;

@@ -908,7 +908,7 @@ struct Driver {
 #endif
   };
 
-  __noinline__ __device__ int32_t new_inst(int kind, int sub, int ntiles) {
+  __forceinline__ __device__ int32_t new_inst(int kind, int sub, int ntiles) {
     if (ninst >= A.inst_cap) {
       fail(CF_E_STACK_BUDGET, -1);
       return -1;
@@ -947,7 +947,7 @@ struct Driver {
     }
     return id;
   }
-  __noinline__ __device__ void add_dep(int32_t id, int32_t w) {
+  __forceinline__ __device__ void add_dep(int32_t id, int32_t w) {
     if (done(w)) return;
     const int ws = w & kRingMask;
     if (r_last[ws] == id) return;   // dedupe repeated inputs from the same producer
@@ -964,7 +964,7 @@ struct Driver {
   }
   // two rings: critical-path work (high) and filler work (low: dW chunks) so that the
   // recurrence never queues behind throughput work
-  __noinline__ __device__ void publish(int32_t id) {
+  __forceinline__ __device__ void publish(int32_t id) {
     const int sl = id & kRingMask;
     if ((r_kfi[sl] & 255) == HK_SWAP) {   // to the host I/O thread's copy streams
       const Inst& I = A.insts[id];
@@ -1055,7 +1055,7 @@ struct Driver {
   }
 
   // ---------------------------------------------------------------- placement
-  __noinline__ __device__ bool place(const DNode& d, int port, int64_t* ptr) {
+  __forceinline__ __device__ bool place(const DNode& d, int port, int64_t* ptr) {
     const PlaceDesc& pl = places_[d.place_off + port];
     int it = cur_frame >= 0 ? iter : 0;
     switch (pl.kind) {
@@ -1103,7 +1103,7 @@ struct Driver {
   // ---------------------------------------------------------------- operand registry
   // pointer -> (tensor map, slot) for a bf16 [rows][cols] GEMM operand; kind 0 = K-major A
   // (box 64x128), 1 = K-major B (box 64x256), 2 = MN-major (box 64x64)
-  __noinline__ __device__ bool resolve(int64_t p, int rows, int cols, int kind, int64_t* map, int64_t* slot) {
+  __forceinline__ __device__ bool resolve(int64_t p, int rows, int cols, int kind, int64_t* map, int64_t* slot) {
     // entries are sorted by base (host): binary search for the last base <= p, then the
     // entries sharing that base (one buffer registered under several shapes)
     int lo = 0, hi = P.n_reg - 1, at = -1;
@@ -1137,7 +1137,7 @@ struct Driver {
   }
 
   // per-run weight preparation (bf16 permuted W / W^T), created on first use of the node
-  __noinline__ __device__ int32_t prep(const DNode& d, int nid, int kind, int64_t dst) {
+  __forceinline__ __device__ int32_t prep(const DNode& d, int nid, int kind, int64_t dst) {
     if (prep_inst_[nid] >= 0) return prep_inst_[nid];
     const int64_t In = d.imm[1], H = d.imm[2], KT = In + H;
     int ntiles = kind == HK_PREP_WP ? (int)((4 * H + 15) / 16) : (int)((KT / 64) * (4 * H / 128));
@@ -1163,12 +1163,17 @@ struct Driver {
     const int64_t B = d.imm[0], In = d.imm[1], H = d.imm[2], KT = In + H;
     auto ip = [&](int j) { return in_tok(d, j).v; };
     if (kind == HK_LSTM_FWD) {
+      long long q0 = A.prof ? clock64() : 0;
       int32_t pw = prep(d, nid, HK_PREP_WP, outp[4]);
       int64_t mx, sx, mh, sh, mw, sw;
       if (!resolve(ip(0), (int)B, (int)In, 0, &mx, &sx) || !resolve(ip(1), (int)B, (int)H, 0, &mh, &sh) ||
           !resolve(outp[4], (int)(4 * H), (int)KT, 1, &mw, &sw))
         return EV_ERROR;
+      long long q1 = A.prof ? clock64() : 0;
+      if (A.prof) { op_cyc[32 + 14] += q1 - q0; op_cnt[32 + 14]++; }
       int32_t id = new_inst(HK_LSTM_FWD_TC, masked, (int)(((B + 127) / 128) * (H / 64)));
+      long long q2 = A.prof ? clock64() : 0;
+      if (A.prof) { op_cyc[32 + 15] += q2 - q1; op_cnt[32 + 15]++; }
       if (id < 0) return EV_ERROR;
       Inst& I = A.insts[id];
       I.m = B; I.k = In; I.n = H;
@@ -1177,13 +1182,18 @@ struct Driver {
       I.p[6] = ip(1);
       for (int p = 0; p < 4; ++p) I.p[8 + p] = outp[p];
       I.s[0] = t; I.s[1] = d.aux[2]; I.s[2] = sx; I.s[3] = sh;
+      long long q3 = A.prof ? clock64() : 0;
+      if (A.prof) { op_cyc[32 + 16] += q3 - q2; op_cnt[32 + 16]++; }
       for (int j = 0; j < d.n_in; ++j) add_dep(id, in_tok(d, j).writer);
       add_dep(id, pw);
+      long long q4 = A.prof ? clock64() : 0;
+      if (A.prof) { op_cyc[32 + 17] += q4 - q3; op_cnt[32 + 17]++; }
       set_out(d, 0, ptr_tok(outp[0], id, D_BF16));
       set_out(d, 1, ptr_tok(outp[1], id, D_F32));
       set_out(d, 2, ptr_tok(outp[2], id, D_BF16));
       set_out(d, 3, ptr_tok(outp[3], id, D_BF16));
       submit(id);
+      if (A.prof) { op_cyc[32 + 18] += clock64() - q4; op_cnt[32 + 18]++; }
       return EV_OK;
     }
     // ---- backward: EW (dz, dc, db partials) -> DXH (dx, dh) and DW (dW, db)
@@ -1297,8 +1307,10 @@ struct Driver {
     int nplace = d.n_out;
     if (kind == HK_LSTM_BWD_EW) nplace += tcm ? 2 : 1;
     if (kind == HK_LSTM_FWD && tcm) nplace += 1;
+    long long q0 = A.prof ? clock64() : 0;
     for (int p = 0; p < nplace; ++p)
       if (!place(d, p, &outp[p])) return st->error ? EV_ERROR : EV_BLOCKED;
+    if (A.prof) { op_cyc[32 + 19] += clock64() - q0; op_cnt[32 + 19]++; }
     if (tcm && (kind == HK_LSTM_FWD || kind == HK_LSTM_BWD_EW)) return eval_lstm_tc(d, nid, outp);
     auto ip = [&](int j) { return in_tok(d, j).v; };
     auto dep_all = [&](int32_t id) {
@@ -2312,6 +2324,8 @@ struct Driver {
       st->op_count[k] = op_cnt[k];
       st->op_cycles[k] = op_cyc[k];
     }
+    st->op_count[31] = st->smem_mask;   // profiling: which driver arrays live in smem
+    st->op_cycles[31] = st->smem_used;
     st->pushes = n_push;
     st->pops = n_pop;
     st->sends = n_sent;
@@ -2505,6 +2519,12 @@ __global__ void __launch_bounds__(kThreads, 1) cf_driver_kernel(RunArgs A_param)
     int32_t* s_iter = (int32_t*)carve(4 * (int64_t)P.iter_counters);
     int32_t* s_ring = (int32_t*)drv_smem;
     DStack* s_stk = (DStack*)carve((int64_t)P.n_stacks * sizeof(DStack));
+    if (threadIdx.x == 0) {
+      A.st->smem_mask = (toks != A.toks) | (smn ? 2 : 0) | (s_pl ? 4 : 0) | (s_reg ? 8 : 0) |
+                        (s_sd ? 16 : 0) | (s_prep ? 32 : 0) | (s_dwc ? 64 : 0) | (s_accw ? 128 : 0) |
+                        (s_iter ? 256 : 0) | (s_stk ? 512 : 0);
+      A.st->smem_used = (int32_t)used;
+    }
     for (int i = threadIdx.x; s_pl && i < P.n_places; i += blockDim.x) s_pl[i] = P.places[i];
     for (int i = threadIdx.x; s_reg && i < P.n_reg; i += blockDim.x) s_reg[i] = P.reg[i];
     for (int i = threadIdx.x; s_sd && i < P.n_stacks; i += blockDim.x) s_sd[i] = 0;

@@ -63,10 +63,11 @@ OPS = ["NOP", "PLACEHOLDER", "CONST", "PASS", "SWITCH", "MERGE", "MERGE_LOOP", "
        "NEXTITER", "SCALAR", "REDUCE_I", "SLICE_I", "FLOW", "TA_CREATE", "TA_READ", "TA_WRITE",
        "TA_STACK", "TA_UNSTACK", "TA_GRAD", "STACK_CREATE", "STACK_PUSH", "STACK_POP", "HEAVY", "ACC",
        "SEND", "RECV"]
-OPS = OPS + ["?%d" % k for k in range(len(OPS), 32)]
+OPS = OPS + ["?%d" % k for k in range(len(OPS), 31)] + ["SMEM_MASK"]
 OPS += ["R_RUN_BODY", "R_NEW_INST", "R_PUBLISH", "R_RESOLVE", "R_DRAIN", "R_ADD_DEP", "R_PLACE",
         "R_PREP", "R_FLUSH_DW", "R_EVAL_LSTM_TC", "R_EVAL_HEAVY", "R_DRAIN_IO", "R_COMPLETE",
-        "R_WAVE"]
+        "R_WAVE", "F_PREP_RESOLVE", "F_NEW_INST", "F_FIELDS", "F_ADD_DEPS", "F_OUT_SUBMIT",
+        "H_PLACES"]
 OPS = OPS + ["?%d" % k for k in range(len(OPS), 62)] + ["R_SWITCH_FAST", "?63"]
 res["driver"] = {OPS[k]: {"n": n, "us": cyc / 1965.0}
                  for k, (n, cyc) in enumerate(s.driver_ops) if n}
