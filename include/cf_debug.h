@@ -18,11 +18,15 @@ int32_t cf_debug_tc_gemm(int32_t M, int32_t N, int32_t K, int32_t bn, int32_t a_
 /* Profiling hook: with cf_run_opts.reserved[0] = 1 at session creation, the driver records
  * per heavy instance 6 x u64 {create ns, publish ns, first tile start ns, last tile end ns,
  * summed tile busy ns, (kind << 32) | ntiles} (%globaltimer). Copies up to cap u64 of the
- * last run into out; *n_inst = records available; t0 (66 x u64) = {run start ns, run end ns,
- * 32 per-opcode driver evaluation counts, 32 per-opcode driver cycles}. */
+ * last run into out; *n_inst = records available; t0 (130 x u64) = {run start ns, run end ns,
+ * 64 driver counts, 64 driver cycles: opcodes [0,32), profiled regions [32,64)}. */
 struct cf_session;
 int32_t cf_debug_session_profile(const struct cf_session* s, unsigned long long* out, int64_t cap,
                                  int64_t* n_inst, unsigned long long* t0);
+/* Batch size from which the forward and d[x,h] GEMMs use 256-row tiles (two TMEM accumulators
+ * per CTA); default 1024. Lets tests exercise that tile shape at small sizes. Returns 0 or
+ * CF_E_CUDA. */
+int32_t cf_debug_set_m2_rows(int32_t rows);
 #ifdef __cplusplus
 }
 #endif

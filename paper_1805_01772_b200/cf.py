@@ -116,6 +116,7 @@ _sig = {
     "cf_session_ipc_handle": (C.c_int32, [_P, C.c_void_p]),
     "cf_session_connect": (C.c_int32, [_P, C.c_int32, C.c_void_p, C.c_int32, C.POINTER(C.c_int64)]),
     # include/cf_debug.h (test hooks)
+    "cf_debug_set_m2_rows": (C.c_int32, [C.c_int32]),
     "cf_debug_session_profile": (C.c_int32, [_P, C.c_void_p, C.c_int64, C.POINTER(C.c_int64),
                                              C.c_void_p]),
     "cf_debug_tc_gemm": (C.c_int32, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
@@ -568,3 +569,8 @@ def debug_tc_gemm(M, N, K, bn, a_mn, b_mn, A, B, Cout, stream=None):
 
 def version() -> str:
     return _lib.cf_version().decode()
+
+
+def debug_set_m2_rows(rows: int) -> None:
+    """Test hook (include/cf_debug.h): batch size from which 256-row GEMM tiles are used."""
+    _check(_lib.cf_debug_set_m2_rows(rows))

@@ -52,6 +52,8 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kEwTile = 4096;
 constexpr int kEwBig = 16384;   // elementwise (HK_EW) tile
+// forward / d[x,h] GEMMs use 256-row tiles from this batch size on (dW always does)
+__device__ int kM2MinRows = 1024;
 
 // ----------------------------------------------------------------------------- helpers
 __device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long* p) {
@@ -1171,7 +1173,11 @@ struct Driver {
         return EV_ERROR;
       long long q1 = A.prof ? clock64() : 0;
       if (A.prof) { op_cyc[32 + 14] += q1 - q0; op_cnt[32 + 14]++; }
-      int32_t id = new_inst(HK_LSTM_FWD_TC, masked, (int)(((B + 127) / 128) * (H / 64)));
+      // 256-row tiles (tc_tile2) trade tile count for operand bytes: only for large batches;
+      // the recurrence wants many short tiles (measured on cfg3)
+      const bool m2 = B >= kM2MinRows;
+      int32_t id = new_inst(HK_LSTM_FWD_TC, masked | (m2 ? 2 : 0),
+                            (int)((m2 ? (B + 255) / 256 : (B + 127) / 128) * (H / 64)));
       long long q2 = A.prof ? clock64() : 0;
       if (A.prof) { op_cyc[32 + 15] += q2 - q1; op_cnt[32 + 15]++; }
       if (id < 0) return EV_ERROR;
@@ -1224,7 +1230,9 @@ struct Driver {
         !resolve(ip(0), (int)B, (int)In, 2, &mxn, &sxn) ||
         !resolve(ip(1), (int)B, (int)H, 2, &mhn, &shn))
       return EV_ERROR;
-    int32_t x = new_inst(HK_LSTM_DXH_TC, masked, (int)(((B + 127) / 128) * (KT / 256)));
+    const bool m2 = B >= kM2MinRows;
+    int32_t x = new_inst(HK_LSTM_DXH_TC, masked | (m2 ? 2 : 0),
+                         (int)((m2 ? (B + 255) / 256 : (B + 127) / 128) * (KT / 256)));
     if (x < 0) return EV_ERROR;
     {
       Inst& I = A.insts[x];
@@ -1270,7 +1278,7 @@ struct Driver {
     const int64_t B = d.imm[0], In = d.imm[1], H = d.imm[2], KT = In + H;
     const int acc_w = d.aux[3], acc_b = d.aux[4];
     int32_t w = new_inst(HK_LSTM_DW_TC, d.aux[1] & 1,
-                         (int)((4 * H / 128) * (KT / 256) + (4 * H + 255) / 256));
+                         (int)((4 * H / 256) * (KT / 256) + (4 * H + 255) / 256));
     if (w < 0) return -1;
     Inst& I = A.insts[w];
     I.m = B; I.k = In; I.n = H;
@@ -2353,7 +2361,7 @@ __device__ void worker_loop(const RunArgs& A) {
   RunState* st = A.st;
   const bool tcmode = A.prog.precision == D_BF16;
   tc::TcShared ts{};
-  uint32_t tc_cnt = 0, tc_tiles = 0;
+  uint32_t tc_cnt = 0, tc_cnt2 = 0, tc_tiles = 0;
   if (tcmode) {
     ts = tc::tc_carve(dyn_smem);
     tc::tc_setup(ts);
@@ -2418,10 +2426,10 @@ __device__ void worker_loop(const RunArgs& A) {
       case HK_LSTM_BWD_MM: tile_lstm_bwd_mm(I, tile, sm); break;
       case HK_PREP_WP: tile_prep_wp(I, tile); break;
       case HK_PREP_WT: tile_prep_wt(I, tile, (float*)dyn_smem); break;
-      case HK_LSTM_FWD_TC: tile_lstm_fwd_tc(I, tile, ts, tc_cnt, tc_tiles); break;
+      case HK_LSTM_FWD_TC: tile_lstm_fwd_tc(I, tile, ts, tc_cnt, tc_cnt2, tc_tiles); break;
       case HK_LSTM_BWD_EW_BF: tile_lstm_bwd_ew_bf(I, tile, sm); break;
-      case HK_LSTM_DXH_TC: tile_lstm_dxh_tc(I, tile, ts, tc_cnt, tc_tiles); break;
-      case HK_LSTM_DW_TC: tile_lstm_dw_tc(I, tile, ts, tc_cnt, tc_tiles); break;
+      case HK_LSTM_DXH_TC: tile_lstm_dxh_tc(I, tile, ts, tc_cnt, tc_cnt2, tc_tiles); break;
+      case HK_LSTM_DW_TC: tile_lstm_dw_tc(I, tile, ts, tc_cnt, tc_cnt2, tc_tiles); break;
       default: break;
     }
     // epilogue stores (generic proxy) must be visible to later TMA (async proxy) reads
@@ -3266,6 +3274,10 @@ cf_status cf_session_connect(cf_session* s, int32_t peer, const void* handle, in
     cf::set_error(e.what());
     return e.code;
   }
+}
+
+int32_t cf_debug_set_m2_rows(int32_t rows) {
+  return cudaMemcpyToSymbol(kM2MinRows, &rows, sizeof(rows)) == cudaSuccess ? CF_OK : CF_E_CUDA;
 }
 
 // profiling hook (include/cf_debug.h): per-instance timing of the last cf_run

@@ -15,14 +15,24 @@ constexpr int kStages = 4;
 constexpr int kStageA = BM * BK * 2;      // 16 KiB
 constexpr int kStageBmax = 256 * BK * 2;  // 32 KiB
 constexpr int kSmemTC = kStages * (kStageA + kStageBmax) + 1024 /*align*/ + 256 /*barriers*/;
+// 256-row mode (two 128 x 256 accumulators sharing each B stage): 3 stages of 64 KiB in the
+// same shared memory; 1.5x fewer operand bytes per flop than 128-row tiles
+constexpr int kStages2 = 3;
+constexpr int kStage2A = 2 * kStageA;     // 32 KiB: rows [0,128) then [128,256)
+constexpr int kStage2 = kStage2A + kStageBmax;
+static_assert(kStages2 * kStage2 <= kStages * (kStageA + kStageBmax), "256-row stages fit");
 
 struct TcShared {
   uint8_t* a[kStages];
   uint8_t* b[kStages];
+  uint8_t* a2[kStages2];
+  uint8_t* b2[kStages2];
   uint64_t* full;    // [kStages]
   uint64_t* empty;   // [kStages]
   uint64_t* done;    // [1]
   uint32_t* tmem_slot;
+  uint64_t* full2;   // [kStages2]
+  uint64_t* empty2;  // [kStages2]
 };
 
 // carve the dynamic smem buffer (1024-aligned for SWIZZLE_128B)
@@ -41,7 +51,13 @@ __device__ inline TcShared tc_carve(uint8_t* dyn) {
   s.full = (uint64_t*)p;
   s.empty = s.full + kStages;
   s.done = s.empty + kStages;
-  s.tmem_slot = (uint32_t*)(s.done + 1);
+  s.full2 = s.done + 1;
+  s.empty2 = s.full2 + kStages2;
+  s.tmem_slot = (uint32_t*)(s.empty2 + kStages2);
+  for (int i = 0; i < kStages2; ++i) {
+    s.a2[i] = (uint8_t*)base + i * kStage2;
+    s.b2[i] = s.a2[i] + kStage2A;
+  }
   return s;
 }
 
@@ -52,10 +68,14 @@ __device__ inline void tc_setup(TcShared& s) {
       mbar_init(&s.full[i], 1);
       mbar_init(&s.empty[i], 1);
     }
+    for (int i = 0; i < kStages2; ++i) {
+      mbar_init(&s.full2[i], 1);
+      mbar_init(&s.empty2[i], 1);
+    }
     mbar_init(s.done, 1);
     fence_barrier_init();
   }
-  if (threadIdx.x / 32 == 2) tmem_alloc<256>(s.tmem_slot);
+  if (threadIdx.x / 32 == 2) tmem_alloc<512>(s.tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -64,7 +84,7 @@ __device__ inline void tc_teardown(TcShared& s) {
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (threadIdx.x / 32 == 2) tmem_dealloc<256>(*s.tmem_slot);
+  if (threadIdx.x / 32 == 2) tmem_dealloc<512>(*s.tmem_slot);
 }
 
 // box load request: which map, coordinates, smem byte offset within the stage buffer
@@ -128,6 +148,65 @@ __device__ inline void tc_tile(TcShared& s, int nk, int bn, int a_mn, int b_mn, 
   }
   cnt += nk;
   // everyone waits for the accumulator
+  mbar_wait(s.done, tiles & 1);
+  tiles++;
+  tc_fence_after();
+}
+
+// 256-row tile: rows [0,128) accumulate in TMEM columns [0,256), rows [128,256) in [256,512);
+// both MMAs of a k16 step read the same B stage. Plans fill A boxes at offsets within the
+// 32 KiB A region (rows 128.. at +16 KiB) and B boxes as in tc_tile. Own barriers and k-block
+// counter (cnt2); the done barrier / tile counter are shared with tc_tile.
+template <class PlanA, class PlanB>
+__device__ inline void tc_tile2(TcShared& s, int nk, int a_mn, int b_mn, uint32_t& cnt2,
+                                uint32_t& tiles, PlanA plan_a, PlanB plan_b) {
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (warp == 0) {
+    if (lane == 0) {
+      uint32_t c = cnt2;
+      for (int kb = 0; kb < nk; ++kb, ++c) {
+        const int st = c % kStages2;
+        const uint32_t round = c / kStages2;
+        mbar_wait(&s.empty2[st], (round & 1) ^ 1);
+        mbar_arrive_expect_tx(&s.full2[st], kStage2A + kStageBmax);
+        Box bx[8];
+        int na = plan_a(kb, bx);
+        for (int i = 0; i < na; ++i)
+          tma_load_3d(s.a2[st] + bx[i].off, bx[i].map, &s.full2[st], bx[i].c0, bx[i].c1, bx[i].c2);
+        int nb = plan_b(kb, bx);
+        for (int i = 0; i < nb; ++i)
+          tma_load_3d(s.b2[st] + bx[i].off, bx[i].map, &s.full2[st], bx[i].c0, bx[i].c1, bx[i].c2);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc = idesc_bf16(BM, 256, a_mn, b_mn);
+      const uint32_t tmem = *s.tmem_slot;
+      uint32_t c = cnt2;
+      for (int kb = 0; kb < nk; ++kb, ++c) {
+        const int st = c % kStages2;
+        const uint32_t round = c / kStages2;
+        mbar_wait(&s.full2[st], round & 1);
+        tc_fence_after();
+        const uint32_t sa = smem_u32(s.a2[st]), sb = smem_u32(s.b2[st]);
+#pragma unroll
+        for (int k = 0; k < BK / 16; ++k) {
+          const uint32_t ko = a_mn ? k * 2048 : k * 32;
+          uint64_t da0 = a_mn ? sdesc_sw128(sa + ko, 8192, 1024) : sdesc_sw128(sa + ko, 16, 1024);
+          uint64_t da1 = a_mn ? sdesc_sw128(sa + kStageA + ko, 8192, 1024)
+                              : sdesc_sw128(sa + kStageA + ko, 16, 1024);
+          uint64_t db = b_mn ? sdesc_sw128(sb + k * 2048, 8192, 1024) : sdesc_sw128(sb + k * 32, 16, 1024);
+          mma_bf16(tmem, da0, db, idesc, (kb | k) != 0);
+          mma_bf16(tmem + 256, da1, db, idesc, (kb | k) != 0);
+        }
+        mma_commit(&s.empty2[st]);
+      }
+      mma_commit(s.done);
+    }
+    __syncwarp();
+  }
+  cnt2 += nk;
   mbar_wait(s.done, tiles & 1);
   tiles++;
   tc_fence_after();

@@ -105,29 +105,35 @@ __device__ void tile_prep_wt(const Inst& I, int tile, float* sm) {
 //    8 h_next(bf16), 9 c_next(f32), 10 out(bf16), 11 gates(bf16, tile-interleaved)
 // s: 0 t, 1 forget bias bits, 2 x slot, 3 h slot
 __device__ void tile_lstm_fwd_tc(const Inst& I, int tile, tc::TcShared& ts, uint32_t& cnt,
-                                 uint32_t& ntile) {
+                                 uint32_t& cnt2, uint32_t& ntile) {
   const int B = (int)I.m, In = (int)I.k, H = (int)I.n;
   const int nkx = In / 64, nk = (In + H) / 64;
   const int tn = H / 64;
+  const bool m2 = I.sub & 2;   // 256-row tile (two accumulators)
   const int mt = tile / tn, nt = tile % tn;
-  const int m0 = mt * tc::BM;
+  const int m0 = mt * (m2 ? 2 * tc::BM : tc::BM);
   const CUtensorMap* mx = (const CUtensorMap*)I.p[0];
   const CUtensorMap* mh = (const CUtensorMap*)I.p[1];
   const CUtensorMap* mw = (const CUtensorMap*)I.p[3];
   const int sx = (int)I.s[2], sh = (int)I.s[3];
   auto plan_a = [&](int kb, tc::Box* b) {
-    if (kb < nkx) b[0] = {mx, kb * 64, m0, sx, 0};
-    else b[0] = {mh, (kb - nkx) * 64, m0, sh, 0};
-    return 1;
+    for (int hh = 0; hh < (m2 ? 2 : 1); ++hh) {
+      if (kb < nkx) b[hh] = {mx, kb * 64, m0 + 128 * hh, sx, hh * tc::kStageA};
+      else b[hh] = {mh, (kb - nkx) * 64, m0 + 128 * hh, sh, hh * tc::kStageA};
+    }
+    return m2 ? 2 : 1;
   };
   auto plan_b = [&](int kb, tc::Box* b) {
     b[0] = {mw, kb * 64, nt * 256, 0, 0};
     return 1;
   };
-  tc::tc_tile(ts, nk, 256, 0, 0, cnt, ntile, plan_a, plan_b);
+  if (m2) tc::tc_tile2(ts, nk, 0, 0, cnt2, ntile, plan_a, plan_b);
+  else tc::tc_tile(ts, nk, 256, 0, 0, cnt, ntile, plan_a, plan_b);
+  for (int half = 0; half < (m2 ? 2 : 1); ++half) {
   // ---- fused epilogue
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int r = m0 + 32 * (warp % 4) + lane;
+  const int r = m0 + 128 * half + 32 * (warp % 4) + lane;
+  const int tcol = 256 * half;
   const bool masked = I.sub & 1;
   const int64_t t = I.s[0];
   const float fb = __int_as_float((int)I.s[1]);
@@ -142,10 +148,10 @@ __device__ void tile_lstm_fwd_tc(const Inst& I, int tile, tc::TcShared& ts, uint
   const bool live = r < B && (!masked || t < lens[r]);
   for (int cu = (warp / 4) * 32; cu < (warp / 4) * 32 + 32; cu += 16) {
     float zi[16], zf[16], zg[16], zo[16];
-    tc::tc_acc16(ts, 0 * 64 + cu, zi);
-    tc::tc_acc16(ts, 1 * 64 + cu, zf);
-    tc::tc_acc16(ts, 2 * 64 + cu, zg);
-    tc::tc_acc16(ts, 3 * 64 + cu, zo);
+    tc::tc_acc16(ts, tcol + 0 * 64 + cu, zi);
+    tc::tc_acc16(ts, tcol + 1 * 64 + cu, zf);
+    tc::tc_acc16(ts, tcol + 2 * 64 + cu, zg);
+    tc::tc_acc16(ts, tcol + 3 * 64 + cu, zo);
     if (r >= B) continue;
     const int u0 = nt * 64 + cu;
     const int64_t o = (int64_t)r * H + u0;
@@ -180,6 +186,7 @@ __device__ void tile_lstm_fwd_tc(const Inst& I, int tile, tc::TcShared& ts, uint
 #pragma unroll
       for (int q = 0; q < 4; ++q) ((float4*)(c_next + o))[q] = *(float4*)&cp[4 * q];
     }
+  }
   }
   tc::tc_tile_end();
 }
@@ -278,25 +285,30 @@ __device__ void tile_lstm_bwd_ew_bf(const Inst& I, int tile, float* sm) {
 // ---------------------------------------------------------------- backward d[x,h]
 // p: 0 dz-map (KA), 1 WT-map (KB), 5 lens, 6 dh_next(f32), 11 dx(f32), 12 dh(f32); s: 0 t, 2 dz slot
 __device__ void tile_lstm_dxh_tc(const Inst& I, int tile, tc::TcShared& ts, uint32_t& cnt,
-                                 uint32_t& ntile) {
+                                 uint32_t& cnt2, uint32_t& ntile) {
   const int B = (int)I.m, In = (int)I.k, H = (int)I.n, KT = In + H;
   const int tn = KT / 256;
+  const bool m2 = I.sub & 2;
   const int mt = tile / tn, nt = tile % tn;
-  const int m0 = mt * tc::BM;
+  const int m0 = mt * (m2 ? 2 * tc::BM : tc::BM);
   const CUtensorMap* mz = (const CUtensorMap*)I.p[0];
   const CUtensorMap* mwt = (const CUtensorMap*)I.p[1];
   const int sz = (int)I.s[2];
   auto plan_a = [&](int kb, tc::Box* b) {
     b[0] = {mz, kb * 64, m0, sz, 0};
-    return 1;
+    if (m2) b[1] = {mz, kb * 64, m0 + 128, sz, tc::kStageA};
+    return m2 ? 2 : 1;
   };
   auto plan_b = [&](int kb, tc::Box* b) {
     b[0] = {mwt, kb * 64, nt * 256, 0, 0};
     return 1;
   };
-  tc::tc_tile(ts, (4 * H) / 64, 256, 0, 0, cnt, ntile, plan_a, plan_b);
+  if (m2) tc::tc_tile2(ts, (4 * H) / 64, 0, 0, cnt2, ntile, plan_a, plan_b);
+  else tc::tc_tile(ts, (4 * H) / 64, 256, 0, 0, cnt, ntile, plan_a, plan_b);
+  for (int half = 0; half < (m2 ? 2 : 1); ++half) {
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int r = m0 + 32 * (warp % 4) + lane;
+  const int r = m0 + 128 * half + 32 * (warp % 4) + lane;
+  const int tcol = 256 * half;
   const bool masked = I.sub & 1;
   const int64_t t = I.s[0];
   const int64_t* lens = (const int64_t*)I.p[5];
@@ -306,7 +318,7 @@ __device__ void tile_lstm_dxh_tc(const Inst& I, int tile, tc::TcShared& ts, uint
   const bool dead_row = r < B && masked && !(t < lens[r]);
   for (int c = (warp / 4) * 128; c < (warp / 4) * 128 + 128; c += 16) {
     float v[16];
-    tc::tc_acc16(ts, c, v);
+    tc::tc_acc16(ts, tcol + c, v);
     if (r >= B) continue;
     const int n = nt * 256 + c;
     if (n < In) {
@@ -323,6 +335,7 @@ __device__ void tile_lstm_dxh_tc(const Inst& I, int tile, tc::TcShared& ts, uint
       for (int q = 0; q < 4; ++q) ((float4*)(dh + o))[q] = *(float4*)&v[4 * q];
     }
   }
+  }
   tc::tc_tile_end();
 }
 
@@ -332,10 +345,10 @@ __device__ void tile_lstm_dxh_tc(const Inst& I, int tile, tc::TcShared& ts, uint
 // (6 x i64 per step: dz slot, x-map, x slot, h-map, h slot, db-partials ptr);
 // s: 6 flags (bit0 accumulate dW, bit1 accumulate db), 7 number of steps
 __device__ void tile_lstm_dw_tc(const Inst& I, int tile, tc::TcShared& ts, uint32_t& cnt,
-                                uint32_t& ntile) {
+                                uint32_t& cnt2, uint32_t& ntile) {
   const int B = (int)I.m, In = (int)I.k, H = (int)I.n, KT = In + H, G = 4 * H;
   const int tn = KT / 256;
-  const int n_dw = (G / tc::BM) * tn;
+  const int n_dw = (G / (2 * tc::BM)) * tn;   // 256 gate rows per tile
   const int flags = (int)I.s[6];
   const int ns = (int)I.s[7];
   const int64_t* ax = (const int64_t*)I.p[6];
@@ -354,7 +367,7 @@ __device__ void tile_lstm_dw_tc(const Inst& I, int tile, tc::TcShared& ts, uint3
     return;
   }
   const int mt = tile / tn, nt = tile % tn;
-  const int m0 = mt * tc::BM;
+  const int m0 = mt * 2 * tc::BM;
   const CUtensorMap* mz = (const CUtensorMap*)I.p[0];
   const bool xpart = nt * 256 < In;
   const int col0 = xpart ? nt * 256 : nt * 256 - In;
@@ -362,9 +375,8 @@ __device__ void tile_lstm_dw_tc(const Inst& I, int tile, tc::TcShared& ts, uint3
   auto plan_a = [&](int kb, tc::Box* b) {
     const int q = kb / nkb, r = kb % nkb;
     const int sz = (int)ax[q * 6 + 0];
-    b[0] = {mz, m0, r * 64, sz, 0};
-    b[1] = {mz, m0 + 64, r * 64, sz, 8192};
-    return 2;
+    for (int j = 0; j < 4; ++j) b[j] = {mz, m0 + 64 * j, r * 64, sz, j * 8192};
+    return 4;
   };
   auto plan_b = [&](int kb, tc::Box* b) {
     const int q = kb / nkb, r = kb % nkb;
@@ -373,15 +385,16 @@ __device__ void tile_lstm_dw_tc(const Inst& I, int tile, tc::TcShared& ts, uint3
     for (int j = 0; j < 4; ++j) b[j] = {mb, col0 + 64 * j, r * 64, sb, j * 8192};
     return 4;
   };
-  tc::tc_tile(ts, ns * nkb, 256, 1, 1, cnt, ntile, plan_a, plan_b);
+  tc::tc_tile2(ts, ns * nkb, 1, 1, cnt2, ntile, plan_a, plan_b);
+  for (int half = 0; half < 2; ++half) {
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int m = m0 + 32 * (warp % 4) + lane;
+  const int m = m0 + 128 * half + 32 * (warp % 4) + lane;
   float* dW = (float*)I.p[3] + (int64_t)m * KT + nt * 256;
   const bool acc = flags & 1;
   for (int c = (warp / 4) * 128; c < (warp / 4) * 128 + 128; c += 32) {
     float v[32];
-    tc::tc_acc16(ts, c, v);
-    tc::tc_acc16(ts, c + 16, v + 16);
+    tc::tc_acc16(ts, 256 * half + c, v);
+    tc::tc_acc16(ts, 256 * half + c + 16, v + 16);
     float4* d = (float4*)(dW + c);
     if (acc) {
       float4 old[8];
@@ -397,6 +410,7 @@ __device__ void tile_lstm_dw_tc(const Inst& I, int tile, tc::TcShared& ts, uint3
     }
 #pragma unroll
     for (int q = 0; q < 8; ++q) d[q] = *(float4*)&v[4 * q];
+  }
   }
   tc::tc_tile_end();
 }

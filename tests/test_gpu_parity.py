@@ -131,6 +131,16 @@ def test_bf16_multilayer_capped():
     check_parity(8, 130, 256, 512, 3, "capped", seed=1, tol=BF16_TOL, precision=cf.BF16)
 
 
+def test_bf16_wide_batch_256_row_tiles():
+    """B >= 256: the forward and d[x,h] GEMMs use 256-row tiles (two TMEM accumulators per
+    CTA); B = 300 leaves a ragged second half-tile."""
+    cf.debug_set_m2_rows(256)
+    try:
+        check_parity(4, 300, 256, 256, 2, "uniform", seed=3, tol=BF16_TOL, precision=cf.BF16)
+    finally:
+        cf.debug_set_m2_rows(1024)
+
+
 def test_bf16_cfg2_shape():
     """BASELINE.json configs[1] shape on the tcgen05 path."""
     check_parity(100, 64, 512, 512, 1, "uniform", seed=2, tol=BF16_TOL, precision=cf.BF16)
