@@ -1156,7 +1156,7 @@ struct Driver {
     return id;
   }
 
-  __noinline__ __device__ int eval_lstm_tc(const DNode& d, int nid, const int64_t* outp) {
+  __forceinline__ __device__ int eval_lstm_tc(const DNode& d, int nid, const int64_t* outp) {
     Region rg(this, 32 + 9);
     const int kind = d.aux[0];
     const bool masked = d.aux[1] & 1;
@@ -1307,7 +1307,7 @@ struct Driver {
   }
 
   // ---------------------------------------------------------------- heavy ops
-  __noinline__ __device__ int eval_heavy(const DNode& d, int nid) {
+  __forceinline__ __device__ int eval_heavy(const DNode& d, int nid) {
     Region rg(this, 32 + 10);
     const int kind = d.aux[0];
     int64_t outp[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -1675,6 +1675,22 @@ struct Driver {
       return EV_OK;
     }
     return eval_cold(d, nid);
+  }
+
+  // heavy node straight from the body loop (one call level: eval_heavy / eval_lstm_tc inline)
+  __noinline__ __device__ int eval_heavy_node(const DNode& d, int nid) {
+    bool dead = false;
+    for (int j = 0; j < d.n_in; ++j) dead |= in_tok(d, j).dead != 0;
+    for (int j = 0; j < d.n_ctrl; ++j) dead |= toks_[iv_[d.ctrl_off + j]].dead != 0;
+    if (dead) {
+      set_dead_all(d);
+      n_dead++;
+    } else {
+      const int r = eval_heavy(d, nid);
+      if (r != EV_OK) return r;
+    }
+    toks_[d.ctrl_vid] = Tok{0, -1, (uint8_t)dead, TK_FLOW, 0, 0};
+    return EV_OK;
   }
 
   __noinline__ __device__ int eval_cold(const DNode& d, int nid) {
@@ -2182,7 +2198,7 @@ struct Driver {
       }
       body_pc = pc;
       long long c0 = prof ? clock64() : 0;
-      int r = eval(*d, P.order[F.body_off + pc]);
+      int r = op == OP_HEAVY ? eval_heavy_node(*d, P.order[F.body_off + pc]) : eval(*d, P.order[F.body_off + pc]);
       if (prof) {
         op_cyc[op & 31] += clock64() - c0;
         op_cnt[op & 31]++;
