@@ -4,6 +4,7 @@
  */
 #ifndef CF_DEBUG_H_
 #define CF_DEBUG_H_
+#include <stddef.h>
 #include <stdint.h>
 #ifdef __cplusplus
 extern "C" {
@@ -27,6 +28,14 @@ int32_t cf_debug_session_profile(const struct cf_session* s, unsigned long long*
  * per CTA); default 1024. Lets tests exercise that tile shape at small sizes. Returns 0 or
  * CF_E_CUDA. */
 int32_t cf_debug_set_m2_rows(int32_t rows);
+/* Compile a graph for the device program without a GPU and write its description and body
+ * programs (one node per line, evaluation order) into buf; *needed = length + 1. */
+struct cf_graph;
+typedef struct { int32_t node, port; } cf_debug_tensor;
+int32_t cf_debug_program_listing(const struct cf_graph* g, int32_t precision,
+                                 int32_t parallel_iterations, int32_t n_fetch,
+                                 const cf_debug_tensor* fetches, char* buf, size_t cap,
+                                 size_t* needed);
 #ifdef __cplusplus
 }
 #endif

@@ -117,6 +117,8 @@ _sig = {
     "cf_session_connect": (C.c_int32, [_P, C.c_int32, C.c_void_p, C.c_int32, C.POINTER(C.c_int64)]),
     # include/cf_debug.h (test hooks)
     "cf_debug_set_m2_rows": (C.c_int32, [C.c_int32]),
+    "cf_debug_program_listing": (C.c_int32, [_P, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
+                                             C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
     "cf_debug_session_profile": (C.c_int32, [_P, C.c_void_p, C.c_int64, C.POINTER(C.c_int64),
                                              C.c_void_p]),
     "cf_debug_tc_gemm": (C.c_int32, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
@@ -574,3 +576,15 @@ def version() -> str:
 def debug_set_m2_rows(rows: int) -> None:
     """Test hook (include/cf_debug.h): batch size from which 256-row GEMM tiles are used."""
     _check(_lib.cf_debug_set_m2_rows(rows))
+
+
+def debug_program_listing(g: "Graph", fetches, precision: int = F32, parallel_iterations: int = 0) -> str:
+    """Test hook: the device program (description + body programs) without a GPU."""
+    arr = (cf_tensor * max(len(fetches), 1))(*[t.c for t in fetches])
+    need = C.c_size_t()
+    _check(_lib.cf_debug_program_listing(g.h, precision, parallel_iterations, len(fetches), arr,
+                                          None, 0, C.byref(need)))
+    buf = C.create_string_buffer(need.value)
+    _check(_lib.cf_debug_program_listing(g.h, precision, parallel_iterations, len(fetches), arr,
+                                          buf, len(buf), None))
+    return buf.value.decode()

@@ -3,6 +3,7 @@
 #include <cstring>
 #include <string>
 
+#include "compiler.h"
 #include "ir.h"
 
 struct cf_graph {
@@ -292,6 +293,27 @@ cf_status cf_tensor_info(const cf_graph* g, cf_tensor t, int32_t* dtype, int32_t
   if (rank) *rank = (int32_t)s.size();
   if (shape)
     for (size_t j = 0; j < s.size() && j < 8; ++j) shape[j] = s[j];
+  CF_CATCH
+}
+
+// debug hook (include/cf_debug.h): compile without a device and list the body programs
+int32_t cf_debug_program_listing(const cf_graph* g, int32_t precision, int32_t parallel_iterations,
+                                 int32_t n_fetch, const cf_tensor* fetches, char* buf, size_t cap,
+                                 size_t* needed) {
+  CF_TRY
+  if (!g) throw CfError(CF_E_INVALID_GRAPH, "null graph");
+  cf::CompileOpts o;
+  o.precision = precision ? precision : CF_F32;
+  o.parallel_iterations = parallel_iterations;
+  std::vector<TRef> fv;
+  for (int i = 0; i < n_fetch; ++i) fv.push_back(tr(fetches[i]));
+  cf::HostProgram P = cf::compile(g->g, o, fv);
+  std::string txt = P.describe + P.listing;
+  if (needed) *needed = txt.size() + 1;
+  if (buf && cap) {
+    std::strncpy(buf, txt.c_str(), cap - 1);
+    buf[cap - 1] = 0;
+  }
   CF_CATCH
 }
 

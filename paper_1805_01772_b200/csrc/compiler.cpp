@@ -1350,6 +1350,25 @@ HostProgram compile(const Graph& g, const CompileOpts& o, const std::vector<TRef
   if (!errs.empty()) throw CfError(CF_E_INVALID_GRAPH, errs[0]);
   Compiler c(g, o);
   c.run(fetches);
+  // body program listing (debug hook cf_debug_program_listing)
+  {
+    std::ostringstream ls;
+    for (size_t f = 0; f < c.P.frames.size(); ++f) {
+      const auto& F = c.P.frames[f];
+      ls << "frame " << c.P.frame_names[f] << "\n";
+      for (int k = 0; k < F.n_body; ++k) {
+        const auto& bn = c.P.body_nodes[F.bn_off + k];
+        const int nid = c.P.order[F.body_off + k];
+        ls << k << " " << (bn.op == OP_WAVE ? std::string("WAVE") : g.nodes[nid].op) << " node=" << nid
+           << " ctx=" << bn.ctx << " gctx=" << g.nodes[nid].ctx;
+        if (bn.op == OP_WAVE) ls << " n=" << bn.aux[0];
+        ls << " in=";
+        for (int j = 0; j < bn.n_in; ++j) ls << c.P.body_ivids[F.bi_off + bn.in_off + j] << ",";
+        ls << " out=" << bn.out_vid << "\n";
+      }
+    }
+    c.P.listing = ls.str();
+  }
   c.P.vdt = c.vdt;
   c.P.precision = o.precision;
   return std::move(c.P);

@@ -82,6 +82,7 @@ struct HostProgram {
   std::map<std::string, FeedInfo> feeds;
   std::vector<FetchInfo> fetches;
   std::string describe;
+  std::string listing;   // body programs, one node per line (debug hook)
 };
 
 struct CompileOpts {

@@ -2203,7 +2203,7 @@ struct Driver {
         op_cyc[op & 31] += clock64() - c0;
         op_cnt[op & 31]++;
       }
-      if (r != EV_OK) return progress;
+      if (r != EV_OK) break;   // blocked / error: resume at this node (counters folded below)
       ++pc;
       progress = true;
     }
