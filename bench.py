@@ -255,6 +255,9 @@ def main():
     c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     copy_ms = 0.0
     torch.cuda.synchronize()
+    if pg:
+        pg.barrier()   # every rank has its pinned inputs ready before the clock starts
+        torch.cuda.synchronize()
     e0.record(stream)
     for _ in range(e2e_steps):
         c0.record(stream)
@@ -268,6 +271,9 @@ def main():
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1) / e2e_steps
     copy_ms /= e2e_steps
+    if os.environ.get("BENCH_DEBUG"):
+        print(f"[rank {rank}] ms={ms:.2f} e2e_ms={e2e_ms:.2f} copy_ms={copy_ms:.2f} "
+              f"kernel_ms={statistics.mean(kernel_ms):.2f}", file=sys.stderr, flush=True)
     if pg:
         t = torch.tensor([e2e_ms], device=f"cuda:{local}")
         pg.all_reduce(t, op=pg.ReduceOp.MAX)
