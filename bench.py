@@ -120,10 +120,13 @@ def run_reference(args, c, cfg_name):
     p = dynamic_rnn_lstm(T_s, c["B"], c["I"], c["H"], c["L"])
     f = rnn_inputs(T_s, c["B"], c["I"], c["H"], c["L"], seed=0, len_mode=c["len_mode"])
     lens_sum = int(np.minimum(f["len"], T_s).sum())
-    for _ in range(args.warmup_ref):
+    # the driver's --steps / --warmup; each step is one bounded sample (truncated T)
+    n_steps = max(1, args.steps if args.steps else args.steps_ref)
+    n_warm = args.warmup if args.warmup is not None else args.warmup_ref
+    for _ in range(n_warm):
         run_program(p, f)
     ts = []
-    for _ in range(args.steps_ref):
+    for _ in range(n_steps):
         t0 = time.perf_counter()
         run_program(p, f)
         ts.append(time.perf_counter() - t0)
@@ -131,14 +134,14 @@ def run_reference(args, c, cfg_name):
     cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
     v = lens_sum / t
     line = {"impl": "reference", "metric": "LSTM fwd+bwd sequence-steps/sec", "value": v,
-            "unit": "sequence-steps/s", "n_gpus": world, "steps": args.steps_ref,
-            "warmup": args.warmup_ref, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "unit": "sequence-steps/s", "n_gpus": world, "steps": n_steps,
+            "warmup": n_warm, "ms_per_step": t * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": cfg_name, **{k: c[k] for k in ("T", "B", "I", "H", "L")},
                        "sample_T": T_s},
             "cpu_baseline": {"value": v, "unit": "sequence-steps/s", "cores": cores, "kind": "oracle",
                              "sample": f"{cfg_name} truncated to T={T_s} (full B/H/L), median of "
-                                       f"{args.steps_ref}"},
+                                       f"{n_steps} steps"},
             "e2e": {"value": v, "unit": "sequence-steps/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
