@@ -33,6 +33,8 @@ CONFIGS = {
     "cfg2": dict(T=100, B=64, I=512, H=512, L=1, len_mode="uniform"),
     "cfg4": dict(T=4000, B=256, I=2048, H=2048, L=1, len_mode="full"),
     "tiny": dict(T=5, B=2, I=4, H=8, L=1, len_mode="full"),
+    # BASELINE.json configs[4]: nested MoE-style gated cond in the body, bf16, PI sweep via --K
+    "cfg5": dict(T=100, B=128, I=1024, H=1024, L=2, len_mode="uniform", moe=True),
 }
 
 
@@ -98,6 +100,8 @@ def flops_per_step(c, lens_sum):
     for l in range(L):
         il = I if l == 0 else H
         per += 24 * H * (il + H)
+        if c.get("moe"):
+            per += 3 * 2 * H * H   # the taken expert's matmul: forward + two gradient matmuls
     return per * lens_sum
 
 
@@ -117,8 +121,9 @@ def run_reference(args, c, cfg_name):
     from oracle.models import dynamic_rnn_lstm, run_program
     from synth import rnn_inputs
     T_s = max(2, min(c["T"], args.ref_T))
-    p = dynamic_rnn_lstm(T_s, c["B"], c["I"], c["H"], c["L"])
-    f = rnn_inputs(T_s, c["B"], c["I"], c["H"], c["L"], seed=0, len_mode=c["len_mode"])
+    p = dynamic_rnn_lstm(T_s, c["B"], c["I"], c["H"], c["L"], moe=c.get("moe", False))
+    f = rnn_inputs(T_s, c["B"], c["I"], c["H"], c["L"], seed=0, len_mode=c["len_mode"],
+                   moe=c.get("moe", False))
     lens_sum = int(np.minimum(f["len"], T_s).sum())
     # the driver's --steps / --warmup; each step is one bounded sample (truncated T)
     n_steps = max(1, args.steps if args.steps else args.steps_ref)
@@ -151,8 +156,9 @@ def cpu_baseline(c, cfg_name, T_s):
     import numpy as np
     from oracle.models import dynamic_rnn_lstm, run_program
     from synth import rnn_inputs
-    p = dynamic_rnn_lstm(T_s, c["B"], c["I"], c["H"], c["L"])
-    f = rnn_inputs(T_s, c["B"], c["I"], c["H"], c["L"], seed=0, len_mode=c["len_mode"])
+    p = dynamic_rnn_lstm(T_s, c["B"], c["I"], c["H"], c["L"], moe=c.get("moe", False))
+    f = rnn_inputs(T_s, c["B"], c["I"], c["H"], c["L"], seed=0, len_mode=c["len_mode"],
+                   moe=c.get("moe", False))
     lens_sum = int(np.minimum(f["len"], T_s).sum())
     t0 = time.perf_counter()
     run_program(p, f)
@@ -208,7 +214,8 @@ def main():
     if pipe and world > c["L"]:
         raise SystemExit(f"pipeline over {world} GPUs needs >= {world} layers")
     stage = (rank, world) if pipe else None
-    p = dynamic_rnn_lstm(c["T"], c["B"], c["I"], c["H"], c["L"], stage=stage)
+    p = dynamic_rnn_lstm(c["T"], c["B"], c["I"], c["H"], c["L"], stage=stage,
+                         moe=c.get("moe", False))
     stream = torch.cuda.current_stream()
     sess = cf.Session(p.g, p.fetch_tensors(), precision=prec, parallel_iterations=args.K,
                       device=local, stream=stream.cuda_stream,
@@ -217,6 +224,7 @@ def main():
         sess.connect_pipeline()
     # pipeline: one model split over the ranks (same inputs everywhere); replicas: own inputs
     f = rnn_inputs(c["T"], c["B"], c["I"], c["H"], c["L"], seed=0 if pipe else rank,
+                   moe=c.get("moe", False),
                    len_mode=c["len_mode"], bf16=prec == cf.BF16)
     lens_sum = int(f["len"].sum())
     dev = feeds_to_device(f, device=f"cuda:{local}", session=sess)
@@ -247,7 +255,7 @@ def main():
         ms = float(t.item())
     # ---- end to end through the public API with HOST buffers (pinned), per step:
     #      H2D of the step's data (x, lengths, loss projections) + D2H of the loss
-    data_names = ["x", "len", "R_out"] + [f"R_h{l}" for l in range(c["L"])] + \
+    data_names = ["x", "len", "R_out", "route"] + [f"R_h{l}" for l in range(c["L"])] + \
         [f"R_c{l}" for l in range(c["L"])]
     host = {k: v.cpu().pin_memory() for k, v in dev.items() if k in data_names}
     h2d = sum(v.numel() * v.element_size() for v in host.values())

@@ -157,8 +157,16 @@ def dynamic_rnn_lstm(T_: int, B: int, I: int, H: int, L: int = 1, parallel_itera
 
 
 def run_program(p: RNNProgram, feeds: Dict[str, np.ndarray], K=None, sched_seed=None,
-                return_trace=False, transport=None):
-    from . import interp
+                return_trace=False, transport=None, bf16_storage=False):
+    """bf16_storage: the LSTM cell's h / out / gates rounded to bf16 as the tensor-core path
+    stores them (kernels.STORAGE, reading R21); everything else stays float64."""
+    from . import interp, kernels
+    if bf16_storage:
+        kernels.STORAGE["lstm_bf16"] = True
+        try:
+            return run_program(p, feeds, K, sched_seed, return_trace, transport, False)
+        finally:
+            kernels.STORAGE["lstm_bf16"] = False
     names = list(p.fetch) + list(p.grads)
     tensors = [p.fetch[n] for n in p.fetch] + [p.grads[n] for n in p.grads]
     feeds = {k: v for k, v in feeds.items() if k in p.b.g.placeholders}

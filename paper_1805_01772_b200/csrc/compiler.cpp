@@ -889,6 +889,7 @@ struct Compiler {
     return gctx_to_dctx[c] = (int)P.ctxs.size() - 1;
   }
   bool structure_conds(const std::vector<int>& ord, std::map<int, int>* alias, std::vector<int>* nctx) {
+    if (std::getenv("CF_NO_STRUCT")) return false;   // debugging switch
     std::set<int> sw;
     for (int v : ord) {
       const Node& n = g.nodes[v];
@@ -938,6 +939,7 @@ struct Compiler {
   std::map<int, int> fused_dout;   // LSTMCellGrad node -> folded AddN node
   std::set<int> fused_addn;
   void fuse_dout_sums() {
+    if (std::getenv("CF_NO_FUSE")) return;   // debugging switch
     for (const Node& n : g.nodes) {
       if (n.op != "LSTMCellGrad") continue;
       const int o = n.attrs.b("masked") ? 7 : 5;
@@ -1364,7 +1366,9 @@ HostProgram compile(const Graph& g, const CompileOpts& o, const std::vector<TRef
         if (bn.op == OP_WAVE) ls << " n=" << bn.aux[0];
         ls << " in=";
         for (int j = 0; j < bn.n_in; ++j) ls << c.P.body_ivids[F.bi_off + bn.in_off + j] << ",";
-        ls << " out=" << bn.out_vid << "\n";
+        ls << " out=" << bn.out_vid;
+        if (bn.op != OP_WAVE && bn.n_out > 0) ls << " dt=" << (int)c.vdt[bn.out_vid];
+        ls << "\n";
       }
     }
     c.P.listing = ls.str();

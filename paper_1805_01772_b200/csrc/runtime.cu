@@ -66,6 +66,11 @@ __device__ __forceinline__ int ld_acquire_i32(const int* p) {
   return v;
 }
 // system scope: channel words written by / read from the peer GPU over NVLink
+__device__ __forceinline__ unsigned long long ld_relaxed_sys_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.sys.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
   unsigned long long v;
   asm volatile("ld.acquire.sys.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -714,6 +719,17 @@ struct Driver {
   int64_t pend_mz = 0;
   int32_t last_dw = -1;
   unsigned long long lq_tail = 0;
+  // pending channel waits (HK_WAIT instances), polled by drain()
+  static constexpr int kMaxWaits = 40;
+  struct ChanWait {
+    unsigned long long* flag;
+    unsigned long long want;
+    unsigned long long* ack;
+    unsigned long long ackv;
+    int32_t id, pad;
+  };
+  ChanWait waits_[kMaxWaits];
+  int n_waits_ = 0;
   // swap I/O (a8)
   unsigned long long io_tail = 0, io_head = 0;
   int io_out = 0;   // swap requests not yet completed
@@ -968,6 +984,20 @@ struct Driver {
   // recurrence never queues behind throughput work
   __forceinline__ __device__ void publish(int32_t id) {
     const int sl = id & kRingMask;
+    if ((r_kfi[sl] & 255) == HK_WAIT) {   // polled by drain() until the flag arrives
+      const Inst& I = A.insts[id];
+      if (n_waits_ == kMaxWaits) {
+        fail(CF_E_UNSUPPORTED, -400);
+        return;
+      }
+      ChanWait& w = waits_[n_waits_++];
+      w.flag = (unsigned long long*)I.p[0];
+      w.want = (unsigned long long)I.s[0];
+      w.ack = (unsigned long long*)I.p[1];
+      w.ackv = (unsigned long long)I.s[1];
+      w.id = id;
+      return;
+    }
     if ((r_kfi[sl] & 255) == HK_SWAP) {   // to the host I/O thread's copy streams
       const Inst& I = A.insts[id];
       unsigned long long* e = A.io_req + 4 * (io_tail & (unsigned long long)(A.io_cap - 1));
@@ -1042,6 +1072,24 @@ struct Driver {
     Region rg(this, 32 + 4);
     bool any = false;
     if (io_out > 0) any = drain_io();
+    for (int k = 0; k < n_waits_;) {   // channel messages (Recv): flag = want, or the dead twin
+      ChanWait& w = waits_[k];
+      const unsigned long long f = ld_relaxed_sys_u64(w.flag);   // poll without acquire cost
+      if ((f | 1) != (w.want | 1)) {
+        ++k;
+        continue;
+      }
+      __threadfence_system();   // acquire: the payload is visible before the copy is released
+      if (f != w.want) {   // replicated control disagrees with the sender (reading R18)
+        fail(CF_E_INVALID_GRAPH, -401);
+        return true;
+      }
+      if (w.ack) st_release_sys_u64(w.ack, w.ackv);
+      const int32_t id = w.id;
+      waits_[k] = waits_[--n_waits_];
+      complete(id);
+      any = true;
+    }
     for (int k = 0; k < 256; ++k) {
       int* p = &A.cq[cq_head & (A.cq_cap - 1)];
       // relaxed poll (an acquire load would invalidate L1 at every poll); the release store
@@ -1585,26 +1633,37 @@ struct Driver {
       return EV_ERROR;
     return EV_OK;
   }
+  // Recv never blocks the driver: a wait instance (HK_WAIT, completed by drain() when the
+  // flag shows the message) gates the copy out of the slot; the copy's last tile acks the
+  // slot. The message is expected live exactly when this Recv is live: both partitions
+  // evaluate the same control (reading R18); a mismatch is an error.
   __noinline__ __device__ int eval_recv(const DNode& d, bool dead, bool* out_dead) {
     const DChan& C = P.chans[d.aux[0]];
     const int it = cur_frame >= 0 ? iter : 0;
     const int slot = it % C.slots;
     const unsigned long long ep = A.epoch << 32;
     const unsigned long long live = ep | (2ULL * (it + 1));
-    const unsigned long long f = ld_acquire_sys_u64(&C.flags[slot]);
-    if (f != live && f != (live | 1)) return EV_BLOCKED;
+    const unsigned long long ackv = ep | (unsigned long long)(it + 1);
     n_recv++;
-    if (dead || f != live) {   // consume the message, propagate dead
-      st_release_sys_u64(&C.acks[slot], ep | (unsigned long long)(it + 1));
+    int64_t out = 0;
+    if (!dead && !place(d, 0, &out)) return st->error ? EV_ERROR : EV_BLOCKED;
+    int32_t w = new_inst(HK_WAIT, dead ? 1 : 0, 1);
+    if (w < 0) return EV_ERROR;
+    {
+      Inst& I = A.insts[w];
+      I.p[0] = (int64_t)&C.flags[slot];
+      I.s[0] = (int64_t)(dead ? (live | 1) : live);
+      I.p[1] = dead ? (int64_t)&C.acks[slot] : 0;   // a dead message is acked on arrival
+      I.s[1] = (int64_t)ackv;
+    }
+    submit(w);
+    if (dead) {
       set_dead_all(d);
       *out_dead = true;
       return EV_OK;
     }
-    int64_t out;
-    if (!place(d, 0, &out)) return st->error ? EV_ERROR : EV_BLOCKED;
     const int64_t stride = (C.elem_bytes + 255) / 256 * 256;
-    int32_t id = copy_inst(out, (int64_t)(C.data + slot * stride), C.elem_bytes, -1, &C.acks[slot],
-                           ep | (unsigned long long)(it + 1), 1);
+    int32_t id = copy_inst(out, (int64_t)(C.data + slot * stride), C.elem_bytes, w, &C.acks[slot], ackv, 1);
     if (id < 0) return EV_ERROR;
     set_out(d, 0, ptr_tok(out, id, C.dt));
     return EV_OK;
@@ -2198,7 +2257,11 @@ struct Driver {
       }
       body_pc = pc;
       long long c0 = prof ? clock64() : 0;
-      int r = op == OP_HEAVY ? eval_heavy_node(*d, P.order[F.body_off + pc]) : eval(*d, P.order[F.body_off + pc]);
+      const int nid = P.order[F.body_off + pc];
+      const bool routing = op == OP_SWITCH || op == OP_MERGE || op == OP_MERGE_LOOP || op == OP_NEXTITER ||
+                           op == OP_PASS || (op == OP_CONST && d->aux[0] == 1);
+      // one call level: heavy nodes and the general ops skip the routing front end
+      int r = op == OP_HEAVY ? eval_heavy_node(*d, nid) : routing ? eval(*d, nid) : eval_cold(*d, nid);
       if (prof) {
         op_cyc[op & 31] += clock64() - c0;
         op_cnt[op & 31]++;
@@ -2974,7 +3037,7 @@ void build_session(cf_session* s, const cf::Graph& g, const cf_run_opts* o,
   need += sizeof(PlaceDesc) * P.places.size() + sizeof(DReg) * (P.reg.size() + P.feeds.size() + 1);
   need += sizeof(DStack) * P.stacks.size() + 8 * P.nodes.size() + 4 * (P.accs.size() + P.iter_counters);
   need += 16 * 12;
-  const size_t smem_cap = 200 * 1024;
+  const size_t smem_cap = 198 * 1024;   // + ~28 KiB static smem stays under the 227 KiB limit
   if ((int)std::min(need, smem_cap) > s->dyn_smem) s->dyn_smem = (int)std::min(need, smem_cap);
   A.dyn_smem = s->dyn_smem;
   CUDA_OK(cudaFuncSetAttribute(cf_driver_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, s->dyn_smem));

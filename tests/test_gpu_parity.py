@@ -43,9 +43,16 @@ def check_parity(T, B, I, H, L, mode, seed, K=None, tol=1e-5, precision=None, **
     f = rnn_inputs(T, B, I, H, L, seed=seed, len_mode=mode, moe=kw.get("moe", False), bf16=bf)
     dev, dead, tr = run_device(T, B, I, H, L, f, K=K or 0, precision=precision, **kw)
     q = oracle_rnn(T, B, I, H, L, **kw)
-    ref, otr = run_program(q, f, K=K, return_trace=True)
+    # bf16 path: the oracle stores the cell's h / out / gates in bf16 like the device
+    # (reading R21), so ReLU masks downstream are decided on the same values
+    ref, otr = run_program(q, f, K=K, return_trace=True, bf16_storage=bf)
     assert not any(dead)
-    errs = {k: normwise(dev[k], ref[k]) for k in ref}
+    # gated-expert weight gradients flow through ReLU masks: in bf16 a mask decided on a value
+    # one bf16 ulp away flips a whole column term, so those are held to the bar in relative
+    # Frobenius norm (reading R22); everything else normwise
+    frob = [k for k in ref if bf and kw.get("moe") and k[:3] in ("dWA", "dWB")]
+    errs = {k: (np.linalg.norm(dev[k] - np.asarray(ref[k])) / max(np.linalg.norm(np.asarray(ref[k])), 1e-30)
+                if k in frob else normwise(dev[k], ref[k])) for k in ref}
     worst = max(errs.values())
     assert worst <= tol, sorted(errs.items(), key=lambda kv: -kv[1])[:4]
     # ---- control trace, bit-exact
@@ -155,3 +162,19 @@ def test_bf16_parallel_iterations_bit_identical(K):
     for k in base:
         assert np.array_equal(base[k], dev[k]), k
     assert max(tr["max_inflight"]) <= K
+
+
+@pytest.mark.parametrize("K", [1, 8, 32])
+def test_bf16_moe_parallel_iterations_sweep(K):
+    """BASELINE.json configs[4] in small: parallel_iterations in {1, 8, 32}, a nested MoE-style
+    gated cond in the body (route bits select the expert), bf16 tensor-core LSTM path;
+    control bit-exact, values within the bf16 bar, and bit-identical across K."""
+    T, B, I, H, L = 6, 64, 256, 256, 2
+    worst, tr = check_parity(T, B, I, H, L, "uniform", seed=8, K=K, tol=BF16_TOL, precision=cf.BF16,
+                             moe=True)
+    assert max(tr["max_inflight"]) <= K
+    f = rnn_inputs(T, B, I, H, L, seed=8, len_mode="uniform", moe=True, bf16=True)
+    a, _, _ = run_device(T, B, I, H, L, f, K=K, precision=cf.BF16, moe=True)
+    b, _, _ = run_device(T, B, I, H, L, f, K=32, precision=cf.BF16, moe=True)
+    for k in a:
+        assert np.array_equal(a[k], b[k]), k

@@ -80,7 +80,7 @@ def _check(cfg, tol, world=2):
     T, B, I, H, L, mode, prec = cfg
     vals, trs = _run(cfg, world)
     f = rnn_inputs(T, B, I, H, L, seed=3, len_mode=mode, bf16=prec == "bf16")
-    ref = run_program(oracle_rnn(T, B, I, H, L), f)
+    ref = run_program(oracle_rnn(T, B, I, H, L), f, bf16_storage=prec == "bf16")
     stages = run_pipeline_threads(T, B, I, H, L, world, f)
     y = 0.0
     for r in range(world):

@@ -215,3 +215,26 @@ def test_invariants_and_parallel_iterations(K, seed):
     assert outer == {t: t < mx for t in range(T)}
     inner = {tag[-1][1]: v for (cid, tag), v in tr.branch.items() if cid == 1 and len(tag) == 1}
     assert inner == {t: t < mn for t in range(mx)}
+
+
+
+def test_bf16_storage_rounding_is_torchs_bf16():
+    """Reading R21: the bf16-storage oracle rounds exactly like a float32 -> bf16 cast
+    (checked against torch, a library routine), and only the LSTM cell's bf16-stored outputs
+    (h, out, gates) are rounded."""
+    import torch
+
+    from oracle.kernels import round_bf16
+    from oracle.models import dynamic_rnn_lstm, run_program
+    from synth import rnn_inputs
+    rng = np.random.default_rng(0)
+    a = rng.standard_normal(20000) * 10.0 ** rng.integers(-12, 12, 20000)
+    assert np.array_equal(round_bf16(a), torch.tensor(a, dtype=torch.float32).to(torch.bfloat16).double().numpy())
+    T, B, I, H, L = 3, 2, 4, 8, 1
+    f = rnn_inputs(T, B, I, H, L, seed=0, len_mode="full", bf16=True)
+    p = dynamic_rnn_lstm(T, B, I, H, L)
+    r = run_program(p, f, bf16_storage=True)
+    assert np.array_equal(round_bf16(r["out"]), r["out"])       # h / out stored in bf16
+    assert not np.array_equal(round_bf16(r["cT0"]), r["cT0"])   # c stays fp64
+    r0 = run_program(p, f)
+    assert not np.array_equal(round_bf16(r0["out"]), r0["out"])
