@@ -185,6 +185,8 @@ def main():
     ap.add_argument("--stack-budget", type=int, default=0,
                     help="device bytes for stacked activations; beyond it stacks swap to pinned "
                          "host memory (0 = no swapping, 1 = swap every eligible value)")
+    ap.add_argument("--swap-smallest-first", action="store_true",
+                    help="with --stack-budget: swap the smallest stacked values first")
     ap.add_argument("--parallel", default="pipeline", choices=["pipeline", "replicas"],
                     help="N>1: layer-partitioned pipeline (strong scaling, SURVEY.md a14) or "
                          "independent replicas (weak scaling)")
@@ -219,7 +221,8 @@ def main():
     stream = torch.cuda.current_stream()
     sess = cf.Session(p.g, p.fetch_tensors(), precision=prec, parallel_iterations=args.K,
                       device=local, stream=stream.cuda_stream,
-                      watchdog_ms=300000 if pipe else 0, stack_budget_bytes=args.stack_budget)
+                      watchdog_ms=300000 if pipe else 0, stack_budget_bytes=args.stack_budget,
+                      swap_smallest_first=args.swap_smallest_first)
     if pipe:
         sess.connect_pipeline()
     # pipeline: one model split over the ranks (same inputs everywhere); replicas: own inputs
@@ -244,7 +247,8 @@ def main():
             kernel_ms.append(tr["wall_ms"])
         ev1.record(stream)
         torch.cuda.synchronize()
-    swap = {"stack_budget_bytes": args.stack_budget, "swap_out": tr["swap_out"],
+    swap = {"stack_budget_bytes": args.stack_budget, "smallest_first": args.swap_smallest_first,
+            "swap_out": tr["swap_out"],
             "swap_in": tr["swap_in"], "bytes_d2h": tr["bytes_d2h"], "bytes_h2d": tr["bytes_h2d"]}
     if pg:
         pg.barrier()

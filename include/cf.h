@@ -174,6 +174,10 @@ typedef struct {
    * nothing); 1 = swap every eligible value. */
   int64_t stack_budget_bytes;
   int64_t swap_min_bytes;       /* 0 = 4096 ("do not swap small tensors") */
+  int32_t swap_smallest_first;  /* 0: swap the largest stacked values first (fewest swaps);
+                                   1: smallest first (fewest bytes per step, for a link that
+                                   cannot hide the largest ones)                           */
+  int32_t pad_;
 } cf_run_opts;
 
 /* Control trace -- compared bit-exact with the oracle's. */

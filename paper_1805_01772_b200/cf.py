@@ -48,7 +48,8 @@ class cf_run_opts(C.Structure):
                 ("device", C.c_int32), ("num_workers", C.c_int32), ("stream", C.c_void_p),
                 ("max_iterations", C.c_int64), ("watchdog_ms", C.c_int64),
                 ("sched_seed", C.c_int32), ("reserved", C.c_int32 * 7),
-                ("stack_budget_bytes", C.c_int64), ("swap_min_bytes", C.c_int64)]
+                ("stack_budget_bytes", C.c_int64), ("swap_min_bytes", C.c_int64),
+                ("swap_smallest_first", C.c_int32), ("pad_", C.c_int32)]
 
 
 class cf_trace(C.Structure):
@@ -408,7 +409,7 @@ class Session:
                  parallel_iterations: int = 0, device: int = 0, stream=None,
                  max_iterations: int = 0, watchdog_ms: int = 0, num_workers: int = 0,
                  sched_seed: int = 0, profile: bool = False, stack_budget_bytes: int = 0,
-                 swap_min_bytes: int = 0):
+                 swap_min_bytes: int = 0, swap_smallest_first: bool = False):
         self.g = g
         self.fetches = list(fetches)
         o = cf_run_opts()
@@ -423,6 +424,7 @@ class Session:
         o.reserved[0] = 1 if profile else 0
         o.stack_budget_bytes = stack_budget_bytes
         o.swap_min_bytes = swap_min_bytes
+        o.swap_smallest_first = 1 if swap_smallest_first else 0
         arr = (cf_tensor * max(len(fetches), 1))(*[t.c for t in fetches])
         h = _P()
         _check(_lib.cf_session_create(g.h, C.byref(o), len(fetches), arr, C.byref(h)))

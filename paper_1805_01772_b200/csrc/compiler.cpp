@@ -1083,7 +1083,9 @@ struct Compiler {
       std::vector<Ar> cand;
       for (auto& a : ars)
         if (P.places[P.nodes[a.node].place_off + a.port].elem_bytes >= o.swap_min_bytes) cand.push_back(a);
-      std::stable_sort(cand.begin(), cand.end(), [](const Ar& x, const Ar& y) { return x.bytes > y.bytes; });
+      const bool small = o.swap_smallest_first;
+      std::stable_sort(cand.begin(), cand.end(),
+                       [small](const Ar& x, const Ar& y) { return small ? x.bytes < y.bytes : x.bytes > y.bytes; });
       for (auto& a : cand) {
         if (total <= o.stack_budget_bytes) break;
         swap_set.insert({a.node, a.port});

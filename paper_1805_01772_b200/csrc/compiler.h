@@ -91,6 +91,7 @@ struct CompileOpts {
   int64_t max_iterations = 0;
   int64_t stack_budget_bytes = -1;   // -1: never swap
   int64_t swap_min_bytes = 4096;
+  bool swap_smallest_first = false;
 };
 
 HostProgram compile(const Graph& g, const CompileOpts& o, const std::vector<TRef>& fetches);

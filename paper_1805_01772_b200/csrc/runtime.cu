@@ -2768,8 +2768,26 @@ void* dalloc(cf_session* s, size_t bytes) {
 // Host I/O executor (one thread per run of a session with swapped stacks): takes the driver's
 // swap requests from the mapped ring in order and issues them on the D2H / H2D copy streams,
 // each followed by a 4-byte completion write into io_cq (stream-ordered after the data).
+// stream-ordered 32-bit store (driver API cuStreamWriteValue32): the completion word needs no
+// copy-engine transfer of its own
+typedef CUresult (*PFN_writeValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+static PFN_writeValue32 get_write_value32() {
+  static PFN_writeValue32 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_writeValue32)p;
+  }
+  return fn;
+}
+
 void io_executor(cf_session* s, std::atomic<bool>* stop, std::atomic<int>* err) {
   cudaSetDevice(s->device);
+  PFN_writeValue32 wv = get_write_value32();
   const unsigned long long m = (unsigned long long)(s->args.io_cap - 1);
   unsigned long long head = 0;
   int idle = 0;
@@ -2784,9 +2802,15 @@ void io_executor(cf_session* s, std::atomic<bool>* stop, std::atomic<int>* err) 
       s->io_ids_host[head & m] = id + 1;
       cudaError_t r = cudaMemcpyAsync((void*)dst, (const void*)src, bytes,
                                       dir == 0 ? cudaMemcpyDeviceToHost : cudaMemcpyHostToDevice, st);
-      if (r == cudaSuccess)
-        r = cudaMemcpyAsync(s->args.io_cq + (head & m), s->io_ids_host + (head & m), 4,
-                            cudaMemcpyHostToDevice, st);
+      if (r == cudaSuccess) {
+        if (wv) {
+          if (wv((CUstream)st, (CUdeviceptr)(s->args.io_cq + (head & m)), (cuuint32_t)(id + 1), 0) != CUDA_SUCCESS)
+            r = cudaErrorUnknown;
+        } else {
+          r = cudaMemcpyAsync(s->args.io_cq + (head & m), s->io_ids_host + (head & m), 4,
+                              cudaMemcpyHostToDevice, st);
+        }
+      }
       if (r != cudaSuccess) err->store(1);
       head++;
       idle = 0;
@@ -2806,6 +2830,7 @@ void build_session(cf_session* s, const cf::Graph& g, const cf_run_opts* o,
     co.max_iterations = o->max_iterations;
     co.stack_budget_bytes = o->stack_budget_bytes > 0 ? o->stack_budget_bytes : -1;
     co.swap_min_bytes = o->swap_min_bytes > 0 ? o->swap_min_bytes : 4096;
+    co.swap_smallest_first = o->swap_smallest_first != 0;
     s->device = o->device;
     if (o->watchdog_ms > 0) s->watchdog_ns = o->watchdog_ms * 1000000LL;
     s->sched_seed = o->sched_seed;

@@ -38,6 +38,8 @@ def main():
     ap.add_argument("--precision", default="bf16")
     ap.add_argument("--T", type=int, default=0)
     ap.add_argument("--K", type=int, default=0)
+    ap.add_argument("--stack-budget", type=int, default=0)
+    ap.add_argument("--swap-smallest-first", action="store_true")
     ap.add_argument("--out", default="gpurun_out/profile.json")
     a = ap.parse_args()
     c = dict(CONFIGS[a.config])
@@ -45,7 +47,8 @@ def main():
         c["T"] = a.T
     prec = cf.BF16 if a.precision == "bf16" else cf.F32
     p = dynamic_rnn_lstm(c["T"], c["B"], c["I"], c["H"], c["L"])
-    s = cf.Session(p.g, p.fetch_tensors(), precision=prec, parallel_iterations=a.K, profile=True)
+    s = cf.Session(p.g, p.fetch_tensors(), precision=prec, parallel_iterations=a.K, profile=True,
+                   stack_budget_bytes=a.stack_budget, swap_smallest_first=a.swap_smallest_first)
     f = rnn_inputs(c["T"], c["B"], c["I"], c["H"], c["L"], seed=0, len_mode=c["len_mode"], bf16=prec == cf.BF16)
     dev = feeds_to_device(f, session=s)
     outs = s.alloc_outputs()
