@@ -2743,7 +2743,10 @@ struct cf_session {
   unsigned long long* io_req_host = nullptr;    // mapped [io_cap][4]
   unsigned long long* io_tail_host = nullptr;   // mapped, written by the driver
   int32_t* io_ids_host = nullptr;               // pinned completion words (id + 1)
-  cudaStream_t io_d2h = nullptr, io_h2d = nullptr;
+  // several copy streams per direction so that the per-copy setup of the 1-4 MB swap copies
+  // overlaps the previous transfer (round robin)
+  static constexpr int kIoStreams = 3;
+  cudaStream_t io_d2h[kIoStreams] = {}, io_h2d[kIoStreams] = {};
 };
 
 namespace {
@@ -2798,7 +2801,8 @@ void io_executor(cf_session* s, std::atomic<bool>* stop, std::atomic<int>* err) 
       volatile unsigned long long* e = s->io_req_host + 4 * (head & m);
       const unsigned long long src = e[0], dst = e[1], bytes = e[2], w = e[3];
       const int id = (int)(w & 0xffffffffULL), dir = (int)(w >> 32);
-      cudaStream_t st = dir == 0 ? s->io_d2h : s->io_h2d;
+      cudaStream_t st = dir == 0 ? s->io_d2h[head % cf_session::kIoStreams]
+                                 : s->io_h2d[head % cf_session::kIoStreams];
       s->io_ids_host[head & m] = id + 1;
       cudaError_t r = cudaMemcpyAsync((void*)dst, (const void*)src, bytes,
                                       dir == 0 ? cudaMemcpyDeviceToHost : cudaMemcpyHostToDevice, st);
@@ -2991,8 +2995,10 @@ void build_session(cf_session* s, const cf::Graph& g, const cf_run_opts* o,
     CUDA_OK(cudaHostGetDevicePointer((void**)&A.io_req_tail, s->io_tail_host, 0));
     A.io_cq = (int32_t*)dalloc(s, 4 * (size_t)A.io_cap);
     s->zero_each_run.push_back({A.io_cq, 4 * (size_t)A.io_cap});
-    CUDA_OK(cudaStreamCreateWithFlags(&s->io_d2h, cudaStreamNonBlocking));
-    CUDA_OK(cudaStreamCreateWithFlags(&s->io_h2d, cudaStreamNonBlocking));
+    for (int k = 0; k < cf_session::kIoStreams; ++k) {
+      CUDA_OK(cudaStreamCreateWithFlags(&s->io_d2h[k], cudaStreamNonBlocking));
+      CUDA_OK(cudaStreamCreateWithFlags(&s->io_h2d[k], cudaStreamNonBlocking));
+    }
   }
   A.inst_aux = (int64_t*)dalloc(s, 8 * 48 * (size_t)P.inst_bound);
   A.dw_count = (int32_t*)dalloc(s, 4 * P.nodes.size());
@@ -3220,8 +3226,10 @@ cf_status cf_run(cf_session* s, int32_t n_feed, const char* const* feed_names,
     if (io.joinable()) {
       io_stop = true;
       io.join();
-      cudaStreamSynchronize(s->io_d2h);
-      cudaStreamSynchronize(s->io_h2d);
+      for (int k = 0; k < cf_session::kIoStreams; ++k) {
+        cudaStreamSynchronize(s->io_d2h[k]);
+        cudaStreamSynchronize(s->io_h2d[k]);
+      }
     }
     CUDA_OK(lerr);
     if (io_err.load()) throw cf::CfError(CF_E_CUDA, "swap I/O copy failed");
@@ -3412,8 +3420,10 @@ void cf_session_destroy(cf_session* s) {
   for (void* p : s->allocs) cudaFree(p);
   for (auto& [r, p] : s->peer_mem) cudaIpcCloseMemHandle(p);
   for (void* h : s->host_allocs) cudaFreeHost(h);
-  if (s->io_d2h) cudaStreamDestroy(s->io_d2h);
-  if (s->io_h2d) cudaStreamDestroy(s->io_h2d);
+  for (int k = 0; k < cf_session::kIoStreams; ++k) {
+    if (s->io_d2h[k]) cudaStreamDestroy(s->io_d2h[k]);
+    if (s->io_h2d[k]) cudaStreamDestroy(s->io_h2d[k]);
+  }
   if (s->chan_mem) cudaFree(s->chan_mem);
   if (s->ev0) cudaEventDestroy(s->ev0);
   if (s->ev1) cudaEventDestroy(s->ev1);
