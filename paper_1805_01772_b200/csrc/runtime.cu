@@ -1153,7 +1153,28 @@ struct Driver {
   // ---------------------------------------------------------------- operand registry
   // pointer -> (tensor map, slot) for a bf16 [rows][cols] GEMM operand; kind 0 = K-major A
   // (box 64x128), 1 = K-major B (box 64x256), 2 = MN-major (box 64x64)
-  __forceinline__ __device__ bool resolve(int64_t p, int rows, int cols, int kind, int64_t* map, int64_t* slot) {
+  // registry entry i as the answer for (p, rows, cols)? -> slot, map
+  __device__ __forceinline__ bool reg_match(int i, int64_t p, int rows, int cols, int kind, int64_t* map,
+                                            int64_t* slot) {
+    const DReg& r = reg_[i];
+    if (r.rows != rows || r.cols != cols) return false;
+    if (p < r.base || p >= r.base + (int64_t)r.slots * r.slot_bytes) return false;
+    const int64_t off = p - r.base;
+    int64_t q = (int64_t)((double)off * r.inv_slot);
+    int64_t rem = off - q * r.slot_bytes;
+    if (rem < 0) { --q; rem += r.slot_bytes; }
+    else if (rem >= r.slot_bytes) { ++q; rem -= r.slot_bytes; }
+    if (rem) return false;
+    *slot = q;
+    *map = (int64_t)((const uint8_t*)P.maps + (int64_t)(r.map0 + kind) * 128);
+    return true;
+  }
+  // with a per-(node, operand) hint: the entry found last time is tried first (an operand of a
+  // given node nearly always lives in the same ring / arena / TensorArray)
+  __forceinline__ __device__ bool resolve(int64_t p, int rows, int cols, int kind, int64_t* map, int64_t* slot,
+                                          int16_t* hint) {
+    const int h = *hint;
+    if (h >= 0 && h < P.n_reg && reg_match(h, p, rows, cols, kind, map, slot)) return true;
     // entries are sorted by base (host): binary search for the last base <= p, then the
     // entries sharing that base (one buffer registered under several shapes)
     int lo = 0, hi = P.n_reg - 1, at = -1;
@@ -1162,17 +1183,8 @@ struct Driver {
       if (reg_[mid].base <= p) { at = mid; lo = mid + 1; } else hi = mid - 1;
     }
     for (int i = at; i >= 0 && reg_[i].base == reg_[at].base; --i) {
-      const DReg& r = reg_[i];
-      if (r.rows != rows || r.cols != cols) continue;
-      if (p >= r.base + (int64_t)r.slots * r.slot_bytes) continue;
-      const int64_t off = p - r.base;
-      int64_t q = (int64_t)((double)off * r.inv_slot);
-      int64_t rem = off - q * r.slot_bytes;
-      if (rem < 0) { --q; rem += r.slot_bytes; }
-      else if (rem >= r.slot_bytes) { ++q; rem -= r.slot_bytes; }
-      if (rem) continue;
-      *slot = q;
-      *map = (int64_t)((const uint8_t*)P.maps + (int64_t)(r.map0 + kind) * 128);
+      if (!reg_match(i, p, rows, cols, kind, map, slot)) continue;
+      *hint = (int16_t)i;
       return true;
     }
     fail(CF_E_UNSUPPORTED, -100 - rows);
@@ -1205,6 +1217,8 @@ struct Driver {
   }
 
   __forceinline__ __device__ int eval_lstm_tc(const DNode& d, int nid, const int64_t* outp) {
+    // operand-registry hints live in the (driver-private) body-program copy of the node
+    int16_t* hint = (int16_t*)const_cast<DNode&>(d).pad;
     Region rg(this, 32 + 9);
     const int kind = d.aux[0];
     const bool masked = d.aux[1] & 1;
@@ -1216,8 +1230,8 @@ struct Driver {
       long long q0 = A.prof ? clock64() : 0;
       int32_t pw = prep(d, nid, HK_PREP_WP, outp[4]);
       int64_t mx, sx, mh, sh, mw, sw;
-      if (!resolve(ip(0), (int)B, (int)In, 0, &mx, &sx) || !resolve(ip(1), (int)B, (int)H, 0, &mh, &sh) ||
-          !resolve(outp[4], (int)(4 * H), (int)KT, 1, &mw, &sw))
+      if (!resolve(ip(0), (int)B, (int)In, 0, &mx, &sx, hint + 0) || !resolve(ip(1), (int)B, (int)H, 0, &mh, &sh, hint + 1) ||
+          !resolve(outp[4], (int)(4 * H), (int)KT, 1, &mw, &sw, hint + 2))
         return EV_ERROR;
       long long q1 = A.prof ? clock64() : 0;
       if (A.prof) { op_cyc[32 + 14] += q1 - q0; op_cnt[32 + 14]++; }
@@ -1272,11 +1286,11 @@ struct Driver {
       for (int j = 0; j < d.n_in; ++j) add_dep(e, in_tok(d, j).writer);
     }
     int64_t mz, sz, mwt, swt, mzn, szn, mxn, sxn, mhn, shn;
-    if (!resolve(dz_ptr, (int)B, (int)(4 * H), 0, &mz, &sz) ||
-        !resolve(outp[6], (int)KT, (int)(4 * H), 1, &mwt, &swt) ||
-        !resolve(dz_ptr, (int)B, (int)(4 * H), 2, &mzn, &szn) ||
-        !resolve(ip(0), (int)B, (int)In, 2, &mxn, &sxn) ||
-        !resolve(ip(1), (int)B, (int)H, 2, &mhn, &shn))
+    if (!resolve(dz_ptr, (int)B, (int)(4 * H), 0, &mz, &sz, hint + 0) ||
+        !resolve(outp[6], (int)KT, (int)(4 * H), 1, &mwt, &swt, hint + 1) ||
+        !resolve(dz_ptr, (int)B, (int)(4 * H), 2, &mzn, &szn, hint + 2) ||
+        !resolve(ip(0), (int)B, (int)In, 2, &mxn, &sxn, hint + 3) ||
+        !resolve(ip(1), (int)B, (int)H, 2, &mhn, &shn, hint + 4))
       return EV_ERROR;
     const bool m2 = B >= kM2MinRows;
     int32_t x = new_inst(HK_LSTM_DXH_TC, masked | (m2 ? 2 : 0),
