@@ -11,7 +11,8 @@ import os
 from typing import Callable, Dict, List, Optional, Sequence
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libcf.so")
+# CF_LIB=libcf_prof.so selects the profiling build (tools/profile_run.py); default libcf.so
+LIB_PATH = os.path.join(HERE, os.environ.get("CF_LIB", "libcf.so"))
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"libcf.so not built ({LIB_PATH}); run python -c 'import __graft_entry__ as "
@@ -118,6 +119,7 @@ _sig = {
     "cf_session_connect": (C.c_int32, [_P, C.c_int32, C.c_void_p, C.c_int32, C.POINTER(C.c_int64)]),
     # include/cf_debug.h (test hooks)
     "cf_debug_set_m2_rows": (C.c_int32, [C.c_int32]),
+    "cf_debug_set_flags": (C.c_int32, [C.c_int32]),
     "cf_debug_program_listing": (C.c_int32, [_P, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
                                              C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
     "cf_debug_session_profile": (C.c_int32, [_P, C.c_void_p, C.c_int64, C.POINTER(C.c_int64),
@@ -573,6 +575,11 @@ def debug_tc_gemm(M, N, K, bn, a_mn, b_mn, A, B, Cout, stream=None):
 
 def version() -> str:
     return _lib.cf_version().decode()
+
+
+def debug_set_flags(flags: int) -> None:
+    """Profiling knob (cf_debug.h): bit 0 = workers skip tile bodies (driver cost alone)."""
+    _check(_lib.cf_debug_set_flags(flags))
 
 
 def debug_set_m2_rows(rows: int) -> None:

@@ -961,6 +961,15 @@ struct Compiler {
 
   bool waveable(int v) const {
     const DNode& d = P.nodes[v];
+    switch (d.op) {
+      // value-free ops with a fast path on the helper warps (runtime.cu fast_node); control
+      // inputs allowed. TA reads / zero-copy writes and scalar ops on immediates too: a node
+      // the fast path declines is evaluated by the driver right after its wave.
+      case OP_CONST: case OP_PASS: case OP_FLOW: case OP_SCALAR: case OP_ACC: case OP_TA_GRAD:
+      case OP_TA_READ: case OP_TA_WRITE:
+        return true;
+      default: break;
+    }
     if (d.n_ctrl != 0) return false;
     switch (d.op) {
       case OP_MERGE: case OP_MERGE_LOOP: case OP_NEXTITER: case OP_SWITCH: return true;
@@ -1250,6 +1259,8 @@ struct Compiler {
           P.n_waves++;
         }
         DNode bn = P.nodes[v];
+        // node id for the device driver (pad[2] high half; pad[0..2] low are registry hints)
+        ((int16_t*)bn.pad)[5] = (int16_t)(v < 32768 ? v : -1);
         bn.ctx = node_ctx[k];
         if (bn.ctx || alias.size()) P.nodes[v].ctx = bn.ctx;
         if (bn.op == OP_MERGE && !alias.empty()) {

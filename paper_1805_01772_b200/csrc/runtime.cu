@@ -51,9 +51,17 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kEwTile = 4096;
+#ifdef CF_PROFILE
+constexpr bool kProfBuild = true;    // libcf_prof.so: driver region/instance profiler compiled in
+#else
+constexpr bool kProfBuild = false;   // libcf.so: no profiler code on the driver's path
+#endif
 constexpr int kEwBig = 16384;   // elementwise (HK_EW) tile
 // forward / d[x,h] GEMMs use 256-row tiles from this batch size on (dW always does)
 __device__ int kM2MinRows = 1024;
+// test/profiling knob (cf_debug_set_flags): bit 0 = workers skip the tile bodies (isolates the
+// driver's own cost; results are garbage)
+__device__ int kDbgFlags = 0;
 
 // ----------------------------------------------------------------------------- helpers
 __device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long* p) {
@@ -577,6 +585,14 @@ struct FastEnv {
   const DStack* stacks;
   int32_t* depth;
   int4* pool;
+  // accumulators and TensorArray bookkeeping (ACC / TA_READ / TA_WRITE fast paths)
+  const DAcc* accs;
+  const int32_t* accw;
+  const DTA* tas;
+  const int64_t* tab;
+  const int32_t* tso;
+  int32_t* ta_writer;
+  uint8_t* ta_written;
 };
 struct FastCount {
   int push, pop, maxd, err, err_info;
@@ -624,6 +640,105 @@ __device__ __forceinline__ int fast_node(const DNode* d, const FastEnv& e, FastC
     const int4 o = tk[iv[d->in_off + (op == OP_MERGE_LOOP && e.it != 0 ? 1 : 0)]];
     tk[d->out_vid] = o;
     tk[d->ctrl_vid] = make_int4(0, 0, -1, (TK_FLOW << 8) | (o.w & 0xff));
+    return 1;
+  }
+  if ((op >= OP_CONST && op <= OP_TA_GRAD) || op == OP_ACC) {
+    // value-free ops: dead if any data or control input is dead
+    int dead = 0;
+    for (int j = 0; j < d->n_in; ++j) dead |= tk[iv[d->in_off + j]].w & 0xff;
+    for (int j = 0; j < d->n_ctrl; ++j) dead |= tk[iv[d->ctrl_off + j]].w & 0xff;
+    dead = dead ? 1 : 0;
+    const int4 ctrl = make_int4(0, 0, -1, (TK_FLOW << 8) | dead);
+    switch (op) {
+      case OP_CONST: {
+        const long long v = d->imm[0];
+        tk[d->out_vid] = make_int4((int)(v & 0xffffffffLL), (int)(v >> 32), -1,
+                                   dead | ((d->aux[0] == 1 ? TK_IMM : TK_PTR) << 8) | ((d->aux[1] & 0xff) << 16));
+        break;
+      }
+      case OP_PASS:
+      case OP_FLOW: {
+        int4 t = op == OP_PASS && d->n_in ? tk[iv[d->in_off]] : make_int4(0, 0, 0, 0);
+        if (op == OP_FLOW) t = make_int4(0, 0, -1, TK_FLOW << 8);
+        t.w = (t.w & ~0xff) | dead;
+        for (int p = 0; p < d->n_out; ++p) tk[d->out_vid + p] = t;
+        break;
+      }
+      case OP_SCALAR: {
+        if (dead) {
+          for (int p = 0; p < d->n_out; ++p) tk[d->out_vid + p] = make_int4(0, 0, -1, 1);
+          break;
+        }
+        long long ab[2] = {0, 0};
+        for (int j = 0; j < d->n_in && j < 2; ++j) {
+          const int4 t = tk[iv[d->in_off + j]];
+          const int kind = (t.w >> 8) & 0xff;
+          if (kind == TK_PTR) return 0;   // device value: the general evaluator waits for it
+          if (kind == TK_IMM) ab[j] = (long long)(((unsigned long long)(unsigned)t.y << 32) | (unsigned)t.x);
+        }
+        const long long a = ab[0], b = ab[1];
+        long long r = 0;
+        switch (d->aux[0]) {
+          case SC_ADD: r = a + b; break;
+          case SC_SUB: r = a - b; break;
+          case SC_MUL: r = a * b; break;
+          case SC_LESS: r = a < b; break;
+          case SC_LEQ: r = a <= b; break;
+          case SC_GREATER: r = a > b; break;
+          case SC_EQ: r = a == b; break;
+          case SC_AND: r = (a != 0) && (b != 0); break;
+          case SC_NOT: r = a == 0; break;
+          case SC_CAST: r = d->aux[1] == D_BOOL ? (a != 0) : a; break;
+        }
+        tk[d->out_vid] = make_int4((int)(r & 0xffffffffLL), (int)(r >> 32), -1,
+                                   (TK_IMM << 8) | ((d->aux[1] & 0xff) << 16));
+        break;
+      }
+      case OP_ACC: {   // fused accumulator: producers added in place
+        const long long v = e.accs[d->aux[0]].base;
+        tk[d->out_vid] = make_int4((int)(v & 0xffffffffLL), (int)(v >> 32), e.accw[d->aux[0]],
+                                   dead | (TK_PTR << 8) | (D_F32 << 16));
+        break;
+      }
+      case OP_TA_GRAD: {
+        tk[d->out_vid] = make_int4(d->aux[0], 0, -1, dead | (TK_HANDLE << 8));
+        tk[d->out_vid + 1] = make_int4(0, 0, -1, dead | (TK_FLOW << 8));
+        break;
+      }
+      case OP_TA_READ:
+      case OP_TA_WRITE: {
+        if (dead) {
+          if (op == OP_TA_READ) tk[d->out_vid] = make_int4(0, 0, -1, 1);
+          else tk[d->out_vid] = make_int4(0, 0, -1, 1 | (TK_FLOW << 8));
+          break;
+        }
+        const int4 ht = tk[iv[d->in_off]], it = tk[iv[d->in_off + 1]];
+        if (((it.w >> 8) & 0xff) != TK_IMM) return 0;
+        const int ta = ht.x;
+        const long long ix = (long long)(((unsigned long long)(unsigned)it.y << 32) | (unsigned)it.x);
+        const DTA& T = e.tas[ta];
+        if (ix < 0 || ix >= T.size) return 0;   // the general evaluator reports it
+        const int so = e.tso[ta] + (int)ix;
+        const long long addr = e.tab[ta] + ix * T.elem_bytes;
+        if (op == OP_TA_READ) {
+          if (!T.is_grad && !e.ta_written[so]) return 0;
+          tk[d->out_vid] = make_int4((int)(addr & 0xffffffffLL), (int)(addr >> 32), e.ta_writer[so],
+                                     (TK_PTR << 8) | ((T.dt & 0xff) << 16));
+        } else {
+          // zero-copy write only (the producer was placed in the slot); first write
+          const int4 v = tk[iv[d->in_off + 2]];
+          const long long vp = (long long)(((unsigned long long)(unsigned)v.y << 32) | (unsigned)v.x);
+          if (vp != addr || e.ta_written[so]) return 0;
+          e.ta_writer[so] = v.z;
+          e.ta_written[so] = 1;
+          tk[d->out_vid] = make_int4(0, 0, -1, TK_FLOW << 8);
+        }
+        break;
+      }
+      default:
+        return 0;
+    }
+    tk[d->ctrl_vid] = ctrl;
     return 1;
   }
   if ((op == OP_STACK_PUSH || op == OP_STACK_POP) && !d->n_ctrl) {
@@ -710,7 +825,8 @@ struct Driver {
   const Prog& P;
   RunState* st;
   int32_t ninst = 0, nedge = 0;
-  unsigned long long q_tail = 0, cq_head = 0;
+  unsigned long long q_tail = 0;
+  unsigned long long cq_head_ = 0;
   int64_t outstanding = 0;     // created - completed
   int32_t root_pc = 0, cur_frame = -1, iter = 0, body_pc = 0;
   bool iter_started = false, fetched = false;
@@ -745,6 +861,10 @@ struct Driver {
   int32_t* acc_writer_;
   int32_t* iter_out_;
   const DStack* stacks_;
+  // TensorArray metadata (shared memory when it fits, else the global tables)
+  const DTA* tas_;
+  int64_t* tab_;
+  const int32_t* tso_;
   long long n_push = 0, n_pop = 0, n_dead = 0, n_inst = 0, n_tiles = 0, n_sent = 0, n_recv = 0;
   long long op_cnt[64] = {}, op_cyc[64] = {};   // [0, 32) opcodes, [32, 64) regions
   int32_t max_depth = 0, n_exitf = 0;
@@ -766,6 +886,7 @@ struct Driver {
       : A(a), P(a.prog), st(a.st), places_(a.prog.places), reg_(a.prog.reg),
         stack_depth_(a.stack_depth), prep_inst_(a.prep_inst), dw_count_(a.dw_count),
         acc_writer_(a.acc_writer), iter_out_(a.iter_outstanding), stacks_(a.prog.stacks),
+        tas_(a.prog.tas), tab_(a.ta_base), tso_(a.ta_slot_off),
         toks_(t), iv_(a.prog.in_vids), bn_(nullptr), sm_nodes_(smn), sm_iv_(smi), req_(req) {}
   Wave* wave_ = nullptr;
 
@@ -780,6 +901,13 @@ struct Driver {
     e.stacks = stacks_;
     e.depth = stack_depth_;
     e.pool = (int4*)A.stack_pool;
+    e.accs = P.accs;
+    e.accw = acc_writer_;
+    e.tas = tas_;
+    e.tab = tab_;
+    e.tso = tso_;
+    e.ta_writer = A.ta_writer;
+    e.ta_written = A.ta_written;
     return e;
   }
 
@@ -802,6 +930,7 @@ struct Driver {
     __threadfence_block();
     *(volatile int*)&w.seq = w.seq + 1;
     while (*(volatile int*)&w.done < kWaveWarps) {
+      drain();   // the helper warps touch tokens and stacks only, never instance state
     }
     __threadfence_block();
     n_push += w.cnt.push;
@@ -913,20 +1042,29 @@ struct Driver {
   int32_t* r_kfi;    // kind (8) | frame + 1 (8) | iter (16)
 
   __device__ bool done(int32_t w) const { return w < 0 || r_id[w & kRingMask] != w; }
+  // per-frame iteration-counter offsets, cached (a global load on every submit/complete)
+  static constexpr int kIbCache = 16;
+  int32_t ib_[kIbCache];
+  __device__ __forceinline__ int frame_ib(int f) const { return f < kIbCache ? ib_[f] : P.frames[f].iter_base; }
+  // successors of an in-flight instance: up to kInlineSucc in shared memory (r_sn count,
+  // r_sv ids), the rest in the global edge list (r_succ head)
+  static constexpr int kInlineSucc = 4;
+  int32_t* r_sn;
+  int32_t* r_sv;
   // region profiler (profiling runs only): cycles + count into op_cyc/op_cnt[slot]
   struct Region {
     Driver* d; int slot; long long c0;
 #ifdef __CUDA_ARCH__
-    __device__ Region(Driver* dd, int s) : d(dd), slot(s), c0(dd->A.prof ? clock64() : 0) {}
+    __device__ Region(Driver* dd, int s) : d(dd), slot(s), c0((kProfBuild && dd->A.prof) ? clock64() : 0) {}
     __device__ ~Region() {
-      if (d->A.prof) { d->op_cyc[slot] += clock64() - c0; d->op_cnt[slot]++; }
+      if (kProfBuild && d->A.prof) { d->op_cyc[slot] += clock64() - c0; d->op_cnt[slot]++; }
     }
 #else
     __device__ Region(Driver* dd, int s) : d(dd), slot(s), c0(0) {}
 #endif
   };
 
-  __forceinline__ __device__ int32_t new_inst(int kind, int sub, int ntiles) {
+  __noinline__ __device__ int32_t new_inst(int kind, int sub, int ntiles) {
     if (ninst >= A.inst_cap) {
       fail(CF_E_STACK_BUDGET, -1);
       return -1;
@@ -942,6 +1080,7 @@ struct Driver {
     r_pend[sl] = 0;
     r_succ[sl] = -1;
     r_last[sl] = -1;
+    r_sn[sl] = 0;
     r_nt[sl] = ntiles;
     r_kfi[sl] = (kind & 255) | (((cur_frame + 1) & 255) << 8) | ((cur_frame >= 0 ? iter : 0) << 16);
     Inst& I = A.insts[id];
@@ -954,7 +1093,7 @@ struct Driver {
     for (int j = 0; j < 4; ++j) I.s[j] = 0;
     I.n = I.m = I.k = 0;
     I.signal = nullptr;
-    if (A.prof) {
+    if (kProfBuild && A.prof) {
       unsigned long long* pr = A.prof + 6 * (int64_t)id;
       pr[0] = globaltimer();
       pr[1] = 0;
@@ -969,6 +1108,14 @@ struct Driver {
     if (done(w)) return;
     const int ws = w & kRingMask;
     if (r_last[ws] == id) return;   // dedupe repeated inputs from the same producer
+    const int ns = r_sn[ws];
+    if (ns < kInlineSucc) {
+      r_sv[ws * kInlineSucc + ns] = id;
+      r_sn[ws] = ns + 1;
+      r_last[ws] = id;
+      r_pend[id & kRingMask]++;
+      return;
+    }
     if (nedge >= A.edge_cap) {
       fail(CF_E_STACK_BUDGET, -2);
       return;
@@ -982,7 +1129,7 @@ struct Driver {
   }
   // two rings: critical-path work (high) and filler work (low: dW chunks) so that the
   // recurrence never queues behind throughput work
-  __forceinline__ __device__ void publish(int32_t id) {
+  __noinline__ __device__ void publish(int32_t id) {
     const int sl = id & kRingMask;
     if ((r_kfi[sl] & 255) == HK_WAIT) {   // polled by drain() until the flag arrives
       const Inst& I = A.insts[id];
@@ -1013,7 +1160,7 @@ struct Driver {
     const bool low = (r_kfi[sl] & 255) == HK_LSTM_DW_TC;
     // one entry per instance; workers claim its tiles through tile_next[id]. At most kRing
     // instances are in flight, so the 2^22-entry rings never wrap onto live entries.
-    if (A.prof) A.prof[6 * (int64_t)id + 1] = globaltimer();
+    if (kProfBuild && A.prof) A.prof[6 * (int64_t)id + 1] = globaltimer();
     unsigned long long* ring = low ? A.lq : A.queue;
     unsigned long long& tail = low ? lq_tail : q_tail;
     ring[tail & (A.q_cap - 1)] = (unsigned long long)id;
@@ -1027,7 +1174,7 @@ struct Driver {
     outstanding++;
     n_inst++;
     n_tiles += r_nt[sl];
-    if (cur_frame >= 0) iter_out_[P.frames[cur_frame].iter_base + iter]++;
+    if (cur_frame >= 0) iter_out_[frame_ib(cur_frame) + iter]++;
     if (r_pend[sl] == 0) publish(id);
   }
   __noinline__ __device__ void complete(int32_t id) {
@@ -1035,9 +1182,14 @@ struct Driver {
     outstanding--;
     const int kfi = r_kfi[sl];
     const int fr = ((kfi >> 8) & 255) - 1;
-    if (fr >= 0) iter_out_[P.frames[fr].iter_base + (kfi >> 16)]--;
+    if (fr >= 0) iter_out_[frame_ib(fr) + (kfi >> 16)]--;
     int32_t e = r_succ[sl];
+    const int ns = r_sn[sl];
     r_id[sl] = -1;   // done
+    for (int k = 0; k < ns; ++k) {
+      const int32_t s2 = r_sv[sl * kInlineSucc + k];
+      if (--r_pend[s2 & kRingMask] == 0) publish(s2);
+    }
     while (e >= 0) {
       const int32_t s2 = A.edge_to[e];
       const int32_t nx = A.edge_next[e];
@@ -1090,14 +1242,15 @@ struct Driver {
       complete(id);
       any = true;
     }
+    // relaxed poll (an acquire load would invalidate L1 at every poll); the release store
+    // that publishes successors orders this observation before them (fence.acq_rel).
+    // (A helper warp mirroring this queue into shared memory measured 5% slower.)
     for (int k = 0; k < 256; ++k) {
-      int* p = &A.cq[cq_head & (A.cq_cap - 1)];
-      // relaxed poll (an acquire load would invalidate L1 at every poll); the release store
-      // that publishes successors orders this observation before them (fence.acq_rel)
+      int* p = &A.cq[cq_head_ & (A.cq_cap - 1)];
       int v = ld_volatile_i32(p);
       if (v == 0) break;
       *(volatile int*)p = 0;
-      cq_head++;
+      cq_head_++;
       complete(v - 1);
       any = true;
     }
@@ -1105,7 +1258,18 @@ struct Driver {
   }
 
   // ---------------------------------------------------------------- placement
+  // code size matters on the driver's path (the I-cache is 32 KB): the placement and the
+  // operand-registry lookups are out of line, returning their results in registers
   __forceinline__ __device__ bool place(const DNode& d, int port, int64_t* ptr) {
+    const int64_t v = place_(d, port);
+    *ptr = v;
+    return v != -1;
+  }
+  __noinline__ __device__ int64_t place_(const DNode& d, int port) {
+    int64_t r = -1;
+    return place_core(d, port, &r) ? r : -1;
+  }
+  __forceinline__ __device__ bool place_core(const DNode& d, int port, int64_t* ptr) {
     const PlaceDesc& pl = places_[d.place_off + port];
     int it = cur_frame >= 0 ? iter : 0;
     switch (pl.kind) {
@@ -1129,12 +1293,12 @@ struct Driver {
       case PL_TA: {
         int64_t ix;
         if (!scalar(toks_[pl.index_vid], &ix)) return false;
-        const DTA& ta = P.tas[pl.ta];
+        const DTA& ta = tas_[pl.ta];
         if (ix < 0 || ix >= ta.size) {
           fail(CF_E_SHAPE, ix);
           return false;
         }
-        *ptr = A.ta_base[pl.ta] + ix * pl.elem_bytes;
+        *ptr = tab_[pl.ta] + ix * pl.elem_bytes;
         return true;
       }
     }
@@ -1171,8 +1335,23 @@ struct Driver {
   }
   // with a per-(node, operand) hint: the entry found last time is tried first (an operand of a
   // given node nearly always lives in the same ring / arena / TensorArray)
+  struct MapSlot {
+    int64_t map, slot;
+  };
   __forceinline__ __device__ bool resolve(int64_t p, int rows, int cols, int kind, int64_t* map, int64_t* slot,
                                           int16_t* hint) {
+    const MapSlot r = resolve_(p, rows, cols, kind, hint);
+    *map = r.map;
+    *slot = r.slot;
+    return r.map != 0;
+  }
+  __noinline__ __device__ MapSlot resolve_(int64_t p, int rows, int cols, int kind, int16_t* hint) {
+    MapSlot r{0, 0};
+    if (!resolve_core(p, rows, cols, kind, &r.map, &r.slot, hint)) r.map = 0;
+    return r;
+  }
+  __forceinline__ __device__ bool resolve_core(int64_t p, int rows, int cols, int kind, int64_t* map, int64_t* slot,
+                                               int16_t* hint) {
     const int h = *hint;
     if (h >= 0 && h < P.n_reg && reg_match(h, p, rows, cols, kind, map, slot)) return true;
     // entries are sorted by base (host): binary search for the last base <= p, then the
@@ -1199,7 +1378,7 @@ struct Driver {
   }
 
   // per-run weight preparation (bf16 permuted W / W^T), created on first use of the node
-  __forceinline__ __device__ int32_t prep(const DNode& d, int nid, int kind, int64_t dst) {
+  __noinline__ __device__ int32_t prep(const DNode& d, int nid, int kind, int64_t dst) {
     if (prep_inst_[nid] >= 0) return prep_inst_[nid];
     const int64_t In = d.imm[1], H = d.imm[2], KT = In + H;
     int ntiles = kind == HK_PREP_WP ? (int)((4 * H + 15) / 16) : (int)((KT / 64) * (4 * H / 128));
@@ -1216,7 +1395,7 @@ struct Driver {
     return id;
   }
 
-  __forceinline__ __device__ int eval_lstm_tc(const DNode& d, int nid, const int64_t* outp) {
+  __noinline__ __device__ int eval_lstm_tc(const DNode& d, int nid, const int64_t* outp) {
     // operand-registry hints live in the (driver-private) body-program copy of the node
     int16_t* hint = (int16_t*)const_cast<DNode&>(d).pad;
     Region rg(this, 32 + 9);
@@ -1227,21 +1406,21 @@ struct Driver {
     const int64_t B = d.imm[0], In = d.imm[1], H = d.imm[2], KT = In + H;
     auto ip = [&](int j) { return in_tok(d, j).v; };
     if (kind == HK_LSTM_FWD) {
-      long long q0 = A.prof ? clock64() : 0;
+      long long q0 = (kProfBuild && A.prof) ? clock64() : 0;
       int32_t pw = prep(d, nid, HK_PREP_WP, outp[4]);
       int64_t mx, sx, mh, sh, mw, sw;
       if (!resolve(ip(0), (int)B, (int)In, 0, &mx, &sx, hint + 0) || !resolve(ip(1), (int)B, (int)H, 0, &mh, &sh, hint + 1) ||
           !resolve(outp[4], (int)(4 * H), (int)KT, 1, &mw, &sw, hint + 2))
         return EV_ERROR;
-      long long q1 = A.prof ? clock64() : 0;
-      if (A.prof) { op_cyc[32 + 14] += q1 - q0; op_cnt[32 + 14]++; }
+      long long q1 = (kProfBuild && A.prof) ? clock64() : 0;
+      if (kProfBuild && A.prof) { op_cyc[32 + 14] += q1 - q0; op_cnt[32 + 14]++; }
       // 256-row tiles (tc_tile2) trade tile count for operand bytes: only for large batches;
       // the recurrence wants many short tiles (measured on cfg3)
       const bool m2 = B >= kM2MinRows;
       int32_t id = new_inst(HK_LSTM_FWD_TC, masked | (m2 ? 2 : 0),
                             (int)((m2 ? (B + 255) / 256 : (B + 127) / 128) * (H / 64)));
-      long long q2 = A.prof ? clock64() : 0;
-      if (A.prof) { op_cyc[32 + 15] += q2 - q1; op_cnt[32 + 15]++; }
+      long long q2 = (kProfBuild && A.prof) ? clock64() : 0;
+      if (kProfBuild && A.prof) { op_cyc[32 + 15] += q2 - q1; op_cnt[32 + 15]++; }
       if (id < 0) return EV_ERROR;
       Inst& I = A.insts[id];
       I.m = B; I.k = In; I.n = H;
@@ -1250,18 +1429,18 @@ struct Driver {
       I.p[6] = ip(1);
       for (int p = 0; p < 4; ++p) I.p[8 + p] = outp[p];
       I.s[0] = t; I.s[1] = d.aux[2]; I.s[2] = sx; I.s[3] = sh;
-      long long q3 = A.prof ? clock64() : 0;
-      if (A.prof) { op_cyc[32 + 16] += q3 - q2; op_cnt[32 + 16]++; }
+      long long q3 = (kProfBuild && A.prof) ? clock64() : 0;
+      if (kProfBuild && A.prof) { op_cyc[32 + 16] += q3 - q2; op_cnt[32 + 16]++; }
       for (int j = 0; j < d.n_in; ++j) add_dep(id, in_tok(d, j).writer);
       add_dep(id, pw);
-      long long q4 = A.prof ? clock64() : 0;
-      if (A.prof) { op_cyc[32 + 17] += q4 - q3; op_cnt[32 + 17]++; }
+      long long q4 = (kProfBuild && A.prof) ? clock64() : 0;
+      if (kProfBuild && A.prof) { op_cyc[32 + 17] += q4 - q3; op_cnt[32 + 17]++; }
       set_out(d, 0, ptr_tok(outp[0], id, D_BF16));
       set_out(d, 1, ptr_tok(outp[1], id, D_F32));
       set_out(d, 2, ptr_tok(outp[2], id, D_BF16));
       set_out(d, 3, ptr_tok(outp[3], id, D_BF16));
       submit(id);
-      if (A.prof) { op_cyc[32 + 18] += clock64() - q4; op_cnt[32 + 18]++; }
+      if (kProfBuild && A.prof) { op_cyc[32 + 18] += clock64() - q4; op_cnt[32 + 18]++; }
       return EV_OK;
     }
     // ---- backward: EW (dz, dc, db partials) -> DXH (dx, dh) and DW (dW, db)
@@ -1377,10 +1556,10 @@ struct Driver {
     int nplace = d.n_out;
     if (kind == HK_LSTM_BWD_EW) nplace += tcm ? 2 : 1;
     if (kind == HK_LSTM_FWD && tcm) nplace += 1;
-    long long q0 = A.prof ? clock64() : 0;
+    long long q0 = (kProfBuild && A.prof) ? clock64() : 0;
     for (int p = 0; p < nplace; ++p)
       if (!place(d, p, &outp[p])) return st->error ? EV_ERROR : EV_BLOCKED;
-    if (A.prof) { op_cyc[32 + 19] += clock64() - q0; op_cnt[32 + 19]++; }
+    if (kProfBuild && A.prof) { op_cyc[32 + 19] += clock64() - q0; op_cnt[32 + 19]++; }
     if (tcm && (kind == HK_LSTM_FWD || kind == HK_LSTM_BWD_EW)) return eval_lstm_tc(d, nid, outp);
     auto ip = [&](int j) { return in_tok(d, j).v; };
     auto dep_all = [&](int32_t id) {
@@ -1759,6 +1938,7 @@ struct Driver {
       set_dead_all(d);
       n_dead++;
     } else {
+      drain();   // completions first: a producer's consumers are published with little delay
       const int r = eval_heavy(d, nid);
       if (r != EV_OK) return r;
     }
@@ -1950,17 +2130,17 @@ struct Driver {
         int ta = (int)in_tok(d, 0).v;
         int64_t ix;
         if (!scalar(in_tok(d, 1), &ix)) return EV_BLOCKED;
-        const DTA& T = P.tas[ta];
+        const DTA& T = tas_[ta];
         if (ix < 0 || ix >= T.size) {
           fail(CF_E_SHAPE, ix);
           return EV_ERROR;
         }
-        int so = A.ta_slot_off[ta] + (int)ix;
+        int so = tso_[ta] + (int)ix;
         if (!T.is_grad && !A.ta_written[so]) {
           fail(CF_E_INVALID_GRAPH, ix);
           return EV_ERROR;
         }
-        set_out(d, 0, ptr_tok(A.ta_base[ta] + ix * T.elem_bytes, A.ta_writer[so], T.dt));
+        set_out(d, 0, ptr_tok(tab_[ta] + ix * T.elem_bytes, A.ta_writer[so], T.dt));
         break;
       }
       case OP_TA_WRITE: {
@@ -1972,14 +2152,14 @@ struct Driver {
           int ta = (int)in_tok(d, 0).v;
           int64_t ix;
           if (!scalar(in_tok(d, 1), &ix)) return EV_BLOCKED;
-          const DTA& T = P.tas[ta];
+          const DTA& T = tas_[ta];
           if (ix < 0 || ix >= T.size) {
             fail(CF_E_SHAPE, ix);
             return EV_ERROR;
           }
-          int so = A.ta_slot_off[ta] + (int)ix;
+          int so = tso_[ta] + (int)ix;
           const Tok& v = in_tok(d, 2);
-          int64_t dst = A.ta_base[ta] + ix * T.elem_bytes;
+          int64_t dst = tab_[ta] + ix * T.elem_bytes;
           if (A.ta_written[so]) {
             if (!T.is_grad) {
               fail(CF_E_DOUBLE_WRITE, ix);
@@ -2011,11 +2191,11 @@ struct Driver {
           break;
         }
         int ta = (int)in_tok(d, 0).v;
-        const DTA& T = P.tas[ta];
+        const DTA& T = tas_[ta];
         int32_t join = new_inst(HK_NOP, 0, 1);
         if (join < 0) return EV_ERROR;
         for (int i = 0; i < T.size; ++i) {
-          int so = A.ta_slot_off[ta] + i;
+          int so = tso_[ta] + i;
           if (!T.is_grad && !A.ta_written[so]) {
             fail(CF_E_INVALID_GRAPH, i);
             return EV_ERROR;
@@ -2023,7 +2203,7 @@ struct Driver {
           add_dep(join, A.ta_writer[so]);
         }
         submit(join);
-        set_out(d, 0, ptr_tok(A.ta_base[ta], join, T.dt));
+        set_out(d, 0, ptr_tok(tab_[ta], join, T.dt));
         break;
       }
       case OP_TA_UNSTACK: {
@@ -2033,15 +2213,15 @@ struct Driver {
         f.dead = dead;
         if (!dead) {
           int ta = (int)in_tok(d, 0).v;
-          const DTA& T = P.tas[ta];
+          const DTA& T = tas_[ta];
           const Tok& v = in_tok(d, 1);
           bool any = false;
-          for (int i = 0; i < T.size; ++i) any |= A.ta_written[A.ta_slot_off[ta] + i] != 0;
+          for (int i = 0; i < T.size; ++i) any |= A.ta_written[tso_[ta] + i] != 0;
           if (!any) {
-            A.ta_base[ta] = v.v;   // alias the unstacked tensor (no copy)
+            tab_[ta] = v.v;   // alias the unstacked tensor (no copy)
             for (int i = 0; i < T.size; ++i) {
-              A.ta_writer[A.ta_slot_off[ta] + i] = v.writer;
-              A.ta_written[A.ta_slot_off[ta] + i] = 1;
+              A.ta_writer[tso_[ta] + i] = v.writer;
+              A.ta_written[tso_[ta] + i] = 1;
             }
           } else {
             fail(CF_E_DOUBLE_WRITE, 0);
@@ -2229,15 +2409,22 @@ struct Driver {
   __noinline__ __device__ bool run_body(const DFrame& F) {
     Region rg(this, 32 + 0);
     bool progress = false;
-    const bool prof = A.prof != nullptr;
+    const bool prof = (kProfBuild && A.prof != nullptr);
     const int n_body = F.n_body;
     int pc = body_pc;
     const FastEnv env = fast_env();
     FastCount fc{0, 0, 0, 0, 0};
+    int since_drain = 0;
     while (pc < n_body) {
-      if ((pc & 15) == 0) drain();
       const DNode* d = bn_ + pc;
       const int op = d->op;
+      // completions are picked up every few nodes and before every heavy node: the latency
+      // from a producer's last tile to its consumers' publication is on the recurrence's
+      // critical path
+      if (++since_drain >= 16) {
+        drain();
+        since_drain = 0;
+      }
       if (d->ctx) {   // node of a structured cond branch: skip it when the branch is dead
         const int l = lval_[d->ctx] >= 0 && lstamp_[d->ctx] == lgen_ ? lval_[d->ctx] : ctx_live(d->ctx);
         if (l < 0) break;
@@ -2255,7 +2442,7 @@ struct Driver {
         continue;
       }
       if (op == OP_MERGE && d->aux[5] && (ctx_live(d->aux[6]) < 0 || ctx_live(d->aux[5]) < 0)) break;
-      if (op <= OP_NEXTITER || op == OP_STACK_PUSH || op == OP_STACK_POP) {
+      if (op <= OP_TA_GRAD || op == OP_ACC || op == OP_STACK_PUSH || op == OP_STACK_POP) {
         long long cs0 = prof ? clock64() : 0;
         const int r = P.n_swaps && (op == OP_STACK_PUSH || op == OP_STACK_POP) ? 0 : fast_node(d, env, fc);
         if (r < 0) {
@@ -2271,7 +2458,8 @@ struct Driver {
       }
       body_pc = pc;
       long long c0 = prof ? clock64() : 0;
-      const int nid = P.order[F.body_off + pc];
+      const int16_t hn = ((const int16_t*)d->pad)[5];   // node id (compiler; -1: look it up)
+      const int nid = hn >= 0 ? hn : P.order[F.body_off + pc];
       const bool routing = op == OP_SWITCH || op == OP_MERGE || op == OP_MERGE_LOOP || op == OP_NEXTITER ||
                            op == OP_PASS || (op == OP_CONST && d->aux[0] == 1);
       // one call level: heavy nodes and the general ops skip the routing front end
@@ -2402,7 +2590,7 @@ struct Driver {
     }
     last_progress = globaltimer();
     while (!st->error) {
-      long long ci = A.prof ? clock64() : 0;
+      long long ci = (kProfBuild && A.prof) ? clock64() : 0;
       bool p = drain();
       if (st->error) break;
       p |= step();
@@ -2499,13 +2687,13 @@ __device__ void worker_loop(const RunArgs& A) {
     if (e == ~0ULL) break;
     const int32_t id = (int32_t)(e >> 32);
     const int tile = (int)(e & 0xffffffffULL);
-    unsigned long long t_tile0 = A.prof ? globaltimer() : 0;
+    unsigned long long t_tile0 = (kProfBuild && A.prof) ? globaltimer() : 0;
     __shared__ Inst s_inst;
     if (threadIdx.x < (int)(sizeof(Inst) / 8))
       ((int64_t*)&s_inst)[threadIdx.x] = ((volatile const int64_t*)(A.insts + id))[threadIdx.x];
     __syncthreads();
     const Inst I = s_inst;
-    switch (I.kind) {
+    switch (kDbgFlags & 1 ? (int)HK_NOP : (int)I.kind) {
       case HK_NOP: break;
       case HK_EW: tile_ew(I, tile); break;
       case HK_FILL: tile_fill(I, tile); break;
@@ -2529,7 +2717,7 @@ __device__ void worker_loop(const RunArgs& A) {
     if (tcmode) tc::fence_proxy_async_global();
     __syncthreads();
     if (threadIdx.x == 0) {
-      if (A.prof) {
+      if (kProfBuild && A.prof) {
         unsigned long long t1 = globaltimer();
         unsigned long long* pr = A.prof + 6 * (int64_t)id;
         atomicMin(&pr[2], t_tile0);
@@ -2583,7 +2771,8 @@ __global__ void __launch_bounds__(kThreads, 1) cf_driver_kernel(RunArgs A_param)
     Tok* toks = A.toks;
     DNode* smn = nullptr;
     int32_t* smi = nullptr;
-    const int64_t ring_b = 6 * 4 * 1024;   // in-flight instance ring (always in smem)
+    // in-flight instance ring + completion mirror ring (always in smem)
+    const int64_t ring_b = (7 + Driver::kInlineSucc) * 4 * 1024;   // in-flight ring (always in smem)
     uint8_t* base = drv_smem + ring_b;
     const int64_t avail = A.dyn_smem - ring_b;
     const int64_t tok_b = (int64_t)A.prog.n_vids * (int64_t)sizeof(Tok);
@@ -2611,6 +2800,9 @@ __global__ void __launch_bounds__(kThreads, 1) cf_driver_kernel(RunArgs A_param)
       return p;
     };
     const Prog& P = A.prog;
+    DTA* s_tas = (DTA*)carve((int64_t)P.n_tas * sizeof(DTA));
+    int64_t* s_tab = (int64_t*)carve(8 * (int64_t)P.n_tas);
+    int32_t* s_tso = (int32_t*)carve(4 * (int64_t)P.n_tas);
     PlaceDesc* s_pl = (PlaceDesc*)carve((int64_t)P.n_places * sizeof(PlaceDesc));
     DReg* s_reg = (DReg*)carve((int64_t)P.n_reg * sizeof(DReg));
     int32_t* s_sd = (int32_t*)carve(4 * (int64_t)P.n_stacks);
@@ -2626,6 +2818,9 @@ __global__ void __launch_bounds__(kThreads, 1) cf_driver_kernel(RunArgs A_param)
                         (s_iter ? 256 : 0) | (s_stk ? 512 : 0);
       A.st->smem_used = (int32_t)used;
     }
+    for (int i = threadIdx.x; s_tas && i < P.n_tas; i += blockDim.x) s_tas[i] = P.tas[i];
+    for (int i = threadIdx.x; s_tab && i < P.n_tas; i += blockDim.x) s_tab[i] = A.ta_base[i];
+    for (int i = threadIdx.x; s_tso && i < P.n_tas; i += blockDim.x) s_tso[i] = A.ta_slot_off[i];
     for (int i = threadIdx.x; s_pl && i < P.n_places; i += blockDim.x) s_pl[i] = P.places[i];
     for (int i = threadIdx.x; s_reg && i < P.n_reg; i += blockDim.x) s_reg[i] = P.reg[i];
     for (int i = threadIdx.x; s_sd && i < P.n_stacks; i += blockDim.x) s_sd[i] = 0;
@@ -2664,8 +2859,16 @@ __global__ void __launch_bounds__(kThreads, 1) cf_driver_kernel(RunArgs A_param)
         d.r_last = s_ring + 3072;
         d.r_nt = s_ring + 4096;
         d.r_kfi = s_ring + 5120;
+        d.r_sn = s_ring + 6144;
+        d.r_sv = s_ring + 7168;
       }
       if (s_stk) d.stacks_ = s_stk;
+      if (s_tas && s_tab && s_tso) {
+        d.tas_ = s_tas;
+        d.tab_ = s_tab;
+        d.tso_ = s_tso;
+      }
+      for (int f = 0; f < P.n_frames && f < Driver::kIbCache; ++f) d.ib_[f] = P.frames[f].iter_base;
       for (int c = 0; c < P.n_ctxs && c < Driver::kMaxCtx; ++c) {
         d.ctxs_[c] = P.ctxs[c];
         d.lstamp_[c] = 0;
@@ -3076,11 +3279,12 @@ void build_session(cf_session* s, const cf::Graph& g, const cf_run_opts* o,
   int sms = 0, per_sm = 0;
   s->dyn_smem = s->precision == CF_BF16 ? tc::kSmemTC : 0;
   // driver CTA: ring + tokens + body program + private arrays; capped below the opt-in limit
-  size_t need = 6 * 4 * 1024;
+  size_t need = (7 + 4) * 4 * 1024;   // in-flight ring incl. inline successors (kInlineSucc)
   need += (sizeof(Tok) * (size_t)P.n_vids + 15) / 16 * 16;
   need += sizeof(DNode) * (size_t)P.max_body + ((size_t)P.max_bi * 4 + 15) / 16 * 16;
   need += sizeof(PlaceDesc) * P.places.size() + sizeof(DReg) * (P.reg.size() + P.feeds.size() + 1);
   need += sizeof(DStack) * P.stacks.size() + 8 * P.nodes.size() + 4 * (P.accs.size() + P.iter_counters);
+  need += (sizeof(DTA) + 12) * P.tas.size() + 48;
   need += 16 * 12;
   const size_t smem_cap = 198 * 1024;   // + ~28 KiB static smem stays under the 227 KiB limit
   if ((int)std::min(need, smem_cap) > s->dyn_smem) s->dyn_smem = (int)std::min(need, smem_cap);
@@ -3402,6 +3606,9 @@ cf_status cf_session_connect(cf_session* s, int32_t peer, const void* handle, in
   }
 }
 
+int32_t cf_debug_set_flags(int32_t flags) {
+  return cudaMemcpyToSymbol(kDbgFlags, &flags, sizeof(flags)) == cudaSuccess ? CF_OK : CF_E_CUDA;
+}
 int32_t cf_debug_set_m2_rows(int32_t rows) {
   return cudaMemcpyToSymbol(kM2MinRows, &rows, sizeof(rows)) == cudaSuccess ? CF_OK : CF_E_CUDA;
 }

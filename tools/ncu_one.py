@@ -19,11 +19,14 @@ ap.add_argument("--config", default="cfg3")
 ap.add_argument("--precision", default="bf16")
 ap.add_argument("--T", type=int, default=0)
 ap.add_argument("--runs", type=int, default=2)
+ap.add_argument("--no-tiles", action="store_true", help="workers skip tile bodies (driver alone)")
 a = ap.parse_args()
 c = dict(CONFIGS[a.config])
 if a.T:
     c["T"] = a.T
 prec = cf.BF16 if a.precision == "bf16" else cf.F32
+if a.no_tiles:
+    cf.debug_set_flags(1)
 p = dynamic_rnn_lstm(c["T"], c["B"], c["I"], c["H"], c["L"])
 s = cf.Session(p.g, p.fetch_tensors(), precision=prec)
 f = rnn_inputs(c["T"], c["B"], c["I"], c["H"], c["L"], seed=0, len_mode=c["len_mode"], bf16=prec == cf.BF16)

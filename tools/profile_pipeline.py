@@ -13,7 +13,9 @@ import torch.distributed as dist  # noqa: E402
 
 import __graft_entry__  # noqa: E402
 
-__graft_entry__.build()
+# the profiler is compiled into libcf_prof.so only: build it and select it before cf loads
+os.environ["CF_LIB"] = "libcf_prof.so"
+__graft_entry__.build(profile=True)
 from bench import CONFIGS  # noqa: E402
 from paper_1805_01772_b200 import cf  # noqa: E402
 from paper_1805_01772_b200.models import dynamic_rnn_lstm, feeds_to_device  # noqa: E402

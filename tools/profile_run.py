@@ -10,7 +10,9 @@ import torch  # noqa: E402
 
 import __graft_entry__  # noqa: E402
 
-__graft_entry__.build()
+# the profiler is compiled into libcf_prof.so only: build it and select it before cf loads
+os.environ["CF_LIB"] = "libcf_prof.so"
+__graft_entry__.build(profile=True)
 from bench import CONFIGS  # noqa: E402
 from paper_1805_01772_b200 import cf  # noqa: E402
 from paper_1805_01772_b200.models import dynamic_rnn_lstm, feeds_to_device  # noqa: E402
@@ -41,11 +43,14 @@ def main():
     ap.add_argument("--stack-budget", type=int, default=0)
     ap.add_argument("--swap-smallest-first", action="store_true")
     ap.add_argument("--out", default="gpurun_out/profile.json")
+    ap.add_argument("--no-tiles", action="store_true", help="workers skip tile bodies (driver alone)")
     a = ap.parse_args()
     c = dict(CONFIGS[a.config])
     if a.T:
         c["T"] = a.T
     prec = cf.BF16 if a.precision == "bf16" else cf.F32
+    if a.no_tiles:
+        cf.debug_set_flags(1)
     p = dynamic_rnn_lstm(c["T"], c["B"], c["I"], c["H"], c["L"])
     s = cf.Session(p.g, p.fetch_tensors(), precision=prec, parallel_iterations=a.K, profile=True,
                    stack_budget_bytes=a.stack_budget, swap_smallest_first=a.swap_smallest_first)
