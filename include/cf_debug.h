@@ -28,8 +28,9 @@ int32_t cf_debug_session_profile(const struct cf_session* s, unsigned long long*
  * per CTA); default 1024. Lets tests exercise that tile shape at small sizes. Returns 0 or
  * CF_E_CUDA. */
 int32_t cf_debug_set_m2_rows(int32_t rows);
-/* Profiling knob: bit 0 = workers skip every tile body (the device driver's own cost in
- * isolation; results are garbage). Returns 0 or CF_E_CUDA. */
+/* Profiling knobs: bit 0 = workers skip every tile body (the device driver's own cost in
+ * isolation; results are garbage); bit 2 = the driver polls completions after every node
+ * instead of rate-limiting the poll (A/B). Returns 0 or CF_E_CUDA. */
 int32_t cf_debug_set_flags(int32_t flags);
 /* Compile a graph for the device program without a GPU and write its description and body
  * programs (one node per line, evaluation order) into buf; *needed = length + 1. */

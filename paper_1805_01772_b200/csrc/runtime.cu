@@ -58,7 +58,7 @@ constexpr bool kProfBuild = false;   // libcf.so: no profiler code on the driver
 #endif
 constexpr int kEwBig = 16384;   // elementwise (HK_EW) tile
 // forward / d[x,h] GEMMs use 256-row tiles from this batch size on (dW always does)
-__device__ int kM2MinRows = 1024;
+__device__ int kM2MinRows = 512;   // measured on cfg3 (B = 512): 2% faster than 1024
 // test/profiling knob (cf_debug_set_flags): bit 0 = workers skip the tile bodies (isolates the
 // driver's own cost; results are garbage)
 __device__ int kDbgFlags = 0;
@@ -930,7 +930,7 @@ struct Driver {
     __threadfence_block();
     *(volatile int*)&w.seq = w.seq + 1;
     while (*(volatile int*)&w.done < kWaveWarps) {
-      drain();   // the helper warps touch tokens and stacks only, never instance state
+      maybe_drain();   // the helper warps touch tokens and stacks only, never instance state
     }
     __threadfence_block();
     n_push += w.cnt.push;
@@ -1220,8 +1220,17 @@ struct Driver {
     }
     return any;
   }
+  // the completion poll is an L2 round trip: on the body path it is issued at most every
+  // kDrainCycles (bounds the completion latency without polling after every node)
+  static constexpr long long kDrainCycles = 3000;
+  long long last_drain_ = 0;
+  int dbg_ = 0;
+  __forceinline__ __device__ void maybe_drain() {
+    if ((dbg_ & 4) || clock64() - last_drain_ > kDrainCycles) drain();
+  }
   __noinline__ __device__ bool drain() {
     Region rg(this, 32 + 4);
+    last_drain_ = clock64();
     bool any = false;
     if (io_out > 0) any = drain_io();
     for (int k = 0; k < n_waits_;) {   // channel messages (Recv): flag = want, or the dead twin
@@ -1938,7 +1947,7 @@ struct Driver {
       set_dead_all(d);
       n_dead++;
     } else {
-      drain();   // completions first: a producer's consumers are published with little delay
+      maybe_drain();   // completions first: a producer's consumers are published with little delay
       const int r = eval_heavy(d, nid);
       if (r != EV_OK) return r;
     }
@@ -2422,7 +2431,7 @@ struct Driver {
       // from a producer's last tile to its consumers' publication is on the recurrence's
       // critical path
       if (++since_drain >= 16) {
-        drain();
+        maybe_drain();
         since_drain = 0;
       }
       if (d->ctx) {   // node of a structured cond branch: skip it when the branch is dead
@@ -2843,6 +2852,7 @@ __global__ void __launch_bounds__(kThreads, 1) cf_driver_kernel(RunArgs A_param)
     if (threadIdx.x == 0) {
       Driver& d = *new (drv_obj) Driver(A, toks, smn, smi, req);
       d.wave_ = &wave;
+      d.dbg_ = kDbgFlags;
       if (s_pl) d.places_ = s_pl;
       if (s_reg) d.reg_ = s_reg;
       if (s_sd) d.stack_depth_ = s_sd;

@@ -193,91 +193,111 @@ __device__ void tile_lstm_fwd_tc(const Inst& I, int tile, tc::TcShared& ts, uint
 
 // ---------------------------------------------------------------- backward elementwise
 // p: 2 c_prev(f32), 4 gates(bf16 interleaved), 5 lens, 6 dh_next(f32), 7 dc_next(f32),
-//    8 dout(dt s[4]), 9 dc(f32 out), 10 dz(bf16 out, [B][4H] natural) + partials
-// tile = 128 rows x 64 units; thread: unit t%64, rows t/64 + 4i
+//    8 dout(dt s[4]), 9 dc(f32 out), 10 dz(bf16 out, [B][4H] natural) + partials,
+//    14/15 folded AddN terms of dout (f32, optional)
+// tile = 128 rows x 64 units; thread: 4 consecutive units (16-byte fp32 / 8-byte bf16 vector
+// accesses), rows t/16 + 16i. HBM-bound: every operand is read once, dz / dc written once.
+__device__ __forceinline__ float4 ld4f(const float* p) { return *(const float4*)p; }
+__device__ __forceinline__ void bf4(const __nv_bfloat16* p, float* o) {
+  const uint2 v = *(const uint2*)p;
+  const __nv_bfloat162 a = *(const __nv_bfloat162*)&v.x, b = *(const __nv_bfloat162*)&v.y;
+  const float2 fa = __bfloat1622float2(a), fb = __bfloat1622float2(b);
+  o[0] = fa.x; o[1] = fa.y; o[2] = fb.x; o[3] = fb.y;
+}
 __device__ void tile_lstm_bwd_ew_bf(const Inst& I, int tile, float* sm) {
   const int B = (int)I.m, H = (int)I.n;
   const int tu = H / 64;
   const int rt = tile / tu, ut = tile % tu;
-  const int u = ut * 64 + threadIdx.x % 64, rg = threadIdx.x / 64;
+  const int ul = (threadIdx.x % 16) * 4;          // unit within the 64-unit slice
+  const int u = ut * 64 + ul, rg = threadIdx.x / 16;
   const float* c_prev = (const float*)I.p[2];
   const __nv_bfloat16* gates = (const __nv_bfloat16*)I.p[4];
   const int64_t* lens = (const int64_t*)I.p[5];
   const float* dhn = (const float*)I.p[6];
   const float* dcn = (const float*)I.p[7];
   const void* dout = (const void*)I.p[8];
-  const int dout_dt = (int)I.s[4];
+  const bool dout_bf = (int)I.s[4] == D_BF16;
+  const float* add0 = (const float*)I.p[14];
+  const float* add1 = (const float*)I.p[15];
   float* dc = (float*)I.p[9];
   __nv_bfloat16* dz = (__nv_bfloat16*)I.p[10];
   float* partial = (float*)(I.p[10] + I.s[5]);
   const bool masked = I.sub & 1;
   const int64_t t = I.s[0];
-  float sdb[4] = {0.f, 0.f, 0.f, 0.f};
+  float sdb[4][4] = {};
   const int nrow = min(128, B - rt * 128);
-  for (int i0 = 0; i0 < 32; i0 += 4) {
-    float ig[4], fg[4], gg[4], og[4], cp[4], dhv[4], dcn_[4];
-    int64_t len4[4];
-    bool ok[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int rr = rg + 4 * (i0 + j);
-      ok[j] = rr < nrow;
-      const int r = rt * 128 + (ok[j] ? rr : 0);
-      const int64_t e = (int64_t)r * H + u;
-      const __nv_bfloat16* gr = gates + (int64_t)r * 4 * H + ut * 256 + threadIdx.x % 64;
-      ig[j] = bf2f(gr[0]);
-      fg[j] = bf2f(gr[64]);
-      gg[j] = bf2f(gr[128]);
-      og[j] = bf2f(gr[192]);
-      cp[j] = c_prev[e];
-      dhv[j] = dhn[e] + ldf(dout, dout_dt, e);
-      if (I.p[14]) dhv[j] += ((const float*)I.p[14])[e];   // folded AddN terms
-      if (I.p[15]) dhv[j] += ((const float*)I.p[15])[e];
-      dcn_[j] = dcn[e];
-      len4[j] = masked ? lens[r] : 0;
+#pragma unroll 2
+  for (int i = 0; i < 8; ++i) {
+    const int rr = rg + 16 * i;
+    if (rr >= nrow) break;
+    const int r = rt * 128 + rr;
+    const int64_t e = (int64_t)r * H + u;
+    const __nv_bfloat16* gr = gates + (int64_t)r * 4 * H + ut * 256 + ul;
+    float ig[4], fg[4], gg[4], og[4];
+    bf4(gr, ig);
+    bf4(gr + 64, fg);
+    bf4(gr + 128, gg);
+    bf4(gr + 192, og);
+    const float4 cp = ld4f(c_prev + e), dn = ld4f(dhn + e), dcv = ld4f(dcn + e);
+    float dov[4];
+    if (dout_bf) bf4((const __nv_bfloat16*)dout + e, dov);
+    else {
+      const float4 d4 = ld4f((const float*)dout + e);
+      dov[0] = d4.x; dov[1] = d4.y; dov[2] = d4.z; dov[3] = d4.w;
     }
+    float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0;
+    if (add0) a0 = ld4f(add0 + e);   // folded AddN terms
+    if (add1) a1 = ld4f(add1 + e);
+    const bool live = !masked || t < lens[r];
+    const float cpa[4] = {cp.x, cp.y, cp.z, cp.w};
+    const float dna[4] = {dn.x + a0.x + a1.x, dn.y + a0.y + a1.y, dn.z + a0.z + a1.z, dn.w + a0.w + a1.w};
+    const float dca[4] = {dcv.x, dcv.y, dcv.z, dcv.w};
+    float zf[4][4];
+    float dco[4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      if (!ok[j]) continue;
-      const int r = rt * 128 + rg + 4 * (i0 + j);
-      const int64_t e = (int64_t)r * H + u;
-      float cn = fg[j] * cp[j] + ig[j] * gg[j];
-      float tc_ = tanhf(cn);
-      float dh = dhv[j];
-      float dcs = dh * og[j] * (1.0f - tc_ * tc_) + dcn_[j];
-      float z0 = dcs * gg[j] * ig[j] * (1.0f - ig[j]);
-      float z1 = dcs * cp[j] * fg[j] * (1.0f - fg[j]);
-      float z2 = dcs * ig[j] * (1.0f - gg[j] * gg[j]);
-      float z3 = dh * tc_ * og[j] * (1.0f - og[j]);
-      float dcp = dcs * fg[j];
-      if (masked && !(t < len4[j])) {
-        z0 = z1 = z2 = z3 = 0.0f;
-        dcp = dcn_[j];
+    for (int k = 0; k < 4; ++k) {
+      const float cn = fg[k] * cpa[k] + ig[k] * gg[k];
+      const float tc_ = tanhf(cn);
+      const float dh = dna[k] + dov[k];
+      const float dcs = dh * og[k] * (1.0f - tc_ * tc_) + dca[k];
+      zf[0][k] = dcs * gg[k] * ig[k] * (1.0f - ig[k]);
+      zf[1][k] = dcs * cpa[k] * fg[k] * (1.0f - fg[k]);
+      zf[2][k] = dcs * ig[k] * (1.0f - gg[k] * gg[k]);
+      zf[3][k] = dh * tc_ * og[k] * (1.0f - og[k]);
+      dco[k] = dcs * fg[k];
+      if (!live) {
+        zf[0][k] = zf[1][k] = zf[2][k] = zf[3][k] = 0.0f;
+        dco[k] = dca[k];
       }
-      __nv_bfloat16* zr = dz + (int64_t)r * 4 * H;
-      __nv_bfloat16 b0 = __float2bfloat16(z0), b1 = __float2bfloat16(z1),
-                    b2 = __float2bfloat16(z2), b3 = __float2bfloat16(z3);
-      zr[u] = b0;
-      zr[H + u] = b1;
-      zr[2 * H + u] = b2;
-      zr[3 * H + u] = b3;
-      // db sums the bf16-rounded dz, exactly what the dW GEMM consumes
-      sdb[0] += bf2f(b0);
-      sdb[1] += bf2f(b1);
-      sdb[2] += bf2f(b2);
-      sdb[3] += bf2f(b3);
-      dc[e] = dcp;
     }
-  }
-  // reduce the 4 row groups: sm[rg][g][64]
-  for (int g = 0; g < 4; ++g) sm[(rg * 4 + g) * 64 + threadIdx.x % 64] = sdb[g];
-  __syncthreads();
-  if (rg == 0) {
+    __nv_bfloat16* zr = dz + (int64_t)r * 4 * H + u;
+#pragma unroll
     for (int g = 0; g < 4; ++g) {
-      float s = 0.f;
-      for (int q = 0; q < 4; ++q) s += sm[(q * 4 + g) * 64 + threadIdx.x % 64];
-      partial[(int64_t)rt * 4 * H + g * H + u] = s;
+      const __nv_bfloat162 lo = __floats2bfloat162_rn(zf[g][0], zf[g][1]);
+      const __nv_bfloat162 hi = __floats2bfloat162_rn(zf[g][2], zf[g][3]);
+      // db sums the bf16-rounded dz, exactly what the dW GEMM consumes
+      sdb[g][0] += __low2float(lo);
+      sdb[g][1] += __high2float(lo);
+      sdb[g][2] += __low2float(hi);
+      sdb[g][3] += __high2float(hi);
+      uint2 pk;
+      pk.x = *(const uint32_t*)&lo;
+      pk.y = *(const uint32_t*)&hi;
+      *(uint2*)(zr + (int64_t)g * H) = pk;
     }
+    *(float4*)(dc + e) = make_float4(dco[0], dco[1], dco[2], dco[3]);
+  }
+  // reduce the 16 row groups: sm[rg][g][64]
+#pragma unroll
+  for (int g = 0; g < 4; ++g)
+    *(float4*)&sm[(rg * 4 + g) * 64 + ul] = make_float4(sdb[g][0], sdb[g][1], sdb[g][2], sdb[g][3]);
+  __syncthreads();
+  {
+    const int g = threadIdx.x / 64, uu = threadIdx.x % 64;   // 256 threads = 4 gates x 64 units
+    float acc = 0.f;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) acc += sm[(q * 4 + g) * 64 + uu];
+    partial[(int64_t)rt * 4 * H + g * H + ut * 64 + uu] = acc;
   }
   __syncthreads();
 }

@@ -20,6 +20,9 @@ s = cf.Session(p.g, p.fetch_tensors(), precision=cf.BF16)
 f = rnn_inputs(c["T"], c["B"], c["I"], c["H"], c["L"], seed=0, len_mode=c["len_mode"], bf16=True)
 dev = feeds_to_device(f, session=s)
 outs = s.alloc_outputs()
+if os.environ.get("M2"):
+    cf.debug_set_m2_rows(int(os.environ["M2"]))
+    print("m2 rows", os.environ["M2"])
 for flags in [int(x) for x in (sys.argv[2] if len(sys.argv) > 2 else '0,1,0').split(',')]:
     cf.debug_set_flags(flags)
     ts = []
