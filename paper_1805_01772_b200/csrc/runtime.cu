@@ -800,6 +800,7 @@ struct Wave {
   FastCount cnt;
   const DNode* bn;
   FastEnv env;
+  int env_frame;          // frame whose FastEnv is in env (-2: none); env.it is per wave
   int slow[256];          // wave positions left for the general evaluator
 };
 
@@ -925,10 +926,15 @@ struct Driver {
     w.nslow = 0;
     w.cnt = FastCount{0, 0, 0, 0, 0};
     w.bn = bn_;
-    w.env = fast_env();
+    if (w.env_frame != cur_frame) {   // the environment changes with the frame only
+      w.env = fast_env();
+      w.env_frame = cur_frame;
+    }
+    w.env.it = cur_frame >= 0 ? iter : 0;
     w.done = 0;
     __threadfence_block();
     *(volatile int*)&w.seq = w.seq + 1;
+    flush_publish();
     while (*(volatile int*)&w.done < kWaveWarps) {
       maybe_drain();   // the helper warps touch tokens and stacks only, never instance state
     }
@@ -1165,8 +1171,19 @@ struct Driver {
     unsigned long long& tail = low ? lq_tail : q_tail;
     ring[tail & (A.q_cap - 1)] = (unsigned long long)id;
     tail += 1;
-    // release: instance record + queue entries visible before the new tail
-    st_release_u64(low ? &st->lq_tail : &st->q_tail, tail);
+    // the tail is released by flush_publish() at the end of the current driver step (drain,
+    // heavy node, wave): one release fence covers every instance published in the step, and
+    // the record stores have mostly completed by then
+    dirty_ |= low ? 2 : 1;
+    if (dbg_ & 16) flush_publish();   // A/B knob: release after every publication
+  }
+  int dirty_ = 0;
+  __forceinline__ __device__ void flush_publish() {
+    if (!dirty_) return;
+    // release: instance records + queue entries visible before the new tails
+    if (dirty_ & 1) st_release_u64(&st->q_tail, q_tail);
+    if (dirty_ & 2) st_release_u64(&st->lq_tail, lq_tail);
+    dirty_ = 0;
   }
   __device__ void submit(int32_t id, bool = false) {
     if (id < 0) return;
@@ -1263,6 +1280,7 @@ struct Driver {
       complete(v - 1);
       any = true;
     }
+    flush_publish();
     return any;
   }
 
@@ -1949,6 +1967,7 @@ struct Driver {
     } else {
       maybe_drain();   // completions first: a producer's consumers are published with little delay
       const int r = eval_heavy(d, nid);
+      flush_publish();
       if (r != EV_OK) return r;
     }
     toks_[d.ctrl_vid] = Tok{0, -1, (uint8_t)dead, TK_FLOW, 0, 0};
@@ -2603,6 +2622,7 @@ struct Driver {
       bool p = drain();
       if (st->error) break;
       p |= step();
+      flush_publish();
       (void)ci;
       if (st->error) break;
       if (fetched && cur_frame < 0 && root_pc >= P.n_root_steps && outstanding == 0) break;
@@ -2844,6 +2864,7 @@ __global__ void __launch_bounds__(kThreads, 1) cf_driver_kernel(RunArgs A_param)
       req[1] = 0;
       wave.seq = 0;
       wave.done = 0;
+      wave.env_frame = -2;
     }
     __syncthreads();
     // the driver object itself lives in shared memory: its members are touched on every node
@@ -2889,6 +2910,7 @@ __global__ void __launch_bounds__(kThreads, 1) cf_driver_kernel(RunArgs A_param)
     } else if (threadIdx.x >= 32) {
       // helper warps: cooperative smem staging on request from the driver thread
       int seen = 0, wseen = 0;
+      const bool nosleep = kDbgFlags & 8;   // A/B knob: wave helpers spin without sleeping
       const int h = threadIdx.x - 32, nh = blockDim.x - 32;
       while (true) {
         int q = *(volatile int*)&req[0];
@@ -2904,7 +2926,8 @@ __global__ void __launch_bounds__(kThreads, 1) cf_driver_kernel(RunArgs A_param)
           continue;
         }
         if (q == seen) {
-          __nanosleep((threadIdx.x >> 5) == 4 ? 500 : 20);
+          if ((threadIdx.x >> 5) == 4) __nanosleep(500);
+          else if (!nosleep) __nanosleep(20);
           continue;
         }
         seen = q;
