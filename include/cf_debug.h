@@ -20,7 +20,9 @@ int32_t cf_debug_tc_gemm(int32_t M, int32_t N, int32_t K, int32_t bn, int32_t a_
  * per heavy instance 6 x u64 {create ns, publish ns, first tile start ns, last tile end ns,
  * summed tile busy ns, (kind << 32) | ntiles} (%globaltimer). Copies up to cap u64 of the
  * last run into out; *n_inst = records available; t0 (130 x u64) = {run start ns, run end ns,
- * 64 driver counts, 64 driver cycles: opcodes [0,32), profiled regions [32,64)}. */
+ * 64 driver counts, 64 driver cycles: opcodes [0,32), profiled regions [32,64)}; count/cycle
+ * slot 31 = the driver's shared-memory staging mask / bytes. Without profiling only t0 is
+ * filled (*n_inst = 0). */
 struct cf_session;
 int32_t cf_debug_session_profile(const struct cf_session* s, unsigned long long* out, int64_t cap,
                                  int64_t* n_inst, unsigned long long* t0);

@@ -3649,10 +3649,11 @@ int32_t cf_debug_set_m2_rows(int32_t rows) {
 // profiling hook (include/cf_debug.h): per-instance timing of the last cf_run
 int32_t cf_debug_session_profile(const cf_session* s, unsigned long long* out, int64_t cap,
                                  int64_t* n_inst, unsigned long long* t0) {
-  if (!s || !s->args.prof) return CF_E_INVALID_GRAPH;
+  if (!s) return CF_E_INVALID_GRAPH;
   RunState st;
   if (cudaMemcpy(&st, s->args.st, sizeof(RunState), cudaMemcpyDeviceToHost) != cudaSuccess) return CF_E_CUDA;
-  int64_t n = std::min<int64_t>(st.instances + 64, s->args.inst_cap);
+  // without the profiling build / profile=True only the driver counters (t0) are available
+  int64_t n = s->args.prof ? std::min<int64_t>(st.instances + 64, s->args.inst_cap) : 0;
   if (n_inst) *n_inst = n;
   if (t0) {
     t0[0] = st.t_start;
@@ -3662,7 +3663,7 @@ int32_t cf_debug_session_profile(const cf_session* s, unsigned long long* out, i
       t0[66 + k] = (unsigned long long)st.op_cycles[k];
     }
   }
-  if (out && cap > 0) {
+  if (out && cap > 0 && n > 0) {
     int64_t k = std::min(cap, 6 * n);
     if (cudaMemcpy(out, s->args.prof, 8 * k, cudaMemcpyDeviceToHost) != cudaSuccess) return CF_E_CUDA;
   }
