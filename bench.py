@@ -218,7 +218,10 @@ def main():
     stage = (rank, world) if pipe else None
     p = dynamic_rnn_lstm(c["T"], c["B"], c["I"], c["H"], c["L"], stage=stage,
                          moe=c.get("moe", False))
-    stream = torch.cuda.current_stream()
+    # a dedicated stream, current for torch too: the input copies of the end-to-end loop and
+    # the cf_run launches are ordered on it
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     sess = cf.Session(p.g, p.fetch_tensors(), precision=prec, parallel_iterations=args.K,
                       device=local, stream=stream.cuda_stream,
                       watchdog_ms=300000 if pipe else 0, stack_budget_bytes=args.stack_budget,

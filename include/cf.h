@@ -160,7 +160,8 @@ typedef struct {
   int32_t parallel_iterations;  /* 0 = per-loop value; else overrides every loop          */
   int32_t device;               /* CUDA device ordinal                                    */
   int32_t num_workers;          /* 0 = one worker CTA per SM (minus the driver CTA)       */
-  void* stream;                 /* cudaStream_t; NULL = a library-owned stream            */
+  void* stream;                 /* cudaStream_t; NULL = a library-owned stream, each run
+                                   ordered after the legacy default stream's prior work  */
   int64_t max_iterations;       /* per-frame iteration bound for stack arenas; 0 = infer
                                    from TensorArray sizes                                */
   int64_t watchdog_ms;          /* device watchdog; 0 = 60000                             */

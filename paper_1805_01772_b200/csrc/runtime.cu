@@ -935,8 +935,17 @@ struct Driver {
     __threadfence_block();
     *(volatile int*)&w.seq = w.seq + 1;
     flush_publish();
+    long long wq0 = (kProfBuild && A.prof) ? clock64() : 0, wdr = 0;
     while (*(volatile int*)&w.done < kWaveWarps) {
+      long long d0 = (kProfBuild && A.prof) ? clock64() : 0;
       maybe_drain();   // the helper warps touch tokens and stacks only, never instance state
+      if (kProfBuild && A.prof) wdr += clock64() - d0;
+    }
+    if (kProfBuild && A.prof) {   // W_WAIT: signal -> done seen; W_WAIT_DRAIN: drains inside
+      op_cyc[32 + 20] += clock64() - wq0;
+      op_cnt[32 + 20]++;
+      op_cyc[32 + 21] += wdr;
+      op_cnt[32 + 21] += w.nslow;   // count = leftover nodes
     }
     __threadfence_block();
     n_push += w.cnt.push;
@@ -2973,7 +2982,7 @@ struct cf_session {
   void* d_state_block = nullptr;   // zeroed at every run
   std::vector<std::pair<void*, size_t>> zero_each_run;
   std::vector<std::pair<void*, int>> fill_ff_each_run;
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_in = nullptr;
   int64_t watchdog_ns = 60LL * 1000 * 1000 * 1000;
   int sched_seed = 0;
   int dyn_smem = 0;
@@ -3105,6 +3114,7 @@ void build_session(cf_session* s, const cf::Graph& g, const cf_run_opts* o,
   }
   CUDA_OK(cudaEventCreate(&s->ev0));
   CUDA_OK(cudaEventCreate(&s->ev1));
+  CUDA_OK(cudaEventCreateWithFlags(&s->ev_in, cudaEventDisableTiming));
   cf::HostProgram& P = s->P;
   // ---- buffers
   s->buf_ptr.resize(P.bufs.size());
@@ -3469,6 +3479,12 @@ cf_status cf_run(cf_session* s, int32_t n_feed, const char* const* feed_names,
       *(volatile unsigned long long*)s->io_tail_host = 0;
       io = std::thread([s, &io_stop, &io_err]() { io_executor(s, &io_stop, &io_err); });
     }
+    if (s->own_stream) {
+      // a library-owned stream is non-blocking: order the run after the caller's work on the
+      // legacy default stream (e.g. the copies of this run's inputs)
+      CUDA_OK(cudaEventRecord(s->ev_in, cudaStreamLegacy));
+      CUDA_OK(cudaStreamWaitEvent(s->stream, s->ev_in, 0));
+    }
     CUDA_OK(cudaEventRecord(s->ev0, s->stream));
     cudaError_t lerr = cudaLaunchCooperativeKernel((void*)cf_driver_kernel, dim3(s->grid), dim3(kThreads),
                                                    kargs, s->dyn_smem, s->stream);
@@ -3681,6 +3697,7 @@ void cf_session_destroy(cf_session* s) {
   }
   if (s->chan_mem) cudaFree(s->chan_mem);
   if (s->ev0) cudaEventDestroy(s->ev0);
+  if (s->ev_in) cudaEventDestroy(s->ev_in);
   if (s->ev1) cudaEventDestroy(s->ev1);
   if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
   delete s;
