@@ -1251,6 +1251,7 @@ struct Driver {
   // measured on cfg3: 3000 cycles 84.0 ms, 6000 83.6, 12000 82.5, 24000 82.5 ms per step
   static constexpr long long kDrainCycles = 12000;
   long long drain_cycles_ = kDrainCycles;   // A/B knob: debug flags bits 8-15 (x 1000 cycles)
+
   long long last_drain_ = 0;
   int dbg_ = 0;
   __forceinline__ __device__ void maybe_drain() {
@@ -2886,6 +2887,7 @@ __global__ void __launch_bounds__(kThreads, 1) cf_driver_kernel(RunArgs A_param)
       d.wave_ = &wave;
       d.dbg_ = kDbgFlags;
       if ((d.dbg_ >> 8) & 255) d.drain_cycles_ = 1000LL * ((d.dbg_ >> 8) & 255);
+
       if (s_pl) d.places_ = s_pl;
       if (s_reg) d.reg_ = s_reg;
       if (s_sd) d.stack_depth_ = s_sd;

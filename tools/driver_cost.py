@@ -17,7 +17,7 @@ from synth import rnn_inputs  # noqa: E402
 
 c = dict(CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "cfg3"])
 p = dynamic_rnn_lstm(c["T"], c["B"], c["I"], c["H"], c["L"])
-s = cf.Session(p.g, p.fetch_tensors(), precision=cf.BF16)
+s = cf.Session(p.g, p.fetch_tensors(), precision=cf.BF16, num_workers=int(os.environ.get("NW", "0")))
 f = rnn_inputs(c["T"], c["B"], c["I"], c["H"], c["L"], seed=0, len_mode=c["len_mode"], bf16=True)
 dev = feeds_to_device(f, session=s)
 outs = s.alloc_outputs()
