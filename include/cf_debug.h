@@ -31,8 +31,11 @@ int32_t cf_debug_session_profile(const struct cf_session* s, unsigned long long*
  * CF_E_CUDA. */
 int32_t cf_debug_set_m2_rows(int32_t rows);
 /* Profiling knobs: bit 0 = workers skip every tile body (the device driver's own cost in
- * isolation; results are garbage); bit 2 = the driver polls completions after every node
- * instead of rate-limiting the poll (A/B). Returns 0 or CF_E_CUDA. */
+ * isolation; results are garbage); A/B switches (results unchanged): bit 2 = poll
+ * completions after every node, bit 3 = wave helpers spin without sleeping, bit 4 = release
+ * the queue tail after every publication, bit 7 = tensor-core LSTM nodes prepared by the
+ * driver thread instead of the helper lanes; bits 8-15 = completion-poll interval in 1000
+ * cycles (0 = default). Returns 0 or CF_E_CUDA. */
 int32_t cf_debug_set_flags(int32_t flags);
 /* Compile a graph for the device program without a GPU and write its description and body
  * programs (one node per line, evaluation order) into buf; *needed = length + 1. */

@@ -801,6 +801,13 @@ struct Wave {
   const DNode* bn;
   FastEnv env;
   int env_frame;          // frame whose FastEnv is in env (-2: none); env.it is per wave
+  // job 1: preparation of a tensor-core LSTM node (Driver::heavy_prep_lane): dead check,
+  // output placements, operand-registry lookups, computed by the helper lanes in parallel
+  int job;
+  const DNode* hd;
+  int hdead, hfail;
+  int64_t houtp[8];
+  int64_t hmap[5], hslot[5];
   int slow[256];          // wave positions left for the general evaluator
 };
 
@@ -973,6 +980,61 @@ struct Driver {
       }
     }
     return n + 1;
+  }
+
+  // ---- heavy-node preparation on the helper lanes (job 1). Everything here is read-only
+  // for driver bookkeeping (tokens, placements, registry, TensorArray bases; hint slots in
+  // the node copy): the driver thread waits for the job and then builds the instances.
+  __device__ int prep_nplace(const DNode& d) const {
+    return d.n_out + (d.aux[0] == HK_LSTM_BWD_EW ? 2 : 1);
+  }
+  __device__ void heavy_prep_lane(Wave& w, int h) {
+    const DNode& d = *w.hd;
+    if (h < d.n_in) {
+      if (in_tok(d, h).dead) atomicOr(&w.hdead, 1);
+    } else if (h >= 32 && h < 32 + d.n_ctrl) {
+      if (toks_[iv_[d.ctrl_off + h - 32]].dead) atomicOr(&w.hdead, 1);
+    } else if (h >= 64 && h < 64 + prep_nplace(d)) {
+      int64_t v = 0;
+      if (!place_core(d, h - 64, &v)) atomicOr(&w.hfail, 1);
+      else w.houtp[h - 64] = v;
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(32 * kWaveWarps) : "memory");
+    if (w.hdead || w.hfail || h >= 5) return;
+    const int64_t B = d.imm[0], In = d.imm[1], H = d.imm[2], KT = In + H;
+    int16_t* hint = (int16_t*)const_cast<DNode&>(d).pad;
+    int64_t p = 0;
+    int rows = 0, cols = 0, kind = 0;
+    if (d.aux[0] == HK_LSTM_FWD) {
+      if (h == 0) { p = in_tok(d, 0).v; rows = (int)B; cols = (int)In; kind = 0; }
+      else if (h == 1) { p = in_tok(d, 1).v; rows = (int)B; cols = (int)H; kind = 0; }
+      else if (h == 2) { p = w.houtp[4]; rows = (int)(4 * H); cols = (int)KT; kind = 1; }
+      else return;
+    } else {
+      if (h == 0) { p = w.houtp[5]; rows = (int)B; cols = (int)(4 * H); kind = 0; }
+      else if (h == 1) { p = w.houtp[6]; rows = (int)KT; cols = (int)(4 * H); kind = 1; }
+      else if (h == 2) { p = w.houtp[5]; rows = (int)B; cols = (int)(4 * H); kind = 2; }
+      else if (h == 3) { p = in_tok(d, 0).v; rows = (int)B; cols = (int)In; kind = 2; }
+      else { p = in_tok(d, 1).v; rows = (int)B; cols = (int)H; kind = 2; }
+    }
+    if (!resolve_core(p, rows, cols, kind, &w.hmap[h], &w.hslot[h], hint + h)) atomicOr(&w.hfail, 2);
+  }
+  // dispatch job 1 for node d and wait; the results are in *wave_
+  __noinline__ __device__ void run_heavy_prep(const DNode& d) {
+    Wave& w = *wave_;
+    w.job = 1;
+    w.hd = &d;
+    w.hdead = 0;
+    w.hfail = 0;
+    w.done = 0;
+    __threadfence_block();
+    *(volatile int*)&w.seq = w.seq + 1;
+    flush_publish();
+    while (*(volatile int*)&w.done < kWaveWarps) {
+      maybe_drain();
+    }
+    __threadfence_block();
+    w.job = 0;
   }
 
   // ask the helper warps to copy [src, src+bytes) -> dst (16 B aligned), wait for them
@@ -1434,7 +1496,9 @@ struct Driver {
     return id;
   }
 
-  __noinline__ __device__ int eval_lstm_tc(const DNode& d, int nid, const int64_t* outp) {
+  // pm / ps: operand-registry lookups already made by the helper lanes (nullptr: here)
+  __noinline__ __device__ int eval_lstm_tc(const DNode& d, int nid, const int64_t* outp,
+                                           const int64_t* pm = nullptr, const int64_t* ps = nullptr) {
     // operand-registry hints live in the (driver-private) body-program copy of the node
     int16_t* hint = (int16_t*)const_cast<DNode&>(d).pad;
     Region rg(this, 32 + 9);
@@ -1448,9 +1512,13 @@ struct Driver {
       long long q0 = (kProfBuild && A.prof) ? clock64() : 0;
       int32_t pw = prep(d, nid, HK_PREP_WP, outp[4]);
       int64_t mx, sx, mh, sh, mw, sw;
-      if (!resolve(ip(0), (int)B, (int)In, 0, &mx, &sx, hint + 0) || !resolve(ip(1), (int)B, (int)H, 0, &mh, &sh, hint + 1) ||
-          !resolve(outp[4], (int)(4 * H), (int)KT, 1, &mw, &sw, hint + 2))
+      if (pm) {
+        mx = pm[0]; sx = ps[0]; mh = pm[1]; sh = ps[1]; mw = pm[2]; sw = ps[2];
+      } else if (!resolve(ip(0), (int)B, (int)In, 0, &mx, &sx, hint + 0) ||
+                 !resolve(ip(1), (int)B, (int)H, 0, &mh, &sh, hint + 1) ||
+                 !resolve(outp[4], (int)(4 * H), (int)KT, 1, &mw, &sw, hint + 2)) {
         return EV_ERROR;
+      }
       long long q1 = (kProfBuild && A.prof) ? clock64() : 0;
       if (kProfBuild && A.prof) { op_cyc[32 + 14] += q1 - q0; op_cnt[32 + 14]++; }
       // 256-row tiles (tc_tile2) trade tile count for operand bytes: only for large batches;
@@ -1504,12 +1572,16 @@ struct Driver {
       for (int j = 0; j < d.n_in; ++j) add_dep(e, in_tok(d, j).writer);
     }
     int64_t mz, sz, mwt, swt, mzn, szn, mxn, sxn, mhn, shn;
-    if (!resolve(dz_ptr, (int)B, (int)(4 * H), 0, &mz, &sz, hint + 0) ||
-        !resolve(outp[6], (int)KT, (int)(4 * H), 1, &mwt, &swt, hint + 1) ||
-        !resolve(dz_ptr, (int)B, (int)(4 * H), 2, &mzn, &szn, hint + 2) ||
-        !resolve(ip(0), (int)B, (int)In, 2, &mxn, &sxn, hint + 3) ||
-        !resolve(ip(1), (int)B, (int)H, 2, &mhn, &shn, hint + 4))
+    if (pm) {
+      mz = pm[0]; sz = ps[0]; mwt = pm[1]; swt = ps[1]; mzn = pm[2]; szn = ps[2];
+      mxn = pm[3]; sxn = ps[3]; mhn = pm[4]; shn = ps[4];
+    } else if (!resolve(dz_ptr, (int)B, (int)(4 * H), 0, &mz, &sz, hint + 0) ||
+               !resolve(outp[6], (int)KT, (int)(4 * H), 1, &mwt, &swt, hint + 1) ||
+               !resolve(dz_ptr, (int)B, (int)(4 * H), 2, &mzn, &szn, hint + 2) ||
+               !resolve(ip(0), (int)B, (int)In, 2, &mxn, &sxn, hint + 3) ||
+               !resolve(ip(1), (int)B, (int)H, 2, &mhn, &shn, hint + 4)) {
       return EV_ERROR;
+    }
     const bool m2 = B >= kM2MinRows;
     int32_t x = new_inst(HK_LSTM_DXH_TC, masked | (m2 ? 2 : 0),
                          (int)((m2 ? (B + 255) / 256 : (B + 127) / 128) * (KT / 256)));
@@ -1971,14 +2043,24 @@ struct Driver {
   // heavy node straight from the body loop (one call level: eval_heavy / eval_lstm_tc inline)
   __noinline__ __device__ int eval_heavy_node(const DNode& d, int nid) {
     bool dead = false;
-    for (int j = 0; j < d.n_in; ++j) dead |= in_tok(d, j).dead != 0;
-    for (int j = 0; j < d.n_ctrl; ++j) dead |= toks_[iv_[d.ctrl_off + j]].dead != 0;
+    const bool prepped = P.precision == D_BF16 && !P.n_swaps && !(dbg_ & 128) &&
+                         (d.aux[0] == HK_LSTM_FWD || d.aux[0] == HK_LSTM_BWD_EW) &&
+                         d.n_in <= 32 && d.n_ctrl <= 32 && prep_nplace(d) <= 8;
+    if (prepped) {   // dead check, placements and lookups on the helper lanes
+      run_heavy_prep(d);
+      dead = wave_->hdead != 0;
+    } else {
+      for (int j = 0; j < d.n_in; ++j) dead |= in_tok(d, j).dead != 0;
+      for (int j = 0; j < d.n_ctrl; ++j) dead |= toks_[iv_[d.ctrl_off + j]].dead != 0;
+    }
     if (dead) {
       set_dead_all(d);
       n_dead++;
     } else {
       maybe_drain();   // completions first: a producer's consumers are published with little delay
-      const int r = eval_heavy(d, nid);
+      const bool use = prepped && !wave_->hfail;
+      const int r = use ? eval_lstm_tc(d, nid, wave_->houtp, wave_->hmap, wave_->hslot)
+                        : eval_heavy(d, nid);
       flush_publish();
       if (r != EV_OK) return r;
     }
@@ -2877,6 +2959,7 @@ __global__ void __launch_bounds__(kThreads, 1) cf_driver_kernel(RunArgs A_param)
       wave.seq = 0;
       wave.done = 0;
       wave.env_frame = -2;
+      wave.job = 0;
     }
     __syncthreads();
     // the driver object itself lives in shared memory: its members are touched on every node
@@ -2933,7 +3016,8 @@ __global__ void __launch_bounds__(kThreads, 1) cf_driver_kernel(RunArgs A_param)
         if (ws != wseen) {
           wseen = ws;
           __threadfence_block();
-          wave_work(wave, wave_lane(threadIdx.x), 32 * kWaveWarps);
+          if (wave.job == 1) ((Driver*)drv_obj)->heavy_prep_lane(wave, wave_lane(threadIdx.x));
+          else wave_work(wave, wave_lane(threadIdx.x), 32 * kWaveWarps);
           __threadfence_block();
           __syncwarp();
           if ((threadIdx.x & 31) == 0) atomicAdd(&wave.done, 1);
