@@ -805,6 +805,7 @@ struct Wave {
   // output placements, operand-registry lookups, computed by the helper lanes in parallel
   int job;
   const DNode* hd;
+  int chain;              // routing wave followed by the preparation of node hd (same job)
   int hdead, hfail;
   int64_t houtp[8];
   int64_t hmap[5], hslot[5];
@@ -924,6 +925,7 @@ struct Driver {
   // Returns the number of body positions consumed (n + 1), or 1 to run the nodes serially.
   __noinline__ __device__ int run_wave(const DFrame& F, int pc, int n) {
     Region rg(this, 32 + 13);
+    chain_ok_ = false;
     // contexts whose liveness the wave's nodes read (bit mask from the compiler, marker imm0)
     for (unsigned long long m = (unsigned long long)bn_[pc].imm[0]; m; m &= m - 1)
       if (ctx_live(__ffsll((long long)m) - 1) < 0) return 1;
@@ -931,6 +933,22 @@ struct Driver {
     w.start = pc + 1;
     w.n = n;
     w.nslow = 0;
+    // chain the preparation of the next body node when it is a tensor-core LSTM node whose
+    // cond context is already known to be live (saves one helper round trip)
+    w.chain = 0;
+    chain_ok_ = false;
+    if (pc + n + 1 < F.n_body && !(dbg_ & (1 << 24))) {   // bit 24: no chaining (A/B)
+      // liveness must already be known for this iteration (its predicate may come from
+      // this very wave otherwise)
+      const DNode& nx = bn_[pc + n + 1];
+      if (nx.op == OP_HEAVY && prep_ok(nx) &&
+          (nx.ctx == 0 || (lstamp_[nx.ctx] == lgen_ && lval_[nx.ctx] == 1))) {
+        w.chain = 1;
+        w.hd = &nx;
+        w.hdead = 0;
+        w.hfail = 0;
+      }
+    }
     w.cnt = FastCount{0, 0, 0, 0, 0};
     w.bn = bn_;
     if (w.env_frame != cur_frame) {   // the environment changes with the frame only
@@ -955,6 +973,10 @@ struct Driver {
       op_cnt[32 + 21] += w.nslow;   // count = leftover nodes
     }
     __threadfence_block();
+    if (w.chain && w.nslow == 0) {   // wave_->hd prepared for this frame iteration
+      chain_ok_ = true;
+      chain_key_ = ((long long)(cur_frame + 1) << 32) | (unsigned)iter;
+    }
     n_push += w.cnt.push;
     n_pop += w.cnt.pop;
     if (w.cnt.maxd > max_depth) max_depth = w.cnt.maxd;
@@ -985,6 +1007,13 @@ struct Driver {
   // ---- heavy-node preparation on the helper lanes (job 1). Everything here is read-only
   // for driver bookkeeping (tokens, placements, registry, TensorArray bases; hint slots in
   // the node copy): the driver thread waits for the job and then builds the instances.
+  bool chain_ok_ = false;
+  long long chain_key_ = -1;
+  __device__ bool prep_ok(const DNode& d) const {
+    return P.precision == D_BF16 && !P.n_swaps && !(dbg_ & 128) &&
+           (d.aux[0] == HK_LSTM_FWD || d.aux[0] == HK_LSTM_BWD_EW) && d.n_in <= 32 &&
+           d.n_ctrl <= 32 && prep_nplace(d) <= 8;
+  }
   __device__ int prep_nplace(const DNode& d) const {
     return d.n_out + (d.aux[0] == HK_LSTM_BWD_EW ? 2 : 1);
   }
@@ -1023,6 +1052,7 @@ struct Driver {
   __noinline__ __device__ void run_heavy_prep(const DNode& d) {
     Wave& w = *wave_;
     w.job = 1;
+    w.chain = 0;
     w.hd = &d;
     w.hdead = 0;
     w.hfail = 0;
@@ -2043,11 +2073,12 @@ struct Driver {
   // heavy node straight from the body loop (one call level: eval_heavy / eval_lstm_tc inline)
   __noinline__ __device__ int eval_heavy_node(const DNode& d, int nid) {
     bool dead = false;
-    const bool prepped = P.precision == D_BF16 && !P.n_swaps && !(dbg_ & 128) &&
-                         (d.aux[0] == HK_LSTM_FWD || d.aux[0] == HK_LSTM_BWD_EW) &&
-                         d.n_in <= 32 && d.n_ctrl <= 32 && prep_nplace(d) <= 8;
+    const bool prepped = prep_ok(d);
     if (prepped) {   // dead check, placements and lookups on the helper lanes
-      run_heavy_prep(d);
+      const long long key = ((long long)(cur_frame + 1) << 32) | (unsigned)iter;
+      if (!(chain_ok_ && wave_->hd == &d && chain_key_ == key)) run_heavy_prep(d);   // else done
+                                                                                     // by the last wave
+      chain_ok_ = false;
       dead = wave_->hdead != 0;
     } else {
       for (int j = 0; j < d.n_in; ++j) dead |= in_tok(d, j).dead != 0;
@@ -2960,6 +2991,7 @@ __global__ void __launch_bounds__(kThreads, 1) cf_driver_kernel(RunArgs A_param)
       wave.done = 0;
       wave.env_frame = -2;
       wave.job = 0;
+      wave.chain = 0;
     }
     __syncthreads();
     // the driver object itself lives in shared memory: its members are touched on every node
@@ -3016,8 +3048,16 @@ __global__ void __launch_bounds__(kThreads, 1) cf_driver_kernel(RunArgs A_param)
         if (ws != wseen) {
           wseen = ws;
           __threadfence_block();
-          if (wave.job == 1) ((Driver*)drv_obj)->heavy_prep_lane(wave, wave_lane(threadIdx.x));
-          else wave_work(wave, wave_lane(threadIdx.x), 32 * kWaveWarps);
+          if (wave.job == 1) {
+            ((Driver*)drv_obj)->heavy_prep_lane(wave, wave_lane(threadIdx.x));
+          } else {
+            wave_work(wave, wave_lane(threadIdx.x), 32 * kWaveWarps);
+            if (wave.chain) {   // the next node's preparation reads this wave's tokens
+              __threadfence_block();
+              asm volatile("bar.sync 1, %0;" ::"r"(32 * kWaveWarps) : "memory");
+              if (wave.nslow == 0) ((Driver*)drv_obj)->heavy_prep_lane(wave, wave_lane(threadIdx.x));
+            }
+          }
           __threadfence_block();
           __syncwarp();
           if ((threadIdx.x & 31) == 0) atomicAdd(&wave.done, 1);
