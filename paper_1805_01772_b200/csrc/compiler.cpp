@@ -968,6 +968,7 @@ struct Compiler {
       case OP_CONST: case OP_PASS: case OP_FLOW: case OP_SCALAR: case OP_ACC: case OP_TA_GRAD:
       case OP_TA_READ: case OP_TA_WRITE:
         return true;
+      case OP_STACK_PUSH: case OP_STACK_POP: return P.swaps.empty();   // control inputs too
       default: break;
     }
     if (d.n_ctrl != 0) return false;

@@ -741,10 +741,11 @@ __device__ __forceinline__ int fast_node(const DNode* d, const FastEnv& e, FastC
     tk[d->ctrl_vid] = ctrl;
     return 1;
   }
-  if ((op == OP_STACK_PUSH || op == OP_STACK_POP) && !d->n_ctrl) {
+  if (op == OP_STACK_PUSH || op == OP_STACK_POP) {
     const int4 h = tk[iv[d->in_off]];
     const int4 v = op == OP_STACK_PUSH ? tk[iv[d->in_off + 1]] : h;
-    const int dead = (h.w | v.w) & 0xff;
+    int dead = (h.w | v.w) & 0xff;
+    for (int j = 0; j < d->n_ctrl; ++j) dead |= tk[iv[d->ctrl_off + j]].w & 0xff;
     if (dead) {   // dead push: nothing stored; dead pop: dead output
       if (op == OP_STACK_POP) {
         int4 t = make_int4(0, 0, -1, 1);
@@ -806,16 +807,18 @@ struct Wave {
   int job;
   const DNode* hd;
   int chain;              // routing wave followed by the preparation of node hd (same job)
+  int nlev, lev_stop;     // fused levels; levels completed (set by the helpers)
+  int lev_start[16], lev_n[16];
   int hdead, hfail;
   int64_t houtp[8];
   int64_t hmap[5], hslot[5];
   int slow[256];          // wave positions left for the general evaluator
 };
 
-__device__ void wave_work(Wave& w, int h, int nh) {
+__device__ void wave_work(Wave& w, int start, int n, int h, int nh) {
   FastCount c{0, 0, 0, 0, 0};
-  for (int j = h; j < w.n; j += nh) {
-    const DNode* d = w.bn + w.start + j;
+  for (int j = h; j < n; j += nh) {
+    const DNode* d = w.bn + start + j;
     if (d->ctx && !w.env.lval[d->ctx]) continue;   // node of a dead cond branch
     const int r = fast_node(d, w.env, c);
     if (r == 0) w.slow[atomicAdd(&w.nslow, 1)] = j;
@@ -923,6 +926,11 @@ struct Driver {
   // OP_WAVE at body position pc: liveness of the contexts its nodes need, then the helper
   // warps evaluate the n nodes in parallel; leftovers go through the general evaluator.
   // Returns the number of body positions consumed (n + 1), or 1 to run the nodes serially.
+  // OP_WAVE at body position pc, fused with the directly following waves (up to kMaxLev
+  // levels, one helper job; the helpers separate the levels with a named barrier). A level
+  // joins only if the cond contexts it reads are already known for this iteration. Returns
+  // the number of body positions consumed, or 1 to run the first wave's nodes serially.
+  static constexpr int kMaxLev = 16;
   __noinline__ __device__ int run_wave(const DFrame& F, int pc, int n) {
     Region rg(this, 32 + 13);
     chain_ok_ = false;
@@ -930,17 +938,29 @@ struct Driver {
     for (unsigned long long m = (unsigned long long)bn_[pc].imm[0]; m; m &= m - 1)
       if (ctx_live(__ffsll((long long)m) - 1) < 0) return 1;
     Wave& w = *wave_;
-    w.start = pc + 1;
-    w.n = n;
+    int nlev = 0, q = pc;
+    while (true) {
+      w.lev_start[nlev] = q + 1;
+      w.lev_n[nlev] = bn_[q].aux[0];
+      ++nlev;
+      q += bn_[q].aux[0] + 1;
+      if (nlev == kMaxLev || q >= F.n_body || bn_[q].op != OP_WAVE || (dbg_ & (1 << 25))) break;
+      bool known = true;   // bit 25: no fusion (A/B)
+      for (unsigned long long m = (unsigned long long)bn_[q].imm[0]; m && known; m &= m - 1) {
+        const int c = __ffsll((long long)m) - 1;
+        for (int x = c; x; x = ctxs_[x].parent)
+          if (lstamp_[x] != lgen_) known = false;
+      }
+      if (!known) break;
+    }
+    w.nlev = nlev;
+    w.lev_stop = nlev;
     w.nslow = 0;
-    // chain the preparation of the next body node when it is a tensor-core LSTM node whose
-    // cond context is already known to be live (saves one helper round trip)
+    // chain the preparation of the node after the last level when it is a tensor-core LSTM
+    // node whose cond context is already known to be live (saves one helper round trip)
     w.chain = 0;
-    chain_ok_ = false;
-    if (pc + n + 1 < F.n_body && !(dbg_ & (1 << 24))) {   // bit 24: no chaining (A/B)
-      // liveness must already be known for this iteration (its predicate may come from
-      // this very wave otherwise)
-      const DNode& nx = bn_[pc + n + 1];
+    if (q < F.n_body && !(dbg_ & (1 << 24))) {   // bit 24: no chaining (A/B)
+      const DNode& nx = bn_[q];
       if (nx.op == OP_HEAVY && prep_ok(nx) &&
           (nx.ctx == 0 || (lstamp_[nx.ctx] == lgen_ && lval_[nx.ctx] == 1))) {
         w.chain = 1;
@@ -973,7 +993,10 @@ struct Driver {
       op_cnt[32 + 21] += w.nslow;   // count = leftover nodes
     }
     __threadfence_block();
-    if (w.chain && w.nslow == 0) {   // wave_->hd prepared for this frame iteration
+    const int stop = w.lev_stop;   // levels completed (a level with leftovers ends the job)
+    const int last = stop < nlev ? stop : nlev - 1;
+    const int end = w.lev_start[last] + w.lev_n[last];   // body position after that level
+    if (w.chain && w.nslow == 0 && stop == nlev) {   // wave_->hd prepared for this iteration
       chain_ok_ = true;
       chain_key_ = ((long long)(cur_frame + 1) << 32) | (unsigned)iter;
     }
@@ -982,9 +1005,9 @@ struct Driver {
     if (w.cnt.maxd > max_depth) max_depth = w.cnt.maxd;
     if (w.cnt.err) {
       fail(w.cnt.err, w.cnt.err_info);
-      return n + 1;
+      return end - pc;
     }
-    // leftovers (e.g. a Switch whose predicate is a device value): in wave order
+    // leftovers of the last level run (e.g. a Switch whose predicate is a device value)
     for (int a = 0; a < w.nslow; ++a)
       for (int b = a + 1; b < w.nslow; ++b)
         if (w.slow[b] < w.slow[a]) {
@@ -993,15 +1016,15 @@ struct Driver {
           w.slow[b] = t;
         }
     for (int a = 0; a < w.nslow; ++a) {
-      const int q = pc + 1 + w.slow[a];
+      const int q2 = w.lev_start[last] + w.slow[a];
       while (true) {
-        const int r = eval(bn_[q], P.order[F.body_off + q]);
+        const int r = eval(bn_[q2], P.order[F.body_off + q2]);
         if (r == EV_OK) break;
-        if (r == EV_ERROR || st->error) return n + 1;
+        if (r == EV_ERROR || st->error) return end - pc;
         drain();   // the predicate's producer has to finish first
       }
     }
-    return n + 1;
+    return end - pc;
   }
 
   // ---- heavy-node preparation on the helper lanes (job 1). Everything here is read-only
@@ -3051,12 +3074,18 @@ __global__ void __launch_bounds__(kThreads, 1) cf_driver_kernel(RunArgs A_param)
           if (wave.job == 1) {
             ((Driver*)drv_obj)->heavy_prep_lane(wave, wave_lane(threadIdx.x));
           } else {
-            wave_work(wave, wave_lane(threadIdx.x), 32 * kWaveWarps);
-            if (wave.chain) {   // the next node's preparation reads this wave's tokens
+            // fused levels: each reads the previous one's tokens (named barrier between)
+            const int hl = wave_lane(threadIdx.x);
+            int k = 0;
+            for (; k < wave.nlev; ++k) {
+              wave_work(wave, wave.lev_start[k], wave.lev_n[k], hl, 32 * kWaveWarps);
               __threadfence_block();
               asm volatile("bar.sync 1, %0;" ::"r"(32 * kWaveWarps) : "memory");
-              if (wave.nslow == 0) ((Driver*)drv_obj)->heavy_prep_lane(wave, wave_lane(threadIdx.x));
+              if (wave.nslow || wave.cnt.err) break;   // the driver evaluates the leftovers
             }
+            if (hl == 0) wave.lev_stop = k < wave.nlev ? k : wave.nlev;
+            if (k == wave.nlev && wave.chain)   // the next node's preparation
+              ((Driver*)drv_obj)->heavy_prep_lane(wave, hl);
           }
           __threadfence_block();
           __syncwarp();
