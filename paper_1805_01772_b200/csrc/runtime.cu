@@ -1398,14 +1398,21 @@ struct Driver {
     // relaxed poll (an acquire load would invalidate L1 at every poll); the release store
     // that publishes successors orders this observation before them (fence.acq_rel).
     // (A helper warp mirroring this queue into shared memory measured 5% slower.)
-    for (int k = 0; k < 256; ++k) {
-      int* p = &A.cq[cq_head_ & (A.cq_cap - 1)];
-      int v = ld_volatile_i32(p);
-      if (v == 0) break;
-      *(volatile int*)p = 0;
-      cq_head_++;
-      complete(v - 1);
-      any = true;
+    // four slots per round trip (the loads are independent): a drain that finds one
+    // completion costs one L2 latency, not two
+    for (int round = 0; round < 64; ++round) {
+      const unsigned long long m = (unsigned long long)(A.cq_cap - 1);
+      int v[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) v[q] = ld_volatile_i32(&A.cq[(cq_head_ + q) & m]);
+      int k = 0;
+      for (; k < 4 && v[k] != 0; ++k) {
+        *(volatile int*)&A.cq[(cq_head_ + k) & m] = 0;
+        complete(v[k] - 1);
+      }
+      cq_head_ += k;
+      if (k) any = true;
+      if (k < 4) break;
     }
     flush_publish();
     return any;
@@ -2111,7 +2118,8 @@ struct Driver {
       set_dead_all(d);
       n_dead++;
     } else {
-      maybe_drain();   // completions first: a producer's consumers are published with little delay
+      if (dbg_ & (1 << 26)) maybe_drain();   // bit 26: poll before each heavy node (A/B; the
+                                              // wave waits poll often enough, measured ~1%)
       const bool use = prepped && !wave_->hfail;
       const int r = use ? eval_lstm_tc(d, nid, wave_->houtp, wave_->hmap, wave_->hslot)
                         : eval_heavy(d, nid);
