@@ -36,7 +36,9 @@ int32_t cf_debug_set_m2_rows(int32_t rows);
  * the queue tail after every publication, bit 7 = tensor-core LSTM nodes prepared by the
  * driver thread instead of the helper lanes; bits 8-15 = completion-poll interval in 1000
  * cycles (0 = default); bit 24 = no chaining of a node's preparation onto the preceding
- * wave; bit 25 = no fusion of consecutive waves into one helper job. Returns 0 or CF_E_CUDA. */
+ * wave; bit 25 = no fusion of consecutive waves into one helper job;
+ * bit 26 = poll completions before each heavy node; bit 27 = no overlap of the next wave job
+ * with an LSTM node's instance construction. Returns 0 or CF_E_CUDA. */
 int32_t cf_debug_set_flags(int32_t flags);
 /* Compile a graph for the device program without a GPU and write its description and body
  * programs (one node per line, evaluation order) into buf; *needed = length + 1. */

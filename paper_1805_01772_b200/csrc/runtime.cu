@@ -931,12 +931,52 @@ struct Driver {
   // joins only if the cond contexts it reads are already known for this iteration. Returns
   // the number of body positions consumed, or 1 to run the first wave's nodes serially.
   static constexpr int kMaxLev = 16;
+  // a wave job started early (by the forward LSTM node before it, overlapping the driver's
+  // instance construction) and not yet finished: body position and frame iteration
+  int pend_wave_pc_ = -1;
+  long long pend_wave_key_ = -1;
+  int cur_pc_ = 0;
+  const DFrame* cur_F_ = nullptr;
+  __forceinline__ __device__ long long iter_key() const {
+    return ((long long)(cur_frame + 1) << 32) | (unsigned)iter;
+  }
   __noinline__ __device__ int run_wave(const DFrame& F, int pc, int n) {
+    if (pend_wave_pc_ >= 0) {
+      const bool mine = pend_wave_pc_ == pc && pend_wave_key_ == iter_key();
+      pend_wave_pc_ = -1;
+      if (mine) return wave_finish(F, pc);
+      wave_wait();   // (not expected) never leave a job in flight
+    }
+    if (!wave_start(F, pc)) return 1;
+    return wave_finish(F, pc);
+  }
+  // forward LSTM node: its output tokens are set, so the wave job after it (skipping dead
+  // twins in the other cond branch) can start while the driver builds the instance
+  __device__ void start_next_wave() {
+    if ((dbg_ & (1 << 27)) || !cur_F_ || pend_wave_pc_ >= 0) return;   // bit 27: off (A/B)
+    const DFrame& F = *cur_F_;
+    int q = cur_pc_ + 1;
+    while (q < F.n_body && bn_[q].op == OP_HEAVY && bn_[q].ctx && lstamp_[bn_[q].ctx] == lgen_ &&
+           lval_[bn_[q].ctx] == 0)
+      ++q;
+    if (q < F.n_body && bn_[q].op == OP_WAVE && wave_start(F, q)) {
+      pend_wave_pc_ = q;
+      pend_wave_key_ = iter_key();
+    }
+  }
+  __device__ void wave_wait() {
+    while (*(volatile int*)&wave_->done < kWaveWarps) {
+    }
+    __threadfence_block();
+  }
+  // dispatch the wave job at body position pc (fused with the following waves); false: the
+  // first wave's cond contexts are not known yet (run its nodes serially)
+  __noinline__ __device__ bool wave_start(const DFrame& F, int pc) {
     Region rg(this, 32 + 13);
     chain_ok_ = false;
     // contexts whose liveness the wave's nodes read (bit mask from the compiler, marker imm0)
     for (unsigned long long m = (unsigned long long)bn_[pc].imm[0]; m; m &= m - 1)
-      if (ctx_live(__ffsll((long long)m) - 1) < 0) return 1;
+      if (ctx_live(__ffsll((long long)m) - 1) < 0) return false;
     Wave& w = *wave_;
     int nlev = 0, q = pc;
     while (true) {
@@ -980,6 +1020,12 @@ struct Driver {
     __threadfence_block();
     *(volatile int*)&w.seq = w.seq + 1;
     flush_publish();
+    return true;
+  }
+  // wait for the wave job of position pc, evaluate its leftovers; positions consumed
+  __noinline__ __device__ int wave_finish(const DFrame& F, int pc) {
+    Wave& w = *wave_;
+    const int nlev = w.nlev;
     long long wq0 = (kProfBuild && A.prof) ? clock64() : 0, wdr = 0;
     while (*(volatile int*)&w.done < kWaveWarps) {
       long long d0 = (kProfBuild && A.prof) ? clock64() : 0;
@@ -1074,6 +1120,11 @@ struct Driver {
   // dispatch job 1 for node d and wait; the results are in *wave_
   __noinline__ __device__ void run_heavy_prep(const DNode& d) {
     Wave& w = *wave_;
+    if (pend_wave_pc_ >= 0) {   // a started wave job must be finished by run_wave first
+      fail(CF_E_UNSUPPORTED, -500);
+      wave_wait();
+      return;
+    }
     w.job = 1;
     w.chain = 0;
     w.hd = &d;
@@ -1570,13 +1621,17 @@ struct Driver {
     auto ip = [&](int j) { return in_tok(d, j).v; };
     if (kind == HK_LSTM_FWD) {
       long long q0 = (kProfBuild && A.prof) ? clock64() : 0;
-      int32_t pw = prep(d, nid, HK_PREP_WP, outp[4]);
+      // outp / pm / ps may live in the Wave (helper results): copy them before the next wave
+      // job is started below
+      int64_t op_[5];
+      for (int k = 0; k < 5; ++k) op_[k] = outp[k];
+      int32_t pw = prep(d, nid, HK_PREP_WP, op_[4]);
       int64_t mx, sx, mh, sh, mw, sw;
       if (pm) {
         mx = pm[0]; sx = ps[0]; mh = pm[1]; sh = ps[1]; mw = pm[2]; sw = ps[2];
       } else if (!resolve(ip(0), (int)B, (int)In, 0, &mx, &sx, hint + 0) ||
                  !resolve(ip(1), (int)B, (int)H, 0, &mh, &sh, hint + 1) ||
-                 !resolve(outp[4], (int)(4 * H), (int)KT, 1, &mw, &sw, hint + 2)) {
+                 !resolve(op_[4], (int)(4 * H), (int)KT, 1, &mw, &sw, hint + 2)) {
         return EV_ERROR;
       }
       long long q1 = (kProfBuild && A.prof) ? clock64() : 0;
@@ -1589,12 +1644,19 @@ struct Driver {
       long long q2 = (kProfBuild && A.prof) ? clock64() : 0;
       if (kProfBuild && A.prof) { op_cyc[32 + 15] += q2 - q1; op_cnt[32 + 15]++; }
       if (id < 0) return EV_ERROR;
+      // tokens first: the next wave job then overlaps this instance's construction
+      set_out(d, 0, ptr_tok(op_[0], id, D_BF16));
+      set_out(d, 1, ptr_tok(op_[1], id, D_F32));
+      set_out(d, 2, ptr_tok(op_[2], id, D_BF16));
+      set_out(d, 3, ptr_tok(op_[3], id, D_BF16));
+      toks_[d.ctrl_vid] = Tok{0, -1, 0, TK_FLOW, 0, 0};
+      start_next_wave();
       Inst& I = A.insts[id];
       I.m = B; I.k = In; I.n = H;
       I.p[0] = mx; I.p[1] = mh; I.p[2] = ip(2); I.p[3] = mw; I.p[4] = ip(4);
       I.p[5] = masked ? ip(6) : 0;
       I.p[6] = ip(1);
-      for (int p = 0; p < 4; ++p) I.p[8 + p] = outp[p];
+      for (int p = 0; p < 4; ++p) I.p[8 + p] = op_[p];
       I.s[0] = t; I.s[1] = d.aux[2]; I.s[2] = sx; I.s[3] = sh;
       long long q3 = (kProfBuild && A.prof) ? clock64() : 0;
       if (kProfBuild && A.prof) { op_cyc[32 + 16] += q3 - q2; op_cnt[32 + 16]++; }
@@ -1602,10 +1664,6 @@ struct Driver {
       add_dep(id, pw);
       long long q4 = (kProfBuild && A.prof) ? clock64() : 0;
       if (kProfBuild && A.prof) { op_cyc[32 + 17] += q4 - q3; op_cnt[32 + 17]++; }
-      set_out(d, 0, ptr_tok(outp[0], id, D_BF16));
-      set_out(d, 1, ptr_tok(outp[1], id, D_F32));
-      set_out(d, 2, ptr_tok(outp[2], id, D_BF16));
-      set_out(d, 3, ptr_tok(outp[3], id, D_BF16));
       submit(id);
       if (kProfBuild && A.prof) { op_cyc[32 + 18] += clock64() - q4; op_cnt[32 + 18]++; }
       return EV_OK;
@@ -2647,6 +2705,8 @@ struct Driver {
       const bool routing = op == OP_SWITCH || op == OP_MERGE || op == OP_MERGE_LOOP || op == OP_NEXTITER ||
                            op == OP_PASS || (op == OP_CONST && d->aux[0] == 1);
       // one call level: heavy nodes and the general ops skip the routing front end
+      cur_pc_ = pc;
+      cur_F_ = &F;
       int r = op == OP_HEAVY ? eval_heavy_node(*d, nid) : routing ? eval(*d, nid) : eval_cold(*d, nid);
       if (prof) {
         op_cyc[op & 31] += clock64() - c0;
