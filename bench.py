@@ -270,23 +270,41 @@ def main():
     d2h = y_host.numel() * y_host.element_size()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e2e_steps = max(2, min(args.steps, 5))
-    c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    copy_ms = 0.0
+    # the step's inputs are copied on a copy stream into one of two device input sets while
+    # the previous step computes (double buffering, as a data loader would); every copy is
+    # inside the timed region and each cf_run waits for its own inputs
+    sets = [dev, dict(dev)]
+    for k in host:
+        sets[1][k] = torch.empty_like(dev[k])
+    copy_stream = torch.cuda.Stream()
+    copied = [torch.cuda.Event(), torch.cuda.Event()]
+    cev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(e2e_steps)]
+
+    def issue_copy(i):
+        with torch.cuda.stream(copy_stream):
+            cev[i][0].record(copy_stream)
+            for k, v in host.items():
+                sets[i % 2][k].copy_(v, non_blocking=True)
+            cev[i][1].record(copy_stream)
+            copied[i % 2].record(copy_stream)
+
     torch.cuda.synchronize()
     if pg:
         pg.barrier()   # every rank has its pinned inputs ready before the clock starts
         torch.cuda.synchronize()
     e0.record(stream)
-    for _ in range(e2e_steps):
-        c0.record(stream)
-        for k, v in host.items():
-            dev[k].copy_(v, non_blocking=True)
-        c1.record(stream)
-        sess.run(dev, outs)
-        copy_ms += c0.elapsed_time(c1)
+    copy_stream.wait_event(e0)
+    issue_copy(0)
+    for i in range(e2e_steps):
+        stream.wait_event(copied[i % 2])
+        if i + 1 < e2e_steps:
+            issue_copy(i + 1)   # the set it overwrites was used by step i - 1 (finished)
+        sess.run(sets[i % 2], outs)
         y_host.copy_(outs[0], non_blocking=True)
     e1.record(stream)
     torch.cuda.synchronize()
+    copy_ms = sum(a.elapsed_time(b) for a, b in cev)
     e2e_ms = e0.elapsed_time(e1) / e2e_steps
     copy_ms /= e2e_steps
     if os.environ.get("BENCH_DEBUG"):

@@ -20,16 +20,28 @@ def _stale(lib: str) -> bool:
     if not os.path.exists(lib):
         return True
     t = os.path.getmtime(lib)
-    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + \
+    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cu", ".cpp", ".h", ".cuh"))] + \
         [os.path.join(HERE, "..", "include", f) for f in ("cf.h", "cf_debug.h")] + [__file__]
     return any(os.path.getmtime(p) > t for p in deps if os.path.exists(p))
 
 
 def build(force: bool = False, verbose: bool = False, profile: bool = False) -> str:
     lib = LIB_PROF if profile else LIB
-    tag = "_prof" if profile else ""
     if not force and not _stale(lib):
         return lib
+    # one builder at a time (e.g. every rank of a torchrun job): the others wait, then find
+    # the library fresh
+    import fcntl
+    os.makedirs(os.path.join(CSRC, "build"), exist_ok=True)
+    with open(os.path.join(CSRC, "build", ".lock"), "w") as lk:
+        fcntl.flock(lk, fcntl.LOCK_EX)
+        if not force and not _stale(lib):
+            return lib
+        return _build_locked(lib, force, verbose, profile)
+
+
+def _build_locked(lib: str, force: bool, verbose: bool, profile: bool) -> str:
+    tag = "_prof" if profile else ""
     objs = []
     # headers (and this script) invalidate every object; a source only its own
     hdrs = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))] + \
