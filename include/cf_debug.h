@@ -38,7 +38,8 @@ int32_t cf_debug_set_m2_rows(int32_t rows);
  * cycles (0 = default); bit 24 = no chaining of a node's preparation onto the preceding
  * wave; bit 25 = no fusion of consecutive waves into one helper job;
  * bit 26 = poll completions before each heavy node; bit 27 = no overlap of the next wave job
- * with an LSTM node's instance construction. Returns 0 or CF_E_CUDA. */
+ * with a forward LSTM node's instance construction, bit 29 = the same for a backward node
+ * (steps that do not close a dW chunk). Returns 0 or CF_E_CUDA. */
 int32_t cf_debug_set_flags(int32_t flags);
 /* Compile a graph for the device program without a GPU and write its description and body
  * programs (one node per line, evaluation order) into buf; *needed = length + 1. */

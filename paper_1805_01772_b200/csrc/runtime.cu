@@ -1668,13 +1668,45 @@ struct Driver {
       if (kProfBuild && A.prof) { op_cyc[32 + 18] += clock64() - q4; op_cnt[32 + 18]++; }
       return EV_OK;
     }
-    // ---- backward: EW (dz, dc, db partials) -> DXH (dx, dh) and DW (dW, db)
+    // ---- backward: EW (dz, dc, db partials) -> DXH (dx, dh) and DW (dW, db). On steps that
+    // do not close a dW chunk (7 of 8 when the gradients accumulate in place) the ids and
+    // tokens come first and the next wave job overlaps the records and dependency edges.
+    int64_t op_[7];
+    for (int k = 0; k < 7; ++k) op_[k] = outp[k];   // may live in the Wave (helper results)
+    outp = op_;
+    const int acc_w = d.aux[3], acc_b = d.aux[4];
+    const int cnt0 = dw_count_[nid];
+    const bool early = !(dbg_ & (1 << 29)) && acc_w >= 0 && acc_b >= 0 && cnt0 + 1 < 8;   // bit 29: off
     const int o = masked ? 7 : 5;
     const int64_t dz_ptr = outp[5];
     const int64_t dz_bytes = ((B * 4 * H * 2 + 1023) / 1024) * 1024;
     int32_t pw = prep(d, nid, HK_PREP_WT, outp[6]);
+    int64_t mz, sz, mwt, swt, mzn, szn, mxn, sxn, mhn, shn;
+    if (pm) {
+      mz = pm[0]; sz = ps[0]; mwt = pm[1]; swt = ps[1]; mzn = pm[2]; szn = ps[2];
+      mxn = pm[3]; sxn = ps[3]; mhn = pm[4]; shn = ps[4];
+    } else if (!resolve(dz_ptr, (int)B, (int)(4 * H), 0, &mz, &sz, hint + 0) ||
+               !resolve(outp[6], (int)KT, (int)(4 * H), 1, &mwt, &swt, hint + 1) ||
+               !resolve(dz_ptr, (int)B, (int)(4 * H), 2, &mzn, &szn, hint + 2) ||
+               !resolve(ip(0), (int)B, (int)In, 2, &mxn, &sxn, hint + 3) ||
+               !resolve(ip(1), (int)B, (int)H, 2, &mhn, &shn, hint + 4)) {
+      return EV_ERROR;
+    }
     int32_t e = new_inst(HK_LSTM_BWD_EW_BF, masked, (int)(((B + 127) / 128) * (H / 64)));
     if (e < 0) return EV_ERROR;
+    const bool m2 = B >= kM2MinRows;
+    int32_t x = new_inst(HK_LSTM_DXH_TC, masked | (m2 ? 2 : 0),
+                         (int)((m2 ? (B + 255) / 256 : (B + 127) / 128) * (KT / 256)));
+    if (x < 0) return EV_ERROR;
+    if (early) {
+      set_out(d, 0, ptr_tok(outp[0], x, D_F32));
+      set_out(d, 1, ptr_tok(outp[1], x, D_F32));
+      set_out(d, 2, ptr_tok(outp[2], e, D_F32));
+      set_out(d, 3, ptr_tok(outp[3], acc_writer_[acc_w], D_F32));
+      set_out(d, 4, ptr_tok(outp[4], acc_writer_[acc_b], D_F32));
+      toks_[d.ctrl_vid] = Tok{0, -1, 0, TK_FLOW, 0, 0};
+      start_next_wave();
+    }
     {
       Inst& I = A.insts[e];
       I.m = B; I.k = In; I.n = H;
@@ -1689,21 +1721,6 @@ struct Driver {
       I.s[0] = t; I.s[4] = in_tok(d, o + 2).dt; I.s[5] = dz_bytes;
       for (int j = 0; j < d.n_in; ++j) add_dep(e, in_tok(d, j).writer);
     }
-    int64_t mz, sz, mwt, swt, mzn, szn, mxn, sxn, mhn, shn;
-    if (pm) {
-      mz = pm[0]; sz = ps[0]; mwt = pm[1]; swt = ps[1]; mzn = pm[2]; szn = ps[2];
-      mxn = pm[3]; sxn = ps[3]; mhn = pm[4]; shn = ps[4];
-    } else if (!resolve(dz_ptr, (int)B, (int)(4 * H), 0, &mz, &sz, hint + 0) ||
-               !resolve(outp[6], (int)KT, (int)(4 * H), 1, &mwt, &swt, hint + 1) ||
-               !resolve(dz_ptr, (int)B, (int)(4 * H), 2, &mzn, &szn, hint + 2) ||
-               !resolve(ip(0), (int)B, (int)In, 2, &mxn, &sxn, hint + 3) ||
-               !resolve(ip(1), (int)B, (int)H, 2, &mhn, &shn, hint + 4)) {
-      return EV_ERROR;
-    }
-    const bool m2 = B >= kM2MinRows;
-    int32_t x = new_inst(HK_LSTM_DXH_TC, masked | (m2 ? 2 : 0),
-                         (int)((m2 ? (B + 255) / 256 : (B + 127) / 128) * (KT / 256)));
-    if (x < 0) return EV_ERROR;
     {
       Inst& I = A.insts[x];
       I.m = B; I.k = In; I.n = H;
@@ -1714,7 +1731,6 @@ struct Driver {
       add_dep(x, pw);
       add_dep(x, in_tok(d, o).writer);
     }
-    const int acc_w = d.aux[3], acc_b = d.aux[4];
     // dW / db: steps are queued and multiplied in chunks of up to 8 (K = 8 B) when both
     // gradients accumulate in place; otherwise one step per instance
     {
@@ -1730,11 +1746,13 @@ struct Driver {
         if (flush_dw(d, nid, mzn, outp[3], outp[4]) < 0) return EV_ERROR;
       }
     }
-    set_out(d, 0, ptr_tok(outp[0], x, D_F32));
-    set_out(d, 1, ptr_tok(outp[1], x, D_F32));
-    set_out(d, 2, ptr_tok(outp[2], e, D_F32));
-    set_out(d, 3, ptr_tok(outp[3], acc_w >= 0 ? acc_writer_[acc_w] : last_dw, D_F32));
-    set_out(d, 4, ptr_tok(outp[4], acc_b >= 0 ? acc_writer_[acc_b] : last_dw, D_F32));
+    if (!early) {
+      set_out(d, 0, ptr_tok(outp[0], x, D_F32));
+      set_out(d, 1, ptr_tok(outp[1], x, D_F32));
+      set_out(d, 2, ptr_tok(outp[2], e, D_F32));
+      set_out(d, 3, ptr_tok(outp[3], acc_w >= 0 ? acc_writer_[acc_w] : last_dw, D_F32));
+      set_out(d, 4, ptr_tok(outp[4], acc_b >= 0 ? acc_writer_[acc_b] : last_dw, D_F32));
+    }
     submit(e);
     submit(x);
     return EV_OK;

@@ -18,9 +18,10 @@ from synth import rnn_inputs  # noqa: E402
 
 # A/B switches (results must not change): poll after every node, helpers spin, release after
 # every publication, driver-side LSTM preparation, short poll interval, no prep chaining,
-# no wave fusion, poll before heavy nodes, no overlap of the next wave with a forward node
-FLAGS = [4, 8, 16, 128, 1 << 8, 1 << 24, 1 << 25, 1 << 26, 1 << 27,
-         128 | (1 << 24) | (1 << 25) | (1 << 27)]
+# no wave fusion, poll before heavy nodes, no overlap of the next wave with a forward node /
+# a backward node
+FLAGS = [4, 8, 16, 128, 1 << 8, 1 << 24, 1 << 25, 1 << 26, 1 << 27, 1 << 29,
+         128 | (1 << 24) | (1 << 25) | (1 << 27) | (1 << 29)]
 
 
 def _run(s, p, dev):
