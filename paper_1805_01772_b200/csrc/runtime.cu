@@ -1263,7 +1263,10 @@ struct Driver {
     r_last[sl] = -1;
     r_sn[sl] = 0;
     r_nt[sl] = ntiles;
-    r_kfi[sl] = (kind & 255) | (((cur_frame + 1) & 255) << 8) | ((cur_frame >= 0 ? iter : 0) << 16);
+    // iteration in the top 16 bits; 0xFFFF = read the full iteration from the record (loops
+    // longer than 65534 iterations)
+    r_kfi[sl] = (int)((unsigned)(kind & 255) | ((unsigned)((cur_frame + 1) & 255) << 8) |
+                      ((unsigned)min(cur_frame >= 0 ? iter : 0, 0xFFFF) << 16));
     Inst& I = A.insts[id];
     I.kind = kind;
     I.sub = sub;
@@ -1372,9 +1375,13 @@ struct Driver {
   __noinline__ __device__ void complete(int32_t id) {
     const int sl = id & kRingMask;
     outstanding--;
-    const int kfi = r_kfi[sl];
-    const int fr = ((kfi >> 8) & 255) - 1;
-    if (fr >= 0) iter_out_[frame_ib(fr) + (kfi >> 16)]--;
+    const unsigned kfi = (unsigned)r_kfi[sl];
+    const int fr = (int)((kfi >> 8) & 255) - 1;
+    if (fr >= 0) {
+      int it = (int)(kfi >> 16);
+      if (it == 0xFFFF) it = A.insts[id].iter;
+      iter_out_[frame_ib(fr) + it]--;
+    }
     int32_t e = r_succ[sl];
     const int ns = r_sn[sl];
     r_id[sl] = -1;   // done
