@@ -17,3 +17,24 @@ def test_trivial_loop_closed_form(n, width, K):
     r = co.run(n, width=width, K=K, reps=1, warmup=0)
     assert r["trip_count"] == n
     assert r["closed_form_ok"], r
+
+
+def test_ring_exchange_two_gpus():
+    """Each iteration Sends the loop value to the next rank and Recvs the previous rank's
+    (PAPER.md:780-829); closed form a == n on every rank, K 1 and 8."""
+    import json
+    import subprocess
+
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29517",
+           os.path.join(root, "tools", "control_overhead_mgpu.py"),
+           "--iters", "1", "300", "--K", "1", "8", "--reps", "1"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=240, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    rows = [json.loads(l) for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(rows) == 4
+    assert all(r["closed_form_ok"] and r["n_gpus"] == 2 for r in rows), rows
