@@ -1065,7 +1065,15 @@ struct Compiler {
     // CF_MIN_WAVE overrides it (A/B)
     int min_wave = 1;   // measured on cfg3: 1 -> 80.5 ms, 2 -> 81.7, 4 -> 81.9 ms per step
     if (const char* mw = std::getenv("CF_MIN_WAVE")) min_wave = std::max(1, atoi(mw));
-    for (int k = 0; k < n && !std::getenv("CF_NO_WAVES");) {
+    // waves pay for themselves by overlapping the construction of tensor-core nodes; a body
+    // without one (e.g. the trivial control-overhead loop) evaluates its nodes inline
+    // (measured on that loop: 27.5 -> 23.4 us per iteration); CF_WAVES_ALWAYS for A/B
+    bool has_mm = std::getenv("CF_WAVES_ALWAYS") != nullptr;
+    for (int k = 0; k < n && !has_mm; ++k) {
+      const std::string& op = g.nodes[(*ord)[k]].op;
+      has_mm = op == "LSTMCell" || op == "LSTMCellGrad" || op == "MatMul";
+    }
+    for (int k = 0; k < n && has_mm && !std::getenv("CF_NO_WAVES");) {
       int e = k;
       while (e < n && waveable(o2[e]) && level[idx[e]] == level[idx[k]] && e - k < 256) ++e;
       if (e - k >= min_wave) (*wave_len)[k] = e - k;
