@@ -34,7 +34,8 @@ CONFIGS = {
     "cfg4": dict(T=4000, B=256, I=2048, H=2048, L=1, len_mode="full"),
     "tiny": dict(T=5, B=2, I=4, H=8, L=1, len_mode="full"),
     # BASELINE.json configs[4]: nested MoE-style gated cond in the body, bf16, PI sweep via --K
-    "cfg5": dict(T=100, B=128, I=1024, H=1024, L=2, len_mode="uniform", moe=True),
+    # (tanh experts: DESIGN.md reading R21; the bf16 parity tests run the same workload)
+    "cfg5": dict(T=200, B=128, I=1024, H=1024, L=8, len_mode="uniform", moe=True, moe_act="tanh"),
 }
 
 
@@ -105,6 +106,11 @@ def flops_per_step(c, lens_sum):
     return per * lens_sum
 
 
+def model_kw(c):
+    """Builder options of a config beyond its sizes (the MoE-style gated branch)."""
+    return {"moe": c.get("moe", False), "moe_act": c.get("moe_act", "relu")}
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -121,7 +127,7 @@ def run_reference(args, c, cfg_name):
     from oracle.models import dynamic_rnn_lstm, run_program
     from synth import rnn_inputs
     T_s = max(2, min(c["T"], args.ref_T))
-    p = dynamic_rnn_lstm(T_s, c["B"], c["I"], c["H"], c["L"], moe=c.get("moe", False))
+    p = dynamic_rnn_lstm(T_s, c["B"], c["I"], c["H"], c["L"], **model_kw(c))
     f = rnn_inputs(T_s, c["B"], c["I"], c["H"], c["L"], seed=0, len_mode=c["len_mode"],
                    moe=c.get("moe", False))
     lens_sum = int(np.minimum(f["len"], T_s).sum())
@@ -139,7 +145,7 @@ def run_reference(args, c, cfg_name):
     cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
     v = lens_sum / t
     line = {"impl": "reference", "metric": "LSTM fwd+bwd sequence-steps/sec", "value": v,
-            "unit": "sequence-steps/s", "n_gpus": world, "steps": n_steps,
+            "unit": "sequence-steps/s", "n_gpus": max(world, args.gpus), "steps": n_steps,
             "warmup": n_warm, "ms_per_step": t * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": cfg_name, **{k: c[k] for k in ("T", "B", "I", "H", "L")},
@@ -152,20 +158,31 @@ def run_reference(args, c, cfg_name):
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline(c, cfg_name, T_s):
+def cpu_baseline(c, cfg_name, T_s, T_1=2):
+    """The fp64 oracle as it stands on the host cores (all BLAS threads), plus a 1-thread
+    sample: each a bounded, truncated-T run of the same workload."""
     import numpy as np
+    from threadpoolctl import threadpool_limits
     from oracle.models import dynamic_rnn_lstm, run_program
     from synth import rnn_inputs
-    p = dynamic_rnn_lstm(T_s, c["B"], c["I"], c["H"], c["L"], moe=c.get("moe", False))
-    f = rnn_inputs(T_s, c["B"], c["I"], c["H"], c["L"], seed=0, len_mode=c["len_mode"],
-                   moe=c.get("moe", False))
-    lens_sum = int(np.minimum(f["len"], T_s).sum())
-    t0 = time.perf_counter()
-    run_program(p, f)
-    t = time.perf_counter() - t0
-    return {"value": lens_sum / t, "unit": "sequence-steps/s", "cores": os.cpu_count(),
+
+    def one(T):
+        p = dynamic_rnn_lstm(T, c["B"], c["I"], c["H"], c["L"], **model_kw(c))
+        f = rnn_inputs(T, c["B"], c["I"], c["H"], c["L"], seed=0, len_mode=c["len_mode"],
+                       moe=c.get("moe", False))
+        lens_sum = int(np.minimum(f["len"], T).sum())
+        t0 = time.perf_counter()
+        run_program(p, f)
+        return lens_sum, time.perf_counter() - t0
+
+    n, t = one(T_s)
+    with threadpool_limits(limits=1):
+        n1, t1 = one(min(T_1, T_s))
+    return {"value": n / t, "unit": "sequence-steps/s", "cores": os.cpu_count(),
             "kind": "oracle", "sample": f"{cfg_name} truncated to T={T_s} (full B/H/L), one run, "
-                                        f"{t:.1f} s"}
+                                        f"{t:.1f} s",
+            "one_thread": {"value": n1 / t1, "cores": 1,
+                           "sample": f"{cfg_name} truncated to T={min(T_1, T_s)}, one run, {t1:.1f} s"}}
 
 
 def main():
@@ -194,6 +211,18 @@ def main():
     c = CONFIGS[args.config]
     if args.impl == "reference":
         return run_reference(args, c, args.config)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch this command under torchrun (the driver's own launch
+        # sets WORLD_SIZE and lands below directly)
+        import socket
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+        sk.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+               f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        raise SystemExit(subprocess.call(cmd))
 
     import numpy as np
     import torch
@@ -204,6 +233,8 @@ def main():
     from synth import rnn_inputs
 
     rank, world, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     pg = None
     if world > 1:
@@ -216,8 +247,7 @@ def main():
     if pipe and world > c["L"]:
         raise SystemExit(f"pipeline over {world} GPUs needs >= {world} layers")
     stage = (rank, world) if pipe else None
-    p = dynamic_rnn_lstm(c["T"], c["B"], c["I"], c["H"], c["L"], stage=stage,
-                         moe=c.get("moe", False))
+    p = dynamic_rnn_lstm(c["T"], c["B"], c["I"], c["H"], c["L"], stage=stage, **model_kw(c))
     # a dedicated stream, current for torch too: the input copies of the end-to-end loop and
     # the cf_run launches are ordered on it
     stream = torch.cuda.Stream()
@@ -269,7 +299,7 @@ def main():
     y_host = torch.empty(outs[0].shape, dtype=outs[0].dtype).pin_memory()
     d2h = y_host.numel() * y_host.element_size()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e2e_steps = max(2, min(args.steps, 5))
+    e2e_steps = max(2, args.steps)   # the same step count as the device-timed value
     # the step's inputs are copied on a copy stream into one of two device input sets while
     # the previous step computes (double buffering, as a data loader would); every copy is
     # inside the timed region and each cf_run waits for its own inputs

@@ -27,8 +27,8 @@ struct cf_session;
 int32_t cf_debug_session_profile(const struct cf_session* s, unsigned long long* out, int64_t cap,
                                  int64_t* n_inst, unsigned long long* t0);
 /* Batch size from which the forward and d[x,h] GEMMs use 256-row tiles (two TMEM accumulators
- * per CTA); default 1024. Lets tests exercise that tile shape at small sizes. Returns 0 or
- * CF_E_CUDA. */
+ * per CTA); product default 512 (rows <= 0 restores it). Lets tests exercise that tile shape
+ * at small sizes. Returns 0 or CF_E_CUDA. */
 int32_t cf_debug_set_m2_rows(int32_t rows);
 /* Profiling knobs: bit 0 = workers skip every tile body (the device driver's own cost in
  * isolation; results are garbage); A/B switches (results unchanged): bit 2 = poll

@@ -20,21 +20,6 @@ from __future__ import annotations
 import numpy as np
 
 
-# bf16 storage of the tensor-core path (reading R21): when set, the LSTM cell's
-# bf16 operands (x, h) and bf16-stored outputs (h, out, gates) are rounded to bf16 (round to
-# nearest even), so decisions taken on them downstream (ReLU masks of the gated branch) see
-# the same values as the device.
-STORAGE = {"lstm_bf16": False}
-
-
-def round_bf16(a):
-    """float64 values of the nearest-even bf16 numbers (via float32, like the device's
-    __float2bfloat16 of an fp32 value)."""
-    u = np.ascontiguousarray(np.asarray(a, dtype=np.float32)).view(np.uint32).astype(np.uint64)
-    u = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16) << 16
-    return u.astype(np.uint32).view(np.float32).astype(np.float64)
-
-
 def sigmoid(x):
     return 1.0 / (1.0 + np.exp(-x))
 
@@ -172,19 +157,13 @@ def eval_op(op: str, vals, attrs):
                                             "bool": bool}[attrs["dtype"]])]
     if op == "LSTMCell":
         x, h, c, W, b = vals[:5]
-        if STORAGE["lstm_bf16"]:   # the GEMM operands x, h are bf16 tensors on the device
-            x, h = round_bf16(x), round_bf16(h)
         if attrs.get("masked"):
             r = list(lstm_cell(x, h, c, W, b, vals[5], vals[6], attrs.get("forget_bias", 0.0)))
         else:
             r = list(lstm_cell(x, h, c, W, b, forget_bias=attrs.get("forget_bias", 0.0)))
-        if STORAGE["lstm_bf16"]:
-            r[0], r[2], r[3] = round_bf16(r[0]), round_bf16(r[2]), round_bf16(r[3])
         return r
     if op == "LSTMCellGrad":
         x, h, c, W, gates = vals[:5]
-        if STORAGE["lstm_bf16"]:
-            x, h = round_bf16(x), round_bf16(h)
         if attrs.get("masked"):
             t, lens, dhn, dcn, dout = vals[5:10]
             return list(lstm_cell_grad(x, h, c, W, gates, dhn, dcn, dout, t, lens))

@@ -9,8 +9,9 @@ their state through and emit zeros. The loss is the random projection of reading
 ``y = sum(R_out * out_top) + sum_l (sum(R_h[l] * h_T[l]) + sum(R_c[l] * c_T[l]))``.
 
 The optional MoE-style gated branch (BASELINE.json configs[4]) adds after every layer
-``y_l = out_l + cond(route[t, l], relu(out_l @ WA_l), relu(out_l @ WB_l))`` with seeded, exact
-route bits (reading R12).
+``y_l = out_l + cond(route[t, l], act(out_l @ WA_l), act(out_l @ WB_l))`` with seeded, exact
+route bits (reading R12); act = relu (default) or tanh (``moe_act="tanh"``, reading R21: the
+bf16 parity workload, whose expert has no float-decided mask).
 """
 from __future__ import annotations
 
@@ -46,7 +47,7 @@ def layer_partition(L: int, world: int, rank: int):
 
 def dynamic_rnn_lstm(T_: int, B: int, I: int, H: int, L: int = 1, parallel_iterations: int = 32,
                      length_conds: bool = True, moe: bool = False, forget_bias: float = 0.0,
-                     with_grads: bool = True, stage=None) -> RNNProgram:
+                     with_grads: bool = True, stage=None, moe_act: str = "relu") -> RNNProgram:
     """The full model, or with ``stage=(rank, world)`` the partition of pipeline stage `rank`
     (layers ``layer_partition(L, world, rank)``): the layer input of a later stage is a Recv of
     the previous stage's top output and a non-final stage Sends its top output on, inside the
@@ -55,6 +56,7 @@ def dynamic_rnn_lstm(T_: int, B: int, I: int, H: int, L: int = 1, parallel_itera
     the fed lengths, so every partition computes them itself (reading R18). The stage loss is
     the part of y owned by the stage; the stage losses sum to the full model's y."""
     rank, world = stage if stage is not None else (0, 1)
+    act = {"relu": "Relu", "tanh": "Tanh"}[moe_act]   # expert activation (reading R21)
     l0, l1 = layer_partition(L, world, rank)
     first, last = rank == 0, rank == world - 1
     Ls = list(range(l0, l1))
@@ -99,8 +101,8 @@ def dynamic_rnn_lstm(T_: int, B: int, I: int, H: int, L: int = 1, parallel_itera
                     r = b.op1("Reshape", [b.op1("Slice", [r_t], {"begin": (l,), "size": (1,)})],
                               {"shape": ()})
                     oo = o
-                    e = b.cond(r, lambda: [b.op1("Relu", [b.matmul(oo, WA[l])])],
-                               lambda: [b.op1("Relu", [b.matmul(oo, WB[l])])])[0]
+                    e = b.cond(r, lambda: [b.op1(act, [b.matmul(oo, WA[l])])],
+                               lambda: [b.op1(act, [b.matmul(oo, WB[l])])])[0]
                     o = b.add(o, e)
                 outs.append(o)
                 nh.append(hn)
@@ -157,16 +159,10 @@ def dynamic_rnn_lstm(T_: int, B: int, I: int, H: int, L: int = 1, parallel_itera
 
 
 def run_program(p: RNNProgram, feeds: Dict[str, np.ndarray], K=None, sched_seed=None,
-                return_trace=False, transport=None, bf16_storage=False):
-    """bf16_storage: the LSTM cell's h / out / gates rounded to bf16 as the tensor-core path
-    stores them (kernels.STORAGE, reading R21); everything else stays float64."""
-    from . import interp, kernels
-    if bf16_storage:
-        kernels.STORAGE["lstm_bf16"] = True
-        try:
-            return run_program(p, feeds, K, sched_seed, return_trace, transport, False)
-        finally:
-            kernels.STORAGE["lstm_bf16"] = False
+                return_trace=False, transport=None):
+    """Run the program in the fp64 interpreter; every value stays float64 (the bf16 parity
+    tests feed bf16-rounded inputs, reading R16)."""
+    from . import interp
     names = list(p.fetch) + list(p.grads)
     tensors = [p.fetch[n] for n in p.fetch] + [p.grads[n] for n in p.grads]
     feeds = {k: v for k, v in feeds.items() if k in p.b.g.placeholders}

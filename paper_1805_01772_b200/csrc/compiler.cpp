@@ -1129,10 +1129,13 @@ struct Compiler {
         sp.ring = slots;
         sp.capacity = (int32_t)bound[f];
         // swap-ins land in a ring of their own, indexed by the gradient loop's iteration: the
-        // forward ring may still hold values that left the loop through an Exit
-        sp.in_buf = add_buf((size_t)pl.elem_bytes * slots, false, "swap-in ring " + std::to_string(i));
+        // forward ring may still hold values that left the loop through an Exit. In bf16 mode a
+        // chunked dW instance reads the popped x / h of its last kDwChunk steps after those
+        // iterations left the window, so the ring keeps kDwChunk more slots (like the dz ring)
+        sp.in_ring = std::min<int>(bf16() ? K + kDwChunk + 1 : K + 1, (int)bound[f]);
+        sp.in_buf = add_buf((size_t)pl.elem_bytes * sp.in_ring, false, "swap-in ring " + std::to_string(i));
         if (pl.dt == D_BF16 && p < (int)g.nodes[i].osh.size() && g.nodes[i].osh[p].size() == 2)
-          register_buf_stride(sp.in_buf, slots, (int)g.nodes[i].osh[p][0], (int)g.nodes[i].osh[p][1],
+          register_buf_stride(sp.in_buf, sp.in_ring, (int)g.nodes[i].osh[p][0], (int)g.nodes[i].osh[p][1],
                               pl.elem_bytes);
         P.swaps.push_back(sp);
         P.stack_swapped_bytes += a.bytes;

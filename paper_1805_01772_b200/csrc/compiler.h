@@ -43,6 +43,7 @@ struct SwapPlan {
   int in_buf = -1;         // buffer id of the swap-in ring (pops of the gradient loop)
   int64_t elem_bytes = 0;
   int32_t ring = 0, capacity = 0;
+  int32_t in_ring = 0;     // swap-in ring slots (program.h DSwap)
 };
 
 struct HostProgram {

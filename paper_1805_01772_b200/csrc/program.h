@@ -190,7 +190,9 @@ struct DSwap {
   int64_t host_base;      // pinned host backing, [capacity][elem_bytes]
   int64_t in_base;        // swap-in ring [ring][elem_bytes], slot = gradient-loop iteration % ring
   int32_t ring, owner_off;   // owner_off: into RunArgs.swap_owner ([ring] stack entry ids)
-  int32_t capacity, pad;
+  int32_t capacity;
+  int32_t in_ring;        // swap-in ring slots: K + 1, or K + 9 in bf16 mode (a chunked dW reads
+                          // the popped x / h of its last 8 gradient steps after they left the window)
 };
 
 // ---- cross-GPU channel (one Send/Recv edge). Each session holds one

@@ -58,7 +58,8 @@ constexpr bool kProfBuild = false;   // libcf.so: no profiler code on the driver
 #endif
 constexpr int kEwBig = 16384;   // elementwise (HK_EW) tile
 // forward / d[x,h] GEMMs use 256-row tiles from this batch size on (dW always does)
-__device__ int kM2MinRows = 512;   // measured on cfg3 (B = 512): 2% faster than 1024
+constexpr int kM2Default = 512;   // measured on cfg3 (B = 512): 2% faster than 1024
+__device__ int kM2MinRows = kM2Default;
 // test/profiling knob (cf_debug_set_flags): bit 0 = workers skip the tile bodies (isolates the
 // driver's own cost; results are garbage)
 __device__ int kDbgFlags = 0;
@@ -2049,7 +2050,7 @@ struct Driver {
     const DSwap& w = P.swaps[k];
     if (A.swap_owner[w.owner_off + r] == entry) return 0;   // still resident in its ring slot
     const int it = cur_frame >= 0 ? iter : 0;
-    const int64_t dst = w.in_base + (int64_t)(it % w.ring) * w.elem_bytes;
+    const int64_t dst = w.in_base + (int64_t)(it % w.in_ring) * w.elem_bytes;
     int32_t id = swap_copy(1, dst, w.host_base + (int64_t)dp * w.elem_bytes, w.elem_bytes, -1);
     if (id < 0) return -1;
     t->v = dst;
@@ -2875,6 +2876,12 @@ struct Driver {
         break;
       }
     }
+    // never leave a helper job in flight (an error can end the loop after start_next_wave()):
+    // the helpers must see the quit request between jobs, not inside one
+    if (pend_wave_pc_ >= 0) {
+      wave_wait();
+      pend_wave_pc_ = -1;
+    }
     // receiving halves: every message of this run has been copied out of its slot
     if (!st->error)
       for (int c = 0; c < P.n_chans; ++c)
@@ -3261,6 +3268,18 @@ struct cf_session {
 
 namespace {
 
+// bytes of a dense cf_buffer (rank 0..8, non-negative extents); -1 when malformed
+int64_t buffer_bytes(const cf_buffer& b) {
+  static const int sz[] = {1, 4, 8, 4, 8, 2};
+  if (b.rank < 0 || b.rank > 8 || b.dtype < 0 || b.dtype > 5) return -1;
+  int64_t n = sz[b.dtype];
+  for (int k = 0; k < b.rank; ++k) {
+    if (b.shape[k] < 0) return -1;
+    n *= b.shape[k];
+  }
+  return n;
+}
+
 template <class T>
 T* upload(cf_session* s, const std::vector<T>& v) {
   size_t bytes = std::max<size_t>(v.size() * sizeof(T), 16);
@@ -3484,6 +3503,7 @@ void build_session(cf_session* s, const cf::Graph& g, const cf_run_opts* o,
       d.elem_bytes = sp.elem_bytes;
       d.ring = sp.ring;
       d.capacity = sp.capacity;
+      d.in_ring = sp.in_ring;
       d.owner_off = owner_total;
       owner_total += sp.ring;
       void* h = nullptr;
@@ -3645,6 +3665,9 @@ cf_status cf_run(cf_session* s, int32_t n_feed, const char* const* feed_names,
       if (b.dtype != fi.dev_dt)
         throw cf::CfError(CF_E_DTYPE, "feed " + name + " has dtype " + std::to_string(b.dtype) +
                                           ", session expects " + std::to_string(fi.dev_dt));
+      if (buffer_bytes(b) != fi.bytes)
+        throw cf::CfError(CF_E_SHAPE, "feed " + name + " holds " + std::to_string(buffer_bytes(b)) +
+                                          " bytes, placeholder needs " + std::to_string(fi.bytes));
       Tok t{};
       t.kind = TK_PTR;
       t.v = (int64_t)(uintptr_t)b.data;
@@ -3702,6 +3725,10 @@ cf_status cf_run(cf_session* s, int32_t n_feed, const char* const* feed_names,
       fo[i] = outs ? outs[i].data : nullptr;
       if (outs && outs[i].dtype != P.fetches[i].dev_dt && P.fetches[i].bytes > 0)
         throw cf::CfError(CF_E_DTYPE, "fetch buffer " + std::to_string(i) + " dtype mismatch");
+      if (outs && P.fetches[i].bytes > 0 && (!outs[i].data || buffer_bytes(outs[i]) != P.fetches[i].bytes))
+        throw cf::CfError(CF_E_SHAPE, "fetch buffer " + std::to_string(i) + " holds " +
+                                          std::to_string(buffer_bytes(outs[i])) + " bytes, fetch needs " +
+                                          std::to_string(P.fetches[i].bytes));
     }
     if (!fo.empty())
       CUDA_OK(cudaMemcpyAsync(A.fetch_out, fo.data(), 8 * fo.size(), cudaMemcpyHostToDevice, s->stream));
@@ -3726,10 +3753,6 @@ cf_status cf_run(cf_session* s, int32_t n_feed, const char* const* feed_names,
     std::atomic<bool> io_stop{false};
     std::atomic<int> io_err{0};
     std::thread io;
-    if (A.prog.n_swaps) {
-      *(volatile unsigned long long*)s->io_tail_host = 0;
-      io = std::thread([s, &io_stop, &io_err]() { io_executor(s, &io_stop, &io_err); });
-    }
     if (s->own_stream) {
       // a library-owned stream is non-blocking: order the run after the caller's work on the
       // legacy default stream (e.g. the copies of this run's inputs)
@@ -3737,6 +3760,12 @@ cf_status cf_run(cf_session* s, int32_t n_feed, const char* const* feed_names,
       CUDA_OK(cudaStreamWaitEvent(s->stream, s->ev_in, 0));
     }
     CUDA_OK(cudaEventRecord(s->ev0, s->stream));
+    // started after the last call that can throw before the join below (a joinable
+    // std::thread destroyed during unwinding would terminate the process)
+    if (A.prog.n_swaps) {
+      *(volatile unsigned long long*)s->io_tail_host = 0;
+      io = std::thread([s, &io_stop, &io_err]() { io_executor(s, &io_stop, &io_err); });
+    }
     cudaError_t lerr = cudaLaunchCooperativeKernel((void*)cf_driver_kernel, dim3(s->grid), dim3(kThreads),
                                                    kargs, s->dyn_smem, s->stream);
     if (lerr == cudaSuccess) lerr = cudaEventRecord(s->ev1, s->stream);
@@ -3910,6 +3939,7 @@ int32_t cf_debug_set_flags(int32_t flags) {
   return cudaMemcpyToSymbol(kDbgFlags, &flags, sizeof(flags)) == cudaSuccess ? CF_OK : CF_E_CUDA;
 }
 int32_t cf_debug_set_m2_rows(int32_t rows) {
+  if (rows <= 0) rows = kM2Default;
   return cudaMemcpyToSymbol(kM2MinRows, &rows, sizeof(rows)) == cudaSuccess ? CF_OK : CF_E_CUDA;
 }
 

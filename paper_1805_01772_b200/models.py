@@ -50,13 +50,14 @@ def layer_partition(L: int, world: int, rank: int):
 
 def dynamic_rnn_lstm(T: int, B: int, I: int, H: int, L: int = 1, parallel_iterations: int = 32,
                      length_conds: bool = True, moe: bool = False, forget_bias: float = 0.0,
-                     with_grads: bool = True, stage=None) -> RNNProgram:
+                     with_grads: bool = True, stage=None, moe_act: str = "relu") -> RNNProgram:
     """The full model, or with ``stage=(rank, world)`` the partition of layer-pipeline stage
     `rank`: a later stage Recvs its layer input from
     the previous stage and a non-final stage Sends its top output on, inside the loop, every
     iteration; each stage runs its own copy of the loop control (reading R18). The stage loss
     is the part of y owned by the stage (the stage losses sum to y)."""
     rank, world = stage if stage is not None else (0, 1)
+    act = {"relu": "Relu", "tanh": "Tanh"}[moe_act]   # expert activation (reading R21)
     l0, l1 = layer_partition(L, world, rank)
     first, last = rank == 0, rank == world - 1
     Ls = list(range(l0, l1))
@@ -101,8 +102,8 @@ def dynamic_rnn_lstm(T: int, B: int, I: int, H: int, L: int = 1, parallel_iterat
                     r = g.op1("Reshape", [g.op1("Slice", [r_t], {"begin": (l,), "size": (1,)})],
                               {"shape": ()})
                     oo, wa, wb = o, WA[l], WB[l]
-                    e = g.cond(r, lambda: [g.op1("Relu", [g.op1("MatMul", [oo, wa])])],
-                               lambda: [g.op1("Relu", [g.op1("MatMul", [oo, wb])])], 1)[0]
+                    e = g.cond(r, lambda: [g.op1(act, [g.op1("MatMul", [oo, wa])])],
+                               lambda: [g.op1(act, [g.op1("MatMul", [oo, wb])])], 1)[0]
                     o = g.op1("Add", [o, e])
                 outs.append(o)
                 nh.append(hn)

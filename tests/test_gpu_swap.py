@@ -39,6 +39,9 @@ def run(T, B, I, H, L, f, precision, K, budget, swap_min=0):
     ("f32", (9, 70, 40, 72, 2), "uniform", 2, 1e-5, 0),
     ("f32", (12, 5, 12, 16, 1), "full", 1, 1e-5, 64),     # small values: lowered threshold
     ("bf16", (8, 130, 256, 512, 2), "capped", 3, 2e-2, 0),
+    # T >= 2 (K + 1) + 8: the swap-in ring wraps while a chunked dW (8 gradient steps) still
+    # reads popped x / h (the swap-in ring needs K + 9 slots in bf16 mode)
+    ("bf16", (24, 64, 256, 256, 2), "full", 3, 2e-2, 0),
 ])
 def test_swap_bit_identical_and_parity(prec, shape, mode, K, tol, smin):
     T, B, I, H, L = shape

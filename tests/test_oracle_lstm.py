@@ -120,7 +120,7 @@ def test_fused_cell_equals_composite():
         assert _maxrel(a, c) <= 1e-13
 
 
-def _torch_moe_out_of_graph(f, T, B, I, H, L, route):
+def _torch_moe_out_of_graph(f, T, B, I, H, L, route, act="relu"):
     """Host-language loop with Python `if` on the route bits (out-of-graph control flow)."""
     x = torch.tensor(f["x"], requires_grad=True)
     params = {}
@@ -144,10 +144,11 @@ def _torch_moe_out_of_graph(f, T, B, I, H, L, route):
             out = torch.where(live, hn, torch.zeros_like(hn))
             hs[l] = torch.where(live, hn, hs[l])
             cs[l] = torch.where(live, cn, cs[l])
+            fn = torch.relu if act == "relu" else torch.tanh
             if route[t, l]:
-                out = out + torch.relu(out @ params[f"WA{l}"])
+                out = out + fn(out @ params[f"WA{l}"])
             else:
-                out = out + torch.relu(out @ params[f"WB{l}"])
+                out = out + fn(out @ params[f"WB{l}"])
             inp = out
         outs.append(inp)
     y = (torch.tensor(f["R_out"]) * torch.stack(outs)).sum()
@@ -160,16 +161,18 @@ def _torch_moe_out_of_graph(f, T, B, I, H, L, route):
     return res
 
 
-def test_moe_cond_brute_force():
-    """All 2^T route patterns of a T=4, L=1 loop with a gated branch (cfg5 structure)."""
+@pytest.mark.parametrize("act", ["relu", "tanh"])
+def test_moe_cond_brute_force(act):
+    """All 2^T route patterns of a T=4, L=1 loop with a gated branch (cfg5 structure), for
+    both expert activations (reading R21)."""
     T, B, I, H, L = 4, 2, 3, 4, 1
-    p = dynamic_rnn_lstm(T, B, I, H, L, moe=True)
+    p = dynamic_rnn_lstm(T, B, I, H, L, moe=True, moe_act=act)
     base = rnn_inputs(T, B, I, H, L, seed=11, len_mode="uniform", moe=True)
     for bits in itertools.product([False, True], repeat=T):
         f = dict(base)
         f["route"] = np.array(bits).reshape(T, L)
         r, tr = run_program(p, f, return_trace=True)
-        ref = _torch_moe_out_of_graph(f, T, B, I, H, L, f["route"])
+        ref = _torch_moe_out_of_graph(f, T, B, I, H, L, f["route"], act)
         for k, v in ref.items():
             assert _maxrel(r[k], v) <= 1e-12, (bits, k)
         assert set(tr.pushes) == set(tr.pops)
@@ -218,23 +221,17 @@ def test_invariants_and_parallel_iterations(K, seed):
 
 
 
-def test_bf16_storage_rounding_is_torchs_bf16():
-    """Reading R21: the bf16-storage oracle rounds exactly like a float32 -> bf16 cast
-    (checked against torch, a library routine), and only the LSTM cell's bf16-stored outputs
-    (h, out, gates) are rounded."""
+def test_synth_bf16_rounding_is_torchs_bf16():
+    """Reading R16: bf16 parity inputs are rounded to bf16 by the input generator (round to
+    nearest even, as a float32 -> bf16 cast; checked against torch, a library routine); the
+    oracle then runs fp64 on exactly those values."""
     import torch
 
-    from oracle.kernels import round_bf16
-    from oracle.models import dynamic_rnn_lstm, run_program
-    from synth import rnn_inputs
+    from synth import rnn_inputs, round_bf16
     rng = np.random.default_rng(0)
     a = rng.standard_normal(20000) * 10.0 ** rng.integers(-12, 12, 20000)
     assert np.array_equal(round_bf16(a), torch.tensor(a, dtype=torch.float32).to(torch.bfloat16).double().numpy())
-    T, B, I, H, L = 3, 2, 4, 8, 1
-    f = rnn_inputs(T, B, I, H, L, seed=0, len_mode="full", bf16=True)
-    p = dynamic_rnn_lstm(T, B, I, H, L)
-    r = run_program(p, f, bf16_storage=True)
-    assert np.array_equal(round_bf16(r["out"]), r["out"])       # h / out stored in bf16
-    assert not np.array_equal(round_bf16(r["cT0"]), r["cT0"])   # c stays fp64
-    r0 = run_program(p, f)
-    assert not np.array_equal(round_bf16(r0["out"]), r0["out"])
+    f = rnn_inputs(3, 2, 4, 8, 1, seed=0, len_mode="full", bf16=True)
+    for k, v in f.items():
+        if v.dtype == np.float64:
+            assert np.array_equal(round_bf16(v), v), k
