@@ -135,6 +135,10 @@ for _name, (_res, _args) in _sig.items():
 EXPORTED = list(_sig)
 
 
+def _dtype_size(d: int) -> int:
+    return {BOOL: 1, I32: 4, I64: 8, F32: 4, F64: 8, BF16: 2}[d]
+
+
 def _check(st: int):
     if st != 0:
         raise CfError(st, _lib.cf_last_error().decode())
@@ -540,6 +544,10 @@ class Session:
             obufs[i].data = t.data_ptr()
             obufs[i].dtype = self.fetch_dtypes[i]
             obufs[i].rank = t.dim()
+            for k, sz in enumerate(t.shape):
+                obufs[i].shape[k] = sz
+            if not t.is_contiguous() or t.element_size() != _dtype_size(self.fetch_dtypes[i]):
+                raise CfError(2, f"fetch buffer {i} must be contiguous with the session dtype")
         dead = (C.c_uint8 * max(len(outs), 1))()
         tr = cf_trace()
         bits = None
