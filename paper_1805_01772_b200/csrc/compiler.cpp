@@ -536,7 +536,8 @@ struct Compiler {
     for (auto& pl : P.places) counts[pl.kind]++;
     ds << "accumulators=" << P.accs.size() << " tma_operands=" << P.reg.size() << "\n";
     ds << "structured frames=" << P.structured_frames << " cond contexts="
-       << (P.ctxs.empty() ? 0 : P.ctxs.size() - 1) << " waves=" << P.n_waves << "\n";
+       << (P.ctxs.empty() ? 0 : P.ctxs.size() - 1) << " waves=" << P.n_waves
+       << " heavy_batches=" << P.n_batches << "\n";
     ds << "stacks: resident bytes=" << P.stack_resident_bytes << " swapped arenas=" << P.swaps.size()
        << " swapped bytes=" << P.stack_swapped_bytes << "\n";
     ds << "placements root=" << counts[0] << " ring=" << counts[1] << " arena=" << counts[2]
@@ -978,10 +979,18 @@ struct Compiler {
       default: return false;
     }
   }
+  // heavy nodes the driver constructs as one batch (runtime.cu run_batch): the tensor-core LSTM
+  // cell nodes of the bf16 path (no swapped stacks: a swap copy is created while a node is built)
+  bool batchable(int v) const {
+    const DNode& d = P.nodes[v];
+    return bf16() && P.swaps.empty() && !std::getenv("CF_NO_BATCH") && d.op == OP_HEAVY &&
+           (d.aux[0] == HK_LSTM_FWD || d.aux[0] == HK_LSTM_BWD_EW) && d.n_in <= 32 && d.n_ctrl <= 32;
+  }
   void form_waves(int f, std::vector<int>* ord, std::vector<int>* nctx, const std::map<int, int>& alias,
-                  std::vector<int>* wave_len) {
+                  std::vector<int>* wave_len, std::vector<int>* batch_len) {
     const int n = (int)ord->size();
     wave_len->assign(n, 0);
+    batch_len->assign(n, 0);
     if (std::getenv("CF_NO_LEVEL_ORDER")) return;   // debugging switch
     std::map<int, int> pos;
     for (int k = 0; k < n; ++k) pos[(*ord)[k]] = k;
@@ -1049,9 +1058,21 @@ struct Compiler {
           if (pos.count(c) && pos[c] < k) preds[k].push_back(pos[c]);
     for (int k = 0; k < n; ++k)   // ord is topological: predecessors come first
       for (int q : preds[k]) level[k] = std::max(level[k], level[q] + 1);
+    // phases: a chain of batchable heavy nodes (e.g. the layers of one cell branch) stays in one
+    // phase; any other node that consumes a batchable node's output starts the next phase. Within
+    // a phase the other nodes come first (level order, waves), then the phase's batchable nodes
+    // as ONE batch: the driver builds their instances together (runtime.cu run_batch) instead of
+    // one node at a time between routing waves. Any topological order is a valid evaluation
+    // order of the dataflow graph (PAPER.md:209-214 non-strict semantics).
+    std::vector<int> phase(n, 0), bat(n, 0);
+    for (int k = 0; k < n; ++k) bat[k] = batchable((*ord)[k]) ? 1 : 0;
+    for (int k = 0; k < n; ++k)
+      for (int q : preds[k]) phase[k] = std::max(phase[k], phase[q] + ((bat[q] && !bat[k]) ? 1 : 0));
     std::vector<int> idx(n);
     for (int k = 0; k < n; ++k) idx[k] = k;
     std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) {
+      if (phase[a] != phase[b]) return phase[a] < phase[b];
+      if (bat[a] != bat[b]) return bat[a] < bat[b];
       if (level[a] != level[b]) return level[a] < level[b];
       return waveable((*ord)[a]) > waveable((*ord)[b]);
     });
@@ -1061,6 +1082,17 @@ struct Compiler {
       c2.push_back((*nctx)[k]);
     }
     wave_len->assign(n, 0);
+    batch_len->assign(n, 0);
+    for (int k = 0; k < n;) {   // batches: consecutive batchable nodes of one phase (<= 32)
+      if (!bat[idx[k]]) {
+        ++k;
+        continue;
+      }
+      int e = k;
+      while (e < n && bat[idx[e]] && phase[idx[e]] == phase[idx[k]] && e - k < 32) ++e;
+      if (e - k >= 2) (*batch_len)[k] = e - k;
+      k = e;
+    }
     // smallest level group evaluated as a wave (helper round trip vs serial evaluation);
     // CF_MIN_WAVE overrides it (A/B)
     int min_wave = 1;   // measured on cfg3: 1 -> 80.5 ms, 2 -> 81.7, 4 -> 81.9 ms per step
@@ -1228,13 +1260,14 @@ struct Compiler {
       // ---- waves: order the body by dependency level and group each level's routing / stack
       //      nodes (independent by construction) behind an OP_WAVE marker
       std::vector<int> wave_len;   // per ord position: > 0 = a wave of that many starts here
-      form_waves(f, &ord, &node_ctx, alias, &wave_len);
+      std::vector<int> batch_len;  // per ord position: > 0 = a heavy batch of that many starts here
+      form_waves(f, &ord, &node_ctx, alias, &wave_len, &batch_len);
       DFrame& F = P.frames[f];
       F.K = o.parallel_iterations > 0 ? o.parallel_iterations : ctx.K;
       F.bound = (int32_t)bound[f];
       F.body_off = (int)P.order.size();
       for (size_t k = 0; k < ord.size(); ++k) {
-        if (wave_len[k] > 0) P.order.push_back(ord[k]);   // the marker's slot (never evaluated)
+        if (wave_len[k] > 0 || batch_len[k] > 0) P.order.push_back(ord[k]);   // the marker's slot (never evaluated)
         P.order.push_back(ord[k]);
       }
       F.n_body = (int)P.order.size() - F.body_off;
@@ -1273,6 +1306,31 @@ struct Compiler {
           wm.in_off = wm.ctrl_off = (int)P.body_ivids.size() - F.bi_off;
           P.body_nodes.push_back(wm);
           P.n_waves++;
+        }
+        if (batch_len[k] > 0) {
+          DNode bm{};
+          bm.op = OP_HEAVY_BATCH;
+          bm.aux[0] = batch_len[k];
+          bm.place_off = -1;
+          bm.in_off = bm.ctrl_off = (int)P.body_ivids.size() - F.bi_off;
+          P.body_nodes.push_back(bm);
+          P.n_batches++;
+          // per member: bit j of aux[6] = data input j is an output of an earlier member of the
+          // same batch (its liveness follows that member's; the driver checks the others)
+          std::map<int, int> out_of;   // value id -> member
+          for (int q = 0; q < batch_len[k]; ++q) {
+            const int u = ord[k + q];
+            for (int p2 = 0; p2 < P.nodes[u].n_out; ++p2) out_of[P.nodes[u].out_vid + p2] = q;
+          }
+          for (int q = 0; q < batch_len[k]; ++q) {
+            DNode& mu = P.nodes[ord[k + q]];
+            uint32_t m = 0;
+            for (int j = 0; j < mu.n_in && j < 32; ++j) {
+              auto it = out_of.find(res(P.in_vids[mu.in_off + j]));
+              if (it != out_of.end() && it->second < q) m |= 1u << j;
+            }
+            mu.aux[6] = (int32_t)m;
+          }
         }
         DNode bn = P.nodes[v];
         // node id for the device driver (pad[2] high half; pad[0..2] low are registry hints)
@@ -1390,9 +1448,9 @@ HostProgram compile(const Graph& g, const CompileOpts& o, const std::vector<TRef
       for (int k = 0; k < F.n_body; ++k) {
         const auto& bn = c.P.body_nodes[F.bn_off + k];
         const int nid = c.P.order[F.body_off + k];
-        ls << k << " " << (bn.op == OP_WAVE ? std::string("WAVE") : g.nodes[nid].op) << " node=" << nid
+        ls << k << " " << (bn.op == OP_WAVE ? std::string("WAVE") : bn.op == OP_HEAVY_BATCH ? std::string("BATCH") : g.nodes[nid].op) << " node=" << nid
            << " ctx=" << bn.ctx << " gctx=" << g.nodes[nid].ctx;
-        if (bn.op == OP_WAVE) ls << " n=" << bn.aux[0];
+        if (bn.op == OP_WAVE || bn.op == OP_HEAVY_BATCH) ls << " n=" << bn.aux[0];
         ls << " in=";
         for (int j = 0; j < bn.n_in; ++j) ls << c.P.body_ivids[F.bi_off + bn.in_off + j] << ",";
         ls << " out=" << bn.out_vid;

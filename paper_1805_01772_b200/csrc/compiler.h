@@ -78,6 +78,7 @@ struct HostProgram {
   std::vector<cfdev::DCtx> ctxs;     // [0] = loop level (unused entry)
   int structured_frames = 0;
   int n_waves = 0;
+  int n_batches = 0;
   int64_t stack_resident_bytes = 0, stack_swapped_bytes = 0;
   int64_t chan_bytes = 0;
   std::map<std::string, FeedInfo> feeds;

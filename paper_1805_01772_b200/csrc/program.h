@@ -53,6 +53,9 @@ enum Op : int32_t {
   OP_RECV,          // cross-GPU Recv (aux0: channel index); output placed like a heavy output
   OP_WAVE,          // body-program marker: the next aux0 nodes are independent routing / stack
                     // nodes, evaluated in parallel by the driver CTA's helper warps
+  OP_HEAVY_BATCH,   // body-program marker: the next aux0 nodes are tensor-core LSTM nodes of one
+                    // phase (each input an earlier member's output or ready before the marker);
+                    // their instances are built together, one helper lane per node
   OP__COUNT
 };
 

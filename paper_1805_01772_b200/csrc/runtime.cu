@@ -814,6 +814,11 @@ struct Wave {
   int64_t houtp[8];
   int64_t hmap[5], hslot[5];
   int slow[256];          // wave positions left for the general evaluator
+  // job 2: a heavy batch (Driver::run_batch): helper warp 1 builds the members' instances,
+  // lane m = member m; ids reserved by the driver thread (-1: none / member not live)
+  int bpc, bcount, bfail;
+  int bid[32][4];         // per member: main (fwd) / EW (bwd), DXH (bwd), dW flush, weight prep
+  int bnid[32];           // per member: graph node id
 };
 
 __device__ void wave_work(Wave& w, int start, int n, int h, int nh) {
@@ -1247,6 +1252,12 @@ struct Driver {
   };
 
   __noinline__ __device__ int32_t new_inst(int kind, int sub, int ntiles) {
+    const int32_t id = reserve_inst(kind, ntiles);
+    if (id >= 0) inst_header(id, kind, sub, ntiles);
+    return id;
+  }
+  // an instance id and its in-flight ring slot (driver-private shared-memory bookkeeping)
+  __noinline__ __device__ int32_t reserve_inst(int kind, int ntiles) {
     if (ninst >= A.inst_cap) {
       fail(CF_E_STACK_BUDGET, -1);
       return -1;
@@ -1268,6 +1279,11 @@ struct Driver {
     // longer than 65534 iterations)
     r_kfi[sl] = (int)((unsigned)(kind & 255) | ((unsigned)((cur_frame + 1) & 255) << 8) |
                       ((unsigned)min(cur_frame >= 0 ? iter : 0, 0xFFFF) << 16));
+    return id;
+  }
+  // the instance record's header (global memory; also written by the helper lanes of a batch)
+  __device__ void inst_header(int32_t id, int kind, int sub, int ntiles) {
+    ntiles = max(ntiles, 1);
     Inst& I = A.insts[id];
     I.kind = kind;
     I.sub = sub;
@@ -1287,7 +1303,26 @@ struct Driver {
       pr[4] = 0;
       pr[5] = ((unsigned long long)kind << 32) | (unsigned)ntiles;
     }
-    return id;
+  }
+  // add_dep for the helper lanes of a batch (several lanes register successors concurrently;
+  // the driver thread waits meanwhile, so no completion runs): shared-memory atomics, no
+  // dedupe across lanes (a repeated producer just counts twice, consistently)
+  __device__ void add_dep_atomic(int32_t id, int32_t w) {
+    if (done(w)) return;
+    const int ws = w & kRingMask;
+    const int ns = atomicAdd(&r_sn[ws], 1);
+    if (ns < kInlineSucc) {
+      r_sv[ws * kInlineSucc + ns] = id;
+    } else {
+      const int32_t e = atomicAdd(&nedge, 1);
+      if (e >= A.edge_cap) {
+        fail(CF_E_STACK_BUDGET, -2);
+        return;
+      }
+      A.edge_to[e] = id;
+      A.edge_next[e] = atomicExch(&r_succ[ws], e);
+    }
+    atomicAdd(&r_pend[id & kRingMask], 1);
   }
   __forceinline__ __device__ void add_dep(int32_t id, int32_t w) {
     if (done(w)) return;
@@ -1384,7 +1419,7 @@ struct Driver {
       iter_out_[frame_ib(fr) + it]--;
     }
     int32_t e = r_succ[sl];
-    const int ns = r_sn[sl];
+    const int ns = min(r_sn[sl], kInlineSucc);   // helper lanes count past the inline slots
     r_id[sl] = -1;   // done
     for (int k = 0; k < ns; ++k) {
       const int32_t s2 = r_sv[sl * kInlineSucc + k];
@@ -1764,6 +1799,273 @@ struct Driver {
     submit(e);
     submit(x);
     return EV_OK;
+  }
+
+  // ---------------------------------------------------------------- heavy batches
+  // OP_HEAVY_BATCH at body position pc: the next n nodes are tensor-core LSTM nodes of one
+  // phase (compiler.cpp form_waves): every input is ready before the marker or an output of an
+  // earlier member. The driver thread checks liveness and reserves the instance ids; helper
+  // warp 1 builds all members at once (lane m = member m: placements and output tokens, then
+  // operand-registry lookups, records and dependency edges); the driver then submits. Returns
+  // the body positions consumed: n + 1, or 1 when the members must go through the general
+  // path one by one (a context or a scalar not known yet, a dead member, a pending wave job).
+  __noinline__ __device__ int run_batch(const DFrame& F, int pc, int n) {
+    Region rg(this, 32 + 23);
+    if (pend_wave_pc_ >= 0 || P.precision != D_BF16 || P.n_swaps || (dbg_ & (1 << 30))) return 1;
+    Wave& w = *wave_;
+    // liveness: contexts first (no state is changed before every member is known)
+    unsigned live = 0;
+    for (int m = 0; m < n; ++m) {
+      const DNode& d = bn_[pc + 1 + m];
+      int l = 1;
+      if (d.ctx) {
+        l = lstamp_[d.ctx] == lgen_ && lval_[d.ctx] >= 0 ? lval_[d.ctx] : ctx_live(d.ctx);
+        if (l < 0) return 1;
+      }
+      if (!l) continue;
+      // inputs that are not earlier members' outputs, and control inputs, must be live; the
+      // masked cells' time step must be an immediate
+      const unsigned inb = (unsigned)d.aux[6];
+      for (int j = 0; j < d.n_in; ++j)
+        if (!(inb >> j & 1) && in_tok(d, j).dead) return 1;
+      for (int j = 0; j < d.n_ctrl; ++j)
+        if (toks_[iv_[d.ctrl_off + j]].dead) return 1;
+      if ((d.aux[1] & 1) && in_tok(d, 5).kind != TK_IMM) return 1;
+      live |= 1u << m;
+    }
+    // reserve the ids (ring slots: may drain completions, so before the helpers start)
+    const bool m2rows = bn_[pc + 1].imm[0] >= kM2MinRows;
+    int32_t last_flush = -1;
+    for (int m = 0; m < n; ++m) {
+      int* id = w.bid[m];
+      id[0] = id[1] = id[2] = id[3] = -1;
+      if (!(live >> m & 1)) {
+        n_dead++;
+        continue;
+      }
+      const DNode& d = bn_[pc + 1 + m];
+      const int nid = ((const int16_t*)d.pad)[5] >= 0 ? ((const int16_t*)d.pad)[5] : P.order[F.body_off + pc + 1 + m];
+      w.bnid[m] = nid;
+      const int64_t B = d.imm[0], In = d.imm[1], H = d.imm[2], KT = In + H;
+      const bool masked = d.aux[1] & 1;
+      const bool m2 = B >= kM2MinRows;
+      (void)m2rows;
+      if (d.aux[0] == HK_LSTM_FWD) {
+        if (prep_inst_[nid] < 0) {
+          id[3] = reserve_inst(HK_PREP_WP, (int)((4 * H + 15) / 16));
+          prep_inst_[nid] = id[3];
+        }
+        id[0] = reserve_inst(HK_LSTM_FWD_TC, (int)((m2 ? (B + 255) / 256 : (B + 127) / 128) * (H / 64)));
+      } else {
+        if (prep_inst_[nid] < 0) {
+          id[3] = reserve_inst(HK_PREP_WT, (int)((KT / 64) * (4 * H / 128)));
+          prep_inst_[nid] = id[3];
+        }
+        const int acc_w = d.aux[3], acc_b = d.aux[4];
+        if (!(acc_w >= 0 && acc_b >= 0) || dw_count_[nid] + 1 == 8) {
+          id[2] = reserve_inst(HK_LSTM_DW_TC, (int)((4 * H / 256) * (KT / 256) + (4 * H + 255) / 256));
+          last_flush = id[2];
+        }
+        id[0] = reserve_inst(HK_LSTM_BWD_EW_BF, (int)(((B + 127) / 128) * (H / 64)));
+        id[1] = reserve_inst(HK_LSTM_DXH_TC, (int)((m2 ? (B + 255) / 256 : (B + 127) / 128) * (KT / 256)));
+      }
+      (void)masked;
+      if (st->error) return n + 1;
+    }
+    w.job = 2;
+    w.bpc = pc + 1;
+    w.bcount = n;
+    w.bfail = 0;
+    w.chain = 0;
+    w.done = 0;
+    __threadfence_block();
+    *(volatile int*)&w.seq = w.seq + 1;
+    flush_publish();
+    while (*(volatile int*)&w.done < kWaveWarps) {
+    }
+    __threadfence_block();
+    w.job = 0;
+    if (w.bfail && !st->error) fail(CF_E_UNSUPPORTED, -600);
+    if (last_flush >= 0) last_dw = last_flush;
+    // submit in creation order (weight prep, dW chunk, then the members' own instances)
+    for (int m = 0; m < n; ++m) {
+      const int* id = w.bid[m];
+      if (id[3] >= 0) submit(id[3]);
+      if (id[2] >= 0) submit(id[2], true);
+      if (id[0] >= 0) submit(id[0]);
+      if (id[1] >= 0) submit(id[1]);
+    }
+    flush_publish();
+    return n + 1;
+  }
+
+  // helper lane m of warp 1: member m of the batch dispatched by run_batch
+  __device__ void batch_lane(Wave& w, int m) {
+    const bool mine = m < w.bcount && w.bid[m][0] >= 0;
+    const DNode* dp = mine ? &bn_[w.bpc + m] : nullptr;
+    int64_t outp[8];
+    bool ok = true;
+    // phase A: placements and output tokens (later members read them in phase B)
+    if (mine) {
+      const DNode& d = *dp;
+      const int np = prep_nplace(d);
+      for (int q = 0; q < np; ++q)
+        if (!place_core(d, q, &outp[q])) ok = false;
+      const int* id = w.bid[m];
+      if (ok) {
+        if (d.aux[0] == HK_LSTM_FWD) {
+          set_out(d, 0, ptr_tok(outp[0], id[0], D_BF16));
+          set_out(d, 1, ptr_tok(outp[1], id[0], D_F32));
+          set_out(d, 2, ptr_tok(outp[2], id[0], D_BF16));
+          set_out(d, 3, ptr_tok(outp[3], id[0], D_BF16));
+        } else {
+          const int acc_w = d.aux[3], acc_b = d.aux[4];
+          set_out(d, 0, ptr_tok(outp[0], id[1], D_F32));
+          set_out(d, 1, ptr_tok(outp[1], id[1], D_F32));
+          set_out(d, 2, ptr_tok(outp[2], id[0], D_F32));
+          set_out(d, 3, ptr_tok(outp[3], id[2] >= 0 ? id[2] : acc_writer_[acc_w], D_F32));
+          set_out(d, 4, ptr_tok(outp[4], id[2] >= 0 ? id[2] : acc_writer_[acc_b], D_F32));
+        }
+        toks_[d.ctrl_vid] = Tok{0, -1, 0, TK_FLOW, 0, 0};
+      }
+    }
+    __syncwarp();
+    // phase B: operand lookups, records, dependency edges
+    if (mine && ok) ok = batch_build(*dp, w.bnid[m], w.bid[m], outp);
+    if (mine && !ok) atomicOr(&w.bfail, 1);
+    __syncwarp();
+  }
+
+  __device__ bool batch_build(const DNode& d, int nid, const int* id, const int64_t* outp) {
+    int16_t* hint = (int16_t*)const_cast<DNode&>(d).pad;
+    const bool masked = d.aux[1] & 1;
+    const int64_t t = masked ? in_tok(d, 5).v : 0;
+    const int64_t B = d.imm[0], In = d.imm[1], H = d.imm[2], KT = In + H;
+    const bool m2 = B >= kM2MinRows;
+    auto ip = [&](int j) { return in_tok(d, j).v; };
+    // the same dependency added twice by one lane is counted once
+    int32_t seen[12];
+    int ns = 0;
+    auto dep = [&](int32_t idd, int32_t wr) {
+      if (wr < 0) return;
+      for (int k = 0; k < ns; ++k)
+        if (seen[k] == wr) return;
+      if (ns < 12) seen[ns++] = wr;
+      add_dep_atomic(idd, wr);
+    };
+    if (d.aux[0] == HK_LSTM_FWD) {
+      int32_t pw = prep_inst_[nid];
+      if (id[3] >= 0) {   // per-run weight preparation (gate-interleaved bf16 W)
+        inst_header(id[3], HK_PREP_WP, 0, (int)((4 * H + 15) / 16));
+        Inst& Q = A.insts[id[3]];
+        Q.n = H;
+        Q.k = KT;
+        Q.p[0] = in_tok(d, 3).v;
+        Q.p[13] = outp[4];
+        add_dep_atomic(id[3], in_tok(d, 3).writer);
+      }
+      int64_t mx, sx, mh, sh, mw, sw;
+      if (!resolve_core(ip(0), (int)B, (int)In, 0, &mx, &sx, hint + 0) ||
+          !resolve_core(ip(1), (int)B, (int)H, 0, &mh, &sh, hint + 1) ||
+          !resolve_core(outp[4], (int)(4 * H), (int)KT, 1, &mw, &sw, hint + 2))
+        return false;
+      const int ntiles = (int)((m2 ? (B + 255) / 256 : (B + 127) / 128) * (H / 64));
+      inst_header(id[0], HK_LSTM_FWD_TC, masked | (m2 ? 2 : 0), ntiles);
+      Inst& I = A.insts[id[0]];
+      I.m = B; I.k = In; I.n = H;
+      I.p[0] = mx; I.p[1] = mh; I.p[2] = ip(2); I.p[3] = mw; I.p[4] = ip(4);
+      I.p[5] = masked ? ip(6) : 0;
+      I.p[6] = ip(1);
+      for (int q = 0; q < 4; ++q) I.p[8 + q] = outp[q];
+      I.s[0] = t; I.s[1] = d.aux[2]; I.s[2] = sx; I.s[3] = sh;
+      for (int j = 0; j < d.n_in; ++j) dep(id[0], in_tok(d, j).writer);
+      dep(id[0], pw);
+      return true;
+    }
+    // backward: EW (dz, dc, db partials) -> DXH (dx, dh); dW / db chunked over 8 steps
+    const int acc_w = d.aux[3], acc_b = d.aux[4];
+    const int o = masked ? 7 : 5;
+    const int64_t dz_ptr = outp[5];
+    const int64_t dz_bytes = ((B * 4 * H * 2 + 1023) / 1024) * 1024;
+    const int32_t pw = prep_inst_[nid];
+    if (id[3] >= 0) {   // per-run weight preparation (bf16 W^T)
+      inst_header(id[3], HK_PREP_WT, 0, (int)((KT / 64) * (4 * H / 128)));
+      Inst& Q = A.insts[id[3]];
+      Q.n = H;
+      Q.k = KT;
+      Q.p[0] = in_tok(d, 3).v;
+      Q.p[13] = outp[6];
+      add_dep_atomic(id[3], in_tok(d, 3).writer);
+    }
+    int64_t mz, sz, mwt, swt, mzn, szn, mxn, sxn, mhn, shn;
+    if (!resolve_core(dz_ptr, (int)B, (int)(4 * H), 0, &mz, &sz, hint + 0) ||
+        !resolve_core(outp[6], (int)KT, (int)(4 * H), 1, &mwt, &swt, hint + 1) ||
+        !resolve_core(dz_ptr, (int)B, (int)(4 * H), 2, &mzn, &szn, hint + 2) ||
+        !resolve_core(ip(0), (int)B, (int)In, 2, &mxn, &sxn, hint + 3) ||
+        !resolve_core(ip(1), (int)B, (int)H, 2, &mhn, &shn, hint + 4))
+      return false;
+    const int32_t e = id[0], x = id[1];
+    inst_header(e, HK_LSTM_BWD_EW_BF, masked, (int)(((B + 127) / 128) * (H / 64)));
+    inst_header(x, HK_LSTM_DXH_TC, masked | (m2 ? 2 : 0),
+                (int)((m2 ? (B + 255) / 256 : (B + 127) / 128) * (KT / 256)));
+    {
+      Inst& I = A.insts[e];
+      I.m = B; I.k = In; I.n = H;
+      I.p[2] = ip(2); I.p[4] = ip(4); I.p[5] = masked ? ip(6) : 0;
+      I.p[6] = ip(o); I.p[7] = ip(o + 1); I.p[8] = ip(o + 2);
+      const int nx = d.aux[5], base = d.n_in - nx;   // folded AddN terms of dout
+      I.p[14] = nx > 0 ? ip(base) : 0;
+      I.p[15] = nx > 1 ? ip(base + 1) : 0;
+      I.p[9] = outp[2]; I.p[10] = dz_ptr;
+      I.s[0] = t; I.s[4] = in_tok(d, o + 2).dt; I.s[5] = dz_bytes;
+      for (int j = 0; j < d.n_in; ++j) dep(e, in_tok(d, j).writer);
+    }
+    {
+      ns = 0;
+      Inst& I = A.insts[x];
+      I.m = B; I.k = In; I.n = H;
+      I.p[0] = mz; I.p[1] = mwt; I.p[5] = masked ? ip(6) : 0; I.p[6] = ip(o);
+      I.p[11] = outp[0]; I.p[12] = outp[1];
+      I.s[0] = t; I.s[2] = sz;
+      dep(x, e);
+      dep(x, pw);
+      dep(x, in_tok(d, o).writer);
+    }
+    const int cnt = dw_count_[nid];
+    int64_t* rec = A.dw_pend + ((int64_t)nid * 8 + cnt) * 10;
+    rec[0] = szn; rec[1] = mxn; rec[2] = sxn; rec[3] = mhn; rec[4] = shn;
+    rec[5] = dz_ptr + dz_bytes;
+    rec[6] = e; rec[7] = in_tok(d, 0).writer; rec[8] = in_tok(d, 1).writer;
+    A.dw_pend[(int64_t)nid * 80 + 9] = mzn;
+    dw_count_[nid] = cnt + 1;
+    if (id[2] >= 0) {   // close the dW chunk (the driver reserved its id)
+      const int32_t wd = id[2];
+      const int c2 = cnt + 1;
+      inst_header(wd, HK_LSTM_DW_TC, d.aux[1] & 1, (int)((4 * H / 256) * (KT / 256) + (4 * H + 255) / 256));
+      Inst& I = A.insts[wd];
+      I.m = B; I.k = In; I.n = H;
+      I.p[0] = mzn;
+      I.p[3] = acc_w >= 0 ? P.accs[acc_w].base : outp[3];
+      I.p[4] = acc_b >= 0 ? P.accs[acc_b].base : outp[4];
+      int64_t* ax = A.inst_aux + (int64_t)wd * 48;
+      I.p[6] = (int64_t)ax;
+      I.s[6] = (acc_w >= 0 ? 1 : 0) | (acc_b >= 0 ? 2 : 0);
+      I.s[7] = c2;
+      ns = 0;
+      for (int q = 0; q < c2; ++q) {
+        const int64_t* rq = A.dw_pend + ((int64_t)nid * 8 + q) * 10;
+        for (int k = 0; k < 6; ++k) ax[q * 6 + k] = rq[k];
+        dep(wd, (int32_t)rq[6]);
+        dep(wd, (int32_t)rq[7]);
+        dep(wd, (int32_t)rq[8]);
+      }
+      if (acc_w >= 0) dep(wd, acc_writer_[acc_w]);
+      if (acc_b >= 0) dep(wd, acc_writer_[acc_b]);
+      if (acc_w >= 0) acc_writer_[acc_w] = wd;
+      if (acc_b >= 0) acc_writer_[acc_b] = wd;
+      dw_count_[nid] = 0;
+    }
+    return true;
   }
 
   // create the dW/db instance for the queued steps of LSTMCellGrad node nid
@@ -2709,6 +3011,12 @@ struct Driver {
         if (st->error) break;
         continue;
       }
+      if (op == OP_HEAVY_BATCH) {   // 1: build the members one by one (the general path)
+        pc += run_batch(F, pc, d->aux[0]);
+        progress = true;
+        if (st->error) break;
+        continue;
+      }
       if (op == OP_MERGE && d->aux[5] && (ctx_live(d->aux[6]) < 0 || ctx_live(d->aux[5]) < 0)) break;
       if (op <= OP_TA_GRAD || op == OP_ACC || op == OP_STACK_PUSH || op == OP_STACK_POP) {
         long long cs0 = prof ? clock64() : 0;
@@ -3173,6 +3481,8 @@ __global__ void __launch_bounds__(kThreads, 1) cf_driver_kernel(RunArgs A_param)
           __threadfence_block();
           if (wave.job == 1) {
             ((Driver*)drv_obj)->heavy_prep_lane(wave, wave_lane(threadIdx.x));
+          } else if (wave.job == 2) {
+            if ((threadIdx.x >> 5) == 1) ((Driver*)drv_obj)->batch_lane(wave, threadIdx.x & 31);
           } else {
             // fused levels: each reads the previous one's tokens (named barrier between)
             const int hl = wave_lane(threadIdx.x);

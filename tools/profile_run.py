@@ -30,7 +30,7 @@ OPS = OPS + ["?%d" % k for k in range(len(OPS), 31)] + ["SMEM_MASK"]
 OPS += ["R_RUN_BODY", "R_NEW_INST", "R_PUBLISH", "R_RESOLVE", "R_DRAIN", "R_ADD_DEP", "R_PLACE",
         "R_PREP", "R_FLUSH_DW", "R_EVAL_LSTM_TC", "R_EVAL_HEAVY", "R_DRAIN_IO", "R_COMPLETE",
         "R_WAVE", "F_PREP_RESOLVE", "F_NEW_INST", "F_FIELDS", "F_ADD_DEPS", "F_OUT_SUBMIT",
-        "H_PLACES", "W_WAIT", "W_WAIT_DRAIN", "W_HELPER_BUSY(n=leftovers)"]
+        "H_PLACES", "W_WAIT", "W_WAIT_DRAIN", "W_HELPER_BUSY(n=leftovers)", "R_BATCH"]
 OPS = OPS + ["?%d" % k for k in range(len(OPS), 62)] + ["R_SWITCH_FAST", "?63"]
 
 
