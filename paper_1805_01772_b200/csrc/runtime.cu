@@ -810,6 +810,10 @@ struct Wave {
   int chain;              // routing wave followed by the preparation of node hd (same job)
   int nlev, lev_stop;     // fused levels; levels completed (set by the helpers)
   int lev_start[16], lev_n[16];
+  unsigned long long lev_ctx[16];   // cond contexts each level reads (evaluated by a helper lane
+                                    // before the level when the driver did not know them yet)
+  int cstop;              // level the helpers could not start (a context's predicate was not
+                          // available yet), or -1
   int hdead, hfail;
   int64_t houtp[8];
   int64_t hmap[5], hslot[5];
@@ -985,22 +989,29 @@ struct Driver {
       if (ctx_live(__ffsll((long long)m) - 1) < 0) return false;
     Wave& w = *wave_;
     int nlev = 0, q = pc;
+    // consecutive waves fuse into one job; a level reading cond contexts not known yet has them
+    // evaluated by a helper lane after the previous level (their predicates are computed by
+    // earlier levels of the same job); bit 25: no fusion, bit 31: stop at unknown contexts (A/B)
     while (true) {
       w.lev_start[nlev] = q + 1;
       w.lev_n[nlev] = bn_[q].aux[0];
+      w.lev_ctx[nlev] = (unsigned long long)bn_[q].imm[0];
       ++nlev;
       q += bn_[q].aux[0] + 1;
       if (nlev == kMaxLev || q >= F.n_body || bn_[q].op != OP_WAVE || (dbg_ & (1 << 25))) break;
-      bool known = true;   // bit 25: no fusion (A/B)
-      for (unsigned long long m = (unsigned long long)bn_[q].imm[0]; m && known; m &= m - 1) {
-        const int c = __ffsll((long long)m) - 1;
-        for (int x = c; x; x = ctxs_[x].parent)
-          if (lstamp_[x] != lgen_) known = false;
+      if (dbg_ & (1 << 31)) {
+        bool known = true;
+        for (unsigned long long m = (unsigned long long)bn_[q].imm[0]; m && known; m &= m - 1) {
+          const int c = __ffsll((long long)m) - 1;
+          for (int x = c; x; x = ctxs_[x].parent)
+            if (lstamp_[x] != lgen_) known = false;
+        }
+        if (!known) break;
       }
-      if (!known) break;
     }
     w.nlev = nlev;
     w.lev_stop = nlev;
+    w.cstop = -1;
     w.nslow = 0;
     // chain the preparation of the node after the last level when it is a tensor-core LSTM
     // node whose cond context is already known to be live (saves one helper round trip)
@@ -1047,7 +1058,8 @@ struct Driver {
     __threadfence_block();
     const int stop = w.lev_stop;   // levels completed (a level with leftovers ends the job)
     const int last = stop < nlev ? stop : nlev - 1;
-    const int end = w.lev_start[last] + w.lev_n[last];   // body position after that level
+    // a level the helpers could not start (context not known): resume at its marker
+    const int end = w.cstop > 0 ? w.lev_start[w.cstop] - 1 : w.lev_start[last] + w.lev_n[last];
     if (w.chain && w.nslow == 0 && stop == nlev) {   // wave_->hd prepared for this iteration
       chain_ok_ = true;
       chain_key_ = ((long long)(cur_frame + 1) << 32) | (unsigned)iter;
@@ -2210,6 +2222,7 @@ struct Driver {
     switch (kind) {
       case HK_EW: {
         int64_t n = d.imm[0];
+        if (d.aux[1] == EW_ADDN && d.n_in > 8) return eval_addn_chain(d, outp[0], odt);
         id = new_inst(HK_EW, d.aux[1], (int)((n + kEwBig - 1) / kEwBig));
         if (id < 0) return EV_ERROR;
         Inst& I = A.insts[id];
@@ -2279,6 +2292,46 @@ struct Driver {
     dep_all(id);
     set_out(d, 0, ptr_tok(outp[0], id, odt));
     submit(id);
+    return EV_OK;
+  }
+
+  // AddN of more than 8 terms (e.g. a weight gradient summed over a statically unrolled loop's
+  // steps): a chain of 8-input sums, each adding up to 7 more terms to the running sum in the
+  // output buffer (elementwise, in place)
+  __noinline__ __device__ int eval_addn_chain(const DNode& d, int64_t out, int odt) {
+    const int64_t n = d.imm[0];
+    int32_t prev = -1;
+    for (int j0 = 0; j0 < d.n_in;) {
+      const int first = j0 == 0 ? 0 : 1;
+      const int take = min(8 - first, d.n_in - j0);
+      const int32_t id = new_inst(HK_EW, EW_ADDN, (int)((n + kEwBig - 1) / kEwBig));
+      if (id < 0) return EV_ERROR;
+      Inst& I = A.insts[id];
+      I.n = n;
+      I.m = d.imm[1];
+      int k = 0;
+      int64_t dts = (int64_t)(odt & 15) << 32;
+      if (first) {
+        dts |= (int64_t)(odt & 15) << (4 * k);
+        I.p[k++] = out;
+      }
+      for (int q = 0; q < take; ++q) {
+        const Tok& t = in_tok(d, j0 + q);
+        dts |= (int64_t)(t.dt & 15) << (4 * k);
+        I.p[k++] = t.v;
+        add_dep(id, t.writer);
+      }
+      I.p[13] = out;
+      I.s[0] = k;
+      I.s[1] = 0;
+      I.s[2] = d.aux[3];
+      I.dts = dts;
+      add_dep(id, prev);
+      submit(id);
+      prev = id;
+      j0 += take;
+    }
+    set_out(d, 0, ptr_tok(out, prev, odt));
     return EV_OK;
   }
 
@@ -2971,6 +3024,17 @@ struct Driver {
     return lval_[c];
   }
 
+  // contexts of mask m for a fused wave level, evaluated by a helper lane between levels (the
+  // driver thread is waiting for the job): false when a predicate is not available yet
+  __noinline__ __device__ bool helper_ctx(unsigned long long m) {
+    for (; m; m &= m - 1) {
+      const int c = __ffsll((long long)m) - 1;
+      if (lstamp_[c] == lgen_) continue;
+      if (ctx_live(c) < 0) return false;
+    }
+    return true;
+  }
+
   // The per-iteration control loop: kept small and out of line so that its instructions stay
   // resident in the SM's instruction cache (the routing primitives dominate the node count).
   // The per-iteration control loop. Routing primitives are ~90% of the evaluations, so they
@@ -3292,7 +3356,7 @@ __device__ void worker_loop(const RunArgs& A) {
       case HK_LSTM_BWD_MM: tile_lstm_bwd_mm(I, tile, sm); break;
       case HK_PREP_WP: tile_prep_wp(I, tile); break;
       case HK_PREP_WT: tile_prep_wt(I, tile, (float*)dyn_smem); break;
-      case HK_LSTM_FWD_TC: tile_lstm_fwd_tc(I, tile, ts, tc_cnt, tc_cnt2, tc_tiles); break;
+      case HK_LSTM_FWD_TC: tile_lstm_fwd_tc(I, tile, ts, tc_cnt, tc_cnt2, tc_tiles, sm); break;
       case HK_LSTM_BWD_EW_BF: tile_lstm_bwd_ew_bf(I, tile, sm); break;
       case HK_LSTM_DXH_TC: tile_lstm_dxh_tc(I, tile, ts, tc_cnt, tc_cnt2, tc_tiles); break;
       case HK_LSTM_DW_TC: tile_lstm_dw_tc(I, tile, ts, tc_cnt, tc_cnt2, tc_tiles); break;
@@ -3488,12 +3552,18 @@ __global__ void __launch_bounds__(kThreads, 1) cf_driver_kernel(RunArgs A_param)
             const int hl = wave_lane(threadIdx.x);
             int k = 0;
             for (; k < wave.nlev; ++k) {
+              if (k > 0 && wave.lev_ctx[k]) {   // contexts of this level, known or evaluated now
+                if (hl == 0 && !((Driver*)drv_obj)->helper_ctx(wave.lev_ctx[k])) wave.cstop = k;
+                __threadfence_block();
+                asm volatile("bar.sync 1, %0;" ::"r"(32 * kWaveWarps) : "memory");
+                if (wave.cstop >= 0) break;
+              }
               wave_work(wave, wave.lev_start[k], wave.lev_n[k], hl, 32 * kWaveWarps);
               __threadfence_block();
               asm volatile("bar.sync 1, %0;" ::"r"(32 * kWaveWarps) : "memory");
               if (wave.nslow || wave.cnt.err) break;   // the driver evaluates the leftovers
             }
-            if (hl == 0) wave.lev_stop = k < wave.nlev ? k : wave.nlev;
+            if (hl == 0) wave.lev_stop = wave.cstop >= 0 ? wave.cstop : k < wave.nlev ? k : wave.nlev;
             if (k == wave.nlev && wave.chain)   // the next node's preparation
               ((Driver*)drv_obj)->heavy_prep_lane(wave, hl);
           }
@@ -4246,6 +4316,7 @@ cf_status cf_session_connect(cf_session* s, int32_t peer, const void* handle, in
 }
 
 int32_t cf_debug_set_flags(int32_t flags) {
+  if (cudaMemcpyToSymbol(kDbgFlagsTC, &flags, sizeof(flags)) != cudaSuccess) return CF_E_CUDA;
   return cudaMemcpyToSymbol(kDbgFlags, &flags, sizeof(flags)) == cudaSuccess ? CF_OK : CF_E_CUDA;
 }
 int32_t cf_debug_set_m2_rows(int32_t rows) {

@@ -92,7 +92,12 @@ struct Box {
   const CUtensorMap* map;
   int c0, c1, c2;
   int off;
+  int keep = 0;   // 1: L2 evict-last hint (operands re-read across tiles, e.g. the weights)
 };
+__device__ __forceinline__ void box_load(uint8_t* stage, const Box& b, uint64_t* bar) {
+  if (b.keep) tma_load_3d_hint(stage + b.off, b.map, bar, b.c0, b.c1, b.c2, kL2EvictLast);
+  else tma_load_3d(stage + b.off, b.map, bar, b.c0, b.c1, b.c2);
+}
 
 // Operand plan callbacks: fill up to 4 boxes for operand A / B of k-block kb; return count.
 // Run the K loop of one tile. `cnt` is the CTA-wide running k-block counter (same value in
@@ -115,11 +120,9 @@ __device__ inline void tc_tile(TcShared& s, int nk, int bn, int a_mn, int b_mn, 
       mbar_arrive_expect_tx(&s.full[st], kStageA + stage_b);
       Box bx[4];
       int na = plan_a(kb, bx);
-      for (int i = 0; i < na; ++i)
-        tma_load_3d(s.a[st] + bx[i].off, bx[i].map, &s.full[st], bx[i].c0, bx[i].c1, bx[i].c2);
+      for (int i = 0; i < na; ++i) box_load(s.a[st], bx[i], &s.full[st]);
       int nb = plan_b(kb, bx);
-      for (int i = 0; i < nb; ++i)
-        tma_load_3d(s.b[st] + bx[i].off, bx[i].map, &s.full[st], bx[i].c0, bx[i].c1, bx[i].c2);
+      for (int i = 0; i < nb; ++i) box_load(s.b[st], bx[i], &s.full[st]);
     }
     }
     __syncwarp();
@@ -171,11 +174,9 @@ __device__ inline void tc_tile2(TcShared& s, int nk, int a_mn, int b_mn, uint32_
         mbar_arrive_expect_tx(&s.full2[st], kStage2A + kStageBmax);
         Box bx[8];
         int na = plan_a(kb, bx);
-        for (int i = 0; i < na; ++i)
-          tma_load_3d(s.a2[st] + bx[i].off, bx[i].map, &s.full2[st], bx[i].c0, bx[i].c1, bx[i].c2);
+        for (int i = 0; i < na; ++i) box_load(s.a2[st], bx[i], &s.full2[st]);
         int nb = plan_b(kb, bx);
-        for (int i = 0; i < nb; ++i)
-          tma_load_3d(s.b2[st] + bx[i].off, bx[i].map, &s.full2[st], bx[i].c0, bx[i].c1, bx[i].c2);
+        for (int i = 0; i < nb; ++i) box_load(s.b2[st], bx[i], &s.full2[st]);
       }
     }
     __syncwarp();

@@ -182,3 +182,54 @@ def feeds_to_device(feeds, device="cuda", session=None):
         else:
             out[k] = torch.from_numpy(v.astype(np.int64)).to(device=device).contiguous()
     return out
+
+
+def static_rnn_lstm(T: int, B: int, I: int, H: int, L: int = 1, forget_bias: float = 0.0,
+                    with_grads: bool = True) -> RNNProgram:
+    """The same LSTM statically unrolled: no while_loop, no cond, T x L LSTMCell nodes in the
+    root context (§6.3 "Static vs. Dynamic": the paper
+    compares dynamic_rnn with a statically unrolled graph). Full-length sequences only. The loss
+    and the fetches are the dynamic program's (reading R11), so the two are checked against
+    each other value by value."""
+    g = Graph()
+    x = g.placeholder("x", F32, (T, B, I))
+    Ws, bs, hs, cs = {}, {}, [], []
+    for l in range(L):
+        il = I if l == 0 else H
+        Ws[l] = g.placeholder(f"W{l}", F32, (4 * H, il + H))
+        bs[l] = g.placeholder(f"b{l}", F32, (4 * H,))
+        hs.append(g.placeholder(f"h0_{l}", F32, (B, H)))
+        cs.append(g.placeholder(f"c0_{l}", F32, (B, H)))
+    h0 = list(hs)
+    c0 = list(cs)
+    x_ta = g.tensor_array(T, F32, (B, I)).unstack(x)
+    out_ta = g.tensor_array(T, F32, (B, H))
+    for t in range(T):
+        inp = x_ta.read(g.const(t, I64))
+        for l in range(L):
+            hn, cn, o, _g = g.op("LSTMCell", [inp, hs[l], cs[l], Ws[l], bs[l]],
+                                 {"masked": False, "forget_bias": forget_bias})
+            hs[l], cs[l], inp = hn, cn, o
+        out_ta = out_ta.write(g.const(t, I64), inp)
+    out_top = out_ta.stack()
+    R_out = g.placeholder("R_out", F32, (T, B, H))
+    y = g.op1("ReduceSum", [g.op1("Mul", [R_out, out_top])])
+    fetch = {}
+    for l in range(L):
+        Rh = g.placeholder(f"R_h{l}", F32, (B, H))
+        Rc = g.placeholder(f"R_c{l}", F32, (B, H))
+        y = g.op1("Add", [y, g.op1("Add", [g.op1("ReduceSum", [g.op1("Mul", [Rh, hs[l]])]),
+                                           g.op1("ReduceSum", [g.op1("Mul", [Rc, cs[l]])])])])
+    fetch = {"y": y, "out": out_top}
+    for l in range(L):
+        fetch[f"hT{l}"] = hs[l]
+        fetch[f"cT{l}"] = cs[l]
+    grads = {}
+    if with_grads:
+        names, xs = ["x"], [x]
+        for l in range(L):
+            names += [f"W{l}", f"b{l}", f"h0_{l}", f"c0_{l}"]
+            xs += [Ws[l], bs[l], h0[l], c0[l]]
+        for nm, gt in zip(names, g.gradients(y, xs)):
+            grads["d" + nm] = gt
+    return RNNProgram(g, fetch, grads, T, B, I, H, L)
