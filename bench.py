@@ -204,9 +204,10 @@ def main():
                          "host memory (0 = no swapping, 1 = swap every eligible value)")
     ap.add_argument("--swap-smallest-first", action="store_true",
                     help="with --stack-budget: swap the smallest stacked values first")
-    ap.add_argument("--parallel", default="pipeline", choices=["pipeline", "replicas"],
-                    help="N>1: layer-partitioned pipeline (strong scaling, SURVEY.md a14) or "
-                         "independent replicas (weak scaling)")
+    ap.add_argument("--parallel", default="pipeline", choices=["pipeline", "dp", "replicas"],
+                    help="N>1: layer-partitioned pipeline (strong scaling, SURVEY.md a14), batch "
+                         "data parallelism with the in-graph weight-gradient allreduce (weak "
+                         "scaling, f3), or independent replicas (weak scaling, no exchange)")
     args = ap.parse_args()
     c = CONFIGS[args.config]
     if args.impl == "reference":
@@ -247,19 +248,21 @@ def main():
     if pipe and world > c["L"]:
         raise SystemExit(f"pipeline over {world} GPUs needs >= {world} layers")
     stage = (rank, world) if pipe else None
-    p = dynamic_rnn_lstm(c["T"], c["B"], c["I"], c["H"], c["L"], stage=stage, **model_kw(c))
+    dp = (rank, world) if world > 1 and args.parallel == "dp" else None
+    p = dynamic_rnn_lstm(c["T"], c["B"], c["I"], c["H"], c["L"], stage=stage, dp=dp, **model_kw(c))
     # a dedicated stream, current for torch too: the input copies of the end-to-end loop and
     # the cf_run launches are ordered on it
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     sess = cf.Session(p.g, p.fetch_tensors(), precision=prec, parallel_iterations=args.K,
                       device=local, stream=stream.cuda_stream,
-                      watchdog_ms=300000 if pipe else 0, stack_budget_bytes=args.stack_budget,
+                      watchdog_ms=300000 if (pipe or dp) else 0, stack_budget_bytes=args.stack_budget,
                       swap_smallest_first=args.swap_smallest_first)
-    if pipe:
+    if pipe or dp:
         sess.connect_pipeline()
-    # pipeline: one model split over the ranks (same inputs everywhere); replicas: own inputs
-    f = rnn_inputs(c["T"], c["B"], c["I"], c["H"], c["L"], seed=0 if pipe else rank,
+    # pipeline: one model split over the ranks (same inputs everywhere); dp: the same weights
+    # (and, for timing, the same batch) on every rank; replicas: own inputs
+    f = rnn_inputs(c["T"], c["B"], c["I"], c["H"], c["L"], seed=0 if (pipe or dp) else rank,
                    moe=c.get("moe", False),
                    len_mode=c["len_mode"], bf16=prec == cf.BF16)
     lens_sum = int(f["len"].sum())
@@ -393,8 +396,8 @@ def main():
         "data": "synthetic (seeded; synth.rnn_inputs)",
         "config": {"workload": args.config, **{k: c[k] for k in ("T", "B", "I", "H", "L")},
                    "lengths": c["len_mode"], "parallel_iterations": args.K or 32,
-                   "parallelism": (f"layer-pipeline{world}" if pipe else f"replicas{world}")
-                   if world > 1 else "single",
+                   "parallelism": (f"layer-pipeline{world}" if pipe else f"dp{world}" if dp
+                                   else f"replicas{world}") if world > 1 else "single",
                    "l2": "inputs/activations > L2 (no flush needed)"},
         "loop_iterations_per_s": c["T"] / (ms * 1e-3),
         "kernel_ms": kms,

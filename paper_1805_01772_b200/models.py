@@ -50,7 +50,7 @@ def layer_partition(L: int, world: int, rank: int):
 
 def dynamic_rnn_lstm(T: int, B: int, I: int, H: int, L: int = 1, parallel_iterations: int = 32,
                      length_conds: bool = True, moe: bool = False, forget_bias: float = 0.0,
-                     with_grads: bool = True, stage=None, moe_act: str = "relu") -> RNNProgram:
+                     with_grads: bool = True, stage=None, moe_act: str = "relu", dp=None) -> RNNProgram:
     """The full model, or with ``stage=(rank, world)`` the partition of layer-pipeline stage
     `rank`: a later stage Recvs its layer input from
     the previous stage and a non-final stage Sends its top output on, inside the loop, every
@@ -158,7 +158,52 @@ def dynamic_rnn_lstm(T: int, B: int, I: int, H: int, L: int = 1, parallel_iterat
                 xs += [WA[l], WB[l]]
         for nm, gt in zip(names, g.gradients(y, xs)):
             grads["d" + nm] = gt
+        if dp is not None and dp[1] > 1:
+            grads = _allreduce_weight_grads(g, grads, *dp)
     return RNNProgram(g, fetch, grads, T, B, I, H, L)
+
+
+def _allreduce_weight_grads(g: Graph, grads: Dict[str, Tensor], rank: int, world: int):
+    """Batch data parallelism: every rank runs the whole model on its own
+    batch shard; the weight gradients (W, b and the experts') are summed over the ranks. The
+    loss is a sum over samples, so the sum of the shards' gradients is the full batch's.
+    In-graph, at the root: each rank Sends its gradient to every other rank (NVLink peer
+    stores, PAPER.md:780-829 Send/Recv) and adds what it receives (AddN). The Send of a layer's
+    gradient depends only on that layer's last dW chunk, so the exchange of the upper layers
+    (whose backward finishes first) overlaps the lower layers' backward. Channel id =
+    (tensor * world + sender) * world + receiver."""
+    zero = g.const(0, I64)
+    out = dict(grads)
+    k = 0
+    for nm, gt in grads.items():
+        if not nm.startswith(("dW", "db", "dWA", "dWB")):
+            continue   # dx, dh0, dc0 are per-sample: nothing to sum
+        peers = [p for p in range(world) if p != rank]
+        for p in peers:
+            g.send(gt, zero, (k * world + rank) * world + p, p)
+        terms = [gt] + [g.recv(zero, (k * world + p) * world + rank, p, gt.dtype, gt.shape)
+                        for p in peers]
+        out[nm] = g.op1("AddN", terms)
+        k += 1
+    return out
+
+
+def shard_inputs(feeds, rank: int, world: int):
+    """Rows [rank * B / world, (rank + 1) * B / world) of every per-sample input of a batch
+    (x, R_out: axis 1; len, h0, c0, R_h, R_c: axis 0); weights are shared."""
+    import numpy as np
+    out = {}
+    for k, v in feeds.items():
+        v = np.asarray(v)
+        if k in ("x", "R_out"):
+            b = v.shape[1] // world
+            out[k] = v[:, rank * b:(rank + 1) * b]
+        elif k == "len" or k.startswith(("h0_", "c0_", "R_h", "R_c")):
+            b = v.shape[0] // world
+            out[k] = v[rank * b:(rank + 1) * b]
+        else:
+            out[k] = v
+    return out
 
 
 def feeds_to_device(feeds, device="cuda", session=None):

@@ -19,9 +19,11 @@ def test_trivial_loop_closed_form(n, width, K):
     assert r["closed_form_ok"], r
 
 
-def test_ring_exchange_two_gpus():
+@pytest.mark.parametrize("barrier", [False, True])
+def test_exchange_two_gpus(barrier):
     """Each iteration Sends the loop value to the next rank and Recvs the previous rank's
-    (PAPER.md:780-829); closed form a == n on every rank, K 1 and 8."""
+    (PAPER.md:780-829), or (barrier) exchanges it with every rank and averages (the paper's
+    loop "with a barrier"); closed form a == n on every rank, K 1 and 8."""
     import json
     import subprocess
 
@@ -32,7 +34,7 @@ def test_ring_exchange_two_gpus():
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", "29517",
            os.path.join(root, "tools", "control_overhead_mgpu.py"),
-           "--iters", "1", "300", "--K", "1", "8", "--reps", "1"]
+           "--iters", "1", "300", "--K", "1", "8", "--reps", "1"] + (["--barrier"] if barrier else [])
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=240, cwd=root)
     assert out.returncode == 0, out.stderr[-2000:]
     rows = [json.loads(l) for l in out.stdout.splitlines() if l.startswith("{")]

@@ -9,6 +9,12 @@ rank therefore waits for iteration t of its neighbour; a chain of them is the ba
 Loop on rank r: i = 0; a = 0; while i < n: i += 1; a = recv(i, from r-1) + 1, send(a, to r+1).
 Closed form: a == n elementwise on every rank (checked every run).
 
+--barrier: the per-iteration exchange is all-to-all instead (the paper's "with a barrier",
+P:1253-1255): every rank Sends a to every other rank and the new value is the average of all
+ranks' values plus one, a = (a + sum_p recv_p(a)) / N + 1, so iteration t on any rank waits
+for iteration t of EVERY rank (a barrier plus an allreduce of the loop value). Closed form:
+a == n on every rank.
+
     python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 \
         --master-port 29511 tools/control_overhead_mgpu.py [--iters 10000] [--K 1 32]
 Without torchrun: one rank, no exchange (the 1-GPU loop of tools/control_overhead.py).
@@ -26,7 +32,7 @@ import torch.distributed as dist  # noqa: E402
 from paper_1805_01772_b200 import cf  # noqa: E402
 
 
-def build(rank: int, world: int, width: int):
+def build(rank: int, world: int, width: int, barrier: bool = False):
     g = cf.Graph()
     n = g.placeholder("n", cf.I64, ())
     a0 = g.placeholder("a0", cf.F32, (width,))
@@ -34,7 +40,15 @@ def build(rank: int, world: int, width: int):
     prev, nxt = (rank - 1) % world, (rank + 1) % world
 
     def body(i, a):
-        if world > 1:
+        if world > 1 and barrier:
+            peers = [p for p in range(world) if p != rank]
+            for p in peers:                               # channel = sender * N + receiver
+                g.send(a, i, rank * world + p, p)
+            s = a
+            for p in peers:
+                s = g.op1("Add", [s, g.recv(i, p * world + rank, p, cf.F32, (width,))])
+            a = g.op1("Add", [g.op1("Mul", [s, g.const(1.0 / world, cf.F32)]), g.const(1.0, cf.F32)])
+        elif world > 1:
             g.send(a, i, rank, nxt)                       # channel = sender's rank
             a = g.op1("Add", [g.recv(i, prev, prev, cf.F32, (width,)), g.const(1.0, cf.F32)])
         else:
@@ -52,6 +66,7 @@ def main():
     ap.add_argument("--width", type=int, default=1)
     ap.add_argument("--K", type=int, nargs="+", default=[1, 32])
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--barrier", action="store_true", help="all-to-all exchange every iteration")
     a = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -62,7 +77,7 @@ def main():
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     for K in a.K:
-        g, fetches = build(rank, world, a.width)
+        g, fetches = build(rank, world, a.width, a.barrier)
         nmax = max(a.iters)
         s = cf.Session(g, fetches, precision=cf.F32, parallel_iterations=K, device=local,
                        stream=stream.cuda_stream, max_iterations=nmax + 16, watchdog_ms=120000)
@@ -93,7 +108,8 @@ def main():
             if rank == 0:
                 ms = float(t[0])
                 print(json.dumps({"n_gpus": world, "n": n, "width": a.width,
-                                  "parallel_iterations": K, "exchange": world > 1,
+                                  "parallel_iterations": K,
+                                  "exchange": ("all-to-all barrier" if a.barrier else "ring") if world > 1 else None,
                                   "ms_median_max_over_ranks": ms,
                                   "iterations_per_s": n / (ms * 1e-3),
                                   "us_per_iteration": ms * 1e3 / n,
