@@ -194,6 +194,8 @@ def main():
     ap.add_argument("--config", default="cfg3", choices=list(CONFIGS))
     ap.add_argument("--precision", default="bf16", choices=["f32", "bf16"])
     ap.add_argument("--K", type=int, default=0, help="parallel_iterations override (0 = 32)")
+    ap.add_argument("--T", type=int, default=0, help="override the config's sequence length")
+    ap.add_argument("--watchdog-ms", type=int, default=0, help="device watchdog (0: 300 s multi-GPU)")
     ap.add_argument("--ref-T", type=int, default=8)
     ap.add_argument("--steps-ref", type=int, default=3)
     ap.add_argument("--warmup-ref", type=int, default=0)
@@ -209,7 +211,9 @@ def main():
                          "data parallelism with the in-graph weight-gradient allreduce (weak "
                          "scaling, f3), or independent replicas (weak scaling, no exchange)")
     args = ap.parse_args()
-    c = CONFIGS[args.config]
+    c = dict(CONFIGS[args.config])
+    if args.T:
+        c["T"] = args.T
     if args.impl == "reference":
         return run_reference(args, c, args.config)
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
@@ -256,7 +260,7 @@ def main():
     torch.cuda.set_stream(stream)
     sess = cf.Session(p.g, p.fetch_tensors(), precision=prec, parallel_iterations=args.K,
                       device=local, stream=stream.cuda_stream,
-                      watchdog_ms=300000 if (pipe or dp) else 0, stack_budget_bytes=args.stack_budget,
+                      watchdog_ms=args.watchdog_ms or (300000 if (pipe or dp) else 0), stack_budget_bytes=args.stack_budget,
                       swap_smallest_first=args.swap_smallest_first)
     if pipe or dp:
         sess.connect_pipeline()

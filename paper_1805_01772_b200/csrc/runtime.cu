@@ -1747,7 +1747,7 @@ struct Driver {
                !resolve(ip(1), (int)B, (int)H, 2, &mhn, &shn, hint + 4)) {
       return EV_ERROR;
     }
-    int32_t e = new_inst(HK_LSTM_BWD_EW_BF, masked, (int)(((B + 127) / 128) * (H / 64)));
+    int32_t e = new_inst(HK_LSTM_BWD_EW_BF, masked, (int)(((B + 127) / 128) * ((H + kEwUnits - 1) / kEwUnits)));
     if (e < 0) return EV_ERROR;
     const bool m2 = B >= kM2MinRows;
     int32_t x = new_inst(HK_LSTM_DXH_TC, masked | (m2 ? 2 : 0),
@@ -1878,7 +1878,7 @@ struct Driver {
           id[2] = reserve_inst(HK_LSTM_DW_TC, (int)((4 * H / 256) * (KT / 256) + (4 * H + 255) / 256));
           last_flush = id[2];
         }
-        id[0] = reserve_inst(HK_LSTM_BWD_EW_BF, (int)(((B + 127) / 128) * (H / 64)));
+        id[0] = reserve_inst(HK_LSTM_BWD_EW_BF, (int)(((B + 127) / 128) * ((H + kEwUnits - 1) / kEwUnits)));
         id[1] = reserve_inst(HK_LSTM_DXH_TC, (int)((m2 ? (B + 255) / 256 : (B + 127) / 128) * (KT / 256)));
       }
       (void)masked;
@@ -2017,7 +2017,7 @@ struct Driver {
         !resolve_core(ip(1), (int)B, (int)H, 2, &mhn, &shn, hint + 4))
       return false;
     const int32_t e = id[0], x = id[1];
-    inst_header(e, HK_LSTM_BWD_EW_BF, masked, (int)(((B + 127) / 128) * (H / 64)));
+    inst_header(e, HK_LSTM_BWD_EW_BF, masked, (int)(((B + 127) / 128) * ((H + kEwUnits - 1) / kEwUnits)));
     inst_header(x, HK_LSTM_DXH_TC, masked | (m2 ? 2 : 0),
                 (int)((m2 ? (B + 255) / 256 : (B + 127) / 128) * (KT / 256)));
     {

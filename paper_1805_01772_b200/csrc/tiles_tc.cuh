@@ -244,12 +244,16 @@ __device__ __forceinline__ void bf4(const __nv_bfloat16* p, float* o) {
   const float2 fa = __bfloat1622float2(a), fb = __bfloat1622float2(b);
   o[0] = fa.x; o[1] = fa.y; o[2] = fb.x; o[3] = fb.y;
 }
+// tile = 128 rows x 256 units (4 gate-interleaved 64-unit slices): few large tiles amortise
+// the per-tile claim / record / completion cost; each thread keeps 4 rows' operands in flight
+constexpr int kEwUnits = 256;
 __device__ void tile_lstm_bwd_ew_bf(const Inst& I, int tile, float* sm) {
   const int B = (int)I.m, H = (int)I.n;
-  const int tu = H / 64;
-  const int rt = tile / tu, ut = tile % tu;
-  const int ul = (threadIdx.x % 16) * 4;          // unit within the 64-unit slice
-  const int u = ut * 64 + ul, rg = threadIdx.x / 16;
+  const int tu = (H + kEwUnits - 1) / kEwUnits;
+  const int rt = tile / tu, ut0 = (tile % tu) * (kEwUnits / 64);   // first 64-unit slice
+  const int nsl = min(kEwUnits / 64, H / 64 - ut0);
+  const int ul = (threadIdx.x % 16) * 4;          // unit within a 64-unit slice
+  const int rg = threadIdx.x / 16;
   const float* c_prev = (const float*)I.p[2];
   const __nv_bfloat16* gates = (const __nv_bfloat16*)I.p[4];
   const int64_t* lens = (const int64_t*)I.p[5];
@@ -264,85 +268,94 @@ __device__ void tile_lstm_bwd_ew_bf(const Inst& I, int tile, float* sm) {
   float* partial = (float*)(I.p[10] + I.s[5]);
   const bool masked = I.sub & 1;
   const int64_t t = I.s[0];
-  float sdb[4][4] = {};
   const int nrow = min(128, B - rt * 128);
-  // 4 rows' operands in flight at a time (the tile is load-latency bound; all 8 measured
-  // slower: 15.3 vs 11.8 us per tile): rows past the batch read row 0 and store nothing
-#pragma unroll 4
+  bool live_r[8];
+#pragma unroll
   for (int i = 0; i < 8; ++i) {
     const int rr = rg + 16 * i;
-    const bool valid = rr < nrow;
-    const int r = rt * 128 + (valid ? rr : 0);
-    const int64_t e = (int64_t)r * H + u;
-    const __nv_bfloat16* gr = gates + (int64_t)r * 4 * H + ut * 256 + ul;
-    float ig[4], fg[4], gg[4], og[4];
-    bf4(gr, ig);
-    bf4(gr + 64, fg);
-    bf4(gr + 128, gg);
-    bf4(gr + 192, og);
-    const float4 cp = ld4f(c_prev + e), dn = ld4f(dhn + e), dcv = ld4f(dcn + e);
-    float dov[4];
-    if (dout_bf) bf4((const __nv_bfloat16*)dout + e, dov);
-    else {
-      const float4 d4 = ld4f((const float*)dout + e);
-      dov[0] = d4.x; dov[1] = d4.y; dov[2] = d4.z; dov[3] = d4.w;
-    }
-    float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0;
-    if (add0) a0 = ld4f(add0 + e);   // folded AddN terms
-    if (add1) a1 = ld4f(add1 + e);
-    const bool live = !masked || t < lens[r];
-    const float cpa[4] = {cp.x, cp.y, cp.z, cp.w};
-    const float dna[4] = {dn.x + a0.x + a1.x, dn.y + a0.y + a1.y, dn.z + a0.z + a1.z, dn.w + a0.w + a1.w};
-    const float dca[4] = {dcv.x, dcv.y, dcv.z, dcv.w};
-    float zf[4][4];
-    float dco[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const float cn = fg[k] * cpa[k] + ig[k] * gg[k];
-      const float tc_ = tanhf(cn);
-      const float dh = dna[k] + dov[k];
-      const float dcs = dh * og[k] * (1.0f - tc_ * tc_) + dca[k];
-      zf[0][k] = dcs * gg[k] * ig[k] * (1.0f - ig[k]);
-      zf[1][k] = dcs * cpa[k] * fg[k] * (1.0f - fg[k]);
-      zf[2][k] = dcs * ig[k] * (1.0f - gg[k] * gg[k]);
-      zf[3][k] = dh * tc_ * og[k] * (1.0f - og[k]);
-      dco[k] = dcs * fg[k];
-      if (!live) {
-        zf[0][k] = zf[1][k] = zf[2][k] = zf[3][k] = 0.0f;
-        dco[k] = dca[k];
+    live_r[i] = !masked || (rr < nrow && t < lens[rt * 128 + rr]);
+  }
+  for (int sl = 0; sl < nsl; ++sl) {
+    const int ut = ut0 + sl;
+    const int u = ut * 64 + ul;
+    float sdb[4][4] = {};
+    // rows past the batch read row 0 and store nothing
+#pragma unroll 4
+    for (int i = 0; i < 8; ++i) {
+      const int rr = rg + 16 * i;
+      const bool valid = rr < nrow;
+      const int r = rt * 128 + (valid ? rr : 0);
+      const int64_t e = (int64_t)r * H + u;
+      const __nv_bfloat16* gr = gates + (int64_t)r * 4 * H + ut * 256 + ul;
+      float ig[4], fg[4], gg[4], og[4];
+      bf4(gr, ig);
+      bf4(gr + 64, fg);
+      bf4(gr + 128, gg);
+      bf4(gr + 192, og);
+      const float4 cp = ld4f(c_prev + e), dn = ld4f(dhn + e), dcv = ld4f(dcn + e);
+      float dov[4];
+      if (dout_bf) bf4((const __nv_bfloat16*)dout + e, dov);
+      else {
+        const float4 d4 = ld4f((const float*)dout + e);
+        dov[0] = d4.x; dov[1] = d4.y; dov[2] = d4.z; dov[3] = d4.w;
       }
+      float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0;
+      if (add0) a0 = ld4f(add0 + e);   // folded AddN terms
+      if (add1) a1 = ld4f(add1 + e);
+      const bool live = live_r[i];
+      const float cpa[4] = {cp.x, cp.y, cp.z, cp.w};
+      const float dna[4] = {dn.x + a0.x + a1.x, dn.y + a0.y + a1.y, dn.z + a0.z + a1.z, dn.w + a0.w + a1.w};
+      const float dca[4] = {dcv.x, dcv.y, dcv.z, dcv.w};
+      float zf[4][4];
+      float dco[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float cn = fg[k] * cpa[k] + ig[k] * gg[k];
+        const float tc_ = tanhf(cn);
+        const float dh = dna[k] + dov[k];
+        const float dcs = dh * og[k] * (1.0f - tc_ * tc_) + dca[k];
+        zf[0][k] = dcs * gg[k] * ig[k] * (1.0f - ig[k]);
+        zf[1][k] = dcs * cpa[k] * fg[k] * (1.0f - fg[k]);
+        zf[2][k] = dcs * ig[k] * (1.0f - gg[k] * gg[k]);
+        zf[3][k] = dh * tc_ * og[k] * (1.0f - og[k]);
+        dco[k] = dcs * fg[k];
+        if (!live) {
+          zf[0][k] = zf[1][k] = zf[2][k] = zf[3][k] = 0.0f;
+          dco[k] = dca[k];
+        }
+      }
+      if (!valid) continue;
+      __nv_bfloat16* zr = dz + (int64_t)r * 4 * H + u;
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        const __nv_bfloat162 lo = __floats2bfloat162_rn(zf[g][0], zf[g][1]);
+        const __nv_bfloat162 hi = __floats2bfloat162_rn(zf[g][2], zf[g][3]);
+        // db sums the bf16-rounded dz, exactly what the dW GEMM consumes
+        sdb[g][0] += __low2float(lo);
+        sdb[g][1] += __high2float(lo);
+        sdb[g][2] += __low2float(hi);
+        sdb[g][3] += __high2float(hi);
+        uint2 pk;
+        pk.x = *(const uint32_t*)&lo;
+        pk.y = *(const uint32_t*)&hi;
+        *(uint2*)(zr + (int64_t)g * H) = pk;
+      }
+      *(float4*)(dc + e) = make_float4(dco[0], dco[1], dco[2], dco[3]);
     }
-    if (!valid) continue;
-    __nv_bfloat16* zr = dz + (int64_t)r * 4 * H + u;
+    // reduce the 16 row groups of this slice: sm[rg][g][64]
 #pragma unroll
-    for (int g = 0; g < 4; ++g) {
-      const __nv_bfloat162 lo = __floats2bfloat162_rn(zf[g][0], zf[g][1]);
-      const __nv_bfloat162 hi = __floats2bfloat162_rn(zf[g][2], zf[g][3]);
-      // db sums the bf16-rounded dz, exactly what the dW GEMM consumes
-      sdb[g][0] += __low2float(lo);
-      sdb[g][1] += __high2float(lo);
-      sdb[g][2] += __low2float(hi);
-      sdb[g][3] += __high2float(hi);
-      uint2 pk;
-      pk.x = *(const uint32_t*)&lo;
-      pk.y = *(const uint32_t*)&hi;
-      *(uint2*)(zr + (int64_t)g * H) = pk;
+    for (int g = 0; g < 4; ++g)
+      *(float4*)&sm[(rg * 4 + g) * 64 + ul] = make_float4(sdb[g][0], sdb[g][1], sdb[g][2], sdb[g][3]);
+    __syncthreads();
+    {
+      const int g = threadIdx.x / 64, uu = threadIdx.x % 64;   // 256 threads = 4 gates x 64 units
+      float acc = 0.f;
+#pragma unroll
+      for (int q = 0; q < 16; ++q) acc += sm[(q * 4 + g) * 64 + uu];
+      partial[(int64_t)rt * 4 * H + g * H + ut * 64 + uu] = acc;
     }
-    *(float4*)(dc + e) = make_float4(dco[0], dco[1], dco[2], dco[3]);
+    __syncthreads();
   }
-  // reduce the 16 row groups: sm[rg][g][64]
-#pragma unroll
-  for (int g = 0; g < 4; ++g)
-    *(float4*)&sm[(rg * 4 + g) * 64 + ul] = make_float4(sdb[g][0], sdb[g][1], sdb[g][2], sdb[g][3]);
-  __syncthreads();
-  {
-    const int g = threadIdx.x / 64, uu = threadIdx.x % 64;   // 256 threads = 4 gates x 64 units
-    float acc = 0.f;
-#pragma unroll
-    for (int q = 0; q < 16; ++q) acc += sm[(q * 4 + g) * 64 + uu];
-    partial[(int64_t)rt * 4 * H + g * H + ut * 64 + uu] = acc;
-  }
-  __syncthreads();
 }
 
 // ---------------------------------------------------------------- backward d[x,h]

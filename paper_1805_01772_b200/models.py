@@ -188,24 +188,6 @@ def _allreduce_weight_grads(g: Graph, grads: Dict[str, Tensor], rank: int, world
     return out
 
 
-def shard_inputs(feeds, rank: int, world: int):
-    """Rows [rank * B / world, (rank + 1) * B / world) of every per-sample input of a batch
-    (x, R_out: axis 1; len, h0, c0, R_h, R_c: axis 0); weights are shared."""
-    import numpy as np
-    out = {}
-    for k, v in feeds.items():
-        v = np.asarray(v)
-        if k in ("x", "R_out"):
-            b = v.shape[1] // world
-            out[k] = v[:, rank * b:(rank + 1) * b]
-        elif k == "len" or k.startswith(("h0_", "c0_", "R_h", "R_c")):
-            b = v.shape[0] // world
-            out[k] = v[rank * b:(rank + 1) * b]
-        else:
-            out[k] = v
-    return out
-
-
 def feeds_to_device(feeds, device="cuda", session=None):
     """numpy feeds (synth.rnn_inputs) -> contiguous CUDA tensors in the session's feed dtypes
     (bf16 for the LSTM GEMM operands on the CF_BF16 path, fp32 / int64 / bool otherwise)."""

@@ -73,3 +73,21 @@ def rnn_inputs(T: int, B: int, I: int, H: int, L: int = 1, seed: int = 0,
             if v.dtype == np.float64:
                 f[name] = round_bf16(v)
     return f
+
+
+def shard_inputs(feeds: Dict[str, np.ndarray], rank: int, world: int) -> Dict[str, np.ndarray]:
+    """Batch shard `rank` of `world` (batch data parallelism): rows [rank * B / world,
+    (rank + 1) * B / world) of every per-sample input (x, R_out: axis 1; len, h0, c0, R_h,
+    R_c: axis 0); the weights are shared. Pure slicing."""
+    out = {}
+    for k, v in feeds.items():
+        v = np.asarray(v)
+        if k in ("x", "R_out"):
+            b = v.shape[1] // world
+            out[k] = v[:, rank * b:(rank + 1) * b]
+        elif k == "len" or k.startswith(("h0_", "c0_", "R_h", "R_c")):
+            b = v.shape[0] // world
+            out[k] = v[rank * b:(rank + 1) * b]
+        else:
+            out[k] = v
+    return out

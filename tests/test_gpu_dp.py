@@ -28,7 +28,8 @@ def _worker(rank, world, port, cfg, outdir):
     import torch.distributed as dist
 
     from paper_1805_01772_b200 import cf
-    from paper_1805_01772_b200.models import dynamic_rnn_lstm, feeds_to_device, shard_inputs
+    from paper_1805_01772_b200.models import dynamic_rnn_lstm, feeds_to_device
+    from synth import shard_inputs
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
