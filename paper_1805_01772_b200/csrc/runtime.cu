@@ -1751,7 +1751,7 @@ struct Driver {
     if (e < 0) return EV_ERROR;
     const bool m2 = B >= kM2MinRows;
     int32_t x = new_inst(HK_LSTM_DXH_TC, masked | (m2 ? 2 : 0),
-                         (int)((m2 ? (B + 255) / 256 : (B + 127) / 128) * (KT / 256)));
+                         (int)((m2 ? (B + 255) / 256 : (B + 127) / 128) * (m2 ? KT / kDxhN2 : KT / 256)));
     if (x < 0) return EV_ERROR;
     if (early) {
       set_out(d, 0, ptr_tok(outp[0], x, D_F32));
@@ -1879,7 +1879,7 @@ struct Driver {
           last_flush = id[2];
         }
         id[0] = reserve_inst(HK_LSTM_BWD_EW_BF, (int)(((B + 127) / 128) * ((H + kEwUnits - 1) / kEwUnits)));
-        id[1] = reserve_inst(HK_LSTM_DXH_TC, (int)((m2 ? (B + 255) / 256 : (B + 127) / 128) * (KT / 256)));
+        id[1] = reserve_inst(HK_LSTM_DXH_TC, (int)((m2 ? (B + 255) / 256 : (B + 127) / 128) * (m2 ? KT / kDxhN2 : KT / 256)));
       }
       (void)masked;
       if (st->error) return n + 1;
@@ -2019,7 +2019,7 @@ struct Driver {
     const int32_t e = id[0], x = id[1];
     inst_header(e, HK_LSTM_BWD_EW_BF, masked, (int)(((B + 127) / 128) * ((H + kEwUnits - 1) / kEwUnits)));
     inst_header(x, HK_LSTM_DXH_TC, masked | (m2 ? 2 : 0),
-                (int)((m2 ? (B + 255) / 256 : (B + 127) / 128) * (KT / 256)));
+                (int)((m2 ? (B + 255) / 256 : (B + 127) / 128) * (m2 ? KT / kDxhN2 : KT / 256)));
     {
       Inst& I = A.insts[e];
       I.m = B; I.k = In; I.n = H;

@@ -156,13 +156,13 @@ __device__ inline void tc_tile(TcShared& s, int nk, int bn, int a_mn, int b_mn, 
   tc_fence_after();
 }
 
-// 256-row tile: rows [0,128) accumulate in TMEM columns [0,256), rows [128,256) in [256,512);
-// both MMAs of a k16 step read the same B stage. Plans fill A boxes at offsets within the
+// 256-row tile: rows [0,128) accumulate in TMEM columns [0,bn), rows [128,256) in [256,256+bn);
+// both MMAs of a k16 step read the same B stage (bn = 256 or 128 columns). Plans fill A boxes at offsets within the
 // 32 KiB A region (rows 128.. at +16 KiB) and B boxes as in tc_tile. Own barriers and k-block
 // counter (cnt2); the done barrier / tile counter are shared with tc_tile.
 template <class PlanA, class PlanB>
 __device__ inline void tc_tile2(TcShared& s, int nk, int a_mn, int b_mn, uint32_t& cnt2,
-                                uint32_t& tiles, PlanA plan_a, PlanB plan_b) {
+                                uint32_t& tiles, PlanA plan_a, PlanB plan_b, int bn = 256) {
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   if (warp == 0) {
     if (lane == 0) {
@@ -171,7 +171,7 @@ __device__ inline void tc_tile2(TcShared& s, int nk, int a_mn, int b_mn, uint32_
         const int st = c % kStages2;
         const uint32_t round = c / kStages2;
         mbar_wait(&s.empty2[st], (round & 1) ^ 1);
-        mbar_arrive_expect_tx(&s.full2[st], kStage2A + kStageBmax);
+        mbar_arrive_expect_tx(&s.full2[st], kStage2A + (uint32_t)bn * BK * 2);
         Box bx[8];
         int na = plan_a(kb, bx);
         for (int i = 0; i < na; ++i) box_load(s.a2[st], bx[i], &s.full2[st]);
@@ -182,7 +182,7 @@ __device__ inline void tc_tile2(TcShared& s, int nk, int a_mn, int b_mn, uint32_
     __syncwarp();
   } else if (warp == 1) {
     if (lane == 0) {
-      const uint32_t idesc = idesc_bf16(BM, 256, a_mn, b_mn);
+      const uint32_t idesc = idesc_bf16(BM, bn, a_mn, b_mn);
       const uint32_t tmem = *s.tmem_slot;
       uint32_t c = cnt2;
       for (int kb = 0; kb < nk; ++kb, ++c) {

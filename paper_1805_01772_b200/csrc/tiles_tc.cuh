@@ -244,9 +244,10 @@ __device__ __forceinline__ void bf4(const __nv_bfloat16* p, float* o) {
   const float2 fa = __bfloat1622float2(a), fb = __bfloat1622float2(b);
   o[0] = fa.x; o[1] = fa.y; o[2] = fb.x; o[3] = fb.y;
 }
-// tile = 128 rows x 256 units (4 gate-interleaved 64-unit slices): few large tiles amortise
-// the per-tile claim / record / completion cost; each thread keeps 4 rows' operands in flight
-constexpr int kEwUnits = 256;
+// tile = 128 rows x kEwUnits units (64-unit gate-interleaved slices); each thread keeps 4
+// rows' operands in flight. Small tiles: the instance's latency is on the gradient loop's
+// critical path (EW -> d[x,h] -> next step's EW)
+constexpr int kEwUnits = 64;   // 256 measured: 4x fewer tiles, no faster per cell, longer chain
 __device__ void tile_lstm_bwd_ew_bf(const Inst& I, int tile, float* sm) {
   const int B = (int)I.m, H = (int)I.n;
   const int tu = (H + kEwUnits - 1) / kEwUnits;
@@ -359,16 +360,23 @@ __device__ void tile_lstm_bwd_ew_bf(const Inst& I, int tile, float* sm) {
 }
 
 // ---------------------------------------------------------------- backward d[x,h]
-// p: 0 dz-map (KA), 1 WT-map (KB), 5 lens, 6 dh_next(f32), 11 dx(f32), 12 dh(f32); s: 0 t, 2 dz slot
+// p: 0 dz-map (KA), 1 WT-map (KB; the KA map of the same buffer is the one before it),
+//    5 lens, 6 dh_next(f32), 11 dx(f32), 12 dh(f32); s: 0 t, 2 dz slot
+// 256-row tiles (sub bit 1) are 256 rows x 128 columns: twice the tiles of a 256 x 256 split,
+// half the latency per instance. The d[x,h] GEMM sits on the gradient loop's critical path
+// (EW -> d[x,h] -> next step's EW; the backward is latency-bound on cfg3), the operand bytes
+// per flop are 1.5x those of 256 x 256 but the backward's L2 load is well below its cap.
+constexpr int kDxhN2 = 128;
 __device__ void tile_lstm_dxh_tc(const Inst& I, int tile, tc::TcShared& ts, uint32_t& cnt,
                                  uint32_t& cnt2, uint32_t& ntile) {
   const int B = (int)I.m, In = (int)I.k, H = (int)I.n, KT = In + H;
-  const int tn = KT / 256;
   const bool m2 = I.sub & 2;
+  const int bn = m2 ? kDxhN2 : 256;
+  const int tn = KT / bn;
   const int mt = tile / tn, nt = tile % tn;
   const int m0 = mt * (m2 ? 2 * tc::BM : tc::BM);
   const CUtensorMap* mz = (const CUtensorMap*)I.p[0];
-  const CUtensorMap* mwt = (const CUtensorMap*)I.p[1];
+  const CUtensorMap* mwt = (const CUtensorMap*)I.p[1] - (bn == 128 ? 1 : 0);   // box rows = bn
   const int sz = (int)I.s[2];
   auto plan_a = [&](int kb, tc::Box* b) {
     b[0] = {mz, kb * 64, m0, sz, 0};
@@ -377,10 +385,10 @@ __device__ void tile_lstm_dxh_tc(const Inst& I, int tile, tc::TcShared& ts, uint
   };
   const int keep_w = !(kDbgFlagsTC & 32);
   auto plan_b = [&](int kb, tc::Box* b) {
-    b[0] = {mwt, kb * 64, nt * 256, 0, 0, keep_w};
+    b[0] = {mwt, kb * 64, nt * bn, 0, 0, keep_w};
     return 1;
   };
-  if (m2) tc::tc_tile2(ts, (4 * H) / 64, 0, 0, cnt2, ntile, plan_a, plan_b);
+  if (m2) tc::tc_tile2(ts, (4 * H) / 64, 0, 0, cnt2, ntile, plan_a, plan_b, bn);
   else tc::tc_tile(ts, (4 * H) / 64, 256, 0, 0, cnt, ntile, plan_a, plan_b);
   for (int half = 0; half < (m2 ? 2 : 1); ++half) {
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -393,11 +401,12 @@ __device__ void tile_lstm_dxh_tc(const Inst& I, int tile, tc::TcShared& ts, uint
   float* dx = (float*)I.p[11];
   float* dh = (float*)I.p[12];
   const bool dead_row = r < B && masked && !(t < lens[r]);
-  for (int c = (warp / 4) * 128; c < (warp / 4) * 128 + 128; c += 16) {
+  const int cw = bn / 2;   // columns per warp group
+  for (int c = (warp / 4) * cw; c < (warp / 4) * cw + cw; c += 16) {
     float v[16];
     tc::tc_acc16(ts, tcol + c, v);
     if (r >= B) continue;
-    const int n = nt * 256 + c;
+    const int n = nt * bn + c;
     if (n < In) {
       float* d = dx + (int64_t)r * In + n;
 #pragma unroll
