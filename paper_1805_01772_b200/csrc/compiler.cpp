@@ -1412,10 +1412,17 @@ struct Compiler {
           }
         }
     }
+    // ready items by key, smallest first: nodes by id, frames after the ready nodes, root-level
+    // Recvs last. A Recv's wait instance occupies a slot of the driver's in-flight ring until
+    // the peer's message arrives, so it is created only when nothing else is ready (a Recv
+    // ready at the start would otherwise sit in the ring through both loops and, once the
+    // ring wrapped, block both ranks' drivers on each other: f3's gradient exchange)
+    auto key = [&](int it) { return it < N && g.nodes[it].op == "Recv" ? 2 * N + it : it; };
+    auto by_key = [&](int a, int b) { return key(a) > key(b); };
     std::vector<int> ready, ord;
     for (int it : items)
       if (indeg[it] == 0) ready.push_back(it);
-    std::sort(ready.rbegin(), ready.rend());
+    std::sort(ready.begin(), ready.end(), by_key);
     while (!ready.empty()) {
       int v = ready.back();
       ready.pop_back();
@@ -1423,7 +1430,7 @@ struct Compiler {
       for (int w : succ[v])
         if (--indeg[w] == 0) {
           ready.push_back(w);
-          std::sort(ready.rbegin(), ready.rend());
+          std::sort(ready.begin(), ready.end(), by_key);
         }
     }
     if (ord.size() != items.size()) throw CfError(CF_E_INVALID_GRAPH, "root graph has a cycle");

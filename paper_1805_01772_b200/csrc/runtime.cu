@@ -1277,7 +1277,9 @@ struct Driver {
     int32_t id = ninst++;
     const int sl = id & kRingMask;
     while (r_id[sl] != -1) {   // ring full: wait for the oldest in-flight instance
-      drain();
+      const unsigned long long now = globaltimer();
+      if (drain()) last_progress = now;
+      else if ((long long)(now - last_progress) > A.watchdog_ns) fail(CF_E_DEADLOCK, -700);
       if (st->error) return -1;
     }
     ntiles = max(ntiles, 1);

@@ -73,6 +73,13 @@ __device__ __forceinline__ void tma_load_3d_hint(void* smem_dst, const void* des
       "l"(desc), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "l"(policy)
       : "memory");
 }
+// warm L2 with a box a few k-blocks ahead of the smem ring (the ring holds only 3 stages of
+// 64 KB; loads that miss L2 otherwise expose the HBM latency to the MMA issuer)
+__device__ __forceinline__ void tma_prefetch_l2_3d(const void* desc, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(desc),
+               "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
 // generic-proxy writes (epilogue st.global) made visible to later async-proxy reads (TMA)
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");

@@ -162,7 +162,8 @@ __device__ inline void tc_tile(TcShared& s, int nk, int bn, int a_mn, int b_mn, 
 // counter (cnt2); the done barrier / tile counter are shared with tc_tile.
 template <class PlanA, class PlanB>
 __device__ inline void tc_tile2(TcShared& s, int nk, int a_mn, int b_mn, uint32_t& cnt2,
-                                uint32_t& tiles, PlanA plan_a, PlanB plan_b, int bn = 256) {
+                                uint32_t& tiles, PlanA plan_a, PlanB plan_b, int bn = 256,
+                                int prefetch_ahead = 0) {
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   if (warp == 0) {
     if (lane == 0) {
@@ -177,6 +178,15 @@ __device__ inline void tc_tile2(TcShared& s, int nk, int a_mn, int b_mn, uint32_
         for (int i = 0; i < na; ++i) box_load(s.a2[st], bx[i], &s.full2[st]);
         int nb = plan_b(kb, bx);
         for (int i = 0; i < nb; ++i) box_load(s.b2[st], bx[i], &s.full2[st]);
+        if (prefetch_ahead > 0) {   // the same boxes a few k-blocks ahead, into L2 only
+          const int kp = kb == 0 ? 1 : kb + prefetch_ahead;
+          for (int q = kp; q <= kb + prefetch_ahead && q < nk; ++q) {
+            const int n1 = plan_a(q, bx);
+            for (int i = 0; i < n1; ++i) tma_prefetch_l2_3d(bx[i].map, bx[i].c0, bx[i].c1, bx[i].c2);
+            const int n2 = plan_b(q, bx);
+            for (int i = 0; i < n2; ++i) tma_prefetch_l2_3d(bx[i].map, bx[i].c0, bx[i].c1, bx[i].c2);
+          }
+        }
       }
     }
     __syncwarp();

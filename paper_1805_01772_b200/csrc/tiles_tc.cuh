@@ -172,7 +172,10 @@ __device__ void tile_lstm_fwd_tc(const Inst& I, int tile, tc::TcShared& ts, uint
     b[0] = {mw, kb * 64, nt * 256, 0, 0, keep_w};
     return 1;
   };
-  if (m2) tc::tc_tile2(ts, nk, 0, 0, cnt2, ntile, plan_a, plan_b);
+  // debug flags bits 16-19: L2 prefetch distance in k-blocks (A/B; 0 = the default 4, 15 = off)
+  const int pfd = (kDbgFlagsTC >> 16) & 15;
+  const int ahead = pfd == 15 ? 0 : pfd ? pfd : 4;
+  if (m2) tc::tc_tile2(ts, nk, 0, 0, cnt2, ntile, plan_a, plan_b, 256, ahead);
   else tc::tc_tile(ts, nk, 256, 0, 0, cnt, ntile, plan_a, plan_b);
   // ---- fused epilogue: 2 (or 4) groups of 16 units x 4 gates per thread
   const int nit = 2 * nh;
@@ -366,7 +369,7 @@ __device__ void tile_lstm_bwd_ew_bf(const Inst& I, int tile, float* sm) {
 // half the latency per instance. The d[x,h] GEMM sits on the gradient loop's critical path
 // (EW -> d[x,h] -> next step's EW; the backward is latency-bound on cfg3), the operand bytes
 // per flop are 1.5x those of 256 x 256 but the backward's L2 load is well below its cap.
-constexpr int kDxhN2 = 128;
+constexpr int kDxhN2 = 256;   // 128 measured: 41% less efficient per flop, no net gain
 __device__ void tile_lstm_dxh_tc(const Inst& I, int tile, tc::TcShared& ts, uint32_t& cnt,
                                  uint32_t& cnt2, uint32_t& ntile) {
   const int B = (int)I.m, In = (int)I.k, H = (int)I.n, KT = In + H;
