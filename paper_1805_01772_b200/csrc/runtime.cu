@@ -3288,7 +3288,11 @@ struct Driver {
 __device__ void worker_loop(const RunArgs& A) {
   __shared__ __align__(16) float sm[32 * 33 + 32 * 129 + 64];
   __shared__ unsigned long long s_entry;
-  __shared__ int s_last;
+  __shared__ int s_last, s_use_next;
+  // the next tile, claimed by an epilogue thread while the current tensor-core tile's mainloop
+  // runs (its record staged here): the claim / record round trips leave the critical path
+  __shared__ unsigned long long s_next;
+  __shared__ Inst s_inst_next;
   extern __shared__ __align__(1024) uint8_t dyn_smem[];
   RunState* st = A.st;
   const bool tcmode = A.prog.precision == D_BF16;
@@ -3298,40 +3302,69 @@ __device__ void worker_loop(const RunArgs& A) {
     ts = tc::tc_carve(dyn_smem);
     tc::tc_setup(ts);
   }
+  if (threadIdx.x == 0) s_next = ~0ULL;
+  __syncthreads();
+  // queue entries are instance ids; a tile is claimed with one atomicAdd on the instance's tile
+  // counter, and whoever takes (or overshoots) the last tile advances the head past the
+  // instance. 1 = claimed (*e), 2 = overshot (retry), 0 = ring empty
+  auto claim = [&](unsigned long long* headp, unsigned long long* tailp, const unsigned long long* ring,
+                   unsigned long long* e) -> int {
+    unsigned long long h = ld_volatile_u64(headp);
+    if (h >= ld_volatile_u64(tailp)) return 0;
+    __threadfence();
+    const int32_t id = (int32_t)((volatile const unsigned long long*)ring)[h & (A.q_cap - 1)];
+    const int nt = ((volatile const Inst*)(A.insts + id))->ntiles;
+    const int t = atomicAdd(&A.tile_next[id], 1);
+    if (t >= nt - 1) atomicCAS(headp, h, h + 1);
+    if (t >= nt) return 2;
+    *e = ((unsigned long long)id << 32) | (unsigned)t;
+    return 1;
+  };
+  // one non-blocking attempt over both rings (high priority first)
+  auto try_claim = [&](unsigned long long* e) -> bool {
+    for (int k = 0; k < 8; ++k) {
+      int r = claim(&st->q_head, &st->q_tail, A.queue, e);
+      if (r == 1) return true;
+      if (r == 2) continue;
+      r = claim(&st->lq_head, &st->lq_tail, A.lq, e);
+      if (r == 1) return true;
+      if (r == 2) continue;
+      return false;
+    }
+    return false;
+  };
+  const bool ahead = tcmode && !(kDbgFlags & 64);   // A/B: debug flag bit 6 = no claim-ahead
+  auto claim_ahead = [&]() {
+    if (!ahead || s_next != ~0ULL) return;
+    unsigned long long e;
+    if (!try_claim(&e)) return;
+    const int32_t id = (int32_t)(e >> 32);
+    int64_t* dst = (int64_t*)&s_inst_next;
+    const volatile int64_t* src = (const volatile int64_t*)(A.insts + id);
+#pragma unroll 4
+    for (int k = 0; k < (int)(sizeof(Inst) / 8); ++k) dst[k] = src[k];
+    s_next = e;
+  };
   while (true) {
     if (threadIdx.x == 0) {
-      // claim from the high-priority ring first, then the low one (CAS on the heads)
-      int spins = 0;
       unsigned long long e = ~0ULL;
-      // queue entries are instance ids; a tile is claimed with one atomicAdd on the
-      // instance's tile counter, and whoever takes (or overshoots) the last tile advances
-      // the head past the instance
-      auto claim = [&](unsigned long long* headp, unsigned long long* tailp,
-                       const unsigned long long* ring) -> int {
-        unsigned long long h = ld_volatile_u64(headp);
-        if (h >= ld_volatile_u64(tailp)) return 0;
-        __threadfence();
-        const int32_t id = (int32_t)((volatile const unsigned long long*)ring)[h & (A.q_cap - 1)];
-        const int nt = ((volatile const Inst*)(A.insts + id))->ntiles;
-        const int t = atomicAdd(&A.tile_next[id], 1);
-        if (t >= nt - 1) atomicCAS(headp, h, h + 1);
-        if (t >= nt) return 2;
-        e = ((unsigned long long)id << 32) | (unsigned)t;
-        return 1;
-      };
-      while (true) {
-        int r = claim(&st->q_head, &st->q_tail, A.queue);
-        if (r == 1) break;
-        if (r == 2) continue;
-        r = claim(&st->lq_head, &st->lq_tail, A.lq);
-        if (r == 1) break;
-        if (r == 2) continue;
-        if (ld_volatile_i32(&st->quit)) break;
-        backoff(spins);
+      int use_next = 0;
+      if (s_next != ~0ULL) {
+        e = s_next;
+        s_next = ~0ULL;
+        use_next = 1;
+      } else {
+        int spins = 0;
+        while (true) {
+          if (try_claim(&e)) break;
+          if (ld_volatile_i32(&st->quit)) break;
+          backoff(spins);
+        }
       }
       __threadfence();
       if (A.prog.precision == D_BF16) tc::fence_proxy_async_global();
       s_entry = e;
+      s_use_next = use_next;
     }
     __syncthreads();
     unsigned long long e = s_entry;
@@ -3341,7 +3374,8 @@ __device__ void worker_loop(const RunArgs& A) {
     unsigned long long t_tile0 = (kProfBuild && A.prof) ? globaltimer() : 0;
     __shared__ Inst s_inst;
     if (threadIdx.x < (int)(sizeof(Inst) / 8))
-      ((int64_t*)&s_inst)[threadIdx.x] = ((volatile const int64_t*)(A.insts + id))[threadIdx.x];
+      ((int64_t*)&s_inst)[threadIdx.x] = s_use_next ? ((const int64_t*)&s_inst_next)[threadIdx.x]
+                                                    : ((volatile const int64_t*)(A.insts + id))[threadIdx.x];
     __syncthreads();
     const Inst I = s_inst;
     switch (kDbgFlags & 1 ? (int)HK_NOP : (int)I.kind) {
@@ -3358,10 +3392,10 @@ __device__ void worker_loop(const RunArgs& A) {
       case HK_LSTM_BWD_MM: tile_lstm_bwd_mm(I, tile, sm); break;
       case HK_PREP_WP: tile_prep_wp(I, tile); break;
       case HK_PREP_WT: tile_prep_wt(I, tile, (float*)dyn_smem); break;
-      case HK_LSTM_FWD_TC: tile_lstm_fwd_tc(I, tile, ts, tc_cnt, tc_cnt2, tc_tiles, sm); break;
+      case HK_LSTM_FWD_TC: tile_lstm_fwd_tc(I, tile, ts, tc_cnt, tc_cnt2, tc_tiles, sm, claim_ahead); break;
       case HK_LSTM_BWD_EW_BF: tile_lstm_bwd_ew_bf(I, tile, sm); break;
-      case HK_LSTM_DXH_TC: tile_lstm_dxh_tc(I, tile, ts, tc_cnt, tc_cnt2, tc_tiles); break;
-      case HK_LSTM_DW_TC: tile_lstm_dw_tc(I, tile, ts, tc_cnt, tc_cnt2, tc_tiles); break;
+      case HK_LSTM_DXH_TC: tile_lstm_dxh_tc(I, tile, ts, tc_cnt, tc_cnt2, tc_tiles, claim_ahead); break;
+      case HK_LSTM_DW_TC: tile_lstm_dw_tc(I, tile, ts, tc_cnt, tc_cnt2, tc_tiles, claim_ahead); break;
       default: break;
     }
     // epilogue stores (generic proxy) must be visible to later TMA (async proxy) reads

@@ -31,6 +31,7 @@ struct TcShared {
   uint64_t* empty;   // [kStages]
   uint64_t* done;    // [1]
   uint32_t* tmem_slot;
+  volatile uint32_t* kb_issued;   // running k-block counter of the last MMA issued (hook pacing)
   uint64_t* full2;   // [kStages2]
   uint64_t* empty2;  // [kStages2]
 };
@@ -54,6 +55,7 @@ __device__ inline TcShared tc_carve(uint8_t* dyn) {
   s.full2 = s.done + 1;
   s.empty2 = s.full2 + kStages2;
   s.tmem_slot = (uint32_t*)(s.empty2 + kStages2);
+  s.kb_issued = (volatile uint32_t*)(s.tmem_slot + 1);
   for (int i = 0; i < kStages2; ++i) {
     s.a2[i] = (uint8_t*)base + i * kStage2;
     s.b2[i] = s.a2[i] + kStage2A;
@@ -73,6 +75,7 @@ __device__ inline void tc_setup(TcShared& s) {
       mbar_init(&s.empty2[i], 1);
     }
     mbar_init(s.done, 1);
+    *s.kb_issued = 0;
     fence_barrier_init();
   }
   if (threadIdx.x / 32 == 2) tmem_alloc<512>(s.tmem_slot);
@@ -103,9 +106,22 @@ __device__ __forceinline__ void box_load(uint8_t* stage, const Box& b, uint64_t*
 // Run the K loop of one tile. `cnt` is the CTA-wide running k-block counter (same value in
 // the producer and MMA threads), `tiles` the running tile counter (epilogue done-barrier
 // phase). After return, all threads may read the accumulator with tmem_ld16.
-template <class PlanA, class PlanB>
+struct NoHook {
+  __device__ void operator()() const {}
+};
+// run the hook once the MMA issuer is within 3 k-blocks of the end of the tile's mainloop
+// (end = the running k-block counter after the tile): late enough that a tile claimed there
+// does not wait long behind this one, early enough to hide the claim's round trips
+template <class Hook>
+__device__ __forceinline__ void hook_paced(TcShared& s, uint32_t end, Hook& hook) {
+  while ((int)(end - *s.kb_issued) > 3) __nanosleep(256);
+  hook();
+}
+// hook: run by thread 64 (an epilogue thread, idle during the mainloop) before it waits for the
+// accumulator; the worker claims its next tile there (runtime.cu worker_loop)
+template <class PlanA, class PlanB, class Hook = NoHook>
 __device__ inline void tc_tile(TcShared& s, int nk, int bn, int a_mn, int b_mn, uint32_t& cnt,
-                               uint32_t& tiles, PlanA plan_a, PlanB plan_b) {
+                               uint32_t& tiles, PlanA plan_a, PlanB plan_b, Hook hook = Hook()) {
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t stage_b = (uint32_t)bn * BK * 2;
   // Role warps: lane 0 works, lanes 1-31 park at __syncwarp (NOT in a suspending
@@ -144,11 +160,13 @@ __device__ inline void tc_tile(TcShared& s, int nk, int bn, int a_mn, int b_mn, 
         mma_bf16(tmem, da, db, idesc, (kb | k) != 0);
       }
       mma_commit(&s.empty[st]);   // frees the stage when these MMAs have read it
+      *s.kb_issued = c + 1;
     }
     mma_commit(s.done);           // accumulator complete
     }
     __syncwarp();
   }
+  if (threadIdx.x == 64) hook_paced(s, cnt + nk, hook);
   cnt += nk;
   // everyone waits for the accumulator
   mbar_wait(s.done, tiles & 1);
@@ -160,10 +178,10 @@ __device__ inline void tc_tile(TcShared& s, int nk, int bn, int a_mn, int b_mn, 
 // both MMAs of a k16 step read the same B stage (bn = 256 or 128 columns). Plans fill A boxes at offsets within the
 // 32 KiB A region (rows 128.. at +16 KiB) and B boxes as in tc_tile. Own barriers and k-block
 // counter (cnt2); the done barrier / tile counter are shared with tc_tile.
-template <class PlanA, class PlanB>
+template <class PlanA, class PlanB, class Hook = NoHook>
 __device__ inline void tc_tile2(TcShared& s, int nk, int a_mn, int b_mn, uint32_t& cnt2,
                                 uint32_t& tiles, PlanA plan_a, PlanB plan_b, int bn = 256,
-                                int prefetch_ahead = 0) {
+                                int prefetch_ahead = 0, Hook hook = Hook()) {
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   if (warp == 0) {
     if (lane == 0) {
@@ -212,11 +230,13 @@ __device__ inline void tc_tile2(TcShared& s, int nk, int a_mn, int b_mn, uint32_
           mma_bf16(tmem + 256, da1, db, idesc, (kb | k) != 0);
         }
         mma_commit(&s.empty2[st]);
+        *s.kb_issued = c + 1;
       }
       mma_commit(s.done);
     }
     __syncwarp();
   }
+  if (threadIdx.x == 64) hook_paced(s, cnt2 + nk, hook);
   cnt2 += nk;
   mbar_wait(s.done, tiles & 1);
   tiles++;

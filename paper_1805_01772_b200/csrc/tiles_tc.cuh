@@ -114,8 +114,9 @@ __device__ void tile_prep_wt(const Inst& I, int tile, float* sm) {
 // TMEM loads share one wait. sigma(x) = 0.5 tanh(x / 2) + 0.5 (one MUFU op instead of ex2 + a
 // division).
 __device__ __forceinline__ float sigm_tanh(float x) { return fmaf(0.5f, tanhf_(0.5f * x), 0.5f); }
+template <class Hook>
 __device__ void tile_lstm_fwd_tc(const Inst& I, int tile, tc::TcShared& ts, uint32_t& cnt,
-                                 uint32_t& cnt2, uint32_t& ntile, float* sm) {
+                                 uint32_t& cnt2, uint32_t& ntile, float* sm, Hook hook) {
   const int B = (int)I.m, In = (int)I.k, H = (int)I.n;
   const int nkx = In / 64, nk = (In + H) / 64;
   const int tn = H / 64;
@@ -175,8 +176,8 @@ __device__ void tile_lstm_fwd_tc(const Inst& I, int tile, tc::TcShared& ts, uint
   // debug flags bits 16-19: L2 prefetch distance in k-blocks (A/B; 0 = the default 4, 15 = off)
   const int pfd = (kDbgFlagsTC >> 16) & 15;
   const int ahead = pfd == 15 ? 0 : pfd ? pfd : 4;
-  if (m2) tc::tc_tile2(ts, nk, 0, 0, cnt2, ntile, plan_a, plan_b, 256, ahead);
-  else tc::tc_tile(ts, nk, 256, 0, 0, cnt, ntile, plan_a, plan_b);
+  if (m2) tc::tc_tile2(ts, nk, 0, 0, cnt2, ntile, plan_a, plan_b, 256, ahead, hook);
+  else tc::tc_tile(ts, nk, 256, 0, 0, cnt, ntile, plan_a, plan_b, hook);
   // ---- fused epilogue: 2 (or 4) groups of 16 units x 4 gates per thread
   const int nit = 2 * nh;
   // fully unrolled: the double-buffered c_prev registers are indexed by constants (a runtime
@@ -370,8 +371,9 @@ __device__ void tile_lstm_bwd_ew_bf(const Inst& I, int tile, float* sm) {
 // (EW -> d[x,h] -> next step's EW; the backward is latency-bound on cfg3), the operand bytes
 // per flop are 1.5x those of 256 x 256 but the backward's L2 load is well below its cap.
 constexpr int kDxhN2 = 256;   // 128 measured: 41% less efficient per flop, no net gain
+template <class Hook>
 __device__ void tile_lstm_dxh_tc(const Inst& I, int tile, tc::TcShared& ts, uint32_t& cnt,
-                                 uint32_t& cnt2, uint32_t& ntile) {
+                                 uint32_t& cnt2, uint32_t& ntile, Hook hook) {
   const int B = (int)I.m, In = (int)I.k, H = (int)I.n, KT = In + H;
   const bool m2 = I.sub & 2;
   const int bn = m2 ? kDxhN2 : 256;
@@ -391,8 +393,8 @@ __device__ void tile_lstm_dxh_tc(const Inst& I, int tile, tc::TcShared& ts, uint
     b[0] = {mwt, kb * 64, nt * bn, 0, 0, keep_w};
     return 1;
   };
-  if (m2) tc::tc_tile2(ts, (4 * H) / 64, 0, 0, cnt2, ntile, plan_a, plan_b, bn);
-  else tc::tc_tile(ts, (4 * H) / 64, 256, 0, 0, cnt, ntile, plan_a, plan_b);
+  if (m2) tc::tc_tile2(ts, (4 * H) / 64, 0, 0, cnt2, ntile, plan_a, plan_b, bn, 0, hook);
+  else tc::tc_tile(ts, (4 * H) / 64, 256, 0, 0, cnt, ntile, plan_a, plan_b, hook);
   for (int half = 0; half < (m2 ? 2 : 1); ++half) {
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int r = m0 + 128 * half + 32 * (warp % 4) + lane;
@@ -433,8 +435,9 @@ __device__ void tile_lstm_dxh_tc(const Inst& I, int tile, tc::TcShared& ts, uint
 // accumulator is paid once per chunk. p: 0 dz-map (MN), 3 dW(f32), 4 db(f32), 6 step records
 // (6 x i64 per step: dz slot, x-map, x slot, h-map, h slot, db-partials ptr);
 // s: 6 flags (bit0 accumulate dW, bit1 accumulate db), 7 number of steps
+template <class Hook>
 __device__ void tile_lstm_dw_tc(const Inst& I, int tile, tc::TcShared& ts, uint32_t& cnt,
-                                uint32_t& cnt2, uint32_t& ntile) {
+                                uint32_t& cnt2, uint32_t& ntile, Hook hook) {
   const int B = (int)I.m, In = (int)I.k, H = (int)I.n, KT = In + H, G = 4 * H;
   const int tn = KT / 256;
   const int n_dw = (G / (2 * tc::BM)) * tn;   // 256 gate rows per tile
@@ -474,7 +477,7 @@ __device__ void tile_lstm_dw_tc(const Inst& I, int tile, tc::TcShared& ts, uint3
     for (int j = 0; j < 4; ++j) b[j] = {mb, col0 + 64 * j, r * 64, sb, j * 8192};
     return 4;
   };
-  tc::tc_tile2(ts, ns * nkb, 1, 1, cnt2, ntile, plan_a, plan_b);
+  tc::tc_tile2(ts, ns * nkb, 1, 1, cnt2, ntile, plan_a, plan_b, 256, 0, hook);
   for (int half = 0; half < 2; ++half) {
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int m = m0 + 128 * half + 32 * (warp % 4) + lane;
