@@ -30,6 +30,12 @@ int32_t cf_debug_session_profile(const struct cf_session* s, unsigned long long*
  * per CTA); product default 512 (rows <= 0 restores it). Lets tests exercise that tile shape
  * at small sizes. Returns 0 or CF_E_CUDA. */
 int32_t cf_debug_set_m2_rows(int32_t rows);
+/* Mainloop throughput probe of the 256-row tcgen05 engine: one CTA per SM runs every
+ * 256 x 256 tile of C = A B^T (A [M][K], B nb copies of [N][K], bf16, K-major; B copy chosen
+ * round-robin, `reps` passes; L2 prefetch `prefetch` k-blocks ahead, 0 = off) with an
+ * accumulator-read-only epilogue. *ms_out = device time. Returns 0 or CF_E_CUDA. */
+int32_t cf_debug_tc_pipe(int32_t M, int32_t N, int32_t K, int32_t nb, int32_t reps,
+                         int32_t prefetch, const void* A, const void* B, float* ms_out);
 /* Profiling knobs: bit 0 = workers skip every tile body (the device driver's own cost in
  * isolation; results are garbage); A/B switches (results unchanged): bit 2 = poll
  * completions after every node, bit 3 = wave helpers spin without sleeping, bit 4 = release

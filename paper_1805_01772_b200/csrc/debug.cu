@@ -89,3 +89,80 @@ extern "C" int32_t cf_debug_tc_gemm(int32_t M, int32_t N, int32_t K, int32_t bn,
     return 15;
   }
 }
+
+// ---- mainloop throughput probe: persistent CTAs (one per SM) run 256 x 256 tiles of
+// C = A B^T with the worker's 256-row engine (tc_tile2), A [M][K] and B [N][K] K-major, the
+// B operand chosen round-robin from `nb` weight copies (nb x N x K bf16: > L2 when large).
+// The epilogue only reads the accumulator (no stores): the time is the mainloop's.
+namespace {
+__global__ void __launch_bounds__(256, 1)
+    debug_pipe_kernel(const CUtensorMap* maps, int M, int N, int K, int nb, int reps, int pf,
+                      unsigned long long* cycles) {
+  extern __shared__ uint8_t dyn[];
+  tc::TcShared s = tc::tc_carve(dyn);
+  tc::tc_setup(s);
+  const int tm = M / 256, tn = N / 256, nk = K / 64;
+  uint32_t cnt2 = 0, tiles = 0;
+  const long long c0 = clock64();
+  for (int w = blockIdx.x; w < tm * tn * nb * reps; w += gridDim.x) {
+    const int b = (w / (tm * tn)) % nb, mt = (w % (tm * tn)) / tn, nt = w % tn;
+    const CUtensorMap* ma = maps;
+    const CUtensorMap* mb = maps + 1;
+    auto plan_a = [&](int kb, tc::Box* bx) {
+      bx[0] = {ma, kb * 64, mt * 256, 0, 0};
+      bx[1] = {ma, kb * 64, mt * 256 + 128, 0, tc::kStageA};
+      return 2;
+    };
+    auto plan_b = [&](int kb, tc::Box* bx) {
+      bx[0] = {mb, kb * 64, nt * 256, b, 0, 1};
+      return 1;
+    };
+    tc::tc_tile2(s, nk, 0, 0, cnt2, tiles, plan_a, plan_b, 256, pf);
+    float v[16];
+    tc::tc_acc16(s, 0, v);
+    if (v[0] == 12345.f) cycles[1] = 1;   // keep the load
+    tc::tc_tile_end();
+  }
+  if (threadIdx.x == 0) atomicAdd(cycles, (unsigned long long)(clock64() - c0));
+  tc::tc_teardown(s);
+}
+}  // namespace
+
+// ms of the probe (all tiles of `reps` passes over nb weight copies); see debug_pipe_kernel
+extern "C" int32_t cf_debug_tc_pipe(int32_t M, int32_t N, int32_t K, int32_t nb, int32_t reps,
+                                    int32_t prefetch, const void* A, const void* B, float* ms_out) {
+  try {
+    CUtensorMap maps[2];
+    maps[0] = cf::make_map_bf16(A, K, M, 1, 64, 128);
+    maps[1] = cf::make_map_bf16(B, K, N, nb, 64, 256);
+    CUtensorMap* d = nullptr;
+    unsigned long long* cyc = nullptr;
+    if (cudaMalloc(&d, sizeof(maps)) != cudaSuccess) throw std::runtime_error("cudaMalloc");
+    cudaMalloc(&cyc, 16);
+    cudaMemset(cyc, 0, 16);
+    cudaMemcpy(d, maps, sizeof(maps), cudaMemcpyHostToDevice);
+    cudaFuncSetAttribute(debug_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::kSmemTC);
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    debug_pipe_kernel<<<sms, 256, tc::kSmemTC>>>(d, M, N, K, nb, 1, prefetch, cyc);   // warm-up
+    cudaEventRecord(e0);
+    debug_pipe_kernel<<<sms, 256, tc::kSmemTC>>>(d, M, N, K, nb, reps, prefetch, cyc);
+    cudaEventRecord(e1);
+    cudaError_t e = cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    *ms_out = ms;
+    cudaFree(d);
+    cudaFree(cyc);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
+    return 0;
+  } catch (const std::exception& ex) {
+    cf::set_error(ex.what());
+    return 15;
+  }
+}
