@@ -196,7 +196,7 @@ __device__ void tile_lstm_fwd_tc(const Inst& I, int tile, tc::TcShared& ts, uint
 #pragma unroll
     for (int g = 0; g < 4; ++g) tc::tmem_ld16_nowait(ta + 64 * g, zr[g]);
     tc::tmem_wait_ld();
-    if (r >= B) continue;
+    if (r >= B || (kDbgFlagsTC & (1 << 20))) continue;   // bit 20: no epilogue (timing only)
     const int u0 = nt * 64 + cu;
     const int64_t o = (int64_t)r * H + u0;
     float cp[16], hn[16], cn[16], zi[16], zf[16], zg[16], zo[16];
