@@ -82,9 +82,14 @@ class _AD:
             with b.in_ctx(C):
                 b.op("StackPush", [h, t])
             self.stack_of[t] = h
+        # a loop nested in another loop ("for nested loops, we apply our
+        # techniques recursively"): its stack is created once per outer iteration, in the outer
+        # body, so the handle itself is an outer-loop value the gradient needs -- saved on a
+        # stack of the outer loop in turn (fwd recursion); the outer gradient iteration pops
+        # the handle of its own forward iteration, whose inner gradient loop pops the values
+        hp = self.fwd(self.stack_of[t])
         with b.in_ctx(self.mirror[C.id]):
-            v = b.op1("StackPop", [self.stack_of[t]],
-                      {"dtype": self.dtype(t), "elem_shape": self.shape(t)})
+            v = b.op1("StackPop", [hp], {"dtype": self.dtype(t), "elem_shape": self.shape(t)})
         self.pop_of[t] = v
         return v
 

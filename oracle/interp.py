@@ -505,7 +505,9 @@ class Interpreter:
             return [StackObj(n.id, (tag, a["frame"]))]
         if op == "StackPush":
             st: StackObj = vals[0]
-            st.entries.append(np.array(vals[1], copy=True))
+            # a handle (a nested loop's stack, saved for the outer gradient loop) by reference
+            v = vals[1]
+            st.entries.append(v if isinstance(v, StackObj) else np.array(v, copy=True))
             st.pushes += 1
             st.max_depth = max(st.max_depth, len(st.entries))
             self.trace.pushes[st.id] += 1
