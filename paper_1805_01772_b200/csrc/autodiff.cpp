@@ -80,10 +80,15 @@ class AD {
     Attrs pa;
     pa.set("dtype", g_.dtype(t));
     pa.setv("elem_shape", g_.shape(t));
+    // a loop nested in another loop ("for nested loops, we apply our
+    // techniques recursively"): its stack is created once per outer iteration, in the outer
+    // body, so the handle is itself an outer-loop value the gradient needs -- saved on a
+    // stack of the outer loop in turn (fwd recursion)
+    const TRef hp = fwd(stack_of_[t]);
     TRef v;
     {
       CtxGuard guard(g_, mirror_.at(C));
-      v = g_.op1("StackPop", {stack_of_[t]}, pa);
+      v = g_.op1("StackPop", {hp}, pa);
     }
     pop_of_[t] = v;
     return v;
