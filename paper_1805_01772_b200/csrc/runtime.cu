@@ -858,7 +858,7 @@ struct Driver {
   int32_t last_dw = -1;
   unsigned long long lq_tail = 0;
   // pending channel waits (HK_WAIT instances), polled by drain()
-  static constexpr int kMaxWaits = 96;   // f3 at 8 GPUs: 2 weight tensors x 8 layers x 7 peers = 112 > 96 (-400 error)
+  static constexpr int kMaxWaits = 128;   // f3 exchange at 8 GPUs: 2 x 8 layers x 7 peers = 112 Recvs
   struct ChanWait {
     unsigned long long* flag;
     unsigned long long want;
