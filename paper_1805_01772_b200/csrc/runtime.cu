@@ -4016,7 +4016,13 @@ void build_session(cf_session* s, const cf::Graph& g, const cf_run_opts* o,
   need += sizeof(DStack) * P.stacks.size() + 8 * P.nodes.size() + 4 * (P.accs.size() + P.iter_counters);
   need += (sizeof(DTA) + 12) * P.tas.size() + 48;
   need += 16 * 12;
-  const size_t smem_cap = 198 * 1024;   // + ~28 KiB static smem stays under the 227 KiB limit
+  // dynamic shared memory: what the opt-in limit leaves next to the kernel's static smem
+  cudaFuncAttributes fa{};
+  CUDA_OK(cudaFuncGetAttributes(&fa, cf_driver_kernel));
+  int optin = 0;
+  CUDA_OK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, s->device));
+  const size_t smem_cap = (size_t)optin - fa.sharedSizeBytes - 1024;
+  if ((size_t)s->dyn_smem > smem_cap) throw cf::CfError(CF_E_CUDA, "tile engine does not fit in shared memory");
   if ((int)std::min(need, smem_cap) > s->dyn_smem) s->dyn_smem = (int)std::min(need, smem_cap);
   A.dyn_smem = s->dyn_smem;
   CUDA_OK(cudaFuncSetAttribute(cf_driver_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, s->dyn_smem));
