@@ -48,7 +48,8 @@ int32_t cf_debug_tc_pipe(int32_t M, int32_t N, int32_t K, int32_t nb, int32_t re
  * (steps that do not close a dW chunk). Returns 0 or CF_E_CUDA. */
 int32_t cf_debug_set_flags(int32_t flags);
 /* Compile a graph for the device program without a GPU and write its description and body
- * programs (one node per line, evaluation order) into buf; *needed = length + 1. */
+ * programs (one node per line, evaluation order) into buf; *needed = length + 1. The
+ * environment variable CF_DEBUG_MAX_ITERATIONS plays cf_run_opts.max_iterations. */
 struct cf_graph;
 typedef struct { int32_t node, port; } cf_debug_tensor;
 int32_t cf_debug_program_listing(const struct cf_graph* g, int32_t precision,

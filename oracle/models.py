@@ -198,3 +198,34 @@ def run_pipeline_threads(T_, B, I, H, L, world, feeds, K=None, sched_seed=None, 
     if errs:
         raise errs[0]
     return res
+
+
+def ponder_rnn(T_: int, B: int, D: int, K: int = 32) -> RNNProgram:
+    """A while_loop nested in a while_loop (the adaptive-
+    computation RNN shape): for every step t the state takes x[t] and then ponders n[t] times,
+    ``a = tanh(a W + c)``; n[t] is fed (ragged inner trip counts). Loss sum(R * a_T)."""
+    b = Builder()
+    x = b.placeholder("x", FLOAT, (T_, B, D))
+    n = b.placeholder("n", INT, (T_,))
+    W = b.placeholder("W", FLOAT, (D, D))
+    c = b.placeholder("c", FLOAT, (B, D))
+    a0 = b.placeholder("a0", FLOAT, (B, D))
+    R = b.placeholder("R", FLOAT, (B, D))
+    x_ta = b.tensor_array(T_, FLOAT, (B, D)).unstack(x)
+    n_ta = b.tensor_array(T_, INT, ()).unstack(n)
+    t_bound = b.const(T_, INT)
+
+    def step(t, a):
+        a = b.add(a, x_ta.read(t))
+        m = n_ta.read(t)
+        r = b.while_loop(lambda k, s: b.less(k, m),
+                         lambda k, s: [b.add(k, b.const(1, INT)),
+                                       b.op1("Tanh", [b.add(b.matmul(s, W), c)])],
+                         [b.const(0, INT), a], parallel_iterations=K, name="ponder")
+        return [b.add(t, b.const(1, INT)), r[1]]
+    res = b.while_loop(lambda t, a: b.less(t, t_bound), step, [b.const(0, INT), a0],
+                       parallel_iterations=K, name="steps")
+    y = b.reduce_sum(b.mul(R, res[1]))
+    names = ["x", "W", "c", "a0"]
+    grads = {"d" + k: gt for k, gt in zip(names, gradients(b, y, [x, W, c, a0]))}
+    return RNNProgram(b, {"y": y, "aT": res[1]}, grads, T_, B, D, D, 1)

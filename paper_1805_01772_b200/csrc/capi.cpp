@@ -1,6 +1,7 @@
 // extern "C" graph-construction entry points of libcf (include/cf.h). Execution entry points
 // (cf_session_*, cf_run) live in runtime.cu.
 #include <cstring>
+#include <cstdlib>
 #include <string>
 
 #include "compiler.h"
@@ -305,6 +306,8 @@ int32_t cf_debug_program_listing(const cf_graph* g, int32_t precision, int32_t p
   cf::CompileOpts o;
   o.precision = precision ? precision : CF_F32;
   o.parallel_iterations = parallel_iterations;
+  // iteration bound of frames without a TensorArray (cf_run_opts.max_iterations)
+  if (const char* mi = std::getenv("CF_DEBUG_MAX_ITERATIONS")) o.max_iterations = atoll(mi);
   std::vector<TRef> fv;
   for (int i = 0; i < n_fetch; ++i) fv.push_back(tr(fetches[i]));
   cf::HostProgram P = cf::compile(g->g, o, fv);

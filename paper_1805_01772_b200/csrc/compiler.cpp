@@ -62,6 +62,8 @@ struct Compiler {
   std::vector<std::vector<std::pair<int, int>>> cons;   // per value: (consumer node, input idx)
   std::map<std::string, int> frame_id;
   std::vector<int> frame_ctx;
+  std::vector<int> frame_parent;      // enclosing frame of each frame (-1: root context)
+  std::vector<int64_t> frame_total;   // iteration indices over all instances of a frame
   std::map<int, int> ta_id;           // TACreate node -> ta id
   std::map<int, int> stack_id;        // StackCreate node -> stack id
   std::vector<std::vector<std::pair<int, int>>> extra_edges;   // per frame: (before, after)
@@ -222,11 +224,22 @@ struct Compiler {
     frame_of.assign(N, -1);
     for (auto& name : g.frame_order) {
       int c = g.whiles.at(name);
-      if (g.enclosing_while(g.ctxs[c].parent) >= 0)
-        throw CfError(CF_E_UNSUPPORTED, "nested while_loop (frame " + name + ") not lowered yet");
       frame_id[name] = (int)frame_ctx.size();
       frame_ctx.push_back(c);
       P.frame_names.push_back(name);
+    }
+    // a while_loop nested in another one's body: a
+    // frame instance per iteration of the enclosing frame, run by the driver as one step of
+    // the enclosing body (runtime.cu OP_FRAME)
+    frame_parent.assign(frame_ctx.size(), -1);
+    for (size_t f = 0; f < frame_ctx.size(); ++f) {
+      const int pw = g.enclosing_while(g.ctxs[frame_ctx[f]].parent);
+      if (pw >= 0) {
+        frame_parent[f] = frame_id.at(g.ctxs[pw].name);
+        P.nested = true;
+        if (o.stack_budget_bytes >= 0)
+          throw CfError(CF_E_UNSUPPORTED, "stack swapping with nested while_loops");
+      }
     }
     for (auto& n : g.nodes) {
       int w = g.enclosing_while(n.ctx);
@@ -293,14 +306,27 @@ struct Compiler {
         throw CfError(CF_E_UNSUPPORTED, "cannot bound iterations of frame " + P.frame_names[f] +
                                             " (no TensorArray; set max_iterations)");
     }
+    // a nested frame's iteration indices run on over its instances (one instance per
+    // iteration of the enclosing frame): arenas and stack instances are indexed by them
+    frame_total.assign(frame_ctx.size(), 0);
+    std::function<int64_t(int)> total_of = [&](int f) -> int64_t {
+      if (frame_total[f] > 0) return frame_total[f];
+      return frame_total[f] = bound[f] * (frame_parent[f] >= 0 ? total_of(frame_parent[f]) : 1);
+    };
+    for (size_t f = 0; f < frame_ctx.size(); ++f) total_of((int)f);
     for (auto& n : g.nodes) {
       if (n.op == "StackCreate") {
         DStack& s = P.stacks[stack_id.at(n.id)];
         auto it = frame_id.find(n.attrs.s("frame"));
         if (it == frame_id.end()) unsupported(n, "stack of unknown frame");
         s.capacity = (int32_t)bound[it->second];
+        // created once per iteration of the frame around it (a nested loop's stack): one
+        // instance per iteration index of that frame
+        s.instances = frame_of[n.id] >= 0 ? (int32_t)frame_total[frame_of[n.id]] : 1;
         s.entry_off = P.stack_pool;
-        P.stack_pool += s.capacity;
+        s.depth_off = P.stack_depths;
+        P.stack_pool += s.capacity * s.instances;
+        P.stack_depths += s.instances;
       }
     }
     detect_accumulators();
@@ -516,12 +542,15 @@ struct Compiler {
       }
     int64_t total = root_heavy + 64 + (int64_t)fetches.size() + 2 * (int64_t)heavy_nodes.size() +
                     2 * (int64_t)P.accs.size();
-    for (size_t f = 0; f < frame_ctx.size(); ++f) total += frame_heavy[f] * (bound[f] + 1);
+    for (size_t f = 0; f < frame_ctx.size(); ++f)
+      total += frame_heavy[f] * (frame_total[f] + (frame_parent[f] >= 0 ? frame_total[frame_parent[f]] : 1));
     (void)per_iter_heavy;
     (void)max_tiles;
     P.inst_bound = total + 1024;
     P.branch_bound = 1;
-    for (auto b : bound) P.branch_bound = (int)std::max<int64_t>(P.branch_bound, b + 1);
+    // branch bits are indexed by the iteration index over all instances of a nested frame
+    for (size_t f = 0; f < bound.size(); ++f)
+      P.branch_bound = (int)std::max<int64_t>(P.branch_bound, frame_total[f] + 1);
 
     // ---- describe
     std::ostringstream ds;
@@ -539,7 +568,7 @@ struct Compiler {
     ds << "accumulators=" << P.accs.size() << " tma_operands=" << P.reg.size() << "\n";
     ds << "structured frames=" << P.structured_frames << " cond contexts="
        << (P.ctxs.empty() ? 0 : P.ctxs.size() - 1) << " waves=" << P.n_waves
-       << " heavy_batches=" << P.n_batches << "\n";
+       << " heavy_batches=" << P.n_batches << (P.nested ? " nested_frames=1" : "") << "\n";
     ds << "stacks: resident bytes=" << P.stack_resident_bytes << " swapped arenas=" << P.swaps.size()
        << " swapped bytes=" << P.stack_swapped_bytes << "\n";
     ds << "placements root=" << counts[0] << " ring=" << counts[1] << " arena=" << counts[2]
@@ -1114,6 +1143,114 @@ struct Compiler {
     *nctx = c2;
   }
 
+  // the top-most frame below `anc` on node x's frame chain (x inside a frame nested in anc), or -1
+  int child_frame_of(int x, int anc) const {
+    int f = frame_of[x];
+    if (g.nodes[x].op == "Exit") f = frame_id.at(g.nodes[x].attrs.s("frame"));
+    for (; f >= 0; f = frame_parent[f])
+      if (frame_parent[f] == anc) return f;
+    return -1;
+  }
+  // body program of a frame whose body holds nested frames: the nested
+  // frames are single steps (OP_FRAME) of the body, placed after the producers of their Enter
+  // inputs and before the consumers of their Exits; plain topological order (no level order,
+  // routing waves, heavy batches or structured conds in such a body)
+  void build_parent_frame(int f, const Ctx& ctx, const std::vector<int>& body, const std::vector<int>& enters,
+                          const std::vector<int>& exits, const std::vector<int>& children,
+                          const std::vector<int64_t>& bound, int* iter_base) {
+    const int N = (int)g.nodes.size();
+    std::set<int> bset(body.begin(), body.end());
+    auto item_of = [&](int x) -> int {
+      if (bset.count(x)) return x;
+      const int c = child_frame_of(x, f);
+      return c >= 0 ? N + c : -1;
+    };
+    std::vector<int> items(body.begin(), body.end());
+    for (int c : children) items.push_back(N + c);
+    std::map<int, std::set<int>> succ;
+    std::map<int, int> indeg;
+    for (int it : items) indeg[it] = 0;
+    auto edge = [&](int a, int b) {
+      if (a < 0 || b < 0 || a == b || !indeg.count(a) || !indeg.count(b)) return;
+      if (succ[a].insert(b).second) indeg[b]++;
+    };
+    for (int i = 0; i < N; ++i) {
+      const int dst = item_of(i);
+      if (dst < 0) continue;
+      if (dst == i && P.nodes[i].op == OP_MERGE_LOOP) continue;   // sources within an iteration
+      for (auto& t : g.nodes[i].in) edge(item_of(t.node), dst);
+      for (int cc : g.nodes[i].ctrl) edge(item_of(cc), dst);
+    }
+    for (auto& [a, b] : extra_edges[f]) edge(item_of(a), item_of(b));
+    std::vector<int> ready, ord;
+    for (int it : items)
+      if (indeg[it] == 0) ready.push_back(it);
+    std::sort(ready.rbegin(), ready.rend());
+    while (!ready.empty()) {
+      const int v = ready.back();
+      ready.pop_back();
+      ord.push_back(v);
+      for (int w : succ[v])
+        if (--indeg[w] == 0) {
+          ready.push_back(w);
+          std::sort(ready.rbegin(), ready.rend());
+        }
+    }
+    if (ord.size() != items.size())
+      throw CfError(CF_E_INVALID_GRAPH, "frame " + ctx.name + " body has a cycle without NextIteration");
+    DFrame& F = P.frames[f];
+    F.K = o.parallel_iterations > 0 ? o.parallel_iterations : ctx.K;
+    F.bound = (int32_t)bound[f];
+    F.parent = frame_parent[f];
+    F.body_off = (int)P.order.size();
+    for (int v : ord) P.order.push_back(v >= N ? ctx.loop_vars.at(0).enter : v);
+    F.n_body = (int)P.order.size() - F.body_off;
+    F.enter_off = (int)P.order.size();
+    F.n_enter = (int)enters.size();
+    P.order.insert(P.order.end(), enters.begin(), enters.end());
+    F.exit_off = (int)P.order.size();
+    F.n_exit = (int)exits.size();
+    P.order.insert(P.order.end(), exits.begin(), exits.end());
+    F.counter_switch = ctx.loop_vars.at(0).sw;
+    F.counter_enter = ctx.loop_vars.at(0).enter;
+    F.iter_base = *iter_base;
+    *iter_base += (int)bound[f] + 2;
+    F.bn_off = (int)P.body_nodes.size();
+    F.bi_off = (int)P.body_ivids.size();
+    for (int v : ord) {
+      DNode bn{};
+      if (v >= N) {
+        bn.op = OP_FRAME;
+        bn.aux[0] = v - N;
+        bn.place_off = -1;
+        ((int16_t*)bn.pad)[5] = -1;
+        bn.in_off = bn.ctrl_off = (int)P.body_ivids.size() - F.bi_off;
+        P.body_nodes.push_back(bn);
+        continue;
+      }
+      bn = P.nodes[v];
+      ((int16_t*)bn.pad)[5] = (int16_t)(v < 32768 ? v : -1);
+      bn.ctx = 0;
+      const int base = (int)P.body_ivids.size() - F.bi_off;
+      for (int j = 0; j < bn.n_in; ++j) P.body_ivids.push_back(P.in_vids[bn.in_off + j]);
+      for (int j = 0; j < bn.n_ctrl; ++j) P.body_ivids.push_back(P.in_vids[bn.ctrl_off + j]);
+      bn.in_off = base;
+      bn.ctrl_off = base + bn.n_in;
+      P.body_nodes.push_back(bn);
+    }
+    F.bi_count = (int)P.body_ivids.size() - F.bi_off;
+    while (P.body_ivids.size() % 4) P.body_ivids.push_back(0);
+    P.max_body = std::max(P.max_body, F.n_body);
+    P.max_bi = std::max(P.max_bi, F.bi_count);
+    F.acc_off = (int)P.order.size();
+    F.n_acc = 0;
+    for (size_t a = 0; a < P.accs.size(); ++a)
+      if (P.accs[a].frame == f) {
+        P.order.push_back((int)a);
+        F.n_acc++;
+      }
+  }
+
   void build_orders(const std::vector<int64_t>& bound) {
     const int N = (int)g.nodes.size();
     // arena allocation needs the bound. Stack swapping: when all arenas
@@ -1127,7 +1264,7 @@ struct Compiler {
       int np = n_places(g.nodes[i]);
       for (int p = 0; p < np; ++p)
         if (P.places[d.place_off + p].kind == PL_ARENA)
-          ars.push_back({i, p, frame_of[i], P.places[d.place_off + p].elem_bytes * bound[frame_of[i]]});
+          ars.push_back({i, p, frame_of[i], P.places[d.place_off + p].elem_bytes * frame_total[frame_of[i]]});
     }
     std::set<std::pair<int, int>> swap_set;
     if (o.stack_budget_bytes >= 0) {
@@ -1148,7 +1285,7 @@ struct Compiler {
     for (auto& a : ars) {
       const int i = a.node, p = a.port, f = a.frame;
       PlaceDesc& pl = P.places[P.nodes[i].place_off + p];
-      int slots = (int)bound[f];
+      int slots = (int)frame_total[f];   // = bound[f] for a top-level frame
       if (swap_set.count({i, p})) {
         const int K = o.parallel_iterations > 0 ? o.parallel_iterations : g.ctxs[frame_ctx[f]].K;
         slots = std::min<int>(K + 1, (int)bound[f]);
@@ -1190,10 +1327,18 @@ struct Compiler {
       for (int i = 0; i < N; ++i) {
         if (frame_of[i] != (int)f || fused_addn.count(i)) continue;
         if (g.nodes[i].op == "Enter" && g.nodes[i].attrs.s("frame") == ctx.name) enters.push_back(i);
+        else if (g.nodes[i].op == "Exit" && g.nodes[i].attrs.s("frame") != ctx.name) continue;   // a child's
         else body.push_back(i);
       }
       for (int i = 0; i < N; ++i)
         if (g.nodes[i].op == "Exit" && g.nodes[i].attrs.s("frame") == ctx.name) exits.push_back(i);
+      std::vector<int> children;
+      for (size_t c2 = 0; c2 < frame_ctx.size(); ++c2)
+        if (frame_parent[c2] == (int)f) children.push_back((int)c2);
+      if (!children.empty()) {
+        build_parent_frame((int)f, ctx, body, enters, exits, children, bound, &iter_base);
+        continue;
+      }
       std::set<int> bset(body.begin(), body.end());
       std::map<int, std::vector<int>> succ;
       std::map<int, int> indeg;
@@ -1264,6 +1409,7 @@ struct Compiler {
       DFrame& F = P.frames[f];
       F.K = o.parallel_iterations > 0 ? o.parallel_iterations : ctx.K;
       F.bound = (int32_t)bound[f];
+      F.parent = frame_parent[f];
       F.body_off = (int)P.order.size();
       for (size_t k = 0; k < ord.size(); ++k) {
         if (wave_len[k] > 0 || batch_len[k] > 0) P.order.push_back(ord[k]);   // the marker's slot (never evaluated)
@@ -1368,10 +1514,10 @@ struct Compiler {
     std::vector<int> items;
     for (int i = 0; i < N; ++i)
       if (frame_of[i] < 0 && g.nodes[i].op != "Exit") items.push_back(i);
-    for (size_t f = 0; f < frame_ctx.size(); ++f) items.push_back(N + (int)f);
+    for (size_t f = 0; f < frame_ctx.size(); ++f)
+      if (frame_parent[f] < 0) items.push_back(N + (int)f);
     auto item_of = [&](int node) -> int {
-      if (frame_of[node] >= 0) return N + frame_of[node];
-      if (g.nodes[node].op == "Exit") return N + frame_id.at(g.nodes[node].attrs.s("frame"));
+      if (frame_of[node] >= 0 || g.nodes[node].op == "Exit") return N + child_frame_of(node, -1);
       return node;
     };
     std::map<int, std::set<int>> succ;
@@ -1454,7 +1600,8 @@ HostProgram compile(const Graph& g, const CompileOpts& o, const std::vector<TRef
       for (int k = 0; k < F.n_body; ++k) {
         const auto& bn = c.P.body_nodes[F.bn_off + k];
         const int nid = c.P.order[F.body_off + k];
-        ls << k << " " << (bn.op == OP_WAVE ? std::string("WAVE") : bn.op == OP_HEAVY_BATCH ? std::string("BATCH") : g.nodes[nid].op) << " node=" << nid
+        ls << k << " " << (bn.op == OP_WAVE ? std::string("WAVE") : bn.op == OP_HEAVY_BATCH ? std::string("BATCH")
+                           : bn.op == OP_FRAME ? "FRAME " + c.P.frame_names[bn.aux[0]] : g.nodes[nid].op) << " node=" << nid
            << " ctx=" << bn.ctx << " gctx=" << g.nodes[nid].ctx;
         if (bn.op == OP_WAVE || bn.op == OP_HEAVY_BATCH) ls << " n=" << bn.aux[0];
         ls << " in=";

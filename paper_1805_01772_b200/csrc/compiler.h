@@ -69,6 +69,8 @@ struct HostProgram {
   int branch_bound = 1;
   int iter_counters = 0;
   int stack_pool = 0;
+  int stack_depths = 0;              // stack instances (one depth counter each)
+  bool nested = false;               // a frame inside another frame's body
   int ta_slots = 0;
   int64_t inst_bound = 0;            // upper bound of heavy instances per run
   int64_t tile_bound = 0;            // max tiles of one instance

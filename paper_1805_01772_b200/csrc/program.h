@@ -53,6 +53,7 @@ enum Op : int32_t {
   OP_RECV,          // cross-GPU Recv (aux0: channel index); output placed like a heavy output
   OP_WAVE,          // body-program marker: the next aux0 nodes are independent routing / stack
                     // nodes, evaluated in parallel by the driver CTA's helper warps
+  OP_FRAME,         // body-program step: run a nested frame (aux0: frame id) to its Exits
   OP_HEAVY_BATCH,   // body-program marker: the next aux0 nodes are tensor-core LSTM nodes of one
                     // phase (each input an earlier member's output or ready before the marker);
                     // their instances are built together, one helper lane per node
@@ -166,7 +167,7 @@ struct DFrame {
   int32_t acc_off, n_acc;       // accumulators initialised at frame start (into prog.order)
   int32_t bn_off;               // body program: DNodes in evaluation order (prog.body_nodes)
   int32_t bi_off, bi_count;     // their input ids (prog.body_ivids), offsets rebased
-  int32_t pad;
+  int32_t parent;               // enclosing frame (-1: root): one instance per parent iteration
 };
 
 struct DTA {
@@ -179,8 +180,10 @@ struct DTA {
 };
 
 struct DStack {
-  int32_t capacity;
-  int32_t entry_off;    // into the stack entry pool (Tok)
+  int32_t capacity;     // entries per instance
+  int32_t entry_off;    // into the stack entry pool (Tok); instance k at entry_off + k * capacity
+  int32_t instances;    // 1, or one per iteration index of the frame that creates the stack
+  int32_t depth_off;    // into the stack depth array (one depth per instance)
 };
 
 // Root program step: a node id (>= 0) or a frame (-(frame + 1)).
@@ -246,6 +249,8 @@ struct Prog {
   int32_t n_swaps, n_ctxs;
   const DSwap* swaps;
   const DCtx* ctxs;
+  int32_t nested;               // 1: a frame runs inside another frame's body (f2)
+  int32_t n_stack_depths;       // stack instances (depth counters)
 };
 
 // ---- heavy instance record (written by the driver, read by workers)

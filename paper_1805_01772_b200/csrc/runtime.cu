@@ -755,10 +755,13 @@ __device__ __forceinline__ int fast_node(const DNode* d, const FastEnv& e, FastC
       tk[d->ctrl_vid] = make_int4(0, 0, -1, (TK_FLOW << 8) | 1);
       return 1;
     }
-    const int sid = h.x;   // TK_HANDLE: v = stack id
+    // TK_HANDLE: v = stack id | instance << 20 (x = low 32 bits, y = high)
+    const long long hv = (long long)(((unsigned long long)(unsigned)h.y << 32) | (unsigned)h.x);
+    const int sid = (int)(hv & 0xFFFFF), inst = (int)(hv >> 20);
     const DStack& S = e.stacks[sid];
-    const int dp = e.depth[sid];
-    int4* pool = e.pool + S.entry_off;
+    const int di = S.depth_off + inst;
+    const int dp = e.depth[di];
+    int4* pool = e.pool + S.entry_off + (long long)inst * S.capacity;
     if (op == OP_STACK_PUSH) {
       if (dp >= S.capacity) {
         c.err = CF_E_STACK_BUDGET;
@@ -766,7 +769,7 @@ __device__ __forceinline__ int fast_node(const DNode* d, const FastEnv& e, FastC
         return -1;
       }
       pool[dp] = v;
-      e.depth[sid] = dp + 1;
+      e.depth[di] = dp + 1;
       c.push++;
       c.maxd = max(c.maxd, dp + 1);
     } else {
@@ -777,7 +780,7 @@ __device__ __forceinline__ int fast_node(const DNode* d, const FastEnv& e, FastC
       }
       int4 t = pool[dp - 1];
       t.w &= ~0xff;
-      e.depth[sid] = dp - 1;
+      e.depth[di] = dp - 1;
       tk[d->out_vid] = t;
       c.pop++;
     }
@@ -853,6 +856,20 @@ struct Driver {
   int32_t root_pc = 0, cur_frame = -1, iter = 0, body_pc = 0;
   bool iter_started = false, fetched = false;
   int32_t oldest = 0;
+  // nested frames: the enclosing frames' evaluation state, and the
+  // iteration index base of the current frame instance (indices run on over the instances
+  // of a nested frame: arena slots, stack instances and branch bits use them)
+  struct FrameSave {
+    const DNode* bn;
+    const int32_t* iv;
+    int32_t frame, iter, oldest, body_pc, gbase, started;
+  };
+  static constexpr int kMaxNest = 4;
+  FrameSave fstack_[kMaxNest];
+  int fdepth_ = 0;
+  int32_t gbase_ = 0;
+  int32_t gnext_[16] = {};
+  __forceinline__ __device__ int git() const { return cur_frame >= 0 ? gbase_ + iter : 0; }
   unsigned long long last_progress = 0;
   int64_t pend_mz = 0;
   int32_t last_dw = -1;
@@ -916,7 +933,7 @@ struct Driver {
     FastEnv e;
     e.tk = (int4*)toks_;
     e.iv = iv_;
-    e.it = cur_frame >= 0 ? iter : 0;
+    e.it = git();
     e.bb = P.branch_bound;
     e.bbits = A.branch_bits;
     e.lval = lval_;
@@ -1032,7 +1049,7 @@ struct Driver {
       w.env = fast_env();
       w.env_frame = cur_frame;
     }
-    w.env.it = cur_frame >= 0 ? iter : 0;
+    w.env.it = git();
     w.done = 0;
     __threadfence_block();
     *(volatile int*)&w.seq = w.seq + 1;
@@ -1540,7 +1557,7 @@ struct Driver {
   }
   __forceinline__ __device__ bool place_core(const DNode& d, int port, int64_t* ptr) {
     const PlaceDesc& pl = places_[d.place_off + port];
-    int it = cur_frame >= 0 ? iter : 0;
+    const int it = git();   // iteration index over all instances of a nested frame
     switch (pl.kind) {
       case PL_ROOT: *ptr = pl.base; return true;
       case PL_RING: *ptr = pl.base + (int64_t)(it % pl.slots) * pl.elem_bytes; return true;
@@ -2406,7 +2423,7 @@ struct Driver {
     if (k < 0) return 0;
     const DSwap& w = P.swaps[k];
     if (A.swap_owner[w.owner_off + r] == entry) return 0;   // still resident in its ring slot
-    const int it = cur_frame >= 0 ? iter : 0;
+    const int it = git();
     const int64_t dst = w.in_base + (int64_t)(it % w.in_ring) * w.elem_bytes;
     int32_t id = swap_copy(1, dst, w.host_base + (int64_t)dp * w.elem_bytes, w.elem_bytes, -1);
     if (id < 0) return -1;
@@ -2500,7 +2517,7 @@ struct Driver {
           o0.dead = pv != 0;   // false port: dead iff p
           o1.dead = pv == 0;   // true port: dead iff !p
           if (d.aux[0] >= 0) {
-            int it = cur_frame >= 0 ? iter : 0;
+            const int it = git();
             if (it < P.branch_bound) A.branch_bits[d.aux[0] * P.branch_bound + it] = pv ? 2 : 1;
           }
         }
@@ -2624,7 +2641,7 @@ struct Driver {
           o0.dead = pv != 0;   // false port: dead iff p
           o1.dead = pv == 0;   // true port: dead iff !p
           if (d.aux[0] >= 0 && d.aux[0] < P.n_conds) {
-            int it = cur_frame >= 0 ? iter : 0;
+            const int it = git();
             if (it < P.branch_bound) A.branch_bits[d.aux[0] * P.branch_bound + it] = pv ? 2 : 1;
           }
         }
@@ -2859,26 +2876,35 @@ struct Driver {
       case OP_STACK_CREATE: {
         Tok h{};
         h.kind = TK_HANDLE;
-        h.v = d.aux[0];
+        // handle = stack id | instance << 20: a stack created in a loop body (a nested loop's,
+        // SURVEY.md §8(f) f2) has one instance per iteration index of that loop
+        h.v = (int64_t)d.aux[0] | ((int64_t)git() << 20);
         h.writer = -1;
         h.dead = dead;
+        if (!dead && git() >= stacks_[d.aux[0]].instances) {
+          fail(CF_E_STACK_BUDGET, -900);
+          return EV_ERROR;
+        }
         set_out(d, 0, h);
         break;
       }
       case OP_STACK_PUSH: {
         if (!dead) {
-          int s = (int)in_tok(d, 0).v;
+          const int64_t hv = in_tok(d, 0).v;
+          const int s = (int)(hv & 0xFFFFF), inst = (int)(hv >> 20);
           const DStack& S = stacks_[s];
-          int dp = stack_depth_[s];
+          const int di = S.depth_off + inst;
+          const int64_t e0 = S.entry_off + (int64_t)inst * S.capacity;
+          int dp = stack_depth_[di];
           if (dp >= S.capacity) {
             fail(CF_E_STACK_BUDGET, dp);
             return EV_ERROR;
           }
           const Tok& pv = in_tok(d, 1);
-          A.stack_pool[S.entry_off + dp] = pv;
-          stack_depth_[s] = dp + 1;
+          A.stack_pool[e0 + dp] = pv;
+          stack_depth_[di] = dp + 1;
           n_push++;
-          if (P.n_swaps && pv.kind == TK_PTR && swap_out(pv, S.entry_off + dp, dp) < 0) return EV_ERROR;
+          if (P.n_swaps && pv.kind == TK_PTR && swap_out(pv, (int32_t)(e0 + dp), dp) < 0) return EV_ERROR;
           if (dp + 1 > max_depth) max_depth = dp + 1;
         }
         break;
@@ -2888,17 +2914,20 @@ struct Driver {
           set_dead_all(d);
           break;
         }
-        int s = (int)in_tok(d, 0).v;
+        const int64_t hv = in_tok(d, 0).v;
+        const int s = (int)(hv & 0xFFFFF), inst = (int)(hv >> 20);
         const DStack& S = stacks_[s];
-        int dp = stack_depth_[s];
+        const int di = S.depth_off + inst;
+        const int64_t e0 = S.entry_off + (int64_t)inst * S.capacity;
+        int dp = stack_depth_[di];
         if (dp <= 0) {
           fail(CF_E_POP_EMPTY, s);
           return EV_ERROR;
         }
-        Tok t = A.stack_pool[S.entry_off + dp - 1];
-        stack_depth_[s] = dp - 1;
+        Tok t = A.stack_pool[e0 + dp - 1];
+        stack_depth_[di] = dp - 1;
         t.dead = 0;
-        if (P.n_swaps && t.kind == TK_PTR && swap_in(&t, S.entry_off + dp - 1, dp - 1) < 0) return EV_ERROR;
+        if (P.n_swaps && t.kind == TK_PTR && swap_in(&t, (int32_t)(e0 + dp - 1), dp - 1) < 0) return EV_ERROR;
         set_out(d, 0, t);
         n_pop++;
         break;
@@ -2943,6 +2972,44 @@ struct Driver {
   }
 
   // ---------------------------------------------------------------- frames
+  // a frame nested in the current frame's body: one instance per iteration of the
+  // enclosing frame. The instance starts after everything created so far has completed (the
+  // previous instance's storage and the consumers of its Exits are then free); a dead
+  // instance (the enclosing frame's exiting iteration) only fires its Exits, dead.
+  __noinline__ __device__ void enter_nested(int f) {
+    const DFrame& F = P.frames[f];
+    bool dead = true;
+    for (int k = 0; k < F.n_enter && dead; ++k) dead = in_tok_g(node(P.order[F.enter_off + k]), 0).dead != 0;
+    if (dead || fdepth_ >= kMaxNest) {
+      if (!dead) fail(CF_E_UNSUPPORTED, -800);
+      for (int k = 0; k < F.n_exit; ++k) set_dead_all(node(P.order[F.exit_off + k]));
+      n_exitf += F.n_exit;
+      return;
+    }
+    while (outstanding > 0 && !st->error) {
+      const unsigned long long now = globaltimer();
+      if (drain()) last_progress = now;
+      else if ((long long)(now - last_progress) > A.watchdog_ns) fail(CF_E_DEADLOCK, -801);
+    }
+    fstack_[fdepth_++] = FrameSave{bn_, iv_, cur_frame, iter, oldest, body_pc, gbase_, iter_started ? 1 : 0};
+    start_frame(f);
+    gbase_ = f < 16 ? gnext_[f] : 0;
+  }
+  // the nested frame instance has fired its Exits: back to the enclosing body
+  __device__ void leave_nested() {
+    const int f = cur_frame;
+    if (f < 16) gnext_[f] = gbase_ + iter;
+    const FrameSave& s = fstack_[--fdepth_];
+    bn_ = s.bn;
+    iv_ = s.iv;
+    cur_frame = s.frame;
+    iter = s.iter;
+    oldest = s.oldest;
+    body_pc = s.body_pc;
+    gbase_ = s.gbase;
+    iter_started = s.started != 0;
+    cur_F_ = &P.frames[cur_frame];
+  }
   __noinline__ __device__ void start_frame(int f) {
     const DFrame& F = P.frames[f];
     for (int k = 0; k < F.n_enter; ++k) {
@@ -2953,8 +3020,9 @@ struct Driver {
       c.writer = -1;
       toks_[e.ctrl_vid] = c;
     }
-    // the frame's control program: staged in shared memory when there is room
-    if (sm_nodes_) {
+    // the frame's control program: staged in shared memory when there is room (not with
+    // nested frames: the enclosing body's program would be overwritten)
+    if (sm_nodes_ && !P.nested) {
       helper_copy(sm_nodes_, P.body_nodes + F.bn_off, (int64_t)F.n_body * sizeof(DNode), sm_iv_,
                   P.body_ivids + F.bi_off, (int64_t)F.bi_count * 4);
       bn_ = sm_nodes_;
@@ -2968,6 +3036,7 @@ struct Driver {
     oldest = 0;
     body_pc = 0;
     iter_started = false;
+    gbase_ = 0;
     // fused accumulators start from the loop variable's initial value
     for (int k = 0; k < F.n_acc; ++k) {
       int a = P.order[F.acc_off + k];
@@ -3015,7 +3084,7 @@ struct Driver {
           if (pt.kind == TK_IMM) pv = pt.v;
           else if (!scalar(pt, &pv)) return -1;
           live = (pv != 0) == (cx.branch == 1);
-          const int it = cur_frame >= 0 ? iter : 0;
+          const int it = git();
           if (cx.cond_id >= 0 && cx.cond_id < P.n_conds && it < P.branch_bound)
             A.branch_bits[cx.cond_id * P.branch_bound + it] = pv ? 2 : 1;
         }
@@ -3076,6 +3145,15 @@ struct Driver {
         progress = true;
         if (st->error) break;
         continue;
+      }
+      if (op == OP_FRAME) {   // a nested frame: run it to its Exits, then continue here
+        body_pc = pc + 1;
+        enter_nested(d->aux[0]);
+        progress = true;
+        n_push += fc.push;
+        n_pop += fc.pop;
+        if (fc.maxd > max_depth) max_depth = fc.maxd;
+        return progress;
       }
       if (op == OP_HEAVY_BATCH) {   // 1: build the members one by one (the general path)
         pc += run_batch(F, pc, d->aux[0]);
@@ -3186,7 +3264,11 @@ struct Driver {
         toks_[x.ctrl_vid] = c;
       }
       n_exitf += F.n_exit;
-      if (cur_frame < 16) st->trip[cur_frame] = iter;
+      if (cur_frame < 16) st->trip[cur_frame] += iter;   // summed over a nested frame's instances
+      if (F.parent >= 0) {
+        leave_nested();
+        return true;
+      }
       cur_frame = -1;
       root_pc++;
       return true;
@@ -3490,7 +3572,7 @@ __global__ void __launch_bounds__(kThreads, 1) cf_driver_kernel(RunArgs A_param)
     int32_t* s_tso = (int32_t*)carve(4 * (int64_t)P.n_tas);
     PlaceDesc* s_pl = (PlaceDesc*)carve((int64_t)P.n_places * sizeof(PlaceDesc));
     DReg* s_reg = (DReg*)carve((int64_t)P.n_reg * sizeof(DReg));
-    int32_t* s_sd = (int32_t*)carve(4 * (int64_t)P.n_stacks);
+    int32_t* s_sd = (int32_t*)carve(4 * (int64_t)P.n_stack_depths);
     int32_t* s_prep = (int32_t*)carve(4 * (int64_t)P.n_nodes);
     int32_t* s_dwc = (int32_t*)carve(4 * (int64_t)P.n_nodes);
     int32_t* s_accw = (int32_t*)carve(4 * (int64_t)P.n_accs);
@@ -3508,7 +3590,7 @@ __global__ void __launch_bounds__(kThreads, 1) cf_driver_kernel(RunArgs A_param)
     for (int i = threadIdx.x; s_tso && i < P.n_tas; i += blockDim.x) s_tso[i] = A.ta_slot_off[i];
     for (int i = threadIdx.x; s_pl && i < P.n_places; i += blockDim.x) s_pl[i] = P.places[i];
     for (int i = threadIdx.x; s_reg && i < P.n_reg; i += blockDim.x) s_reg[i] = P.reg[i];
-    for (int i = threadIdx.x; s_sd && i < P.n_stacks; i += blockDim.x) s_sd[i] = 0;
+    for (int i = threadIdx.x; s_sd && i < P.n_stack_depths; i += blockDim.x) s_sd[i] = 0;
     for (int i = threadIdx.x; s_prep && i < P.n_nodes; i += blockDim.x) s_prep[i] = -1;
     for (int i = threadIdx.x; s_dwc && i < P.n_nodes; i += blockDim.x) s_dwc[i] = 0;
     for (int i = threadIdx.x; s_accw && i < P.n_accs; i += blockDim.x) s_accw[i] = -1;
@@ -3831,6 +3913,8 @@ void build_session(cf_session* s, const cf::Graph& g, const cf_run_opts* o,
   pg.n_frames = (int)P.frames.size();
   pg.n_tas = (int)P.tas.size();
   pg.n_stacks = (int)P.stacks.size();
+  pg.n_stack_depths = P.stack_depths;
+  pg.nested = P.nested ? 1 : 0;
   pg.n_root_steps = (int)P.root_steps.size();
   pg.n_fetch = (int)P.fetches.size();
   pg.n_conds = P.n_conds;
@@ -3961,8 +4045,8 @@ void build_session(cf_session* s, const cf::Graph& g, const cf_run_opts* o,
   A.toks = (Tok*)dalloc(s, sizeof(Tok) * P.n_vids);
   s->zero_each_run.push_back({A.toks, sizeof(Tok) * P.n_vids});
   A.stack_pool = (Tok*)dalloc(s, sizeof(Tok) * std::max(P.stack_pool, 1));
-  A.stack_depth = (int32_t*)dalloc(s, 4 * std::max<size_t>(P.stacks.size(), 1));
-  s->zero_each_run.push_back({A.stack_depth, 4 * std::max<size_t>(P.stacks.size(), 1)});
+  A.stack_depth = (int32_t*)dalloc(s, 4 * std::max<size_t>(P.stack_depths, 1));
+  s->zero_each_run.push_back({A.stack_depth, 4 * std::max<size_t>(P.stack_depths, 1)});
   A.ta_base = (int64_t*)dalloc(s, 8 * std::max<size_t>(P.tas.size(), 1));
   std::vector<int32_t> slot_off;
   int so = 0;
@@ -4013,7 +4097,8 @@ void build_session(cf_session* s, const cf::Graph& g, const cf_run_opts* o,
   need += (sizeof(Tok) * (size_t)P.n_vids + 15) / 16 * 16;
   need += sizeof(DNode) * (size_t)P.max_body + ((size_t)P.max_bi * 4 + 15) / 16 * 16;
   need += sizeof(PlaceDesc) * P.places.size() + sizeof(DReg) * (P.reg.size() + P.feeds.size() + 1);
-  need += sizeof(DStack) * P.stacks.size() + 8 * P.nodes.size() + 4 * (P.accs.size() + P.iter_counters);
+  need += sizeof(DStack) * P.stacks.size() + 4 * (size_t)P.stack_depths + 8 * P.nodes.size() +
+          4 * (P.accs.size() + P.iter_counters);
   need += (sizeof(DTA) + 12) * P.tas.size() + 48;
   need += 16 * 12;
   // dynamic shared memory: what the opt-in limit leaves next to the kernel's static smem

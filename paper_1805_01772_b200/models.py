@@ -260,3 +260,37 @@ def static_rnn_lstm(T: int, B: int, I: int, H: int, L: int = 1, forget_bias: flo
         for nm, gt in zip(names, g.gradients(y, xs)):
             grads["d" + nm] = gt
     return RNNProgram(g, fetch, grads, T, B, I, H, L)
+
+
+def ponder_rnn(T: int, B: int, D: int, K: int = 32) -> RNNProgram:
+    """A while_loop nested in a while_loop (the adaptive-
+    computation RNN shape) through the C-ABI: for every step t the state takes x[t] and then
+    ponders n[t] times, ``a = tanh(a W + c)``; n[t] is fed (ragged inner trip counts). The
+    device runs the inner loop as a nested frame of the outer body and differentiates it with
+    nested gradient loops whose stacks are created once per outer iteration (their handles
+    saved on a stack of the outer loop). Loss sum(R * a_T)."""
+    g = Graph()
+    x = g.placeholder("x", F32, (T, B, D))
+    n = g.placeholder("n", I64, (T,))
+    W = g.placeholder("W", F32, (D, D))
+    c = g.placeholder("c", F32, (B, D))
+    a0 = g.placeholder("a0", F32, (B, D))
+    R = g.placeholder("R", F32, (B, D))
+    x_ta = g.tensor_array(T, F32, (B, D)).unstack(x)
+    n_ta = g.tensor_array(T, I64, ()).unstack(n)
+    t_bound = g.const(T, I64)
+
+    def step(t, a):
+        a = g.op1("Add", [a, x_ta.read(t)])
+        m = n_ta.read(t)
+        r = g.while_loop(lambda k, s: g.op1("Less", [k, m]),
+                         lambda k, s: [g.op1("Add", [k, g.const(1, I64)]),
+                                       g.op1("Tanh", [g.op1("Add", [g.op1("MatMul", [s, W]), c])])],
+                         [g.const(0, I64), a], K, name="ponder")
+        return [g.op1("Add", [t, g.const(1, I64)]), r[1]]
+    res = g.while_loop(lambda t, a: g.op1("Less", [t, t_bound]), step, [g.const(0, I64), a0], K,
+                       name="steps")
+    y = g.op1("ReduceSum", [g.op1("Mul", [R, res[1]])])
+    names = ["x", "W", "c", "a0"]
+    grads = {"d" + k: gt for k, gt in zip(names, g.gradients(y, [x, W, c, a0]))}
+    return RNNProgram(g, {"y": y, "aT": res[1]}, grads, T, B, D, D, 1)

@@ -51,6 +51,26 @@ def test_structure_matches_oracle(args, kw):
     assert p.g.validate() == []
 
 
+def test_nested_loop_structure_matches_oracle():
+    """f2: a while_loop nested in a while_loop with its recursive gradient (the ponder RNN):
+    same op counts as the oracle's builder + autodiff, and the device compiler lowers it (the
+    inner loop is one step, OP_FRAME, of the outer body; nested gradient loops likewise)."""
+    from paper_1805_01772_b200.models import ponder_rnn as dev_ponder
+    from oracle.models import ponder_rnn as oracle_ponder
+    p = dev_ponder(5, 3, 8)
+    q = oracle_ponder(5, 3, 8)
+    assert p.g.count_ops() == q.b.g.count_ops()
+    assert p.g.validate() == []
+    os.environ["CF_DEBUG_MAX_ITERATIONS"] = "8"
+    try:
+        lst = cf.debug_program_listing(p.g, p.fetch_tensors())
+    finally:
+        del os.environ["CF_DEBUG_MAX_ITERATIONS"]
+    assert "nested_frames=1" in lst
+    assert lst.count("FRAME ponder") == 2   # forward: ponder in steps; gradient: ponder_grad step
+    assert "FRAME ponder_grad" in lst
+
+
 def test_loop_example_structure_and_validate():
     g = cf.Graph()
     x = g.placeholder("x", cf.F32, (1, 1))
