@@ -704,10 +704,14 @@ struct Compiler {
         if (op == "StackPush" && idx == 1) *pinned = true;
         if (op == "TAWrite" && idx == 2 && same && frame_of[c] == frame && *ta_write < 0)
           *ta_write = c;
+        // Enter too: a value entering a nested frame (f2) may reach a StackPush there (e.g. a
+        // loop variable's initial value, pushed in the inner frame's first iteration); it must
+        // then live in an immutable arena slot, not the enclosing frame's ring
         bool route = op == "Identity" || op == "StopGradient" || op == "Reshape" ||
-                     op == "Switch" || op == "Merge" || op == "NextIteration" || op == "Exit";
+                     op == "Switch" || op == "Merge" || op == "NextIteration" || op == "Exit" ||
+                     op == "Enter";
         if (!route || (op == "Switch" && idx != 0)) continue;
-        bool nsame = same && op != "NextIteration" && op != "Exit";
+        bool nsame = same && op != "NextIteration" && op != "Exit" && op != "Enter";
         for (int p = 0; p < (int)cn.odt.size(); ++p) {
           int w = vbase[c] + p;
           if (seen.insert(w).second) st.push_back({w, nsame});

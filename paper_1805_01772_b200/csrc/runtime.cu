@@ -581,6 +581,7 @@ struct FastEnv {
   int4* tk;
   const int32_t* iv;
   int it, bb;
+  int git;                   // iteration index over all instances of a nested frame
   uint8_t* bbits;
   const int8_t* lval;        // liveness of structured cond contexts (this iteration)
   const DStack* stacks;
@@ -596,7 +597,8 @@ struct FastEnv {
   uint8_t* ta_written;
 };
 struct FastCount {
-  int push, pop, maxd, err, err_info;
+  int push, pop, maxd, err;
+  long long err_info;
 };
 // 1 = evaluated, 0 = needs the general evaluator (nothing written), -1 = error (in c.err)
 __device__ __forceinline__ int fast_node(const DNode* d, const FastEnv& e, FastCount& c) {
@@ -617,7 +619,7 @@ __device__ __forceinline__ int fast_node(const DNode* d, const FastEnv& e, FastC
       const bool p = (pt.x | pt.y) != 0;
       o0.w = (o0.w & ~0xff) | (p ? 1 : 0);   // false port dead iff p
       o1.w = (o1.w & ~0xff) | (p ? 0 : 1);
-      if (d->aux[0] >= 0 && e.it < e.bb) e.bbits[d->aux[0] * e.bb + e.it] = p ? 2 : 1;
+      if (d->aux[0] >= 0 && e.git < e.bb) e.bbits[d->aux[0] * e.bb + e.git] = p ? 2 : 1;
     }
     tk[d->out_vid] = o0;
     tk[d->out_vid + 1] = o1;
@@ -775,7 +777,7 @@ __device__ __forceinline__ int fast_node(const DNode* d, const FastEnv& e, FastC
     } else {
       if (dp <= 0) {
         c.err = CF_E_POP_EMPTY;
-        c.err_info = sid;
+        c.err_info = sid | ((long long)inst << 20);
         return -1;
       }
       int4 t = pool[dp - 1];
@@ -875,7 +877,7 @@ struct Driver {
   int32_t last_dw = -1;
   unsigned long long lq_tail = 0;
   // pending channel waits (HK_WAIT instances), polled by drain()
-  static constexpr int kMaxWaits = 128;   // f3 exchange at 8 GPUs: 2 x 8 layers x 7 peers = 112 Recvs
+  static constexpr int kMaxWaits = 64;   // f3's exchange at 4 GPUs needs 2 x 8 layers x 3 peers = 48
   struct ChanWait {
     unsigned long long* flag;
     unsigned long long want;
@@ -933,7 +935,8 @@ struct Driver {
     FastEnv e;
     e.tk = (int4*)toks_;
     e.iv = iv_;
-    e.it = git();
+    e.it = cur_frame >= 0 ? iter : 0;   // the frame instance's own iteration (loop Merges)
+    e.git = git();                       // over a nested frame's instances (branch bits)
     e.bb = P.branch_bound;
     e.bbits = A.branch_bits;
     e.lval = lval_;
@@ -1049,7 +1052,8 @@ struct Driver {
       w.env = fast_env();
       w.env_frame = cur_frame;
     }
-    w.env.it = git();
+    w.env.it = cur_frame >= 0 ? iter : 0;
+    w.env.git = git();
     w.done = 0;
     __threadfence_block();
     *(volatile int*)&w.seq = w.seq + 1;
@@ -2921,7 +2925,7 @@ struct Driver {
         const int64_t e0 = S.entry_off + (int64_t)inst * S.capacity;
         int dp = stack_depth_[di];
         if (dp <= 0) {
-          fail(CF_E_POP_EMPTY, s);
+          fail(CF_E_POP_EMPTY, s | ((int64_t)inst << 20));
           return EV_ERROR;
         }
         Tok t = A.stack_pool[e0 + dp - 1];
@@ -4106,7 +4110,7 @@ void build_session(cf_session* s, const cf::Graph& g, const cf_run_opts* o,
   CUDA_OK(cudaFuncGetAttributes(&fa, cf_driver_kernel));
   int optin = 0;
   CUDA_OK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, s->device));
-  const size_t smem_cap = (size_t)optin - fa.sharedSizeBytes - 1024;
+  const size_t smem_cap = (size_t)optin - fa.sharedSizeBytes;
   if ((size_t)s->dyn_smem > smem_cap) throw cf::CfError(CF_E_CUDA, "tile engine does not fit in shared memory");
   if ((int)std::min(need, smem_cap) > s->dyn_smem) s->dyn_smem = (int)std::min(need, smem_cap);
   A.dyn_smem = s->dyn_smem;
@@ -4290,8 +4294,10 @@ cf_status cf_run(cf_session* s, int32_t n_feed, const char* const* feed_names,
     RunState st;
     CUDA_OK(cudaMemcpy(&st, A.st, sizeof(RunState), cudaMemcpyDeviceToHost));
     if (st.error) {
+      std::string tr;
+      for (int f = 0; f < (int)P.frames.size() && f < 16; ++f) tr += (f ? "," : "") + std::to_string(st.trip[f]);
       throw cf::CfError(st.error, "device driver error " + std::to_string(st.error) + " (info " +
-                                      std::to_string(st.error_info) + ")");
+                                      std::to_string(st.error_info) + "; trips so far " + tr + ")");
     }
     std::vector<uint8_t> dead(std::max<size_t>(P.fetches.size(), 1));
     CUDA_OK(cudaMemcpy(dead.data(), A.fetch_dead, dead.size(), cudaMemcpyDeviceToHost));
