@@ -38,11 +38,14 @@ def _device(T, B, D, f, K):
     return {n: o.double().cpu().numpy() for n, o in zip(p.fetch_names(), outs)}, tr
 
 
+@pytest.mark.parametrize("K", [2, 32])
 @pytest.mark.parametrize("counts", [[2, 2, 2, 2, 2], [1, 3, 0, 2, 4], [0, 0, 1, 0, 0]])
-def test_ponder_rnn_matches_oracle(counts):
+def test_ponder_rnn_matches_oracle(counts, K):
+    """K = 2: the enclosing loop's ring wraps (5 steps, 3 slots); a loop variable's initial
+    value enters the inner frame from that ring and is pushed there: it must be pinned."""
     T, B, D = 5, 3, 64
     f = _feeds(T, B, D, 3, counts)
-    dev, tr = _device(T, B, D, f, 32)
+    dev, tr = _device(T, B, D, f, K)
     ref, otr = run_program(oracle_ponder(T, B, D), f, return_trace=True)
     for k, v in ref.items():
         r = np.asarray(v, dtype=np.float64)
