@@ -948,7 +948,7 @@ struct Compiler {
     }
     nctx->clear();
     for (int v : ord) nctx->push_back(dctx_of(g.nodes[v].ctx));
-    if (P.ctxs.size() > 64) throw CfError(CF_E_UNSUPPORTED, "more than 63 cond contexts in one program");
+    if (P.ctxs.size() > 128) throw CfError(CF_E_UNSUPPORTED, "more than 127 cond contexts in one program");
     // predicates may themselves be captures
     for (auto& d : P.ctxs)
       for (auto it = alias->find(d.pred_vid); it != alias->end(); it = alias->find(d.pred_vid))
@@ -1440,17 +1440,19 @@ struct Compiler {
           DNode wm{};
           wm.op = OP_WAVE;
           wm.aux[0] = wave_len[k];
-          unsigned long long mask = 0;   // contexts the wave's nodes read
+          unsigned long long mask[2] = {0, 0};   // contexts the wave's nodes read (128 bits)
+          auto add = [&](int c) { mask[c >> 6] |= 1ULL << (c & 63); };
           for (int q = 0; q < wave_len[k]; ++q) {
             const int u = ord[k + q];
-            if (node_ctx[k + q] > 0) mask |= 1ULL << node_ctx[k + q];
+            if (node_ctx[k + q] > 0) add(node_ctx[k + q]);
             if (P.nodes[u].op == OP_MERGE && g.nodes[u].attrs.has("cond_id") && !alias.empty()) {
               int c0 = merge_branch_ctx(u, 0), c1 = merge_branch_ctx(u, 1);
-              if (c0 > 0) mask |= 1ULL << c0;
-              if (c1 > 0) mask |= 1ULL << c1;
+              if (c0 > 0) add(c0);
+              if (c1 > 0) add(c1);
             }
           }
-          wm.imm[0] = (int64_t)mask;
+          wm.imm[0] = (int64_t)mask[0];
+          wm.imm[1] = (int64_t)mask[1];
           wm.place_off = -1;
           wm.in_off = wm.ctrl_off = (int)P.body_ivids.size() - F.bi_off;
           P.body_nodes.push_back(wm);

@@ -817,6 +817,7 @@ struct Wave {
   int lev_start[16], lev_n[16];
   unsigned long long lev_ctx[16];   // cond contexts each level reads (evaluated by a helper lane
                                     // before the level when the driver did not know them yet)
+  unsigned long long lev_ctx_hi[16];   // contexts 64..127
   int cstop;              // level the helpers could not start (a context's predicate was not
                           // available yet), or -1
   int hdead, hfail;
@@ -911,11 +912,11 @@ struct Driver {
   int32_t max_depth = 0, n_exitf = 0;
   // structured cond contexts (reading R20): liveness per context, valid for generation lgen_
   // (one generation per started iteration)
-  static constexpr int kMaxCtx = 64;
+  static constexpr int kMaxCtx = 128;
   uint32_t lgen_ = 1;
   uint32_t lstamp_[kMaxCtx];
   int8_t lval_[kMaxCtx];
-  DCtx ctxs_[kMaxCtx];
+  const DCtx* ctxs_ = nullptr;   // the program's table (global memory)
   Tok* toks_;            // token table: driver-CTA shared memory when it fits, else global
   const int32_t* iv_;    // input-id table of the nodes being evaluated
   const DNode* bn_;      // current frame's body program (smem copy or global)
@@ -1005,8 +1006,9 @@ struct Driver {
     Region rg(this, 32 + 13);
     chain_ok_ = false;
     // contexts whose liveness the wave's nodes read (bit mask from the compiler, marker imm0)
-    for (unsigned long long m = (unsigned long long)bn_[pc].imm[0]; m; m &= m - 1)
-      if (ctx_live(__ffsll((long long)m) - 1) < 0) return false;
+    for (int hw = 0; hw < 2; ++hw)
+      for (unsigned long long m = (unsigned long long)bn_[pc].imm[hw]; m; m &= m - 1)
+        if (ctx_live(64 * hw + __ffsll((long long)m) - 1) < 0) return false;
     Wave& w = *wave_;
     int nlev = 0, q = pc;
     // consecutive waves fuse into one job; a level reading cond contexts not known yet has them
@@ -1016,16 +1018,18 @@ struct Driver {
       w.lev_start[nlev] = q + 1;
       w.lev_n[nlev] = bn_[q].aux[0];
       w.lev_ctx[nlev] = (unsigned long long)bn_[q].imm[0];
+      w.lev_ctx_hi[nlev] = (unsigned long long)bn_[q].imm[1];
       ++nlev;
       q += bn_[q].aux[0] + 1;
       if (nlev == kMaxLev || q >= F.n_body || bn_[q].op != OP_WAVE || (dbg_ & (1 << 25))) break;
       if (dbg_ & (1 << 31)) {
         bool known = true;
-        for (unsigned long long m = (unsigned long long)bn_[q].imm[0]; m && known; m &= m - 1) {
-          const int c = __ffsll((long long)m) - 1;
-          for (int x = c; x; x = ctxs_[x].parent)
-            if (lstamp_[x] != lgen_) known = false;
-        }
+        for (int hw = 0; hw < 2; ++hw)
+          for (unsigned long long m = (unsigned long long)bn_[q].imm[hw]; m && known; m &= m - 1) {
+            const int c = 64 * hw + __ffsll((long long)m) - 1;
+            for (int x = c; x; x = ctxs_[x].parent)
+              if (lstamp_[x] != lgen_) known = false;
+          }
         if (!known) break;
       }
     }
@@ -3101,12 +3105,13 @@ struct Driver {
 
   // contexts of mask m for a fused wave level, evaluated by a helper lane between levels (the
   // driver thread is waiting for the job): false when a predicate is not available yet
-  __noinline__ __device__ bool helper_ctx(unsigned long long m) {
-    for (; m; m &= m - 1) {
-      const int c = __ffsll((long long)m) - 1;
-      if (lstamp_[c] == lgen_) continue;
-      if (ctx_live(c) < 0) return false;
-    }
+  __noinline__ __device__ bool helper_ctx(unsigned long long m0, unsigned long long m1) {
+    for (int hw = 0; hw < 2; ++hw)
+      for (unsigned long long m = hw ? m1 : m0; m; m &= m - 1) {
+        const int c = 64 * hw + __ffsll((long long)m) - 1;
+        if (lstamp_[c] == lgen_) continue;
+        if (ctx_live(c) < 0) return false;
+      }
     return true;
   }
 
@@ -3646,8 +3651,8 @@ __global__ void __launch_bounds__(kThreads, 1) cf_driver_kernel(RunArgs A_param)
         d.tso_ = s_tso;
       }
       for (int f = 0; f < P.n_frames && f < Driver::kIbCache; ++f) d.ib_[f] = P.frames[f].iter_base;
+      d.ctxs_ = P.ctxs;
       for (int c = 0; c < P.n_ctxs && c < Driver::kMaxCtx; ++c) {
-        d.ctxs_[c] = P.ctxs[c];
         d.lstamp_[c] = 0;
         d.lval_[c] = 0;
       }
@@ -3674,8 +3679,9 @@ __global__ void __launch_bounds__(kThreads, 1) cf_driver_kernel(RunArgs A_param)
             const int hl = wave_lane(threadIdx.x);
             int k = 0;
             for (; k < wave.nlev; ++k) {
-              if (k > 0 && wave.lev_ctx[k]) {   // contexts of this level, known or evaluated now
-                if (hl == 0 && !((Driver*)drv_obj)->helper_ctx(wave.lev_ctx[k])) wave.cstop = k;
+              if (k > 0 && (wave.lev_ctx[k] | wave.lev_ctx_hi[k])) {   // this level's contexts
+                if (hl == 0 && !((Driver*)drv_obj)->helper_ctx(wave.lev_ctx[k], wave.lev_ctx_hi[k]))
+                  wave.cstop = k;
                 __threadfence_block();
                 asm volatile("bar.sync 1, %0;" ::"r"(32 * kWaveWarps) : "memory");
                 if (wave.cstop >= 0) break;

@@ -114,6 +114,12 @@ __device__ void tile_prep_wt(const Inst& I, int tile, float* sm) {
 // TMEM loads share one wait. sigma(x) = 0.5 tanh(x / 2) + 0.5 (one MUFU op instead of ex2 + a
 // division).
 __device__ __forceinline__ float sigm_tanh(float x) { return fmaf(0.5f, tanhf_(0.5f * x), 0.5f); }
+// staging of the forward epilogue in the tile engine's stage buffers (free once the mainloop
+// completed): gates rows of 512 B and h rows of 128 B, each padded by 16 B (a quarter warp's
+// 16-byte stores to 8 consecutive rows hit distinct banks), then one live flag per row
+constexpr int kFwdGRow = 512 + 16, kFwdHRow = 128 + 16;
+constexpr int kFwdHOff = 256 * kFwdGRow, kFwdLOff = kFwdHOff + 256 * kFwdHRow;
+static_assert(kFwdLOff + 256 <= tc::kStages * (tc::kStageA + tc::kStageBmax), "forward staging fits");
 template <class Hook>
 __device__ void tile_lstm_fwd_tc(const Inst& I, int tile, tc::TcShared& ts, uint32_t& cnt,
                                  uint32_t& cnt2, uint32_t& ntile, float* sm, Hook hook) {
@@ -178,7 +184,11 @@ __device__ void tile_lstm_fwd_tc(const Inst& I, int tile, tc::TcShared& ts, uint
   const int ahead = pfd == 15 ? 0 : pfd ? pfd : 4;
   if (m2) tc::tc_tile2(ts, nk, 0, 0, cnt2, ntile, plan_a, plan_b, 256, ahead, hook);
   else tc::tc_tile(ts, nk, 256, 0, 0, cnt, ntile, plan_a, plan_b, hook);
-  // ---- fused epilogue: 2 (or 4) groups of 16 units x 4 gates per thread
+  // ---- fused epilogue: 2 (or 4) groups of 16 units x 4 gates per thread. The gates and h are
+  // staged in the (now idle) pipeline stage buffers and written out coalesced (debug flag bit
+  // 21: direct per-row stores, A/B)
+  const bool staged = !(kDbgFlagsTC & (1 << 21));
+  uint8_t* stg = ts.a[0];
   const int nit = 2 * nh;
   // fully unrolled: the double-buffered c_prev registers are indexed by constants (a runtime
   // index would put them in local memory)
@@ -211,6 +221,30 @@ __device__ void tile_lstm_fwd_tc(const Inst& I, int tile, tc::TcShared& ts, uint
       cn[i] = zf[i] * cp[i] + zi[i] * zg[i];
       hn[i] = zo[i] * tanhf_(cn[i]);
     }
+    if (staged) {
+      // gates and h into shared memory (padded rows: conflict-free 16-byte stores), c direct
+      const int rl = 128 * half + 32 * (warp % 4) + lane;
+      uint8_t* g0 = stg + rl * kFwdGRow + cu * 2;
+      store_bf16x16((__nv_bfloat16*)(g0 + 0), zi);
+      store_bf16x16((__nv_bfloat16*)(g0 + 128), zf);
+      store_bf16x16((__nv_bfloat16*)(g0 + 256), zg);
+      store_bf16x16((__nv_bfloat16*)(g0 + 384), zo);
+      __nv_bfloat16* h0 = (__nv_bfloat16*)(stg + kFwdHOff + rl * kFwdHRow + cu * 2);
+      if (live_h[half]) {
+        store_bf16x16(h0, hn);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) ((float4*)(c_next + o))[q] = *(float4*)&cn[4 * q];
+      } else {
+        // finished row (reading R10): state copied through, output zero (at the copy-out)
+        float hp[16];
+        load_bf16x16(h_prev + o, hp);
+        store_bf16x16(h0, hp);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) ((float4*)(c_next + o))[q] = *(float4*)&cp[4 * q];
+      }
+      if ((it & 1) == 0) stg[kFwdLOff + rl] = live_h[half] ? 1 : 0;
+      continue;
+    }
     __nv_bfloat16* gr = gates + (int64_t)r * 4 * H + nt * 256 + cu;
     store_bf16x16(gr + 0, zi);
     store_bf16x16(gr + 64, zf);
@@ -231,6 +265,25 @@ __device__ void tile_lstm_fwd_tc(const Inst& I, int tile, tc::TcShared& ts, uint
 #pragma unroll
       for (int q = 0; q < 4; ++q) ((float4*)(c_next + o))[q] = *(float4*)&cp[4 * q];
     }
+  }
+  if (staged && !(kDbgFlagsTC & (1 << 20))) {
+    // coalesced copy-out: a warp writes a whole 512-byte gates row (or four 128-byte h / out
+    // rows) per instruction instead of 32 row fragments
+    __syncthreads();
+    const int nrows = min(128 * nh, B - m0);
+    for (int rr = warp; rr < nrows; rr += 8) {
+      const uint4 v = *(const uint4*)(stg + rr * kFwdGRow + lane * 16);
+      *(uint4*)((uint8_t*)(gates + (int64_t)(m0 + rr) * 4 * H + nt * 256) + lane * 16) = v;
+    }
+    for (int q = threadIdx.x; q < nrows * 8; q += 256) {
+      const int rr = q >> 3, ch = q & 7;
+      const uint4 v = *(const uint4*)(stg + kFwdHOff + rr * kFwdHRow + ch * 16);
+      const int64_t ob = ((int64_t)(m0 + rr) * H + nt * 64) * 2 + ch * 16;
+      *(uint4*)((uint8_t*)h_next + ob) = v;
+      *(uint4*)((uint8_t*)out + ob) = stg[kFwdLOff + rr] ? v : make_uint4(0, 0, 0, 0);
+    }
+    // the next tile's TMA (async proxy) overwrites these stage buffers
+    tc::fence_proxy_async_smem();
   }
   tc::tc_tile_end();
 }
@@ -395,6 +448,11 @@ __device__ void tile_lstm_dxh_tc(const Inst& I, int tile, tc::TcShared& ts, uint
   };
   if (m2) tc::tc_tile2(ts, (4 * H) / 64, 0, 0, cnt2, ntile, plan_a, plan_b, bn, 0, hook);
   else tc::tc_tile(ts, (4 * H) / 64, 256, 0, 0, cnt, ntile, plan_a, plan_b, hook);
+  // epilogue: per 128-row half, the accumulator goes through the (idle) stage buffers and out
+  // as whole 1 KB rows (debug flag bit 21: direct per-row stores, A/B)
+  const bool staged = !(kDbgFlagsTC & (1 << 21)) && bn == 256;
+  uint8_t* stg = ts.a[0];
+  constexpr int kRow = 1024 + 16;   // 256 fp32 + pad (conflict-free 16-byte stores)
   for (int half = 0; half < (m2 ? 2 : 1); ++half) {
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int r = m0 + 128 * half + 32 * (warp % 4) + lane;
@@ -407,26 +465,47 @@ __device__ void tile_lstm_dxh_tc(const Inst& I, int tile, tc::TcShared& ts, uint
   float* dh = (float*)I.p[12];
   const bool dead_row = r < B && masked && !(t < lens[r]);
   const int cw = bn / 2;   // columns per warp group
+  const int rl = 32 * (warp % 4) + lane;
   for (int c = (warp / 4) * cw; c < (warp / 4) * cw + cw; c += 16) {
     float v[16];
     tc::tc_acc16(ts, tcol + c, v);
     if (r >= B) continue;
     const int n = nt * bn + c;
+    if (n >= In && dead_row) {
+      const int64_t o = (int64_t)r * H + (n - In);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) *(float4*)&v[4 * q] = ((const float4*)(dhn + o))[q];
+    }
+    if (staged) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) *(float4*)(stg + rl * kRow + (c + 4 * q) * 4) = *(float4*)&v[4 * q];
+      continue;
+    }
     if (n < In) {
       float* d = dx + (int64_t)r * In + n;
 #pragma unroll
       for (int q = 0; q < 4; ++q) ((float4*)d)[q] = *(float4*)&v[4 * q];
     } else {
       const int64_t o = (int64_t)r * H + (n - In);
-      if (dead_row) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) *(float4*)&v[4 * q] = ((const float4*)(dhn + o))[q];
-      }
 #pragma unroll
       for (int q = 0; q < 4; ++q) ((float4*)(dh + o))[q] = *(float4*)&v[4 * q];
     }
   }
+  if (staged) {
+    __syncthreads();
+    const int n0 = nt * bn;
+    float* dst = n0 < In ? dx + n0 : dh + (n0 - In);
+    const int64_t ld = n0 < In ? In : H;
+    const int nrows = min(128, B - (m0 + 128 * half));
+    for (int q = threadIdx.x; q < nrows * 64; q += 256) {   // 64 x 16 B per row
+      const int rr = q >> 6, ch = q & 63;
+      *(uint4*)((uint8_t*)(dst + (int64_t)(m0 + 128 * half + rr) * ld) + ch * 16) =
+          *(const uint4*)(stg + rr * kRow + ch * 16);
+    }
+    __syncthreads();
   }
+  }
+  if (staged) tc::fence_proxy_async_smem();   // the next tile's TMA overwrites the stage buffers
   tc::tc_tile_end();
 }
 
