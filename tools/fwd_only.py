@@ -15,6 +15,9 @@ from paper_1805_01772_b200.models import dynamic_rnn_lstm, feeds_to_device  # no
 from synth import rnn_inputs  # noqa: E402
 
 c = dict(CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "cfg3"])
+for k in ("B", "T", "L", "H", "I"):   # overrides, e.g. B=1024
+    if os.environ.get(k):
+        c[k] = int(os.environ[k])
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 1
 p = dynamic_rnn_lstm(c["T"], c["B"], c["I"], c["H"], c["L"], with_grads=False)
 s = cf.Session(p.g, p.fetch_tensors(), precision=cf.BF16)
@@ -29,6 +32,6 @@ for fl in flags:
         _, _, tr = s.run(dev, outs, trace=True)
         ts.append(tr["wall_ms"])
     torch.cuda.synchronize()
-    print(f"forward only (flags {fl}): {sorted(ts)[len(ts) // 2]:.2f} ms median of {reps}, "
-          f"{tr['instances']} instances")
+    print(f"forward only (flags {fl}, B={c['B']} T={c['T']} L={c['L']}): {sorted(ts)[len(ts) // 2]:.2f} ms "
+          f"median of {reps}, {tr['instances']} instances")
 cf.debug_set_flags(0)
