@@ -528,7 +528,7 @@ struct Compiler {
     std::vector<int64_t> frame_heavy(frame_ctx.size(), 0);
     for (int nid : heavy_nodes) {
       int f = frame_of[nid];
-      int k = g.nodes[nid].op == "LSTMCellGrad" ? 3 : 1;
+      int k = g.nodes[nid].op == "LSTMCellGrad" ? 3 : xproj(g.nodes[nid]) ? 2 : 1;
       if (g.nodes[nid].op == "AddN" && g.nodes[nid].in.size() > 8)   // a chain of 8-input sums
         k = 1 + (int)((g.nodes[nid].in.size() - 8 + 6) / 7);
       if (f >= 0) frame_heavy[f] += k + 4;
@@ -673,7 +673,7 @@ struct Compiler {
                          "of 256 (use CF_F32 for other shapes)");
       }
       d.aux[0] = op == "LSTMCell" ? HK_LSTM_FWD : HK_LSTM_BWD_EW;
-      d.aux[1] = n.attrs.b("masked");
+      d.aux[1] = n.attrs.b("masked") | (xproj(n) ? 4 : 0);   // bit 2: x-projection split
       d.imm[0] = g.shape(n.in[0])[0];
       d.imm[1] = g.shape(n.in[0])[1];
       d.imm[2] = g.shape(n.in[1])[1];
@@ -811,10 +811,15 @@ struct Compiler {
   }
 
   // number of placement slots of a heavy node: outputs + internal scratch / prep buffers
+  // forward cells whose input projection runs as its own instance ahead of the recurrence
+  // (runtime.cu HK_LSTM_XPROJ_TC; CF_NO_XPROJ=1 keeps one fused instance, A/B)
+  bool xproj(const Node& n) const {
+    return bf16() && n.op == "LSTMCell" && !std::getenv("CF_NO_XPROJ");
+  }
   int n_places(const Node& n) const {
     int np = (int)n.odt.size();
     if (n.op == "LSTMCellGrad") np += bf16() ? 2 : 1;   // dz scratch (+ W^T prep)
-    if (n.op == "LSTMCell" && bf16()) np += 1;           // gate-interleaved W prep
+    if (n.op == "LSTMCell" && bf16()) np += xproj(n) ? 2 : 1;   // W prep (+ x-projection scratch)
     return np;
   }
 
@@ -829,7 +834,7 @@ struct Compiler {
       Shape shp;
       int32_t dd;
       bool internal = p >= nout;
-      enum { NONE, DZ, WPREP, WTPREP } kind = NONE;
+      enum { NONE, DZ, WPREP, WTPREP, ZX } kind = NONE;
       int64_t extra_bytes = 0;
       if (!internal) {
         shp = n.osh[p];
@@ -840,6 +845,10 @@ struct Compiler {
         shp = {B, 4 * H};
         dd = bf16() ? D_BF16 : D_F32;
         if (bf16()) extra_bytes = ((B + 127) / 128) * 4 * H * 4;   // db partials
+      } else if (n.op == "LSTMCell" && p == nout + 1) {
+        kind = ZX;   // x-projection [B, 4H] fp32, gate-interleaved like the gates
+        shp = {g.shape(n.in[0])[0], 4 * g.shape(n.in[1])[1]};
+        dd = D_F32;
       } else {
         kind = n.op == "LSTMCell" ? WPREP : WTPREP;
         Shape w = g.shape(n.in[3]);

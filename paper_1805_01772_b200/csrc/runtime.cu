@@ -1127,7 +1127,8 @@ struct Driver {
            d.n_ctrl <= 32 && prep_nplace(d) <= 8;
   }
   __device__ int prep_nplace(const DNode& d) const {
-    return d.n_out + (d.aux[0] == HK_LSTM_BWD_EW ? 2 : 1);
+    // backward: dz scratch + W^T prep; forward: W prep (+ the x-projection scratch)
+    return d.n_out + (d.aux[0] == HK_LSTM_BWD_EW ? 2 : (d.aux[1] & 4) ? 2 : 1);
   }
   __device__ void heavy_prep_lane(Wave& w, int h) {
     const DNode& d = *w.hd;
@@ -1705,8 +1706,8 @@ struct Driver {
       long long q0 = (kProfBuild && A.prof) ? clock64() : 0;
       // outp / pm / ps may live in the Wave (helper results): copy them before the next wave
       // job is started below
-      int64_t op_[5];
-      for (int k = 0; k < 5; ++k) op_[k] = outp[k];
+      int64_t op_[6];
+      for (int k = 0; k < 6; ++k) op_[k] = outp[k];
       int32_t pw = prep(d, nid, HK_PREP_WP, op_[4]);
       int64_t mx, sx, mh, sh, mw, sw;
       if (pm) {
@@ -1721,8 +1722,21 @@ struct Driver {
       // 256-row tiles (tc_tile2) trade tile count for operand bytes: only for large batches;
       // the recurrence wants many short tiles (measured on cfg3)
       const bool m2 = B >= kM2MinRows;
-      int32_t id = new_inst(HK_LSTM_FWD_TC, masked | (m2 ? 2 : 0),
-                            (int)((m2 ? (B + 255) / 256 : (B + 127) / 128) * (H / 64)));
+      const bool split = d.aux[1] & 4;   // x-projection ahead of the recurrence
+      const int ntiles = (int)((m2 ? (B + 255) / 256 : (B + 127) / 128) * (H / 64));
+      int32_t xp = -1;
+      if (split) {
+        xp = new_inst(HK_LSTM_XPROJ_TC, m2 ? 2 : 0, ntiles);
+        if (xp < 0) return EV_ERROR;
+        Inst& X = A.insts[xp];
+        X.m = B; X.k = In; X.n = H;
+        X.p[0] = mx; X.p[3] = mw; X.p[7] = outp[5];
+        X.s[2] = sx;
+        add_dep(xp, in_tok(d, 0).writer);
+        add_dep(xp, pw);
+        submit(xp);
+      }
+      int32_t id = new_inst(HK_LSTM_FWD_TC, masked | (m2 ? 2 : 0) | (split ? 4 : 0), ntiles);
       long long q2 = (kProfBuild && A.prof) ? clock64() : 0;
       if (kProfBuild && A.prof) { op_cyc[32 + 15] += q2 - q1; op_cnt[32 + 15]++; }
       if (id < 0) return EV_ERROR;
@@ -1740,10 +1754,13 @@ struct Driver {
       I.p[6] = ip(1);
       for (int p = 0; p < 4; ++p) I.p[8 + p] = op_[p];
       I.s[0] = t; I.s[1] = d.aux[2]; I.s[2] = sx; I.s[3] = sh;
+      if (split) I.p[7] = op_[5];
       long long q3 = (kProfBuild && A.prof) ? clock64() : 0;
       if (kProfBuild && A.prof) { op_cyc[32 + 16] += q3 - q2; op_cnt[32 + 16]++; }
-      for (int j = 0; j < d.n_in; ++j) add_dep(id, in_tok(d, j).writer);
+      for (int j = 0; j < d.n_in; ++j)
+        if (!(split && j == 0)) add_dep(id, in_tok(d, j).writer);   // x: through the projection
       add_dep(id, pw);
+      add_dep(id, xp);
       long long q4 = (kProfBuild && A.prof) ? clock64() : 0;
       if (kProfBuild && A.prof) { op_cyc[32 + 17] += q4 - q3; op_cnt[32 + 17]++; }
       submit(id);
@@ -1894,7 +1911,9 @@ struct Driver {
           id[3] = reserve_inst(HK_PREP_WP, (int)((4 * H + 15) / 16));
           prep_inst_[nid] = id[3];
         }
-        id[0] = reserve_inst(HK_LSTM_FWD_TC, (int)((m2 ? (B + 255) / 256 : (B + 127) / 128) * (H / 64)));
+        const int nt = (int)((m2 ? (B + 255) / 256 : (B + 127) / 128) * (H / 64));
+        if (d.aux[1] & 4) id[1] = reserve_inst(HK_LSTM_XPROJ_TC, nt);   // x-projection first
+        id[0] = reserve_inst(HK_LSTM_FWD_TC, nt);
       } else {
         if (prep_inst_[nid] < 0) {
           id[3] = reserve_inst(HK_PREP_WT, (int)((KT / 64) * (4 * H / 128)));
@@ -1929,10 +1948,12 @@ struct Driver {
     // submit in creation order (weight prep, dW chunk, then the members' own instances)
     for (int m = 0; m < n; ++m) {
       const int* id = w.bid[m];
+      const bool fwd = bn_[pc + 1 + m].aux[0] == HK_LSTM_FWD;
       if (id[3] >= 0) submit(id[3]);
       if (id[2] >= 0) submit(id[2], true);
+      if (fwd && id[1] >= 0) submit(id[1]);   // the x-projection before its cell
       if (id[0] >= 0) submit(id[0]);
-      if (id[1] >= 0) submit(id[1]);
+      if (!fwd && id[1] >= 0) submit(id[1]);
     }
     flush_publish();
     return n + 1;
@@ -2009,16 +2030,29 @@ struct Driver {
           !resolve_core(outp[4], (int)(4 * H), (int)KT, 1, &mw, &sw, hint + 2))
         return false;
       const int ntiles = (int)((m2 ? (B + 255) / 256 : (B + 127) / 128) * (H / 64));
-      inst_header(id[0], HK_LSTM_FWD_TC, masked | (m2 ? 2 : 0), ntiles);
+      const bool split = id[1] >= 0;
+      if (split) {   // x-projection ahead of the recurrence (HK_LSTM_XPROJ_TC)
+        inst_header(id[1], HK_LSTM_XPROJ_TC, m2 ? 2 : 0, ntiles);
+        Inst& X = A.insts[id[1]];
+        X.m = B; X.k = In; X.n = H;
+        X.p[0] = mx; X.p[3] = mw; X.p[7] = outp[5];
+        X.s[2] = sx;
+        add_dep_atomic(id[1], in_tok(d, 0).writer);
+        add_dep_atomic(id[1], pw);
+      }
+      inst_header(id[0], HK_LSTM_FWD_TC, masked | (m2 ? 2 : 0) | (split ? 4 : 0), ntiles);
       Inst& I = A.insts[id[0]];
       I.m = B; I.k = In; I.n = H;
       I.p[0] = mx; I.p[1] = mh; I.p[2] = ip(2); I.p[3] = mw; I.p[4] = ip(4);
       I.p[5] = masked ? ip(6) : 0;
       I.p[6] = ip(1);
+      I.p[7] = split ? outp[5] : 0;
       for (int q = 0; q < 4; ++q) I.p[8 + q] = outp[q];
       I.s[0] = t; I.s[1] = d.aux[2]; I.s[2] = sx; I.s[3] = sh;
-      for (int j = 0; j < d.n_in; ++j) dep(id[0], in_tok(d, j).writer);
+      for (int j = 0; j < d.n_in; ++j)
+        if (!(split && j == 0)) dep(id[0], in_tok(d, j).writer);   // x: through the projection
       dep(id[0], pw);
+      if (split) dep(id[0], id[1]);
       return true;
     }
     // backward: EW (dz, dc, db partials) -> DXH (dx, dh); dW / db chunked over 8 steps
@@ -2151,7 +2185,7 @@ struct Driver {
     const bool tcm = P.precision == D_BF16;
     int nplace = d.n_out;
     if (kind == HK_LSTM_BWD_EW) nplace += tcm ? 2 : 1;
-    if (kind == HK_LSTM_FWD && tcm) nplace += 1;
+    if (kind == HK_LSTM_FWD && tcm) nplace += (d.aux[1] & 4) ? 2 : 1;
     long long q0 = (kProfBuild && A.prof) ? clock64() : 0;
     for (int p = 0; p < nplace; ++p)
       if (!place(d, p, &outp[p])) return st->error ? EV_ERROR : EV_BLOCKED;
@@ -3484,6 +3518,7 @@ __device__ void worker_loop(const RunArgs& A) {
       case HK_PREP_WP: tile_prep_wp(I, tile); break;
       case HK_PREP_WT: tile_prep_wt(I, tile, (float*)dyn_smem); break;
       case HK_LSTM_FWD_TC: tile_lstm_fwd_tc(I, tile, ts, tc_cnt, tc_cnt2, tc_tiles, sm, claim_ahead); break;
+      case HK_LSTM_XPROJ_TC: tile_lstm_xproj_tc(I, tile, ts, tc_cnt, tc_cnt2, tc_tiles, claim_ahead); break;
       case HK_LSTM_BWD_EW_BF: tile_lstm_bwd_ew_bf(I, tile, sm); break;
       case HK_LSTM_DXH_TC: tile_lstm_dxh_tc(I, tile, ts, tc_cnt, tc_cnt2, tc_tiles, claim_ahead); break;
       case HK_LSTM_DW_TC: tile_lstm_dw_tc(I, tile, ts, tc_cnt, tc_cnt2, tc_tiles, claim_ahead); break;

@@ -127,6 +127,11 @@ __device__ void tile_lstm_fwd_tc(const Inst& I, int tile, tc::TcShared& ts, uint
   const int nkx = In / 64, nk = (In + H) / 64;
   const int tn = H / 64;
   const bool m2 = I.sub & 2;   // 256-row tile (two accumulators)
+  // sub bit 2: the x-projection Zx = x Wx^T was computed ahead (HK_LSTM_XPROJ_TC, p[7], fp32,
+  // same gate-interleaved columns): only the recurrent k-blocks run here, the epilogue adds Zx
+  const bool xproj = I.sub & 4;
+  const float* zx = (const float*)I.p[7];
+  const int kb0 = xproj ? nkx : 0;
   const int mt = tile / tn, nt = tile % tn;
   const int m0 = mt * (m2 ? 2 * tc::BM : tc::BM);
   const CUtensorMap* mx = (const CUtensorMap*)I.p[0];
@@ -168,6 +173,7 @@ __device__ void tile_lstm_fwd_tc(const Inst& I, int tile, tc::TcShared& ts, uint
   }
   __syncthreads();   // the bias slice is in shared memory
   auto plan_a = [&](int kb, tc::Box* b) {
+    kb += kb0;
     for (int hh = 0; hh < (m2 ? 2 : 1); ++hh) {
       if (kb < nkx) b[hh] = {mx, kb * 64, m0 + 128 * hh, sx, hh * tc::kStageA};
       else b[hh] = {mh, (kb - nkx) * 64, m0 + 128 * hh, sh, hh * tc::kStageA};
@@ -176,14 +182,14 @@ __device__ void tile_lstm_fwd_tc(const Inst& I, int tile, tc::TcShared& ts, uint
   };
   const int keep_w = !(kDbgFlagsTC & 32);   // A/B: debug flag bit 5 drops the L2 hint
   auto plan_b = [&](int kb, tc::Box* b) {
-    b[0] = {mw, kb * 64, nt * 256, 0, 0, keep_w};
+    b[0] = {mw, (kb + kb0) * 64, nt * 256, 0, 0, keep_w};
     return 1;
   };
   // debug flags bits 16-19: L2 prefetch distance in k-blocks (A/B; 0 = the default 4, 15 = off)
   const int pfd = (kDbgFlagsTC >> 16) & 15;
   const int ahead = pfd == 15 ? 0 : pfd ? pfd : 4;
-  if (m2) tc::tc_tile2(ts, nk, 0, 0, cnt2, ntile, plan_a, plan_b, 256, ahead, hook);
-  else tc::tc_tile(ts, nk, 256, 0, 0, cnt, ntile, plan_a, plan_b, hook);
+  if (m2) tc::tc_tile2(ts, nk - kb0, 0, 0, cnt2, ntile, plan_a, plan_b, 256, ahead, hook);
+  else tc::tc_tile(ts, nk - kb0, 256, 0, 0, cnt, ntile, plan_a, plan_b, hook);
   // ---- fused epilogue: 2 (or 4) groups of 16 units x 4 gates per thread. The gates and h are
   // staged in the (now idle) pipeline stage buffers and written out coalesced (debug flag bit
   // 21: direct per-row stores, A/B)
@@ -205,8 +211,27 @@ __device__ void tile_lstm_fwd_tc(const Inst& I, int tile, tc::TcShared& ts, uint
     const uint32_t ta = *ts.tmem_slot + ((uint32_t)(32 * (warp % 4)) << 16) + (uint32_t)(256 * half + cu);
 #pragma unroll
     for (int g = 0; g < 4; ++g) tc::tmem_ld16_nowait(ta + 64 * g, zr[g]);
+    float4 zxv[4][4];
+    if (xproj) {   // the precomputed x-projection of this row's 16 units x 4 gates
+      const float* zrow = zx + (int64_t)(r < B ? r : 0) * 4 * H + nt * 256 + cu;
+#pragma unroll
+      for (int g = 0; g < 4; ++g)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) zxv[g][q] = ((const float4*)(zrow + g * 64))[q];
+    }
     tc::tmem_wait_ld();
     if (r >= B || (kDbgFlagsTC & (1 << 20))) continue;   // bit 20: no epilogue (timing only)
+    if (xproj) {
+#pragma unroll
+      for (int g = 0; g < 4; ++g)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          zr[g][4 * q + 0] = __float_as_uint(__uint_as_float(zr[g][4 * q + 0]) + zxv[g][q].x);
+          zr[g][4 * q + 1] = __float_as_uint(__uint_as_float(zr[g][4 * q + 1]) + zxv[g][q].y);
+          zr[g][4 * q + 2] = __float_as_uint(__uint_as_float(zr[g][4 * q + 2]) + zxv[g][q].z);
+          zr[g][4 * q + 3] = __float_as_uint(__uint_as_float(zr[g][4 * q + 3]) + zxv[g][q].w);
+        }
+    }
     const int u0 = nt * 64 + cu;
     const int64_t o = (int64_t)r * H + u0;
     float cp[16], hn[16], cn[16], zi[16], zf[16], zg[16], zo[16];
@@ -285,6 +310,60 @@ __device__ void tile_lstm_fwd_tc(const Inst& I, int tile, tc::TcShared& ts, uint
     // the next tile's TMA (async proxy) overwrites these stage buffers
     tc::fence_proxy_async_smem();
   }
+  tc::tc_tile_end();
+}
+
+// ---------------------------------------------------------------- forward x-projection
+// Zx = x Wx^T for one (row tile, 256-column gate-interleaved tile): the input part of the gate
+// pre-activations does not depend on h_{t-1}, so it runs as its own instance as soon as x_t is
+// ready (the layer below's step t), off the recurrence's critical chain; the cell instance
+// then runs only the recurrent k-blocks (sub bit 2). fp32 out through the idle stage buffers.
+// p: 0 x-map, 3 Wp-map, 7 Zx (f32 [B][4H]); s: 2 x slot; sub bit 1: 256-row tile
+template <class Hook>
+__device__ void tile_lstm_xproj_tc(const Inst& I, int tile, tc::TcShared& ts, uint32_t& cnt,
+                                   uint32_t& cnt2, uint32_t& ntile, Hook hook) {
+  const int B = (int)I.m, In = (int)I.k, H = (int)I.n;
+  const int nkx = In / 64, tn = H / 64;
+  const bool m2 = I.sub & 2;
+  const int mt = tile / tn, nt = tile % tn;
+  const int m0 = mt * (m2 ? 2 * tc::BM : tc::BM);
+  const CUtensorMap* mx = (const CUtensorMap*)I.p[0];
+  const CUtensorMap* mw = (const CUtensorMap*)I.p[3];
+  float* zx = (float*)I.p[7];
+  const int sx = (int)I.s[2];
+  auto plan_a = [&](int kb, tc::Box* b) {
+    b[0] = {mx, kb * 64, m0, sx, 0};
+    if (m2) b[1] = {mx, kb * 64, m0 + 128, sx, tc::kStageA};
+    return m2 ? 2 : 1;
+  };
+  const int keep_w = !(kDbgFlagsTC & 32);
+  auto plan_b = [&](int kb, tc::Box* b) {
+    b[0] = {mw, kb * 64, nt * 256, 0, 0, keep_w};
+    return 1;
+  };
+  if (m2) tc::tc_tile2(ts, nkx, 0, 0, cnt2, ntile, plan_a, plan_b, 256, 0, hook);
+  else tc::tc_tile(ts, nkx, 256, 0, 0, cnt, ntile, plan_a, plan_b, hook);
+  uint8_t* stg = ts.a[0];
+  constexpr int kRow = 1024 + 16;   // 256 fp32 + pad
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  for (int half = 0; half < (m2 ? 2 : 1); ++half) {
+    const int rl = 32 * (warp % 4) + lane;
+    for (int c = (warp / 4) * 128; c < (warp / 4) * 128 + 128; c += 16) {
+      float v[16];
+      tc::tc_acc16(ts, 256 * half + c, v);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) *(float4*)(stg + rl * kRow + (c + 4 * q) * 4) = *(float4*)&v[4 * q];
+    }
+    __syncthreads();
+    const int nrows = min(128, B - (m0 + 128 * half));
+    for (int q = threadIdx.x; q < nrows * 64; q += 256) {
+      const int rr = q >> 6, ch = q & 63;
+      *(uint4*)((uint8_t*)(zx + (int64_t)(m0 + 128 * half + rr) * 4 * H + nt * 256) + ch * 16) =
+          *(const uint4*)(stg + rr * kRow + ch * 16);
+    }
+    __syncthreads();
+  }
+  tc::fence_proxy_async_smem();
   tc::tc_tile_end();
 }
 

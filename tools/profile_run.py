@@ -20,7 +20,7 @@ from synth import rnn_inputs  # noqa: E402
 
 KINDS = ["NOP", "EW", "FILL", "COPY", "REDUCE_SUM", "REDUCE_SUM0", "MATMUL", "LSTM_FWD",
          "LSTM_BWD_EW", "LSTM_BWD_MM", "ACC", "PREP_WP", "PREP_WT", "LSTM_FWD_TC",
-         "LSTM_BWD_EW_BF", "LSTM_DXH_TC", "LSTM_DW_TC", "SWAP", "WAIT"]
+         "LSTM_BWD_EW_BF", "LSTM_DXH_TC", "LSTM_DW_TC", "SWAP", "WAIT", "LSTM_XPROJ_TC"]
 
 OPS = ["NOP", "PLACEHOLDER", "CONST", "PASS", "SWITCH", "MERGE", "MERGE_LOOP", "ENTER", "EXIT",
        "NEXTITER", "SCALAR", "REDUCE_I", "SLICE_I", "FLOW", "TA_CREATE", "TA_READ", "TA_WRITE",
