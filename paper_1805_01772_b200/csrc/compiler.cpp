@@ -812,9 +812,11 @@ struct Compiler {
 
   // number of placement slots of a heavy node: outputs + internal scratch / prep buffers
   // forward cells whose input projection runs as its own instance ahead of the recurrence
-  // (runtime.cu HK_LSTM_XPROJ_TC; CF_NO_XPROJ=1 keeps one fused instance, A/B)
+  // (runtime.cu HK_LSTM_XPROJ_TC). Off by default, CF_XPROJ=1 enables it: measured on cfg3 the
+  // forward took 33.4 ms with the split vs 24.0 ms fused (the cell tile's time is its
+  // epilogue, which the split does not shorten, and the projection adds 1.5 SM-s of tiles)
   bool xproj(const Node& n) const {
-    return bf16() && n.op == "LSTMCell" && !std::getenv("CF_NO_XPROJ");
+    return bf16() && n.op == "LSTMCell" && std::getenv("CF_XPROJ") != nullptr;
   }
   int n_places(const Node& n) const {
     int np = (int)n.odt.size();
