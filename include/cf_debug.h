@@ -36,6 +36,10 @@ int32_t cf_debug_set_m2_rows(int32_t rows);
  * accumulator-read-only epilogue. *ms_out = device time. Returns 0 or CF_E_CUDA. */
 int32_t cf_debug_tc_pipe(int32_t M, int32_t N, int32_t K, int32_t nb, int32_t reps,
                          int32_t prefetch, const void* A, const void* B, float* ms_out);
+/* Worker roles: the first `low_first` worker CTAs take low-priority work (dW chunks) before
+ * the critical-path ring; with `strict` != 0 the other workers never take low-priority work.
+ * (0, 0) = every worker prefers the critical-path ring (the default). Returns 0 or CF_E_CUDA. */
+int32_t cf_debug_set_worker_roles(int32_t low_first, int32_t strict);
 /* Profiling knobs: bit 0 = workers skip every tile body (the device driver's own cost in
  * isolation; results are garbage); A/B switches (results unchanged): bit 2 = poll
  * completions after every node, bit 3 = wave helpers spin without sleeping, bit 4 = release

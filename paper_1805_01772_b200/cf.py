@@ -119,6 +119,7 @@ _sig = {
     "cf_session_connect": (C.c_int32, [_P, C.c_int32, C.c_void_p, C.c_int32, C.POINTER(C.c_int64)]),
     # include/cf_debug.h (test hooks)
     "cf_debug_set_m2_rows": (C.c_int32, [C.c_int32]),
+    "cf_debug_set_worker_roles": (C.c_int32, [C.c_int32, C.c_int32]),
     "cf_debug_tc_pipe": (C.c_int32, [C.c_int32] * 6 + [C.c_void_p, C.c_void_p, C.POINTER(C.c_float)]),
     "cf_debug_set_flags": (C.c_int32, [C.c_int32]),
     "cf_debug_program_listing": (C.c_int32, [_P, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
@@ -596,6 +597,11 @@ def debug_tc_pipe(M, N, K, nb, reps, prefetch, A, B) -> float:
     ms = C.c_float()
     _check(_lib.cf_debug_tc_pipe(M, N, K, nb, reps, prefetch, A.data_ptr(), B.data_ptr(), C.byref(ms)))
     return ms.value
+
+
+def debug_set_worker_roles(low_first: int, strict: bool = False) -> None:
+    """Test hook (include/cf_debug.h): workers that take dW chunks first / strict roles."""
+    _check(_lib.cf_debug_set_worker_roles(low_first, 1 if strict else 0))
 
 
 def debug_set_m2_rows(rows: int) -> None:

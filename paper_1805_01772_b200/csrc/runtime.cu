@@ -63,6 +63,9 @@ __device__ int kM2MinRows = kM2Default;
 // test/profiling knob (cf_debug_set_flags): bit 0 = workers skip the tile bodies (isolates the
 // driver's own cost; results are garbage)
 __device__ int kDbgFlags = 0;
+// worker roles (cf_debug_set_worker_roles): low 16 bits = workers that take low-priority (dW)
+// work first, bit 16 = the other workers never take it
+__device__ int kLowWorkers = 0;
 
 // ----------------------------------------------------------------------------- helpers
 __device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long* p) {
@@ -1503,6 +1506,12 @@ struct Driver {
 
   long long last_drain_ = 0;
   int dbg_ = 0;
+  // dW chunk length in steps (K = chunk * B per dW tile); debug flag bits 24-27 override the
+  // default 8 for A/B runs (shorter tiles leave workers free sooner for the critical chain)
+  __device__ __forceinline__ int dw_chunk() const {
+    const int c = (dbg_ >> 24) & 15;
+    return c >= 1 && c <= 8 ? c : 8;
+  }
   __forceinline__ __device__ void maybe_drain() {
     if ((dbg_ & 4) || clock64() - last_drain_ > drain_cycles_) drain();
   }
@@ -1775,7 +1784,7 @@ struct Driver {
     outp = op_;
     const int acc_w = d.aux[3], acc_b = d.aux[4];
     const int cnt0 = dw_count_[nid];
-    const bool early = !(dbg_ & (1 << 29)) && acc_w >= 0 && acc_b >= 0 && cnt0 + 1 < 8;   // bit 29: off
+    const bool early = !(dbg_ & (1 << 29)) && acc_w >= 0 && acc_b >= 0 && cnt0 + 1 < dw_chunk();   // bit 29: off
     const int o = masked ? 7 : 5;
     const int64_t dz_ptr = outp[5];
     const int64_t dz_bytes = ((B * 4 * H * 2 + 1023) / 1024) * 1024;
@@ -1841,7 +1850,7 @@ struct Driver {
       A.dw_pend[(int64_t)nid * 80 + 9] = mzn;   // dz map (same for all steps of the node)
       dw_count_[nid] = cnt + 1;
       pend_mz = mzn;
-      if (!(acc_w >= 0 && acc_b >= 0) || cnt + 1 == 8) {
+      if (!(acc_w >= 0 && acc_b >= 0) || cnt + 1 >= dw_chunk()) {
         if (flush_dw(d, nid, mzn, outp[3], outp[4]) < 0) return EV_ERROR;
       }
     }
@@ -1920,7 +1929,7 @@ struct Driver {
           prep_inst_[nid] = id[3];
         }
         const int acc_w = d.aux[3], acc_b = d.aux[4];
-        if (!(acc_w >= 0 && acc_b >= 0) || dw_count_[nid] + 1 == 8) {
+        if (!(acc_w >= 0 && acc_b >= 0) || dw_count_[nid] + 1 >= dw_chunk()) {
           id[2] = reserve_inst(HK_LSTM_DW_TC, (int)((4 * H / 256) * (KT / 256) + (4 * H + 255) / 256));
           last_flush = id[2];
         }
@@ -3446,11 +3455,25 @@ __device__ void worker_loop(const RunArgs& A) {
     return 1;
   };
   // one non-blocking attempt over both rings (high priority first)
+  // SM roles for the low-priority ring (dW chunks, off the critical path): the first n_low
+  // workers take low-priority work first; with `strict`, the others never take it (so a long
+  // dW tile never holds an SM the recurrence's next tile is waiting for). kLowWorkers = 0:
+  // every worker prefers high-priority work (cf_debug_set_worker_roles)
+  const int n_low = kLowWorkers & 0xffff;
+  const bool low_first = (int)blockIdx.x <= n_low;
+  const bool no_low = n_low > 0 && !low_first && (kLowWorkers >> 16);
   auto try_claim = [&](unsigned long long* e) -> bool {
     for (int k = 0; k < 8; ++k) {
-      int r = claim(&st->q_head, &st->q_tail, A.queue, e);
+      int r = 0;
+      if (low_first) {
+        r = claim(&st->lq_head, &st->lq_tail, A.lq, e);
+        if (r == 1) return true;
+        if (r == 2) continue;
+      }
+      r = claim(&st->q_head, &st->q_tail, A.queue, e);
       if (r == 1) return true;
       if (r == 2) continue;
+      if (low_first || no_low) return false;
       r = claim(&st->lq_head, &st->lq_tail, A.lq, e);
       if (r == 1) return true;
       if (r == 2) continue;
@@ -4493,6 +4516,11 @@ int32_t cf_debug_set_flags(int32_t flags) {
   if (cudaMemcpyToSymbol(kDbgFlagsTC, &flags, sizeof(flags)) != cudaSuccess) return CF_E_CUDA;
   return cudaMemcpyToSymbol(kDbgFlags, &flags, sizeof(flags)) == cudaSuccess ? CF_OK : CF_E_CUDA;
 }
+int32_t cf_debug_set_worker_roles(int32_t low_first, int32_t strict) {
+  const int v = (low_first & 0xffff) | (strict ? 1 << 16 : 0);
+  return cudaMemcpyToSymbol(kLowWorkers, &v, sizeof(v)) == cudaSuccess ? CF_OK : CF_E_CUDA;
+}
+
 int32_t cf_debug_set_m2_rows(int32_t rows) {
   if (rows <= 0) rows = kM2Default;
   return cudaMemcpyToSymbol(kM2MinRows, &rows, sizeof(rows)) == cudaSuccess ? CF_OK : CF_E_CUDA;
