@@ -29,7 +29,11 @@ using namespace cfdev;
 
 namespace {
 
-constexpr int kDwChunk = 8;   // gradient-loop steps accumulated per dW tile (K = 8 * batch)
+// gradient-loop steps accumulated per dW tile (K = 8 * batch). Measured on cfg3 (tools/
+// dwchunk_ab.py): 1 step 113.8 ms, 2 94.6, 4 76.6, 8 72.7, 12 71.3-71.9, 16 72.3 -> 8 (the dz and
+// swap-in rings grow by one slot per chunk step); kDwMax bounds it
+constexpr int kDwChunk = 8;
+static_assert(kDwChunk <= kDwMax, "dW chunk records");
 
 int32_t dev_dt(int32_t d, int32_t precision) {
   (void)precision;
@@ -548,6 +552,7 @@ struct Compiler {
     (void)max_tiles;
     P.inst_bound = total + 1024;
     P.branch_bound = 1;
+    P.dw_chunk = bf16() ? kDwChunk : 1;
     // branch bits are indexed by the iteration index over all instances of a nested frame
     for (size_t f = 0; f < bound.size(); ++f)
       P.branch_bound = (int)std::max<int64_t>(P.branch_bound, frame_total[f] + 1);

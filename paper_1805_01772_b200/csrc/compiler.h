@@ -67,6 +67,7 @@ struct HostProgram {
   int n_vids = 0;
   int n_conds = 0;
   int branch_bound = 1;
+  int dw_chunk = 1;              // gradient-loop steps per dW instance (bf16 mode: kDwChunk)
   int iter_counters = 0;
   int stack_pool = 0;
   int stack_depths = 0;              // stack instances (one depth counter each)

@@ -219,13 +219,15 @@ struct DChan {
   unsigned long long* done;         // sending half (local)    | receiving half: peer's done
 };
 
+constexpr int kDwMax = 16;   // most gradient-loop steps one dW instance accumulates
+
 struct Prog {
   int32_t n_nodes, n_vids, n_frames, n_tas, n_stacks;
   int32_t n_root_steps;
   int32_t n_fetch;
   int32_t n_conds;
   int32_t branch_bound;         // iterations recorded per cond in the branch-bit array
-  int32_t pad;
+  int32_t dw_chunk;             // gradient-loop steps per dW instance (rings sized for it)
   const DNode* nodes;
   const int32_t* in_vids;
   const PlaceDesc* places;
@@ -323,9 +325,9 @@ struct RunArgs {
   int32_t sched_seed;
   int32_t num_workers;
   int64_t dyn_smem;          // dynamic shared memory per CTA (driver: token table if it fits)
-  int64_t* inst_aux;         // [inst_cap][48] per-instance side data (chunked dW steps)
+  int64_t* inst_aux;         // [inst_cap][kDwMax * 6] per-instance side data (chunked dW steps)
   int32_t* dw_count;         // [n_nodes] pending dW steps per LSTMCellGrad node (chunking)
-  int64_t* dw_pend;          // [n_nodes][8][8] pending step records
+  int64_t* dw_pend;          // [n_nodes][kDwMax][10] pending step records
   unsigned long long* lq;    // low-priority job ring (same capacity as queue)
   unsigned long long* prof;  // optional: per instance {create, publish, first start, last end,
                              //  busy ns, kind|ntiles} (profiling hook, cf_debug.h)

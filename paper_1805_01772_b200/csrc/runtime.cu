@@ -1506,11 +1506,11 @@ struct Driver {
 
   long long last_drain_ = 0;
   int dbg_ = 0;
-  // dW chunk length in steps (K = chunk * B per dW tile); debug flag bits 24-27 override the
-  // default 8 for A/B runs (shorter tiles leave workers free sooner for the critical chain)
+  // dW chunk length in steps (K = chunk * B per dW tile): the compiler's P.dw_chunk, which
+  // sized the dz and swap-in rings; debug flag bits 24-27 pick a shorter one for A/B runs
   __device__ __forceinline__ int dw_chunk() const {
     const int c = (dbg_ >> 24) & 15;
-    return c >= 1 && c <= 8 ? c : 8;
+    return c >= 1 && c < P.dw_chunk ? c : P.dw_chunk;
   }
   __forceinline__ __device__ void maybe_drain() {
     if ((dbg_ & 4) || clock64() - last_drain_ > drain_cycles_) drain();
@@ -1839,15 +1839,15 @@ struct Driver {
       add_dep(x, pw);
       add_dep(x, in_tok(d, o).writer);
     }
-    // dW / db: steps are queued and multiplied in chunks of up to 8 (K = 8 B) when both
+    // dW / db: steps are queued and multiplied in chunks of up to P.dw_chunk (K = 8 B) when both
     // gradients accumulate in place; otherwise one step per instance
     {
       int cnt = dw_count_[nid];
-      int64_t* rec = A.dw_pend + ((int64_t)nid * 8 + cnt) * 10;
+      int64_t* rec = A.dw_pend + ((int64_t)nid * kDwMax + cnt) * 10;
       rec[0] = szn; rec[1] = mxn; rec[2] = sxn; rec[3] = mhn; rec[4] = shn;
       rec[5] = dz_ptr + dz_bytes;
       rec[6] = e; rec[7] = in_tok(d, 0).writer; rec[8] = in_tok(d, 1).writer;
-      A.dw_pend[(int64_t)nid * 80 + 9] = mzn;   // dz map (same for all steps of the node)
+      A.dw_pend[(int64_t)nid * kDwMax * 10 + 9] = mzn;   // dz map (same for all steps of the node)
       dw_count_[nid] = cnt + 1;
       pend_mz = mzn;
       if (!(acc_w >= 0 && acc_b >= 0) || cnt + 1 >= dw_chunk()) {
@@ -2114,11 +2114,11 @@ struct Driver {
       dep(x, in_tok(d, o).writer);
     }
     const int cnt = dw_count_[nid];
-    int64_t* rec = A.dw_pend + ((int64_t)nid * 8 + cnt) * 10;
+    int64_t* rec = A.dw_pend + ((int64_t)nid * kDwMax + cnt) * 10;
     rec[0] = szn; rec[1] = mxn; rec[2] = sxn; rec[3] = mhn; rec[4] = shn;
     rec[5] = dz_ptr + dz_bytes;
     rec[6] = e; rec[7] = in_tok(d, 0).writer; rec[8] = in_tok(d, 1).writer;
-    A.dw_pend[(int64_t)nid * 80 + 9] = mzn;
+    A.dw_pend[(int64_t)nid * kDwMax * 10 + 9] = mzn;
     dw_count_[nid] = cnt + 1;
     if (id[2] >= 0) {   // close the dW chunk (the driver reserved its id)
       const int32_t wd = id[2];
@@ -2129,13 +2129,13 @@ struct Driver {
       I.p[0] = mzn;
       I.p[3] = acc_w >= 0 ? P.accs[acc_w].base : outp[3];
       I.p[4] = acc_b >= 0 ? P.accs[acc_b].base : outp[4];
-      int64_t* ax = A.inst_aux + (int64_t)wd * 48;
+      int64_t* ax = A.inst_aux + (int64_t)wd * kDwMax * 6;
       I.p[6] = (int64_t)ax;
       I.s[6] = (acc_w >= 0 ? 1 : 0) | (acc_b >= 0 ? 2 : 0);
       I.s[7] = c2;
       ns = 0;
       for (int q = 0; q < c2; ++q) {
-        const int64_t* rq = A.dw_pend + ((int64_t)nid * 8 + q) * 10;
+        const int64_t* rq = A.dw_pend + ((int64_t)nid * kDwMax + q) * 10;
         for (int k = 0; k < 6; ++k) ax[q * 6 + k] = rq[k];
         dep(wd, (int32_t)rq[6]);
         dep(wd, (int32_t)rq[7]);
@@ -2165,12 +2165,12 @@ struct Driver {
     I.p[0] = mzn;
     I.p[3] = acc_w >= 0 ? P.accs[acc_w].base : dw_ptr;
     I.p[4] = acc_b >= 0 ? P.accs[acc_b].base : db_ptr;
-    int64_t* ax = A.inst_aux + (int64_t)w * 48;
+    int64_t* ax = A.inst_aux + (int64_t)w * kDwMax * 6;
     I.p[6] = (int64_t)ax;
     I.s[6] = (acc_w >= 0 ? 1 : 0) | (acc_b >= 0 ? 2 : 0);
     I.s[7] = cnt;
     for (int q = 0; q < cnt; ++q) {
-      const int64_t* rec = A.dw_pend + ((int64_t)nid * 8 + q) * 10;
+      const int64_t* rec = A.dw_pend + ((int64_t)nid * kDwMax + q) * 10;
       for (int k = 0; k < 6; ++k) ax[q * 6 + k] = rec[k];
       add_dep(w, (int32_t)rec[6]);
       add_dep(w, (int32_t)rec[7]);
@@ -3299,7 +3299,7 @@ struct Driver {
         const int nid = P.order[F.body_off + k];
         const DNode& dn = node(nid);
         if (dn.op == OP_HEAVY && dn.aux[0] == HK_LSTM_BWD_EW && dw_count_[nid] > 0) {
-          if (flush_dw(dn, nid, A.dw_pend[(int64_t)nid * 80 + 9], 0, 0) < 0) return false;
+          if (flush_dw(dn, nid, A.dw_pend[(int64_t)nid * kDwMax * 10 + 9], 0, 0) < 0) return false;
         }
       }
       iv_ = P.in_vids;
@@ -3987,6 +3987,7 @@ void build_session(cf_session* s, const cf::Graph& g, const cf_run_opts* o,
   pg.n_fetch = (int)P.fetches.size();
   pg.n_conds = P.n_conds;
   pg.branch_bound = P.branch_bound;
+  pg.dw_chunk = P.dw_chunk;
   pg.nodes = upload(s, P.nodes);
   pg.in_vids = upload(s, P.in_vids);
   pg.places = upload(s, P.places);
@@ -4099,10 +4100,10 @@ void build_session(cf_session* s, const cf::Graph& g, const cf_run_opts* o,
       CUDA_OK(cudaStreamCreateWithFlags(&s->io_h2d[k], cudaStreamNonBlocking));
     }
   }
-  A.inst_aux = (int64_t*)dalloc(s, 8 * 48 * (size_t)P.inst_bound);
+  A.inst_aux = (int64_t*)dalloc(s, 8 * kDwMax * 6 * (size_t)P.inst_bound);
   A.dw_count = (int32_t*)dalloc(s, 4 * P.nodes.size());
   s->zero_each_run.push_back({A.dw_count, 4 * P.nodes.size()});
-  A.dw_pend = (int64_t*)dalloc(s, 8 * 80 * P.nodes.size());
+  A.dw_pend = (int64_t*)dalloc(s, 8 * kDwMax * 10 * P.nodes.size());
   A.prep_inst = (int32_t*)dalloc(s, 4 * P.nodes.size());
   s->fill_ff_each_run.push_back({A.prep_inst, (int)(4 * P.nodes.size())});
   A.acc_writer = (int32_t*)dalloc(s, 4 * std::max<size_t>(P.accs.size(), 1));
