@@ -51,6 +51,17 @@ int32_t cf_debug_set_worker_roles(int32_t low_first, int32_t strict);
  * with a forward LSTM node's instance construction, bit 29 = the same for a backward node
  * (steps that do not close a dW chunk). Returns 0 or CF_E_CUDA. */
 int32_t cf_debug_set_flags(int32_t flags);
+/* A/B knobs, read by the kernel as it runs (0 = default): 0 = how many k-blocks before a
+ * tensor-core tile's last MMA issue the worker claims its next tile (default 8). Returns 0,
+ * CF_E_SHAPE (which outside 0..7) or CF_E_CUDA. */
+int32_t cf_debug_set_knob(int32_t which, int32_t value);
+/* Tile phase clocks, collected while cf_debug_set_flags bit 22 is set: out20[4k + 0] tiles,
+ * [4k + 1] SM cycles from tile entry to the mainloop's first issue, [4k + 2] mainloop cycles
+ * (until the accumulator is complete; for the backward EW the whole tile), [4k + 3] epilogue
+ * cycles; k = 0 forward, 1 d[x,h], 2 dW, 3 backward EW (thread 0 of each tile); [16] forward
+ * epilogue TMEM + math + staging, [17] its barrier wait. reset != 0 zeroes the counters after
+ * the read. Returns 0 or CF_E_CUDA. */
+int32_t cf_debug_tile_phases(uint64_t* out20, int32_t reset);
 /* Compile a graph for the device program without a GPU and write its description and body
  * programs (one node per line, evaluation order) into buf; *needed = length + 1. The
  * environment variable CF_DEBUG_MAX_ITERATIONS plays cf_run_opts.max_iterations. */

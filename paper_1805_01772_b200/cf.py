@@ -120,6 +120,8 @@ _sig = {
     # include/cf_debug.h (test hooks)
     "cf_debug_set_m2_rows": (C.c_int32, [C.c_int32]),
     "cf_debug_set_worker_roles": (C.c_int32, [C.c_int32, C.c_int32]),
+    "cf_debug_tile_phases": (C.c_int32, [C.c_void_p, C.c_int32]),
+    "cf_debug_set_knob": (C.c_int32, [C.c_int32, C.c_int32]),
     "cf_debug_tc_pipe": (C.c_int32, [C.c_int32] * 6 + [C.c_void_p, C.c_void_p, C.POINTER(C.c_float)]),
     "cf_debug_set_flags": (C.c_int32, [C.c_int32]),
     "cf_debug_program_listing": (C.c_int32, [_P, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
@@ -590,6 +592,18 @@ def version() -> str:
 def debug_set_flags(flags: int) -> None:
     """Profiling knob (cf_debug.h): bit 0 = workers skip tile bodies (driver cost alone)."""
     _check(_lib.cf_debug_set_flags(flags))
+
+
+def debug_set_knob(which: int, value: int) -> None:
+    """A/B knob (cf_debug.h): 0 = claim-ahead lead in k-blocks (0 = default)."""
+    _check(_lib.cf_debug_set_knob(which, value))
+
+
+def debug_tile_phases(reset: bool = True) -> list:
+    """Tile phase clocks (cf_debug.h; collected under debug flag bit 22): 20 counters."""
+    buf = (C.c_uint64 * 20)()
+    _check(_lib.cf_debug_tile_phases(buf, 1 if reset else 0))
+    return list(buf)
 
 
 def debug_tc_pipe(M, N, K, nb, reps, prefetch, A, B) -> float:

@@ -512,6 +512,9 @@ struct Compiler {
     P.n_conds = max_cond + 1;
 
     // ---- placements of heavy outputs
+    P.dw_chunk = bf16() ? kDwChunk : 1;
+    if (const char* e = std::getenv("CF_DW_CHUNK"); e && bf16())   // A/B (tools/dwchunk_ab.py)
+      P.dw_chunk = std::max(1, std::min(kDwMax, std::atoi(e)));
     for (int nid : heavy_nodes) place_outputs(g.nodes[nid]);
 
     // ---- evaluation orders
@@ -552,7 +555,6 @@ struct Compiler {
     (void)max_tiles;
     P.inst_bound = total + 1024;
     P.branch_bound = 1;
-    P.dw_chunk = bf16() ? kDwChunk : 1;
     // branch bits are indexed by the iteration index over all instances of a nested frame
     for (size_t f = 0; f < bound.size(); ++f)
       P.branch_bound = (int)std::max<int64_t>(P.branch_bound, frame_total[f] + 1);
@@ -898,8 +900,8 @@ struct Compiler {
         int K = o.parallel_iterations > 0 ? o.parallel_iterations : g.ctxs[frame_ctx[f]].K;
         pl.kind = PL_RING;
         pl.slots = K + 1;
-        // chunked dW reads the dz of the last kDwChunk steps: keep them alive past the window
-        if (kind == DZ && bf16()) pl.slots = K + kDwChunk + 1;
+        // chunked dW reads the dz of the last P.dw_chunk steps: keep them alive past the window
+        if (kind == DZ && bf16()) pl.slots = K + P.dw_chunk + 1;
         pl.base = add_buf((size_t)pl.elem_bytes * pl.slots, false, "ring " + n.op + std::to_string(n.id));
         if (dd == D_BF16 && shp.size() == 2)
           register_buf_stride((int)pl.base, pl.slots, (int)shp[0], (int)shp[1], pl.elem_bytes);
@@ -1318,9 +1320,9 @@ struct Compiler {
         sp.capacity = (int32_t)bound[f];
         // swap-ins land in a ring of their own, indexed by the gradient loop's iteration: the
         // forward ring may still hold values that left the loop through an Exit. In bf16 mode a
-        // chunked dW instance reads the popped x / h of its last kDwChunk steps after those
-        // iterations left the window, so the ring keeps kDwChunk more slots (like the dz ring)
-        sp.in_ring = std::min<int>(bf16() ? K + kDwChunk + 1 : K + 1, (int)bound[f]);
+        // chunked dW instance reads the popped x / h of its last P.dw_chunk steps after those
+        // iterations left the window, so the ring keeps that many more slots (like the dz ring)
+        sp.in_ring = std::min<int>(bf16() ? K + P.dw_chunk + 1 : K + 1, (int)bound[f]);
         sp.in_buf = add_buf((size_t)pl.elem_bytes * sp.in_ring, false, "swap-in ring " + std::to_string(i));
         if (pl.dt == D_BF16 && p < (int)g.nodes[i].osh.size() && g.nodes[i].osh[p].size() == 2)
           register_buf_stride(sp.in_buf, sp.in_ring, (int)g.nodes[i].osh[p][0], (int)g.nodes[i].osh[p][1],

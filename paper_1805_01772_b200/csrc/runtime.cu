@@ -1507,11 +1507,8 @@ struct Driver {
   long long last_drain_ = 0;
   int dbg_ = 0;
   // dW chunk length in steps (K = chunk * B per dW tile): the compiler's P.dw_chunk, which
-  // sized the dz and swap-in rings; debug flag bits 24-27 pick a shorter one for A/B runs
-  __device__ __forceinline__ int dw_chunk() const {
-    const int c = (dbg_ >> 24) & 15;
-    return c >= 1 && c < P.dw_chunk ? c : P.dw_chunk;
-  }
+  // sized the dz and swap-in rings
+  __device__ __forceinline__ int dw_chunk() const { return P.dw_chunk; }
   __forceinline__ __device__ void maybe_drain() {
     if ((dbg_ & 4) || clock64() - last_drain_ > drain_cycles_) drain();
   }
@@ -3487,10 +3484,16 @@ __device__ void worker_loop(const RunArgs& A) {
     unsigned long long e;
     if (!try_claim(&e)) return;
     const int32_t id = (int32_t)(e >> 32);
-    int64_t* dst = (int64_t*)&s_inst_next;
-    const volatile int64_t* src = (const volatile int64_t*)(A.insts + id);
-#pragma unroll 4
-    for (int k = 0; k < (int)(sizeof(Inst) / 8); ++k) dst[k] = src[k];
+    // the record was published before the claim could see it: after the fence, plain L2 loads
+    // (all in flight at once; one round trip instead of one per word)
+    __threadfence();
+    constexpr int kW = (int)(sizeof(Inst) / 8);
+    long long w[kW];
+    const long long* src = (const long long*)(A.insts + id);
+#pragma unroll
+    for (int k = 0; k < kW; ++k) w[k] = __ldcg(src + k);
+#pragma unroll
+    for (int k = 0; k < kW; ++k) ((long long*)&s_inst_next)[k] = w[k];
     s_next = e;
   };
   while (true) {
@@ -3542,13 +3545,14 @@ __device__ void worker_loop(const RunArgs& A) {
       case HK_PREP_WT: tile_prep_wt(I, tile, (float*)dyn_smem); break;
       case HK_LSTM_FWD_TC: tile_lstm_fwd_tc(I, tile, ts, tc_cnt, tc_cnt2, tc_tiles, sm, claim_ahead); break;
       case HK_LSTM_XPROJ_TC: tile_lstm_xproj_tc(I, tile, ts, tc_cnt, tc_cnt2, tc_tiles, claim_ahead); break;
-      case HK_LSTM_BWD_EW_BF: tile_lstm_bwd_ew_bf(I, tile, sm); break;
+      case HK_LSTM_BWD_EW_BF: tile_lstm_bwd_ew_bf(I, tile, sm, ts); break;
       case HK_LSTM_DXH_TC: tile_lstm_dxh_tc(I, tile, ts, tc_cnt, tc_cnt2, tc_tiles, claim_ahead); break;
       case HK_LSTM_DW_TC: tile_lstm_dw_tc(I, tile, ts, tc_cnt, tc_cnt2, tc_tiles, claim_ahead); break;
       default: break;
     }
-    // epilogue stores (generic proxy) must be visible to later TMA (async proxy) reads
-    if (tcmode) tc::fence_proxy_async_global();
+    // epilogue stores (generic proxy) must be visible to later TMA (async proxy) reads, and a
+    // tile's generic shared-memory accesses ordered before the next tile's bulk / TMA writes
+    if (tcmode) tc::fence_proxy_async_all();
     __syncthreads();
     if (threadIdx.x == 0) {
       if (kProfBuild && A.prof) {
@@ -4511,6 +4515,21 @@ cf_status cf_session_connect(cf_session* s, int32_t peer, const void* handle, in
     cf::set_error(e.what());
     return e.code;
   }
+}
+
+int32_t cf_debug_set_knob(int32_t which, int32_t value) {
+  if (which < 0 || which >= 8) return CF_E_SHAPE;
+  return cudaMemcpyToSymbol(tc::kKnobs, &value, sizeof(value), sizeof(int) * which) == cudaSuccess
+             ? CF_OK : CF_E_CUDA;
+}
+
+int32_t cf_debug_tile_phases(uint64_t* out20, int32_t reset) {
+  if (cudaMemcpyFromSymbol(out20, g_tile_phase, 20 * 8) != cudaSuccess) return CF_E_CUDA;
+  if (reset) {
+    const unsigned long long z[20] = {};
+    if (cudaMemcpyToSymbol(g_tile_phase, z, sizeof(z)) != cudaSuccess) return CF_E_CUDA;
+  }
+  return CF_OK;
 }
 
 int32_t cf_debug_set_flags(int32_t flags) {

@@ -34,6 +34,8 @@ struct TcShared {
   volatile uint32_t* kb_issued;   // running k-block counter of the last MMA issued (hook pacing)
   uint64_t* full2;   // [kStages2]
   uint64_t* empty2;  // [kStages2]
+  uint64_t* ew_full;   // [2] bulk-staged elementwise tiles (backward EW): one per buffer
+  uint32_t* ew_uses;   // tiles staged so far (the barriers' phase)
 };
 
 // carve the dynamic smem buffer (1024-aligned for SWIZZLE_128B)
@@ -56,6 +58,8 @@ __device__ inline TcShared tc_carve(uint8_t* dyn) {
   s.empty2 = s.full2 + kStages2;
   s.tmem_slot = (uint32_t*)(s.empty2 + kStages2);
   s.kb_issued = (volatile uint32_t*)(s.tmem_slot + 1);
+  s.ew_full = (uint64_t*)(s.tmem_slot + 2);
+  s.ew_uses = (uint32_t*)(s.ew_full + 2);
   for (int i = 0; i < kStages2; ++i) {
     s.a2[i] = (uint8_t*)base + i * kStage2;
     s.b2[i] = s.a2[i] + kStage2A;
@@ -75,6 +79,9 @@ __device__ inline void tc_setup(TcShared& s) {
       mbar_init(&s.empty2[i], 1);
     }
     mbar_init(s.done, 1);
+    mbar_init(&s.ew_full[0], 1);
+    mbar_init(&s.ew_full[1], 1);
+    *s.ew_uses = 0;
     *s.kb_issued = 0;
     fence_barrier_init();
   }
@@ -112,9 +119,14 @@ struct NoHook {
 // run the hook once the MMA issuer is within 3 k-blocks of the end of the tile's mainloop
 // (end = the running k-block counter after the tile): late enough that a tile claimed there
 // does not wait long behind this one, early enough to hide the claim's round trips
+// A/B knobs (cf_debug_set_knob): [0] hook lead in k-blocks (0 = the default 8). A late hook
+// delays its warp's share of the epilogue (every warp waits for it at the staging barrier):
+// measured on cfg3 with lead 3 the forward epilogue's barrier wait was 3.1 us, with 16 0.6 us
+__device__ int kKnobs[8];
 template <class Hook>
 __device__ __forceinline__ void hook_paced(TcShared& s, uint32_t end, Hook& hook) {
-  while ((int)(end - *s.kb_issued) > 3) __nanosleep(256);
+  const int lead = kKnobs[0] > 0 ? kKnobs[0] : 8;
+  while ((int)(end - *s.kb_issued) > lead) __nanosleep(256);
   hook();
 }
 // hook: run by thread 64 (an epilogue thread, idle during the mainloop) before it waits for the

@@ -23,6 +23,24 @@ namespace cfdev {
 
 // debug flags for the tile code (cf_debug_set_flags; this header belongs to runtime.cu only)
 __device__ int kDbgFlagsTC = 0;
+// debug flag bit 22: per-kind tile phase clocks read by cf_debug_tile_phases. Slot k*4: tiles,
+// +1 cycles entry -> mainloop issue, +2 mainloop (until the accumulator is complete), +3 epilogue
+// (k: 0 forward, 1 d[x,h], 2 dW, 3 backward EW)
+__device__ unsigned long long g_tile_phase[20];   // 16..19: forward epilogue sub-phases
+__device__ __forceinline__ long long phase_now() {
+  return (kDbgFlagsTC & (1 << 22)) && threadIdx.x == 0 ? clock64() : 0;
+}
+__device__ __forceinline__ void phase_add(int k, long long t0, long long t1) {
+  if (t0 == 0) return;
+  const long long t2 = clock64();
+  atomicAdd(&g_tile_phase[4 * k + 0], 1ULL);
+  atomicAdd(&g_tile_phase[4 * k + 1], (unsigned long long)(t1 - t0));
+  atomicAdd(&g_tile_phase[4 * k + 2], (unsigned long long)(t2 - t1));
+}
+__device__ __forceinline__ void phase_epi(int k, long long t2) {
+  if (t2 == 0) return;
+  atomicAdd(&g_tile_phase[4 * k + 3], (unsigned long long)(clock64() - t2));
+}
 
 __device__ __forceinline__ float bf2f(__nv_bfloat16 v) { return __bfloat162float(v); }
 __device__ __forceinline__ float ldf(const void* p, int dt, int64_t i) {
@@ -151,6 +169,7 @@ __device__ void tile_lstm_fwd_tc(const Inst& I, int tile, tc::TcShared& ts, uint
   __nv_bfloat16* out = (__nv_bfloat16*)I.p[10];
   __nv_bfloat16* gates = (__nv_bfloat16*)I.p[11];
   const int nh = m2 ? 2 : 1;
+  const long long ph0 = phase_now();
   // ---- before the mainloop: bias slice -> smem (forget bias folded in), first c_prev, lengths
   {
     const int g = threadIdx.x / 64, u = threadIdx.x % 64;   // 256 threads = 4 gates x 64 units
@@ -188,8 +207,11 @@ __device__ void tile_lstm_fwd_tc(const Inst& I, int tile, tc::TcShared& ts, uint
   // debug flags bits 16-19: L2 prefetch distance in k-blocks (A/B; 0 = the default 4, 15 = off)
   const int pfd = (kDbgFlagsTC >> 16) & 15;
   const int ahead = pfd == 15 ? 0 : pfd ? pfd : 4;
+  const long long ph1 = ph0 ? clock64() : 0;
   if (m2) tc::tc_tile2(ts, nk - kb0, 0, 0, cnt2, ntile, plan_a, plan_b, 256, ahead, hook);
   else tc::tc_tile(ts, nk - kb0, 256, 0, 0, cnt, ntile, plan_a, plan_b, hook);
+  phase_add(0, ph0, ph1);
+  const long long ph2 = ph0 ? clock64() : 0;
   // ---- fused epilogue: 2 (or 4) groups of 16 units x 4 gates per thread. The gates and h are
   // staged in the (now idle) pipeline stage buffers and written out coalesced (debug flag bit
   // 21: direct per-row stores, A/B)
@@ -291,10 +313,16 @@ __device__ void tile_lstm_fwd_tc(const Inst& I, int tile, tc::TcShared& ts, uint
       for (int q = 0; q < 4; ++q) ((float4*)(c_next + o))[q] = *(float4*)&cp[4 * q];
     }
   }
+  const long long ph3 = ph0 ? clock64() : 0;
   if (staged && !(kDbgFlagsTC & (1 << 20))) {
     // coalesced copy-out: a warp writes a whole 512-byte gates row (or four 128-byte h / out
     // rows) per instruction instead of 32 row fragments
     __syncthreads();
+    if (ph0) {
+      const long long ph4 = clock64();
+      atomicAdd(&g_tile_phase[16], (unsigned long long)(ph3 - ph2));   // TMEM + math + staging
+      atomicAdd(&g_tile_phase[17], (unsigned long long)(ph4 - ph3));   // barrier (warp imbalance)
+    }
     const int nrows = min(128 * nh, B - m0);
     for (int rr = warp; rr < nrows; rr += 8) {
       const uint4 v = *(const uint4*)(stg + rr * kFwdGRow + lane * 16);
@@ -311,6 +339,7 @@ __device__ void tile_lstm_fwd_tc(const Inst& I, int tile, tc::TcShared& ts, uint
     tc::fence_proxy_async_smem();
   }
   tc::tc_tile_end();
+  phase_epi(0, ph2);
 }
 
 // ---------------------------------------------------------------- forward x-projection
@@ -380,11 +409,62 @@ __device__ __forceinline__ void bf4(const __nv_bfloat16* p, float* o) {
   const float2 fa = __bfloat1622float2(a), fb = __bfloat1622float2(b);
   o[0] = fa.x; o[1] = fa.y; o[2] = fb.x; o[3] = fb.y;
 }
-// tile = 128 rows x kEwUnits units (64-unit gate-interleaved slices); each thread keeps 4
-// rows' operands in flight. Small tiles: the instance's latency is on the gradient loop's
-// critical path (EW -> d[x,h] -> next step's EW)
+// one row's 4 units of the LSTM cell backward (the forward pass's c recomputed from the stored
+// gates): dz for the 4 gates, dc to the previous step; a finished row (reading R10) passes
+// dc through and has zero dz
+__device__ __forceinline__ void ew_cell4(const float* ig, const float* fg, const float* gg,
+                                         const float* og, const float* cpa, const float* dna,
+                                         const float* dca, const float* dov, bool live,
+                                         float (&zf)[4][4], float (&dco)[4]) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float cn = fg[k] * cpa[k] + ig[k] * gg[k];
+    const float tc_ = tanhf(cn);
+    const float dh = dna[k] + dov[k];
+    const float dcs = dh * og[k] * (1.0f - tc_ * tc_) + dca[k];
+    zf[0][k] = dcs * gg[k] * ig[k] * (1.0f - ig[k]);
+    zf[1][k] = dcs * cpa[k] * fg[k] * (1.0f - fg[k]);
+    zf[2][k] = dcs * ig[k] * (1.0f - gg[k] * gg[k]);
+    zf[3][k] = dh * tc_ * og[k] * (1.0f - og[k]);
+    dco[k] = dcs * fg[k];
+    if (!live) {
+      zf[0][k] = zf[1][k] = zf[2][k] = zf[3][k] = 0.0f;
+      dco[k] = dca[k];
+    }
+  }
+}
+// dz (bf16, natural [B][4H] layout) and dc stores of one row's 4 units; db sums the bf16-rounded
+// dz, exactly what the dW GEMM consumes
+__device__ __forceinline__ void ew_store4(__nv_bfloat16* zr, int64_t H, float* dcp,
+                                          const float (&zf)[4][4], const float (&dco)[4],
+                                          float (&sdb)[4][4]) {
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {
+    const __nv_bfloat162 lo = __floats2bfloat162_rn(zf[g][0], zf[g][1]);
+    const __nv_bfloat162 hi = __floats2bfloat162_rn(zf[g][2], zf[g][3]);
+    sdb[g][0] += __low2float(lo);
+    sdb[g][1] += __high2float(lo);
+    sdb[g][2] += __low2float(hi);
+    sdb[g][3] += __high2float(hi);
+    uint2 pk;
+    pk.x = *(const uint32_t*)&lo;
+    pk.y = *(const uint32_t*)&hi;
+    *(uint2*)(zr + (int64_t)g * H) = pk;
+  }
+  *(float4*)dcp = make_float4(dco[0], dco[1], dco[2], dco[3]);
+}
+// tile = 128 rows x kEwUnits units (64-unit gate-interleaved slices). Small tiles: the
+// instance's latency is on the gradient loop's critical path (EW -> d[x,h] -> next step's EW).
+// Operands go through registers, four rows at a time (the loads of four rows first, then their
+// math and stores). Debug flag bit 23 (A/B) bulk-stages them instead: warp 0 copies each row's
+// slices (gates 512 B, c_prev / dh_next / dc_next 256 B each, dout 128 or 256 B) into the idle
+// stage buffers with cp.async.bulk, 64 rows per buffer and mbarrier, and the first half computes
+// while the second lands -- measured slower on cfg3 (14.6 vs 11.1 us per tile: 640 small bulk
+// copies per tile).
 constexpr int kEwUnits = 64;   // 256 measured: 4x fewer tiles, no faster per cell, longer chain
-__device__ void tile_lstm_bwd_ew_bf(const Inst& I, int tile, float* sm) {
+constexpr int kEwRow = 1536;   // staged bytes per row
+static_assert(128 * kEwRow <= tc::kStages * (tc::kStageA + tc::kStageBmax), "EW staging fits");
+__device__ void tile_lstm_bwd_ew_bf(const Inst& I, int tile, float* sm, tc::TcShared& ts) {
   const int B = (int)I.m, H = (int)I.n;
   const int tu = (H + kEwUnits - 1) / kEwUnits;
   const int rt = tile / tu, ut0 = (tile % tu) * (kEwUnits / 64);   // first 64-unit slice
@@ -406,6 +486,31 @@ __device__ void tile_lstm_bwd_ew_bf(const Inst& I, int tile, float* sm) {
   const bool masked = I.sub & 1;
   const int64_t t = I.s[0];
   const int nrow = min(128, B - rt * 128);
+  const long long ph0 = phase_now();
+  const bool bulk = nsl == 1 && !add0 && !add1 && (kDbgFlagsTC & (1 << 23));
+  uint32_t par = 0;
+  if (bulk) {
+    const int ut = ut0;
+    const uint32_t dob = dout_bf ? 128 : 256;
+    par = *ts.ew_uses & 1;
+    if (threadIdx.x < 32) {
+      for (int pass = 0; pass < 2; ++pass) {
+        const int nv = max(0, min(64, nrow - 64 * pass));
+        uint64_t* bar = &ts.ew_full[pass];
+        if (threadIdx.x == 0) tc::mbar_arrive_expect_tx(bar, (uint32_t)nv * (512 + 768 + dob));
+        __syncwarp();
+        for (int rp = threadIdx.x; rp < nv; rp += 32) {
+          const int64_t r = (int64_t)rt * 128 + 64 * pass + rp;
+          uint8_t* d = ts.a[0] + (64 * pass + rp) * kEwRow;
+          tc::bulk_g2s(d, gates + r * 4 * H + ut * 256, 512, bar);
+          tc::bulk_g2s(d + 512, c_prev + r * H + ut * 64, 256, bar);
+          tc::bulk_g2s(d + 768, dhn + r * H + ut * 64, 256, bar);
+          tc::bulk_g2s(d + 1024, dcn + r * H + ut * 64, 256, bar);
+          tc::bulk_g2s(d + 1280, (const uint8_t*)dout + (r * H + ut * 64) * (dout_bf ? 2 : 4), dob, bar);
+        }
+      }
+    }
+  }
   bool live_r[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
@@ -416,68 +521,69 @@ __device__ void tile_lstm_bwd_ew_bf(const Inst& I, int tile, float* sm) {
     const int ut = ut0 + sl;
     const int u = ut * 64 + ul;
     float sdb[4][4] = {};
-    // rows past the batch read row 0 and store nothing
-#pragma unroll 4
-    for (int i = 0; i < 8; ++i) {
-      const int rr = rg + 16 * i;
-      const bool valid = rr < nrow;
-      const int r = rt * 128 + (valid ? rr : 0);
-      const int64_t e = (int64_t)r * H + u;
-      const __nv_bfloat16* gr = gates + (int64_t)r * 4 * H + ut * 256 + ul;
-      float ig[4], fg[4], gg[4], og[4];
-      bf4(gr, ig);
-      bf4(gr + 64, fg);
-      bf4(gr + 128, gg);
-      bf4(gr + 192, og);
-      const float4 cp = ld4f(c_prev + e), dn = ld4f(dhn + e), dcv = ld4f(dcn + e);
-      float dov[4];
-      if (dout_bf) bf4((const __nv_bfloat16*)dout + e, dov);
-      else {
-        const float4 d4 = ld4f((const float*)dout + e);
-        dov[0] = d4.x; dov[1] = d4.y; dov[2] = d4.z; dov[3] = d4.w;
-      }
-      float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0;
-      if (add0) a0 = ld4f(add0 + e);   // folded AddN terms
-      if (add1) a1 = ld4f(add1 + e);
-      const bool live = live_r[i];
-      const float cpa[4] = {cp.x, cp.y, cp.z, cp.w};
-      const float dna[4] = {dn.x + a0.x + a1.x, dn.y + a0.y + a1.y, dn.z + a0.z + a1.z, dn.w + a0.w + a1.w};
-      const float dca[4] = {dcv.x, dcv.y, dcv.z, dcv.w};
-      float zf[4][4];
-      float dco[4];
+    if (bulk) {
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const float cn = fg[k] * cpa[k] + ig[k] * gg[k];
-        const float tc_ = tanhf(cn);
-        const float dh = dna[k] + dov[k];
-        const float dcs = dh * og[k] * (1.0f - tc_ * tc_) + dca[k];
-        zf[0][k] = dcs * gg[k] * ig[k] * (1.0f - ig[k]);
-        zf[1][k] = dcs * cpa[k] * fg[k] * (1.0f - fg[k]);
-        zf[2][k] = dcs * ig[k] * (1.0f - gg[k] * gg[k]);
-        zf[3][k] = dh * tc_ * og[k] * (1.0f - og[k]);
-        dco[k] = dcs * fg[k];
-        if (!live) {
-          zf[0][k] = zf[1][k] = zf[2][k] = zf[3][k] = 0.0f;
-          dco[k] = dca[k];
+      for (int pass = 0; pass < 2; ++pass) {
+        tc::mbar_wait(&ts.ew_full[pass], par);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int i = 4 * pass + j;
+          const int rr = rg + 16 * i;   // = 64 pass + (rg + 16 j): the staged row
+          if (rr >= nrow) continue;
+          const uint8_t* sr = ts.a[0] + rr * kEwRow;
+          float ga[4][4], dov[4];
+#pragma unroll
+          for (int g = 0; g < 4; ++g) bf4((const __nv_bfloat16*)(sr + 128 * g) + ul, ga[g]);
+          const float4 cp = *(const float4*)(sr + 512 + ul * 4);
+          const float4 dn = *(const float4*)(sr + 768 + ul * 4);
+          const float4 dcv = *(const float4*)(sr + 1024 + ul * 4);
+          if (dout_bf) bf4((const __nv_bfloat16*)(sr + 1280) + ul, dov);
+          else *(float4*)dov = *(const float4*)(sr + 1280 + ul * 4);
+          const float cpa[4] = {cp.x, cp.y, cp.z, cp.w};
+          const float dna[4] = {dn.x, dn.y, dn.z, dn.w};
+          const float dca[4] = {dcv.x, dcv.y, dcv.z, dcv.w};
+          float zf[4][4], dco[4];
+          ew_cell4(ga[0], ga[1], ga[2], ga[3], cpa, dna, dca, dov, live_r[i], zf, dco);
+          const int64_t r = (int64_t)rt * 128 + rr;
+          ew_store4(dz + r * 4 * H + u, H, dc + r * H + u, zf, dco, sdb);
         }
       }
-      if (!valid) continue;
-      __nv_bfloat16* zr = dz + (int64_t)r * 4 * H + u;
+    } else {
+      // rows past the batch read row 0 and store nothing
 #pragma unroll
-      for (int g = 0; g < 4; ++g) {
-        const __nv_bfloat162 lo = __floats2bfloat162_rn(zf[g][0], zf[g][1]);
-        const __nv_bfloat162 hi = __floats2bfloat162_rn(zf[g][2], zf[g][3]);
-        // db sums the bf16-rounded dz, exactly what the dW GEMM consumes
-        sdb[g][0] += __low2float(lo);
-        sdb[g][1] += __high2float(lo);
-        sdb[g][2] += __low2float(hi);
-        sdb[g][3] += __high2float(hi);
-        uint2 pk;
-        pk.x = *(const uint32_t*)&lo;
-        pk.y = *(const uint32_t*)&hi;
-        *(uint2*)(zr + (int64_t)g * H) = pk;
+      for (int i0 = 0; i0 < 8; i0 += 4) {
+        float ga[4][4][4], cpv[4][4], dnv[4][4], dcv4[4][4], dov4[4][4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int rr = rg + 16 * (i0 + j);
+          const int r = rt * 128 + (rr < nrow ? rr : 0);
+          const int64_t e = (int64_t)r * H + u;
+          const __nv_bfloat16* gr = gates + (int64_t)r * 4 * H + ut * 256 + ul;
+#pragma unroll
+          for (int g = 0; g < 4; ++g) bf4(gr + 64 * g, ga[j][g]);
+          const float4 cp = ld4f(c_prev + e), dn = ld4f(dhn + e), dc4 = ld4f(dcn + e);
+          float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0;
+          if (add0) a0 = ld4f(add0 + e);   // folded AddN terms
+          if (add1) a1 = ld4f(add1 + e);
+          if (dout_bf) bf4((const __nv_bfloat16*)dout + e, dov4[j]);
+          else *(float4*)dov4[j] = ld4f((const float*)dout + e);
+          *(float4*)cpv[j] = cp;
+          *(float4*)dcv4[j] = dc4;
+          *(float4*)dnv[j] = make_float4(dn.x + a0.x + a1.x, dn.y + a0.y + a1.y, dn.z + a0.z + a1.z,
+                                         dn.w + a0.w + a1.w);
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int i = i0 + j;
+          const int rr = rg + 16 * i;
+          if (rr >= nrow) continue;
+          float zf[4][4], dco[4];
+          ew_cell4(ga[j][0], ga[j][1], ga[j][2], ga[j][3], cpv[j], dnv[j], dcv4[j], dov4[j],
+                   live_r[i], zf, dco);
+          const int64_t r = (int64_t)rt * 128 + rr;
+          ew_store4(dz + r * 4 * H + u, H, dc + r * H + u, zf, dco, sdb);
+        }
       }
-      *(float4*)(dc + e) = make_float4(dco[0], dco[1], dco[2], dco[3]);
     }
     // reduce the 16 row groups of this slice: sm[rg][g][64]
 #pragma unroll
@@ -493,16 +599,20 @@ __device__ void tile_lstm_bwd_ew_bf(const Inst& I, int tile, float* sm) {
     }
     __syncthreads();
   }
+  if (bulk) {
+    if (threadIdx.x == 0) *ts.ew_uses += 1;   // every thread read the phase before the barrier above
+    tc::fence_proxy_async_smem();             // staged reads before the next tile's async writes
+  }
+  phase_add(3, ph0, ph0);
 }
 
 // ---------------------------------------------------------------- backward d[x,h]
 // p: 0 dz-map (KA), 1 WT-map (KB; the KA map of the same buffer is the one before it),
 //    5 lens, 6 dh_next(f32), 11 dx(f32), 12 dh(f32); s: 0 t, 2 dz slot
-// 256-row tiles (sub bit 1) are 256 rows x 128 columns: twice the tiles of a 256 x 256 split,
-// half the latency per instance. The d[x,h] GEMM sits on the gradient loop's critical path
-// (EW -> d[x,h] -> next step's EW; the backward is latency-bound on cfg3), the operand bytes
-// per flop are 1.5x those of 256 x 256 but the backward's L2 load is well below its cap.
-constexpr int kDxhN2 = 256;   // 128 measured: 41% less efficient per flop, no net gain
+// 256-row tiles (sub bit 1) are 256 rows x kDxhN2 columns. The d[x,h] GEMM sits on the gradient
+// loop's critical path (EW -> d[x,h] -> next step's EW); 128-column tiles (twice the tiles, half
+// the latency each) were measured 41% less efficient per flop with no net gain.
+constexpr int kDxhN2 = 256;
 template <class Hook>
 __device__ void tile_lstm_dxh_tc(const Inst& I, int tile, tc::TcShared& ts, uint32_t& cnt,
                                  uint32_t& cnt2, uint32_t& ntile, Hook hook) {
@@ -525,8 +635,68 @@ __device__ void tile_lstm_dxh_tc(const Inst& I, int tile, tc::TcShared& ts, uint
     b[0] = {mwt, kb * 64, nt * bn, 0, 0, keep_w};
     return 1;
   };
+  const long long ph0 = phase_now();
   if (m2) tc::tc_tile2(ts, (4 * H) / 64, 0, 0, cnt2, ntile, plan_a, plan_b, bn, 0, hook);
   else tc::tc_tile(ts, (4 * H) / 64, 256, 0, 0, cnt, ntile, plan_a, plan_b, hook);
+  phase_add(1, ph0, ph0);
+  const long long ph2 = ph0 ? clock64() : 0;
+  if (m2 && bn == 256 && !(kDbgFlagsTC & (1 << 21))) {
+    // four passes of 128 rows x 128 columns through two stage buffers; the copy engine writes
+    // each 512-byte row (cp.async.bulk) while the next pass is staged (debug flag bit 21: the
+    // legacy thread stores, A/B)
+    constexpr int kRow = 512 + 16;
+    static_assert(2 * 128 * kRow <= tc::kStages * (tc::kStageA + tc::kStageBmax), "d[x,h] staging fits");
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int rl = 32 * (warp % 4) + lane;
+    const bool masked = I.sub & 1;
+    const int64_t t = I.s[0];
+    const int64_t* lens = (const int64_t*)I.p[5];
+    const float* dhn = (const float*)I.p[6];
+    const int n0 = nt * 256;   // the tile is all dx or all dh columns (In % 256 == 0)
+    float* dst0 = n0 < In ? (float*)I.p[11] + n0 : (float*)I.p[12] + (n0 - In);
+    const int64_t ld = n0 < In ? In : H;
+    for (int pass = 0; pass < 4; ++pass) {
+      const int half = pass >> 1, cb = (pass & 1) * 128;
+      uint8_t* stg = ts.a[0] + (pass & 1) * 128 * kRow;
+      if (pass >= 2) {
+        if (threadIdx.x < 128) tc::bulk_wait_read1();
+        __syncthreads();
+      }
+      const int r = m0 + 128 * half + rl;
+      const bool dead_row = r < B && masked && !(t < lens[r]);
+      const int c0 = (warp / 4) * 64;   // this warp's 64 columns of the pass: four loads, one wait
+      uint32_t v[4][16];
+      const uint32_t ta = *ts.tmem_slot + ((uint32_t)(32 * (warp % 4)) << 16) + (uint32_t)(256 * half + cb + c0);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) tc::tmem_ld16_nowait(ta + 16 * j, v[j]);
+      tc::tmem_wait_ld();
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (n0 >= In && dead_row) {   // finished row: dh passes dh_next through (reading R10)
+          const int64_t o = (int64_t)r * H + (n0 - In) + cb + c0 + 16 * j;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) *(float4*)&v[j][4 * q] = ((const float4*)(dhn + o))[q];
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          *(uint4*)(stg + rl * kRow + (c0 + 16 * j + 4 * q) * 4) = *(uint4*)&v[j][4 * q];
+      }
+      tc::fence_proxy_async_smem();
+      __syncthreads();
+      const int rr = m0 + 128 * half + (int)threadIdx.x;
+      if (threadIdx.x < 128 && rr < B) {
+        tc::bulk_s2g(dst0 + (int64_t)rr * ld + cb, stg + threadIdx.x * kRow, 512);
+        tc::bulk_commit();
+      }
+    }
+    if (threadIdx.x < 128) {
+      tc::bulk_wait_all();   // dx / dh written before the tile completes
+      tc::fence_proxy_async_global();
+    }
+    tc::tc_tile_end();
+    phase_epi(1, ph2);
+    return;
+  }
   // epilogue: per 128-row half, the accumulator goes through the (idle) stage buffers and out
   // as whole 1 KB rows (debug flag bit 21: direct per-row stores, A/B)
   const bool staged = !(kDbgFlagsTC & (1 << 21)) && bn == 256;
@@ -586,6 +756,7 @@ __device__ void tile_lstm_dxh_tc(const Inst& I, int tile, tc::TcShared& ts, uint
   }
   if (staged) tc::fence_proxy_async_smem();   // the next tile's TMA overwrites the stage buffers
   tc::tc_tile_end();
+  phase_epi(1, ph2);
 }
 
 // ---------------------------------------------------------------- backward dW / db
@@ -635,12 +806,59 @@ __device__ void tile_lstm_dw_tc(const Inst& I, int tile, tc::TcShared& ts, uint3
     for (int j = 0; j < 4; ++j) b[j] = {mb, col0 + 64 * j, r * 64, sb, j * 8192};
     return 4;
   };
+  const long long ph0 = phase_now();
   tc::tc_tile2(ts, ns * nkb, 1, 1, cnt2, ntile, plan_a, plan_b, 256, 0, hook);
+  phase_add(2, ph0, ph0);
+  const long long ph2 = ph0 ? clock64() : 0;
+  const bool acc = flags & 1;
+  if (!(kDbgFlagsTC & (1 << 21))) {
+    // four passes of 128 rows x 128 columns: the accumulator goes to the (idle) stage buffers
+    // as 512-byte rows and the copy engine adds them into dW in L2 (cp.reduce.async.bulk
+    // .add.f32; a plain bulk copy for the chunk that starts the accumulation). The SM never
+    // reads the old dW, and each pass is staged while the previous one drains (two buffers)
+    constexpr int kRow = 512 + 16;   // padded rows: conflict-free 16-byte stores
+    static_assert(2 * 128 * kRow <= tc::kStages * (tc::kStageA + tc::kStageBmax), "dW staging fits");
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int rl = 32 * (warp % 4) + lane;
+    for (int pass = 0; pass < 4; ++pass) {
+      const int half = pass >> 1, cb = (pass & 1) * 128;   // accumulator, first column
+      uint8_t* stg = ts.a[0] + (pass & 1) * 128 * kRow;
+      if (pass >= 2) {   // this buffer's previous pass has been read by the copy engine
+        if (threadIdx.x < 128) tc::bulk_wait_read1();
+        __syncthreads();
+      }
+      const int c0 = (warp / 4) * 64;   // this warp's 64 columns of the pass: four loads, one wait
+      uint32_t v[4][16];
+      const uint32_t ta = *ts.tmem_slot + ((uint32_t)(32 * (warp % 4)) << 16) + (uint32_t)(256 * half + cb + c0);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) tc::tmem_ld16_nowait(ta + 16 * j, v[j]);
+      tc::tmem_wait_ld();
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          *(uint4*)(stg + rl * kRow + (c0 + 16 * j + 4 * q) * 4) = *(uint4*)&v[j][4 * q];
+      tc::fence_proxy_async_smem();   // generic-proxy stores -> the bulk copy's async reads
+      __syncthreads();
+      if (threadIdx.x < 128) {
+        float* dst = (float*)I.p[3] + (int64_t)(m0 + 128 * half + threadIdx.x) * KT + nt * 256 + cb;
+        if (acc) tc::bulk_s2g_add_f32(dst, stg + threadIdx.x * kRow, 512);
+        else tc::bulk_s2g(dst, stg + threadIdx.x * kRow, 512);
+        tc::bulk_commit();
+      }
+    }
+    if (threadIdx.x < 128) {
+      tc::bulk_wait_all();                // dW written before the tile completes
+      tc::fence_proxy_async_global();
+    }
+    tc::tc_tile_end();                    // (its barrier also keeps the stage buffers until read)
+    phase_epi(2, ph2);
+    return;
+  }
   for (int half = 0; half < 2; ++half) {
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int m = m0 + 128 * half + 32 * (warp % 4) + lane;
   float* dW = (float*)I.p[3] + (int64_t)m * KT + nt * 256;
-  const bool acc = flags & 1;
   for (int c = (warp / 4) * 128; c < (warp / 4) * 128 + 128; c += 32) {
     float v[32];
     tc::tc_acc16(ts, 256 * half + c, v);
@@ -663,6 +881,7 @@ __device__ void tile_lstm_dw_tc(const Inst& I, int tile, tc::TcShared& ts, uint3
   }
   }
   tc::tc_tile_end();
+  phase_epi(2, ph2);
 }
 
 }  // namespace cfdev

@@ -1,7 +1,8 @@
-"""A/B of the dW chunk length (debug flag bits 24-27; 0 = 8 steps) on cfg3: ms per run.
+"""A/B of the dW chunk length (CF_DW_CHUNK at compile time; default 8 steps) on cfg3: ms per run.
 
-Also checks the fetched gradients against the default chunk (fp32 accumulation order is the
-only difference, so they agree to rounding)."""
+One session per chunk length (the dz and swap-in rings are sized for it). Also checks the
+fetched gradients against the first chunk (fp32 accumulation order is the only difference, so
+they agree to rounding) and, with PHASES=1, prints the tile phase clocks of one run."""
 import os
 import sys
 
@@ -18,24 +19,52 @@ from synth import rnn_inputs  # noqa: E402
 
 c = dict(CONFIGS[os.environ.get("CFG", "cfg3")])
 p = dynamic_rnn_lstm(c["T"], c["B"], c["I"], c["H"], c["L"])
-s = cf.Session(p.g, p.fetch_tensors(), precision=cf.BF16)
 f = rnn_inputs(c["T"], c["B"], c["I"], c["H"], c["L"], seed=0, len_mode=c["len_mode"], bf16=True)
-dev = feeds_to_device(f, session=s)
-outs = s.alloc_outputs()
-for _ in range(2):
-    s.run(dev, outs)
-torch.cuda.synchronize()
-ref = [o.clone() for o in outs]
-chunks = [int(x) for x in os.environ.get("CHUNKS", "8 1 2 4 6").split()]
+chunks = [int(x) for x in os.environ.get("CHUNKS", "8 12 16").split()]
+sessions = {}
+for ch in chunks:
+    os.environ["CF_DW_CHUNK"] = str(ch)
+    s = cf.Session(p.g, p.fetch_tensors(), precision=cf.BF16)
+    sessions[ch] = (s, feeds_to_device(f, session=s), s.alloc_outputs())
+os.environ.pop("CF_DW_CHUNK")
+flags = [int(x) for x in os.environ.get("FLAGS", "0").split(",")]   # cf_debug_set_flags A/B
+knob0 = [int(x) for x in os.environ.get("KNOB0", "0").split(",")]   # cf_debug_set_knob(0, v)
+ref = None
 for rep in range(2):
     for ch in chunks:
-        cf.debug_set_flags((ch & 15) << 24)
-        ts = []
-        for _ in range(3):
-            _, _, tr = s.run(dev, outs, trace=True)
-            ts.append(tr["wall_ms"])
-        torch.cuda.synchronize()
-        err = max(float(((a.double() - b.double()).abs().max() /
-                         (b.double().abs().max() + 1e-30))) for a, b in zip(outs, ref))
-        print(f"dw_chunk={ch}: {sorted(ts)[1]:.2f} ms  max rel diff vs chunk 8 {err:.2e}", flush=True)
+        for fl, k0 in [(a, b) for a in flags for b in knob0]:
+            cf.debug_set_flags(fl)
+            cf.debug_set_knob(0, k0)
+            s, dev, outs = sessions[ch]
+            s.run(dev, outs)
+            ts = []
+            for _ in range(3):
+                _, _, tr = s.run(dev, outs, trace=True)
+                ts.append(tr["wall_ms"])
+            torch.cuda.synchronize()
+            if ref is None:
+                ref = [o.clone() for o in outs]
+            err = max(float(((a.double() - b.double()).abs().max() /
+                             (b.double().abs().max() + 1e-30))) for a, b in zip(outs, ref))
+            print(f"dw_chunk={ch} flags={fl} knob0={k0}: {sorted(ts)[1]:.2f} ms  max rel diff vs the first "
+                  f"{err:.2e}", flush=True)
 cf.debug_set_flags(0)
+cf.debug_set_knob(0, 0)
+if os.environ.get("PHASES"):
+    cf.debug_set_knob(0, knob0[-1])
+    s, dev, outs = sessions[chunks[0]]
+    cf.debug_tile_phases(reset=True)
+    cf.debug_set_flags(1 << 22)
+    _, _, tr = s.run(dev, outs, trace=True)
+    torch.cuda.synchronize()
+    cf.debug_set_flags(0)
+    ph = cf.debug_tile_phases(reset=True)
+    ghz = 1.95
+    for k, name in enumerate(["fwd", "dxh", "dw", "bwd_ew"]):
+        n = max(ph[4 * k], 1)
+        print(f"phases {name}: tiles {ph[4 * k]}  setup {ph[4 * k + 1] / n / ghz / 1e3:.2f} us  "
+              f"mainloop {ph[4 * k + 2] / n / ghz / 1e3:.2f} us  epilogue {ph[4 * k + 3] / n / ghz / 1e3:.2f} us"
+              f"  (run {tr['wall_ms']:.2f} ms with the clocks on)", flush=True)
+    n = max(ph[0], 1)
+    print(f"phases fwd epilogue: TMEM+math+staging {ph[16] / n / ghz / 1e3:.2f} us, barrier "
+          f"{ph[17] / n / ghz / 1e3:.2f} us, copy-out = the rest", flush=True)

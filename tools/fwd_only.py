@@ -34,4 +34,9 @@ for fl in flags:
     torch.cuda.synchronize()
     print(f"forward only (flags {fl}, B={c['B']} T={c['T']} L={c['L']}): {sorted(ts)[len(ts) // 2]:.2f} ms "
           f"median of {reps}, {tr['instances']} instances")
+    if fl & (1 << 22):   # tile phase clocks (cf_debug.h), averaged over the reps
+        ph = cf.debug_tile_phases(reset=True)
+        n = max(ph[0], 1)
+        print(f"  fwd tile phases: {ph[0]} tiles, setup {ph[1] / n / 1.95e3:.2f} us, mainloop "
+              f"{ph[2] / n / 1.95e3:.2f} us, epilogue {ph[3] / n / 1.95e3:.2f} us (1.95 GHz)")
 cf.debug_set_flags(0)

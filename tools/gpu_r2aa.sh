@@ -1,0 +1,4 @@
+set -x
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/r2aa_build.log 2>&1
+timeout 1500 python -m pytest tests -m gpu -x -q 2>&1 | tail -4
+PHASES=1 CHUNKS="8" FLAGS=0,2097152 timeout 600 python tools/dwchunk_ab.py 2>&1 | grep "dw_chunk\|phases"
