@@ -59,7 +59,8 @@ int32_t cf_debug_set_knob(int32_t which, int32_t value);
  * [4k + 1] SM cycles from tile entry to the mainloop's first issue, [4k + 2] mainloop cycles
  * (until the accumulator is complete; for the backward EW the whole tile), [4k + 3] epilogue
  * cycles; k = 0 forward, 1 d[x,h], 2 dW, 3 backward EW (thread 0 of each tile); [16] forward
- * epilogue TMEM + math + staging, [17] its barrier wait. reset != 0 zeroes the counters after
+ * epilogue TMEM + math + staging, [17] its barrier wait, [18] / [19] forward tiles' wall-clock
+ * ns / SM cycles (their ratio is the SM clock under load). reset != 0 zeroes the counters after
  * the read. Returns 0 or CF_E_CUDA. */
 int32_t cf_debug_tile_phases(uint64_t* out20, int32_t reset);
 /* Compile a graph for the device program without a GPU and write its description and body

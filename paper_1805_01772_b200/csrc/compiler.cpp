@@ -63,6 +63,11 @@ struct Compiler {
   CompileOpts o;
   HostProgram P;
   std::vector<int> vbase, ctrl_vid, frame_of;   // per node
+  std::vector<bool> root_dead;                  // per node: root code nothing needs
+  std::map<int, int> one_mul;                  // root Mul by a constant one -> kept input
+  std::map<int, TRef> wt_root;                 // LSTMCellGrad node -> root value of its W
+  std::map<int, int> wt_buf;                   // 2 W value id (+1 packed W) -> shared buffer
+  std::map<int, int> wt_leader;                // 2 W value id (+1 packed W) -> preparing node
   std::vector<std::vector<std::pair<int, int>>> cons;   // per value: (consumer node, input idx)
   std::map<std::string, int> frame_id;
   std::vector<int> frame_ctx;
@@ -191,6 +196,45 @@ struct Compiler {
     }
     P.bufs.push_back(std::move(b));
     return (int)P.bufs.size() - 1;
+  }
+
+  // root value of a tensor-core LSTMCellGrad node's weight (-1: not a root value). The weight
+  // reaches the gradient loop through a stack (autodiff saves the forward body's Enter'ed W,
+  // PAPER.md:416-420): follow the pop to its pushes, and the pushed value through Switch /
+  // Identity / Enter to the root value (all pushes must agree)
+  TRef weight_root(const Node& n) {
+    auto stack_of = [&](TRef h) -> int {
+      for (int k = 0; k < 64; ++k) {
+        const Node& hn = g.nodes[h.node];
+        if (hn.op == "StackCreate") return hn.id;
+        if (hn.in.empty()) return -1;
+        h = hn.in[0];
+      }
+      return -1;
+    };
+    std::function<TRef(TRef, int)> root_of = [&](TRef v, int depth) -> TRef {
+      for (int k = 0; k < 64 && v.node >= 0 && depth < 4; ++k) {
+        const Node& m = g.nodes[v.node];
+        if (frame_of[m.id] < 0 && m.op != "Exit") return v;
+        if (m.op == "Enter" || m.op == "Identity" || m.op == "Switch") {
+          v = m.in[0];
+        } else if (m.op == "StackPop") {
+          const int sid = stack_of(m.in[0]);
+          TRef r{-1, 0};
+          for (auto& q : g.nodes)
+            if (q.op == "StackPush" && stack_of(q.in[0]) == sid) {
+              const TRef rq = root_of(q.in[1], depth + 1);
+              if (rq.node < 0 || (r.node >= 0 && !(rq == r))) return TRef{-1, 0};
+              r = rq;
+            }
+          return r;
+        } else {
+          return TRef{-1, 0};
+        }
+      }
+      return TRef{-1, 0};
+    };
+    return root_of(n.in[3], 0);
   }
 
   // trace a TensorArray handle back to its static TA id
@@ -333,6 +377,64 @@ struct Compiler {
         P.stack_depths += s.instances;
       }
     }
+    // ---- root algebra: 1 * v is v exactly. autodiff's gradient of a loss term sum(R * out)
+    // is Fill(dy) * R with dy the seed 1: the Mul becomes a view of R and the Fill dies below
+    auto is_one = [&](TRef t, auto&& self) -> bool {
+      const Node& n = g.nodes[t.node];
+      if (n.op == "Fill" || n.op == "Identity") return self(n.in[0], self);
+      if (n.op != "Const" || !g.shape(t).empty()) return false;
+      if (n.odt[0] == F32 && n.data.size() == 4) {
+        float v;
+        std::memcpy(&v, n.data.data(), 4);
+        return v == 1.0f;
+      }
+      if (n.odt[0] == F64 && n.data.size() == 8) {
+        double v;
+        std::memcpy(&v, n.data.data(), 8);
+        return v == 1.0;
+      }
+      return false;
+    };
+    for (auto& n : g.nodes) {
+      if (n.op != "Mul" || frame_of[n.id] >= 0) continue;
+      for (int j = 0; j < 2; ++j)
+        if (is_one(n.in[j], is_one) && g.shape(n.in[1 - j]) == n.osh[0] &&
+            g.dtype(n.in[1 - j]) == n.odt[0]) {
+          one_mul[n.id] = 1 - j;
+          break;
+        }
+    }
+    // ---- root dead-code elimination: a side-effect-free root op none of whose results reaches
+    // a fetch, a frame or an effectful op is never evaluated (e.g. the gradients autodiff
+    // builds for inputs nobody asked for: d R_out = dy * out of a Mul in the loss)
+    root_dead.assign(N, false);
+    {
+      static const std::set<std::string> pure = {
+          "Mul", "Add", "Sub", "Neg", "Fill", "ReduceSum", "ReduceMax", "ReduceMin", "MatMul",
+          "Tanh", "Sigmoid", "Relu", "Const", "Identity", "Cast", "Transpose", "BiasAdd", "AddN",
+          "ZerosLike", "Less", "LessEqual", "Greater", "Equal", "LogicalAnd", "LogicalNot",
+          "Reshape", "Slice"};
+      std::vector<char> live(N, 0);
+      std::vector<int> work;
+      auto mark = [&](int x) {
+        if (!live[x]) { live[x] = 1; work.push_back(x); }
+      };
+      for (auto& t : fetches) mark(t.node);
+      for (auto& n : g.nodes)
+        if (frame_of[n.id] >= 0 || n.op == "Exit" || !pure.count(n.op)) mark(n.id);
+      while (!work.empty()) {
+        const int x = work.back();
+        work.pop_back();
+        auto om = one_mul.find(x);
+        if (om != one_mul.end()) {   // only the operand the view keeps
+          mark(g.nodes[x].in[om->second].node);
+          continue;
+        }
+        for (auto& t : g.nodes[x].in) mark(t.node);
+        for (int c : g.nodes[x].ctrl) mark(c);
+      }
+      for (int i = 0; i < N; ++i) root_dead[i] = !live[i];
+    }
     detect_accumulators();
     fuse_dout_sums();
 
@@ -345,7 +447,11 @@ struct Compiler {
       d.n_in = (int)n.in.size();
       d.in_off = (int)P.in_vids.size();
       auto fz = fused_dout.find(n.id);
-      if (fz == fused_dout.end()) {
+      auto om = one_mul.find(n.id);
+      if (om != one_mul.end()) {   // 1 * v: a view of v
+        d.n_in = 1;
+        P.in_vids.push_back(vid(n.in[om->second]));
+      } else if (fz == fused_dout.end()) {
         for (auto& t : n.in) P.in_vids.push_back(vid(t));
       } else {
         // LSTMCellGrad with its dout AddN folded in: dout = AddN input 0, the other AddN
@@ -418,7 +524,8 @@ struct Compiler {
           if (dd == D_BF16 && n.osh[0].size() >= 2) register_shape((int)d.imm[0], n.osh[0], 1);
         }
       } else if (op == "Identity" || op == "StopGradient" || op == "Reshape" ||
-                 (op == "Cast" && is_float(odt) && is_float(g.dtype(n.in[0])))) {
+                 (op == "Cast" && is_float(odt) && is_float(g.dtype(n.in[0]))) ||
+                 one_mul.count(n.id)) {
         d.op = OP_PASS;
       } else if (op == "Switch") {
         d.op = OP_SWITCH;
@@ -468,8 +575,8 @@ struct Compiler {
         if (op == "Recv") heavy_nodes.push_back(n.id);   // output placed like a heavy output
       } else if (odt == FLOW) {
         d.op = OP_FLOW;
-      } else if (fused_addn.count(n.id)) {
-        d.op = OP_NOP;   // folded into its LSTMCellGrad consumer (not in any body program)
+      } else if (fused_addn.count(n.id) || root_dead[n.id]) {
+        // folded into its LSTMCellGrad consumer (not in any body program), or dead root code
       } else if (acc_of_add.count(n.id)) {
         d.op = OP_ACC;
         d.aux[0] = acc_of_add.at(n.id);
@@ -515,6 +622,21 @@ struct Compiler {
     P.dw_chunk = bf16() ? kDwChunk : 1;
     if (const char* e = std::getenv("CF_DW_CHUNK"); e && bf16())   // A/B (tools/dwchunk_ab.py)
       P.dw_chunk = std::max(1, std::min(kDwMax, std::atoi(e)));
+    // weights of the tensor-core LSTM nodes: the nodes of one root weight (a layer's masked and
+    // unmasked cells) share one prepared buffer (packed W forward, W^T backward) and one
+    // preparation, issued as a root step (kRootPrep)
+    if (bf16() && std::getenv("CF_NO_ROOT_HINTS") == nullptr)
+      for (int nid : heavy_nodes) {
+        const Node& n = g.nodes[nid];
+        if ((n.op != "LSTMCellGrad" && n.op != "LSTMCell") || frame_of[nid] < 0) continue;
+        const TRef w = weight_root(n);
+        if (w.node < 0 || frame_of[w.node] >= 0 || g.nodes[w.node].op == "Exit") continue;
+        wt_root[nid] = w;
+        const int key = 2 * vid(w) + (n.op == "LSTMCell" ? 1 : 0);   // W^T or packed W of it
+        if (!wt_leader.count(key)) wt_leader[key] = nid;
+        // low 32 bits: root W value id + 1; high 32: the node whose preparation it shares + 1
+        P.nodes[nid].imm[3] = (int64_t)(vid(w) + 1) | ((int64_t)(wt_leader.at(key) + 1) << 32);
+      }
     for (int nid : heavy_nodes) place_outputs(g.nodes[nid]);
 
     // ---- evaluation orders
@@ -878,11 +1000,18 @@ struct Compiler {
         pl.slots = acc_it->second;   // acc id
         pl.base = -1;
         pl.dt = D_F32;
+      } else if ((kind == WTPREP || kind == WPREP) && wt_root.count(n.id) &&
+                 wt_buf.count(2 * vid(wt_root.at(n.id)) + (kind == WPREP ? 1 : 0))) {
+        pl.kind = PL_ROOT;   // the prepared weight another node of the same root weight prepares
+        pl.slots = 1;
+        pl.base = wt_buf.at(2 * vid(wt_root.at(n.id)) + (kind == WPREP ? 1 : 0));
       } else if (kind == WPREP || kind == WTPREP || f < 0) {
         pl.kind = PL_ROOT;
         pl.slots = 1;
         pl.base = add_buf(pl.elem_bytes, false, "root " + n.op + std::to_string(n.id));
         if (dd == D_BF16) register_shape((int)pl.base, shp, 1);
+        if ((kind == WTPREP || kind == WPREP) && wt_root.count(n.id))
+          wt_buf[2 * vid(wt_root.at(n.id)) + (kind == WPREP ? 1 : 0)] = (int)pl.base;
       } else if (taw >= 0 && P.tas[trace_ta(g.nodes[taw].in[0])].elem_bytes == body &&
                  P.tas[trace_ta(g.nodes[taw].in[0])].dt == dd) {
         const Node& w = g.nodes[taw];
@@ -1537,7 +1666,7 @@ struct Compiler {
     // item id: node i -> i ; frame f -> N + f
     std::vector<int> items;
     for (int i = 0; i < N; ++i)
-      if (frame_of[i] < 0 && g.nodes[i].op != "Exit") items.push_back(i);
+      if (frame_of[i] < 0 && g.nodes[i].op != "Exit" && !root_dead[i]) items.push_back(i);
     for (size_t f = 0; f < frame_ctx.size(); ++f)
       if (frame_parent[f] < 0) items.push_back(N + (int)f);
     auto item_of = [&](int node) -> int {
@@ -1548,10 +1677,11 @@ struct Compiler {
     std::map<int, int> indeg;
     for (int it : items) indeg[it] = 0;
     auto edge = [&](int a, int b) {
-      if (a == b) return;
+      if (a == b || (a < N && root_dead[a])) return;   // a view's dropped operand (1 * v)
       if (succ[a].insert(b).second) indeg[b]++;
     };
     for (int i = 0; i < N; ++i) {
+      if (root_dead[i]) continue;   // (its inputs may be live; no edge into a dead item)
       int dst = item_of(i);
       for (auto& t : g.nodes[i].in) edge(item_of(t.node), dst);
       for (int c : g.nodes[i].ctrl) edge(item_of(c), dst);
@@ -1604,7 +1734,46 @@ struct Compiler {
         }
     }
     if (ord.size() != items.size()) throw CfError(CF_E_INVALID_GRAPH, "root graph has a cycle");
-    for (int it : ord) P.root_steps.push_back(it >= N ? -(it - N + 1) : it);
+    // Root scheduling hints (program.h kRootLow / kRootPrep):
+    // - heavy root work no frame depends on (the loss value, fetch-only sums) goes to the
+    //   low-priority queue, where it fills idle workers instead of delaying the next loop;
+    // - each tensor-core LSTMCellGrad's W^T preparation is issued right after its weight is
+    //   available (low priority), so it runs under the forward loop instead of between loops.
+    std::vector<char> for_frame(N, 0);
+    {
+      std::vector<int> work;
+      for (auto& n : g.nodes)
+        if (frame_of[n.id] >= 0 || n.op == "Exit")
+          for (auto& t : n.in)
+            if (frame_of[t.node] < 0 && !for_frame[t.node]) {
+              for_frame[t.node] = 1;
+              work.push_back(t.node);
+            }
+      while (!work.empty()) {
+        const int x = work.back();
+        work.pop_back();
+        for (auto& t : g.nodes[x].in)
+          if (!for_frame[t.node]) {
+            for_frame[t.node] = 1;
+            work.push_back(t.node);
+          }
+      }
+    }
+    const bool hints = std::getenv("CF_NO_ROOT_HINTS") == nullptr;   // A/B switch
+    std::map<int, std::vector<int>> prep_after;   // root producer of W -> leader LSTM nodes
+    if (hints)
+      for (auto& [key, nid] : wt_leader) prep_after[wt_root.at(nid).node].push_back(nid);
+    for (auto& [wn, v] : prep_after)   // the forward's packed W first (LSTMCell ids are lower)
+      std::sort(v.begin(), v.end());
+    for (int it : ord) {
+      if (it >= N) {
+        P.root_steps.push_back(-(it - N + 1));
+        continue;
+      }
+      const bool low = hints && P.nodes[it].op == OP_HEAVY && !for_frame[it];
+      P.root_steps.push_back(low ? it | kRootLow : it);
+      for (int gn : prep_after[it]) P.root_steps.push_back(gn | kRootPrep);
+    }
   }
 };
 
@@ -1618,6 +1787,14 @@ HostProgram compile(const Graph& g, const CompileOpts& o, const std::vector<TRef
   // body program listing (debug hook cf_debug_program_listing)
   {
     std::ostringstream ls;
+    ls << "root";
+    for (int s : c.P.root_steps) {
+      if (s < 0) ls << " [frame " << c.P.frame_names[-s - 1] << "]";
+      else if (s & kRootPrep) ls << " prep(" << g.nodes[s & kRootNode].op << (s & kRootNode) << ")";
+      else if (s & kRootLow) ls << " " << g.nodes[s & kRootNode].op << (s & kRootNode) << "(low)";
+      else ls << " " << g.nodes[s].op << s;
+    }
+    ls << "\n";
     for (size_t f = 0; f < c.P.frames.size(); ++f) {
       const auto& F = c.P.frames[f];
       ls << "frame " << c.P.frame_names[f] << "\n";

@@ -101,9 +101,34 @@ __global__ void __launch_bounds__(256, 1)
   extern __shared__ uint8_t dyn[];
   tc::TcShared s = tc::tc_carve(dyn);
   tc::tc_setup(s);
-  const int tm = M / 256, tn = N / 256, nk = K / 64;
-  uint32_t cnt2 = 0, tiles = 0;
+  const int tn = N / 256, nk = K / 64;
+  uint32_t cnt2 = 0, tiles = 0, cnt = 0;
   const long long c0 = clock64();
+  if (pf < 0) {   // 128-row tiles (tc_tile, one 128 x 256 accumulator)
+    const int tm = M / 128;
+    for (int w = blockIdx.x; w < tm * tn * nb * reps; w += gridDim.x) {
+      const int b = (w / (tm * tn)) % nb, mt = (w % (tm * tn)) / tn, nt = w % tn;
+      const CUtensorMap* ma = maps;
+      const CUtensorMap* mb = maps + 1;
+      auto plan_a = [&](int kb, tc::Box* bx) {
+        bx[0] = {ma, kb * 64, mt * 128, 0, 0};
+        return 1;
+      };
+      auto plan_b = [&](int kb, tc::Box* bx) {
+        bx[0] = {mb, kb * 64, nt * 256, b, 0, 1};
+        return 1;
+      };
+      tc::tc_tile(s, nk, 256, 0, 0, cnt, tiles, plan_a, plan_b);
+      float v[16];
+      tc::tc_acc16(s, 0, v);
+      if (v[0] == 12345.f) cycles[1] = 1;
+      tc::tc_tile_end();
+    }
+    if (threadIdx.x == 0) atomicAdd(cycles, (unsigned long long)(clock64() - c0));
+    tc::tc_teardown(s);
+    return;
+  }
+  const int tm = M / 256;
   for (int w = blockIdx.x; w < tm * tn * nb * reps; w += gridDim.x) {
     const int b = (w / (tm * tn)) % nb, mt = (w % (tm * tn)) / tn, nt = w % tn;
     const CUtensorMap* ma = maps;

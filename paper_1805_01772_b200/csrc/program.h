@@ -220,6 +220,11 @@ struct DChan {
 };
 
 constexpr int kDwMax = 16;   // most gradient-loop steps one dW instance accumulates
+// root step tags (Prog.root_steps: node id, or -(frame + 1)): a heavy root node no frame
+// depends on, published to the low-priority queue; the early W^T preparation of a tensor-core
+// LSTMCellGrad node (the node's imm[3]: root weight's value id + 1 in the low 32 bits, the
+// node whose preparation and W^T buffer it shares + 1 in the high 32 bits)
+constexpr int32_t kRootLow = 1 << 29, kRootPrep = 1 << 30, kRootNode = kRootLow - 1;
 
 struct Prog {
   int32_t n_nodes, n_vids, n_frames, n_tas, n_stacks;

@@ -1320,7 +1320,9 @@ struct Driver {
     r_nt[sl] = ntiles;
     // iteration in the top 16 bits; 0xFFFF = read the full iteration from the record (loops
     // longer than 65534 iterations)
-    r_kfi[sl] = (int)((unsigned)(kind & 255) | ((unsigned)((cur_frame + 1) & 255) << 8) |
+    // bit 7 of the kind byte: low-priority queue (root work no frame depends on)
+    r_kfi[sl] = (int)((unsigned)(kind & 127) | (low_root_ ? 128u : 0u) |
+                      ((unsigned)((cur_frame + 1) & 255) << 8) |
                       ((unsigned)min(cur_frame >= 0 ? iter : 0, 0xFFFF) << 16));
     return id;
   }
@@ -1420,7 +1422,7 @@ struct Driver {
       st_release_sys_u64(A.io_req_tail, io_tail);
       return;
     }
-    const bool low = (r_kfi[sl] & 255) == HK_LSTM_DW_TC;
+    const bool low = (r_kfi[sl] & 255) == HK_LSTM_DW_TC || (r_kfi[sl] & 128);
     // one entry per instance; workers claim its tiles through tile_next[id]. At most kRing
     // instances are in flight, so the 2^22-entry rings never wrap onto live entries.
     if (kProfBuild && A.prof) A.prof[6 * (int64_t)id + 1] = globaltimer();
@@ -1506,6 +1508,7 @@ struct Driver {
 
   long long last_drain_ = 0;
   int dbg_ = 0;
+  bool low_root_ = false;   // the root step being evaluated is low priority (kRootLow)
   // dW chunk length in steps (K = chunk * B per dW tile): the compiler's P.dw_chunk, which
   // sized the dz and swap-in rings
   __device__ __forceinline__ int dw_chunk() const { return P.dw_chunk; }
@@ -1679,6 +1682,37 @@ struct Driver {
   }
 
   // per-run weight preparation (bf16 permuted W / W^T), created on first use of the node
+  // the W^T preparation of tensor-core LSTMCellGrad node nid from its root weight (value id
+  // imm[3] - 1), issued as soon as the weight is available, at low priority: it runs under
+  // the forward loop; the node's first gradient step finds it in prep_inst_
+  // the node whose W^T preparation a gradient LSTM node shares (compiler: one per root weight)
+  __device__ __forceinline__ int prep_slot(const DNode& d, int nid) const {
+    return (d.imm[3] >> 32) > 0 ? (int)(d.imm[3] >> 32) - 1 : nid;
+  }
+  __noinline__ __device__ bool prep_early(int nid) {
+    const DNode& d = node(nid);
+    if (prep_inst_[nid] >= 0 || (d.imm[3] & 0xffffffffLL) <= 0) return true;
+    const Tok& w = toks_[(d.imm[3] & 0xffffffffLL) - 1];
+    const bool fwd = d.aux[0] == HK_LSTM_FWD;   // packed W (needed first) or W^T (low priority)
+    const PlaceDesc& pl = places_[d.place_off + (fwd ? 4 : 6)];
+    if (w.kind != TK_PTR || pl.kind != PL_ROOT) return true;   // the node prepares it itself
+    const int64_t In = d.imm[1], H = d.imm[2], KT = In + H;
+    low_root_ = !fwd;
+    const int32_t id = fwd ? new_inst(HK_PREP_WP, 0, (int)((4 * H + 15) / 16))
+                           : new_inst(HK_PREP_WT, 0, (int)((KT / 64) * (4 * H / 128)));
+    low_root_ = false;
+    if (id < 0) return false;
+    Inst& I = A.insts[id];
+    I.n = H;
+    I.k = KT;
+    I.p[0] = w.v;
+    I.p[13] = pl.base;   // the node's W^T place
+    add_dep(id, w.writer);
+    submit(id);
+    prep_inst_[nid] = id;
+    return true;
+  }
+
   __noinline__ __device__ int32_t prep(const DNode& d, int nid, int kind, int64_t dst) {
     if (prep_inst_[nid] >= 0) return prep_inst_[nid];
     const int64_t In = d.imm[1], H = d.imm[2], KT = In + H;
@@ -1714,7 +1748,7 @@ struct Driver {
       // job is started below
       int64_t op_[6];
       for (int k = 0; k < 6; ++k) op_[k] = outp[k];
-      int32_t pw = prep(d, nid, HK_PREP_WP, op_[4]);
+      int32_t pw = prep(d, prep_slot(d, nid), HK_PREP_WP, op_[4]);
       int64_t mx, sx, mh, sh, mw, sw;
       if (pm) {
         mx = pm[0]; sx = ps[0]; mh = pm[1]; sh = ps[1]; mw = pm[2]; sw = ps[2];
@@ -1785,7 +1819,7 @@ struct Driver {
     const int o = masked ? 7 : 5;
     const int64_t dz_ptr = outp[5];
     const int64_t dz_bytes = ((B * 4 * H * 2 + 1023) / 1024) * 1024;
-    int32_t pw = prep(d, nid, HK_PREP_WT, outp[6]);
+    int32_t pw = prep(d, prep_slot(d, nid), HK_PREP_WT, outp[6]);
     int64_t mz, sz, mwt, swt, mzn, szn, mxn, sxn, mhn, shn;
     if (pm) {
       mz = pm[0]; sz = ps[0]; mwt = pm[1]; swt = ps[1]; mzn = pm[2]; szn = ps[2];
@@ -1913,17 +1947,19 @@ struct Driver {
       const bool m2 = B >= kM2MinRows;
       (void)m2rows;
       if (d.aux[0] == HK_LSTM_FWD) {
-        if (prep_inst_[nid] < 0) {
+        const int ps = prep_slot(d, nid);   // shared with the other nodes of its weight
+        if (prep_inst_[ps] < 0) {
           id[3] = reserve_inst(HK_PREP_WP, (int)((4 * H + 15) / 16));
-          prep_inst_[nid] = id[3];
+          prep_inst_[ps] = id[3];
         }
         const int nt = (int)((m2 ? (B + 255) / 256 : (B + 127) / 128) * (H / 64));
         if (d.aux[1] & 4) id[1] = reserve_inst(HK_LSTM_XPROJ_TC, nt);   // x-projection first
         id[0] = reserve_inst(HK_LSTM_FWD_TC, nt);
       } else {
-        if (prep_inst_[nid] < 0) {
+        const int ps = prep_slot(d, nid);   // shared with the other nodes of its weight
+        if (prep_inst_[ps] < 0) {
           id[3] = reserve_inst(HK_PREP_WT, (int)((KT / 64) * (4 * H / 128)));
-          prep_inst_[nid] = id[3];
+          prep_inst_[ps] = id[3];
         }
         const int acc_w = d.aux[3], acc_b = d.aux[4];
         if (!(acc_w >= 0 && acc_b >= 0) || dw_count_[nid] + 1 >= dw_chunk()) {
@@ -2020,7 +2056,7 @@ struct Driver {
       add_dep_atomic(idd, wr);
     };
     if (d.aux[0] == HK_LSTM_FWD) {
-      int32_t pw = prep_inst_[nid];
+      int32_t pw = prep_inst_[prep_slot(d, nid)];
       if (id[3] >= 0) {   // per-run weight preparation (gate-interleaved bf16 W)
         inst_header(id[3], HK_PREP_WP, 0, (int)((4 * H + 15) / 16));
         Inst& Q = A.insts[id[3]];
@@ -2066,7 +2102,7 @@ struct Driver {
     const int o = masked ? 7 : 5;
     const int64_t dz_ptr = outp[5];
     const int64_t dz_bytes = ((B * 4 * H * 2 + 1023) / 1024) * 1024;
-    const int32_t pw = prep_inst_[nid];
+    const int32_t pw = prep_inst_[prep_slot(d, nid)];
     if (id[3] >= 0) {   // per-run weight preparation (bf16 W^T)
       inst_header(id[3], HK_PREP_WT, 0, (int)((KT / 64) * (4 * H / 128)));
       Inst& Q = A.insts[id[3]];
@@ -3262,8 +3298,16 @@ struct Driver {
         return false;
       }
       int s = P.root_steps[root_pc];
+      if (s >= kRootPrep) {   // early W^T preparation of a tensor-core LSTMCellGrad node
+        if (!prep_early(s & kRootNode)) return false;
+        root_pc++;
+        return true;
+      }
       if (s >= 0) {
-        int r = eval(node(s), s);
+        const int nid = s & kRootNode;
+        low_root_ = (s & kRootLow) != 0;   // instances of a node no frame waits for
+        int r = eval(node(nid), nid);
+        low_root_ = false;
         if (r != EV_OK) return false;
         root_pc++;
         return true;
@@ -3545,7 +3589,7 @@ __device__ void worker_loop(const RunArgs& A) {
       case HK_PREP_WT: tile_prep_wt(I, tile, (float*)dyn_smem); break;
       case HK_LSTM_FWD_TC: tile_lstm_fwd_tc(I, tile, ts, tc_cnt, tc_cnt2, tc_tiles, sm, claim_ahead); break;
       case HK_LSTM_XPROJ_TC: tile_lstm_xproj_tc(I, tile, ts, tc_cnt, tc_cnt2, tc_tiles, claim_ahead); break;
-      case HK_LSTM_BWD_EW_BF: tile_lstm_bwd_ew_bf(I, tile, sm, ts); break;
+      case HK_LSTM_BWD_EW_BF: tile_lstm_bwd_ew_bf(I, tile, sm); break;
       case HK_LSTM_DXH_TC: tile_lstm_dxh_tc(I, tile, ts, tc_cnt, tc_cnt2, tc_tiles, claim_ahead); break;
       case HK_LSTM_DW_TC: tile_lstm_dw_tc(I, tile, ts, tc_cnt, tc_cnt2, tc_tiles, claim_ahead); break;
       default: break;

@@ -34,8 +34,6 @@ struct TcShared {
   volatile uint32_t* kb_issued;   // running k-block counter of the last MMA issued (hook pacing)
   uint64_t* full2;   // [kStages2]
   uint64_t* empty2;  // [kStages2]
-  uint64_t* ew_full;   // [2] bulk-staged elementwise tiles (backward EW): one per buffer
-  uint32_t* ew_uses;   // tiles staged so far (the barriers' phase)
 };
 
 // carve the dynamic smem buffer (1024-aligned for SWIZZLE_128B)
@@ -58,8 +56,6 @@ __device__ inline TcShared tc_carve(uint8_t* dyn) {
   s.empty2 = s.full2 + kStages2;
   s.tmem_slot = (uint32_t*)(s.empty2 + kStages2);
   s.kb_issued = (volatile uint32_t*)(s.tmem_slot + 1);
-  s.ew_full = (uint64_t*)(s.tmem_slot + 2);
-  s.ew_uses = (uint32_t*)(s.ew_full + 2);
   for (int i = 0; i < kStages2; ++i) {
     s.a2[i] = (uint8_t*)base + i * kStage2;
     s.b2[i] = s.a2[i] + kStage2A;
@@ -79,9 +75,6 @@ __device__ inline void tc_setup(TcShared& s) {
       mbar_init(&s.empty2[i], 1);
     }
     mbar_init(s.done, 1);
-    mbar_init(&s.ew_full[0], 1);
-    mbar_init(&s.ew_full[1], 1);
-    *s.ew_uses = 0;
     *s.kb_issued = 0;
     fence_barrier_init();
   }

@@ -170,6 +170,8 @@ __device__ void tile_lstm_fwd_tc(const Inst& I, int tile, tc::TcShared& ts, uint
   __nv_bfloat16* gates = (__nv_bfloat16*)I.p[11];
   const int nh = m2 ? 2 : 1;
   const long long ph0 = phase_now();
+  unsigned long long gt0 = 0;   // wall-clock ns beside the SM cycles (the clock under load)
+  if (ph0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt0));
   // ---- before the mainloop: bias slice -> smem (forget bias folded in), first c_prev, lengths
   {
     const int g = threadIdx.x / 64, u = threadIdx.x % 64;   // 256 threads = 4 gates x 64 units
@@ -340,6 +342,12 @@ __device__ void tile_lstm_fwd_tc(const Inst& I, int tile, tc::TcShared& ts, uint
   }
   tc::tc_tile_end();
   phase_epi(0, ph2);
+  if (ph0) {
+    unsigned long long gt1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt1));
+    atomicAdd(&g_tile_phase[18], gt1 - gt0);
+    atomicAdd(&g_tile_phase[19], (unsigned long long)(clock64() - ph0));
+  }
 }
 
 // ---------------------------------------------------------------- forward x-projection
@@ -455,16 +463,14 @@ __device__ __forceinline__ void ew_store4(__nv_bfloat16* zr, int64_t H, float* d
 }
 // tile = 128 rows x kEwUnits units (64-unit gate-interleaved slices). Small tiles: the
 // instance's latency is on the gradient loop's critical path (EW -> d[x,h] -> next step's EW).
-// Operands go through registers, four rows at a time (the loads of four rows first, then their
-// math and stores). Debug flag bit 23 (A/B) bulk-stages them instead: warp 0 copies each row's
-// slices (gates 512 B, c_prev / dh_next / dc_next 256 B each, dout 128 or 256 B) into the idle
-// stage buffers with cp.async.bulk, 64 rows per buffer and mbarrier, and the first half computes
-// while the second lands -- measured slower on cfg3 (14.6 vs 11.1 us per tile: 640 small bulk
-// copies per tile).
+// Operands go through registers, four rows at a time: the loads of four rows first, then their
+// math and stores (the stores may alias the loads as far as the compiler knows; row by row,
+// every row's loads waited for the previous row's stores: 13.1 -> 11.1 us per tile). Staging
+// the operands in shared memory was measured no better: bulk copies issued by one warp (640 of
+// 128-512 B per tile) 14.6 us, per-thread cp.async copies of all 8 rows 14.5 us (cfg3; the
+// tile's stalls are spread over memory, instruction fetch and issue).
 constexpr int kEwUnits = 64;   // 256 measured: 4x fewer tiles, no faster per cell, longer chain
-constexpr int kEwRow = 1536;   // staged bytes per row
-static_assert(128 * kEwRow <= tc::kStages * (tc::kStageA + tc::kStageBmax), "EW staging fits");
-__device__ void tile_lstm_bwd_ew_bf(const Inst& I, int tile, float* sm, tc::TcShared& ts) {
+__device__ void tile_lstm_bwd_ew_bf(const Inst& I, int tile, float* sm) {
   const int B = (int)I.m, H = (int)I.n;
   const int tu = (H + kEwUnits - 1) / kEwUnits;
   const int rt = tile / tu, ut0 = (tile % tu) * (kEwUnits / 64);   // first 64-unit slice
@@ -487,30 +493,6 @@ __device__ void tile_lstm_bwd_ew_bf(const Inst& I, int tile, float* sm, tc::TcSh
   const int64_t t = I.s[0];
   const int nrow = min(128, B - rt * 128);
   const long long ph0 = phase_now();
-  const bool bulk = nsl == 1 && !add0 && !add1 && (kDbgFlagsTC & (1 << 23));
-  uint32_t par = 0;
-  if (bulk) {
-    const int ut = ut0;
-    const uint32_t dob = dout_bf ? 128 : 256;
-    par = *ts.ew_uses & 1;
-    if (threadIdx.x < 32) {
-      for (int pass = 0; pass < 2; ++pass) {
-        const int nv = max(0, min(64, nrow - 64 * pass));
-        uint64_t* bar = &ts.ew_full[pass];
-        if (threadIdx.x == 0) tc::mbar_arrive_expect_tx(bar, (uint32_t)nv * (512 + 768 + dob));
-        __syncwarp();
-        for (int rp = threadIdx.x; rp < nv; rp += 32) {
-          const int64_t r = (int64_t)rt * 128 + 64 * pass + rp;
-          uint8_t* d = ts.a[0] + (64 * pass + rp) * kEwRow;
-          tc::bulk_g2s(d, gates + r * 4 * H + ut * 256, 512, bar);
-          tc::bulk_g2s(d + 512, c_prev + r * H + ut * 64, 256, bar);
-          tc::bulk_g2s(d + 768, dhn + r * H + ut * 64, 256, bar);
-          tc::bulk_g2s(d + 1024, dcn + r * H + ut * 64, 256, bar);
-          tc::bulk_g2s(d + 1280, (const uint8_t*)dout + (r * H + ut * 64) * (dout_bf ? 2 : 4), dob, bar);
-        }
-      }
-    }
-  }
   bool live_r[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
@@ -521,34 +503,7 @@ __device__ void tile_lstm_bwd_ew_bf(const Inst& I, int tile, float* sm, tc::TcSh
     const int ut = ut0 + sl;
     const int u = ut * 64 + ul;
     float sdb[4][4] = {};
-    if (bulk) {
-#pragma unroll
-      for (int pass = 0; pass < 2; ++pass) {
-        tc::mbar_wait(&ts.ew_full[pass], par);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int i = 4 * pass + j;
-          const int rr = rg + 16 * i;   // = 64 pass + (rg + 16 j): the staged row
-          if (rr >= nrow) continue;
-          const uint8_t* sr = ts.a[0] + rr * kEwRow;
-          float ga[4][4], dov[4];
-#pragma unroll
-          for (int g = 0; g < 4; ++g) bf4((const __nv_bfloat16*)(sr + 128 * g) + ul, ga[g]);
-          const float4 cp = *(const float4*)(sr + 512 + ul * 4);
-          const float4 dn = *(const float4*)(sr + 768 + ul * 4);
-          const float4 dcv = *(const float4*)(sr + 1024 + ul * 4);
-          if (dout_bf) bf4((const __nv_bfloat16*)(sr + 1280) + ul, dov);
-          else *(float4*)dov = *(const float4*)(sr + 1280 + ul * 4);
-          const float cpa[4] = {cp.x, cp.y, cp.z, cp.w};
-          const float dna[4] = {dn.x, dn.y, dn.z, dn.w};
-          const float dca[4] = {dcv.x, dcv.y, dcv.z, dcv.w};
-          float zf[4][4], dco[4];
-          ew_cell4(ga[0], ga[1], ga[2], ga[3], cpa, dna, dca, dov, live_r[i], zf, dco);
-          const int64_t r = (int64_t)rt * 128 + rr;
-          ew_store4(dz + r * 4 * H + u, H, dc + r * H + u, zf, dco, sdb);
-        }
-      }
-    } else {
+    {
       // rows past the batch read row 0 and store nothing
 #pragma unroll
       for (int i0 = 0; i0 < 8; i0 += 4) {
@@ -598,10 +553,6 @@ __device__ void tile_lstm_bwd_ew_bf(const Inst& I, int tile, float* sm, tc::TcSh
       partial[(int64_t)rt * 4 * H + g * H + ut * 64 + uu] = acc;
     }
     __syncthreads();
-  }
-  if (bulk) {
-    if (threadIdx.x == 0) *ts.ew_uses += 1;   // every thread read the phase before the barrier above
-    tc::fence_proxy_async_smem();             // staged reads before the next tile's async writes
   }
   phase_add(3, ph0, ph0);
 }

@@ -59,7 +59,8 @@ if os.environ.get("PHASES"):
     torch.cuda.synchronize()
     cf.debug_set_flags(0)
     ph = cf.debug_tile_phases(reset=True)
-    ghz = 1.95
+    ghz = ph[19] / max(ph[18], 1)   # SM cycles per ns over the forward tiles
+    print(f"phases: SM clock under load {ghz:.3f} GHz (forward tiles' cycles / globaltimer ns)")
     for k, name in enumerate(["fwd", "dxh", "dw", "bwd_ew"]):
         n = max(ph[4 * k], 1)
         print(f"phases {name}: tiles {ph[4 * k]}  setup {ph[4 * k + 1] / n / ghz / 1e3:.2f} us  "
