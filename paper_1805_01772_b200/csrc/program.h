@@ -300,10 +300,19 @@ struct RunState {
   long long op_count[64], op_cycles[64];   // driver self-profile: opcodes [0,32), regions [32,64)
 };
 
+// a placeholder's token for this run, applied to the token table by the driver CTA at start
+struct PresetTok {
+  int64_t vid;
+  Tok t;
+};
+
 struct RunArgs {
   Prog prog;
   RunState* st;
   Tok* toks;                 // [n_vids]
+  const PresetTok* preset;   // [n_preset] this run's placeholder tokens (one upload per run)
+  int32_t n_preset;
+  int32_t pad_preset;
   Tok* stack_pool;           // stack entries
   int32_t* stack_depth;      // [n_stacks]
   int64_t* ta_base;          // [n_tas] runtime base (may alias on unstack)

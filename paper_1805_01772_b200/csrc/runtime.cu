@@ -3503,10 +3503,23 @@ __device__ void worker_loop(const RunArgs& A) {
   const int n_low = kLowWorkers & 0xffff;
   const bool low_first = (int)blockIdx.x <= n_low;
   const bool no_low = n_low > 0 && !low_first && (kLowWorkers >> 16);
+  // race check (cf_run_opts.sched_seed != 0): every claim attempt first sleeps a pseudo-random
+  // 0-4 us and picks the ring order at random, so tiles run in other orders and at other times
+  // than FIFO; results must not change (tests/test_gpu_sched.py)
+  uint32_t sched_ctr = 0;
   auto try_claim = [&](unsigned long long* e) -> bool {
+    bool lf = low_first;
+    if (A.sched_seed) {
+      uint32_t h = (uint32_t)A.sched_seed * 0x9E3779B9u ^ (blockIdx.x * 0x85EBCA6Bu) ^ (++sched_ctr * 0xC2B2AE35u);
+      h ^= h >> 16;
+      h *= 0x7FEB352Du;
+      h ^= h >> 15;
+      __nanosleep(h & 4095);
+      lf = lf || (h >> 31);
+    }
     for (int k = 0; k < 8; ++k) {
       int r = 0;
-      if (low_first) {
+      if (lf) {
         r = claim(&st->lq_head, &st->lq_tail, A.lq, e);
         if (r == 1) return true;
         if (r == 2) continue;
@@ -3514,7 +3527,7 @@ __device__ void worker_loop(const RunArgs& A) {
       r = claim(&st->q_head, &st->q_tail, A.queue, e);
       if (r == 1) return true;
       if (r == 2) continue;
-      if (low_first || no_low) return false;
+      if (lf || no_low) return false;
       r = claim(&st->lq_head, &st->lq_tail, A.lq, e);
       if (r == 1) return true;
       if (r == 2) continue;
@@ -3650,6 +3663,9 @@ __global__ void __launch_bounds__(kThreads, 1) cf_driver_kernel(RunArgs A_param)
     extern __shared__ __align__(1024) uint8_t drv_smem[];
     __shared__ int req[16];   // [0] seq (-1: quit), [1] helpers done, [4..15] copy args
     __shared__ Wave wave;     // routing waves evaluated by the helper warps
+    // this run's placeholder tokens into the (zeroed) table before anything reads it
+    for (int k = threadIdx.x; k < A.n_preset; k += blockDim.x) A.toks[A.preset[k].vid] = A.preset[k].t;
+    __syncthreads();
     Tok* toks = A.toks;
     DNode* smn = nullptr;
     int32_t* smi = nullptr;
@@ -3862,6 +3878,13 @@ struct cf_session {
   std::vector<CUtensorMap> maps_host;
   int n_reg_static = 0;
   std::vector<DReg> reg_sorted;   // per-run upload, sorted by base
+  // per-run parameters (tensor maps of bf16 feeds, registry, TA bases, placeholder tokens,
+  // fetch pointers) go through one pinned staging area: every upload is asynchronous, no
+  // stream synchronisation before the launch
+  uint8_t* stage_host = nullptr;
+  size_t stage_cap = 0;
+  PresetTok* d_preset = nullptr;
+  int preset_cap = 0;
   // cross-GPU channels (a14): this session's halves live in one IPC-exported allocation
   void* chan_mem = nullptr;
   std::vector<DChan> chans;        // device view (remote pointers filled by cf_session_connect)
@@ -4301,6 +4324,7 @@ cf_status cf_run(cf_session* s, int32_t n_feed, const char* const* feed_names,
       preset_vid.push_back(fi.vid);
     }
     // bf16 feeds become TMA operands: registry entries + tensor maps for this run
+    int nf_maps = 0;
     if (s->precision == CF_BF16) {
       int n = s->n_reg_static;
       for (int i = 0; i < n_feed; ++i) {
@@ -4323,27 +4347,14 @@ cf_status cf_run(cf_session* s, int32_t n_feed, const char* const* feed_names,
         s->maps_host[3 * n + 2] = cf::make_map_bf16_strided(b.data, cols, rows, slots, r.slot_bytes, 64, 64);
         ++n;
       }
-      int nf = n - s->n_reg_static;
-      if (nf > 0) {
-        CUDA_OK(cudaMemcpyAsync((uint8_t*)A.prog.maps + sizeof(CUtensorMap) * 3 * s->n_reg_static,
-                                s->maps_host.data() + 3 * s->n_reg_static, sizeof(CUtensorMap) * 3 * nf,
-                                cudaMemcpyHostToDevice, s->stream));
-      }
+      nf_maps = n - s->n_reg_static;
       // the device looks entries up by binary search over base
       s->reg_sorted.assign(s->reg_host.begin(), s->reg_host.begin() + n);
       for (auto& r : s->reg_sorted) r.inv_slot = 1.0 / (double)r.slot_bytes;
       std::sort(s->reg_sorted.begin(), s->reg_sorted.end(),
                 [](const DReg& a, const DReg& b) { return a.base < b.base; });
-      CUDA_OK(cudaMemcpyAsync((void*)A.prog.reg, s->reg_sorted.data(), sizeof(DReg) * n,
-                              cudaMemcpyHostToDevice, s->stream));
       A.prog.n_reg = n;
     }
-    // ta bases reset (unstack may alias)
-    CUDA_OK(cudaMemcpyAsync(A.ta_base, s->ta_base_host.data(), 8 * s->ta_base_host.size(),
-                            cudaMemcpyHostToDevice, s->stream));
-    for (size_t k = 0; k < preset.size(); ++k)
-      CUDA_OK(cudaMemcpyAsync(A.toks + preset_vid[k], &preset[k], sizeof(Tok),
-                              cudaMemcpyHostToDevice, s->stream));
     std::vector<void*> fo(P.fetches.size());
     for (size_t i = 0; i < P.fetches.size(); ++i) {
       fo[i] = outs ? outs[i].data : nullptr;
@@ -4354,23 +4365,56 @@ cf_status cf_run(cf_session* s, int32_t n_feed, const char* const* feed_names,
                                           std::to_string(buffer_bytes(outs[i])) + " bytes, fetch needs " +
                                           std::to_string(P.fetches[i].bytes));
     }
-    if (!fo.empty())
-      CUDA_OK(cudaMemcpyAsync(A.fetch_out, fo.data(), 8 * fo.size(), cudaMemcpyHostToDevice, s->stream));
-    if (!s->chans.empty()) {
+    if (!s->chans.empty())
       for (auto& c : s->chans)
         if (!(c.flags && c.data && c.acks && c.done))
           throw cf::CfError(CF_E_UNSUPPORTED, "channel " + std::to_string(c.channel) + " to rank " +
                                                   std::to_string(c.peer) +
                                                   " not connected (cf_session_connect)");
-      if (s->chans_dirty) {
-        CUDA_OK(cudaMemcpyAsync(s->d_chans, s->chans.data(), sizeof(DChan) * s->chans.size(),
-                                cudaMemcpyHostToDevice, s->stream));
-        s->chans_dirty = false;
-      }
+    // ---- one pinned staging area, then asynchronous uploads from it
+    const bool up_chans = !s->chans.empty() && s->chans_dirty;
+    auto al = [](size_t x) { return (x + 127) / 128 * 128; };
+    const size_t b_maps = sizeof(CUtensorMap) * 3 * (size_t)nf_maps, b_reg = sizeof(DReg) * s->reg_sorted.size();
+    const size_t b_ta = 8 * s->ta_base_host.size(), b_pre = sizeof(PresetTok) * preset.size();
+    const size_t b_fo = 8 * fo.size(), b_ch = up_chans ? sizeof(DChan) * s->chans.size() : 0;
+    const size_t o_maps = 0, o_reg = al(o_maps + b_maps), o_ta = al(o_reg + b_reg), o_pre = al(o_ta + b_ta);
+    const size_t o_fo = al(o_pre + b_pre), o_ch = al(o_fo + b_fo), total = al(o_ch + b_ch);
+    if (total > s->stage_cap) {
+      if (s->stage_host) cudaFreeHost(s->stage_host);
+      s->stage_host = nullptr;
+      s->stage_cap = 0;
+      CUDA_OK(cudaMallocHost((void**)&s->stage_host, total * 2));
+      s->stage_cap = total * 2;
+    }
+    if ((int)preset.size() > s->preset_cap) {
+      if (s->d_preset) cudaFree(s->d_preset);
+      s->d_preset = nullptr;
+      s->preset_cap = 0;
+      CUDA_OK(cudaMalloc((void**)&s->d_preset, sizeof(PresetTok) * preset.size()));
+      s->preset_cap = (int)preset.size();
+    }
+    uint8_t* sh = s->stage_host;
+    auto upload = [&](void* dst, size_t off, const void* src, size_t bytes) {
+      if (!bytes) return;
+      std::memcpy(sh + off, src, bytes);
+      CUDA_OK(cudaMemcpyAsync(dst, sh + off, bytes, cudaMemcpyHostToDevice, s->stream));
+    };
+    upload((uint8_t*)A.prog.maps + sizeof(CUtensorMap) * 3 * s->n_reg_static, o_maps,
+           s->maps_host.data() + 3 * s->n_reg_static, b_maps);
+    upload((void*)A.prog.reg, o_reg, s->reg_sorted.data(), b_reg);
+    upload(A.ta_base, o_ta, s->ta_base_host.data(), b_ta);   // ta bases reset (unstack may alias)
+    std::vector<PresetTok> pt(preset.size());
+    for (size_t k = 0; k < preset.size(); ++k) pt[k] = PresetTok{preset_vid[k], preset[k]};
+    upload(s->d_preset, o_pre, pt.data(), b_pre);
+    A.preset = s->d_preset;
+    A.n_preset = (int32_t)preset.size();
+    upload(A.fetch_out, o_fo, fo.data(), b_fo);
+    if (up_chans) {
+      upload(s->d_chans, o_ch, s->chans.data(), b_ch);
+      s->chans_dirty = false;
     }
     A.epoch = ++s->epoch;
-    // the copies above read pageable host memory; make them complete before it goes away
-    CUDA_OK(cudaStreamSynchronize(s->stream));
+    // (the staging area is rewritten only by the next cf_run, after this one's final sync)
     void* kargs[] = {(void*)&A};
     // host I/O executor for swapped stacks (separate streams for
     // GPU-to-CPU and CPU-to-GPU transfers next to the compute stream)
@@ -4619,6 +4663,8 @@ void cf_session_destroy(cf_session* s) {
   for (void* p : s->allocs) cudaFree(p);
   for (auto& [r, p] : s->peer_mem) cudaIpcCloseMemHandle(p);
   for (void* h : s->host_allocs) cudaFreeHost(h);
+  if (s->stage_host) cudaFreeHost(s->stage_host);
+  if (s->d_preset) cudaFree(s->d_preset);
   for (int k = 0; k < cf_session::kIoStreams; ++k) {
     if (s->io_d2h[k]) cudaStreamDestroy(s->io_d2h[k]);
     if (s->io_h2d[k]) cudaStreamDestroy(s->io_h2d[k]);

@@ -192,7 +192,25 @@ __device__ void tile_lstm_fwd_tc(const Inst& I, int tile, tc::TcShared& ts, uint
     const int r = row_of(h);
     live_h[h] = h < nh && r < B && (!masked || t < lens[r]);
   }
-  __syncthreads();   // the bias slice is in shared memory
+  // a tile whose rows have all finished (t >= len for every row, "we skip
+  // the computation"): no GEMM; every row copies its state through and emits zeros (R10)
+  if (__syncthreads_or(live_h[0] || live_h[1]) == 0) {
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+      if (it >= 2 * nh) break;
+      const int r = row_of(it >> 1);
+      if (r >= B) continue;
+      const int64_t o = (int64_t)r * H + nt * 64 + cbase + 16 * (it & 1);
+      float v[16];
+      load_bf16x16(h_prev + o, v);
+      store_bf16x16(h_next + o, v);
+      float z[16] = {};
+      store_bf16x16(out + o, z);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) ((float4*)(c_next + o))[q] = ((const float4*)(c_prev + o))[q];
+    }
+    return;
+  }
   auto plan_a = [&](int kb, tc::Box* b) {
     kb += kb0;
     for (int hh = 0; hh < (m2 ? 2 : 1); ++hh) {
@@ -494,10 +512,32 @@ __device__ void tile_lstm_bwd_ew_bf(const Inst& I, int tile, float* sm) {
   const int nrow = min(128, B - rt * 128);
   const long long ph0 = phase_now();
   bool live_r[8];
+  bool any = false;
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     const int rr = rg + 16 * i;
     live_r[i] = !masked || (rr < nrow && t < lens[rt * 128 + rr]);
+    any |= rr < nrow && live_r[i];
+  }
+  if (masked && __syncthreads_or(any) == 0) {
+    // no live row: dz = 0, dc passes through, the db partials are 0
+    for (int sl = 0; sl < nsl; ++sl) {
+      const int ut = ut0 + sl;
+      const int u = ut * 64 + ul;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int rr = rg + 16 * i;
+        if (rr >= nrow) continue;
+        const int64_t r = (int64_t)rt * 128 + rr, e = r * H + u;
+        __nv_bfloat16* zr = dz + r * 4 * H + u;
+#pragma unroll
+        for (int g = 0; g < 4; ++g) *(uint2*)(zr + (int64_t)g * H) = make_uint2(0u, 0u);
+        *(float4*)(dc + e) = ld4f(dcn + e);
+      }
+      const int g = threadIdx.x / 64, uu = threadIdx.x % 64;
+      partial[(int64_t)rt * 4 * H + g * H + ut * 64 + uu] = 0.f;
+    }
+    return;
   }
   for (int sl = 0; sl < nsl; ++sl) {
     const int ut = ut0 + sl;
@@ -586,6 +626,30 @@ __device__ void tile_lstm_dxh_tc(const Inst& I, int tile, tc::TcShared& ts, uint
     b[0] = {mwt, kb * 64, nt * bn, 0, 0, keep_w};
     return 1;
   };
+  if (I.sub & 1) {
+    // finished rows have dz = 0 (the EW tile), so their dx is 0 and their dh is dh_next: a
+    // tile with no live row skips the GEMM and writes exactly that
+    const int64_t t = I.s[0];
+    const int64_t* lens = (const int64_t*)I.p[5];
+    const int rows = m2 ? 2 * tc::BM : tc::BM;
+    bool any = false;
+    for (int rr = threadIdx.x; rr < rows; rr += blockDim.x)
+      any |= m0 + rr < B && t < lens[m0 + rr];
+    if (__syncthreads_or(any) == 0) {
+      const int n0 = nt * bn;
+      const float* dhn = (const float*)I.p[6];
+      float* dst = n0 < In ? (float*)I.p[11] + n0 : (float*)I.p[12] + (n0 - In);
+      const int64_t ld = n0 < In ? In : H;
+      const int nr = min(rows, B - m0), nq = bn / 4;
+      for (int q = threadIdx.x; q < nr * nq; q += blockDim.x) {
+        const int rr = q / nq, c = (q % nq) * 4;
+        const int64_t r = m0 + rr;
+        *(float4*)(dst + r * ld + c) = n0 < In ? make_float4(0.f, 0.f, 0.f, 0.f)
+                                               : *(const float4*)(dhn + r * H + (n0 - In) + c);
+      }
+      return;
+    }
+  }
   const long long ph0 = phase_now();
   if (m2) tc::tc_tile2(ts, (4 * H) / 64, 0, 0, cnt2, ntile, plan_a, plan_b, bn, 0, hook);
   else tc::tc_tile(ts, (4 * H) / 64, 256, 0, 0, cnt, ntile, plan_a, plan_b, hook);

@@ -34,6 +34,12 @@ def lengths(rng: np.random.Generator, B: int, T: int, mode: str) -> np.ndarray:
         return l.astype(np.int64)
     if mode == "upper_half":       # len_b ~ U{T/2..T}
         return rng.integers(T // 2, T + 1, size=B).astype(np.int64)
+    if mode == "split_tiles":      # length-sorted batch: first half U{T/2..T} (one row T),
+        h = B // 2                 # second half U{1..T/4}: whole row tiles finish early
+        l = np.concatenate([rng.integers(T // 2, T + 1, size=h),
+                            rng.integers(1, max(1, T // 4) + 1, size=B - h)])
+        l[0] = T
+        return l.astype(np.int64)
     if mode == "with_zero":        # includes a zero-length row and a full row
         l = rng.integers(0, T + 1, size=B)
         l[0] = 0

@@ -154,6 +154,15 @@ def test_bf16_cfg3_shape():
     assert tr["trip_count"] == [8, 8]
 
 
+@pytest.mark.parametrize("B", [512, 640])
+def test_bf16_dead_tile_skip(B):
+    """A length-sorted batch: the second half of the rows finishes by T/4, so whole 256-row
+    forward / d[x,h] tiles and 128-row backward-EW tiles have no live row in later steps and
+    skip their GEMM / math; B = 640 leaves a ragged last tile. Plain fp64
+    oracle, 2e-2 normwise, control trace bit-exact."""
+    check_parity(12, B, 256, 256, 2, "split_tiles", seed=4, tol=BF16_TOL, precision=cf.BF16)
+
+
 def test_bf16_cfg2_shape():
     """BASELINE.json configs[1] shape on the tcgen05 path."""
     check_parity(100, 64, 512, 512, 1, "uniform", seed=2, tol=BF16_TOL, precision=cf.BF16)
