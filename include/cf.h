@@ -179,6 +179,20 @@ typedef struct {
                                    1: smallest first (fewest bytes per step, for a link that
                                    cannot hide the largest ones)                           */
   int32_t pad_;
+  /* Caller allocator: when dev_alloc is set, every device buffer the
+   * session owns (arenas, rings, stack pool, instance records, queues, scratch) comes from
+   * dev_alloc(bytes, alloc_user) -- 256-byte aligned, or NULL to fail with CF_E_CUDA -- and
+   * goes back through dev_free(ptr, alloc_user) in cf_session_destroy. NULL = cudaMalloc /
+   * cudaFree. The IPC-exported channel block of a multi-GPU session (cf_session_ipc_handle)
+   * is always cudaMalloc'ed: cudaIpcGetMemHandle needs an allocation of its own. */
+  void* (*dev_alloc)(size_t bytes, void* alloc_user);
+  void (*dev_free)(void* ptr, void* alloc_user);
+  void* alloc_user;
+  /* Swap copy streams (a8; "separate streams for GPU-to-CPU and
+   * CPU-to-GPU transfers"): cudaStream_t for the device -> host and host -> device copies of
+   * swapped stack entries; NULL = library-owned non-blocking streams (three each). */
+  void* d2h_stream;
+  void* h2d_stream;
 } cf_run_opts;
 
 /* Control trace -- compared bit-exact with the oracle's. */

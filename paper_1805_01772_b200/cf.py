@@ -50,7 +50,13 @@ class cf_run_opts(C.Structure):
                 ("max_iterations", C.c_int64), ("watchdog_ms", C.c_int64),
                 ("sched_seed", C.c_int32), ("reserved", C.c_int32 * 7),
                 ("stack_budget_bytes", C.c_int64), ("swap_min_bytes", C.c_int64),
-                ("swap_smallest_first", C.c_int32), ("pad_", C.c_int32)]
+                ("swap_smallest_first", C.c_int32), ("pad_", C.c_int32),
+                ("dev_alloc", C.c_void_p), ("dev_free", C.c_void_p), ("alloc_user", C.c_void_p),
+                ("d2h_stream", C.c_void_p), ("h2d_stream", C.c_void_p)]
+
+# caller allocator callbacks (cf_run_opts.dev_alloc / dev_free)
+DEV_ALLOC = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p)
+DEV_FREE = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p)
 
 
 class cf_trace(C.Structure):
@@ -419,7 +425,12 @@ class Session:
                  parallel_iterations: int = 0, device: int = 0, stream=None,
                  max_iterations: int = 0, watchdog_ms: int = 0, num_workers: int = 0,
                  sched_seed: int = 0, profile: bool = False, stack_budget_bytes: int = 0,
-                 swap_min_bytes: int = 0, swap_smallest_first: bool = False):
+                 swap_min_bytes: int = 0, swap_smallest_first: bool = False,
+                 dev_alloc=None, dev_free=None, d2h_stream=None, h2d_stream=None):
+        """dev_alloc(bytes) -> int device pointer and dev_free(ptr) (Python callables, both
+        or neither): the session's device buffers come from the caller's allocator
+        (cf_run_opts.dev_alloc / dev_free). d2h_stream / h2d_stream: cudaStream_t handles for
+        the swap copies (cf_run_opts)."""
         self.g = g
         self.fetches = list(fetches)
         o = cf_run_opts()
@@ -435,6 +446,15 @@ class Session:
         o.stack_budget_bytes = stack_budget_bytes
         o.swap_min_bytes = swap_min_bytes
         o.swap_smallest_first = 1 if swap_smallest_first else 0
+        if (dev_alloc is None) != (dev_free is None):
+            raise ValueError("dev_alloc and dev_free go together")
+        if dev_alloc is not None:   # kept alive with the session: the library calls them
+            self._alloc_cb = DEV_ALLOC(lambda n, _u: int(dev_alloc(int(n))) or None)
+            self._free_cb = DEV_FREE(lambda ptr, _u: dev_free(int(ptr or 0)))
+            o.dev_alloc = C.cast(self._alloc_cb, C.c_void_p)
+            o.dev_free = C.cast(self._free_cb, C.c_void_p)
+        o.d2h_stream = d2h_stream
+        o.h2d_stream = h2d_stream
         arr = (cf_tensor * max(len(fetches), 1))(*[t.c for t in fetches])
         h = _P()
         _check(_lib.cf_session_create(g.h, C.byref(o), len(fetches), arr, C.byref(h)))

@@ -3901,6 +3901,10 @@ struct cf_session {
   // overlaps the previous transfer (round robin)
   static constexpr int kIoStreams = 3;
   cudaStream_t io_d2h[kIoStreams] = {}, io_h2d[kIoStreams] = {};
+  cudaStream_t user_d2h = nullptr, user_h2d = nullptr;   // caller's copy streams (cf_run_opts)
+  void* (*dev_alloc)(size_t, void*) = nullptr;           // caller allocator (cf_run_opts)
+  void (*dev_free)(void*, void*) = nullptr;
+  void* alloc_user = nullptr;
 };
 
 namespace {
@@ -3917,21 +3921,29 @@ int64_t buffer_bytes(const cf_buffer& b) {
   return n;
 }
 
-template <class T>
-T* upload(cf_session* s, const std::vector<T>& v) {
-  size_t bytes = std::max<size_t>(v.size() * sizeof(T), 16);
-  void* p = nullptr;
-  CUDA_OK(cudaMalloc(&p, bytes));
-  s->allocs.push_back(p);
-  if (!v.empty()) CUDA_OK(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
-  return (T*)p;
-}
-
+// every session-owned device buffer: the caller's allocator when one is given (cf_run_opts)
 void* dalloc(cf_session* s, size_t bytes) {
   void* p = nullptr;
-  CUDA_OK(cudaMalloc(&p, std::max<size_t>(bytes, 16)));
+  bytes = std::max<size_t>(bytes, 16);
+  if (s->dev_alloc) {
+    p = s->dev_alloc(bytes, s->alloc_user);
+    if (!p) throw cf::CfError(CF_E_CUDA, "caller allocator returned NULL for " + std::to_string(bytes) + " bytes");
+    if ((uintptr_t)p % 256) {
+      s->dev_free(p, s->alloc_user);
+      throw cf::CfError(CF_E_CUDA, "caller allocator returned a pointer not 256-byte aligned");
+    }
+  } else {
+    CUDA_OK(cudaMalloc(&p, bytes));
+  }
   s->allocs.push_back(p);
   return p;
+}
+
+template <class T>
+T* upload(cf_session* s, const std::vector<T>& v) {
+  void* p = dalloc(s, v.size() * sizeof(T));
+  if (!v.empty()) CUDA_OK(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return (T*)p;
 }
 
 // Host I/O executor (one thread per run of a session with swapped stacks): takes the driver's
@@ -4004,6 +4016,13 @@ void build_session(cf_session* s, const cf::Graph& g, const cf_run_opts* o,
     s->device = o->device;
     if (o->watchdog_ms > 0) s->watchdog_ns = o->watchdog_ms * 1000000LL;
     s->sched_seed = o->sched_seed;
+    if ((o->dev_alloc != nullptr) != (o->dev_free != nullptr))
+      throw cf::CfError(CF_E_UNSUPPORTED, "cf_run_opts: dev_alloc and dev_free go together");
+    s->dev_alloc = o->dev_alloc;
+    s->dev_free = o->dev_free;
+    s->alloc_user = o->alloc_user;
+    s->user_d2h = (cudaStream_t)o->d2h_stream;
+    s->user_h2d = (cudaStream_t)o->h2d_stream;
   }
   if (co.precision != CF_F32 && co.precision != CF_BF16)
     throw cf::CfError(CF_E_DTYPE, "precision must be CF_F32 or CF_BF16");
@@ -4167,8 +4186,10 @@ void build_session(cf_session* s, const cf::Graph& g, const cf_run_opts* o,
     A.io_cq = (int32_t*)dalloc(s, 4 * (size_t)A.io_cap);
     s->zero_each_run.push_back({A.io_cq, 4 * (size_t)A.io_cap});
     for (int k = 0; k < cf_session::kIoStreams; ++k) {
-      CUDA_OK(cudaStreamCreateWithFlags(&s->io_d2h[k], cudaStreamNonBlocking));
-      CUDA_OK(cudaStreamCreateWithFlags(&s->io_h2d[k], cudaStreamNonBlocking));
+      if (s->user_d2h) s->io_d2h[k] = s->user_d2h;   // the caller's streams: not destroyed
+      else CUDA_OK(cudaStreamCreateWithFlags(&s->io_d2h[k], cudaStreamNonBlocking));
+      if (s->user_h2d) s->io_h2d[k] = s->user_h2d;
+      else CUDA_OK(cudaStreamCreateWithFlags(&s->io_h2d[k], cudaStreamNonBlocking));
     }
   }
   A.inst_aux = (int64_t*)dalloc(s, 8 * kDwMax * 6 * (size_t)P.inst_bound);
@@ -4183,6 +4204,8 @@ void build_session(cf_session* s, const cf::Graph& g, const cf_run_opts* o,
   A.st = (RunState*)dalloc(s, sizeof(RunState));
   s->zero_each_run.push_back({A.st, sizeof(RunState)});
   A.toks = (Tok*)dalloc(s, sizeof(Tok) * P.n_vids);
+  s->preset_cap = (int)std::max<size_t>(P.feeds.size(), 1);
+  s->d_preset = (PresetTok*)dalloc(s, sizeof(PresetTok) * s->preset_cap);
   s->zero_each_run.push_back({A.toks, sizeof(Tok) * P.n_vids});
   A.stack_pool = (Tok*)dalloc(s, sizeof(Tok) * std::max(P.stack_pool, 1));
   A.stack_depth = (int32_t*)dalloc(s, 4 * std::max<size_t>(P.stack_depths, 1));
@@ -4386,11 +4409,8 @@ cf_status cf_run(cf_session* s, int32_t n_feed, const char* const* feed_names,
       CUDA_OK(cudaMallocHost((void**)&s->stage_host, total * 2));
       s->stage_cap = total * 2;
     }
-    if ((int)preset.size() > s->preset_cap) {
-      if (s->d_preset) cudaFree(s->d_preset);
-      s->d_preset = nullptr;
-      s->preset_cap = 0;
-      CUDA_OK(cudaMalloc((void**)&s->d_preset, sizeof(PresetTok) * preset.size()));
+    if ((int)preset.size() > s->preset_cap) {   // one token per placeholder (sized at creation)
+      s->d_preset = (PresetTok*)dalloc(s, sizeof(PresetTok) * preset.size());
       s->preset_cap = (int)preset.size();
     }
     uint8_t* sh = s->stage_host;
@@ -4660,14 +4680,16 @@ int32_t cf_debug_session_profile(const cf_session* s, unsigned long long* out, i
 
 void cf_session_destroy(cf_session* s) {
   if (!s) return;
-  for (void* p : s->allocs) cudaFree(p);
+  for (void* p : s->allocs) {
+    if (s->dev_free) s->dev_free(p, s->alloc_user);
+    else cudaFree(p);
+  }
   for (auto& [r, p] : s->peer_mem) cudaIpcCloseMemHandle(p);
   for (void* h : s->host_allocs) cudaFreeHost(h);
   if (s->stage_host) cudaFreeHost(s->stage_host);
-  if (s->d_preset) cudaFree(s->d_preset);
   for (int k = 0; k < cf_session::kIoStreams; ++k) {
-    if (s->io_d2h[k]) cudaStreamDestroy(s->io_d2h[k]);
-    if (s->io_h2d[k]) cudaStreamDestroy(s->io_h2d[k]);
+    if (s->io_d2h[k] && s->io_d2h[k] != s->user_d2h) cudaStreamDestroy(s->io_d2h[k]);
+    if (s->io_h2d[k] && s->io_h2d[k] != s->user_h2d) cudaStreamDestroy(s->io_h2d[k]);
   }
   if (s->chan_mem) cudaFree(s->chan_mem);
   if (s->ev0) cudaEventDestroy(s->ev0);
