@@ -832,6 +832,14 @@ struct Wave {
   int bpc, bcount, bfail;
   int bid[32][4];         // per member: main (fwd) / EW (bwd), DXH (bwd), dW flush, weight prep
   int bnid[32];           // per member: graph node id
+  // profiling build: batch phase clocks (issue by the driver, lane 0's start / phase A end,
+  // the slowest lane's end)
+  long long bt_issue, bt_start, bt_a, bt_chk, bt_res, bt_built;
+  unsigned long long bt_end;
+  // job 3 (the whole batch on the lanes): id base, the frame's body offset, and what the
+  // lanes hand back (ids used, tiles, dead members, queue tails touched, last dW chunk)
+  int bbase, bfoff;
+  int bids, btiles, bdead, bdirty, blast;
 };
 
 __device__ void wave_work(Wave& w, int start, int n, int h, int nh) {
@@ -1305,11 +1313,15 @@ struct Driver {
     }
     int32_t id = ninst++;
     const int sl = id & kRingMask;
-    while (r_id[sl] != -1) {   // ring full: wait for the oldest in-flight instance
-      const unsigned long long now = globaltimer();
-      if (drain()) last_progress = now;
-      else if ((long long)(now - last_progress) > A.watchdog_ns) fail(CF_E_DEADLOCK, -700);
-      if (st->error) return -1;
+    if (r_id[sl] != -1) {   // ring full: wait for the oldest in-flight instance
+      const long long rf0 = (kProfBuild && A.prof) ? clock64() : 0;
+      while (r_id[sl] != -1) {
+        const unsigned long long now = globaltimer();
+        if (drain()) last_progress = now;
+        else if ((long long)(now - last_progress) > A.watchdog_ns) fail(CF_E_DEADLOCK, -700);
+        if (st->error) return -1;
+      }
+      if (kProfBuild && A.prof) { op_cyc[27] += clock64() - rf0; op_cnt[27]++; }   // RING_FULL
     }
     ntiles = max(ntiles, 1);
     r_id[sl] = id;
@@ -1907,8 +1919,63 @@ struct Driver {
   // path one by one (a context or a scalar not known yet, a dead member, a pending wave job).
   __noinline__ __device__ int run_batch(const DFrame& F, int pc, int n) {
     Region rg(this, 32 + 23);
+    const long long bt_enter = (kProfBuild && A.prof) ? clock64() : 0;
     if (pend_wave_pc_ >= 0 || P.precision != D_BF16 || P.n_swaps || (dbg_ & (1 << 30))) return 1;
     Wave& w = *wave_;
+    if (!(dbg_ & (1 << 28)) && n <= 32) {
+      // the whole batch on helper warp 1, lane m = member m (job 3, batch_lane_par): liveness,
+      // id reservation, placements and tokens, records and edges, submission. The driver thread
+      // only makes sure every member's cond context is known, waits, and adds the totals.
+      // (Debug flag bit 28: the serial path below, A/B.)
+      for (int m = 0; m < n; ++m) {
+        const int c = bn_[pc + 1 + m].ctx;
+        if (c && !(lstamp_[c] == lgen_ && lval_[c] >= 0) && ctx_live(c) < 0) return 1;
+      }
+      w.job = 3;
+      w.bpc = pc + 1;
+      w.bcount = n;
+      w.bfail = 0;
+      w.chain = 0;
+      w.done = 0;
+      w.bbase = ninst;
+      w.bfoff = F.body_off;
+      w.bids = w.btiles = w.bdead = w.bdirty = 0;
+      w.blast = -1;
+      if (kProfBuild && A.prof) {
+        w.bt_end = 0;
+        w.bt_issue = clock64();
+      }
+      __threadfence_block();
+      *(volatile int*)&w.seq = w.seq + 1;
+      flush_publish();
+      while (*(volatile int*)&w.done < kWaveWarps) {
+      }
+      __threadfence_block();
+      w.job = 0;
+      if (kProfBuild && A.prof) {   // lane-0 clocks: wake, checks, reserve, placements,
+        const long long now = clock64();   // records + edges (slowest lane), submit + tail
+        op_cyc[28] += w.bt_start - w.bt_issue; op_cyc[29] += w.bt_chk - w.bt_start;
+        op_cyc[30] += w.bt_res - w.bt_chk;
+        op_cyc[32 + 25] += w.bt_a - w.bt_res;
+        op_cyc[32 + 26] += (long long)w.bt_end - w.bt_a;
+        op_cyc[32 + 27] += now - (long long)w.bt_end;
+        op_cnt[28]++; op_cnt[29]++; op_cnt[30]++;
+        op_cnt[32 + 25]++; op_cnt[32 + 26]++; op_cnt[32 + 27]++;
+      }
+      if (w.bfail != 2) {   // 2: a member needs the general path; nothing was changed
+        ninst += w.bids;
+        outstanding += w.bids;
+        n_inst += w.bids;
+        n_tiles += w.btiles;
+        n_dead += w.bdead;
+        if (cur_frame >= 0) iter_out_[frame_ib(cur_frame) + iter] += w.bids;
+        if (w.blast >= 0) last_dw = w.blast;
+        dirty_ |= w.bdirty;
+        flush_publish();
+        if (w.bfail && !st->error) fail(CF_E_UNSUPPORTED, -600);
+        return n + 1;
+      }
+    }
     // liveness: contexts first (no state is changed before every member is known)
     unsigned live = 0;
     for (int m = 0; m < n; ++m) {
@@ -1929,6 +1996,7 @@ struct Driver {
       if ((d.aux[1] & 1) && in_tok(d, 5).kind != TK_IMM) return 1;
       live |= 1u << m;
     }
+    const long long bt_live = (kProfBuild && A.prof) ? clock64() : 0;
     // reserve the ids (ring slots: may drain completions, so before the helpers start)
     const bool m2rows = bn_[pc + 1].imm[0] >= kM2MinRows;
     int32_t last_flush = -1;
@@ -1978,12 +2046,23 @@ struct Driver {
     w.bfail = 0;
     w.chain = 0;
     w.done = 0;
+    if (kProfBuild && A.prof) {
+      w.bt_end = 0;
+      w.bt_issue = clock64();
+    }
     __threadfence_block();
     *(volatile int*)&w.seq = w.seq + 1;
     flush_publish();
     while (*(volatile int*)&w.done < kWaveWarps) {
     }
     __threadfence_block();
+    if (kProfBuild && A.prof) {   // B_PHASE_A, B_BUILD (slowest lane; wake-up + tail < 1 us)
+      op_cyc[32 + 25] += w.bt_a - w.bt_issue;
+      op_cyc[32 + 26] += (long long)w.bt_end - w.bt_a;
+      op_cyc[32 + 24] += w.bt_issue - bt_live; op_cyc[32 + 27] += bt_live - bt_enter;
+      for (int k = 24; k < 28; ++k) op_cnt[32 + k]++;
+    }
+    const long long bt_post = (kProfBuild && A.prof) ? clock64() : 0;
     w.job = 0;
     if (w.bfail && !st->error) fail(CF_E_UNSUPPORTED, -600);
     if (last_flush >= 0) last_dw = last_flush;
@@ -1998,11 +2077,13 @@ struct Driver {
       if (!fwd && id[1] >= 0) submit(id[1]);
     }
     flush_publish();
+    if (kProfBuild && A.prof) { op_cyc[32 + 28] += clock64() - bt_post; op_cnt[32 + 28]++; }
     return n + 1;
   }
 
   // helper lane m of warp 1: member m of the batch dispatched by run_batch
   __device__ void batch_lane(Wave& w, int m) {
+    if (kProfBuild && A.prof && m == 0 && w.job == 2) w.bt_start = clock64();
     const bool mine = m < w.bcount && w.bid[m][0] >= 0;
     const DNode* dp = mine ? &bn_[w.bpc + m] : nullptr;
     int64_t outp[8];
@@ -2032,9 +2113,147 @@ struct Driver {
       }
     }
     __syncwarp();
+    if (kProfBuild && A.prof && m == 0) w.bt_a = clock64();
     // phase B: operand lookups, records, dependency edges
     if (mine && ok) ok = batch_build(*dp, w.bnid[m], w.bid[m], outp);
     if (mine && !ok) atomicOr(&w.bfail, 1);
+    if (kProfBuild && A.prof) atomicMax(&w.bt_end, (unsigned long long)clock64());
+    __syncwarp();
+  }
+
+  // job 3: lane m of helper warp 1 runs member m of the batch end to end. Nothing is changed
+  // until every lane has checked its member (a dead input, a control token or a time step not
+  // known yet, or an occupied ring slot hands the whole batch back to the driver: bfail = 2).
+  // While the lanes run, the driver thread only waits: no completion is processed, so the
+  // dependency edges (shared-memory atomics) and the submissions cannot race with one.
+  __device__ void batch_lane_par(Wave& w, int m) {
+    const unsigned full = 0xffffffffu;
+    if (kProfBuild && A.prof && m == 0) w.bt_start = clock64();
+    const int n = w.bcount;
+    const bool in = m < n;
+    const DNode* dp = in ? &bn_[w.bpc + m] : nullptr;
+    // ---- checks (read only)
+    int live = 0, bad = 0, nid = -1, cnt = 0;
+    bool fwd = false, prep = false, xp = false, flush = false;
+    if (in) {
+      const DNode& d = *dp;
+      live = d.ctx ? lval_[d.ctx] : 1;
+      if (live) {
+        const unsigned inb = (unsigned)d.aux[6];
+        for (int j = 0; j < d.n_in; ++j)
+          if (!(inb >> j & 1) && in_tok(d, j).dead) bad = 1;
+        for (int j = 0; j < d.n_ctrl; ++j)
+          if (toks_[iv_[d.ctrl_off + j]].dead) bad = 1;
+        if ((d.aux[1] & 1) && in_tok(d, 5).kind != TK_IMM) bad = 1;
+        nid = ((const int16_t*)d.pad)[5] >= 0 ? ((const int16_t*)d.pad)[5] : P.order[w.bfoff + w.bpc + m];
+        fwd = d.aux[0] == HK_LSTM_FWD;
+        prep = prep_inst_[prep_slot(d, nid)] < 0;
+        if (fwd) {
+          xp = d.aux[1] & 4;
+        } else {
+          const int acc_w = d.aux[3], acc_b = d.aux[4];
+          flush = !(acc_w >= 0 && acc_b >= 0) || dw_count_[nid] + 1 >= dw_chunk();
+        }
+        cnt = 1 + (prep ? 1 : 0) + (fwd ? (xp ? 1 : 0) : 1 + (flush ? 1 : 0));
+      }
+    }
+    // ids: consecutive per member, members in order (the serial path's numbering)
+    int off = cnt;
+#pragma unroll
+    for (int k = 1; k < 32; k <<= 1) {
+      const int v = __shfl_up_sync(full, off, k);
+      if (m >= k) off += v;
+    }
+    const int total = __shfl_sync(full, off, 31);
+    if (kProfBuild && A.prof && m == 0) w.bt_chk = clock64();
+    off -= cnt;
+    int first = w.bbase + off;
+    for (int k = 0; k < cnt; ++k)
+      if (r_id[(first + k) & kRingMask] != -1 || first + k >= A.inst_cap) bad = 1;
+    if (__any_sync(full, bad)) {
+      if (m == 0) w.bfail = 2;
+      __syncwarp();
+      return;
+    }
+    // ---- reserve (the serial path's order: weight prep, dW chunk / x-projection, main)
+    int* id = in ? w.bid[m] : nullptr;
+    int tiles = 0;
+    if (in) {
+      id[0] = id[1] = id[2] = id[3] = -1;
+      if (!live) {
+        atomicAdd(&w.bdead, 1);
+      } else {
+        const DNode& d = *dp;
+        w.bnid[m] = nid;
+        const int64_t B = d.imm[0], In = d.imm[1], H = d.imm[2], KT = In + H;
+        const bool m2 = B >= kM2MinRows;
+        auto take = [&](int kind, int nt) {
+          const int32_t x = first++;
+          const int sl = x & kRingMask;
+          nt = max(nt, 1);
+          r_id[sl] = x;
+          r_pend[sl] = 0;
+          r_succ[sl] = -1;
+          r_last[sl] = -1;
+          r_sn[sl] = 0;
+          r_nt[sl] = nt;
+          r_kfi[sl] = (int)((unsigned)(kind & 127) | ((unsigned)((cur_frame + 1) & 255) << 8) |
+                            ((unsigned)min(cur_frame >= 0 ? iter : 0, 0xFFFF) << 16));
+          tiles += nt;
+          return x;
+        };
+        if (fwd) {
+          if (prep) {
+            id[3] = take(HK_PREP_WP, (int)((4 * H + 15) / 16));
+            prep_inst_[prep_slot(d, nid)] = id[3];
+          }
+          const int nt = (int)((m2 ? (B + 255) / 256 : (B + 127) / 128) * (H / 64));
+          if (xp) id[1] = take(HK_LSTM_XPROJ_TC, nt);
+          id[0] = take(HK_LSTM_FWD_TC, nt);
+        } else {
+          if (prep) {
+            id[3] = take(HK_PREP_WT, (int)((KT / 64) * (4 * H / 128)));
+            prep_inst_[prep_slot(d, nid)] = id[3];
+          }
+          if (flush) {
+            id[2] = take(HK_LSTM_DW_TC, (int)((4 * H / 256) * (KT / 256) + (4 * H + 255) / 256));
+            atomicMax(&w.blast, id[2]);
+          }
+          id[0] = take(HK_LSTM_BWD_EW_BF, (int)(((B + 127) / 128) * ((H + kEwUnits - 1) / kEwUnits)));
+          id[1] = take(HK_LSTM_DXH_TC, (int)((m2 ? (B + 255) / 256 : (B + 127) / 128) *
+                                              (m2 ? KT / kDxhN2 : KT / 256)));
+        }
+      }
+    }
+    if (m == 0) {
+      w.bids = total;
+      w.bcount = n;
+    }
+    __syncwarp();
+    if (kProfBuild && A.prof && m == 0) w.bt_res = clock64();
+    // ---- placements, tokens, records, edges (the job-2 lanes' code)
+    batch_lane(w, m);
+    if (kProfBuild && A.prof && m == 0) w.bt_built = clock64();
+    // ---- submit (every member's edges exist: each lane adds only its own instances' edges)
+    if (in && live) {
+      int dirty = 0;
+      auto sub = [&](int x) {
+        if (x < 0 || r_pend[x & kRingMask] != 0) return;
+        const int sl = x & kRingMask;
+        const bool low = (r_kfi[sl] & 255) == HK_LSTM_DW_TC;
+        if (kProfBuild && A.prof) A.prof[6 * (int64_t)x + 1] = globaltimer();
+        const unsigned long long t = atomicAdd(low ? &lq_tail : &q_tail, 1ULL);
+        (low ? A.lq : A.queue)[t & (A.q_cap - 1)] = (unsigned long long)x;
+        dirty |= low ? 2 : 1;
+      };
+      sub(id[3]);
+      sub(id[2]);
+      if (fwd) sub(id[1]);
+      sub(id[0]);
+      if (!fwd) sub(id[1]);
+      if (dirty) atomicOr(&w.bdirty, dirty);
+      atomicAdd(&w.btiles, tiles);
+    }
     __syncwarp();
   }
 
@@ -2066,11 +2285,14 @@ struct Driver {
         Q.p[13] = outp[4];
         add_dep_atomic(id[3], in_tok(d, 3).writer);
       }
+      const bool pl0 = kProfBuild && A.prof && (threadIdx.x & 31) == 0;
+      long long c0 = pl0 ? clock64() : 0;
       int64_t mx, sx, mh, sh, mw, sw;
       if (!resolve_core(ip(0), (int)B, (int)In, 0, &mx, &sx, hint + 0) ||
           !resolve_core(ip(1), (int)B, (int)H, 0, &mh, &sh, hint + 1) ||
           !resolve_core(outp[4], (int)(4 * H), (int)KT, 1, &mw, &sw, hint + 2))
         return false;
+      long long c1 = pl0 ? clock64() : 0;
       const int ntiles = (int)((m2 ? (B + 255) / 256 : (B + 127) / 128) * (H / 64));
       const bool split = id[1] >= 0;
       if (split) {   // x-projection ahead of the recurrence (HK_LSTM_XPROJ_TC)
@@ -2091,10 +2313,16 @@ struct Driver {
       I.p[7] = split ? outp[5] : 0;
       for (int q = 0; q < 4; ++q) I.p[8 + q] = outp[q];
       I.s[0] = t; I.s[1] = d.aux[2]; I.s[2] = sx; I.s[3] = sh;
+      long long c2 = pl0 ? clock64() : 0;
       for (int j = 0; j < d.n_in; ++j)
         if (!(split && j == 0)) dep(id[0], in_tok(d, j).writer);   // x: through the projection
       dep(id[0], pw);
       if (split) dep(id[0], id[1]);
+      if (pl0) {   // B_F_RECORD (lookups + record), B_F_DEPS (lane 0 of the batch)
+        const long long c3 = clock64();
+        op_cyc[32 + 29] += c2 - c0; op_cyc[63] += c3 - c2;
+        op_cnt[32 + 29]++; op_cnt[63]++;
+      }
       return true;
     }
     // backward: EW (dz, dc, db partials) -> DXH (dx, dh); dW / db chunked over 8 steps
@@ -3796,6 +4024,8 @@ __global__ void __launch_bounds__(kThreads, 1) cf_driver_kernel(RunArgs A_param)
             ((Driver*)drv_obj)->heavy_prep_lane(wave, wave_lane(threadIdx.x));
           } else if (wave.job == 2) {
             if ((threadIdx.x >> 5) == 1) ((Driver*)drv_obj)->batch_lane(wave, threadIdx.x & 31);
+          } else if (wave.job == 3) {
+            if ((threadIdx.x >> 5) == 1) ((Driver*)drv_obj)->batch_lane_par(wave, threadIdx.x & 31);
           } else {
             // fused levels: each reads the previous one's tokens (named barrier between)
             const int hl = wave_lane(threadIdx.x);

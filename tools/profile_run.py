@@ -26,12 +26,13 @@ OPS = ["NOP", "PLACEHOLDER", "CONST", "PASS", "SWITCH", "MERGE", "MERGE_LOOP", "
        "NEXTITER", "SCALAR", "REDUCE_I", "SLICE_I", "FLOW", "TA_CREATE", "TA_READ", "TA_WRITE",
        "TA_STACK", "TA_UNSTACK", "TA_GRAD", "STACK_CREATE", "STACK_PUSH", "STACK_POP", "HEAVY", "ACC",
        "SEND", "RECV"]
-OPS = OPS + ["?%d" % k for k in range(len(OPS), 31)] + ["SMEM_MASK"]
+OPS = OPS + ["RING_FULL_WAIT", "BL_WAKE", "BL_CHECK", "BL_RESERVE"] + ["SMEM_MASK"]
 OPS += ["R_RUN_BODY", "R_NEW_INST", "R_PUBLISH", "R_RESOLVE", "R_DRAIN", "R_ADD_DEP", "R_PLACE",
         "R_PREP", "R_FLUSH_DW", "R_EVAL_LSTM_TC", "R_EVAL_HEAVY", "R_DRAIN_IO", "R_COMPLETE",
         "R_WAVE", "F_PREP_RESOLVE", "F_NEW_INST", "F_FIELDS", "F_ADD_DEPS", "F_OUT_SUBMIT",
-        "H_PLACES", "W_WAIT", "W_WAIT_DRAIN", "W_HELPER_BUSY(n=leftovers)", "R_BATCH"]
-OPS = OPS + ["?%d" % k for k in range(len(OPS), 62)] + ["R_SWITCH_FAST", "?63"]
+        "H_PLACES", "W_WAIT", "W_WAIT_DRAIN", "W_HELPER_BUSY(n=leftovers)", "R_BATCH",
+        "B_DRV_RESERVE", "BL_PLACE", "BL_BUILD", "BL_SUBMIT_TAIL", "B_DRV_SUBMIT", "B_F_RECORD"]
+OPS = OPS + ["?%d" % k for k in range(len(OPS), 62)] + ["R_SWITCH_FAST", "B_F_DEPS"]
 
 
 def main():
@@ -44,6 +45,7 @@ def main():
     ap.add_argument("--swap-smallest-first", action="store_true")
     ap.add_argument("--out", default="gpurun_out/profile.json")
     ap.add_argument("--no-tiles", action="store_true", help="workers skip tile bodies (driver alone)")
+    ap.add_argument("--fwd-only", action="store_true", help="the forward loop alone (no gradients)")
     a = ap.parse_args()
     c = dict(CONFIGS[a.config])
     if a.T:
@@ -51,7 +53,7 @@ def main():
     prec = cf.BF16 if a.precision == "bf16" else cf.F32
     if a.no_tiles:
         cf.debug_set_flags(1)
-    p = dynamic_rnn_lstm(c["T"], c["B"], c["I"], c["H"], c["L"])
+    p = dynamic_rnn_lstm(c["T"], c["B"], c["I"], c["H"], c["L"], with_grads=not a.fwd_only)
     s = cf.Session(p.g, p.fetch_tensors(), precision=prec, parallel_iterations=a.K, profile=True,
                    stack_budget_bytes=a.stack_budget, swap_smallest_first=a.swap_smallest_first)
     f = rnn_inputs(c["T"], c["B"], c["I"], c["H"], c["L"], seed=0, len_mode=c["len_mode"], bf16=prec == cf.BF16)
