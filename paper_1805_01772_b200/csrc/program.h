@@ -310,6 +310,7 @@ struct RunArgs {
   Prog prog;
   RunState* st;
   Tok* toks;                 // [n_vids]
+  int32_t* wait_ovf;         // [4096] channel waits published while the driver's table is full
   const PresetTok* preset;   // [n_preset] this run's placeholder tokens (one upload per run)
   int32_t n_preset;
   int32_t pad_preset;

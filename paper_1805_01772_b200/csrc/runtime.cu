@@ -899,6 +899,18 @@ struct Driver {
   };
   ChanWait waits_[kMaxWaits];
   int n_waits_ = 0;
+  // waits published while the table is full (many Recvs in flight: K iterations x peers)
+  static constexpr int kWaitOvf = 4096;
+  int ovf_head_ = 0, ovf_tail_ = 0;
+  __device__ void add_wait(int32_t id) {
+    const Inst& I = A.insts[id];
+    ChanWait& w = waits_[n_waits_++];
+    w.flag = (unsigned long long*)I.p[0];
+    w.want = (unsigned long long)I.s[0];
+    w.ack = (unsigned long long*)I.p[1];
+    w.ackv = (unsigned long long)I.s[1];
+    w.id = id;
+  }
   // swap I/O (a8)
   unsigned long long io_tail = 0, io_head = 0;
   int io_out = 0;   // swap requests not yet completed
@@ -1409,17 +1421,15 @@ struct Driver {
   __noinline__ __device__ void publish(int32_t id) {
     const int sl = id & kRingMask;
     if ((r_kfi[sl] & 255) == HK_WAIT) {   // polled by drain() until the flag arrives
-      const Inst& I = A.insts[id];
-      if (n_waits_ == kMaxWaits) {
-        fail(CF_E_UNSUPPORTED, -400);
+      if (n_waits_ == kMaxWaits) {   // table full: queued in order, moved in as waits complete
+        if (ovf_tail_ - ovf_head_ >= kWaitOvf) {
+          fail(CF_E_UNSUPPORTED, -400);
+          return;
+        }
+        A.wait_ovf[ovf_tail_++ & (kWaitOvf - 1)] = id;
         return;
       }
-      ChanWait& w = waits_[n_waits_++];
-      w.flag = (unsigned long long*)I.p[0];
-      w.want = (unsigned long long)I.s[0];
-      w.ack = (unsigned long long*)I.p[1];
-      w.ackv = (unsigned long long)I.s[1];
-      w.id = id;
+      add_wait(id);
       return;
     }
     if ((r_kfi[sl] & 255) == HK_SWAP) {   // to the host I/O thread's copy streams
@@ -1550,6 +1560,7 @@ struct Driver {
       complete(id);
       any = true;
     }
+    while (n_waits_ < kMaxWaits && ovf_head_ < ovf_tail_) add_wait(A.wait_ovf[ovf_head_++ & (kWaitOvf - 1)]);
     // relaxed poll (an acquire load would invalidate L1 at every poll); the release store
     // that publishes successors orders this observation before them (fence.acq_rel).
     // (A helper warp mirroring this queue into shared memory measured 5% slower.)
@@ -4434,6 +4445,7 @@ void build_session(cf_session* s, const cf::Graph& g, const cf_run_opts* o,
   A.st = (RunState*)dalloc(s, sizeof(RunState));
   s->zero_each_run.push_back({A.st, sizeof(RunState)});
   A.toks = (Tok*)dalloc(s, sizeof(Tok) * P.n_vids);
+  A.wait_ovf = (int32_t*)dalloc(s, 4 * Driver::kWaitOvf);
   s->preset_cap = (int)std::max<size_t>(P.feeds.size(), 1);
   s->d_preset = (PresetTok*)dalloc(s, sizeof(PresetTok) * s->preset_cap);
   s->zero_each_run.push_back({A.toks, sizeof(Tok) * P.n_vids});
