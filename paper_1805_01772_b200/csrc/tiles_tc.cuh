@@ -445,7 +445,9 @@ __device__ __forceinline__ void ew_cell4(const float* ig, const float* fg, const
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const float cn = fg[k] * cpa[k] + ig[k] * gg[k];
-    const float tc_ = tanhf(cn);
+    // tanh of the recomputed cell state with the same one-MUFU approximation the forward
+    // epilogue used for h (libm tanhf is ~20 instructions; the EW tile issues ~0.8 IPC)
+    const float tc_ = (kDbgFlagsTC & (1 << 23)) ? tanhf(cn) : tanhf_(cn);
     const float dh = dna[k] + dov[k];
     const float dcs = dh * og[k] * (1.0f - tc_ * tc_) + dca[k];
     zf[0][k] = dcs * gg[k] * ig[k] * (1.0f - ig[k]);
