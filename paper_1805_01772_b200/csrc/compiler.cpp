@@ -151,6 +151,10 @@ struct Compiler {
           for (int p : {0, 2, 3}) want[find(vbase[i] + p)] = 1;
         } else if (n.op == "LSTMCellGrad") {
           for (int j : {0, 1, 4}) want[find(vid(n.in[j]))] = 1;
+        } else if (n.op == "MatMul" && std::getenv("CF_NO_TC_MATMUL") == nullptr) {
+          // generic GEMM operands (the MoE-style experts and their gradients) stored in bf16:
+          // TMA operands of the tcgen05 GEMM (runtime.cu HK_MATMUL_TC); fp32 accumulation
+          for (int j : {0, 1}) want[find(vid(n.in[j]))] = 1;
         }
       }
     }

@@ -86,6 +86,7 @@ enum HeavyKind : int32_t {
   HK_SWAP,          // stack swap copy on the host I/O thread's copy stream (sub 0: D2H, 1: H2D)
   HK_WAIT,          // no tiles: completes when a channel flag shows the expected message (a14)
   HK_LSTM_XPROJ_TC, // tcgen05 x-projection of a cell: Zx = x Wx^T (fp32), ahead of the recurrence
+  HK_MATMUL_TC,     // tcgen05 generic GEMM of registered bf16 operands (sub bit0 ta, bit1 tb)
   HK__COUNT
 };
 

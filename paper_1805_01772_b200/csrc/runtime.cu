@@ -1677,6 +1677,21 @@ struct Driver {
     if (!resolve_core(p, rows, cols, kind, &r.map, &r.slot, hint)) r.map = 0;
     return r;
   }
+  // registry lookup that may miss (the generic GEMM then takes the SIMT tile)
+  __noinline__ __device__ bool resolve_try(int64_t p, int rows, int cols, int kind, int64_t* map, int64_t* slot,
+                                           int16_t* hint) {
+    int lo = 0, hi = P.n_reg - 1, at = -1;
+    while (lo <= hi) {
+      const int mid = (lo + hi) >> 1;
+      if (reg_[mid].base <= p) { at = mid; lo = mid + 1; } else hi = mid - 1;
+    }
+    for (int i = at; i >= 0 && reg_[i].base == reg_[at].base; --i)
+      if (reg_match(i, p, rows, cols, kind, map, slot)) {
+        *hint = (int16_t)i;
+        return true;
+      }
+    return false;
+  }
   __forceinline__ __device__ bool resolve_core(int64_t p, int rows, int cols, int kind, int64_t* map, int64_t* slot,
                                                int16_t* hint) {
     const int h = *hint;
@@ -2615,6 +2630,22 @@ struct Driver {
       }
       case HK_MATMUL: {
         int64_t M = d.imm[0], N = d.imm[1], K = d.imm[2];
+        const bool ta = d.aux[1] & 1, tb = d.aux[1] & 2;
+        int64_t ma, sa, mb, sb;
+        int16_t hint_a = -1, hint_b = -1;
+        // the tensor-core GEMM when both operands are registered bf16 buffers (TMA operands)
+        if (tcm && N % 256 == 0 && K % 64 == 0 && !(kDbgFlags & (1 << 1)) &&
+            in_tok(d, 0).dt == D_BF16 && in_tok(d, 1).dt == D_BF16 &&
+            resolve_try(ip(0), (int)(ta ? K : M), (int)(ta ? M : K), ta ? 2 : 0, &ma, &sa, &hint_a) &&
+            resolve_try(ip(1), (int)(tb ? N : K), (int)(tb ? K : N), tb ? 1 : 2, &mb, &sb, &hint_b)) {
+          id = new_inst(HK_MATMUL_TC, d.aux[1], (int)(((M + 127) / 128) * (N / 256)));
+          if (id < 0) return EV_ERROR;
+          Inst& I = A.insts[id];
+          I.m = M; I.n = N; I.k = K;
+          I.p[0] = ma; I.p[1] = mb; I.p[13] = outp[0];
+          I.s[0] = sa; I.s[1] = sb; I.s[2] = odt;
+          break;
+        }
         id = new_inst(HK_MATMUL, d.aux[1], (int)(((M + 63) / 64) * ((N + 63) / 64)));
         if (id < 0) return EV_ERROR;
         Inst& I = A.insts[id];
@@ -3844,6 +3875,7 @@ __device__ void worker_loop(const RunArgs& A) {
       case HK_LSTM_BWD_EW_BF: tile_lstm_bwd_ew_bf(I, tile, sm); break;
       case HK_LSTM_DXH_TC: tile_lstm_dxh_tc(I, tile, ts, tc_cnt, tc_cnt2, tc_tiles, claim_ahead); break;
       case HK_LSTM_DW_TC: tile_lstm_dw_tc(I, tile, ts, tc_cnt, tc_cnt2, tc_tiles, claim_ahead); break;
+      case HK_MATMUL_TC: tile_matmul_tc(I, tile, ts, tc_cnt, tc_tiles, claim_ahead); break;
       default: break;
     }
     // epilogue stores (generic proxy) must be visible to later TMA (async proxy) reads, and a

@@ -599,6 +599,58 @@ __device__ void tile_lstm_bwd_ew_bf(const Inst& I, int tile, float* sm) {
   phase_add(3, ph0, ph0);
 }
 
+// ---------------------------------------------------------------- generic GEMM (MatMul)
+// C[M][N] = op(A) op(B) for bf16 operands in the TMA operand registry (the MoE-style experts
+// and their gradients, cfg5): 128 x 256 tiles on the tcgen05 engine, fp32 accumulation.
+// A stored [M][K] (K-major) or, transposed, [K][M] (MN-major); B stored [K][N] (MN-major) or,
+// transposed, [N][K] (K-major). p: 0 A map, 1 B map, 13 C; s: 0 A slot, 1 B slot, 2 C dtype;
+// sub: bit 0 ta, bit 1 tb
+template <class Hook>
+__device__ void tile_matmul_tc(const Inst& I, int tile, tc::TcShared& ts, uint32_t& cnt,
+                               uint32_t& ntile, Hook hook) {
+  const int M = (int)I.m, N = (int)I.n, K = (int)I.k;
+  const bool ta = I.sub & 1, tb = I.sub & 2;
+  const int tn = N / 256;
+  const int mt = tile / tn, nt = tile % tn;
+  const int m0 = mt * tc::BM, n0 = nt * 256;
+  const CUtensorMap* ma = (const CUtensorMap*)I.p[0];
+  const CUtensorMap* mb = (const CUtensorMap*)I.p[1];
+  const int sa = (int)I.s[0], sb = (int)I.s[1];
+  auto plan_a = [&](int kb, tc::Box* b) {
+    if (!ta) {
+      b[0] = {ma, kb * 64, m0, sa, 0};
+      return 1;
+    }
+    for (int j = 0; j < 2; ++j) b[j] = {ma, m0 + 64 * j, kb * 64, sa, j * 8192};
+    return 2;
+  };
+  auto plan_b = [&](int kb, tc::Box* b) {
+    if (tb) {
+      b[0] = {mb, kb * 64, n0, sb, 0};
+      return 1;
+    }
+    for (int j = 0; j < 4; ++j) b[j] = {mb, n0 + 64 * j, kb * 64, sb, j * 8192};
+    return 4;
+  };
+  tc::tc_tile(ts, K / 64, 256, ta ? 1 : 0, tb ? 0 : 1, cnt, ntile, plan_a, plan_b, hook);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int r = m0 + 32 * (warp % 4) + lane;
+  const bool cbf = (int)I.s[2] == D_BF16;
+  for (int c = (warp / 4) * 128; c < (warp / 4) * 128 + 128; c += 16) {
+    float v[16];
+    tc::tc_acc16(ts, c, v);
+    if (r >= M) continue;
+    const int64_t o = (int64_t)r * N + n0 + c;
+    if (cbf) {
+      store_bf16x16((__nv_bfloat16*)I.p[13] + o, v);
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) ((float4*)((float*)I.p[13] + o))[q] = *(float4*)&v[4 * q];
+    }
+  }
+  tc::tc_tile_end();
+}
+
 // ---------------------------------------------------------------- backward d[x,h]
 // p: 0 dz-map (KA), 1 WT-map (KB; the KA map of the same buffer is the one before it),
 //    5 lens, 6 dh_next(f32), 11 dx(f32), 12 dh(f32); s: 0 t, 2 dz slot

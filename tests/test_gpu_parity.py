@@ -179,6 +179,14 @@ def test_bf16_parallel_iterations_bit_identical(K):
     assert max(tr["max_inflight"]) <= K
 
 
+def test_bf16_moe_tensor_core_experts():
+    """The expert GEMMs and their gradients on the tcgen05 generic GEMM (HK_MATMUL_TC): B = 128,
+    H = 512 (two 256-column tiles, K = 512), the forward o·W, dO = dE·Wᵀ (K-major B) and
+    dW = oᵀ·dE (MN-major A and B) all take it. Plain fp64 oracle, bf16 bar."""
+    check_parity(5, 128, 256, 512, 2, "uniform", seed=9, tol=BF16_TOL, precision=cf.BF16,
+                 moe=True, moe_act="tanh")
+
+
 @pytest.mark.parametrize("K", [1, 8, 32])
 def test_bf16_moe_parallel_iterations_sweep(K):
     """BASELINE.json configs[4] in small: parallel_iterations in {1, 8, 32}, a nested MoE-style

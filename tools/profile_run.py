@@ -20,7 +20,7 @@ from synth import rnn_inputs  # noqa: E402
 
 KINDS = ["NOP", "EW", "FILL", "COPY", "REDUCE_SUM", "REDUCE_SUM0", "MATMUL", "LSTM_FWD",
          "LSTM_BWD_EW", "LSTM_BWD_MM", "ACC", "PREP_WP", "PREP_WT", "LSTM_FWD_TC",
-         "LSTM_BWD_EW_BF", "LSTM_DXH_TC", "LSTM_DW_TC", "SWAP", "WAIT", "LSTM_XPROJ_TC"]
+         "LSTM_BWD_EW_BF", "LSTM_DXH_TC", "LSTM_DW_TC", "SWAP", "WAIT", "LSTM_XPROJ_TC", "MATMUL_TC"]
 
 OPS = ["NOP", "PLACEHOLDER", "CONST", "PASS", "SWITCH", "MERGE", "MERGE_LOOP", "ENTER", "EXIT",
        "NEXTITER", "SCALAR", "REDUCE_I", "SLICE_I", "FLOW", "TA_CREATE", "TA_READ", "TA_WRITE",
@@ -53,10 +53,12 @@ def main():
     prec = cf.BF16 if a.precision == "bf16" else cf.F32
     if a.no_tiles:
         cf.debug_set_flags(1)
-    p = dynamic_rnn_lstm(c["T"], c["B"], c["I"], c["H"], c["L"], with_grads=not a.fwd_only)
+    kw = {"moe": True, "moe_act": c.get("moe_act", "relu")} if c.get("moe") else {}
+    p = dynamic_rnn_lstm(c["T"], c["B"], c["I"], c["H"], c["L"], with_grads=not a.fwd_only, **kw)
     s = cf.Session(p.g, p.fetch_tensors(), precision=prec, parallel_iterations=a.K, profile=True,
                    stack_budget_bytes=a.stack_budget, swap_smallest_first=a.swap_smallest_first)
-    f = rnn_inputs(c["T"], c["B"], c["I"], c["H"], c["L"], seed=0, len_mode=c["len_mode"], bf16=prec == cf.BF16)
+    f = rnn_inputs(c["T"], c["B"], c["I"], c["H"], c["L"], seed=0, len_mode=c["len_mode"], bf16=prec == cf.BF16,
+                   moe=c.get("moe", False))
     dev = feeds_to_device(f, session=s)
     outs = s.alloc_outputs()
     for _ in range(2):

@@ -7,7 +7,7 @@ import numpy as np
 
 KINDS = ["NOP", "EW", "FILL", "COPY", "RSUM", "RSUM0", "MATMUL", "LSTM_FWD", "LSTM_BWD_EW",
          "LSTM_BWD_MM", "ACC", "PREPWP", "PREPWT", "FWD", "EWbf", "DXH", "DW", "SWAP", "WAIT",
-         "XPROJ"]
+         "XPROJ", "MMTC"]
 r = np.load(sys.argv[1])
 binms = float(sys.argv[2]) if len(sys.argv) > 2 else 0.25
 ranges = [tuple(float(v) for v in x.split("-")) for x in sys.argv[3].split(",")] if len(sys.argv) > 3 else None
