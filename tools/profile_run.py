@@ -46,6 +46,7 @@ def main():
     ap.add_argument("--out", default="gpurun_out/profile.json")
     ap.add_argument("--no-tiles", action="store_true", help="workers skip tile bodies (driver alone)")
     ap.add_argument("--fwd-only", action="store_true", help="the forward loop alone (no gradients)")
+    ap.add_argument("--workers", type=int, default=0, help="worker CTAs (0: one per SM but the driver's)")
     a = ap.parse_args()
     c = dict(CONFIGS[a.config])
     if a.T:
@@ -56,6 +57,7 @@ def main():
     kw = {"moe": True, "moe_act": c.get("moe_act", "relu")} if c.get("moe") else {}
     p = dynamic_rnn_lstm(c["T"], c["B"], c["I"], c["H"], c["L"], with_grads=not a.fwd_only, **kw)
     s = cf.Session(p.g, p.fetch_tensors(), precision=prec, parallel_iterations=a.K, profile=True,
+                   num_workers=a.workers,
                    stack_budget_bytes=a.stack_budget, swap_smallest_first=a.swap_smallest_first)
     f = rnn_inputs(c["T"], c["B"], c["I"], c["H"], c["L"], seed=0, len_mode=c["len_mode"], bf16=prec == cf.BF16,
                    moe=c.get("moe", False))
