@@ -51,8 +51,9 @@ int32_t cf_debug_set_worker_roles(int32_t low_first, int32_t strict);
  * with a forward LSTM node's instance construction, bit 29 = the same for a backward node
  * (steps that do not close a dW chunk). Returns 0 or CF_E_CUDA. */
 int32_t cf_debug_set_flags(int32_t flags);
-/* A/B knobs, read by the kernel as it runs (0 = default): 0 = how many k-blocks before a
- * tensor-core tile's last MMA issue the worker claims its next tile (default 8). Returns 0,
+/* A/B knobs, read by the kernel as it runs (0 = default): knob 0 = how many k-blocks before
+ * a tensor-core tile's last MMA issue the worker claims its next tile (default 8); knob 1 = 1:
+ * no overlap of a heavy batch's records and submissions with the routing after it. Returns 0,
  * CF_E_SHAPE (which outside 0..7) or CF_E_CUDA. */
 int32_t cf_debug_set_knob(int32_t which, int32_t value);
 /* Tile phase clocks, collected while cf_debug_set_flags bit 22 is set: out20[4k + 0] tiles,

@@ -801,6 +801,10 @@ __device__ __forceinline__ int wave_lane(int tid) {
   const int w = tid >> 5;
   return w < 4 ? tid - 32 : tid - 64;   // 0..191 for warps 1-3, 5-7
 }
+__device__ __forceinline__ int wave_lane5(int tid) {
+  const int w = tid >> 5;
+  return w < 4 ? tid - 64 : tid - 96;   // 0..159 for warps 2-3, 5-7 (warp 1 busy with a batch)
+}
 
 // a wave request from the driver thread to the helper warps (shared memory)
 struct Wave {
@@ -840,6 +844,12 @@ struct Wave {
   // lanes hand back (ids used, tiles, dead members, queue tails touched, last dW chunk)
   int bbase, bfoff;
   int bids, btiles, bdead, bdirty, blast;
+  // job 3 runs on its own request counter (bseq, warp 1 only) with its own signals: placements
+  // and tokens done (bphase), everything done (bdone). Meanwhile the driver may dispatch the
+  // next wave job to the other five helper warps (nw = 5, skip1): the lanes' records, edges
+  // and submissions overlap the routing after the batch
+  int bseq, bphase, bdone;
+  int nw, skip1;          // warps in the current wave / prep job, warp 1 excluded
 };
 
 __device__ void wave_work(Wave& w, int start, int n, int h, int nh) {
@@ -1019,7 +1029,7 @@ struct Driver {
     }
   }
   __device__ void wave_wait() {
-    while (*(volatile int*)&wave_->done < kWaveWarps) {
+    while (*(volatile int*)&wave_->done < wave_->nw) {
     }
     __threadfence_block();
   }
@@ -1082,6 +1092,8 @@ struct Driver {
     w.env.it = cur_frame >= 0 ? iter : 0;
     w.env.git = git();
     w.done = 0;
+    w.skip1 = pend_batch_ ? 1 : 0;   // warp 1 still runs the batch job
+    w.nw = pend_batch_ ? kWaveWarps - 1 : kWaveWarps;
     __threadfence_block();
     *(volatile int*)&w.seq = w.seq + 1;
     flush_publish();
@@ -1092,7 +1104,7 @@ struct Driver {
     Wave& w = *wave_;
     const int nlev = w.nlev;
     long long wq0 = (kProfBuild && A.prof) ? clock64() : 0, wdr = 0;
-    while (*(volatile int*)&w.done < kWaveWarps) {
+    while (*(volatile int*)&w.done < w.nw) {
       long long d0 = (kProfBuild && A.prof) ? clock64() : 0;
       maybe_drain();   // the helper warps touch tokens and stacks only, never instance state
       if (kProfBuild && A.prof) wdr += clock64() - d0;
@@ -1164,7 +1176,7 @@ struct Driver {
       if (!place_core(d, h - 64, &v)) atomicOr(&w.hfail, 1);
       else w.houtp[h - 64] = v;
     }
-    asm volatile("bar.sync 1, %0;" ::"r"(32 * kWaveWarps) : "memory");
+    asm volatile("bar.sync 1, %0;" ::"r"(32 * w.nw) : "memory");
     if (w.hdead || w.hfail || h >= 5) return;
     const int64_t B = d.imm[0], In = d.imm[1], H = d.imm[2], KT = In + H;
     int16_t* hint = (int16_t*)const_cast<DNode&>(d).pad;
@@ -1198,10 +1210,12 @@ struct Driver {
     w.hdead = 0;
     w.hfail = 0;
     w.done = 0;
+    w.skip1 = pend_batch_ ? 1 : 0;
+    w.nw = pend_batch_ ? kWaveWarps - 1 : kWaveWarps;
     __threadfence_block();
     *(volatile int*)&w.seq = w.seq + 1;
     flush_publish();
-    while (*(volatile int*)&w.done < kWaveWarps) {
+    while (*(volatile int*)&w.done < w.nw) {
       maybe_drain();
     }
     __threadfence_block();
@@ -1319,6 +1333,7 @@ struct Driver {
   }
   // an instance id and its in-flight ring slot (driver-private shared-memory bookkeeping)
   __noinline__ __device__ int32_t reserve_inst(int kind, int ntiles) {
+    finish_batch();
     if (ninst >= A.inst_cap) {
       fail(CF_E_STACK_BUDGET, -1);
       return -1;
@@ -1539,6 +1554,7 @@ struct Driver {
   }
   __noinline__ __device__ bool drain() {
     Region rg(this, 32 + 4);
+    finish_batch();   // completions must not run while a batch's lanes add edges
     last_drain_ = clock64();
     bool any = false;
     if (io_out > 0) any = drain_io();
@@ -1943,9 +1959,40 @@ struct Driver {
   // operand-registry lookups, records and dependency edges); the driver then submits. Returns
   // the body positions consumed: n + 1, or 1 when the members must go through the general
   // path one by one (a context or a scalar not known yet, a dead member, a pending wave job).
+  // settle the batch job in flight (job 3): wait for its lanes, then account its instances
+  bool pend_batch_ = false;
+  __noinline__ __device__ void finish_batch() {
+    if (!pend_batch_) return;
+    Wave& w = *wave_;
+    while (*(volatile int*)&w.bdone == 0) {
+    }
+    __threadfence_block();
+    pend_batch_ = false;
+    if (kProfBuild && A.prof) {   // lane-0 clocks: wake, checks, reserve, placements,
+      const long long now = clock64();   // records + edges (slowest lane), settle
+      op_cyc[28] += w.bt_start - w.bt_issue; op_cyc[29] += w.bt_chk - w.bt_start;
+      op_cyc[30] += w.bt_res - w.bt_chk;
+      op_cyc[32 + 25] += w.bt_a - w.bt_res;
+      op_cyc[32 + 26] += (long long)w.bt_end - w.bt_a;
+      op_cyc[32 + 27] += now - (long long)w.bt_end;
+      op_cnt[28]++; op_cnt[29]++; op_cnt[30]++;
+      op_cnt[32 + 25]++; op_cnt[32 + 26]++; op_cnt[32 + 27]++;
+    }
+    outstanding += w.bids;
+    n_inst += w.bids;
+    n_tiles += w.btiles;
+    n_dead += w.bdead;
+    if (cur_frame >= 0) iter_out_[frame_ib(cur_frame) + iter] += w.bids;
+    if (w.blast >= 0) last_dw = w.blast;
+    dirty_ |= w.bdirty;
+    flush_publish();
+    if (w.bfail && !st->error) fail(CF_E_UNSUPPORTED, -600);
+  }
+
   __noinline__ __device__ int run_batch(const DFrame& F, int pc, int n) {
     Region rg(this, 32 + 23);
     const long long bt_enter = (kProfBuild && A.prof) ? clock64() : 0;
+    finish_batch();
     if (pend_wave_pc_ >= 0 || P.precision != D_BF16 || P.n_swaps || (dbg_ & (1 << 30))) return 1;
     Wave& w = *wave_;
     if (!(dbg_ & (1 << 28)) && n <= 32) {
@@ -1957,12 +2004,12 @@ struct Driver {
         const int c = bn_[pc + 1 + m].ctx;
         if (c && !(lstamp_[c] == lgen_ && lval_[c] >= 0) && ctx_live(c) < 0) return 1;
       }
-      w.job = 3;
+      flush_publish();   // before the lanes start appending to the queues
       w.bpc = pc + 1;
       w.bcount = n;
       w.bfail = 0;
-      w.chain = 0;
-      w.done = 0;
+      w.bphase = 0;
+      w.bdone = 0;
       w.bbase = ninst;
       w.bfoff = F.body_off;
       w.bids = w.btiles = w.bdead = w.bdirty = 0;
@@ -1972,33 +2019,21 @@ struct Driver {
         w.bt_issue = clock64();
       }
       __threadfence_block();
-      *(volatile int*)&w.seq = w.seq + 1;
-      flush_publish();
-      while (*(volatile int*)&w.done < kWaveWarps) {
+      *(volatile int*)&w.bseq = w.bseq + 1;
+      // the member tokens are set once phase A is done; the records, edges and submissions
+      // finish while the driver goes on with the routing (finish_batch settles them before
+      // anything reads or changes instance state)
+      while (*(volatile int*)&w.bphase == 0) {
       }
       __threadfence_block();
-      w.job = 0;
-      if (kProfBuild && A.prof) {   // lane-0 clocks: wake, checks, reserve, placements,
-        const long long now = clock64();   // records + edges (slowest lane), submit + tail
-        op_cyc[28] += w.bt_start - w.bt_issue; op_cyc[29] += w.bt_chk - w.bt_start;
-        op_cyc[30] += w.bt_res - w.bt_chk;
-        op_cyc[32 + 25] += w.bt_a - w.bt_res;
-        op_cyc[32 + 26] += (long long)w.bt_end - w.bt_a;
-        op_cyc[32 + 27] += now - (long long)w.bt_end;
-        op_cnt[28]++; op_cnt[29]++; op_cnt[30]++;
-        op_cnt[32 + 25]++; op_cnt[32 + 26]++; op_cnt[32 + 27]++;
-      }
-      if (w.bfail != 2) {   // 2: a member needs the general path; nothing was changed
+      if (w.bphase == 2) {   // a member needs the general path; nothing was changed
+        while (*(volatile int*)&w.bdone == 0) {
+        }
+        __threadfence_block();
+      } else {
         ninst += w.bids;
-        outstanding += w.bids;
-        n_inst += w.bids;
-        n_tiles += w.btiles;
-        n_dead += w.bdead;
-        if (cur_frame >= 0) iter_out_[frame_ib(cur_frame) + iter] += w.bids;
-        if (w.blast >= 0) last_dw = w.blast;
-        dirty_ |= w.bdirty;
-        flush_publish();
-        if (w.bfail && !st->error) fail(CF_E_UNSUPPORTED, -600);
+        pend_batch_ = true;
+        if (tc::kKnobs[1]) finish_batch();   // A/B knob 1: no overlap
         return n + 1;
       }
     }
@@ -2072,6 +2107,8 @@ struct Driver {
     w.bfail = 0;
     w.chain = 0;
     w.done = 0;
+    w.nw = kWaveWarps;
+    w.skip1 = 0;
     if (kProfBuild && A.prof) {
       w.bt_end = 0;
       w.bt_issue = clock64();
@@ -2108,7 +2145,7 @@ struct Driver {
   }
 
   // helper lane m of warp 1: member m of the batch dispatched by run_batch
-  __device__ void batch_lane(Wave& w, int m) {
+  __device__ void batch_lane(Wave& w, int m, bool signal_a = false) {
     if (kProfBuild && A.prof && m == 0 && w.job == 2) w.bt_start = clock64();
     const bool mine = m < w.bcount && w.bid[m][0] >= 0;
     const DNode* dp = mine ? &bn_[w.bpc + m] : nullptr;
@@ -2140,6 +2177,10 @@ struct Driver {
     }
     __syncwarp();
     if (kProfBuild && A.prof && m == 0) w.bt_a = clock64();
+    if (signal_a) {   // the members' output tokens are set: the driver may go on
+      __threadfence_block();
+      if (m == 0) *(volatile int*)&w.bphase = 1;
+    }
     // phase B: operand lookups, records, dependency edges
     if (mine && ok) ok = batch_build(*dp, w.bnid[m], w.bid[m], outp);
     if (mine && !ok) atomicOr(&w.bfail, 1);
@@ -2199,6 +2240,8 @@ struct Driver {
     if (__any_sync(full, bad)) {
       if (m == 0) w.bfail = 2;
       __syncwarp();
+      __threadfence_block();
+      if (m == 0) *(volatile int*)&w.bphase = 2;
       return;
     }
     // ---- reserve (the serial path's order: weight prep, dW chunk / x-projection, main)
@@ -2257,8 +2300,8 @@ struct Driver {
     }
     __syncwarp();
     if (kProfBuild && A.prof && m == 0) w.bt_res = clock64();
-    // ---- placements, tokens, records, edges (the job-2 lanes' code)
-    batch_lane(w, m);
+    // ---- placements, tokens, records, edges (the job-2 lanes' code; phase A done -> bphase)
+    batch_lane(w, m, true);
     if (kProfBuild && A.prof && m == 0) w.bt_built = clock64();
     // ---- submit (every member's edges exist: each lane adds only its own instances' edges)
     if (in && live) {
@@ -2281,6 +2324,8 @@ struct Driver {
       atomicAdd(&w.btiles, tiles);
     }
     __syncwarp();
+    __threadfence_block();
+    if (m == 0) *(volatile int*)&w.bdone = 1;
   }
 
   __device__ bool batch_build(const DNode& d, int nid, const int* id, const int64_t* outp) {
@@ -3549,6 +3594,7 @@ struct Driver {
       ++pc;
       progress = true;
     }
+    finish_batch();   // the iteration's instances counted before its window state is read
     body_pc = pc;
     n_push += fc.push;
     n_pop += fc.pop;
@@ -4004,6 +4050,11 @@ __global__ void __launch_bounds__(kThreads, 1) cf_driver_kernel(RunArgs A_param)
       req[1] = 0;
       wave.seq = 0;
       wave.done = 0;
+      wave.bseq = 0;
+      wave.bphase = 0;
+      wave.bdone = 0;
+      wave.nw = kWaveWarps;
+      wave.skip1 = 0;
       wave.env_frame = -2;
       wave.job = 0;
       wave.chain = 0;
@@ -4050,40 +4101,51 @@ __global__ void __launch_bounds__(kThreads, 1) cf_driver_kernel(RunArgs A_param)
         d.lval_[c] = 0;
       }
       d.run();
+      d.finish_batch();   // (an error path may leave a batch job's lanes running)
       *(volatile int*)&req[0] = -1;
     } else if (threadIdx.x >= 32) {
       // helper warps: cooperative smem staging on request from the driver thread
-      int seen = 0, wseen = 0;
+      int seen = 0, wseen = 0, bseen = 0;
       const bool nosleep = kDbgFlags & 8;   // A/B knob: wave helpers spin without sleeping
       const int h = threadIdx.x - 32, nh = blockDim.x - 32;
       while (true) {
         int q = *(volatile int*)&req[0];
         if (q < 0) break;
+        if ((threadIdx.x >> 5) == 1) {   // warp 1: batch jobs first (their own counter)
+          const int bs = *(volatile int*)&wave.bseq;
+          if (bs != bseen) {
+            bseen = bs;
+            __threadfence_block();
+            ((Driver*)drv_obj)->batch_lane_par(wave, threadIdx.x & 31);
+            continue;
+          }
+        }
         const int ws = (threadIdx.x >> 5) == 4 ? wseen : *(volatile int*)&wave.seq;
         if (ws != wseen) {
           wseen = ws;
           __threadfence_block();
+          const bool skip = wave.skip1 && (threadIdx.x >> 5) == 1;   // job without warp 1
+          if (skip) continue;
+          const int nthr = 32 * wave.nw;
+          const int hl = wave.skip1 ? wave_lane5(threadIdx.x) : wave_lane(threadIdx.x);
           if (wave.job == 1) {
-            ((Driver*)drv_obj)->heavy_prep_lane(wave, wave_lane(threadIdx.x));
+            ((Driver*)drv_obj)->heavy_prep_lane(wave, hl);
           } else if (wave.job == 2) {
             if ((threadIdx.x >> 5) == 1) ((Driver*)drv_obj)->batch_lane(wave, threadIdx.x & 31);
-          } else if (wave.job == 3) {
-            if ((threadIdx.x >> 5) == 1) ((Driver*)drv_obj)->batch_lane_par(wave, threadIdx.x & 31);
           } else {
             // fused levels: each reads the previous one's tokens (named barrier between)
-            const int hl = wave_lane(threadIdx.x);
             int k = 0;
             for (; k < wave.nlev; ++k) {
               if (k > 0 && (wave.lev_ctx[k] | wave.lev_ctx_hi[k])) {   // this level's contexts
                 if (hl == 0 && !((Driver*)drv_obj)->helper_ctx(wave.lev_ctx[k], wave.lev_ctx_hi[k]))
                   wave.cstop = k;
                 __threadfence_block();
-                asm volatile("bar.sync 1, %0;" ::"r"(32 * kWaveWarps) : "memory");
+                asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
                 if (wave.cstop >= 0) break;
               }
-              wave_work(wave, wave.lev_start[k], wave.lev_n[k], hl, 32 * kWaveWarps);
+              wave_work(wave, wave.lev_start[k], wave.lev_n[k], hl, nthr);
               __threadfence_block();
-              asm volatile("bar.sync 1, %0;" ::"r"(32 * kWaveWarps) : "memory");
+              asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
               if (wave.nslow || wave.cnt.err) break;   // the driver evaluates the leftovers
             }
             if (hl == 0) wave.lev_stop = wave.cstop >= 0 ? wave.cstop : k < wave.nlev ? k : wave.nlev;
