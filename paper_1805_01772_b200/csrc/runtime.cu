@@ -1744,6 +1744,7 @@ struct Driver {
     return (d.imm[3] >> 32) > 0 ? (int)(d.imm[3] >> 32) - 1 : nid;
   }
   __noinline__ __device__ bool prep_early(int nid) {
+    finish_batch();
     const DNode& d = node(nid);
     if (prep_inst_[nid] >= 0 || (d.imm[3] & 0xffffffffLL) <= 0) return true;
     const Tok& w = toks_[(d.imm[3] & 0xffffffffLL) - 1];
@@ -1787,6 +1788,7 @@ struct Driver {
   // pm / ps: operand-registry lookups already made by the helper lanes (nullptr: here)
   __noinline__ __device__ int eval_lstm_tc(const DNode& d, int nid, const int64_t* outp,
                                            const int64_t* pm = nullptr, const int64_t* ps = nullptr) {
+    finish_batch();   // reads the dW / accumulator writers a pending batch may still set
     // operand-registry hints live in the (driver-private) body-program copy of the node
     int16_t* hint = (int16_t*)const_cast<DNode&>(d).pad;
     Region rg(this, 32 + 9);
@@ -1978,11 +1980,8 @@ struct Driver {
       op_cnt[28]++; op_cnt[29]++; op_cnt[30]++;
       op_cnt[32 + 25]++; op_cnt[32 + 26]++; op_cnt[32 + 27]++;
     }
-    outstanding += w.bids;
-    n_inst += w.bids;
     n_tiles += w.btiles;
     n_dead += w.bdead;
-    if (cur_frame >= 0) iter_out_[frame_ib(cur_frame) + iter] += w.bids;
     if (w.blast >= 0) last_dw = w.blast;
     dirty_ |= w.bdirty;
     flush_publish();
@@ -2031,7 +2030,11 @@ struct Driver {
         }
         __threadfence_block();
       } else {
+        // the ids and the iteration's outstanding count now; tiles and queue state at settling
         ninst += w.bids;
+        outstanding += w.bids;
+        n_inst += w.bids;
+        if (cur_frame >= 0) iter_out_[frame_ib(cur_frame) + iter] += w.bids;
         pend_batch_ = true;
         if (tc::kKnobs[1]) finish_batch();   // A/B knob 1: no overlap
         return n + 1;
@@ -3594,7 +3597,6 @@ struct Driver {
       ++pc;
       progress = true;
     }
-    finish_batch();   // the iteration's instances counted before its window state is read
     body_pc = pc;
     n_push += fc.push;
     n_pop += fc.pop;
@@ -3651,6 +3653,7 @@ struct Driver {
     // is dead) => Exit fires once with this iteration's values (reading R2)
     const DNode& cs = node(F.counter_switch);
     if (toks_[cs.out_vid + 1].dead) {
+      finish_batch();   // the frame's last batch settles before the frame exits
       // flush partially filled dW chunks before the accumulators leave the frame
       for (int k = 0; k < F.n_body; ++k) {
         const int nid = P.order[F.body_off + k];
