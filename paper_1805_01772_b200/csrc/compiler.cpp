@@ -1251,6 +1251,20 @@ struct Compiler {
     for (int k = 0; k < n; ++k) bat[k] = batchable((*ord)[k]) ? 1 : 0;
     for (int k = 0; k < n; ++k)
       for (int q : preds[k]) phase[k] = std::max(phase[k], phase[q] + ((bat[q] && !bat[k]) ? 1 : 0));
+    // a batch completes as a unit: a node that reads batch members starts one level after the
+    // batch's LAST member, not after the member it reads (the layers of a cell branch chain
+    // inside the batch, which otherwise turns the routing after it into one level per layer)
+    if (!std::getenv("CF_NO_BATCH_LEVELS")) {
+      std::map<int, int> blev;   // phase -> deepest batchable member
+      for (int k = 0; k < n; ++k)
+        if (bat[k]) blev[phase[k]] = std::max(blev[phase[k]], level[k]);
+      for (int k = 0; k < n; ++k) {
+        if (bat[k]) continue;
+        int lv = 0;
+        for (int q : preds[k]) lv = std::max(lv, (bat[q] ? blev[phase[q]] : level[q]) + 1);
+        level[k] = lv;
+      }
+    }
     std::vector<int> idx(n);
     for (int k = 0; k < n; ++k) idx[k] = k;
     std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) {

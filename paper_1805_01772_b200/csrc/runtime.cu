@@ -1095,7 +1095,7 @@ struct Driver {
     w.skip1 = pend_batch_ ? 1 : 0;   // warp 1 still runs the batch job
     w.nw = pend_batch_ ? kWaveWarps - 1 : kWaveWarps;
     __threadfence_block();
-    *(volatile int*)&w.seq = w.seq + 1;
+    *(volatile int*)&w.seq = (((w.seq >> 1) + 1) << 1) | w.skip1;   // bit 0: warp 1 not in the job
     flush_publish();
     return true;
   }
@@ -1213,7 +1213,7 @@ struct Driver {
     w.skip1 = pend_batch_ ? 1 : 0;
     w.nw = pend_batch_ ? kWaveWarps - 1 : kWaveWarps;
     __threadfence_block();
-    *(volatile int*)&w.seq = w.seq + 1;
+    *(volatile int*)&w.seq = (((w.seq >> 1) + 1) << 1) | w.skip1;   // bit 0: warp 1 not in the job
     flush_publish();
     while (*(volatile int*)&w.done < w.nw) {
       maybe_drain();
@@ -2117,7 +2117,7 @@ struct Driver {
       w.bt_issue = clock64();
     }
     __threadfence_block();
-    *(volatile int*)&w.seq = w.seq + 1;
+    *(volatile int*)&w.seq = (((w.seq >> 1) + 1) << 1) | w.skip1;   // bit 0: warp 1 not in the job
     flush_publish();
     while (*(volatile int*)&w.done < kWaveWarps) {
     }
@@ -2240,11 +2240,14 @@ struct Driver {
     int first = w.bbase + off;
     for (int k = 0; k < cnt; ++k)
       if (r_id[(first + k) & kRingMask] != -1 || first + k >= A.inst_cap) bad = 1;
-    if (__any_sync(full, bad)) {
+    if (__any_sync(full, bad)) {   // handed back: nothing changed, the job is over
       if (m == 0) w.bfail = 2;
       __syncwarp();
       __threadfence_block();
-      if (m == 0) *(volatile int*)&w.bphase = 2;
+      if (m == 0) {
+        *(volatile int*)&w.bdone = 1;
+        *(volatile int*)&w.bphase = 2;
+      }
       return;
     }
     // ---- reserve (the serial path's order: weight prep, dW chunk / x-projection, main)
@@ -4127,10 +4130,12 @@ __global__ void __launch_bounds__(kThreads, 1) cf_driver_kernel(RunArgs A_param)
         if (ws != wseen) {
           wseen = ws;
           __threadfence_block();
-          const bool skip = wave.skip1 && (threadIdx.x >> 5) == 1;   // job without warp 1
-          if (skip) continue;
-          const int nthr = 32 * wave.nw;
-          const int hl = wave.skip1 ? wave_lane5(threadIdx.x) : wave_lane(threadIdx.x);
+          // whether warp 1 takes part comes with the request number itself (bit 0): warp 1 may
+          // read the number of a job it sat out only after the next job's fields were written
+          const bool no1 = ws & 1;
+          if (no1 && (threadIdx.x >> 5) == 1) continue;
+          const int nthr = no1 ? 32 * (kWaveWarps - 1) : 32 * kWaveWarps;
+          const int hl = no1 ? wave_lane5(threadIdx.x) : wave_lane(threadIdx.x);
           if (wave.job == 1) {
             ((Driver*)drv_obj)->heavy_prep_lane(wave, hl);
           } else if (wave.job == 2) {

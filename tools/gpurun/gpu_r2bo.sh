@@ -1,0 +1,5 @@
+python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
+timeout 1800 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+CHUNKS="8" timeout 900 python tools/dwchunk_ab.py 2>&1 | grep "dw_chunk\|Error"
+CF_NO_BATCH_LEVELS=1 CHUNKS="8" timeout 900 python tools/dwchunk_ab.py 2>&1 | grep "dw_chunk\|Error"
+CHUNKS="8" timeout 900 python tools/dwchunk_ab.py 2>&1 | grep "dw_chunk\|Error"
