@@ -849,6 +849,7 @@ struct Wave {
   // next wave job to the other five helper warps (nw = 5, skip1): the lanes' records, edges
   // and submissions overlap the routing after the batch
   int bseq, bphase, bdone;
+  int bgo;                // the driver stopped processing completions: the lanes may add edges
   int nw, skip1;          // warps in the current wave / prep job, warp 1 excluded
 };
 
@@ -2009,6 +2010,7 @@ struct Driver {
       w.bfail = 0;
       w.bphase = 0;
       w.bdone = 0;
+      w.bgo = 0;
       w.bbase = ninst;
       w.bfoff = F.body_off;
       w.bids = w.btiles = w.bdead = w.bdirty = 0;
@@ -2021,10 +2023,13 @@ struct Driver {
       *(volatile int*)&w.bseq = w.bseq + 1;
       // the member tokens are set once phase A is done; the records, edges and submissions
       // finish while the driver goes on with the routing (finish_batch settles them before
-      // anything reads or changes instance state)
+      // anything reads or changes instance state). Until then the lanes only read tokens and
+      // claim free ring slots, so completions may still be processed meanwhile
       while (*(volatile int*)&w.bphase == 0) {
+        maybe_drain();
       }
       __threadfence_block();
+      *(volatile int*)&w.bgo = 1;   // no completion runs from here until finish_batch
       if (w.bphase == 2) {   // a member needs the general path; nothing was changed
         while (*(volatile int*)&w.bdone == 0) {
         }
@@ -2182,7 +2187,15 @@ struct Driver {
     if (kProfBuild && A.prof && m == 0) w.bt_a = clock64();
     if (signal_a) {   // the members' output tokens are set: the driver may go on
       __threadfence_block();
-      if (m == 0) *(volatile int*)&w.bphase = 1;
+      if (m == 0) {
+        *(volatile int*)&w.bphase = 1;
+        // edges only once the driver has left its completion polling (it drains while it
+        // waits for phase A; a completion walking a successor list must not meet a new edge)
+        while (*(volatile int*)&w.bgo == 0) {
+        }
+      }
+      __syncwarp();
+      __threadfence_block();
     }
     // phase B: operand lookups, records, dependency edges
     if (mine && ok) ok = batch_build(*dp, w.bnid[m], w.bid[m], outp);
@@ -4059,6 +4072,7 @@ __global__ void __launch_bounds__(kThreads, 1) cf_driver_kernel(RunArgs A_param)
       wave.bseq = 0;
       wave.bphase = 0;
       wave.bdone = 0;
+      wave.bgo = 0;
       wave.nw = kWaveWarps;
       wave.skip1 = 0;
       wave.env_frame = -2;
