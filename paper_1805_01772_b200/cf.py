@@ -547,31 +547,40 @@ class Session:
         (outputs, dead flags, trace dict | None)."""
         import torch
         names = list(feeds)
-        bufs = (cf_buffer * max(len(names), 1))()
-        keep = []
-        for i, nm in enumerate(names):
-            t = feeds[nm]
-            if not t.is_cuda or not t.is_contiguous():
-                raise CfError(2, f"feed {nm} must be a contiguous CUDA tensor")
-            keep.append(t)
-            bufs[i].data = t.data_ptr()
-            bufs[i].dtype = {torch.bool: BOOL, torch.int32: I32, torch.int64: I64,
-                             torch.float32: F32, torch.bfloat16: BF16}[t.dtype]
-            bufs[i].rank = t.dim()
-            for k, s in enumerate(t.shape):
-                bufs[i].shape[k] = s
-        cnames = (C.c_char_p * max(len(names), 1))(*[n.encode() for n in names])
         if outs is None:
             outs = self.alloc_outputs()
-        obufs = (cf_buffer * max(len(outs), 1))()
-        for i, t in enumerate(outs):
-            obufs[i].data = t.data_ptr()
-            obufs[i].dtype = self.fetch_dtypes[i]
-            obufs[i].rank = t.dim()
-            for k, sz in enumerate(t.shape):
-                obufs[i].shape[k] = sz
-            if not t.is_contiguous() or t.element_size() != _dtype_size(self.fetch_dtypes[i]):
-                raise CfError(2, f"fetch buffer {i} must be contiguous with the session dtype")
+        # the marshalled argument arrays of the previous call are reused when the same tensors
+        # come again (a training loop's resident inputs): one key comparison instead of a
+        # per-feed rebuild
+        key = (tuple((nm, feeds[nm].data_ptr(), feeds[nm].dtype, tuple(feeds[nm].shape),
+                      tuple(feeds[nm].stride()), feeds[nm].is_cuda) for nm in names),
+               tuple((t.data_ptr(), t.dtype, tuple(t.shape), tuple(t.stride())) for t in outs))
+        cached = getattr(self, "_args_cache", None)
+        if cached is not None and cached[0] == key:
+            bufs, cnames, obufs = cached[1]
+        else:
+            bufs = (cf_buffer * max(len(names), 1))()
+            for i, nm in enumerate(names):
+                t = feeds[nm]
+                if not t.is_cuda or not t.is_contiguous():
+                    raise CfError(2, f"feed {nm} must be a contiguous CUDA tensor")
+                bufs[i].data = t.data_ptr()
+                bufs[i].dtype = {torch.bool: BOOL, torch.int32: I32, torch.int64: I64,
+                                 torch.float32: F32, torch.bfloat16: BF16}[t.dtype]
+                bufs[i].rank = t.dim()
+                for k, s in enumerate(t.shape):
+                    bufs[i].shape[k] = s
+            cnames = (C.c_char_p * max(len(names), 1))(*[n.encode() for n in names])
+            obufs = (cf_buffer * max(len(outs), 1))()
+            for i, t in enumerate(outs):
+                obufs[i].data = t.data_ptr()
+                obufs[i].dtype = self.fetch_dtypes[i]
+                obufs[i].rank = t.dim()
+                for k, sz in enumerate(t.shape):
+                    obufs[i].shape[k] = sz
+                if not t.is_contiguous() or t.element_size() != _dtype_size(self.fetch_dtypes[i]):
+                    raise CfError(2, f"fetch buffer {i} must be contiguous with the session dtype")
+            self._args_cache = (key, (bufs, cnames, obufs))
         dead = (C.c_uint8 * max(len(outs), 1))()
         tr = cf_trace()
         bits = None
