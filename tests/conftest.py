@@ -10,3 +10,19 @@ for p in (ROOT, os.path.join(ROOT, "tests")):
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (run via gpurun)")
     config.addinivalue_line("markers", "slow: long-running")
+
+
+import pytest  # noqa: E402
+
+
+@pytest.fixture(autouse=True, scope="session")
+def _debug_knobs():
+    """CF_TEST_KNOBS="2=1,..." runs the GPU tests with cf_debug_set_knob A/B knobs set (e.g.
+    knob 2: completions concurrent with a batch's edge insertion)."""
+    spec = os.environ.get("CF_TEST_KNOBS")
+    if spec:
+        from paper_1805_01772_b200 import cf
+        for kv in spec.split(","):
+            k, v = kv.split("=")
+            cf.debug_set_knob(int(k), int(v))
+    yield
