@@ -850,11 +850,6 @@ struct Wave {
   // and submissions overlap the routing after the batch
   int bseq, bphase, bdone;
   int bgo;                // the driver stopped processing completions: the lanes may add edges
-  // knob 2 (concurrent completions): the lanes add edges while the driver completes
-  // instances (closed successor lists, construction references); instances that are ready
-  // when their lane submits them wait in `ready` for the driver to publish
-  int conc, nready;
-  int ready[128];
   int nw, skip1;          // warps in the current wave / prep job, warp 1 excluded
 };
 
@@ -1362,8 +1357,6 @@ struct Driver {
     r_succ[sl] = -1;
     r_last[sl] = -1;
     r_sn[sl] = 0;
-    if (conc_)
-      for (int k = 0; k < kInlineSucc; ++k) r_sv[sl * kInlineSucc + k] = -1;
     r_nt[sl] = ntiles;
     // iteration in the top 16 bits; 0xFFFF = read the full iteration from the record (loops
     // longer than 65534 iterations)
@@ -1396,37 +1389,13 @@ struct Driver {
       pr[5] = ((unsigned long long)kind << 32) | (unsigned)ntiles;
     }
   }
-  // add_dep for the helper lanes of a batch (several lanes register successors concurrently;
-  // the driver thread waits meanwhile, so no completion runs): shared-memory atomics, no
-  // dedupe across lanes (a repeated producer just counts twice, consistently)
-  static constexpr int kClosed = 1 << 30;   // r_sn: the producer completed, no more edges
-  bool conc_ = false;                        // knob 2 for this run
+  // add_dep for the helper lanes of a batch (several lanes, and the driver's own add_dep while
+  // the batch is pending, register successors concurrently; no completion runs until the
+  // batch is settled): shared-memory atomics, no dedupe across lanes (a repeated producer
+  // just counts twice, consistently)
   __device__ void add_dep_atomic(int32_t id, int32_t w) {
     if (done(w)) return;
     const int ws = w & kRingMask;
-    if (wave_->conc) {   // the driver may be completing w right now
-      atomicAdd(&r_pend[id & kRingMask], 1);
-      const int old = atomicAdd(&r_sn[ws], 1);
-      if (old & kClosed) {   // w completed before this edge: nothing to wait for
-        atomicSub(&r_pend[id & kRingMask], 1);
-        return;
-      }
-      if (old < kInlineSucc) {
-        *(volatile int32_t*)&r_sv[ws * kInlineSucc + old] = id;
-      } else {
-        const int32_t e = atomicAdd(&nedge, 1);
-        if (e >= A.edge_cap) {
-          fail(CF_E_STACK_BUDGET, -2);
-          return;
-        }
-        A.edge_to[e] = id;
-        *(volatile int32_t*)&A.edge_next[e] = -2;   // linked, next not written yet
-        __threadfence_block();
-        const int32_t nx = atomicExch(&r_succ[ws], e);
-        *(volatile int32_t*)&A.edge_next[e] = nx;
-      }
-      return;
-    }
     const int ns = atomicAdd(&r_sn[ws], 1);
     if (ns < kInlineSucc) {
       r_sv[ws * kInlineSucc + ns] = id;
@@ -1466,7 +1435,7 @@ struct Driver {
     A.edge_to[e] = id;
     A.edge_next[e] = r_succ[ws];
     r_succ[ws] = e;
-    r_sn[ws] = ns + 1;   // every successor counted (knob 2's completer walks exactly r_sn)
+    r_sn[ws] = ns + 1;   // every successor counted (the atomic path above counts them too)
     r_last[ws] = id;
     r_pend[id & kRingMask]++;
   }
@@ -1539,41 +1508,6 @@ struct Driver {
       if (it == 0xFFFF) it = A.insts[id].iter;
       iter_out_[frame_ib(fr) + it]--;
     }
-    if (conc_) {   // a batch's lanes may be adding edges to this instance right now
-      const int n = atomicOr(&r_sn[sl], kClosed) & ~kClosed;   // edges reserved before the close
-      r_id[sl] = -1;   // done
-      const int ni = min(n, kInlineSucc);
-      for (int k = 0; k < ni; ++k) {
-        int32_t s2;
-        while ((s2 = *(volatile int32_t*)&r_sv[sl * kInlineSucc + k]) < 0) {
-        }
-        if (atomicSub(&r_pend[s2 & kRingMask], 1) == 1) publish(s2);
-      }
-      const int ne = n - ni;
-      if (ne > 0) {   // wait until every reserved edge is linked, then walk them once
-        while (true) {
-          int cnt = 0;
-          bool ok = true;
-          for (int32_t e = *(volatile int32_t*)&r_succ[sl]; e >= 0;) {
-            const int32_t nx = *(volatile int32_t*)&A.edge_next[e];
-            if (nx == -2) {
-              ok = false;
-              break;
-            }
-            ++cnt;
-            e = nx;
-          }
-          if (ok && cnt == ne) break;
-        }
-        for (int32_t e = r_succ[sl]; e >= 0;) {
-          const int32_t s2 = A.edge_to[e];
-          const int32_t nx = A.edge_next[e];
-          if (atomicSub(&r_pend[s2 & kRingMask], 1) == 1) publish(s2);
-          e = nx;
-        }
-      }
-      return;
-    }
     int32_t e = r_succ[sl];
     const int ns = min(r_sn[sl], kInlineSucc);   // helper lanes count past the inline slots
     r_id[sl] = -1;   // done
@@ -1628,9 +1562,7 @@ struct Driver {
   }
   __noinline__ __device__ bool drain() {
     Region rg(this, 32 + 4);
-    // completions must not run while a batch's lanes add edges (knob 2: they may; the batch
-    // is settled once its lanes are done, which publishes the instances ready at submission)
-    if (!conc_ || (pend_batch_ && *(volatile int*)&wave_->bdone)) finish_batch();
+    finish_batch();   // completions must not run while a batch's lanes add edges
     last_drain_ = clock64();
     bool any = false;
     if (io_out > 0) any = drain_io();
@@ -2059,8 +1991,6 @@ struct Driver {
     n_tiles += w.btiles;
     n_dead += w.bdead;
     if (w.blast >= 0) last_dw = w.blast;
-    for (int k = 0; k < w.nready; ++k) publish(w.ready[k]);   // conc: ready at submission
-    w.nready = 0;
     dirty_ |= w.bdirty;
     flush_publish();
     if (w.bfail && !st->error) fail(CF_E_UNSUPPORTED, -600);
@@ -2088,8 +2018,6 @@ struct Driver {
       w.bphase = 0;
       w.bdone = 0;
       w.bgo = 0;
-      w.conc = conc_ ? 1 : 0;
-      w.nready = 0;
       w.bbase = ninst;
       w.bfoff = F.body_off;
       w.bids = w.btiles = w.bdead = w.bdirty = 0;
@@ -2359,12 +2287,10 @@ struct Driver {
           const int sl = x & kRingMask;
           nt = max(nt, 1);
           r_id[sl] = x;
-          r_pend[sl] = w.conc ? 1 : 0;   // conc: a construction reference, released at submit
+          r_pend[sl] = 0;
           r_succ[sl] = -1;
           r_last[sl] = -1;
           r_sn[sl] = 0;
-          if (w.conc)
-            for (int k = 0; k < kInlineSucc; ++k) r_sv[sl * kInlineSucc + k] = -1;
           r_nt[sl] = nt;
           r_kfi[sl] = (int)((unsigned)(kind & 127) | ((unsigned)((cur_frame + 1) & 255) << 8) |
                             ((unsigned)min(cur_frame >= 0 ? iter : 0, 0xFFFF) << 16));
@@ -2408,10 +2334,6 @@ struct Driver {
       int dirty = 0;
       auto sub = [&](int x) {
         if (x < 0) return;
-        if (w.conc) {   // release the construction reference; ready -> the driver publishes
-          if (atomicSub(&r_pend[x & kRingMask], 1) == 1) w.ready[atomicAdd(&w.nready, 1)] = x;
-          return;
-        }
         if (r_pend[x & kRingMask] != 0) return;
         const int sl = x & kRingMask;
         const bool low = (r_kfi[sl] & 255) == HK_LSTM_DW_TC;
@@ -4159,8 +4081,6 @@ __global__ void __launch_bounds__(kThreads, 1) cf_driver_kernel(RunArgs A_param)
       wave.bphase = 0;
       wave.bdone = 0;
       wave.bgo = 0;
-      wave.conc = 0;
-      wave.nready = 0;
       wave.nw = kWaveWarps;
       wave.skip1 = 0;
       wave.env_frame = -2;
@@ -4175,7 +4095,6 @@ __global__ void __launch_bounds__(kThreads, 1) cf_driver_kernel(RunArgs A_param)
       Driver& d = *new (drv_obj) Driver(A, toks, smn, smi, req);
       d.wave_ = &wave;
       d.dbg_ = kDbgFlags;
-      d.conc_ = tc::kKnobs[2] != 0;
       if ((d.dbg_ >> 8) & 255) d.drain_cycles_ = 1000LL * ((d.dbg_ >> 8) & 255);
 
       if (s_pl) d.places_ = s_pl;

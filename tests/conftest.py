@@ -17,8 +17,8 @@ import pytest  # noqa: E402
 
 @pytest.fixture(autouse=True, scope="session")
 def _debug_knobs():
-    """CF_TEST_KNOBS="2=1,..." runs the GPU tests with cf_debug_set_knob A/B knobs set (e.g.
-    knob 2: completions concurrent with a batch's edge insertion)."""
+    """CF_TEST_KNOBS="0=4,1=1" runs the GPU tests with cf_debug_set_knob A/B knobs set (knob 0:
+    claim-ahead lead in k-blocks, knob 1: no batch/routing overlap)."""
     spec = os.environ.get("CF_TEST_KNOBS")
     if spec:
         from paper_1805_01772_b200 import cf

@@ -30,17 +30,15 @@ os.environ.pop("CF_DW_CHUNK")
 flags = [int(x) for x in os.environ.get("FLAGS", "0").split(",")]   # cf_debug_set_flags A/B
 knob0 = [int(x) for x in os.environ.get("KNOB0", "0").split(",")]   # cf_debug_set_knob(0, v)
 knob1 = [int(x) for x in os.environ.get("KNOB1", "0").split(",")]   # cf_debug_set_knob(1, v)
-knob2 = [int(x) for x in os.environ.get("KNOB2", "0").split(",")]   # cf_debug_set_knob(2, v)
 m2rows = [int(x) for x in os.environ.get("M2ROWS", "0").split(",")]   # cf_debug_set_m2_rows
 ref = None
 for rep in range(2):
     for ch in chunks:
-        for fl, k0, m2, k1, k2 in [(a, b, c, e, g) for a in flags for b in knob0 for c in m2rows
-                                   for e in knob1 for g in knob2]:
+        for fl, k0, m2, k1 in [(a, b, c, e) for a in flags for b in knob0 for c in m2rows
+                                for e in knob1]:
             cf.debug_set_flags(fl)
             cf.debug_set_knob(0, k0)
             cf.debug_set_knob(1, k1)
-            cf.debug_set_knob(2, k2)
             cf.debug_set_m2_rows(m2)
             s, dev, outs = sessions[ch]
             s.run(dev, outs)
@@ -53,7 +51,7 @@ for rep in range(2):
                 ref = [o.clone() for o in outs]
             err = max(float(((a.double() - b.double()).abs().max() /
                              (b.double().abs().max() + 1e-30))) for a, b in zip(outs, ref))
-            print(f"dw_chunk={ch} flags={fl} knob0={k0} knob1={k1} knob2={k2} m2rows={m2}: {sorted(ts)[1]:.2f} ms  max rel diff vs the first "
+            print(f"dw_chunk={ch} flags={fl} knob0={k0} knob1={k1} m2rows={m2}: {sorted(ts)[1]:.2f} ms  max rel diff vs the first "
                   f"{err:.2e}", flush=True)
 cf.debug_set_flags(0)
 cf.debug_set_knob(0, 0)
