@@ -1,0 +1,8 @@
+# 4-GPU re-check of the final tree (after the add_dep race fix): the multi-GPU tests and the
+# 4-GPU pipeline / data-parallel cfg3 benches
+mkdir -p gpurun_out/final2
+python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
+timeout 900 python -m pytest tests/test_gpu_pipeline.py tests/test_gpu_dp.py tests/test_gpu_control_overhead.py -m gpu -q -rs > gpurun_out/final2/gpu_tests_4gpu.log 2>&1; echo tests=$?
+timeout 600 python bench.py --gpus 4 --steps 10 --warmup 3 --no-cpu-baseline 2>/dev/null | tail -1 > gpurun_out/final2/bench_cfg3_pipeline4.jsonl
+timeout 600 python bench.py --gpus 4 --parallel dp --steps 10 --warmup 3 --no-cpu-baseline 2>/dev/null | tail -1 > gpurun_out/final2/bench_cfg3_dp4.jsonl
+tail -1 gpurun_out/final2/gpu_tests_4gpu.log; cut -c1-200 gpurun_out/final2/bench_cfg3_pipeline4.jsonl gpurun_out/final2/bench_cfg3_dp4.jsonl
