@@ -30,9 +30,11 @@ def run(p, f, precision, seed, T, K=0):
     return [o.cpu() for o in outs], tr
 
 
-@pytest.mark.parametrize("case", ["f32_ragged", "bf16_256row", "bf16_moe"])
+@pytest.mark.parametrize("case", ["f32_ragged", "bf16_256row", "bf16_moe", "bf16_cfg3_shape"])
 def test_schedule_perturbation_bit_identical(case):
-    if case == "f32_ragged":
+    if case == "bf16_cfg3_shape":   # 8-member heavy batches: the lanes' edges race the routing after them
+        T, B, I, H, L, prec, kw, mode = 9, 512, 1024, 1024, 8, cf.BF16, {}, "uniform"
+    elif case == "f32_ragged":
         T, B, I, H, L, prec, kw, mode = 7, 40, 24, 32, 3, cf.F32, {}, "uniform"
     elif case == "bf16_256row":   # 256-row tiles, chunked dW (T > 8), ragged lengths
         T, B, I, H, L, prec, kw, mode = 19, 512, 256, 256, 2, cf.BF16, {}, "uniform"
