@@ -336,6 +336,13 @@ def main():
     copied = [torch.cuda.Event(), torch.cuda.Event()]
     cev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(e2e_steps)]
+    # the step itself (after its inputs arrived), to see what the copies cost the kernel
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(e2e_steps)]
+
+    # diagnostics only: "oneset" runs every step on set 0 while the copies still stream in
+    # (separates the copies' cost from the alternation of the input sets)
+    e2e_ab = os.environ.get("BENCH_E2E_AB", "")
 
     def issue_copy(i):
         with torch.cuda.stream(copy_stream):
@@ -356,13 +363,16 @@ def main():
         stream.wait_event(copied[i % 2])
         if i + 1 < e2e_steps:
             issue_copy(i + 1)   # the set it overwrites was used by step i - 1 (finished)
-        sess.run(sets[i % 2], outs)
+        kev[i][0].record(stream)
+        sess.run(sets[0 if e2e_ab == "oneset" else i % 2], outs)
+        kev[i][1].record(stream)
         y_host.copy_(outs[0], non_blocking=True)
     e1.record(stream)
     torch.cuda.synchronize()
     copy_ms = sum(a.elapsed_time(b) for a, b in cev)
     e2e_ms = e0.elapsed_time(e1) / e2e_steps
     copy_ms /= e2e_steps
+    run_ms = sum(a.elapsed_time(b) for a, b in kev) / e2e_steps
     if os.environ.get("BENCH_DEBUG"):
         print(f"[rank {rank}] ms={ms:.2f} e2e_ms={e2e_ms:.2f} copy_ms={copy_ms:.2f} "
               f"kernel_ms={statistics.mean(kernel_ms):.2f}", file=sys.stderr, flush=True)
@@ -431,7 +441,8 @@ def main():
         "e2e": {"value": lens_sum * (1 if pipe else world) / (e2e_ms * 1e-3),
                 "unit": "sequence-steps/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "h2d_ms_per_step": copy_ms},
+                "h2d_ms_per_step": copy_ms,
+                "run_ms_per_step": run_ms},
         "gpu_launches": args.steps,
         "stack_swap": swap,
     }
