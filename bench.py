@@ -90,8 +90,15 @@ class Clocks:
                 if len(r) > 5 + k and r[5 + k].lower() == "active":
                     reasons.add(nm)
         mx = float(self.rows[0][2]) if self.rows and self.rows[0][2].replace(".", "").isdigit() else None
+        pw = []
+        for r in self.rows:
+            try:
+                pw.append(float(r[3]))
+            except (IndexError, ValueError):
+                pass
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                "power_w": statistics.median(pw) if pw else None}
 
 
 def flops_per_step(c, lens_sum):
@@ -356,6 +363,7 @@ def main():
     if pg:
         pg.barrier()   # every rank has its pinned inputs ready before the clock starts
         torch.cuda.synchronize()
+    ck_e2e = Clocks(local).__enter__()
     e0.record(stream)
     copy_stream.wait_event(e0)
     issue_copy(0)
@@ -369,6 +377,7 @@ def main():
         y_host.copy_(outs[0], non_blocking=True)
     e1.record(stream)
     torch.cuda.synchronize()
+    ck_e2e.__exit__(None, None, None)
     copy_ms = sum(a.elapsed_time(b) for a, b in cev)
     e2e_ms = e0.elapsed_time(e1) / e2e_steps
     copy_ms /= e2e_steps
@@ -442,7 +451,8 @@ def main():
                 "unit": "sequence-steps/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "h2d_ms_per_step": copy_ms,
-                "run_ms_per_step": run_ms},
+                "run_ms_per_step": run_ms,
+                "clocks": ck_e2e.summary()},
         "gpu_launches": args.steps,
         "stack_swap": swap,
     }
