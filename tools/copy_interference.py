@@ -1,0 +1,51 @@
+"""How much a concurrent copy slows the cfg3 step (the e2e gap): ms per cf_run
+alone, while 662.7 MB (one step's inputs) stream host->device from pinned memory, and while the
+same bytes are copied device->device, each on a separate copy stream started just before the
+run. Times are CUDA events on the session's stream around each run."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import __graft_entry__  # noqa: E402
+
+__graft_entry__.build()
+from bench import CONFIGS  # noqa: E402
+from paper_1805_01772_b200 import cf  # noqa: E402
+from paper_1805_01772_b200.models import dynamic_rnn_lstm, feeds_to_device  # noqa: E402
+from synth import rnn_inputs  # noqa: E402
+
+c = dict(CONFIGS["cfg3"])
+p = dynamic_rnn_lstm(c["T"], c["B"], c["I"], c["H"], c["L"])
+f = rnn_inputs(c["T"], c["B"], c["I"], c["H"], c["L"], seed=0, len_mode=c["len_mode"], bf16=True)
+stream = torch.cuda.Stream()
+s = cf.Session(p.g, p.fetch_tensors(), precision=cf.BF16, stream=stream.cuda_stream)
+dev = feeds_to_device(f, session=s)
+outs = s.alloc_outputs()
+nbytes = 662704128
+host = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+dst = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+src = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+cs = torch.cuda.Stream()
+
+
+def run(mode, n=6):
+    ts = []
+    for _ in range(n):
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if mode != "alone":
+            with torch.cuda.stream(cs):
+                dst.copy_(host if mode == "h2d" else src, non_blocking=True)
+        a.record(stream)
+        s.run(dev, outs)
+        b.record(stream)
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    return sorted(ts)[len(ts) // 2]
+
+
+s.run(dev, outs)
+for mode in ["alone", "h2d", "d2d", "alone", "h2d", "d2d"]:
+    print(f"{mode}: {run(mode):.2f} ms per run", flush=True)
