@@ -1,7 +1,8 @@
 """How much a concurrent copy slows the cfg3 step (the e2e gap): ms per cf_run
 alone, while 662.7 MB (one step's inputs) stream host->device from pinned memory, and while the
 same bytes are copied device->device, each on a separate copy stream started just before the
-run. Times are CUDA events on the session's stream around each run."""
+run; h2d_64MB_src repeats one 64 MB pinned window (the same DMA rate over far fewer host
+pages). Times are CUDA events on the session's stream around each run."""
 import os
 import sys
 
@@ -35,9 +36,14 @@ def run(mode, n=6):
     for _ in range(n):
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        if mode != "alone":
+        if mode in ("h2d", "d2d"):
             with torch.cuda.stream(cs):
                 dst.copy_(host if mode == "h2d" else src, non_blocking=True)
+        elif mode == "h2d_64MB_src":   # the same bytes from one 64 MB pinned window (few host pages)
+            with torch.cuda.stream(cs):
+                w = 64 << 20
+                for o in range(0, nbytes - w + 1, w):
+                    dst[o:o + w].copy_(host[:w], non_blocking=True)
         a.record(stream)
         s.run(dev, outs)
         b.record(stream)
@@ -47,5 +53,5 @@ def run(mode, n=6):
 
 
 s.run(dev, outs)
-for mode in ["alone", "h2d", "d2d", "alone", "h2d", "d2d"]:
+for mode in ["alone", "h2d", "h2d_64MB_src", "d2d", "alone", "h2d", "h2d_64MB_src", "d2d"]:
     print(f"{mode}: {run(mode):.2f} ms per run", flush=True)
