@@ -453,7 +453,7 @@ def main():
                 "h2d_ms_per_step": copy_ms,
                 "run_ms_per_step": run_ms,
                 "clocks": ck_e2e.summary()},
-        "gpu_launches": args.steps,
+        "gpu_launches": 2 * args.steps,   # per cf_run: cf_stage_kernel + cf_driver_kernel
         "stack_swap": swap,
     }
     print(json.dumps(line), flush=True)

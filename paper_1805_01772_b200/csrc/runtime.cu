@@ -3997,6 +3997,30 @@ __device__ void worker_loop(const RunArgs& A) {
   if (tcmode) tc::tc_teardown(ts);
 }
 
+// per-run parameters (tensor maps, registry, TensorArray bases, feed tokens, fetch targets)
+// copied from the pinned staging area by the SMs, not by a copy engine: a caller's large
+// host->device copy in flight (the next step's inputs) would queue these small uploads behind
+// it and delay the launch by the whole copy (tools/copy_interference.py)
+struct StageJob {
+  uint8_t* dst;
+  const uint8_t* src;   // pinned host memory (UVA: device-accessible)
+  unsigned long long bytes;
+};
+struct StageJobs {
+  StageJob j[6];
+  int n;
+};
+__global__ void __launch_bounds__(256) cf_stage_kernel(StageJobs J) {
+  const size_t t0 = blockIdx.x * (size_t)blockDim.x + threadIdx.x, nt = (size_t)gridDim.x * blockDim.x;
+  for (int k = 0; k < J.n; ++k) {
+    const StageJob& sj = J.j[k];
+    const bool v16 = (((uintptr_t)sj.dst | (uintptr_t)sj.src) & 15) == 0;
+    const size_t n16 = v16 ? sj.bytes / 16 : 0;
+    for (size_t i = t0; i < n16; i += nt) ((uint4*)sj.dst)[i] = ((const uint4*)sj.src)[i];
+    for (size_t i = n16 * 16 + t0; i < sj.bytes; i += nt) sj.dst[i] = sj.src[i];
+  }
+}
+
 __global__ void __launch_bounds__(kThreads, 1) cf_driver_kernel(RunArgs A_param) {
   // kernel parameters are addressed through references below; keep them in shared memory
   // (a reference to the parameter block would force a local-memory copy)
@@ -4780,10 +4804,11 @@ cf_status cf_run(cf_session* s, int32_t n_feed, const char* const* feed_names,
       s->preset_cap = (int)preset.size();
     }
     uint8_t* sh = s->stage_host;
+    StageJobs jobs{};
     auto upload = [&](void* dst, size_t off, const void* src, size_t bytes) {
       if (!bytes) return;
       std::memcpy(sh + off, src, bytes);
-      CUDA_OK(cudaMemcpyAsync(dst, sh + off, bytes, cudaMemcpyHostToDevice, s->stream));
+      jobs.j[jobs.n++] = StageJob{(uint8_t*)dst, sh + off, (unsigned long long)bytes};
     };
     upload((uint8_t*)A.prog.maps + sizeof(CUtensorMap) * 3 * s->n_reg_static, o_maps,
            s->maps_host.data() + 3 * s->n_reg_static, b_maps);
@@ -4798,6 +4823,12 @@ cf_status cf_run(cf_session* s, int32_t n_feed, const char* const* feed_names,
     if (up_chans) {
       upload(s->d_chans, o_ch, s->chans.data(), b_ch);
       s->chans_dirty = false;
+    }
+    if (jobs.n) {
+      const size_t tot = o_ch + b_ch;
+      const int nb = (int)std::min<size_t>(32, std::max<size_t>(1, tot / 16384));
+      cf_stage_kernel<<<nb, 256, 0, s->stream>>>(jobs);
+      CUDA_OK(cudaGetLastError());
     }
     A.epoch = ++s->epoch;
     // (the staging area is rewritten only by the next cf_run, after this one's final sync)

@@ -2,9 +2,12 @@
 alone, while 662.7 MB (one step's inputs) stream host->device from pinned memory, and while the
 same bytes are copied device->device, each on a separate copy stream started just before the
 run; h2d_64MB_src repeats one 64 MB pinned window (the same DMA rate over far fewer host
-pages). Times are CUDA events on the session's stream around each run."""
+pages); h2d_late_N issues the H2D copy N ms after the launch from a helper thread (cf_run blocks
+the host for the whole run), so it overlaps a later part of the step. Times are CUDA events on the session's stream around each run."""
 import os
 import sys
+import threading
+import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
@@ -31,6 +34,9 @@ src = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
 cs = torch.cuda.Stream()
 
 
+host_ms = []
+
+
 def run(mode, n=6):
     ts = []
     for _ in range(n):
@@ -44,14 +50,31 @@ def run(mode, n=6):
                 w = 64 << 20
                 for o in range(0, nbytes - w + 1, w):
                     dst[o:o + w].copy_(host[:w], non_blocking=True)
+        th = None
+        if mode.startswith("h2d_late"):   # cf_run blocks the host: a helper thread issues the copy
+            delay = int(mode.split("_")[-1]) * 1e-3
+
+            def late():
+                time.sleep(delay)
+                with torch.cuda.stream(cs):
+                    dst.copy_(host, non_blocking=True)
+            th = threading.Thread(target=late)
         a.record(stream)
+        t0 = time.perf_counter()
+        if th:
+            th.start()
         s.run(dev, outs)
+        host_ms.append(1e3 * (time.perf_counter() - t0))
         b.record(stream)
+        if th:
+            th.join()
         torch.cuda.synchronize()
         ts.append(a.elapsed_time(b))
     return sorted(ts)[len(ts) // 2]
 
 
 s.run(dev, outs)
-for mode in ["alone", "h2d", "h2d_64MB_src", "d2d", "alone", "h2d", "h2d_64MB_src", "d2d"]:
-    print(f"{mode}: {run(mode):.2f} ms per run", flush=True)
+for mode in ["alone", "h2d", "h2d_late_10", "h2d_late_20", "h2d_late_30", "h2d_late_40"] * 2:
+    host_ms.clear()
+    print(f"{mode}: {run(mode):.2f} ms per run (host time in cf_run {sorted(host_ms)[len(host_ms) // 2]:.2f} ms)",
+          flush=True)
